@@ -1,0 +1,234 @@
+"""ctypes harness over the HODLR2D CPU oracle (oracle/hodlr2d_oracle.cpp).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs.  The product package never imports this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "hodlr2d_oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+KERNELS = {"log": 0, "imq": 1, "one_over_r": 2, "test_lowrank": 100}
+
+
+def compile_oracle(force: bool = False) -> str:
+    """g++ -O2 -ffp-contract=off (no fast-math) -fopenmp; R14."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        cmd = ["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+               "-shared", "-fPIC", "-o", tmp, _SRC]
+        subprocess.check_call(cmd)
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            compile_oracle()
+            L = C.CDLL(_LIB)
+            d, i, i64, vp = C.c_double, C.c_int, C.c_int64, C.c_void_p
+            L.oracle_last_error.restype = C.c_char_p
+            L.oracle_depth.argtypes = [i64, i]
+            L.oracle_kernel.argtypes = [i, d, i, d, d, d, d]
+            L.oracle_kernel.restype = d
+            L.oracle_tree.argtypes = [vp, i64, d, d, d, i, vp, vp, vp]
+            L.oracle_box_sets.argtypes = [i, i, vp, vp, vp, vp, vp, vp]
+            L.oracle_classify.argtypes = [i, i, i, i]
+            L.oracle_level_lists.argtypes = [i, vp, vp]
+            L.oracle_level_lists.restype = i64
+            L.oracle_near_lists.argtypes = [i, vp, vp]
+            L.oracle_near_lists.restype = i64
+            L.oracle_aca_dense.argtypes = [vp, i, i, d, i, i, i, vp, vp, vp, vp]
+            L.oracle_dense_matvec.argtypes = [vp, i64, i, d, d, d, i, vp, vp]
+            L.oracle_dense_rows.argtypes = [vp, i64, i, d, d, d, i, vp, vp, i64, vp]
+            L.oracle_build.argtypes = [vp, i64, i, d, d, d, i, i, d, d, d, d, i, i, i, i, i64, i64]
+            L.oracle_build.restype = vp
+            L.oracle_destroy.argtypes = [vp]
+            L.oracle_kappa.argtypes = [vp]
+            L.oracle_build_seconds.argtypes = [vp]
+            L.oracle_build_seconds.restype = d
+            L.oracle_get_tree.argtypes = [vp, vp, vp]
+            L.oracle_num_blocks.argtypes = [vp, i]
+            L.oracle_num_blocks.restype = i64
+            L.oracle_get_ranks.argtypes = [vp, i, vp, vp]
+            L.oracle_get_block.argtypes = [vp, i, i64, vp, vp, vp, vp, vp]
+            L.oracle_factor_values.argtypes = [vp]
+            L.oracle_factor_values.restype = i64
+            L.oracle_matvec.argtypes = [vp, vp, vp, i]
+            L.oracle_save_factors.argtypes = [vp, C.c_char_p]
+            L.oracle_set_threads.argtypes = [i]
+            _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def set_threads(t: int) -> None:
+    lib().oracle_set_threads(int(t))
+
+
+def max_threads() -> int:
+    return int(lib().oracle_max_threads())
+
+
+def last_error() -> str:
+    return lib().oracle_last_error().decode()
+
+
+def depth(n: int, leaf_size: int) -> int:
+    return int(lib().oracle_depth(n, leaf_size))
+
+
+def kernel(kernel_id: int, p, q, c: float = 1.0, test_rank: int = 1) -> float:
+    return float(lib().oracle_kernel(kernel_id, c, test_rank, p[0], p[1], q[0], q[1]))
+
+
+def tree(points: np.ndarray, lo, side: float, kappa: int):
+    """(codes in tree order u32, perm i32, leaf_start i32)."""
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    n = pts.shape[0]
+    codes = np.zeros(n, np.uint32)
+    perm = np.zeros(n, np.int32)
+    ls = np.zeros((1 << (2 * kappa)) + 1, np.int32)
+    rc = lib().oracle_tree(_p(pts), n, lo[0], lo[1], side, kappa, _p(codes), _p(perm), _p(ls))
+    if rc != 0:
+        raise ValueError(f"oracle_tree rc={rc}: {last_error()}")
+    return codes, perm, ls
+
+
+def box_sets(level: int, box: int):
+    E = np.zeros(8, np.int32); clan = np.zeros(32, np.int32); il = np.zeros(32, np.int32)
+    nE = C.c_int(); nc = C.c_int(); ni = C.c_int()
+    lib().oracle_box_sets(level, box, _p(E), C.byref(nE), _p(clan), C.byref(nc), _p(il), C.byref(ni))
+    return list(E[:nE.value]), list(clan[:nc.value]), list(il[:ni.value])
+
+
+def classify(a, b) -> int:
+    return int(lib().oracle_classify(a[0], a[1], b[0], b[1]))
+
+
+def level_lists(level: int):
+    tot = lib().oracle_level_lists(level, None, None)
+    off = np.zeros((1 << (2 * level)) + 1, np.int32)
+    col = np.zeros(tot, np.int32)
+    lib().oracle_level_lists(level, _p(off), _p(col))
+    return off, col
+
+
+def near_lists(kappa: int):
+    tot = lib().oracle_near_lists(kappa, None, None)
+    off = np.zeros((1 << (2 * kappa)) + 1, np.int32)
+    col = np.zeros(tot, np.int32)
+    lib().oracle_near_lists(kappa, _p(off), _p(col))
+    return off, col
+
+
+def aca_dense(A: np.ndarray, tol: float, max_rank: int = 128, consecutive: int = 2, trim: int = 2):
+    A = np.asfortranarray(A, dtype=np.float64)
+    m, n = A.shape
+    kmax = min(m, n, max_rank)
+    U = np.zeros(m * kmax + 1); V = np.zeros(n * kmax + 1)
+    r = C.c_int(); tr = C.c_int()
+    Af = A.ravel(order="F")
+    lib().oracle_aca_dense(_p(Af), m, n, tol, max_rank, consecutive, trim, _p(U), _p(V),
+                           C.byref(r), C.byref(tr))
+    k = r.value
+    return U[: m * k].reshape(k, m).T.copy(), V[: n * k].reshape(k, n).T.copy(), bool(tr.value)
+
+
+def dense_matvec(points, x, kernel_id=0, c=1.0, scale=1.0, shift=0.0, test_rank=1):
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros_like(x)
+    lib().oracle_dense_matvec(_p(pts), pts.shape[0], kernel_id, c, scale, shift, test_rank, _p(x), _p(y))
+    return y
+
+
+def dense_rows(points, x, rows, kernel_id=0, c=1.0, scale=1.0, shift=0.0, test_rank=1):
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.zeros(rows.shape[0])
+    lib().oracle_dense_rows(_p(pts), pts.shape[0], kernel_id, c, scale, shift, test_rank, _p(x),
+                            _p(rows), rows.shape[0], _p(out))
+    return out
+
+
+class Operator:
+    """Oracle HODLR2D operator (Alg. 1 build, Alg. 2 matvec)."""
+
+    def __init__(self, points, kernel_id=0, leaf_size=64, tol=1e-10, c=1.0, scale=1.0, shift=0.0,
+                 test_rank=1, box_lo=(0.0, 0.0), box_side=0.0, depth=-1, max_rank=128,
+                 consecutive=2, trim=2, row_range=None):
+        self.points = np.ascontiguousarray(points, dtype=np.float64)
+        self.n = self.points.shape[0]
+        lo, hi = row_range if row_range is not None else (0, 0)
+        self._h = lib().oracle_build(_p(self.points), self.n, kernel_id, c, scale, shift, test_rank,
+                                     leaf_size, tol, box_lo[0], box_lo[1], box_side, depth, max_rank,
+                                     consecutive, trim, lo, hi)
+        if not self._h:
+            raise ValueError(f"oracle_build failed: {last_error()}")
+        self.kappa = int(lib().oracle_kappa(self._h))
+        self.build_seconds = float(lib().oracle_build_seconds(self._h))
+
+    def close(self):
+        if self._h:
+            lib().oracle_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def tree(self):
+        perm = np.zeros(self.n, np.int32)
+        ls = np.zeros((1 << (2 * self.kappa)) + 1, np.int32)
+        lib().oracle_get_tree(self._h, _p(perm), _p(ls))
+        return perm, ls
+
+    def num_blocks(self, level):
+        return int(lib().oracle_num_blocks(self._h, level))
+
+    def ranks(self, level):
+        nb = self.num_blocks(level)
+        r = np.zeros(nb, np.int32); t = np.zeros(nb, np.int32)
+        lib().oracle_get_ranks(self._h, level, _p(r), _p(t))
+        return r, t
+
+    def block(self, level, e):
+        m = C.c_int(); n = C.c_int(); r = C.c_int()
+        lib().oracle_get_block(self._h, level, e, C.byref(m), C.byref(n), C.byref(r), None, None)
+        U = np.zeros(m.value * r.value + 1); V = np.zeros(n.value * r.value + 1)
+        lib().oracle_get_block(self._h, level, e, C.byref(m), C.byref(n), C.byref(r), _p(U), _p(V))
+        k = r.value
+        return (U[: m.value * k].reshape(k, m.value).T.copy(), V[: n.value * k].reshape(k, n.value).T.copy())
+
+    def factor_values(self):
+        return int(lib().oracle_factor_values(self._h))
+
+    def matvec(self, x, order="original"):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros(self.n)
+        lib().oracle_matvec(self._h, _p(x), _p(y), 0 if order == "original" else 1)
+        return y
+
+    def save_factors(self, path):
+        rc = lib().oracle_save_factors(self._h, str(path).encode())
+        if rc != 0:
+            raise ValueError(last_error())

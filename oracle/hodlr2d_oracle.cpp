@@ -1,0 +1,720 @@
+// =====================================================================================
+//  HODLR2D CPU ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+//  Plain, slow, obviously-correct C++17 implementation of what the HODLR2D hot path
+//  computes (Kandappan, Gujjula, Ambikasaran, arXiv 2204.05536; PAPER.md line numbers
+//  "P:L" below).  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+//  --impl reference legs may load this library.  The product path
+//  (paper_2204_05536_b200/) shares NO code, header, table or helper with this file and
+//  never calls it.
+//
+//  Build: g++ -std=c++17 -O2 -ffp-contract=off -fopenmp -shared -fPIC (no -ffast-math),
+//  so the quantisation of A3 is bit-reproducible (R3, R14).
+//
+//  Contents (each follows the paper's statement or a DESIGN.md reading):
+//    kernel entry          A(i,j) = shift*[i==j] + scale*K(|p_i-p_j|)   P:218-224, R8
+//    depth rule            R1 (nominal leaf size; P:878 contradicts config 1)
+//    quadtree + Morton     P:583-666 (Fig. sdomain01), R2-R4
+//    relations E/V/W/clan  Defs 4.1-4.4, literal classification on integer
+//                          box closures; interaction list Eq. eq:ilist P:704-712
+//    near field            Alg. 1 l.5; Remark P:811-813
+//    ACA                   partial pivoting, P:42 / P:882 (variant unspecified) -> R7
+//    build                 Alg. 1 InitializeHODLR2D
+//    matvec                Alg. 2, P:887-912 (loop bound typo P:901 -> R6)
+//    dense product         plain definition (R10)
+//    factor file           R11
+//
+//  Parity pins: see tests/test_oracle_*.py.  Functions without an independent pin:
+//    - the IMQ kernel and the I + h^2 K stand-in are "parity unpinned by the paper"
+//      (the paper never uses them); they are pinned only by the generic pins
+//      (tiling, dense brute force, error-vs-tol), see DESIGN.md §Parity.
+// =====================================================================================
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace {
+
+enum { K_LOG = 0, K_IMQ = 1, K_ONE_OVER_R = 2, K_TEST_LOWRANK = 100 };
+
+struct KernelSpec {
+    int id = K_LOG;
+    double c = 1.0;      // IMQ shape
+    double scale = 1.0;  // A = shift*I + scale*K
+    double shift = 0.0;
+    int test_rank = 1;   // TEST_LOWRANK only
+};
+
+// K(p, q) with the r == 0 convention of reading R8: K(0) := 0 (log), 1 (IMQ).
+double kernel_value(const KernelSpec& k, double px, double py, double qx, double qy) {
+    double dx = px - qx, dy = py - qy;
+    if (k.id == K_TEST_LOWRANK) {
+        // K(p,q) = sum_s phi_s(p) phi_s(q), phi_s(p) = cos((s+1) p.x + 0.5 s p.y): rank <= test_rank
+        double acc = 0.0;
+        for (int s = 0; s < k.test_rank; ++s)
+            acc += std::cos((s + 1) * px + 0.5 * s * py) * std::cos((s + 1) * qx + 0.5 * s * qy);
+        return acc;
+    }
+    double r = std::sqrt(dx * dx + dy * dy);
+    if (k.id == K_LOG) {
+        if (r == 0.0) return 0.0;
+        return std::log(r);                                   // K = log r
+    }
+    if (k.id == K_ONE_OVER_R) {                               // Eq. eq:1byr, paper anchor
+        if (r == 0.0) return 0.0;
+        return 1.0 / r;
+    }
+    // inverse multiquadric 1/sqrt(1 + (r/c)^2)  (BASELINE.json configs 2 and 5)
+    double rc = r / k.c;
+    return 1.0 / std::sqrt(1.0 + rc * rc);
+}
+
+// Morton interleave, x bit at even positions (R4).
+uint32_t interleave(uint32_t ix, uint32_t iy) {
+    uint32_t code = 0;
+    for (int b = 0; b < 16; ++b) {
+        code |= ((ix >> b) & 1u) << (2 * b);
+        code |= ((iy >> b) & 1u) << (2 * b + 1);
+    }
+    return code;
+}
+void deinterleave(uint32_t code, int* ix, int* iy) {
+    uint32_t x = 0, y = 0;
+    for (int b = 0; b < 16; ++b) {
+        x |= ((code >> (2 * b)) & 1u) << b;
+        y |= ((code >> (2 * b + 1)) & 1u) << b;
+    }
+    *ix = (int)x;
+    *iy = (int)y;
+}
+
+// ---------------- relations, Defs 4.1-4.3 on integer box closures -----------------
+// Box (ix, iy) at level l is the closed square [ix, ix+1] x [iy, iy+1] in level units.
+enum Rel { SELF = 0, EDGE = 1, VERTEX = 2, WELLSEP = 3 };
+Rel classify(int ax, int ay, int bx, int by) {
+    // intersection of closures: [max(ax,bx), min(ax,bx)+1] per axis
+    int lx = std::max(ax, bx), hx = std::min(ax, bx) + 1;
+    int ly = std::max(ay, by), hy = std::min(ay, by) + 1;
+    if (lx > hx || ly > hy) return WELLSEP;            // do not share boundary (Def 4.3)
+    int wx = hx - lx, wy = hy - ly;                      // 1 = full overlap, 0 = touching
+    if (wx == 1 && wy == 1) return SELF;
+    if (wx + wy == 1) return EDGE;                        // intersection is a segment (Def 4.1)
+    return VERTEX;                                        // intersection is one point (Def 4.2)
+}
+
+// Edge-sharing set E_C (Def 4.1) of box b at level l.  A box that shares an edge lies in
+// the 3x3 neighbourhood, so enumerating it and classifying each candidate is the literal set.
+std::vector<int> edge_set(int l, int b) {
+    std::vector<int> out;
+    int ix, iy;
+    deinterleave((uint32_t)b, &ix, &iy);
+    int side = 1 << l;
+    for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+            int jx = ix + dx, jy = iy + dy;
+            if (jx < 0 || jy < 0 || jx >= side || jy >= side) continue;
+            if (classify(ix, iy, jx, jy) == EDGE) out.push_back((int)interleave(jx, jy));
+        }
+    std::sort(out.begin(), out.end());
+    return out;
+}
+
+// Clan set (Def 4.4): siblings(C) ∪ children(E_parent(C)).
+std::vector<int> clan_set(int l, int b) {
+    std::vector<int> out;
+    int parent = b >> 2;
+    for (int c = 0; c < 4; ++c)
+        if ((parent << 2 | c) != b) out.push_back(parent << 2 | c);        // siblings
+    if (l >= 2) {
+        for (int e : edge_set(l - 1, parent))
+            for (int c = 0; c < 4; ++c) out.push_back(e << 2 | c);         // children of E_parent
+    }
+    std::sort(out.begin(), out.end());
+    out.erase(std::unique(out.begin(), out.end()), out.end());
+    return out;
+}
+
+// Interaction list, Eq. eq:ilist: I_C = (Clan ∩ V_C) ∪ (Clan ∩ W_C), ascending Morton (R5).
+std::vector<int> interaction_list(int l, int b) {
+    std::vector<int> out;
+    int ix, iy;
+    deinterleave((uint32_t)b, &ix, &iy);
+    for (int d : clan_set(l, b)) {
+        int jx, jy;
+        deinterleave((uint32_t)d, &jx, &jy);
+        Rel r = classify(ix, iy, jx, jy);
+        if (r == VERTEX || r == WELLSEP) out.push_back(d);
+    }
+    return out;  // clan is sorted -> ascending
+}
+
+// ---------------- ACA (R7): partial pivoting, 2 hits + trim by default -----------------
+struct AcaParams {
+    double tol;
+    int max_rank;
+    int consecutive;  // tolerance hits in a row needed to stop
+    int trim;         // streak terms dropped on a tolerance stop
+};
+struct AcaResult {
+    int rank = 0;
+    int truncated = 0;
+    std::vector<double> U, V;  // column-major m x rank, n x rank
+};
+
+template <class Entry>
+AcaResult aca(Entry A, int m, int n, const AcaParams& p) {
+    AcaResult res;
+    if (m == 0 || n == 0) return res;
+    int kmax = std::min(std::min(m, n), p.max_rank);
+    std::vector<std::vector<double>> Us, Vs;
+    std::vector<char> used(m, 0);
+    std::vector<double> row(n), u(m), v(n);
+    int istar = 0, zero_streak = 0, hits = 0, k = 0;
+    bool tol_stop = false;
+    double S2 = 0.0;
+    while (true) {
+        // (1) residual row R(i*,:) = A(i*,Y) - sum_q U[i*,q] V[:,q]
+        for (int j = 0; j < n; ++j) {
+            double a = A(istar, j);
+            for (int q = 0; q < k; ++q) a -= Us[q][istar] * Vs[q][j];
+            row[j] = a;
+        }
+        used[istar] = 1;
+        // (2) j* = argmax |R(i*,:)|, ties -> smallest j
+        int jstar = 0;
+        double best = std::fabs(row[0]);
+        for (int j = 1; j < n; ++j)
+            if (std::fabs(row[j]) > best) { best = std::fabs(row[j]); jstar = j; }
+        // (3) zero pivot: mark used, move to the smallest unused row
+        if (best == 0.0) {
+            ++zero_streak;
+            int nxt = -1;
+            for (int i = 0; i < m; ++i) if (!used[i]) { nxt = i; break; }
+            if (zero_streak >= 3 || nxt < 0) break;
+            istar = nxt;
+            continue;
+        }
+        zero_streak = 0;
+        // (4) v = R(i*,:)/R(i*,j*);  u = A(X,j*) - sum_q V[j*,q] U[:,q]
+        double piv = row[jstar];
+        for (int j = 0; j < n; ++j) v[j] = row[j] / piv;
+        for (int i = 0; i < m; ++i) {
+            double a = A(i, jstar);
+            for (int q = 0; q < k; ++q) a -= Vs[q][jstar] * Us[q][i];
+            u[i] = a;
+        }
+        // (5) ||S_k||_F^2 += 2 sum_q (u.U_q)(V_q.v) + ||u||^2 ||v||^2
+        double cross = 0.0;
+        for (int q = 0; q < k; ++q) {
+            double du = 0.0, dv = 0.0;
+            for (int i = 0; i < m; ++i) du += u[i] * Us[q][i];
+            for (int j = 0; j < n; ++j) dv += Vs[q][j] * v[j];
+            cross += du * dv;
+        }
+        double nu2 = 0.0, nv2 = 0.0;
+        for (int i = 0; i < m; ++i) nu2 += u[i] * u[i];
+        for (int j = 0; j < n; ++j) nv2 += v[j] * v[j];
+        S2 += 2.0 * cross + nu2 * nv2;
+        // (6) append the term
+        Us.push_back(u);
+        Vs.push_back(v);
+        ++k;
+        // (7) stopping: ||u|| ||v|| <= tol ||S_k||_F on `consecutive` steps in a row
+        if (std::sqrt(nu2) * std::sqrt(nv2) <= p.tol * std::sqrt(S2)) ++hits; else hits = 0;
+        if (hits >= p.consecutive) { tol_stop = true; break; }
+        if (k == kmax) {
+            if (k == p.max_rank && k < std::min(m, n)) res.truncated = 1;
+            break;
+        }
+        // (8) next row = argmax_{unused} |u|, ties -> smallest
+        int nxt = -1;
+        double bu = -1.0;
+        for (int i = 0; i < m; ++i)
+            if (!used[i] && std::fabs(u[i]) > bu) { bu = std::fabs(u[i]); nxt = i; }
+        if (nxt < 0) break;  // rows exhausted
+        istar = nxt;
+    }
+    int rank = tol_stop ? k - std::min(p.trim, k) : k;
+    res.rank = rank;
+    res.U.assign((size_t)m * rank, 0.0);
+    res.V.assign((size_t)n * rank, 0.0);
+    for (int q = 0; q < rank; ++q) {
+        std::copy(Us[q].begin(), Us[q].end(), res.U.begin() + (size_t)q * m);
+        std::copy(Vs[q].begin(), Vs[q].end(), res.V.begin() + (size_t)q * n);
+    }
+    return res;
+}
+
+// ---------------- the operator -----------------
+struct Block {
+    int X = 0, Y = 0;
+    int64_t r0 = 0, c0 = 0;
+    int m = 0, n = 0;
+    AcaResult f;
+    bool built = false;
+};
+
+struct Oracle {
+    int64_t N = 0;
+    int kappa = 0;
+    double lo[2] = {0, 0}, side = 1;
+    KernelSpec K;
+    AcaParams aca{1e-10, 128, 2, 2};
+    std::vector<double> px, py;          // tree order
+    std::vector<int32_t> perm;           // tree position -> original index
+    std::vector<int32_t> leaf_start;     // 4^kappa + 1
+    std::vector<std::vector<int32_t>> il_off, il_col;  // index l = 1..kappa (0 unused)
+    std::vector<int32_t> nf_off, nf_col;
+    std::vector<std::vector<Block>> blocks;              // per level, CSR order
+    std::vector<std::vector<double>> dense;              // per near-field pair, row-major |X|x|Y|
+    int64_t row_lo = 0, row_hi = 0;                      // rows this operator serves (tree order)
+    double build_seconds = 0;
+
+    int64_t box_begin(int l, int b) const { return leaf_start[(size_t)b << (2 * (kappa - l))]; }
+    int64_t box_end(int l, int b) const { return leaf_start[(size_t)(b + 1) << (2 * (kappa - l))]; }
+    double entry(int64_t i, int64_t j) const {
+        double a = K.scale * kernel_value(K, px[i], py[i], px[j], py[j]);
+        if (i == j) a += K.shift;
+        return a;
+    }
+    bool row_box_active(int l, int b) const {
+        return box_begin(l, b) < row_hi && box_end(l, b) > row_lo;
+    }
+};
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& s) {
+    g_err = s;
+    return code;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* oracle_last_error() { return g_err.c_str(); }
+
+void oracle_set_threads(int t) {
+#ifdef _OPENMP
+    if (t > 0) omp_set_num_threads(t);
+#else
+    (void)t;
+#endif
+}
+
+int oracle_max_threads() {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+// R1: smallest kappa >= 0 with N <= leaf_size * 4^kappa.
+int oracle_depth(int64_t n, int leaf_size) {
+    if (n < 1 || leaf_size < 1) return -1;
+    int k = 0;
+    while ((double)leaf_size * std::pow(4.0, k) < (double)n) ++k;
+    return k;
+}
+
+double oracle_kernel(int kernel_id, double c, int test_rank, double px, double py, double qx,
+                     double qy) {
+    KernelSpec k;
+    k.id = kernel_id;
+    k.c = c;
+    k.test_rank = test_rank;
+    return kernel_value(k, px, py, qx, qy);
+}
+
+// Quadtree (R2-R4): quantise, Morton code, stable sort, leaf ranges.
+// codes_out[n] (tree order), perm[n], leaf_start[4^kappa + 1].
+int oracle_tree(const double* pts, int64_t n, double lo_x, double lo_y, double side, int kappa,
+                uint32_t* codes_out, int32_t* perm, int32_t* leaf_start) {
+    if (n < 1) return set_err(-1, "empty point set");
+    if (kappa < 0 || kappa > 15) return set_err(-1, "depth out of range");
+    std::vector<uint32_t> code((size_t)n);
+    const double scale = std::ldexp(1.0, kappa);
+    const int maxc = (1 << kappa) - 1;
+    for (int64_t i = 0; i < n; ++i) {
+        double x = pts[2 * i], y = pts[2 * i + 1];
+        if (!std::isfinite(x) || !std::isfinite(y)) return set_err(-1, "non-finite point " + std::to_string(i));
+        double qx = (x - lo_x) / side, qy = (y - lo_y) / side;   // correctly rounded, no FMA
+        if (!(qx >= 0.0 && qx <= 1.0 && qy >= 0.0 && qy <= 1.0))
+            return set_err(-2, "point " + std::to_string(i) + " outside the root box");
+        int ix = (int)std::floor(qx * scale), iy = (int)std::floor(qy * scale);
+        ix = std::min(ix, maxc);
+        iy = std::min(iy, maxc);
+        code[(size_t)i] = interleave((uint32_t)ix, (uint32_t)iy);
+    }
+    std::vector<int32_t> idx((size_t)n);
+    for (int64_t i = 0; i < n; ++i) idx[(size_t)i] = (int32_t)i;
+    std::stable_sort(idx.begin(), idx.end(),
+                     [&](int32_t a, int32_t b) { return code[(size_t)a] < code[(size_t)b]; });
+    int64_t nleaf = (int64_t)1 << (2 * kappa);
+    for (int64_t i = 0; i < n; ++i) {
+        perm[i] = idx[(size_t)i];
+        if (codes_out) codes_out[i] = code[(size_t)idx[(size_t)i]];
+    }
+    // leaf_start[b] = first tree position whose code >= b
+    int64_t pos = 0;
+    for (int64_t b = 0; b <= nleaf; ++b) {
+        while (pos < n && (int64_t)code[(size_t)idx[(size_t)pos]] < b) ++pos;
+        leaf_start[b] = (int32_t)pos;
+    }
+    return 0;
+}
+
+// Literal relation sets for one box (used by tests to pin Defs 4.1-4.5).
+// Returns counts; out arrays sized >= 8 (E), >= 20 (clan), >= 20 (I).
+int oracle_box_sets(int level, int box, int32_t* E, int* nE, int32_t* clan, int* nclan,
+                    int32_t* il, int* nil) {
+    auto e = edge_set(level, box);
+    auto c = level >= 1 ? clan_set(level, box) : std::vector<int>();
+    auto i = level >= 1 ? interaction_list(level, box) : std::vector<int>();
+    *nE = (int)e.size();
+    *nclan = (int)c.size();
+    *nil = (int)i.size();
+    for (size_t k = 0; k < e.size(); ++k) E[k] = e[k];
+    for (size_t k = 0; k < c.size(); ++k) clan[k] = c[k];
+    for (size_t k = 0; k < i.size(); ++k) il[k] = i[k];
+    return 0;
+}
+
+int oracle_classify(int ax, int ay, int bx, int by) { return (int)classify(ax, ay, bx, by); }
+
+// CSR interaction lists of one level: off[4^l + 1]; col may be null (count only).
+int64_t oracle_level_lists(int level, int32_t* off, int32_t* col) {
+    int64_t nb = (int64_t)1 << (2 * level);
+    int64_t tot = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        auto L = interaction_list(level, (int)b);
+        if (off) off[b] = (int32_t)tot;
+        if (col) for (size_t k = 0; k < L.size(); ++k) col[tot + (int64_t)k] = L[k];
+        tot += (int64_t)L.size();
+    }
+    if (off) off[nb] = (int32_t)tot;
+    return tot;
+}
+
+// Leaf near field {X} ∪ E_X (Alg. 1 l.5), ascending Morton.
+int64_t oracle_near_lists(int kappa, int32_t* off, int32_t* col) {
+    int64_t nb = (int64_t)1 << (2 * kappa);
+    int64_t tot = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        auto L = edge_set(kappa, (int)b);
+        L.push_back((int)b);
+        std::sort(L.begin(), L.end());
+        if (off) off[b] = (int32_t)tot;
+        if (col) for (size_t k = 0; k < L.size(); ++k) col[tot + (int64_t)k] = L[k];
+        tot += (int64_t)L.size();
+    }
+    if (off) off[nb] = (int32_t)tot;
+    return tot;
+}
+
+// ACA on an explicit column-major m x n matrix (test entry point for the R7 pins).
+int oracle_aca_dense(const double* A, int m, int n, double tol, int max_rank, int consecutive,
+                     int trim, double* U, double* V, int* rank, int* truncated) {
+    AcaParams p{tol, max_rank, consecutive, trim};
+    auto res = aca([&](int i, int j) { return A[(size_t)j * m + i]; }, m, n, p);
+    *rank = res.rank;
+    *truncated = res.truncated;
+    std::copy(res.U.begin(), res.U.end(), U);
+    std::copy(res.V.begin(), res.V.end(), V);
+    return 0;
+}
+
+// Dense product y = A x (R10), ORIGINAL order, rows in parallel.
+int oracle_dense_matvec(const double* pts, int64_t n, int kernel_id, double c, double scale,
+                        double shift, int test_rank, const double* x, double* y) {
+    KernelSpec k{kernel_id, c, scale, shift, test_rank};
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t i = 0; i < n; ++i) {
+        double acc = 0.0;
+        for (int64_t j = 0; j < n; ++j) {
+            double a = scale * kernel_value(k, pts[2 * i], pts[2 * i + 1], pts[2 * j], pts[2 * j + 1]);
+            if (i == j) a += shift;
+            acc += a * x[j];
+        }
+        y[i] = acc;
+    }
+    return 0;
+}
+
+// Sampled rows of the dense product: out[s] = (A x)_{rows[s]} exactly over all n columns.
+int oracle_dense_rows(const double* pts, int64_t n, int kernel_id, double c, double scale,
+                      double shift, int test_rank, const double* x, const int64_t* rows,
+                      int64_t nrows, double* out) {
+    KernelSpec k{kernel_id, c, scale, shift, test_rank};
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t s = 0; s < nrows; ++s) {
+        int64_t i = rows[s];
+        double acc = 0.0;
+        for (int64_t j = 0; j < n; ++j) {
+            double a = scale * kernel_value(k, pts[2 * i], pts[2 * i + 1], pts[2 * j], pts[2 * j + 1]);
+            if (i == j) a += shift;
+            acc += a * x[j];
+        }
+        out[s] = acc;
+    }
+    return 0;
+}
+
+// Alg. 1 InitializeHODLR2D.  box_side <= 0 -> bounding square (R2); depth < 0 -> R1.
+// [row_lo, row_hi) restricts the operator to the rows (tree order) one partition serves
+// (row_hi <= 0 -> all rows): only blocks whose row box intersects it are built.
+void* oracle_build(const double* pts, int64_t n, int kernel_id, double c, double scale,
+                   double shift, int test_rank, int leaf_size, double tol, double box_lo_x,
+                   double box_lo_y, double box_side, int depth, int max_rank, int consecutive,
+                   int trim, int64_t row_lo, int64_t row_hi) {
+    if (n < 1) { set_err(-1, "n < 1"); return nullptr; }
+    if (leaf_size < 1) { set_err(-1, "leaf_size < 1"); return nullptr; }
+    if (!(tol > 0.0 && tol < 1.0)) { set_err(-1, "aca_tol not in (0,1)"); return nullptr; }
+    if (trim > consecutive) { set_err(-1, "trim > consecutive"); return nullptr; }
+#ifdef _OPENMP
+    double t0 = omp_get_wtime();
+#endif
+    auto* o = new Oracle();
+    o->N = n;
+    o->K = KernelSpec{kernel_id, c, scale, shift, test_rank};
+    o->aca = AcaParams{tol, max_rank, consecutive, trim};
+    // R2 root box
+    if (box_side > 0) {
+        o->lo[0] = box_lo_x; o->lo[1] = box_lo_y; o->side = box_side;
+    } else {
+        double mnx = pts[0], mny = pts[1], mxx = pts[0], mxy = pts[1];
+        for (int64_t i = 0; i < n; ++i) {
+            mnx = std::min(mnx, pts[2 * i]); mxx = std::max(mxx, pts[2 * i]);
+            mny = std::min(mny, pts[2 * i + 1]); mxy = std::max(mxy, pts[2 * i + 1]);
+        }
+        o->lo[0] = mnx; o->lo[1] = mny;
+        o->side = std::max(mxx - mnx, mxy - mny);
+        if (o->side == 0.0) o->side = 1.0;
+    }
+    o->kappa = depth >= 0 ? depth : oracle_depth(n, leaf_size);
+    int kappa = o->kappa;
+    int64_t nleaf = (int64_t)1 << (2 * kappa);
+    o->perm.resize((size_t)n);
+    o->leaf_start.resize((size_t)nleaf + 1);
+    int rc = oracle_tree(pts, n, o->lo[0], o->lo[1], o->side, kappa, nullptr, o->perm.data(),
+                         o->leaf_start.data());
+    if (rc != 0) { delete o; return nullptr; }
+    o->px.resize((size_t)n); o->py.resize((size_t)n);
+    for (int64_t s = 0; s < n; ++s) {
+        o->px[(size_t)s] = pts[2 * (int64_t)o->perm[(size_t)s]];
+        o->py[(size_t)s] = pts[2 * (int64_t)o->perm[(size_t)s] + 1];
+    }
+    o->row_lo = 0; o->row_hi = n;
+    if (row_hi > 0) { o->row_lo = std::max<int64_t>(0, row_lo); o->row_hi = std::min<int64_t>(n, row_hi); }
+    // Alg. 1 l.4: lists
+    o->il_off.resize((size_t)kappa + 1);
+    o->il_col.resize((size_t)kappa + 1);
+    o->blocks.resize((size_t)kappa + 1);
+    for (int l = 1; l <= kappa; ++l) {
+        int64_t nb = (int64_t)1 << (2 * l);
+        int64_t tot = oracle_level_lists(l, nullptr, nullptr);
+        o->il_off[l].resize((size_t)nb + 1);
+        o->il_col[l].resize((size_t)tot);
+        oracle_level_lists(l, o->il_off[l].data(), o->il_col[l].data());
+        o->blocks[l].resize((size_t)tot);
+        for (int64_t X = 0; X < nb; ++X)
+            for (int32_t e = o->il_off[l][X]; e < o->il_off[l][X + 1]; ++e) {
+                Block& B = o->blocks[l][(size_t)e];
+                B.X = (int)X;
+                B.Y = o->il_col[l][(size_t)e];
+                B.r0 = o->box_begin(l, B.X);
+                B.m = (int)(o->box_end(l, B.X) - B.r0);
+                B.c0 = o->box_begin(l, B.Y);
+                B.n = (int)(o->box_end(l, B.Y) - B.c0);
+            }
+    }
+    int64_t nnf = oracle_near_lists(kappa, nullptr, nullptr);
+    o->nf_off.resize((size_t)nleaf + 1);
+    o->nf_col.resize((size_t)nnf);
+    oracle_near_lists(kappa, o->nf_off.data(), o->nf_col.data());
+    // Alg. 1 l.5: dense self + edge blocks at the leaves (only for served rows)
+    o->dense.resize((size_t)nnf);
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t X = 0; X < nleaf; ++X) {
+        if (!o->row_box_active(kappa, (int)X)) continue;
+        int64_t r0 = o->box_begin(kappa, (int)X), m = o->box_end(kappa, (int)X) - r0;
+        for (int32_t e = o->nf_off[X]; e < o->nf_off[X + 1]; ++e) {
+            int Y = o->nf_col[(size_t)e];
+            int64_t c0 = o->box_begin(kappa, Y), nn = o->box_end(kappa, Y) - c0;
+            auto& D = o->dense[(size_t)e];
+            D.resize((size_t)(m * nn));
+            for (int64_t i = 0; i < m; ++i)
+                for (int64_t j = 0; j < nn; ++j) D[(size_t)(i * nn + j)] = o->entry(r0 + i, c0 + j);
+        }
+    }
+    // Alg. 1 l.6: ACA for every member of every interaction list, l = kappa..1
+    for (int l = kappa; l >= 1; --l) {
+        auto& BL = o->blocks[l];
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int64_t e = 0; e < (int64_t)BL.size(); ++e) {
+            Block& B = BL[(size_t)e];
+            if (!o->row_box_active(l, B.X)) continue;
+            const Oracle* oc = o;
+            int64_t r0 = B.r0, c0 = B.c0;
+            B.f = aca([oc, r0, c0](int i, int j) { return oc->entry(r0 + i, c0 + j); }, B.m, B.n, o->aca);
+            B.built = true;
+        }
+    }
+#ifdef _OPENMP
+    o->build_seconds = omp_get_wtime() - t0;
+#endif
+    return o;
+}
+
+void oracle_destroy(void* h) { delete static_cast<Oracle*>(h); }
+
+int oracle_kappa(void* h) { return static_cast<Oracle*>(h)->kappa; }
+double oracle_build_seconds(void* h) { return static_cast<Oracle*>(h)->build_seconds; }
+
+int oracle_get_tree(void* h, int32_t* perm, int32_t* leaf_start) {
+    auto* o = static_cast<Oracle*>(h);
+    if (perm) std::copy(o->perm.begin(), o->perm.end(), perm);
+    if (leaf_start) std::copy(o->leaf_start.begin(), o->leaf_start.end(), leaf_start);
+    return 0;
+}
+
+int64_t oracle_num_blocks(void* h, int level) {
+    auto* o = static_cast<Oracle*>(h);
+    if (level < 1 || level > o->kappa) return 0;
+    return (int64_t)o->blocks[level].size();
+}
+
+// ranks of one level in CSR order (-1 for blocks not built in a row-restricted operator)
+int oracle_get_ranks(void* h, int level, int32_t* ranks, int32_t* truncated) {
+    auto* o = static_cast<Oracle*>(h);
+    auto& BL = o->blocks[level];
+    for (size_t e = 0; e < BL.size(); ++e) {
+        ranks[e] = BL[e].built ? BL[e].f.rank : -1;
+        if (truncated) truncated[e] = BL[e].f.truncated;
+    }
+    return 0;
+}
+
+// copy the factors of one block: U (m x r col-major), V (n x r col-major)
+int oracle_get_block(void* h, int level, int64_t e, int* m, int* n, int* r, double* U, double* V) {
+    auto* o = static_cast<Oracle*>(h);
+    const Block& B = o->blocks[level][(size_t)e];
+    *m = B.m; *n = B.n; *r = B.f.rank;
+    if (U) std::copy(B.f.U.begin(), B.f.U.end(), U);
+    if (V) std::copy(B.f.V.begin(), B.f.V.end(), V);
+    return 0;
+}
+
+// Sum over built blocks of r*(m+n) (stored FP64 values of the low-rank part).
+int64_t oracle_factor_values(void* h) {
+    auto* o = static_cast<Oracle*>(h);
+    int64_t tot = 0;
+    for (int l = 1; l <= o->kappa; ++l)
+        for (auto& B : o->blocks[l]) if (B.built) tot += (int64_t)B.f.rank * (B.m + B.n);
+    return tot;
+}
+
+// Alg. 2 MatVec.  x, y in ORIGINAL order (order = 0) or TREE order (order = 1).
+// Rows outside [row_lo, row_hi) of a restricted operator are set to 0.
+int oracle_matvec(void* h, const double* x_in, double* y_out, int order) {
+    auto* o = static_cast<Oracle*>(h);
+    int64_t n = o->N;
+    int kappa = o->kappa;
+    std::vector<double> x((size_t)n), b((size_t)n, 0.0);
+    for (int64_t s = 0; s < n; ++s) x[(size_t)s] = order == 0 ? x_in[o->perm[(size_t)s]] : x_in[s];
+    int64_t nleaf = (int64_t)1 << (2 * kappa);
+    // lines 2-9: dense self and edge-sharing blocks at the leaves
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t X = 0; X < nleaf; ++X) {
+        if (!o->row_box_active(kappa, (int)X)) continue;
+        int64_t r0 = o->box_begin(kappa, (int)X), m = o->box_end(kappa, (int)X) - r0;
+        for (int32_t e = o->nf_off[X]; e < o->nf_off[X + 1]; ++e) {
+            int Y = o->nf_col[(size_t)e];
+            int64_t c0 = o->box_begin(kappa, Y), nn = o->box_end(kappa, Y) - c0;
+            const auto& D = o->dense[(size_t)e];
+            for (int64_t i = 0; i < m; ++i) {
+                double acc = 0.0;
+                for (int64_t j = 0; j < nn; ++j) acc += D[(size_t)(i * nn + j)] * x[(size_t)(c0 + j)];
+                b[(size_t)(r0 + i)] += acc;
+            }
+        }
+    }
+    // lines 11-18: low-rank blocks, l = 1..kappa, boxes of level l (R6), partners ascending
+    for (int l = 1; l <= kappa; ++l) {
+        int64_t nb = (int64_t)1 << (2 * l);
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int64_t X = 0; X < nb; ++X) {
+            if (!o->row_box_active(l, (int)X)) continue;
+            std::vector<double> t;
+            for (int32_t e = o->il_off[l][X]; e < o->il_off[l][X + 1]; ++e) {
+                const Block& B = o->blocks[l][(size_t)e];
+                int r = B.f.rank;
+                t.assign((size_t)r, 0.0);
+                for (int q = 0; q < r; ++q) {          // t = V^T psi(Y)
+                    double acc = 0.0;
+                    for (int j = 0; j < B.n; ++j) acc += B.f.V[(size_t)q * B.n + j] * x[(size_t)(B.c0 + j)];
+                    t[(size_t)q] = acc;
+                }
+                for (int i = 0; i < B.m; ++i) {        // b(X) += U t
+                    double acc = 0.0;
+                    for (int q = 0; q < r; ++q) acc += B.f.U[(size_t)q * B.m + i] * t[(size_t)q];
+                    b[(size_t)(B.r0 + i)] += acc;
+                }
+            }
+        }
+    }
+    for (int64_t s = 0; s < n; ++s) {
+        double v = (s >= o->row_lo && s < o->row_hi) ? b[(size_t)s] : 0.0;
+        if (order == 0) y_out[o->perm[(size_t)s]] = v; else y_out[s] = v;
+    }
+    return 0;
+}
+
+// R11 factor interchange file.
+//   char magic[8] = "H2DFAC01"; int64 N; int32 kappa; int32 kernel_id; double tol, c, scale,
+//   shift, lo_x, lo_y, side; int32 test_rank; int32 reserved;
+//   int32 perm[N]; then for l = 1..kappa: int64 nblocks; per block (CSR order):
+//   int32 rank; double U[m*rank] (col-major); double V[n*rank] (col-major).
+int oracle_save_factors(void* h, const char* path) {
+    auto* o = static_cast<Oracle*>(h);
+    if (o->row_lo != 0 || o->row_hi != o->N) return set_err(-1, "row-restricted operator");
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return set_err(-1, std::string("cannot open ") + path);
+    const char magic[8] = {'H', '2', 'D', 'F', 'A', 'C', '0', '1'};
+    std::fwrite(magic, 1, 8, f);
+    int64_t N = o->N;
+    int32_t kap = o->kappa, kid = o->K.id, tr = o->K.test_rank, res = 0;
+    double d[7] = {o->aca.tol, o->K.c, o->K.scale, o->K.shift, o->lo[0], o->lo[1], o->side};
+    std::fwrite(&N, 8, 1, f);
+    std::fwrite(&kap, 4, 1, f);
+    std::fwrite(&kid, 4, 1, f);
+    std::fwrite(d, 8, 7, f);
+    std::fwrite(&tr, 4, 1, f);
+    std::fwrite(&res, 4, 1, f);
+    std::fwrite(o->perm.data(), 4, (size_t)N, f);
+    for (int l = 1; l <= o->kappa; ++l) {
+        int64_t nbk = (int64_t)o->blocks[l].size();
+        std::fwrite(&nbk, 8, 1, f);
+        for (auto& B : o->blocks[l]) {
+            int32_t r = B.f.rank;
+            std::fwrite(&r, 4, 1, f);
+            if (r) {
+                std::fwrite(B.f.U.data(), 8, (size_t)B.m * r, f);
+                std::fwrite(B.f.V.data(), 8, (size_t)B.n * r, f);
+            }
+        }
+    }
+    std::fclose(f);
+    return 0;
+}
+
+}  // extern "C"
