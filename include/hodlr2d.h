@@ -1,0 +1,184 @@
+/* =====================================================================================
+ *  hodlr2d.h — C ABI of the B200-native HODLR2D fast matrix-vector product.
+ *
+ *  Method: Kandappan, Gujjula, Ambikasaran, "HODLR2D: A new class of hierarchical
+ *  matrices", arXiv 2204.05536.  Citations "P:L" are PAPER.md line numbers.
+ *
+ *  Problem statement followed by the two main calls (BASELINE.json north_star):
+ *    build : given N points, a kernel, N_max and an ACA tolerance epsilon, build the
+ *            HODLR2D operator — balanced quadtree, interaction lists I_C and edge sharers
+ *            E_C, dense leaf near field, ACA low-rank U V^T for every I_C member
+ *            (Alg. 1 "InitializeHODLR2D").
+ *    matvec: b = K psi (Alg. 2 "MatVec").
+ *  The operator is A = shift*I + scale*K with K_ij = K(|p_i - p_j|), K(0) := K0
+ *  (log: 0; IMQ: 1; 1/r: 0, Eq. eq:1byr P:951-958).  See DESIGN.md for every
+ *  reading of a point where the paper is silent (R1..R19).
+ *
+ *  Conventions shared by all calls:
+ *   - fp64 only.  Points are interleaved (x, y) pairs, N x 2, in the caller's ORIGINAL
+ *     order.  "TREE order" is the Morton order of the quadtree (R4).
+ *   - Pointers may be host or device (CUDA) memory; the library detects which with
+ *     cudaPointerGetAttributes.  Device pointers must be on the handle's device.
+ *   - All device work is ordered on the stream given in the options (default: the
+ *     legacy default stream).  With device x/y, matvec is asynchronous w.r.t. the host;
+ *     with host x/y it returns after y has been written.
+ *   - The handle owns every device allocation it makes; the caller owns points, x, y.
+ *   - Return codes: 0 = OK, > 0 = warning, < 0 = error.  The thread-local message of
+ *     the last error is returned by hodlr2d_last_error().  A failed build returns no
+ *     handle; a handle stays valid after a failed matvec.
+ *   - Not thread-safe per handle; distinct handles may be used concurrently.
+ * ===================================================================================== */
+#ifndef HODLR2D_H
+#define HODLR2D_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hodlr2d_s* hodlr2d_t; /* opaque handle */
+
+enum {
+  H2D_OK = 0,
+  H2D_WTRUNC = 1,        /* warning: some ACA block hit max_rank (see info.truncated)      */
+  H2D_EINVAL = -1,       /* bad argument: n < 1, leaf_size < 1, tol not in (0,1), NaN/Inf  */
+  H2D_EOUTOFBOX = -2,    /* a point lies outside the explicit root box (message: index)    */
+  H2D_ECOINCIDENT = -3,  /* reserved (coincident points are legal: K(r=0) := K0, R8)      */
+  H2D_ENOMEM = -4,       /* device or host allocation failed                               */
+  H2D_ECUDA = -5,        /* CUDA runtime / kernel error                                    */
+  H2D_ENCCL = -6,        /* multi-GPU communication error                                  */
+  H2D_EFACTORS = -7      /* factor file unreadable or inconsistent with the handle         */
+};
+
+enum {
+  H2D_KERNEL_LOG = 0,           /* K(r) = log r, K(0) = 0          */
+  H2D_KERNEL_IMQ = 1,           /* K(r) = 1/sqrt(1 + (r/c)^2), K(0)=1 (BASELINE configs 2,5) */
+  H2D_KERNEL_ONE_OVER_R = 2,    /* K(r) = 1/r, K(0) = 0             (Eq. eq:1byr)  */
+  H2D_KERNEL_TEST_LOWRANK = 100 /* test-only: K(p,q) = sum_{s<test_rank} phi_s(p) phi_s(q),
+                                   phi_s(p) = cos((s+1) p.x + 0.5 s p.y) (exact rank)     */
+};
+
+enum { H2D_ORDER_ORIGINAL = 0, H2D_ORDER_TREE = 1 };
+
+/* Options of hodlr2d_build_ex.  Always start from hodlr2d_default_options(). */
+typedef struct {
+  double c;               /* IMQ shape parameter, c > 0                        (default 1)  */
+  double scale;           /* A = shift*I + scale*K                             (default 1)  */
+  double shift;           /*                                                   (default 0)  */
+  double box_lo[2];       /* root square lower-left corner                                  */
+  double box_side;        /* root square side; <= 0 -> bounding square of the points (R2)   */
+  int depth;              /* kappa; < 0 -> R1 depth rule from leaf_size        (default -1) */
+  int max_rank;           /* ACA rank cap per block; hitting it sets H2D_WTRUNC (def. 128)  */
+  int aca_consecutive;    /* tolerance hits in a row that stop ACA (R7)        (default 2)  */
+  int aca_trim;           /* streak terms dropped on a tolerance stop (R7)     (default 2)  */
+  int test_rank;          /* H2D_KERNEL_TEST_LOWRANK only                      (default 1)  */
+  void* stream;           /* cudaStream_t for all work                         (default 0)  */
+  int world;              /* Morton-range partition: number of ranks           (default 1)  */
+  int rank;               /* this rank, 0 <= rank < world                      (default 0)  */
+  int64_t row_begin;      /* explicit served TREE-order range [row_begin, row_end) snapped  */
+  int64_t row_end;        /*   to leaf boundaries; row_end <= 0 -> from world/rank (def 0)  */
+  size_t aca_scratch_bytes; /* ACA scratch budget; 0 -> 40 % of free device memory         */
+  int timing;             /* 1 -> record per-stage CUDA events in every matvec (default 0)  */
+  int skip_aca;           /* 1 -> build tree + lists only (factors via load_factors)        */
+} hodlr2d_options;
+
+#define H2D_MAX_LEVELS 16
+#define H2D_NUM_STAGES 4 /* 0 permute-in, 1 stage A (t = V^T x), 2 t-partial reduce,
+                            3 stage B + near-field P2P (y = U t + K_near x + shift x)   */
+
+typedef struct {
+  int64_t n;                 /* N                                                     */
+  int kappa;                 /* tree depth                                            */
+  int world, rank;
+  int64_t row_begin, row_end;/* TREE-order rows this handle serves                    */
+  int64_t leaf_begin, leaf_end;
+  double box_lo[2], box_side;
+  int64_t blocks_per_level[H2D_MAX_LEVELS + 1]; /* directed blocks (all, l = 1..kappa)   */
+  int64_t blocks_built;      /* blocks this handle stores                             */
+  int rank_max;              /* r_m                                           */
+  int64_t rank_hist[129];    /* blocks with rank r (r >= 128 -> bin 128)               */
+  int64_t u_values, v_values;/* stored fp64 factor values (U and V panels)            */
+  int64_t near_pairs;        /* sum over served leaves of |X| * |{X} u E_X|           */
+  double compression_ratio;  /* (factor values + near pairs) / N^2  (CR)        */
+  int64_t truncated;         /* blocks that hit max_rank                              */
+  double tree_seconds, aca_seconds, pack_seconds, build_seconds;
+  int64_t matvec_bytes;      /* algorithmic HBM bytes of one matvec */
+  int64_t stageA_bytes, stageB_bytes;
+  double p2p_pairs;          /* near-field pair evaluations per matvec                */
+  int64_t device_bytes;      /* device memory held by the handle                      */
+} hodlr2d_info;
+
+/* Fill *opts with the defaults listed above. */
+void hodlr2d_default_options(hodlr2d_options* opts);
+
+/* Build with default options (c = 1, scale = 1, shift = 0, bounding-square root box,
+ * R1 depth rule).  points: N x 2 fp64 (host or device), copied; n >= 1; leaf_size >= 1
+ * (N_max of Alg. 1); aca_tol in (0, 1).  *out receives the handle on success (return
+ * 0 or H2D_WTRUNC), is set to NULL on error. */
+int hodlr2d_build(const double* points, int64_t n, int kernel_id, int leaf_size, double aca_tol,
+                  hodlr2d_t* out);
+
+/* Same with explicit options (root box, kernel parameters, partition, stream ...). */
+int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_size, double aca_tol,
+                     const hodlr2d_options* opts, hodlr2d_t* out);
+
+/* y = A x, both length N in ORIGINAL order (single-rank handles).  y is overwritten. */
+int hodlr2d_matvec(hodlr2d_t h, const double* x, double* y);
+
+/* y = A x with an explicit ordering.  order = H2D_ORDER_TREE: x is the full length-N
+ * vector in TREE order and y receives rows [row_begin, row_end) in TREE order
+ * (length row_end - row_begin).  order = H2D_ORDER_ORIGINAL: as hodlr2d_matvec
+ * (single-rank handles only).  For multi-rank handles the caller assembles x_tree
+ * (e.g. one NCCL all-gather of the rank slices). */
+int hodlr2d_matvec_ex(hodlr2d_t h, const double* x, double* y, int order);
+
+/* Statistics of the built operator (host struct). */
+int hodlr2d_get_info(hodlr2d_t h, hodlr2d_info* info);
+
+/* Copy the tree to host arrays: perm[N] (TREE position -> ORIGINAL index) and
+ * leaf_start[4^kappa + 1].  Either pointer may be NULL. */
+int hodlr2d_copy_tree(hodlr2d_t h, int32_t* perm, int32_t* leaf_start);
+
+/* Copy the CSR interaction list of level 1 <= level <= kappa to host arrays:
+ * off[4^level + 1], col[off[4^level]] (partner Morton index, ascending).
+ * level = 0 copies the leaf near field {X} u E_X (off[4^kappa + 1]). */
+int hodlr2d_copy_lists(hodlr2d_t h, int level, int32_t* off, int32_t* col);
+
+/* Number of directed blocks of a level (CSR length); -1 if level is out of range. */
+int64_t hodlr2d_num_blocks(hodlr2d_t h, int level);
+
+/* Ranks of the blocks of one level in CSR order (host array); -1 = not stored by this rank. */
+int hodlr2d_copy_ranks(hodlr2d_t h, int level, int32_t* ranks);
+
+/* Copy the factors of block `e` (CSR order) of `level` to host: U (m x r) and V (n x r),
+ * column-major.  Pass NULL arrays to query m, n, r only. */
+int hodlr2d_copy_block(hodlr2d_t h, int level, int64_t e, int* m, int* n, int* r, double* U,
+                       double* V);
+
+/* Replace the factors by those of an oracle interchange file (R11); the file's
+ * N, kappa and perm must match the handle.  Used for the oracle-factor parity test. */
+int hodlr2d_load_factors(hodlr2d_t h, const char* path);
+
+/* Write the handle's factors in the same interchange format (single-rank handles). */
+int hodlr2d_save_factors(hodlr2d_t h, const char* path);
+
+/* Accumulated device time (ms) per stage over the matvecs run since the last reset,
+ * measured with CUDA events on the handle's stream (options.timing = 1).  ms[] has
+ * H2D_NUM_STAGES entries; *count receives the number of matvecs.  Synchronises. */
+int hodlr2d_stage_times(hodlr2d_t h, double* ms, int64_t* count, int reset);
+
+/* Enable / disable stage timing after the build. */
+int hodlr2d_set_timing(hodlr2d_t h, int on);
+
+/* Release every resource of the handle.  NULL is accepted. */
+int hodlr2d_destroy(hodlr2d_t h);
+
+/* Message of the last error on this thread ("" if none). */
+const char* hodlr2d_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HODLR2D_H */

@@ -1,0 +1,300 @@
+"""B200-native HODLR2D fast matvec (arXiv 2204.05536) — thin ctypes binding of the C ABI.
+
+Every entry point mirrors a function of ``include/hodlr2d.h`` (same names, argument
+marshalling only).  All arithmetic of the build and the matvec runs in the CUDA kernels
+of ``libhodlr2d.so``; there is no CPU fallback: if the library is missing, importing the
+binding's functions raises.  PyTorch is used only for device memory and streams.
+
+Quick use::
+
+    import torch, paper_2204_05536_b200 as h2d
+    pts = torch.rand(1 << 20, 2, dtype=torch.float64, device="cuda") * 2 - 1
+    op = h2d.Hodlr2d.build(pts, kernel="log", leaf_size=64, aca_tol=1e-8,
+                           box_lo=(-1, -1), box_side=2.0)
+    y = op.matvec(torch.randn(1 << 20, dtype=torch.float64, device="cuda"))
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhodlr2d.so")
+
+H2D_OK, H2D_WTRUNC = 0, 1
+H2D_EINVAL, H2D_EOUTOFBOX, H2D_ECOINCIDENT, H2D_ENOMEM = -1, -2, -3, -4
+H2D_ECUDA, H2D_ENCCL, H2D_EFACTORS = -5, -6, -7
+KERNELS = {"log": 0, "imq": 1, "one_over_r": 2, "test_lowrank": 100}
+ORDER_ORIGINAL, ORDER_TREE = 0, 1
+MAX_LEVELS = 16
+NUM_STAGES = 4
+STAGE_NAMES = ("permute_in", "stageA_VTx", "t_reduce", "stageB_Ut_p2p")
+
+# Every function declared in include/hodlr2d.h (checked by tests/test_abi.py).
+ABI_FUNCTIONS = (
+    "hodlr2d_default_options", "hodlr2d_build", "hodlr2d_build_ex", "hodlr2d_matvec",
+    "hodlr2d_matvec_ex", "hodlr2d_get_info", "hodlr2d_copy_tree", "hodlr2d_copy_lists",
+    "hodlr2d_num_blocks", "hodlr2d_copy_ranks", "hodlr2d_copy_block", "hodlr2d_load_factors",
+    "hodlr2d_save_factors", "hodlr2d_stage_times", "hodlr2d_set_timing", "hodlr2d_destroy",
+    "hodlr2d_last_error",
+)
+
+
+class Options(C.Structure):
+    """Mirror of ``hodlr2d_options``."""
+    _fields_ = [
+        ("c", C.c_double), ("scale", C.c_double), ("shift", C.c_double),
+        ("box_lo", C.c_double * 2), ("box_side", C.c_double),
+        ("depth", C.c_int), ("max_rank", C.c_int), ("aca_consecutive", C.c_int),
+        ("aca_trim", C.c_int), ("test_rank", C.c_int),
+        ("stream", C.c_void_p), ("world", C.c_int), ("rank", C.c_int),
+        ("row_begin", C.c_int64), ("row_end", C.c_int64),
+        ("aca_scratch_bytes", C.c_size_t), ("timing", C.c_int), ("skip_aca", C.c_int),
+    ]
+
+
+class Info(C.Structure):
+    """Mirror of ``hodlr2d_info``."""
+    _fields_ = [
+        ("n", C.c_int64), ("kappa", C.c_int), ("world", C.c_int), ("rank", C.c_int),
+        ("row_begin", C.c_int64), ("row_end", C.c_int64),
+        ("leaf_begin", C.c_int64), ("leaf_end", C.c_int64),
+        ("box_lo", C.c_double * 2), ("box_side", C.c_double),
+        ("blocks_per_level", C.c_int64 * (MAX_LEVELS + 1)), ("blocks_built", C.c_int64),
+        ("rank_max", C.c_int), ("rank_hist", C.c_int64 * 129),
+        ("u_values", C.c_int64), ("v_values", C.c_int64), ("near_pairs", C.c_int64),
+        ("compression_ratio", C.c_double), ("truncated", C.c_int64),
+        ("tree_seconds", C.c_double), ("aca_seconds", C.c_double), ("pack_seconds", C.c_double),
+        ("build_seconds", C.c_double), ("matvec_bytes", C.c_int64),
+        ("stageA_bytes", C.c_int64), ("stageB_bytes", C.c_int64), ("p2p_pairs", C.c_double),
+        ("device_bytes", C.c_int64),
+    ]
+
+    def as_dict(self) -> dict:
+        d = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            if hasattr(v, "__len__"):
+                v = list(v)
+            d[name] = v
+        d["blocks_per_level"] = d["blocks_per_level"][1: self.kappa + 1]
+        d["rank_hist"] = {r: c for r, c in enumerate(d["rank_hist"]) if c}
+        return d
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libhodlr2d.so (built in-tree by ``__graft_entry__.build()``).  Raises if absent."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build it with `python -m paper_2204_05536_b200.build` "
+                    "(there is no CPU fallback)")
+            L = C.CDLL(LIB_PATH)
+            vp, i, i64, d = C.c_void_p, C.c_int, C.c_int64, C.c_double
+            L.hodlr2d_default_options.argtypes = [C.POINTER(Options)]
+            L.hodlr2d_default_options.restype = None
+            L.hodlr2d_build.argtypes = [vp, i64, i, i, d, C.POINTER(vp)]
+            L.hodlr2d_build_ex.argtypes = [vp, i64, i, i, d, C.POINTER(Options), C.POINTER(vp)]
+            L.hodlr2d_matvec.argtypes = [vp, vp, vp]
+            L.hodlr2d_matvec_ex.argtypes = [vp, vp, vp, i]
+            L.hodlr2d_get_info.argtypes = [vp, C.POINTER(Info)]
+            L.hodlr2d_copy_tree.argtypes = [vp, vp, vp]
+            L.hodlr2d_copy_lists.argtypes = [vp, i, vp, vp]
+            L.hodlr2d_num_blocks.argtypes = [vp, i]
+            L.hodlr2d_num_blocks.restype = i64
+            L.hodlr2d_copy_ranks.argtypes = [vp, i, vp]
+            L.hodlr2d_copy_block.argtypes = [vp, i, i64, C.POINTER(i), C.POINTER(i), C.POINTER(i), vp, vp]
+            L.hodlr2d_load_factors.argtypes = [vp, C.c_char_p]
+            L.hodlr2d_save_factors.argtypes = [vp, C.c_char_p]
+            L.hodlr2d_stage_times.argtypes = [vp, vp, C.POINTER(i64), i]
+            L.hodlr2d_set_timing.argtypes = [vp, i]
+            L.hodlr2d_destroy.argtypes = [vp]
+            L.hodlr2d_last_error.restype = C.c_char_p
+            _lib = L
+    return _lib
+
+
+class Hodlr2dError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def _check(rc: int) -> int:
+    if rc < 0:
+        raise Hodlr2dError(rc, lib().hodlr2d_last_error().decode())
+    return rc
+
+
+def _ptr(a) -> int:
+    """Raw pointer of a torch tensor (host or CUDA) or a numpy array (host)."""
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"] or a.dtype != np.float64:
+            raise ValueError("numpy arrays must be C-contiguous float64")
+        return a.ctypes.data
+    if not a.is_contiguous() or str(a.dtype) != "torch.float64":
+        raise ValueError("tensors must be contiguous float64")
+    return a.data_ptr()
+
+
+def default_options() -> Options:
+    o = Options()
+    lib().hodlr2d_default_options(C.byref(o))
+    return o
+
+
+class Hodlr2d:
+    """Owner of a ``hodlr2d_t`` handle."""
+
+    def __init__(self, handle: int, n: int, keepalive=None):
+        self._h = C.c_void_p(handle)
+        self.n = n
+        self._keep = keepalive
+        self.status = H2D_OK
+
+    # -------------------------------------------------------------- build
+    @classmethod
+    def build(cls, points, kernel="log", leaf_size=64, aca_tol=1e-10, *, c=1.0, scale=1.0,
+              shift=0.0, box_lo=(0.0, 0.0), box_side=0.0, depth=-1, max_rank=128,
+              aca_consecutive=2, aca_trim=2, test_rank=1, stream=None, world=1, rank=0,
+              row_range=None, aca_scratch_bytes=0, timing=False, skip_aca=False):
+        """hodlr2d_build_ex.  ``points``: (N, 2) float64 torch tensor (CUDA or CPU) or numpy array."""
+        kid = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
+        o = default_options()
+        o.c, o.scale, o.shift = c, scale, shift
+        o.box_lo[0], o.box_lo[1] = box_lo
+        o.box_side = box_side
+        o.depth, o.max_rank = depth, max_rank
+        o.aca_consecutive, o.aca_trim, o.test_rank = aca_consecutive, aca_trim, test_rank
+        if stream is None:
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    stream = torch.cuda.current_stream().cuda_stream
+            except Exception:
+                stream = None
+        o.stream = stream or None
+        o.world, o.rank = world, rank
+        if row_range is not None:
+            o.row_begin, o.row_end = row_range
+        o.aca_scratch_bytes = aca_scratch_bytes
+        o.timing = int(bool(timing))
+        o.skip_aca = int(bool(skip_aca))
+        n = points.shape[0]
+        h = C.c_void_p()
+        rc = _check(lib().hodlr2d_build_ex(_ptr(points), n, kid, leaf_size, aca_tol, C.byref(o), C.byref(h)))
+        op = cls(h.value, n)
+        op.status = rc
+        return op
+
+    @classmethod
+    def build_default(cls, points, kernel_id: int, leaf_size: int, aca_tol: float):
+        """hodlr2d_build (the four-argument north-star call, default options)."""
+        h = C.c_void_p()
+        rc = _check(lib().hodlr2d_build(_ptr(points), points.shape[0], kernel_id, leaf_size, aca_tol, C.byref(h)))
+        op = cls(h.value, points.shape[0])
+        op.status = rc
+        return op
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib().hodlr2d_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -------------------------------------------------------------- matvec
+    def matvec(self, x, out=None, order="original"):
+        """hodlr2d_matvec / hodlr2d_matvec_ex.  Returns ``out`` (allocated like x if None)."""
+        o = ORDER_ORIGINAL if order == "original" else ORDER_TREE
+        if out is None:
+            if o == ORDER_TREE:
+                inf = self.info()
+                m = inf["row_end"] - inf["row_begin"]
+            else:
+                m = self.n
+            if isinstance(x, np.ndarray):
+                out = np.empty(m, dtype=np.float64)
+            else:
+                import torch
+                out = torch.empty(m, dtype=torch.float64, device=x.device)
+        if o == ORDER_ORIGINAL:
+            _check(lib().hodlr2d_matvec(self._h, _ptr(x), _ptr(out)))
+        else:
+            _check(lib().hodlr2d_matvec_ex(self._h, _ptr(x), _ptr(out), o))
+        return out
+
+    def matvec_raw(self, x_ptr: int, y_ptr: int, order: int = ORDER_ORIGINAL):
+        _check(lib().hodlr2d_matvec_ex(self._h, x_ptr, y_ptr, order))
+
+    # -------------------------------------------------------------- inspection
+    def info(self) -> dict:
+        inf = Info()
+        _check(lib().hodlr2d_get_info(self._h, C.byref(inf)))
+        return inf.as_dict()
+
+    def tree(self):
+        inf = self.info()
+        perm = np.zeros(self.n, np.int32)
+        ls = np.zeros((1 << (2 * inf["kappa"])) + 1, np.int32)
+        _check(lib().hodlr2d_copy_tree(self._h, perm.ctypes.data, ls.ctypes.data))
+        return perm, ls
+
+    def lists(self, level: int):
+        kappa = self.info()["kappa"]
+        tot = lib().hodlr2d_num_blocks(self._h, level)
+        nbox = 1 << (2 * (kappa if level == 0 else level))
+        off = np.zeros(nbox + 1, np.int32)
+        col = np.zeros(max(tot, 1), np.int32)
+        _check(lib().hodlr2d_copy_lists(self._h, level, off.ctypes.data, col.ctypes.data))
+        return off, col[:tot]
+
+    def ranks(self, level: int):
+        nb = lib().hodlr2d_num_blocks(self._h, level)
+        r = np.zeros(max(nb, 1), np.int32)
+        _check(lib().hodlr2d_copy_ranks(self._h, level, r.ctypes.data))
+        return r[:nb]
+
+    def block(self, level: int, e: int):
+        m, n, r = C.c_int(), C.c_int(), C.c_int()
+        _check(lib().hodlr2d_copy_block(self._h, level, e, C.byref(m), C.byref(n), C.byref(r), None, None))
+        U = np.zeros(m.value * r.value + 1)
+        V = np.zeros(n.value * r.value + 1)
+        _check(lib().hodlr2d_copy_block(self._h, level, e, C.byref(m), C.byref(n), C.byref(r),
+                                        U.ctypes.data, V.ctypes.data))
+        k = r.value
+        return (U[: m.value * k].reshape(k, m.value).T.copy(), V[: n.value * k].reshape(k, n.value).T.copy())
+
+    def load_factors(self, path):
+        _check(lib().hodlr2d_load_factors(self._h, str(path).encode()))
+
+    def save_factors(self, path):
+        _check(lib().hodlr2d_save_factors(self._h, str(path).encode()))
+
+    def set_timing(self, on: bool):
+        _check(lib().hodlr2d_set_timing(self._h, int(bool(on))))
+
+    def stage_times(self, reset: bool = True):
+        ms = (C.c_double * NUM_STAGES)()
+        cnt = C.c_int64()
+        _check(lib().hodlr2d_stage_times(self._h, C.cast(ms, C.c_void_p), C.byref(cnt), int(bool(reset))))
+        return dict(zip(STAGE_NAMES, list(ms))), cnt.value

@@ -1,0 +1,479 @@
+// Factor packing (G7) and the matvec hot path (S7-S10).
+//
+// HBM layout:
+//   U panel of row box X at level l : column-major m_X x R_X, the concatenation
+//                                     [U_b1 | U_b2 | ...] of the blocks (X, Y), Y in I_X
+//                                     ascending.  A leaf L inside X owns the contiguous
+//                                     row segment [a, a + |L|) of every column.
+//   V panel of column box Y         : row-major n_Y x RV_Y, the columns of the blocks
+//                                     (X, Y), X in I_Y ascending.  Row i of the panel is the
+//                                     RV_Y values that multiply x_i.
+//   t                               : one value per (block, rank index), grouped by column
+//                                     box (the V panel column order).
+// Matvec (Alg. 2; stage order is free, R18):
+//   stage A  t = V^T x          one CTA per (column box, row chunk); thread q owns panel
+//                               column q, so every load is coalesced and no cross-thread
+//                               reduction is needed except across row groups (smem).
+//   reduce   t = sum of chunk partials (only for boxes split over several CTAs).
+//   stage B  per leaf L: y_L = shift x_L + scale * sum_{Y in {L} u E_L} K(L, Y) x_Y
+//                               + sum_l U_{X_l}[rows of L, :] t_{X_l}
+//                               one CTA per leaf, one y write per row (no atomics).
+#include <algorithm>
+
+#include "h2d_internal.cuh"
+
+namespace h2d {
+namespace {
+
+constexpr int kAThreads = 256;
+constexpr int kBThreads = 256;
+constexpr int kTile = 512;           // near-field points staged in smem per tile
+constexpr int64_t kATarget = 32768;  // stage-A elements per CTA
+
+struct CopyItem {
+  const double* src;
+  double* dst;
+  int64_t count;
+};
+__global__ void copy_items_kernel(const CopyItem* __restrict__ items) {
+  const CopyItem it = items[blockIdx.x];
+  for (int64_t i = threadIdx.x; i < it.count; i += blockDim.x) it.dst[i] = it.src[i];
+}
+
+struct VPackItem {
+  const double* src;  // column-major n x r
+  double* dst;        // row-major panel, first column of the block
+  int32_t n, r, ld;
+  int32_t pad;
+};
+__global__ void vpack_kernel(const VPackItem* __restrict__ items) {
+  const VPackItem it = items[blockIdx.x];
+  const int64_t tot = (int64_t)it.n * it.r;
+  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+    int64_t j = e / it.r, q = e - j * it.r;
+    it.dst[j * it.ld + q] = it.src[j + q * it.n];
+  }
+}
+
+template <class T>
+T* upload_tmp(const std::vector<T>& v, cudaStream_t s) {
+  T* p = nullptr;
+  H2D_CUDA(cudaMallocAsync(&p, std::max<size_t>(1, v.size()) * sizeof(T), s));
+  if (!v.empty())
+    H2D_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return p;
+}
+
+// ---------------------------------------------------------------- stage A: t = V^T x
+__global__ void __launch_bounds__(kAThreads)
+stageA_kernel(const AItem* __restrict__ items, LevelPtrs lp, const double* __restrict__ x,
+              double* __restrict__ t, double* __restrict__ tpart) {
+  __shared__ double red[kAThreads];
+  const AItem it = items[blockIdx.x];
+  const double* __restrict__ V = lp.V[it.level] + it.v_off;
+  const double* __restrict__ xx = x + it.x_off;
+  double* out = it.out >= 0 ? t + it.out : tpart + (-(int64_t)it.out - 1);
+  const int R = it.R, nrows = it.nrows, tid = threadIdx.x;
+  if (R <= kAThreads) {
+    const int G = kAThreads / R;
+    const int g = tid / R, q = tid - g * R;
+    double acc = 0.0;
+    if (g < G) {
+      const double* p = V + (int64_t)g * R + q;
+      const int64_t step = (int64_t)G * R;
+      int i = g;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      for (; i + 3 * G < nrows; i += 4 * G, p += 4 * step) {
+        double v0 = __ldcs(p), v1 = __ldcs(p + step), v2 = __ldcs(p + 2 * step),
+               v3 = __ldcs(p + 3 * step);
+        a0 = fma(v0, __ldg(xx + i), a0);
+        a1 = fma(v1, __ldg(xx + i + G), a1);
+        a2 = fma(v2, __ldg(xx + i + 2 * G), a2);
+        a3 = fma(v3, __ldg(xx + i + 3 * G), a3);
+      }
+      for (; i < nrows; i += G, p += step) a0 = fma(__ldcs(p), __ldg(xx + i), a0);
+      acc = (a0 + a1) + (a2 + a3);
+    }
+    if (G == 1) {
+      if (tid < R) out[tid] = acc;
+      return;
+    }
+    red[tid] = acc;
+    __syncthreads();
+    if (tid < R) {
+      double s = 0.0;
+      for (int gg = 0; gg < G; ++gg) s += red[gg * R + tid];
+      out[tid] = s;
+    }
+  } else {
+    for (int q0 = 0; q0 < R; q0 += kAThreads) {
+      const int q = q0 + tid;
+      if (q >= R) break;
+      const double* p = V + q;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int i = 0;
+      for (; i + 3 < nrows; i += 4, p += 4 * (int64_t)R) {
+        a0 = fma(__ldcs(p), __ldg(xx + i), a0);
+        a1 = fma(__ldcs(p + R), __ldg(xx + i + 1), a1);
+        a2 = fma(__ldcs(p + 2 * (int64_t)R), __ldg(xx + i + 2), a2);
+        a3 = fma(__ldcs(p + 3 * (int64_t)R), __ldg(xx + i + 3), a3);
+      }
+      for (; i < nrows; ++i, p += R) a0 = fma(__ldcs(p), __ldg(xx + i), a0);
+      out[q] = (a0 + a1) + (a2 + a3);
+    }
+  }
+}
+
+__global__ void reduce_kernel(const RItem* __restrict__ items, const double* __restrict__ tpart,
+                              double* __restrict__ t) {
+  const RItem it = items[blockIdx.x];
+  for (int q = threadIdx.x; q < it.R; q += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < it.nchunks; ++c) s += tpart[it.p_off + (int64_t)c * it.R + q];
+    t[it.t_off + q] = s;
+  }
+}
+
+// ---------------------------------------------------------------- stage B + near-field P2P
+// dynamic smem: tX[rmax] + tile (3 * kTile) + red[kBThreads]
+__global__ void __launch_bounds__(kBThreads)
+stageB_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_start, LevelPtrs lp,
+              const double* __restrict__ t, const int32_t* __restrict__ nf_off,
+              const int32_t* __restrict__ nf_col, const double* __restrict__ px,
+              const double* __restrict__ py, const double* __restrict__ x, KernelParams kp,
+              double* __restrict__ y, const int32_t* __restrict__ perm, int order_out,
+              int64_t y_row0, int rmax) {
+  extern __shared__ double sm[];
+  double* tX = sm;
+  double* tpx = sm + rmax;
+  double* tpy = tpx + kTile;
+  double* txv = tpy + kTile;
+  double* red = txv + kTile;
+  const int64_t L = leaf_begin + blockIdx.x;
+  const int64_t s0 = leaf_start[L];
+  const int mL = leaf_start[L + 1] - (int)s0;
+  if (mL <= 0) return;
+  const int tid = threadIdx.x;
+  // near-field segments (<= 5 leaves)
+  const int nf0 = nf_off[L], nfn = nf_off[L + 1] - nf0;
+  int seg_s[5], seg_n[5], tot_near = 0;
+  for (int k = 0; k < 5; ++k) {
+    if (k < nfn) {
+      int Y = nf_col[nf0 + k];
+      seg_s[k] = leaf_start[Y];
+      seg_n[k] = leaf_start[Y + 1] - seg_s[k];
+    } else {
+      seg_s[k] = 0;
+      seg_n[k] = 0;
+    }
+    tot_near += seg_n[k];
+  }
+  for (int rp = 0; rp < mL; rp += kBThreads) {
+    const int RT = min(mL - rp, kBThreads);
+    const int G = kBThreads / RT;
+    const int g = tid / RT;
+    const int il = tid - g * RT;
+    const bool act = g < G;
+    const int64_t row = s0 + rp + il;
+    double acc = 0.0;
+    // ---- low-rank: sum over levels of U panel rows x t
+    for (int l = 1; l <= kappa; ++l) {
+      const int sh = 2 * (kappa - l);
+      const int64_t X = L >> sh;
+      const int32_t cb = lp.ucolbase[l][X];
+      const int R = lp.ucolbase[l][X + 1] - cb;
+      if (R == 0) continue;
+      const int64_t bx0 = leaf_start[X << sh];
+      const int64_t mX = leaf_start[(X + 1) << sh] - bx0;
+      __syncthreads();
+      const int32_t* __restrict__ ti = lp.tidx[l] + cb;
+      for (int q = tid; q < R; q += kBThreads) tX[q] = t[ti[q]];
+      __syncthreads();
+      if (act) {
+        const double* __restrict__ p = lp.U[l] + lp.upan_off[l][X] + (s0 - bx0) + rp + il +
+                                       (int64_t)g * mX;
+        const int64_t step = (int64_t)G * mX;
+        int q = g;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (; q + 3 * G < R; q += 4 * G, p += 4 * step) {
+          double u0 = __ldcs(p), u1 = __ldcs(p + step), u2 = __ldcs(p + 2 * step),
+                 u3 = __ldcs(p + 3 * step);
+          a0 = fma(u0, tX[q], a0);
+          a1 = fma(u1, tX[q + G], a1);
+          a2 = fma(u2, tX[q + 2 * G], a2);
+          a3 = fma(u3, tX[q + 3 * G], a3);
+        }
+        for (; q < R; q += G, p += step) a0 = fma(__ldcs(p), tX[q], a0);
+        acc += (a0 + a1) + (a2 + a3);
+      }
+    }
+    // ---- near field P2P from shared-memory tiles
+    double pxi = 0.0, pyi = 0.0;
+    if (act) { pxi = px[row]; pyi = py[row]; }
+    double near = 0.0;
+    for (int t0 = 0; t0 < tot_near; t0 += kTile) {
+      const int tn = min(kTile, tot_near - t0);
+      __syncthreads();
+      for (int e = tid; e < tn; e += kBThreads) {
+        int idx = t0 + e, k = 0;
+        while (idx >= seg_n[k]) { idx -= seg_n[k]; ++k; }
+        const int64_t src = seg_s[k] + idx;
+        tpx[e] = px[src];
+        tpy[e] = py[src];
+        txv[e] = x[src];
+      }
+      __syncthreads();
+      if (act) {
+        double b0 = 0.0, b1 = 0.0;
+        int j = g;
+        for (; j + G < tn; j += 2 * G) {
+          b0 = fma(kernel_eval(kp, pxi, pyi, tpx[j], tpy[j]), txv[j], b0);
+          b1 = fma(kernel_eval(kp, pxi, pyi, tpx[j + G], tpy[j + G]), txv[j + G], b1);
+        }
+        for (; j < tn; j += G) b0 = fma(kernel_eval(kp, pxi, pyi, tpx[j], tpy[j]), txv[j], b0);
+        near += b0 + b1;
+      }
+    }
+    acc = fma(kp.scale, near, acc);
+    __syncthreads();
+    red[tid] = acc;
+    __syncthreads();
+    if (tid < RT) {
+      double s = 0.0;
+      for (int gg = 0; gg < G; ++gg) s += red[gg * RT + tid];
+      const int64_t r = s0 + rp + tid;
+      s = fma(kp.shift, x[r], s);
+      if (order_out == H2D_ORDER_ORIGINAL) y[perm[r]] = s;
+      else y[r - y_row0] = s;
+    }
+  }
+}
+
+__global__ void permute_in_kernel(const double* __restrict__ x, const int32_t* __restrict__ perm,
+                                  int64_t n, double* __restrict__ xt) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x)
+    xt[s] = x[perm[s]];
+}
+
+}  // namespace
+
+// Pack one level's factors (per-block sources, column-major U_b m x r and V_b n x r) into
+// the U / V panels and fill the level's panel metadata.
+void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
+                const std::vector<const double*>& srcV) {
+  cudaStream_t s = h.stream;
+  const int l = L.l;
+  const int64_t nbox = L.nbox;
+  auto rank_of = [&](int64_t e) { return std::max<int32_t>(0, L.rank[(size_t)e]); };
+  L.ucol.assign((size_t)L.nblocks, 0);
+  L.vcol.assign((size_t)L.nblocks, 0);
+  L.upan_off.assign((size_t)nbox, 0);
+  L.vpan_off.assign((size_t)nbox, 0);
+  L.ucolbase.assign((size_t)nbox + 1, 0);
+  L.vR.assign((size_t)nbox, 0);
+  int64_t uo = 0, vo = 0;
+  int32_t cb = 0;
+  for (int64_t X = 0; X < nbox; ++X) {
+    const int64_t m = h.box_end(l, X) - h.box_begin(l, X);
+    int32_t R = 0;
+    for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
+      L.ucol[(size_t)e] = R;
+      R += rank_of(e);
+    }
+    L.ucolbase[(size_t)X] = cb;
+    cb += R;
+    L.upan_off[(size_t)X] = uo;
+    uo += m * R;
+    // V panel of column box X: blocks (Z, X) for Z in I_X ascending
+    int32_t RV = 0;
+    for (int32_t e2 = L.off[(size_t)X]; e2 < L.off[(size_t)X + 1]; ++e2) {
+      const int32_t b = L.trans[(size_t)e2];
+      L.vcol[(size_t)b] = RV;
+      RV += rank_of(b);
+    }
+    L.vR[(size_t)X] = RV;
+    L.vpan_off[(size_t)X] = vo;
+    vo += m * RV;
+  }
+  L.ucolbase[(size_t)nbox] = cb;
+  L.u_values = uo;
+  L.v_values = vo;
+  L.U = h.alloc<double>(uo);
+  L.V = h.alloc<double>(vo);
+  std::vector<CopyItem> citems;
+  std::vector<VPackItem> vitems;
+  for (int64_t X = 0; X < nbox; ++X) {
+    const int64_t mX = h.box_end(l, X) - h.box_begin(l, X);
+    for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
+      const int r = rank_of(e);
+      if (r == 0) continue;
+      const int64_t Y = L.col[(size_t)e];
+      const int64_t nY = h.box_end(l, Y) - h.box_begin(l, Y);
+      if (mX * r > 0)
+        citems.push_back(CopyItem{srcU[(size_t)e], L.U + L.upan_off[(size_t)X] + (int64_t)L.ucol[(size_t)e] * mX,
+                                  mX * r});
+      if (nY * r > 0)
+        vitems.push_back(VPackItem{srcV[(size_t)e], L.V + L.vpan_off[(size_t)Y] + L.vcol[(size_t)e],
+                                   (int32_t)nY, r, L.vR[(size_t)Y], 0});
+    }
+  }
+  const size_t CH = 1 << 20;
+  for (size_t c0 = 0; c0 < citems.size(); c0 += CH) {
+    std::vector<CopyItem> part(citems.begin() + c0, citems.begin() + std::min(citems.size(), c0 + CH));
+    CopyItem* d = upload_tmp(part, s);
+    copy_items_kernel<<<(int)part.size(), 256, 0, s>>>(d);
+    H2D_LAUNCH_CHECK();
+    H2D_CUDA(cudaFreeAsync(d, s));
+  }
+  for (size_t c0 = 0; c0 < vitems.size(); c0 += CH) {
+    std::vector<VPackItem> part(vitems.begin() + c0, vitems.begin() + std::min(vitems.size(), c0 + CH));
+    VPackItem* d = upload_tmp(part, s);
+    vpack_kernel<<<(int)part.size(), 256, 0, s>>>(d);
+    H2D_LAUNCH_CHECK();
+    H2D_CUDA(cudaFreeAsync(d, s));
+  }
+  H2D_CUDA(cudaStreamSynchronize(s));
+}
+
+static int max_panel_width(const Handle& h) {
+  int r = 1;
+  for (int l = 1; l <= h.kappa; ++l) {
+    const Level& L = h.levels[(size_t)l];
+    for (int64_t X = 0; X < L.nbox; ++X)
+      r = std::max(r, L.ucolbase[(size_t)X + 1] - L.ucolbase[(size_t)X]);
+  }
+  return r;
+}
+
+// Build the stage-A / reduce schedule, t layout and the per-level device tables.
+void finalize_schedule(Handle& h) {
+  cudaStream_t s = h.stream;
+  int64_t t_len = 0, tpart_len = 0;
+  std::vector<AItem> aitems;
+  std::vector<RItem> ritems;
+  for (int l = 1; l <= h.kappa; ++l) {
+    Level& L = h.levels[(size_t)l];
+    L.t_off.assign((size_t)L.nbox, 0);
+    for (int64_t Y = 0; Y < L.nbox; ++Y) {
+      L.t_off[(size_t)Y] = t_len;
+      t_len += L.vR[(size_t)Y];
+    }
+  }
+  if (t_len > INT32_MAX) throw Error{H2D_EINVAL, "t vector exceeds 2^31 entries"};
+  for (int l = 1; l <= h.kappa; ++l) {
+    Level& L = h.levels[(size_t)l];
+    // t index of every U-panel column
+    std::vector<int32_t> tidx((size_t)L.ucolbase[(size_t)L.nbox]);
+    for (int64_t X = 0; X < L.nbox; ++X)
+      for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
+        const int r = std::max<int32_t>(0, L.rank[(size_t)e]);
+        const int64_t Y = L.col[(size_t)e];
+        for (int q = 0; q < r; ++q)
+          tidx[(size_t)(L.ucolbase[(size_t)X] + L.ucol[(size_t)e] + q)] =
+              (int32_t)(L.t_off[(size_t)Y] + L.vcol[(size_t)e] + q);
+      }
+    L.d_tidx = h.alloc<int32_t>(tidx.size());
+    L.d_ucolbase = h.alloc<int32_t>(L.ucolbase.size());
+    L.d_upan_off = h.alloc<int64_t>(L.upan_off.size());
+    if (!tidx.empty())
+      H2D_CUDA(cudaMemcpyAsync(L.d_tidx, tidx.data(), tidx.size() * 4, cudaMemcpyHostToDevice, s));
+    H2D_CUDA(cudaMemcpyAsync(L.d_ucolbase, L.ucolbase.data(), L.ucolbase.size() * 4,
+                             cudaMemcpyHostToDevice, s));
+    H2D_CUDA(cudaMemcpyAsync(L.d_upan_off, L.upan_off.data(), L.upan_off.size() * 8,
+                             cudaMemcpyHostToDevice, s));
+    H2D_CUDA(cudaStreamSynchronize(s));
+    h.lp.U[l] = L.U;
+    h.lp.V[l] = L.V;
+    h.lp.ucolbase[l] = L.d_ucolbase;
+    h.lp.upan_off[l] = L.d_upan_off;
+    h.lp.tidx[l] = L.d_tidx;
+    // stage-A items
+    for (int64_t Y = 0; Y < L.nbox; ++Y) {
+      const int R = L.vR[(size_t)Y];
+      const int64_t y0 = h.box_begin(l, Y);
+      const int64_t nY = h.box_end(l, Y) - y0;
+      if (R == 0 || nY == 0) continue;
+      int64_t nch = std::min<int64_t>(nY, std::max<int64_t>(1, (nY * R + kATarget - 1) / kATarget));
+      const int64_t rows = (nY + nch - 1) / nch;
+      nch = (nY + rows - 1) / rows;
+      if (nch == 1) {
+        aitems.push_back(AItem{L.vpan_off[(size_t)Y], y0, (int32_t)nY, R, (int32_t)L.t_off[(size_t)Y], l});
+      } else {
+        if (tpart_len + nch * R > INT32_MAX) throw Error{H2D_EINVAL, "partial buffer too large"};
+        ritems.push_back(RItem{(int32_t)L.t_off[(size_t)Y], (int32_t)tpart_len, R, (int32_t)nch});
+        for (int64_t c = 0; c < nch; ++c) {
+          const int64_t r0 = c * rows, nr = std::min(rows, nY - r0);
+          aitems.push_back(AItem{L.vpan_off[(size_t)Y] + r0 * R, y0 + r0, (int32_t)nr, R,
+                                 (int32_t)(-(tpart_len + c * R) - 1), l});
+        }
+        tpart_len += nch * R;
+      }
+    }
+  }
+  h.t_len = t_len;
+  h.tpart_len = tpart_len;
+  h.rmax_panel = max_panel_width(h);
+  h.d_t = h.alloc<double>(t_len);
+  h.d_tpart = h.alloc<double>(tpart_len);
+  h.n_aitems = (int64_t)aitems.size();
+  h.n_ritems = (int64_t)ritems.size();
+  h.d_aitems = h.alloc<AItem>(aitems.size());
+  h.d_ritems = h.alloc<RItem>(ritems.size());
+  if (!aitems.empty())
+    H2D_CUDA(cudaMemcpyAsync(h.d_aitems, aitems.data(), aitems.size() * sizeof(AItem),
+                             cudaMemcpyHostToDevice, s));
+  if (!ritems.empty())
+    H2D_CUDA(cudaMemcpyAsync(h.d_ritems, ritems.data(), ritems.size() * sizeof(RItem),
+                             cudaMemcpyHostToDevice, s));
+  H2D_CUDA(cudaStreamSynchronize(s));
+}
+
+void permute_in(Handle& h, const double* d_x, double* d_xtree) {
+  int blocks = (int)std::min<int64_t>((h.n + 255) / 256, 148 * 16);
+  permute_in_kernel<<<blocks, 256, 0, h.stream>>>(d_x, h.d_perm, h.n, d_xtree);
+  H2D_LAUNCH_CHECK();
+}
+
+static cudaEvent_t next_event(Handle& h) {
+  if (h.ev_used >= (int64_t)h.ev_pool.size()) {
+    cudaEvent_t e;
+    H2D_CUDA(cudaEventCreate(&e));
+    h.ev_pool.push_back(e);
+  }
+  return h.ev_pool[(size_t)h.ev_used++];
+}
+
+void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, int64_t y_row0) {
+  cudaStream_t s = h.stream;
+  cudaEvent_t e1 = nullptr, e2 = nullptr, e3 = nullptr;
+  if (h.timing) { e1 = next_event(h); H2D_CUDA(cudaEventRecord(e1, s)); }
+  if (h.n_aitems > 0) {
+    stageA_kernel<<<(int)h.n_aitems, kAThreads, 0, s>>>(h.d_aitems, h.lp, d_xtree, h.d_t, h.d_tpart);
+    H2D_LAUNCH_CHECK();
+  }
+  if (h.timing) { e2 = next_event(h); H2D_CUDA(cudaEventRecord(e2, s)); }
+  if (h.n_ritems > 0) {
+    reduce_kernel<<<(int)h.n_ritems, 128, 0, s>>>(h.d_ritems, h.d_tpart, h.d_t);
+    H2D_LAUNCH_CHECK();
+  }
+  if (h.timing) { e3 = next_event(h); H2D_CUDA(cudaEventRecord(e3, s)); }
+  const int64_t nleaves = h.leaf_end - h.leaf_begin;
+  if (nleaves > 0) {
+    static_assert(kBThreads == 256, "");
+    const int rmax = h.rmax_panel;
+    const size_t smem = ((size_t)rmax + 3 * kTile + kBThreads) * sizeof(double);
+    if (smem > 48 * 1024)
+      H2D_CUDA(cudaFuncSetAttribute(stageB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    stageB_kernel<<<(int)nleaves, kBThreads, smem, s>>>(
+        h.kappa, h.leaf_begin, h.d_leaf_start, h.lp, h.d_t, h.d_nf_off, h.d_nf_col, h.d_px, h.d_py,
+        d_xtree, h.kp, d_y, h.d_perm, order_out, y_row0, rmax);
+    H2D_LAUNCH_CHECK();
+  }
+  if (h.timing) {
+    cudaEvent_t e4 = next_event(h);
+    H2D_CUDA(cudaEventRecord(e4, s));
+  }
+}
+
+}  // namespace h2d

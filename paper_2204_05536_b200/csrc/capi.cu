@@ -1,0 +1,607 @@
+// C ABI of the B200 HODLR2D library (include/hodlr2d.h): handle lifecycle, build
+// orchestration (Alg. 1), matvec entry points (Alg. 2), factor
+// interchange file (R11), statistics and stage timing.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <new>
+
+#include "h2d_internal.cuh"
+
+namespace h2d {
+
+static thread_local std::string g_last_error;
+
+void set_error(int code, const std::string& msg) {
+  (void)code;
+  g_last_error = msg;
+}
+
+void Handle::release(void* p) {
+  if (!p) return;
+  auto it = std::find(allocs.begin(), allocs.end(), p);
+  if (it != allocs.end()) {
+    allocs.erase(it);
+    cudaFree(p);
+  }
+}
+
+Handle::~Handle() {
+  cudaStreamSynchronize(stream);
+  for (void* p : allocs) cudaFree(p);
+  for (auto e : ev_pool) cudaEventDestroy(e);
+}
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static int depth_rule(int64_t n, int leaf_size) {  // R1
+  int k = 0;
+  while ((double)leaf_size * std::ldexp(1.0, 2 * k) < (double)n) ++k;
+  return k;
+}
+
+// Release factor panels and the matvec schedule (before re-packing).
+static void clear_factors(Handle& h) {
+  for (int l = 1; l <= h.kappa; ++l) {
+    Level& L = h.levels[(size_t)l];
+    h.release(L.U); L.U = nullptr;
+    h.release(L.V); L.V = nullptr;
+    h.release(L.d_tidx); L.d_tidx = nullptr;
+    h.release(L.d_ucolbase); L.d_ucolbase = nullptr;
+    h.release(L.d_upan_off); L.d_upan_off = nullptr;
+  }
+  h.release(h.d_aitems); h.d_aitems = nullptr;
+  h.release(h.d_ritems); h.d_ritems = nullptr;
+  h.release(h.d_t); h.d_t = nullptr;
+  h.release(h.d_tpart); h.d_tpart = nullptr;
+  h.n_aitems = h.n_ritems = 0;
+}
+
+static void set_partition(Handle& h) {
+  const int64_t nleaf = (int64_t)1 << (2 * h.kappa);
+  if (h.opts.row_end > 0) {
+    // snap an explicit row range to leaf boundaries
+    auto snap = [&](int64_t r) {
+      return (int64_t)(std::lower_bound(h.leaf_start.begin(), h.leaf_start.end(), (int32_t)r) -
+                       h.leaf_start.begin());
+    };
+    h.leaf_begin = std::min<int64_t>(snap(std::max<int64_t>(0, h.opts.row_begin)), nleaf);
+    h.leaf_end = std::min<int64_t>(snap(std::min<int64_t>(h.n, h.opts.row_end)), nleaf);
+    if (h.opts.row_end >= h.n) h.leaf_end = nleaf;
+  } else if (h.opts.world > 1) {
+    // contiguous Morton ranges of leaves with equal point shares (load model of
+    // Eq. eq:par, is proportional to the points for balanced trees)
+    auto cut = [&](int r) {
+      if (r <= 0) return (int64_t)0;
+      if (r >= h.opts.world) return nleaf;
+      const int64_t target = (h.n * r + h.opts.world / 2) / h.opts.world;
+      return (int64_t)(std::lower_bound(h.leaf_start.begin(), h.leaf_start.end(), (int32_t)target) -
+                       h.leaf_start.begin());
+    };
+    h.leaf_begin = std::min(cut(h.opts.rank), nleaf);
+    h.leaf_end = std::min(cut(h.opts.rank + 1), nleaf);
+  } else {
+    h.leaf_begin = 0;
+    h.leaf_end = nleaf;
+  }
+  h.row_begin = h.leaf_start[(size_t)h.leaf_begin];
+  h.row_end = h.leaf_start[(size_t)h.leaf_end];
+}
+
+static void skip_factors(Handle& h) {
+  for (int l = 1; l <= h.kappa; ++l) {
+    Level& L = h.levels[(size_t)l];
+    L.rank.assign((size_t)L.nblocks, -1);
+    L.truncated.assign((size_t)L.nblocks, 0);
+    std::vector<const double*> su((size_t)L.nblocks, nullptr), sv((size_t)L.nblocks, nullptr);
+    pack_level(h, L, su, sv);
+  }
+}
+
+static void do_matvec(Handle& h, const double* x, double* y, int order) {
+  if (order != H2D_ORDER_ORIGINAL && order != H2D_ORDER_TREE) throw Error{H2D_EINVAL, "bad order"};
+  if (!x || !y) throw Error{H2D_EINVAL, "null x or y"};
+  const bool part = h.row_begin != 0 || h.row_end != h.n;
+  if (order == H2D_ORDER_ORIGINAL && part)
+    throw Error{H2D_EINVAL, "ORIGINAL order needs a single-rank (full-range) handle"};
+  cudaStream_t s = h.stream;
+  const bool xdev = is_device_ptr(x), ydev = is_device_ptr(y);
+  const int64_t ylen = order == H2D_ORDER_ORIGINAL ? h.n : (h.row_end - h.row_begin);
+  cudaEvent_t e0 = nullptr;
+  if (h.timing) {
+    if (h.ev_used >= (int64_t)h.ev_pool.size()) {
+      cudaEvent_t e;
+      H2D_CUDA(cudaEventCreate(&e));
+      h.ev_pool.push_back(e);
+    }
+    e0 = h.ev_pool[(size_t)h.ev_used++];
+    H2D_CUDA(cudaEventRecord(e0, s));
+  }
+  const double* xin = x;
+  if (!xdev) {
+    if (!h.d_xbuf) h.d_xbuf = h.alloc<double>(h.n);
+    H2D_CUDA(cudaMemcpyAsync(h.d_xbuf, x, h.n * sizeof(double), cudaMemcpyHostToDevice, s));
+    xin = h.d_xbuf;
+  }
+  double* yout = y;
+  if (!ydev) {
+    if (!h.d_ybuf) h.d_ybuf = h.alloc<double>(h.n);
+    yout = h.d_ybuf;
+  }
+  const double* xt = xin;
+  if (order == H2D_ORDER_ORIGINAL) {
+    permute_in(h, xin, h.d_xtree);
+    xt = h.d_xtree;
+  }
+  matvec_tree(h, xt, yout, order, h.row_begin);
+  if (h.timing) h.timed_count++;
+  if (!ydev) {
+    H2D_CUDA(cudaMemcpyAsync(y, yout, ylen * sizeof(double), cudaMemcpyDeviceToHost, s));
+    H2D_CUDA(cudaStreamSynchronize(s));
+  } else if (!xdev) {
+    H2D_CUDA(cudaStreamSynchronize(s));  // x may be reused by the caller once we return
+  }
+}
+
+// ---------------------------------------------------------------- factor interchange (R11)
+struct FileHeader {
+  int64_t N;
+  int32_t kappa, kid;
+  double tol, c, scale, shift, lo_x, lo_y, side;
+  int32_t test_rank, reserved;
+};
+
+static void load_factors(Handle& h, const char* path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw Error{H2D_EFACTORS, std::string("cannot open ") + path};
+  char magic[8];
+  f.read(magic, 8);
+  if (!f || std::memcmp(magic, "H2DFAC01", 8) != 0) throw Error{H2D_EFACTORS, "bad magic"};
+  FileHeader hd{};
+  f.read((char*)&hd.N, 8);
+  f.read((char*)&hd.kappa, 4);
+  f.read((char*)&hd.kid, 4);
+  double d[7];
+  f.read((char*)d, 56);
+  f.read((char*)&hd.test_rank, 4);
+  f.read((char*)&hd.reserved, 4);
+  if (!f) throw Error{H2D_EFACTORS, "truncated header"};
+  if (hd.N != h.n || hd.kappa != h.kappa)
+    throw Error{H2D_EFACTORS, "file N/kappa do not match the handle"};
+  std::vector<int32_t> fperm((size_t)hd.N), perm((size_t)h.n);
+  f.read((char*)fperm.data(), hd.N * 4);
+  H2D_CUDA(cudaMemcpy(perm.data(), h.d_perm, h.n * 4, cudaMemcpyDeviceToHost));
+  if (fperm != perm) throw Error{H2D_EFACTORS, "file permutation does not match the handle's tree"};
+  clear_factors(h);
+  h.truncated = 0;
+  for (int l = 1; l <= h.kappa; ++l) {
+    Level& L = h.levels[(size_t)l];
+    int64_t nb = 0;
+    f.read((char*)&nb, 8);
+    if (!f || nb != L.nblocks) throw Error{H2D_EFACTORS, "block count mismatch at level " + std::to_string(l)};
+    std::vector<double> host;
+    std::vector<int64_t> uo((size_t)nb, -1), vo((size_t)nb, -1);
+    L.rank.assign((size_t)nb, -1);
+    L.truncated.assign((size_t)nb, 0);
+    for (int64_t X = 0; X < L.nbox; ++X) {
+      const int64_t m = h.box_end(l, X) - h.box_begin(l, X);
+      const bool keep = h.row_box_active(l, X);
+      for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
+        const int64_t Y = L.col[(size_t)e];
+        const int64_t n = h.box_end(l, Y) - h.box_begin(l, Y);
+        int32_t r = 0;
+        f.read((char*)&r, 4);
+        if (!f || r < 0) throw Error{H2D_EFACTORS, "bad rank"};
+        const size_t cnt = (size_t)r * (size_t)(m + n);
+        if (keep) {
+          L.rank[(size_t)e] = r;
+          uo[(size_t)e] = (int64_t)host.size();
+          vo[(size_t)e] = (int64_t)host.size() + (int64_t)r * m;
+          size_t o = host.size();
+          host.resize(o + cnt);
+          f.read((char*)(host.data() + o), cnt * 8);
+        } else {
+          f.seekg((std::streamoff)(cnt * 8), std::ios::cur);
+        }
+        if (!f) throw Error{H2D_EFACTORS, "truncated factors at level " + std::to_string(l)};
+      }
+    }
+    double* d = nullptr;
+    H2D_CUDA(cudaMalloc(&d, std::max<size_t>(1, host.size()) * 8));
+    if (!host.empty()) H2D_CUDA(cudaMemcpy(d, host.data(), host.size() * 8, cudaMemcpyHostToDevice));
+    std::vector<const double*> su((size_t)nb, nullptr), sv((size_t)nb, nullptr);
+    for (int64_t e = 0; e < nb; ++e)
+      if (uo[(size_t)e] >= 0) { su[(size_t)e] = d + uo[(size_t)e]; sv[(size_t)e] = d + vo[(size_t)e]; }
+    pack_level(h, L, su, sv);
+    H2D_CUDA(cudaFree(d));
+  }
+  finalize_schedule(h);
+}
+
+// Extract block e of level l from the panels: U (m x r col-major), V (n x r col-major).
+static void extract_block(Handle& h, int l, int64_t e, int* m, int* n, int* r, double* U, double* V) {
+  Level& L = h.levels[(size_t)l];
+  const int64_t X = (int64_t)(std::upper_bound(L.off.begin(), L.off.end(), (int32_t)e) - L.off.begin()) - 1;
+  const int64_t Y = L.col[(size_t)e];
+  const int64_t mm = h.box_end(l, X) - h.box_begin(l, X);
+  const int64_t nn = h.box_end(l, Y) - h.box_begin(l, Y);
+  const int rr = std::max<int32_t>(0, L.rank[(size_t)e]);
+  *m = (int)mm; *n = (int)nn; *r = rr;
+  if (rr == 0) return;
+  if (U)
+    H2D_CUDA(cudaMemcpy(U, L.U + L.upan_off[(size_t)X] + (int64_t)L.ucol[(size_t)e] * mm,
+                        mm * rr * 8, cudaMemcpyDeviceToHost));
+  if (V) {
+    std::vector<double> rm((size_t)(nn * rr));
+    if (nn > 0)
+      H2D_CUDA(cudaMemcpy2D(rm.data(), rr * 8, L.V + L.vpan_off[(size_t)Y] + L.vcol[(size_t)e],
+                            (size_t)L.vR[(size_t)Y] * 8, rr * 8, nn, cudaMemcpyDeviceToHost));
+    for (int64_t j = 0; j < nn; ++j)
+      for (int q = 0; q < rr; ++q) V[j + (int64_t)q * nn] = rm[(size_t)(j * rr + q)];
+  }
+}
+
+}  // namespace h2d
+
+using namespace h2d;
+
+struct hodlr2d_s {
+  Handle h;
+};
+
+#define H2D_TRY try {
+#define H2D_CATCH                                                   \
+  }                                                                 \
+  catch (const Error& err) {                                        \
+    set_error(err.code, err.msg);                                   \
+    return err.code;                                                \
+  }                                                                 \
+  catch (const std::bad_alloc&) {                                   \
+    set_error(H2D_ENOMEM, "host allocation failed");               \
+    return H2D_ENOMEM;                                              \
+  }                                                                 \
+  catch (const std::exception& ex) {                                \
+    set_error(H2D_ECUDA, ex.what());                                \
+    return H2D_ECUDA;                                               \
+  }
+
+extern "C" {
+
+void hodlr2d_default_options(hodlr2d_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->c = 1.0;
+  o->scale = 1.0;
+  o->shift = 0.0;
+  o->box_side = 0.0;
+  o->depth = -1;
+  o->max_rank = 128;
+  o->aca_consecutive = 2;
+  o->aca_trim = 2;
+  o->test_rank = 1;
+  o->stream = nullptr;
+  o->world = 1;
+  o->rank = 0;
+  o->row_begin = 0;
+  o->row_end = 0;
+  o->aca_scratch_bytes = 0;
+  o->timing = 0;
+  o->skip_aca = 0;
+}
+
+int hodlr2d_build(const double* points, int64_t n, int kernel_id, int leaf_size, double aca_tol,
+                  hodlr2d_t* out) {
+  hodlr2d_options o;
+  hodlr2d_default_options(&o);
+  return hodlr2d_build_ex(points, n, kernel_id, leaf_size, aca_tol, &o, out);
+}
+
+int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_size, double aca_tol,
+                     const hodlr2d_options* opts, hodlr2d_t* out) {
+  if (out) *out = nullptr;
+  hodlr2d_s* H = nullptr;
+  H2D_TRY
+  if (!out || !points || !opts) throw Error{H2D_EINVAL, "null argument"};
+  if (n < 1) throw Error{H2D_EINVAL, "n < 1"};
+  if (n > INT32_MAX) throw Error{H2D_EINVAL, "n >= 2^31 not supported"};
+  if (leaf_size < 1) throw Error{H2D_EINVAL, "leaf_size < 1"};
+  if (!(aca_tol > 0.0 && aca_tol < 1.0)) throw Error{H2D_EINVAL, "aca_tol not in (0, 1)"};
+  if (kernel_id != H2D_KERNEL_LOG && kernel_id != H2D_KERNEL_IMQ && kernel_id != H2D_KERNEL_ONE_OVER_R &&
+      kernel_id != H2D_KERNEL_TEST_LOWRANK)
+    throw Error{H2D_EINVAL, "unknown kernel_id"};
+  if (kernel_id == H2D_KERNEL_IMQ && !(opts->c > 0.0)) throw Error{H2D_EINVAL, "IMQ needs c > 0"};
+  if (opts->max_rank < 1 || opts->aca_consecutive < 1 || opts->aca_trim < 0 ||
+      opts->aca_trim > opts->aca_consecutive)
+    throw Error{H2D_EINVAL, "bad ACA options"};
+  if (opts->world < 1 || opts->rank < 0 || opts->rank >= opts->world)
+    throw Error{H2D_EINVAL, "bad world/rank"};
+  if (!std::isfinite(opts->scale) || !std::isfinite(opts->shift)) throw Error{H2D_EINVAL, "non-finite scale/shift"};
+  double t0 = now_s();
+  H = new hodlr2d_s();
+  Handle& h = H->h;
+  h.opts = *opts;
+  h.stream = (cudaStream_t)opts->stream;
+  H2D_CUDA(cudaGetDevice(&h.device));
+  h.kernel_id = kernel_id;
+  h.leaf_size = leaf_size;
+  h.tol = aca_tol;
+  h.n = n;
+  h.kp.id = kernel_id;
+  h.kp.inv_c2 = kernel_id == H2D_KERNEL_IMQ ? 1.0 / (opts->c * opts->c) : 0.0;
+  h.kp.scale = opts->scale;
+  h.kp.shift = opts->shift;
+  h.kp.test_rank = opts->test_rank;
+  h.kappa = opts->depth >= 0 ? opts->depth : depth_rule(n, leaf_size);
+  if (h.kappa > 15) throw Error{H2D_EINVAL, "depth > 15"};
+  if (h.kappa > H2D_MAX_LEVELS) throw Error{H2D_EINVAL, "depth > H2D_MAX_LEVELS"};
+  h.timing = opts->timing;
+  const double* d_pts = points;
+  double* tmp = nullptr;
+  if (!is_device_ptr(points)) {
+    H2D_CUDA(cudaMallocAsync(&tmp, n * 2 * sizeof(double), h.stream));
+    H2D_CUDA(cudaMemcpyAsync(tmp, points, n * 2 * sizeof(double), cudaMemcpyHostToDevice, h.stream));
+    d_pts = tmp;
+  }
+  build_tree(h, d_pts);
+  if (tmp) H2D_CUDA(cudaFreeAsync(tmp, h.stream));
+  build_lists(h);
+  set_partition(h);
+  h.tree_seconds = now_s() - t0;
+  if (opts->skip_aca) skip_factors(h); else run_aca(h);
+  finalize_schedule(h);
+  h.d_xtree = h.alloc<double>(n);
+  H2D_CUDA(cudaStreamSynchronize(h.stream));
+  h.build_seconds = now_s() - t0;
+  *out = H;
+  return h.truncated > 0 ? H2D_WTRUNC : H2D_OK;
+  }
+  catch (const Error& err) {
+    delete H;
+    set_error(err.code, err.msg);
+    return err.code;
+  }
+  catch (const std::bad_alloc&) {
+    delete H;
+    set_error(H2D_ENOMEM, "host allocation failed");
+    return H2D_ENOMEM;
+  }
+}
+
+int hodlr2d_matvec(hodlr2d_t H, const double* x, double* y) {
+  H2D_TRY
+  if (!H) throw Error{H2D_EINVAL, "null handle"};
+  do_matvec(H->h, x, y, H2D_ORDER_ORIGINAL);
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_matvec_ex(hodlr2d_t H, const double* x, double* y, int order) {
+  H2D_TRY
+  if (!H) throw Error{H2D_EINVAL, "null handle"};
+  do_matvec(H->h, x, y, order);
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
+  H2D_TRY
+  if (!H || !info) throw Error{H2D_EINVAL, "null argument"};
+  Handle& h = H->h;
+  std::memset(info, 0, sizeof(*info));
+  info->n = h.n;
+  info->kappa = h.kappa;
+  info->world = h.opts.world;
+  info->rank = h.opts.rank;
+  info->row_begin = h.row_begin;
+  info->row_end = h.row_end;
+  info->leaf_begin = h.leaf_begin;
+  info->leaf_end = h.leaf_end;
+  info->box_lo[0] = h.lo[0];
+  info->box_lo[1] = h.lo[1];
+  info->box_side = h.side;
+  int64_t uv = 0, vv = 0, built = 0, rsum = 0;
+  int rmax = 0;
+  for (int l = 1; l <= h.kappa; ++l) {
+    const Level& L = h.levels[(size_t)l];
+    info->blocks_per_level[l] = L.nblocks;
+    for (int32_t r : L.rank) {
+      if (r < 0) continue;
+      ++built;
+      rsum += r;
+      rmax = std::max(rmax, r);
+      info->rank_hist[std::min(r, 128)]++;
+    }
+    uv += L.u_values;
+    vv += L.v_values;
+  }
+  info->blocks_built = built;
+  info->rank_max = rmax;
+  info->u_values = uv;
+  info->v_values = vv;
+  int64_t near = 0;
+  for (int64_t X = h.leaf_begin; X < h.leaf_end; ++X) {
+    const int64_t m = h.leaf_start[(size_t)X + 1] - h.leaf_start[(size_t)X];
+    for (int32_t e = h.nf_off[(size_t)X]; e < h.nf_off[(size_t)X + 1]; ++e) {
+      const int32_t Y = h.nf_col[(size_t)e];
+      near += m * (h.leaf_start[(size_t)Y + 1] - h.leaf_start[(size_t)Y]);
+    }
+  }
+  info->near_pairs = near;
+  info->p2p_pairs = (double)near;
+  info->compression_ratio = ((double)(uv + vv) + (double)near) / ((double)h.n * (double)h.n);
+  info->truncated = h.truncated;
+  info->tree_seconds = h.tree_seconds;
+  info->aca_seconds = h.aca_seconds;
+  info->pack_seconds = h.pack_seconds;
+  info->build_seconds = h.build_seconds;
+  // algorithmic bytes: stage A reads V + x per chunk and writes t;
+  // stage B reads U + t (+ tidx) + near-field points/x and writes y.
+  const int64_t served = h.row_end - h.row_begin;
+  info->stageA_bytes = 8 * vv + 8 * (int64_t)h.n + 8 * h.t_len;
+  info->stageB_bytes = 8 * uv + 8 * h.t_len + 24 * (int64_t)h.n + 8 * served;
+  info->matvec_bytes = info->stageA_bytes + info->stageB_bytes;
+  info->device_bytes = (int64_t)h.device_bytes;
+  (void)rsum;
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_copy_tree(hodlr2d_t H, int32_t* perm, int32_t* leaf_start) {
+  H2D_TRY
+  if (!H) throw Error{H2D_EINVAL, "null handle"};
+  Handle& h = H->h;
+  if (perm) H2D_CUDA(cudaMemcpy(perm, h.d_perm, h.n * 4, cudaMemcpyDeviceToHost));
+  if (leaf_start) std::memcpy(leaf_start, h.leaf_start.data(), h.leaf_start.size() * 4);
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_copy_lists(hodlr2d_t H, int level, int32_t* off, int32_t* col) {
+  H2D_TRY
+  if (!H) throw Error{H2D_EINVAL, "null handle"};
+  Handle& h = H->h;
+  if (level < 0 || level > h.kappa) throw Error{H2D_EINVAL, "level out of range"};
+  const int32_t* d_off = level == 0 ? h.d_nf_off : h.levels[(size_t)level].d_off;
+  const int32_t* d_col = level == 0 ? h.d_nf_col : h.levels[(size_t)level].d_col;
+  const int64_t nbox = (int64_t)1 << (2 * (level == 0 ? h.kappa : level));
+  const int64_t tot = level == 0 ? h.nf_off[(size_t)nbox] : h.levels[(size_t)level].nblocks;
+  // copy from the DEVICE arrays (what the kernels use)
+  if (off) H2D_CUDA(cudaMemcpy(off, d_off, (nbox + 1) * 4, cudaMemcpyDeviceToHost));
+  if (col && tot) H2D_CUDA(cudaMemcpy(col, d_col, tot * 4, cudaMemcpyDeviceToHost));
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int64_t hodlr2d_num_blocks(hodlr2d_t H, int level) {
+  if (!H || level < 0 || level > H->h.kappa) return -1;
+  if (level == 0) return H->h.nf_off.empty() ? 0 : H->h.nf_off.back();
+  return H->h.levels[(size_t)level].nblocks;
+}
+
+int hodlr2d_copy_ranks(hodlr2d_t H, int level, int32_t* ranks) {
+  H2D_TRY
+  if (!H || !ranks) throw Error{H2D_EINVAL, "null argument"};
+  Handle& h = H->h;
+  if (level < 1 || level > h.kappa) throw Error{H2D_EINVAL, "level out of range"};
+  const Level& L = h.levels[(size_t)level];
+  std::memcpy(ranks, L.rank.data(), L.rank.size() * 4);
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_copy_block(hodlr2d_t H, int level, int64_t e, int* m, int* n, int* r, double* U,
+                       double* V) {
+  H2D_TRY
+  if (!H || !m || !n || !r) throw Error{H2D_EINVAL, "null argument"};
+  Handle& h = H->h;
+  if (level < 1 || level > h.kappa) throw Error{H2D_EINVAL, "level out of range"};
+  if (e < 0 || e >= h.levels[(size_t)level].nblocks) throw Error{H2D_EINVAL, "block out of range"};
+  extract_block(h, level, e, m, n, r, U, V);
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_load_factors(hodlr2d_t H, const char* path) {
+  H2D_TRY
+  if (!H || !path) throw Error{H2D_EINVAL, "null argument"};
+  load_factors(H->h, path);
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_save_factors(hodlr2d_t H, const char* path) {
+  H2D_TRY
+  if (!H || !path) throw Error{H2D_EINVAL, "null argument"};
+  Handle& h = H->h;
+  if (h.row_begin != 0 || h.row_end != h.n) throw Error{H2D_EINVAL, "row-restricted handle"};
+  std::ofstream f(path, std::ios::binary);
+  if (!f) throw Error{H2D_EFACTORS, std::string("cannot open ") + path};
+  f.write("H2DFAC01", 8);
+  int64_t N = h.n;
+  int32_t kap = h.kappa, kid = h.kernel_id, tr = h.opts.test_rank, res = 0;
+  double c = h.kp.inv_c2 > 0 ? 1.0 / std::sqrt(h.kp.inv_c2) : h.opts.c;
+  double d[7] = {h.tol, c, h.kp.scale, h.kp.shift, h.lo[0], h.lo[1], h.side};
+  f.write((char*)&N, 8);
+  f.write((char*)&kap, 4);
+  f.write((char*)&kid, 4);
+  f.write((char*)d, 56);
+  f.write((char*)&tr, 4);
+  f.write((char*)&res, 4);
+  std::vector<int32_t> perm((size_t)h.n);
+  H2D_CUDA(cudaMemcpy(perm.data(), h.d_perm, h.n * 4, cudaMemcpyDeviceToHost));
+  f.write((char*)perm.data(), h.n * 4);
+  for (int l = 1; l <= h.kappa; ++l) {
+    const Level& L = h.levels[(size_t)l];
+    int64_t nb = L.nblocks;
+    f.write((char*)&nb, 8);
+    std::vector<double> U, V;
+    for (int64_t e = 0; e < nb; ++e) {
+      int m, n, r;
+      extract_block(h, l, e, &m, &n, &r, nullptr, nullptr);
+      U.resize((size_t)m * r + 1);
+      V.resize((size_t)n * r + 1);
+      extract_block(h, l, e, &m, &n, &r, U.data(), V.data());
+      int32_t rr = r;
+      f.write((char*)&rr, 4);
+      if (r) {
+        f.write((char*)U.data(), (size_t)m * r * 8);
+        f.write((char*)V.data(), (size_t)n * r * 8);
+      }
+    }
+  }
+  if (!f) throw Error{H2D_EFACTORS, "write failed"};
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_set_timing(hodlr2d_t H, int on) {
+  if (!H) return H2D_EINVAL;
+  H->h.timing = on ? 1 : 0;
+  return H2D_OK;
+}
+
+int hodlr2d_stage_times(hodlr2d_t H, double* ms, int64_t* count, int reset) {
+  H2D_TRY
+  if (!H) throw Error{H2D_EINVAL, "null handle"};
+  Handle& h = H->h;
+  H2D_CUDA(cudaStreamSynchronize(h.stream));
+  // events come in groups of 5 per matvec: start, after A-prep, after A, after reduce, end
+  double acc[H2D_NUM_STAGES] = {0, 0, 0, 0};
+  const int64_t groups = h.ev_used / 5;
+  for (int64_t g = 0; g < groups; ++g) {
+    for (int k = 0; k < H2D_NUM_STAGES; ++k) {
+      float t = 0.f;
+      H2D_CUDA(cudaEventElapsedTime(&t, h.ev_pool[(size_t)(5 * g + k)], h.ev_pool[(size_t)(5 * g + k + 1)]));
+      acc[k] += t;
+    }
+  }
+  if (ms)
+    for (int k = 0; k < H2D_NUM_STAGES; ++k) ms[k] = acc[k];
+  if (count) *count = groups;
+  if (reset) { h.ev_used = 0; h.timed_count = 0; }
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_destroy(hodlr2d_t H) {
+  delete H;
+  return H2D_OK;
+}
+
+const char* hodlr2d_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,204 @@
+// Internal declarations of the B200 HODLR2D library (not part of the C ABI).
+// Product code only: nothing here is shared with oracle/ (DESIGN.md §Independence).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/hodlr2d.h"
+
+namespace h2d {
+
+// ------------------------------------------------------------------ errors
+struct Error {
+  int code;
+  std::string msg;
+};
+void set_error(int code, const std::string& msg);
+#define H2D_CUDA(call)                                                                     \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      throw ::h2d::Error{_e == cudaErrorMemoryAllocation ? H2D_ENOMEM : H2D_ECUDA,        \
+                         std::string(#call) + ": " + cudaGetErrorString(_e) + " at " +    \
+                             __FILE__ + ":" + std::to_string(__LINE__)};                  \
+  } while (0)
+#define H2D_LAUNCH_CHECK() H2D_CUDA(cudaGetLastError())
+
+// ------------------------------------------------------------------ kernel entries
+struct KernelParams {
+  int id;          // H2D_KERNEL_*
+  double inv_c2;   // 1 / c^2 (IMQ)
+  double scale;    // A = shift I + scale K
+  double shift;
+  int test_rank;
+};
+
+// K(p, q) for r^2 = |p - q|^2; K(r = 0) := K0 (R8) by distance, not by index.
+__device__ __forceinline__ double kernel_eval(const KernelParams& k, double px, double py,
+                                              double qx, double qy) {
+  double dx = px - qx, dy = py - qy;
+  double r2 = fma(dx, dx, dy * dy);
+  if (k.id == H2D_KERNEL_LOG) {
+    return r2 > 0.0 ? 0.5 * log(r2) : 0.0;
+  } else if (k.id == H2D_KERNEL_IMQ) {
+    return rsqrt(fma(r2, k.inv_c2, 1.0));
+  } else if (k.id == H2D_KERNEL_ONE_OVER_R) {
+    return r2 > 0.0 ? rsqrt(r2) : 0.0;
+  } else {
+    double acc = 0.0;
+    for (int s = 0; s < k.test_rank; ++s)
+      acc = fma(cos((s + 1) * px + 0.5 * s * py), cos((s + 1) * qx + 0.5 * s * qy), acc);
+    return acc;
+  }
+}
+
+// ------------------------------------------------------------------ operator storage
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Level {
+  int l = 0;
+  int64_t nbox = 0;          // 4^l
+  int64_t nblocks = 0;       // directed blocks (CSR length)
+  // lists (device + host copy)
+  int32_t* d_off = nullptr;  // [nbox + 1]
+  int32_t* d_col = nullptr;  // [nblocks]
+  std::vector<int32_t> off, col;
+  std::vector<int32_t> trans;  // block id of (Y, X) for block (X, Y)
+  // per block (host): rank, built flag, panel columns
+  std::vector<int32_t> rank;   // -1 = not built on this rank
+  std::vector<uint8_t> truncated;
+  std::vector<int32_t> ucol;   // first column inside the U panel of the row box
+  std::vector<int32_t> vcol;   // first column inside the V panel of the column box
+  // panels (device): U panel of row box X: col-major m_X x R_X at U + upan_off[X];
+  // V panel of column box Y: row-major n_Y x RV_Y at V + vpan_off[Y].
+  double* U = nullptr;
+  double* V = nullptr;
+  int64_t u_values = 0, v_values = 0;
+  std::vector<int64_t> upan_off, vpan_off;  // per box
+  std::vector<int32_t> ucolbase;            // per box + 1 (prefix of R_X)
+  std::vector<int32_t> vR;                  // per box RV_Y
+  std::vector<int64_t> t_off;               // per box: t of column box Y (global t index)
+  int32_t* d_ucolbase = nullptr;            // [nbox + 1]
+  int64_t* d_upan_off = nullptr;            // [nbox]
+  int32_t* d_tidx = nullptr;                // [sum R_X]: t index of every U-panel column
+};
+
+// Stage-A work item: one row chunk of one V panel.
+struct AItem {
+  int64_t v_off;   // element offset of the chunk's first row inside the level V array
+  int64_t x_off;   // TREE index of the chunk's first row
+  int32_t nrows;
+  int32_t R;       // panel width RV_Y
+  int32_t out;     // output index (into t or the partial buffer)
+  int32_t level;
+};
+// Reduction of multi-chunk partials: t[t_off + q] = sum_c part[p_off + c*R + q]
+struct RItem {
+  int32_t t_off;
+  int32_t p_off;
+  int32_t R;
+  int32_t nchunks;
+};
+
+struct LevelPtrs {
+  const double* U[H2D_MAX_LEVELS + 1];
+  const double* V[H2D_MAX_LEVELS + 1];
+  const int32_t* ucolbase[H2D_MAX_LEVELS + 1];
+  const int64_t* upan_off[H2D_MAX_LEVELS + 1];
+  const int32_t* tidx[H2D_MAX_LEVELS + 1];
+};
+
+struct Handle {
+  int device = 0;
+  cudaStream_t stream = 0;
+  hodlr2d_options opts{};
+  KernelParams kp{};
+  int kernel_id = 0;
+  int leaf_size = 0;
+  double tol = 0;
+  int64_t n = 0;
+  int kappa = 0;
+  double lo[2] = {0, 0}, side = 1;
+  int64_t row_begin = 0, row_end = 0;     // served TREE rows
+  int64_t leaf_begin = 0, leaf_end = 0;   // served leaves
+  // tree (device)
+  double* d_px = nullptr;
+  double* d_py = nullptr;
+  int32_t* d_perm = nullptr;
+  int32_t* d_leaf_start = nullptr;
+  std::vector<int32_t> leaf_start;        // host copy
+  // near field (device + host)
+  int32_t* d_nf_off = nullptr;
+  int32_t* d_nf_col = nullptr;
+  std::vector<int32_t> nf_off, nf_col;
+  // levels 1..kappa
+  std::vector<Level> levels;
+  // stage A / reduce schedule
+  AItem* d_aitems = nullptr;
+  int64_t n_aitems = 0;
+  RItem* d_ritems = nullptr;
+  int64_t n_ritems = 0;
+  double* d_t = nullptr;                  // all t values
+  int64_t t_len = 0;
+  double* d_tpart = nullptr;              // multi-chunk partials
+  int64_t tpart_len = 0;
+  LevelPtrs lp{};
+  int rmax_panel = 1;                     // widest U panel (smem size of stage B)
+  // matvec work buffers
+  double* d_xtree = nullptr;              // [n]
+  double* d_ybuf = nullptr;               // [n] staging for host y
+  double* d_xbuf = nullptr;               // [n] staging for host x
+  // stats
+  double tree_seconds = 0, aca_seconds = 0, pack_seconds = 0, build_seconds = 0;
+  int64_t truncated = 0;
+  // timing
+  int timing = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  int64_t ev_used = 0;
+  int64_t timed_count = 0;
+  double stage_ms[H2D_NUM_STAGES] = {0, 0, 0, 0};
+  // allocations
+  std::vector<void*> allocs;
+  size_t device_bytes = 0;
+
+  int64_t box_begin(int l, int64_t b) const {
+    return leaf_start[(size_t)(b << (2 * (kappa - l)))];
+  }
+  int64_t box_end(int l, int64_t b) const {
+    return leaf_start[(size_t)((b + 1) << (2 * (kappa - l)))];
+  }
+  bool row_box_active(int l, int64_t b) const {
+    return box_begin(l, b) < row_end && box_end(l, b) > row_begin;
+  }
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    H2D_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    allocs.push_back(p);
+    device_bytes += count * sizeof(T);
+    return static_cast<T*>(p);
+  }
+  void release(void* p);
+  ~Handle();
+};
+
+// ------------------------------------------------------------------ host drivers
+void build_tree(Handle& h, const double* d_points);              // tree.cu (G1-G4)
+void build_lists(Handle& h);                                      // tree.cu (G5)
+void run_aca(Handle& h);                                          // aca.cu (G6) + pack (G7)
+// Pack the given per-block factor sources of one level into panels (apply.cu).
+void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
+                const std::vector<const double*>& srcV);
+void finalize_schedule(Handle& h);                                // apply.cu
+void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out,
+                 int64_t y_row0);                                 // apply.cu (S7-S9)
+void permute_in(Handle& h, const double* d_x, double* d_xtree);   // apply.cu (S10)
+
+}  // namespace h2d
