@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""HODLR2D fp64 matvec benchmark (BASELINE.json metric: matvecs/sec at N = 2^20..2^24).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+One step = one HODLR2D matvec (Alg. 2: every row of SURVEY §8(a) S7-S10 on
+the hot path) of a fresh seeded x over the config's N points; the operator is built once
+before timing (build seconds reported separately).  N = 1: the whole matvec on one GPU.
+N > 1 (torchrun): contiguous Morton row ranges per rank, one NCCL all-gather of x per
+matvec, max over ranks; total work is fixed -> "scaling": "strong".
+
+Rank 0 prints ONE JSON line.  --impl reference times the CPU oracle (oracle/) on a
+bounded Morton slice of the same workload (this tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=sorted(W.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.p = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        busy = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- oracle arm
+
+def oracle_sample(cfg, threads=None):
+    """Build the oracle restricted to the rows of Morton box 0 at level 2 (1/16 of the rows)."""
+    import oracle
+    if threads:
+        oracle.set_threads(threads)
+    pts = W.config_points(cfg)
+    kappa = oracle.depth(cfg.n, cfg.leaf_size)
+    lvl = min(2, kappa)
+    _, _, ls = oracle.tree(pts, cfg.box_lo, cfg.box_side, kappa)
+    rows = int(ls[1 << (2 * (kappa - lvl))])
+    t0 = time.time()
+    op = oracle.Operator(pts, cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c, scale=cfg.scale,
+                         shift=cfg.shift, box_lo=cfg.box_lo, box_side=cfg.box_side,
+                         row_range=(0, rows))
+    build_s = time.time() - t0
+    frac = rows / cfg.n
+    desc = (f"oracle (C++ -O2, OpenMP) restricted to TREE rows [0, {rows}) = Morton box 0 of "
+            f"level {lvl} ({frac:.4f} of the rows); matvec time extrapolated x{1 / frac:.1f} "
+            f"(its V^T x work at levels < {lvl} is whole-block, so the extrapolation slightly "
+            f"overstates the oracle's time)")
+    return op, frac, build_s, desc
+
+
+def time_oracle(op, cfg, frac, steps, warmup):
+    xs = [W.config_x(cfg, k) for k in range(min(steps + warmup, 4))]
+    for k in range(warmup):
+        op.matvec(xs[k % len(xs)])
+    ts = []
+    for k in range(steps):
+        t0 = time.perf_counter()
+        op.matvec(xs[k % len(xs)])
+        ts.append(time.perf_counter() - t0)
+    t_full = statistics.mean(ts) / frac
+    return 1.0 / t_full, t_full
+
+
+def cpu_baseline(cfg):
+    import oracle
+    op, frac, build_s, desc = oracle_sample(cfg)
+    value, _ = time_oracle(op, cfg, frac, 5, 1)
+    return {"value": value, "unit": "matvecs/s", "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": desc, "sample_build_seconds": round(build_s, 3)}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    op, frac, build_s, desc = oracle_sample(cfg)
+    value, t_full = time_oracle(op, cfg, frac, args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": "HODLR2D fp64 matvecs/sec", "value": value,
+        "unit": "matvecs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_full * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(cfg, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "matvecs/s", "cores": oracle.max_threads(),
+                         "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": "matvecs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, ngpu):
+    kname = {0: "log", 1: "imq", 2: "one_over_r"}[cfg.kernel]
+    return {"workload": f"{cfg.name}: N={cfg.n} {cfg.points} points, kernel {kname}"
+                        + (f" c={cfg.c}" if cfg.kernel == 1 else "")
+                        + (f", A = {cfg.shift:g} I + {cfg.scale:g} K" if cfg.shift or cfg.scale != 1 else "")
+                        + f", leaf {cfg.leaf_size}, ACA tol {cfg.tol:g}, fresh x per matvec",
+            "n_points": cfg.n, "leaf_size": cfg.leaf_size, "aca_tol": cfg.tol,
+            "parallelism": f"morton-rows{ngpu}" if ngpu > 1 else "single",
+            "l2": "factor stream (>= 20 GB) far exceeds the 126 MB L2; no flush needed"}
+
+
+# ---------------------------------------------------------------------------- GPU arm
+
+def run_ours(args, cfg):
+    import torch
+    import paper_2204_05536_b200 as h2d
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    pts = W.config_points(cfg)
+    d_pts = torch.from_numpy(pts).cuda()
+    t0 = time.time()
+    op = h2d.Hodlr2d.build(d_pts, cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c, scale=cfg.scale,
+                           shift=cfg.shift, box_lo=cfg.box_lo, box_side=cfg.box_side,
+                           world=world, rank=rank, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    del d_pts
+    inf = op.info()
+    nx = min(args.steps + args.warmup, 100)
+    # fresh x per matvec, generated on the host (seeded) and resident in HBM before timing
+    if world == 1:
+        xs = torch.stack([torch.from_numpy(W.config_x(cfg, k)) for k in range(nx)]).cuda()
+        y = torch.empty(cfg.n, dtype=torch.float64, device="cuda")
+
+        def step(k):
+            op.matvec_raw(xs[k % nx].data_ptr(), y.data_ptr(), h2d.ORDER_ORIGINAL)
+    else:
+        perm, _ = op.tree()
+        rb, re_ = inf["row_begin"], inf["row_end"]
+        cnt = torch.tensor([re_ - rb], device="cuda")
+        allc = [torch.zeros_like(cnt) for _ in range(world)]
+        dist.all_gather(allc, cnt)
+        cmax = int(max(int(c.item()) for c in allc))
+        # each rank owns x_tree[rb:re]; the gathered [world x cmax] buffer is unpadded by the
+        # library (ORDER_GATHERED)
+        xs = torch.zeros(nx, cmax, dtype=torch.float64, device="cuda")
+        for k in range(nx):
+            xk = W.config_x(cfg, k)[perm][rb:re_]
+            xs[k, : re_ - rb] = torch.from_numpy(xk)
+        xg = torch.empty(world * cmax, dtype=torch.float64, device="cuda")
+        y = torch.empty(re_ - rb, dtype=torch.float64, device="cuda")
+        assert cmax == inf["gather_stride"], (cmax, inf["gather_stride"])
+
+        def step(k):
+            dist.all_gather_into_tensor(xg, xs[k % nx])
+            op.matvec_raw(xg.data_ptr(), y.data_ptr(), h2d.ORDER_GATHERED)
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    op.stage_times(reset=True)
+    op.set_timing(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ev0.record(stream)
+        for k in range(args.steps):
+            step(args.warmup + k)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    op.set_timing(False)
+    ms = ev0.elapsed_time(ev1)
+    stages, cnt = op.stage_times(reset=True)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = 1e3 / ms_step  # whole-job matvecs/s (each matvec covers all N rows)
+
+    # roofline: dominant kernel, algorithmic bytes / its CUDA-event duration on this stream
+    peak, peak_kind = peaks()
+    a_ms = stages["stageA_VTx"] / max(cnt, 1)
+    b_ms = stages["stageB_Ut_p2p"] / max(cnt, 1)
+    if b_ms >= a_ms:
+        dom, dom_ms, dom_bytes = "stageB_Ut_p2p", b_ms, inf["stageB_bytes"]
+    else:
+        dom, dom_ms, dom_bytes = "stageA_VTx", a_ms, inf["stageA_bytes"]
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "traffic": None, "bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4),
+            "stage_ms_per_matvec": {k: round(v / max(cnt, 1), 4) for k, v in stages.items()},
+            "whole_matvec_frac": round(inf["matvec_bytes"] / (ms_step * 1e-3) / 1e9 / peak, 4)}
+
+    # e2e through the public API with host (pinned) buffers, copies inside the timed region
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        xh = torch.empty(cfg.n, dtype=torch.float64).pin_memory()
+        yh = torch.empty(cfg.n, dtype=torch.float64).pin_memory()
+        xh.copy_(xs[0].cpu())
+        for _ in range(2):
+            op.matvec_raw(xh.data_ptr(), yh.data_ptr(), h2d.ORDER_ORIGINAL)
+        torch.cuda.synchronize()
+        ke = max(10, args.steps // 2)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ke):
+            op.matvec_raw(xh.data_ptr(), yh.data_ptr(), h2d.ORDER_ORIGINAL)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e = {"value": 1e3 * ke / e0.elapsed_time(e1), "unit": "matvecs/s",
+               "h2d_bytes_per_step": 8 * cfg.n, "d2h_bytes_per_step": 8 * cfg.n}
+
+    if rank == 0:
+        line = {
+            "metric": "HODLR2D fp64 matvecs/sec", "value": value, "unit": "matvecs/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(cfg, world),
+            "points_matvecs_per_s": value * cfg.n,
+            "build_seconds": round(build_s, 3),
+            "operator": {k: inf[k] for k in ("kappa", "rank_max", "u_values", "v_values", "near_pairs",
+                                               "compression_ratio", "truncated", "matvec_bytes",
+                                               "tree_seconds", "aca_seconds", "pack_seconds")},
+            "roofline": roof, "e2e": e2e,
+            "gpu_launches": args.steps * launches_per_matvec(inf, world),
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline(cfg)
+            except Exception as ex:  # the GPU number stands on its own
+                line["cpu_baseline"] = {"error": str(ex)}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def launches_per_matvec(inf, world):
+    # permute-in (1-GPU ORIGINAL order) or unpad (gathered), stage A, t-reduce, stage B
+    return 4
+
+
+def main():
+    args = parse()
+    cfg = W.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

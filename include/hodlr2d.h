@@ -60,7 +60,14 @@ enum {
                                    phi_s(p) = cos((s+1) p.x + 0.5 s p.y) (exact rank)     */
 };
 
-enum { H2D_ORDER_ORIGINAL = 0, H2D_ORDER_TREE = 1 };
+/* Orderings of x and y in hodlr2d_matvec_ex:
+ *   ORIGINAL : x, y full length N in the caller's point order (single-rank handles);
+ *   TREE     : x full length N in TREE order; y = rows [row_begin, row_end) in TREE order;
+ *   GATHERED : x = world slots of info.gather_stride values, slot r holding rank r's TREE
+ *              rows [row_begin_r, row_end_r) followed by padding — exactly the output of one
+ *              equal-count all-gather (ncclAllGather / all_gather_into_tensor) of every
+ *              rank's padded slice; y as for TREE. */
+enum { H2D_ORDER_ORIGINAL = 0, H2D_ORDER_TREE = 1, H2D_ORDER_GATHERED = 2 };
 
 /* Options of hodlr2d_build_ex.  Always start from hodlr2d_default_options(). */
 typedef struct {
@@ -71,8 +78,8 @@ typedef struct {
   double box_side;        /* root square side; <= 0 -> bounding square of the points (R2)   */
   int depth;              /* kappa; < 0 -> R1 depth rule from leaf_size        (default -1) */
   int max_rank;           /* ACA rank cap per block; hitting it sets H2D_WTRUNC (def. 128)  */
-  int aca_consecutive;    /* tolerance hits in a row that stop ACA (R7)        (default 2)  */
-  int aca_trim;           /* streak terms dropped on a tolerance stop (R7)     (default 2)  */
+  int aca_consecutive;    /* tolerance hits in a row that stop ACA (R7)        (default 3)  */
+  int aca_trim;           /* streak terms dropped on a tolerance stop (R7)     (default 3)  */
   int test_rank;          /* H2D_KERNEL_TEST_LOWRANK only                      (default 1)  */
   void* stream;           /* cudaStream_t for all work                         (default 0)  */
   int world;              /* Morton-range partition: number of ranks           (default 1)  */
@@ -108,6 +115,7 @@ typedef struct {
   int64_t stageA_bytes, stageB_bytes;
   double p2p_pairs;          /* near-field pair evaluations per matvec                */
   int64_t device_bytes;      /* device memory held by the handle                      */
+  int64_t gather_stride;     /* max rows over ranks (slot size of H2D_ORDER_GATHERED) */
 } hodlr2d_info;
 
 /* Fill *opts with the defaults listed above. */
@@ -129,9 +137,10 @@ int hodlr2d_matvec(hodlr2d_t h, const double* x, double* y);
 
 /* y = A x with an explicit ordering.  order = H2D_ORDER_TREE: x is the full length-N
  * vector in TREE order and y receives rows [row_begin, row_end) in TREE order
- * (length row_end - row_begin).  order = H2D_ORDER_ORIGINAL: as hodlr2d_matvec
- * (single-rank handles only).  For multi-rank handles the caller assembles x_tree
- * (e.g. one NCCL all-gather of the rank slices). */
+ * (length row_end - row_begin).  order = H2D_ORDER_GATHERED: x is the padded
+ * all-gather buffer (world * info.gather_stride values, see the enum above); the library
+ * unpads it into its TREE-order x inside the matvec.  order = H2D_ORDER_ORIGINAL: as
+ * hodlr2d_matvec (single-rank handles only). */
 int hodlr2d_matvec_ex(hodlr2d_t h, const double* x, double* y, int order);
 
 /* Statistics of the built operator (host struct). */
@@ -171,6 +180,15 @@ int hodlr2d_stage_times(hodlr2d_t h, double* ms, int64_t* count, int reset);
 
 /* Enable / disable stage timing after the build. */
 int hodlr2d_set_timing(hodlr2d_t h, int on);
+
+/* Host-only helper (no device work; callable without a GPU): the Morton-range partition
+ * every rank of a world uses.  leaf_start: the tree's 4^kappa + 1 leaf offsets (see
+ * hodlr2d_copy_tree); n = leaf_start[4^kappa].  Rank r serves leaves
+ * [*leaf_begin, *leaf_end): contiguous Morton ranges cut at the leaf boundary nearest to
+ * r * n / world points (equal point shares; Eq. eq:par's per-node load, is
+ * proportional to the points for the balanced trees of the configs). */
+int hodlr2d_partition(const int32_t* leaf_start, int kappa, int world, int rank,
+                      int64_t* leaf_begin, int64_t* leaf_end);
 
 /* Release every resource of the handle.  NULL is accepted. */
 int hodlr2d_destroy(hodlr2d_t h);

@@ -137,7 +137,7 @@ def near_lists(kappa: int):
     return off, col
 
 
-def aca_dense(A: np.ndarray, tol: float, max_rank: int = 128, consecutive: int = 2, trim: int = 2):
+def aca_dense(A: np.ndarray, tol: float, max_rank: int = 128, consecutive: int = 3, trim: int = 3):
     A = np.asfortranarray(A, dtype=np.float64)
     m, n = A.shape
     kmax = min(m, n, max_rank)
@@ -173,7 +173,7 @@ class Operator:
 
     def __init__(self, points, kernel_id=0, leaf_size=64, tol=1e-10, c=1.0, scale=1.0, shift=0.0,
                  test_rank=1, box_lo=(0.0, 0.0), box_side=0.0, depth=-1, max_rank=128,
-                 consecutive=2, trim=2, row_range=None):
+                 consecutive=3, trim=3, row_range=None):
         self.points = np.ascontiguousarray(points, dtype=np.float64)
         self.n = self.points.shape[0]
         lo, hi = row_range if row_range is not None else (0, 0)

@@ -665,6 +665,7 @@ int oracle_matvec(void* h, const double* x_in, double* y_out, int order) {
                     t[(size_t)q] = acc;
                 }
                 for (int i = 0; i < B.m; ++i) {        // b(X) += U t
+                    if (B.r0 + i < o->row_lo || B.r0 + i >= o->row_hi) continue;  // rows served
                     double acc = 0.0;
                     for (int q = 0; q < r; ++q) acc += B.f.U[(size_t)q * B.m + i] * t[(size_t)q];
                     b[(size_t)(B.r0 + i)] += acc;

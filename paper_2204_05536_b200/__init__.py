@@ -28,7 +28,8 @@ H2D_OK, H2D_WTRUNC = 0, 1
 H2D_EINVAL, H2D_EOUTOFBOX, H2D_ECOINCIDENT, H2D_ENOMEM = -1, -2, -3, -4
 H2D_ECUDA, H2D_ENCCL, H2D_EFACTORS = -5, -6, -7
 KERNELS = {"log": 0, "imq": 1, "one_over_r": 2, "test_lowrank": 100}
-ORDER_ORIGINAL, ORDER_TREE = 0, 1
+ORDER_ORIGINAL, ORDER_TREE, ORDER_GATHERED = 0, 1, 2
+ORDERS = {"original": 0, "tree": 1, "gathered": 2}
 MAX_LEVELS = 16
 NUM_STAGES = 4
 STAGE_NAMES = ("permute_in", "stageA_VTx", "t_reduce", "stageB_Ut_p2p")
@@ -39,7 +40,7 @@ ABI_FUNCTIONS = (
     "hodlr2d_matvec_ex", "hodlr2d_get_info", "hodlr2d_copy_tree", "hodlr2d_copy_lists",
     "hodlr2d_num_blocks", "hodlr2d_copy_ranks", "hodlr2d_copy_block", "hodlr2d_load_factors",
     "hodlr2d_save_factors", "hodlr2d_stage_times", "hodlr2d_set_timing", "hodlr2d_destroy",
-    "hodlr2d_last_error",
+    "hodlr2d_last_error", "hodlr2d_partition",
 )
 
 
@@ -70,7 +71,7 @@ class Info(C.Structure):
         ("tree_seconds", C.c_double), ("aca_seconds", C.c_double), ("pack_seconds", C.c_double),
         ("build_seconds", C.c_double), ("matvec_bytes", C.c_int64),
         ("stageA_bytes", C.c_int64), ("stageB_bytes", C.c_int64), ("p2p_pairs", C.c_double),
-        ("device_bytes", C.c_int64),
+        ("device_bytes", C.c_int64), ("gather_stride", C.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -119,6 +120,7 @@ def lib() -> C.CDLL:
             L.hodlr2d_set_timing.argtypes = [vp, i]
             L.hodlr2d_destroy.argtypes = [vp]
             L.hodlr2d_last_error.restype = C.c_char_p
+            L.hodlr2d_partition.argtypes = [vp, i, i, i, C.POINTER(i64), C.POINTER(i64)]
             _lib = L
     return _lib
 
@@ -146,6 +148,14 @@ def _ptr(a) -> int:
     return a.data_ptr()
 
 
+def partition(leaf_start: np.ndarray, kappa: int, world: int, rank: int):
+    """hodlr2d_partition (host only): leaves [begin, end) served by `rank` of `world`."""
+    ls = np.ascontiguousarray(leaf_start, dtype=np.int32)
+    lb, le = C.c_int64(), C.c_int64()
+    _check(lib().hodlr2d_partition(ls.ctypes.data, kappa, world, rank, C.byref(lb), C.byref(le)))
+    return lb.value, le.value
+
+
 def default_options() -> Options:
     o = Options()
     lib().hodlr2d_default_options(C.byref(o))
@@ -165,7 +175,7 @@ class Hodlr2d:
     @classmethod
     def build(cls, points, kernel="log", leaf_size=64, aca_tol=1e-10, *, c=1.0, scale=1.0,
               shift=0.0, box_lo=(0.0, 0.0), box_side=0.0, depth=-1, max_rank=128,
-              aca_consecutive=2, aca_trim=2, test_rank=1, stream=None, world=1, rank=0,
+              aca_consecutive=3, aca_trim=3, test_rank=1, stream=None, world=1, rank=0,
               row_range=None, aca_scratch_bytes=0, timing=False, skip_aca=False):
         """hodlr2d_build_ex.  ``points``: (N, 2) float64 torch tensor (CUDA or CPU) or numpy array."""
         kid = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
@@ -225,9 +235,9 @@ class Hodlr2d:
     # -------------------------------------------------------------- matvec
     def matvec(self, x, out=None, order="original"):
         """hodlr2d_matvec / hodlr2d_matvec_ex.  Returns ``out`` (allocated like x if None)."""
-        o = ORDER_ORIGINAL if order == "original" else ORDER_TREE
+        o = ORDERS[order]
         if out is None:
-            if o == ORDER_TREE:
+            if o != ORDER_ORIGINAL:
                 inf = self.info()
                 m = inf["row_end"] - inf["row_begin"]
             else:

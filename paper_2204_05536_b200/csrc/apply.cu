@@ -256,7 +256,25 @@ __global__ void permute_in_kernel(const double* __restrict__ x, const int32_t* _
     xt[s] = x[perm[s]];
 }
 
+// x_tree[s] = xg[r * stride + (s - rows[r])] for the rank r owning TREE row s.
+__global__ void unpad_kernel(const double* __restrict__ xg, const int64_t* __restrict__ rows,
+                             int world, int64_t stride, int64_t n, double* __restrict__ xt) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int r = 0;
+    while (r + 1 < world && rows[r + 1] <= s) ++r;
+    xt[s] = xg[r * stride + (s - rows[r])];
+  }
+}
+
 }  // namespace
+
+void unpad_gathered(Handle& h, const double* d_xg, double* d_xtree) {
+  int blocks = (int)std::min<int64_t>((h.n + 255) / 256, 148 * 16);
+  unpad_kernel<<<blocks, 256, 0, h.stream>>>(d_xg, h.d_rank_rows, h.opts.world, h.gather_stride, h.n,
+                                             d_xtree);
+  H2D_LAUNCH_CHECK();
+}
 
 // Pack one level's factors (per-block sources, column-major U_b m x r and V_b n x r) into
 // the U / V panels and fill the level's panel metadata.

@@ -71,6 +71,22 @@ static void clear_factors(Handle& h) {
   h.n_aitems = h.n_ritems = 0;
 }
 
+// Contiguous Morton ranges of leaves with equal point shares: the cut before rank r is the
+// first leaf whose start is >= r * n / world (rounded).
+static void partition_leaves(const int32_t* ls, int kappa, int world, int rank, int64_t* lb,
+                             int64_t* le) {
+  const int64_t nleaf = (int64_t)1 << (2 * kappa);
+  const int64_t n = ls[nleaf];
+  auto cut = [&](int r) {
+    if (r <= 0) return (int64_t)0;
+    if (r >= world) return nleaf;
+    const int64_t target = (n * r + world / 2) / world;
+    return (int64_t)(std::lower_bound(ls, ls + nleaf + 1, (int32_t)target) - ls);
+  };
+  *lb = std::min(cut(rank), nleaf);
+  *le = std::min(cut(rank + 1), nleaf);
+}
+
 static void set_partition(Handle& h) {
   const int64_t nleaf = (int64_t)1 << (2 * h.kappa);
   if (h.opts.row_end > 0) {
@@ -82,21 +98,20 @@ static void set_partition(Handle& h) {
     h.leaf_begin = std::min<int64_t>(snap(std::max<int64_t>(0, h.opts.row_begin)), nleaf);
     h.leaf_end = std::min<int64_t>(snap(std::min<int64_t>(h.n, h.opts.row_end)), nleaf);
     if (h.opts.row_end >= h.n) h.leaf_end = nleaf;
-  } else if (h.opts.world > 1) {
-    // contiguous Morton ranges of leaves with equal point shares (load model of
-    // Eq. eq:par, is proportional to the points for balanced trees)
-    auto cut = [&](int r) {
-      if (r <= 0) return (int64_t)0;
-      if (r >= h.opts.world) return nleaf;
-      const int64_t target = (h.n * r + h.opts.world / 2) / h.opts.world;
-      return (int64_t)(std::lower_bound(h.leaf_start.begin(), h.leaf_start.end(), (int32_t)target) -
-                       h.leaf_start.begin());
-    };
-    h.leaf_begin = std::min(cut(h.opts.rank), nleaf);
-    h.leaf_end = std::min(cut(h.opts.rank + 1), nleaf);
   } else {
-    h.leaf_begin = 0;
-    h.leaf_end = nleaf;
+    partition_leaves(h.leaf_start.data(), h.kappa, h.opts.world, h.opts.rank, &h.leaf_begin,
+                     &h.leaf_end);
+    // every rank's rows: layout of the padded all-gather (H2D_ORDER_GATHERED)
+    h.rank_rows.assign((size_t)h.opts.world + 1, 0);
+    for (int r = 0; r < h.opts.world; ++r) {
+      int64_t lb = 0, le = 0;
+      partition_leaves(h.leaf_start.data(), h.kappa, h.opts.world, r, &lb, &le);
+      h.rank_rows[(size_t)r] = h.leaf_start[(size_t)lb];
+      h.rank_rows[(size_t)r + 1] = h.leaf_start[(size_t)le];
+      h.gather_stride = std::max<int64_t>(h.gather_stride, h.leaf_start[(size_t)le] - h.leaf_start[(size_t)lb]);
+    }
+    h.d_rank_rows = h.alloc<int64_t>(h.rank_rows.size());
+    H2D_CUDA(cudaMemcpy(h.d_rank_rows, h.rank_rows.data(), h.rank_rows.size() * 8, cudaMemcpyHostToDevice));
   }
   h.row_begin = h.leaf_start[(size_t)h.leaf_begin];
   h.row_end = h.leaf_start[(size_t)h.leaf_end];
@@ -113,11 +128,15 @@ static void skip_factors(Handle& h) {
 }
 
 static void do_matvec(Handle& h, const double* x, double* y, int order) {
-  if (order != H2D_ORDER_ORIGINAL && order != H2D_ORDER_TREE) throw Error{H2D_EINVAL, "bad order"};
+  if (order != H2D_ORDER_ORIGINAL && order != H2D_ORDER_TREE && order != H2D_ORDER_GATHERED)
+    throw Error{H2D_EINVAL, "bad order"};
   if (!x || !y) throw Error{H2D_EINVAL, "null x or y"};
   const bool part = h.row_begin != 0 || h.row_end != h.n;
   if (order == H2D_ORDER_ORIGINAL && part)
     throw Error{H2D_EINVAL, "ORIGINAL order needs a single-rank (full-range) handle"};
+  if (order == H2D_ORDER_GATHERED && h.rank_rows.empty())
+    throw Error{H2D_EINVAL, "GATHERED order needs a world/rank partition"};
+  const int64_t xlen = order == H2D_ORDER_GATHERED ? h.gather_stride * h.opts.world : h.n;
   cudaStream_t s = h.stream;
   const bool xdev = is_device_ptr(x), ydev = is_device_ptr(y);
   const int64_t ylen = order == H2D_ORDER_ORIGINAL ? h.n : (h.row_end - h.row_begin);
@@ -133,8 +152,8 @@ static void do_matvec(Handle& h, const double* x, double* y, int order) {
   }
   const double* xin = x;
   if (!xdev) {
-    if (!h.d_xbuf) h.d_xbuf = h.alloc<double>(h.n);
-    H2D_CUDA(cudaMemcpyAsync(h.d_xbuf, x, h.n * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (!h.d_xbuf) h.d_xbuf = h.alloc<double>(std::max<int64_t>(h.n, h.gather_stride * h.opts.world));
+    H2D_CUDA(cudaMemcpyAsync(h.d_xbuf, x, xlen * sizeof(double), cudaMemcpyHostToDevice, s));
     xin = h.d_xbuf;
   }
   double* yout = y;
@@ -146,8 +165,12 @@ static void do_matvec(Handle& h, const double* x, double* y, int order) {
   if (order == H2D_ORDER_ORIGINAL) {
     permute_in(h, xin, h.d_xtree);
     xt = h.d_xtree;
+  } else if (order == H2D_ORDER_GATHERED) {
+    unpad_gathered(h, xin, h.d_xtree);
+    xt = h.d_xtree;
   }
-  matvec_tree(h, xt, yout, order, h.row_begin);
+  matvec_tree(h, xt, yout, order == H2D_ORDER_ORIGINAL ? H2D_ORDER_ORIGINAL : H2D_ORDER_TREE,
+              h.row_begin);
   if (h.timing) h.timed_count++;
   if (!ydev) {
     H2D_CUDA(cudaMemcpyAsync(y, yout, ylen * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -290,8 +313,8 @@ void hodlr2d_default_options(hodlr2d_options* o) {
   o->box_side = 0.0;
   o->depth = -1;
   o->max_rank = 128;
-  o->aca_consecutive = 2;
-  o->aca_trim = 2;
+  o->aca_consecutive = 3;
+  o->aca_trim = 3;
   o->test_rank = 1;
   o->stream = nullptr;
   o->world = 1;
@@ -455,6 +478,7 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   info->stageB_bytes = 8 * uv + 8 * h.t_len + 24 * (int64_t)h.n + 8 * served;
   info->matvec_bytes = info->stageA_bytes + info->stageB_bytes;
   info->device_bytes = (int64_t)h.device_bytes;
+  info->gather_stride = h.gather_stride;
   (void)rsum;
   return H2D_OK;
   H2D_CATCH
@@ -603,5 +627,16 @@ int hodlr2d_destroy(hodlr2d_t H) {
 }
 
 const char* hodlr2d_last_error(void) { return g_last_error.c_str(); }
+
+int hodlr2d_partition(const int32_t* leaf_start, int kappa, int world, int rank,
+                      int64_t* leaf_begin, int64_t* leaf_end) {
+  if (!leaf_start || !leaf_begin || !leaf_end || kappa < 0 || kappa > 15 || world < 1 || rank < 0 ||
+      rank >= world) {
+    set_error(H2D_EINVAL, "bad partition arguments");
+    return H2D_EINVAL;
+  }
+  partition_leaves(leaf_start, kappa, world, rank, leaf_begin, leaf_end);
+  return H2D_OK;
+}
 
 }  // extern "C"

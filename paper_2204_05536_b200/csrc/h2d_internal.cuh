@@ -127,6 +127,9 @@ struct Handle {
   double lo[2] = {0, 0}, side = 1;
   int64_t row_begin = 0, row_end = 0;     // served TREE rows
   int64_t leaf_begin = 0, leaf_end = 0;   // served leaves
+  std::vector<int64_t> rank_rows;         // [world + 1] first TREE row of every rank
+  int64_t* d_rank_rows = nullptr;
+  int64_t gather_stride = 0;              // max rows over ranks (padded all-gather slot)
   // tree (device)
   double* d_px = nullptr;
   double* d_py = nullptr;
@@ -200,5 +203,6 @@ void finalize_schedule(Handle& h);                                // apply.cu
 void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out,
                  int64_t y_row0);                                 // apply.cu (S7-S9)
 void permute_in(Handle& h, const double* d_x, double* d_xtree);   // apply.cu (S10)
+void unpad_gathered(Handle& h, const double* d_xg, double* d_xtree);  // apply.cu (S11 epilogue)
 
 }  // namespace h2d

@@ -66,7 +66,7 @@ int main(void) {{
 def test_default_options(h2d):
     o = h2d.default_options()
     assert (o.c, o.scale, o.shift, o.depth, o.max_rank) == (1.0, 1.0, 0.0, -1, 128)
-    assert (o.aca_consecutive, o.aca_trim, o.world, o.rank, o.timing) == (2, 2, 1, 0, 0)
+    assert (o.aca_consecutive, o.aca_trim, o.world, o.rank, o.timing) == (3, 3, 1, 0, 0)
 
 
 def test_argument_validation_codes(h2d):
