@@ -263,17 +263,23 @@ def run_ours(args, cfg):
 
     # roofline: dominant kernel, algorithmic bytes / its CUDA-event duration on this stream
     peak, peak_kind = peaks()
-    a_ms = stages["stageA_VTx"] / max(cnt, 1)
-    b_ms = stages["stageB_Ut_p2p"] / max(cnt, 1)
+    per = {k: v / max(cnt, 1) for k, v in stages.items()}
+    a_ms, b_ms = per["stageA_VTx"], per["stageB_Ut"]
     if b_ms >= a_ms:
-        dom, dom_ms, dom_bytes = "stageB_Ut_p2p", b_ms, inf["stageB_bytes"]
+        dom, dom_ms, dom_bytes = "stageB_Ut", b_ms, inf["stageB_bytes"]
     else:
         dom, dom_ms, dom_bytes = "stageA_VTx", a_ms, inf["stageA_bytes"]
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    other = "stageA_VTx" if dom == "stageB_Ut" else "stageB_Ut"
+    other_bytes = inf["stageA_bytes"] if dom == "stageB_Ut" else inf["stageB_bytes"]
+    clk_mhz = None
     roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
             "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "traffic": None, "bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4),
-            "stage_ms_per_matvec": {k: round(v / max(cnt, 1), 4) for k, v in stages.items()},
+            "other_hbm_kernel": {"kernel": other, "ms_per_launch": round(per[other], 4),
+                                 "bytes_per_launch": other_bytes,
+                                 "frac": round(other_bytes / (per[other] * 1e-3) / 1e9 / peak, 4)},
+            "stage_ms_per_matvec": {k: round(v, 4) for k, v in per.items()},
             "whole_matvec_frac": round(inf["matvec_bytes"] / (ms_step * 1e-3) / 1e9 / peak, 4)}
 
     # e2e through the public API with host (pinned) buffers, copies inside the timed region
@@ -295,6 +301,19 @@ def run_ours(args, cfg):
         e2e = {"value": 1e3 * ke / e0.elapsed_time(e1), "unit": "matvecs/s",
                "h2d_bytes_per_step": 8 * cfg.n, "d2h_bytes_per_step": 8 * cfg.n}
 
+    # near-field P2P against the FP64 pipe: pairs x FP64-pipe instructions per pair (from
+    # the kernel's SASS) / (148 SMs x 64 FP64 lanes x SM clock)
+    csum = clk.summary()
+    p2p_ms = per["p2p_near"]
+    ops_pair = P2P_FP64_OPS_PER_PAIR.get(cfg.kernel)
+    sm_hz = (csum["sm_mhz"] or 1965.0) * 1e6
+    p2p = {"pairs": int(inf["p2p_pairs"]), "ms_per_launch": round(p2p_ms, 4),
+           "pairs_per_s": inf["p2p_pairs"] / (p2p_ms * 1e-3) if p2p_ms > 0 else None,
+           "fp64_ops_per_pair": ops_pair, "peak_lane_ops_per_s": 148 * 64 * sm_hz,
+           "frac_fp64_pipe": (inf["p2p_pairs"] * ops_pair / (p2p_ms * 1e-3) / (148 * 64 * sm_hz))
+           if (p2p_ms > 0 and ops_pair) else None,
+           "overlapped_with": "stageA_VTx (second stream)"}
+    roof["p2p"] = p2p
     if rank == 0:
         line = {
             "metric": "HODLR2D fp64 matvecs/sec", "value": value, "unit": "matvecs/s",
@@ -308,7 +327,7 @@ def run_ours(args, cfg):
                                                "tree_seconds", "aca_seconds", "pack_seconds")},
             "roofline": roof, "e2e": e2e,
             "gpu_launches": args.steps * launches_per_matvec(inf, world),
-            "clocks": clk.summary(),
+            "clocks": csum,
         }
         if not args.no_cpu_baseline:
             try:
@@ -322,8 +341,13 @@ def run_ours(args, cfg):
 
 
 def launches_per_matvec(inf, world):
-    # permute-in (1-GPU ORIGINAL order) or unpad (gathered), stage A, t-reduce, stage B
-    return 4
+    # permute-in (1-GPU ORIGINAL order) or unpad (gathered), P2P, stage A, t-reduce, stage B
+    return 5
+
+
+# FP64-pipe instructions per near-field pair in p2p_kernel's inner loop, counted from
+# `cuobjdump -sass` of libhodlr2d.so; keyed by kernel id.
+P2P_FP64_OPS_PER_PAIR = {0: 35, 1: 11, 2: 11}
 
 
 def main():

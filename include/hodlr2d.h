@@ -92,8 +92,10 @@ typedef struct {
 } hodlr2d_options;
 
 #define H2D_MAX_LEVELS 16
-#define H2D_NUM_STAGES 4 /* 0 permute-in, 1 stage A (t = V^T x), 2 t-partial reduce,
-                            3 stage B + near-field P2P (y = U t + K_near x + shift x)   */
+#define H2D_NUM_STAGES 6 /* 0 input permute / unpad, 1 stage A (t = V^T x), 2 t-partial
+                            reduce, 3 wait for the near-field P2P, 4 stage B (y = ynear +
+                            U t), 5 near-field P2P (ynear = shift x + scale K_near x; runs on
+                            a second stream concurrently with stages 1-2)               */
 
 typedef struct {
   int64_t n;                 /* N                                                     */
@@ -116,6 +118,7 @@ typedef struct {
   double p2p_pairs;          /* near-field pair evaluations per matvec                */
   int64_t device_bytes;      /* device memory held by the handle                      */
   int64_t gather_stride;     /* max rows over ranks (slot size of H2D_ORDER_GATHERED) */
+  int64_t p2p_bytes;         /* algorithmic bytes of the near-field P2P kernel        */
 } hodlr2d_info;
 
 /* Fill *opts with the defaults listed above. */

@@ -31,8 +31,8 @@ KERNELS = {"log": 0, "imq": 1, "one_over_r": 2, "test_lowrank": 100}
 ORDER_ORIGINAL, ORDER_TREE, ORDER_GATHERED = 0, 1, 2
 ORDERS = {"original": 0, "tree": 1, "gathered": 2}
 MAX_LEVELS = 16
-NUM_STAGES = 4
-STAGE_NAMES = ("permute_in", "stageA_VTx", "t_reduce", "stageB_Ut_p2p")
+NUM_STAGES = 6
+STAGE_NAMES = ("input_permute", "stageA_VTx", "t_reduce", "p2p_join_wait", "stageB_Ut", "p2p_near")
 
 # Every function declared in include/hodlr2d.h (checked by tests/test_abi.py).
 ABI_FUNCTIONS = (
@@ -71,7 +71,7 @@ class Info(C.Structure):
         ("tree_seconds", C.c_double), ("aca_seconds", C.c_double), ("pack_seconds", C.c_double),
         ("build_seconds", C.c_double), ("matvec_bytes", C.c_int64),
         ("stageA_bytes", C.c_int64), ("stageB_bytes", C.c_int64), ("p2p_pairs", C.c_double),
-        ("device_bytes", C.c_int64), ("gather_stride", C.c_int64),
+        ("device_bytes", C.c_int64), ("gather_stride", C.c_int64), ("p2p_bytes", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

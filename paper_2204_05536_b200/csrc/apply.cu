@@ -65,109 +65,102 @@ T* upload_tmp(const std::vector<T>& v, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- stage A: t = V^T x
-__global__ void __launch_bounds__(kAThreads)
+// One CTA per (column box, row chunk).  The chunk is a contiguous row-major block
+// nrows x R of the V panel; thread (g, q) owns panel column q and rows g, g+G, ... so
+// each step of the CTA reads G*R consecutive doubles (fully coalesced), 8 rows in flight
+// per thread; x_chunk is staged once in shared memory.
+constexpr int kAUnroll = 8;
+constexpr int kAMaxRows = 1024;
+__global__ void __launch_bounds__(kAThreads, 6)
 stageA_kernel(const AItem* __restrict__ items, LevelPtrs lp, const double* __restrict__ x,
               double* __restrict__ t, double* __restrict__ tpart) {
   __shared__ double red[kAThreads];
+  __shared__ double xs[kAMaxRows];
   const AItem it = items[blockIdx.x];
   const double* __restrict__ V = lp.V[it.level] + it.v_off;
-  const double* __restrict__ xx = x + it.x_off;
   double* out = it.out >= 0 ? t + it.out : tpart + (-(int64_t)it.out - 1);
   const int R = it.R, nrows = it.nrows, tid = threadIdx.x;
-  if (R <= kAThreads) {
-    const int G = kAThreads / R;
-    const int g = tid / R, q = tid - g * R;
+  for (int i = tid; i < nrows; i += kAThreads) xs[i] = __ldg(x + it.x_off + i);
+  __syncthreads();
+  for (int q0 = 0; q0 < R; q0 += kAThreads) {
+    const int W = min(R - q0, kAThreads);      // columns handled in this pass
+    const int G = kAThreads / W;               // row groups
+    const int g = tid / W, q = tid - g * W;
     double acc = 0.0;
     if (g < G) {
-      const double* p = V + (int64_t)g * R + q;
+      const double* __restrict__ p = V + (int64_t)g * R + q0 + q;
       const int64_t step = (int64_t)G * R;
       int i = g;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      for (; i + 3 * G < nrows; i += 4 * G, p += 4 * step) {
-        double v0 = __ldcs(p), v1 = __ldcs(p + step), v2 = __ldcs(p + 2 * step),
-               v3 = __ldcs(p + 3 * step);
-        a0 = fma(v0, __ldg(xx + i), a0);
-        a1 = fma(v1, __ldg(xx + i + G), a1);
-        a2 = fma(v2, __ldg(xx + i + 2 * G), a2);
-        a3 = fma(v3, __ldg(xx + i + 3 * G), a3);
+      double a[4] = {0.0, 0.0, 0.0, 0.0};
+      for (; i + (kAUnroll - 1) * G < nrows; i += kAUnroll * G, p += kAUnroll * step) {
+        double v[kAUnroll];
+#pragma unroll
+        for (int u = 0; u < kAUnroll; ++u) v[u] = __ldcs(p + u * step);
+#pragma unroll
+        for (int u = 0; u < kAUnroll; ++u) a[u & 3] = fma(v[u], xs[i + u * G], a[u & 3]);
       }
-      for (; i < nrows; i += G, p += step) a0 = fma(__ldcs(p), __ldg(xx + i), a0);
-      acc = (a0 + a1) + (a2 + a3);
+      for (; i < nrows; i += G, p += step) a[0] = fma(__ldcs(p), xs[i], a[0]);
+      acc = (a[0] + a[1]) + (a[2] + a[3]);
     }
     if (G == 1) {
-      if (tid < R) out[tid] = acc;
-      return;
+      if (tid < W) out[q0 + tid] = acc;
+      continue;
     }
+    __syncthreads();
     red[tid] = acc;
     __syncthreads();
-    if (tid < R) {
+    if (tid < W) {
       double s = 0.0;
-      for (int gg = 0; gg < G; ++gg) s += red[gg * R + tid];
-      out[tid] = s;
-    }
-  } else {
-    for (int q0 = 0; q0 < R; q0 += kAThreads) {
-      const int q = q0 + tid;
-      if (q >= R) break;
-      const double* p = V + q;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int i = 0;
-      for (; i + 3 < nrows; i += 4, p += 4 * (int64_t)R) {
-        a0 = fma(__ldcs(p), __ldg(xx + i), a0);
-        a1 = fma(__ldcs(p + R), __ldg(xx + i + 1), a1);
-        a2 = fma(__ldcs(p + 2 * (int64_t)R), __ldg(xx + i + 2), a2);
-        a3 = fma(__ldcs(p + 3 * (int64_t)R), __ldg(xx + i + 3), a3);
-      }
-      for (; i < nrows; ++i, p += R) a0 = fma(__ldcs(p), __ldg(xx + i), a0);
-      out[q] = (a0 + a1) + (a2 + a3);
+      for (int gg = 0; gg < G; ++gg) s += red[gg * W + tid];
+      out[q0 + tid] = s;
     }
   }
 }
 
+// t[t_off + q] = sum_c tpart[p_off + c*R + q]: one warp per (item, q), lanes over chunks,
+// fixed shuffle tree (deterministic).
 __global__ void reduce_kernel(const RItem* __restrict__ items, const double* __restrict__ tpart,
                               double* __restrict__ t) {
   const RItem it = items[blockIdx.x];
-  for (int q = threadIdx.x; q < it.R; q += blockDim.x) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int q = blockIdx.y * nw + w; q < it.R; q += gridDim.y * nw) {
     double s = 0.0;
-    for (int c = 0; c < it.nchunks; ++c) s += tpart[it.p_off + (int64_t)c * it.R + q];
-    t[it.t_off + q] = s;
+    for (int c = lane; c < it.nchunks; c += 32) s += tpart[it.p_off + (int64_t)c * it.R + q];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) t[it.t_off + q] = s;
   }
 }
 
-// ---------------------------------------------------------------- stage B + near-field P2P
-// dynamic smem: tX[rmax] + tile (3 * kTile) + red[kBThreads]
+// ---------------------------------------------------------------- near-field P2P
+// ynear_L = shift x_L + scale * sum_{Y in {L} u E_L} K(L, Y) x_Y   (Alg. 2 l.4, l.7)
+// One CTA per leaf; the <= 5 near leaves' points and x are staged in shared-memory tiles,
+// thread (g, i) owns row i and columns j = g, g+G, ...; entries are evaluated on the fly.
 __global__ void __launch_bounds__(kBThreads)
-stageB_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_start, LevelPtrs lp,
-              const double* __restrict__ t, const int32_t* __restrict__ nf_off,
-              const int32_t* __restrict__ nf_col, const double* __restrict__ px,
-              const double* __restrict__ py, const double* __restrict__ x, KernelParams kp,
-              double* __restrict__ y, const int32_t* __restrict__ perm, int order_out,
-              int64_t y_row0, int rmax) {
-  extern __shared__ double sm[];
-  double* tX = sm;
-  double* tpx = sm + rmax;
-  double* tpy = tpx + kTile;
-  double* txv = tpy + kTile;
-  double* red = txv + kTile;
+p2p_kernel(int64_t leaf_begin, const int32_t* __restrict__ leaf_start,
+           const int32_t* __restrict__ nf_off, const int32_t* __restrict__ nf_col,
+           const double* __restrict__ px, const double* __restrict__ py,
+           const double* __restrict__ x, KernelParams kp, double* __restrict__ ynear) {
+  __shared__ double tpx[kTile], tpy[kTile], txv[kTile];
+  __shared__ double red[kBThreads];
+  __shared__ int seg_s[5], seg_n[5];
   const int64_t L = leaf_begin + blockIdx.x;
   const int64_t s0 = leaf_start[L];
   const int mL = leaf_start[L + 1] - (int)s0;
   if (mL <= 0) return;
   const int tid = threadIdx.x;
-  // near-field segments (<= 5 leaves)
-  const int nf0 = nf_off[L], nfn = nf_off[L + 1] - nf0;
-  int seg_s[5], seg_n[5], tot_near = 0;
-  for (int k = 0; k < 5; ++k) {
-    if (k < nfn) {
-      int Y = nf_col[nf0 + k];
-      seg_s[k] = leaf_start[Y];
-      seg_n[k] = leaf_start[Y + 1] - seg_s[k];
-    } else {
-      seg_s[k] = 0;
-      seg_n[k] = 0;
+  if (tid < 5) {
+    const int nf0 = nf_off[L], nfn = nf_off[L + 1] - nf0;
+    int a = 0, n = 0;
+    if (tid < nfn) {
+      const int Y = nf_col[nf0 + tid];
+      a = leaf_start[Y];
+      n = leaf_start[Y + 1] - a;
     }
-    tot_near += seg_n[k];
+    seg_s[tid] = a;
+    seg_n[tid] = n;
   }
+  __syncthreads();
+  const int tot_near = seg_n[0] + seg_n[1] + seg_n[2] + seg_n[3] + seg_n[4];
   for (int rp = 0; rp < mL; rp += kBThreads) {
     const int RT = min(mL - rp, kBThreads);
     const int G = kBThreads / RT;
@@ -175,39 +168,6 @@ stageB_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_st
     const int il = tid - g * RT;
     const bool act = g < G;
     const int64_t row = s0 + rp + il;
-    double acc = 0.0;
-    // ---- low-rank: sum over levels of U panel rows x t
-    for (int l = 1; l <= kappa; ++l) {
-      const int sh = 2 * (kappa - l);
-      const int64_t X = L >> sh;
-      const int32_t cb = lp.ucolbase[l][X];
-      const int R = lp.ucolbase[l][X + 1] - cb;
-      if (R == 0) continue;
-      const int64_t bx0 = leaf_start[X << sh];
-      const int64_t mX = leaf_start[(X + 1) << sh] - bx0;
-      __syncthreads();
-      const int32_t* __restrict__ ti = lp.tidx[l] + cb;
-      for (int q = tid; q < R; q += kBThreads) tX[q] = t[ti[q]];
-      __syncthreads();
-      if (act) {
-        const double* __restrict__ p = lp.U[l] + lp.upan_off[l][X] + (s0 - bx0) + rp + il +
-                                       (int64_t)g * mX;
-        const int64_t step = (int64_t)G * mX;
-        int q = g;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        for (; q + 3 * G < R; q += 4 * G, p += 4 * step) {
-          double u0 = __ldcs(p), u1 = __ldcs(p + step), u2 = __ldcs(p + 2 * step),
-                 u3 = __ldcs(p + 3 * step);
-          a0 = fma(u0, tX[q], a0);
-          a1 = fma(u1, tX[q + G], a1);
-          a2 = fma(u2, tX[q + 2 * G], a2);
-          a3 = fma(u3, tX[q + 3 * G], a3);
-        }
-        for (; q < R; q += G, p += step) a0 = fma(__ldcs(p), tX[q], a0);
-        acc += (a0 + a1) + (a2 + a3);
-      }
-    }
-    // ---- near field P2P from shared-memory tiles
     double pxi = 0.0, pyi = 0.0;
     if (act) { pxi = px[row]; pyi = py[row]; }
     double near = 0.0;
@@ -234,15 +194,93 @@ stageB_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_st
         near += b0 + b1;
       }
     }
-    acc = fma(kp.scale, near, acc);
     __syncthreads();
-    red[tid] = acc;
+    red[tid] = near;
     __syncthreads();
     if (tid < RT) {
       double s = 0.0;
       for (int gg = 0; gg < G; ++gg) s += red[gg * RT + tid];
       const int64_t r = s0 + rp + tid;
-      s = fma(kp.shift, x[r], s);
+      ynear[r] = fma(kp.shift, x[r], kp.scale * s);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- stage B: y = ynear + U t
+// One CTA per leaf L.  Phase 1 gathers t for every ancestor box X_l (all levels at once,
+// one barrier); phase 2 streams the leaf's contiguous row segment of every column of every
+// U panel (8 loads in flight per thread, no barrier); one y write per row.
+constexpr int kBUnroll = 8;
+__global__ void __launch_bounds__(kBThreads)
+stageB_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_start, LevelPtrs lp,
+              const double* __restrict__ t, const double* __restrict__ ynear,
+              double* __restrict__ y, const int32_t* __restrict__ perm, int order_out,
+              int64_t y_row0) {
+  extern __shared__ double tX[];                 // sum over levels of R_l
+  __shared__ double red[kBThreads];
+  __shared__ int s_R[H2D_MAX_LEVELS + 1], s_off[H2D_MAX_LEVELS + 2];
+  __shared__ int s_cb[H2D_MAX_LEVELS + 1];
+  __shared__ int64_t s_base[H2D_MAX_LEVELS + 1], s_mX[H2D_MAX_LEVELS + 1];
+  const int64_t L = leaf_begin + blockIdx.x;
+  const int64_t s0 = leaf_start[L];
+  const int mL = leaf_start[L + 1] - (int)s0;
+  if (mL <= 0) return;
+  const int tid = threadIdx.x;
+  if (tid >= 1 && tid <= kappa) {
+    const int l = tid, sh = 2 * (kappa - l);
+    const int64_t X = L >> sh;
+    const int32_t cb = lp.ucolbase[l][X];
+    const int64_t bx0 = leaf_start[X << sh];
+    s_R[l] = lp.ucolbase[l][X + 1] - cb;
+    s_cb[l] = cb;
+    s_mX[l] = leaf_start[(X + 1) << sh] - bx0;
+    s_base[l] = lp.upan_off[l][X] + (s0 - bx0);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int o = 0;
+    for (int l = 1; l <= kappa; ++l) { s_off[l] = o; o += s_R[l]; }
+    s_off[kappa + 1] = o;
+  }
+  __syncthreads();
+  for (int l = 1; l <= kappa; ++l) {
+    const int32_t* __restrict__ ti = lp.tidx[l] + s_cb[l];
+    double* dst = tX + s_off[l];
+    for (int q = tid; q < s_R[l]; q += kBThreads) dst[q] = t[ti[q]];
+  }
+  __syncthreads();
+  for (int rp = 0; rp < mL; rp += kBThreads) {
+    const int RT = min(mL - rp, kBThreads);
+    const int G = kBThreads / RT;
+    const int g = tid / RT;
+    const int il = tid - g * RT;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    if (g < G) {
+      for (int l = 1; l <= kappa; ++l) {
+        const int R = s_R[l];
+        const int64_t mX = s_mX[l];
+        const double* __restrict__ p = lp.U[l] + s_base[l] + rp + il + (int64_t)g * mX;
+        const double* tx = tX + s_off[l];
+        const int64_t step = (int64_t)G * mX;
+        int q = g;
+        for (; q + (kBUnroll - 1) * G < R; q += kBUnroll * G, p += kBUnroll * step) {
+          double u[kBUnroll];
+#pragma unroll
+          for (int k = 0; k < kBUnroll; ++k) u[k] = __ldcs(p + k * step);
+#pragma unroll
+          for (int k = 0; k < kBUnroll; ++k) a[k & 3] = fma(u[k], tx[q + k * G], a[k & 3]);
+        }
+        for (; q < R; q += G, p += step) a[0] = fma(__ldcs(p), tx[q], a[0]);
+      }
+    }
+    __syncthreads();
+    red[tid] = (a[0] + a[1]) + (a[2] + a[3]);
+    __syncthreads();
+    if (tid < RT) {
+      double s = 0.0;
+      for (int gg = 0; gg < G; ++gg) s += red[gg * RT + tid];
+      const int64_t r = s0 + rp + tid;
+      s += ynear[r];
       if (order_out == H2D_ORDER_ORIGINAL) y[perm[r]] = s;
       else y[r - y_row0] = s;
     }
@@ -354,14 +392,19 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
   H2D_CUDA(cudaStreamSynchronize(s));
 }
 
-static int max_panel_width(const Handle& h) {
-  int r = 1;
-  for (int l = 1; l <= h.kappa; ++l) {
-    const Level& L = h.levels[(size_t)l];
-    for (int64_t X = 0; X < L.nbox; ++X)
-      r = std::max(r, L.ucolbase[(size_t)X + 1] - L.ucolbase[(size_t)X]);
+// Widest t gather of stage B: max over served leaves of sum_l R_{X_l(L)}.
+static int max_gather_width(const Handle& h) {
+  int64_t best = 1;
+  for (int64_t L = h.leaf_begin; L < h.leaf_end; ++L) {
+    int64_t tot = 0;
+    for (int l = 1; l <= h.kappa; ++l) {
+      const Level& Lv = h.levels[(size_t)l];
+      const int64_t X = L >> (2 * (h.kappa - l));
+      tot += Lv.ucolbase[(size_t)X + 1] - Lv.ucolbase[(size_t)X];
+    }
+    best = std::max(best, tot);
   }
-  return r;
+  return (int)best;
 }
 
 // Build the stage-A / reduce schedule, t layout and the per-level device tables.
@@ -406,13 +449,14 @@ void finalize_schedule(Handle& h) {
     h.lp.ucolbase[l] = L.d_ucolbase;
     h.lp.upan_off[l] = L.d_upan_off;
     h.lp.tidx[l] = L.d_tidx;
-    // stage-A items
+    // stage-A items: chunks of <= kATarget elements and <= kAMaxRows rows
     for (int64_t Y = 0; Y < L.nbox; ++Y) {
       const int R = L.vR[(size_t)Y];
       const int64_t y0 = h.box_begin(l, Y);
       const int64_t nY = h.box_end(l, Y) - y0;
       if (R == 0 || nY == 0) continue;
-      int64_t nch = std::min<int64_t>(nY, std::max<int64_t>(1, (nY * R + kATarget - 1) / kATarget));
+      int64_t nch = std::max<int64_t>((nY * R + kATarget - 1) / kATarget, (nY + kAMaxRows - 1) / kAMaxRows);
+      nch = std::min<int64_t>(nY, std::max<int64_t>(1, nch));
       const int64_t rows = (nY + nch - 1) / nch;
       nch = (nY + rows - 1) / rows;
       if (nch == 1) {
@@ -431,7 +475,9 @@ void finalize_schedule(Handle& h) {
   }
   h.t_len = t_len;
   h.tpart_len = tpart_len;
-  h.rmax_panel = max_panel_width(h);
+  h.rmax_panel = max_gather_width(h);
+  h.max_ritem_R = 1;
+  for (auto& r : ritems) h.max_ritem_R = std::max(h.max_ritem_R, (int)r.R);
   h.d_t = h.alloc<double>(t_len);
   h.d_tpart = h.alloc<double>(tpart_len);
   h.n_aitems = (int64_t)aitems.size();
@@ -444,6 +490,17 @@ void finalize_schedule(Handle& h) {
   if (!ritems.empty())
     H2D_CUDA(cudaMemcpyAsync(h.d_ritems, ritems.data(), ritems.size() * sizeof(RItem),
                              cudaMemcpyHostToDevice, s));
+  if (!h.d_ynear) h.d_ynear = h.alloc<double>(h.n);
+  if (!h.aux_stream) {
+    H2D_CUDA(cudaStreamCreateWithFlags(&h.aux_stream, cudaStreamNonBlocking));
+    H2D_CUDA(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
+    H2D_CUDA(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
+  }
+  const size_t smem = (size_t)h.rmax_panel * sizeof(double);
+  if (smem > 40 * 1024)
+    H2D_CUDA(cudaFuncSetAttribute(stageB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::min<size_t>(smem, 200 * 1024)));
+  if (smem > 200 * 1024) throw Error{H2D_EINVAL, "U panels too wide for stage B shared memory"};
   H2D_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -453,45 +510,63 @@ void permute_in(Handle& h, const double* d_x, double* d_xtree) {
   H2D_LAUNCH_CHECK();
 }
 
-static cudaEvent_t next_event(Handle& h) {
-  if (h.ev_used >= (int64_t)h.ev_pool.size()) {
+static void record(Handle& h, int slot, cudaStream_t s) {
+  if (!h.timing) return;
+  const int64_t idx = h.ev_base + slot;
+  while ((int64_t)h.ev_pool.size() <= idx) {
     cudaEvent_t e;
     H2D_CUDA(cudaEventCreate(&e));
     h.ev_pool.push_back(e);
   }
-  return h.ev_pool[(size_t)h.ev_used++];
+  H2D_CUDA(cudaEventRecord(h.ev_pool[(size_t)idx], s));
 }
 
+void begin_matvec_timing(Handle& h) {
+  if (!h.timing) return;
+  h.ev_base = h.ev_used;
+  h.ev_used += kEventsPerMatvec;
+  record(h, 0, h.stream);
+}
+
+void mark_after_input(Handle& h) { record(h, 1, h.stream); }
+
+// Matvec on TREE-order x (S7-S9).  The near-field P2P (compute-bound) runs on the aux
+// stream concurrently with stage A (HBM-bound); stage B joins both.
 void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, int64_t y_row0) {
-  cudaStream_t s = h.stream;
-  cudaEvent_t e1 = nullptr, e2 = nullptr, e3 = nullptr;
-  if (h.timing) { e1 = next_event(h); H2D_CUDA(cudaEventRecord(e1, s)); }
+  cudaStream_t s = h.stream, a = h.aux_stream;
+  const int64_t nleaves = h.leaf_end - h.leaf_begin;
+  H2D_CUDA(cudaEventRecord(h.ev_fork, s));
+  H2D_CUDA(cudaStreamWaitEvent(a, h.ev_fork, 0));
+  record(h, 6, a);
+  if (nleaves > 0) {
+    p2p_kernel<<<(int)nleaves, kBThreads, 0, a>>>(h.leaf_begin, h.d_leaf_start, h.d_nf_off,
+                                                   h.d_nf_col, h.d_px, h.d_py, d_xtree, h.kp,
+                                                   h.d_ynear);
+    H2D_LAUNCH_CHECK();
+  }
+  record(h, 7, a);
+  H2D_CUDA(cudaEventRecord(h.ev_join, a));
   if (h.n_aitems > 0) {
     stageA_kernel<<<(int)h.n_aitems, kAThreads, 0, s>>>(h.d_aitems, h.lp, d_xtree, h.d_t, h.d_tpart);
     H2D_LAUNCH_CHECK();
   }
-  if (h.timing) { e2 = next_event(h); H2D_CUDA(cudaEventRecord(e2, s)); }
+  record(h, 2, s);
   if (h.n_ritems > 0) {
-    reduce_kernel<<<(int)h.n_ritems, 128, 0, s>>>(h.d_ritems, h.d_tpart, h.d_t);
+    dim3 grid((unsigned)h.n_ritems, (unsigned)std::max(1, (h.max_ritem_R + 7) / 8));
+    reduce_kernel<<<grid, 256, 0, s>>>(h.d_ritems, h.d_tpart, h.d_t);
     H2D_LAUNCH_CHECK();
   }
-  if (h.timing) { e3 = next_event(h); H2D_CUDA(cudaEventRecord(e3, s)); }
-  const int64_t nleaves = h.leaf_end - h.leaf_begin;
+  record(h, 3, s);
+  H2D_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
+  record(h, 4, s);
   if (nleaves > 0) {
-    static_assert(kBThreads == 256, "");
-    const int rmax = h.rmax_panel;
-    const size_t smem = ((size_t)rmax + 3 * kTile + kBThreads) * sizeof(double);
-    if (smem > 48 * 1024)
-      H2D_CUDA(cudaFuncSetAttribute(stageB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    stageB_kernel<<<(int)nleaves, kBThreads, smem, s>>>(
-        h.kappa, h.leaf_begin, h.d_leaf_start, h.lp, h.d_t, h.d_nf_off, h.d_nf_col, h.d_px, h.d_py,
-        d_xtree, h.kp, d_y, h.d_perm, order_out, y_row0, rmax);
+    const size_t smem = (size_t)h.rmax_panel * sizeof(double);
+    stageB_kernel<<<(int)nleaves, kBThreads, smem, s>>>(h.kappa, h.leaf_begin, h.d_leaf_start, h.lp,
+                                                         h.d_t, h.d_ynear, d_y, h.d_perm, order_out,
+                                                         y_row0);
     H2D_LAUNCH_CHECK();
   }
-  if (h.timing) {
-    cudaEvent_t e4 = next_event(h);
-    H2D_CUDA(cudaEventRecord(e4, s));
-  }
+  record(h, 5, s);
 }
 
 }  // namespace h2d

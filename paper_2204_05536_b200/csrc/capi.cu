@@ -33,6 +33,9 @@ Handle::~Handle() {
   cudaStreamSynchronize(stream);
   for (void* p : allocs) cudaFree(p);
   for (auto e : ev_pool) cudaEventDestroy(e);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  if (aux_stream) cudaStreamDestroy(aux_stream);
 }
 
 static double now_s() {
@@ -140,16 +143,7 @@ static void do_matvec(Handle& h, const double* x, double* y, int order) {
   cudaStream_t s = h.stream;
   const bool xdev = is_device_ptr(x), ydev = is_device_ptr(y);
   const int64_t ylen = order == H2D_ORDER_ORIGINAL ? h.n : (h.row_end - h.row_begin);
-  cudaEvent_t e0 = nullptr;
-  if (h.timing) {
-    if (h.ev_used >= (int64_t)h.ev_pool.size()) {
-      cudaEvent_t e;
-      H2D_CUDA(cudaEventCreate(&e));
-      h.ev_pool.push_back(e);
-    }
-    e0 = h.ev_pool[(size_t)h.ev_used++];
-    H2D_CUDA(cudaEventRecord(e0, s));
-  }
+  begin_matvec_timing(h);
   const double* xin = x;
   if (!xdev) {
     if (!h.d_xbuf) h.d_xbuf = h.alloc<double>(std::max<int64_t>(h.n, h.gather_stride * h.opts.world));
@@ -169,6 +163,7 @@ static void do_matvec(Handle& h, const double* x, double* y, int order) {
     unpad_gathered(h, xin, h.d_xtree);
     xt = h.d_xtree;
   }
+  mark_after_input(h);
   matvec_tree(h, xt, yout, order == H2D_ORDER_ORIGINAL ? H2D_ORDER_ORIGINAL : H2D_ORDER_TREE,
               h.row_begin);
   if (h.timing) h.timed_count++;
@@ -474,9 +469,14 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   // algorithmic bytes: stage A reads V + x per chunk and writes t;
   // stage B reads U + t (+ tidx) + near-field points/x and writes y.
   const int64_t served = h.row_end - h.row_begin;
+  // stage A: V panels once, x once, t written once.  stage B: U panels once, t + its
+  // index read once, ynear read once, y written once.  P2P: points + x + ynear.
+  int64_t tidx_len = 0;
+  for (int l = 1; l <= h.kappa; ++l) tidx_len += h.levels[(size_t)l].ucolbase.empty() ? 0 : h.levels[(size_t)l].ucolbase.back();
   info->stageA_bytes = 8 * vv + 8 * (int64_t)h.n + 8 * h.t_len;
-  info->stageB_bytes = 8 * uv + 8 * h.t_len + 24 * (int64_t)h.n + 8 * served;
-  info->matvec_bytes = info->stageA_bytes + info->stageB_bytes;
+  info->stageB_bytes = 8 * uv + 8 * h.t_len + 4 * tidx_len + 16 * served;
+  info->p2p_bytes = 24 * served + 8 * served;
+  info->matvec_bytes = info->stageA_bytes + info->stageB_bytes + info->p2p_bytes;
   info->device_bytes = (int64_t)h.device_bytes;
   info->gather_stride = h.gather_stride;
   (void)rsum;
@@ -603,13 +603,16 @@ int hodlr2d_stage_times(hodlr2d_t H, double* ms, int64_t* count, int reset) {
   if (!H) throw Error{H2D_EINVAL, "null handle"};
   Handle& h = H->h;
   H2D_CUDA(cudaStreamSynchronize(h.stream));
-  // events come in groups of 5 per matvec: start, after A-prep, after A, after reduce, end
-  double acc[H2D_NUM_STAGES] = {0, 0, 0, 0};
-  const int64_t groups = h.ev_used / 5;
+  // kEventsPerMatvec events per matvec (see h2d_internal.cuh)
+  static const int from[H2D_NUM_STAGES] = {0, 1, 2, 3, 4, 6};
+  static const int to[H2D_NUM_STAGES] = {1, 2, 3, 4, 5, 7};
+  double acc[H2D_NUM_STAGES] = {};
+  const int64_t groups = h.ev_used / kEventsPerMatvec;
   for (int64_t g = 0; g < groups; ++g) {
+    const size_t b = (size_t)(g * kEventsPerMatvec);
     for (int k = 0; k < H2D_NUM_STAGES; ++k) {
       float t = 0.f;
-      H2D_CUDA(cudaEventElapsedTime(&t, h.ev_pool[(size_t)(5 * g + k)], h.ev_pool[(size_t)(5 * g + k + 1)]));
+      H2D_CUDA(cudaEventElapsedTime(&t, h.ev_pool[b + from[k]], h.ev_pool[b + to[k]]));
       acc[k] += t;
     }
   }

@@ -152,7 +152,11 @@ struct Handle {
   double* d_tpart = nullptr;              // multi-chunk partials
   int64_t tpart_len = 0;
   LevelPtrs lp{};
-  int rmax_panel = 1;                     // widest U panel (smem size of stage B)
+  int rmax_panel = 1;                     // widest per-leaf t gather (smem of stage B)
+  int max_ritem_R = 1;
+  double* d_ynear = nullptr;              // [n] near field + shift x (P2P output)
+  cudaStream_t aux_stream = nullptr;      // P2P runs here, concurrent with stage A
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // matvec work buffers
   double* d_xtree = nullptr;              // [n]
   double* d_ybuf = nullptr;               // [n] staging for host y
@@ -164,8 +168,9 @@ struct Handle {
   int timing = 0;
   std::vector<cudaEvent_t> ev_pool;
   int64_t ev_used = 0;
+  int64_t ev_base = 0;
   int64_t timed_count = 0;
-  double stage_ms[H2D_NUM_STAGES] = {0, 0, 0, 0};
+  double stage_ms[H2D_NUM_STAGES] = {};
   // allocations
   std::vector<void*> allocs;
   size_t device_bytes = 0;
@@ -203,6 +208,11 @@ void finalize_schedule(Handle& h);                                // apply.cu
 void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out,
                  int64_t y_row0);                                 // apply.cu (S7-S9)
 void permute_in(Handle& h, const double* d_x, double* d_xtree);   // apply.cu (S10)
+// per-matvec CUDA events (timing mode): 0 start, 1 after input permute/unpad, 2 after
+// stage A, 3 after t-reduce, 4 after joining P2P, 5 end (main stream); 6/7 P2P (aux)
+constexpr int kEventsPerMatvec = 8;
+void begin_matvec_timing(Handle& h);
+void mark_after_input(Handle& h);
 void unpad_gathered(Handle& h, const double* d_xg, double* d_xtree);  // apply.cu (S11 epilogue)
 
 }  // namespace h2d
