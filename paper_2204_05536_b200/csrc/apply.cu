@@ -1,6 +1,6 @@
 // Factor packing (G7) and the matvec hot path (S7-S10).
 //
-// HBM layout (DESIGN.md §Layout):
+// HBM layout (DESIGN.md §5):
 //   U panel of row box X at level l : column-major m_X x R_X, the concatenation
 //                                     [U_b1 | U_b2 | ...] of the blocks (X, Y), Y in I_X
 //                                     ascending.  A leaf L inside X owns the contiguous
@@ -8,16 +8,15 @@
 //   V panel of column box Y         : row-major n_Y x RV_Y, the columns of the blocks
 //                                     (X, Y), X in I_Y ascending.  Row i of the panel is the
 //                                     RV_Y values that multiply x_i.
-//   t                               : one value per (block, rank index), grouped by column
-//                                     box (the V panel column order).
+//   t                               : one value per (block, rank index) in U-panel column
+//                                     order, so a row box's t is contiguous; stage A writes
+//                                     it through vdst (V-panel column -> t position).
 // Matvec (Alg. 2; stage order is free, R18):
-//   stage A  t = V^T x          one CTA per (column box, row chunk); thread q owns panel
-//                               column q, so every load is coalesced and no cross-thread
-//                               reduction is needed except across row groups (smem).
-//   reduce   t = sum of chunk partials (only for boxes split over several CTAs).
-//   stage B  per leaf L: y_L = shift x_L + scale * sum_{Y in {L} u E_L} K(L, Y) x_Y
-//                               + sum_l U_{X_l}[rows of L, :] t_{X_l}
-//                               one CTA per leaf, one y write per row (no atomics).
+//   p2p      ynear = shift x + scale K_near x  (second stream, overlaps stage A)
+//   stage A  t = V^T x          one CTA per (column box, row chunk)
+//   reduce   t = sum of chunk partials (boxes split over several CTAs only)
+//   stage B  per leaf L: y_L = ynear_L + sum_l U_{X_l}[rows of L, :] t_{X_l}
+//                               one CTA per leaf, one y write per row, no atomics.
 #include <algorithm>
 
 #include "h2d_internal.cuh"
@@ -29,6 +28,9 @@ constexpr int kAThreads = 256;
 constexpr int kBThreads = 256;
 constexpr int kTile = 512;           // near-field points staged in smem per tile
 constexpr int64_t kATarget = 32768;  // stage-A elements per CTA
+constexpr int kAUnroll = 8;
+constexpr int kAMaxRows = 2048;      // rows per stage-A chunk (x staged in smem)
+constexpr int kBUnroll = 8;
 
 struct CopyItem {
   const double* src;
@@ -65,20 +67,17 @@ T* upload_tmp(const std::vector<T>& v, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- stage A: t = V^T x
-// One CTA per (column box, row chunk).  The chunk is a contiguous row-major block
-// nrows x R of the V panel; thread (g, q) owns panel column q and rows g, g+G, ... so
-// each step of the CTA reads G*R consecutive doubles (fully coalesced), 8 rows in flight
-// per thread; x_chunk is staged once in shared memory.
-constexpr int kAUnroll = 8;
-constexpr int kAMaxRows = 1024;
+// The chunk is a contiguous row-major block nrows x R of the V panel; thread (g, q) owns
+// panel column q and rows g, g+G, ..., so each CTA step reads G*R consecutive doubles,
+// 8 rows in flight per thread; x_chunk is staged once in shared memory.
 __global__ void __launch_bounds__(kAThreads, 6)
 stageA_kernel(const AItem* __restrict__ items, LevelPtrs lp, const double* __restrict__ x,
-              double* __restrict__ t, double* __restrict__ tpart) {
+              const int32_t* __restrict__ vdst, double* __restrict__ t,
+              double* __restrict__ tpart) {
   __shared__ double red[kAThreads];
   __shared__ double xs[kAMaxRows];
   const AItem it = items[blockIdx.x];
   const double* __restrict__ V = lp.V[it.level] + it.v_off;
-  double* out = it.out >= 0 ? t + it.out : tpart + (-(int64_t)it.out - 1);
   const int R = it.R, nrows = it.nrows, tid = threadIdx.x;
   for (int i = tid; i < nrows; i += kAThreads) xs[i] = __ldg(x + it.x_off + i);
   __syncthreads();
@@ -102,32 +101,34 @@ stageA_kernel(const AItem* __restrict__ items, LevelPtrs lp, const double* __res
       for (; i < nrows; i += G, p += step) a[0] = fma(__ldcs(p), xs[i], a[0]);
       acc = (a[0] + a[1]) + (a[2] + a[3]);
     }
-    if (G == 1) {
-      if (tid < W) out[q0 + tid] = acc;
-      continue;
+    if (G > 1) {
+      __syncthreads();
+      red[tid] = acc;
+      __syncthreads();
+      if (tid < W) {
+        double s = 0.0;
+        for (int gg = 0; gg < G; ++gg) s += red[gg * W + tid];
+        acc = s;
+      }
     }
-    __syncthreads();
-    red[tid] = acc;
-    __syncthreads();
     if (tid < W) {
-      double s = 0.0;
-      for (int gg = 0; gg < G; ++gg) s += red[gg * W + tid];
-      out[q0 + tid] = s;
+      if (it.out >= 0) t[vdst[it.out + q0 + tid]] = acc;
+      else tpart[(-(int64_t)it.out - 1) + q0 + tid] = acc;
     }
   }
 }
 
-// t[t_off + q] = sum_c tpart[p_off + c*R + q]: one warp per (item, q), lanes over chunks,
-// fixed shuffle tree (deterministic).
+// t[vdst[vpos + q]] = sum_c tpart[p_off + c*R + q]: one CTA per item, one warp per q,
+// lanes over chunks, fixed shuffle tree (deterministic).
 __global__ void reduce_kernel(const RItem* __restrict__ items, const double* __restrict__ tpart,
-                              double* __restrict__ t) {
+                              const int32_t* __restrict__ vdst, double* __restrict__ t) {
   const RItem it = items[blockIdx.x];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int q = blockIdx.y * nw + w; q < it.R; q += gridDim.y * nw) {
+  for (int q = w; q < it.R; q += nw) {
     double s = 0.0;
     for (int c = lane; c < it.nchunks; c += 32) s += tpart[it.p_off + (int64_t)c * it.R + q];
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) t[it.t_off + q] = s;
+    if (lane == 0) t[vdst[it.vpos + q]] = s;
   }
 }
 
@@ -207,48 +208,20 @@ p2p_kernel(int64_t leaf_begin, const int32_t* __restrict__ leaf_start,
 }
 
 // ---------------------------------------------------------------- stage B: y = ynear + U t
-// One CTA per leaf L.  Phase 1 gathers t for every ancestor box X_l (all levels at once,
-// one barrier); phase 2 streams the leaf's contiguous row segment of every column of every
-// U panel (8 loads in flight per thread, no barrier); one y write per row.
-constexpr int kBUnroll = 8;
-__global__ void __launch_bounds__(kBThreads)
+// One CTA per leaf L.  Thread (g, i) owns row i of the leaf and columns q = g, g+G, ... of
+// every ancestor U panel: it streams the contiguous row segment of each column (8 loads in
+// flight) and reads the matching t entries straight from L1/L2 (t is contiguous per row
+// box and shared by all rows), so there is no barrier until the final row reduction.
+__global__ void __launch_bounds__(kBThreads, 4)
 stageB_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_start, LevelPtrs lp,
-              const double* __restrict__ t, const double* __restrict__ ynear,
-              double* __restrict__ y, const int32_t* __restrict__ perm, int order_out,
-              int64_t y_row0) {
-  extern __shared__ double tX[];                 // sum over levels of R_l
+              const double* __restrict__ ynear, double* __restrict__ y,
+              const int32_t* __restrict__ perm, int order_out, int64_t y_row0) {
   __shared__ double red[kBThreads];
-  __shared__ int s_R[H2D_MAX_LEVELS + 1], s_off[H2D_MAX_LEVELS + 2];
-  __shared__ int s_cb[H2D_MAX_LEVELS + 1];
-  __shared__ int64_t s_base[H2D_MAX_LEVELS + 1], s_mX[H2D_MAX_LEVELS + 1];
   const int64_t L = leaf_begin + blockIdx.x;
   const int64_t s0 = leaf_start[L];
   const int mL = leaf_start[L + 1] - (int)s0;
   if (mL <= 0) return;
   const int tid = threadIdx.x;
-  if (tid >= 1 && tid <= kappa) {
-    const int l = tid, sh = 2 * (kappa - l);
-    const int64_t X = L >> sh;
-    const int32_t cb = lp.ucolbase[l][X];
-    const int64_t bx0 = leaf_start[X << sh];
-    s_R[l] = lp.ucolbase[l][X + 1] - cb;
-    s_cb[l] = cb;
-    s_mX[l] = leaf_start[(X + 1) << sh] - bx0;
-    s_base[l] = lp.upan_off[l][X] + (s0 - bx0);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int o = 0;
-    for (int l = 1; l <= kappa; ++l) { s_off[l] = o; o += s_R[l]; }
-    s_off[kappa + 1] = o;
-  }
-  __syncthreads();
-  for (int l = 1; l <= kappa; ++l) {
-    const int32_t* __restrict__ ti = lp.tidx[l] + s_cb[l];
-    double* dst = tX + s_off[l];
-    for (int q = tid; q < s_R[l]; q += kBThreads) dst[q] = t[ti[q]];
-  }
-  __syncthreads();
   for (int rp = 0; rp < mL; rp += kBThreads) {
     const int RT = min(mL - rp, kBThreads);
     const int G = kBThreads / RT;
@@ -257,24 +230,41 @@ stageB_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_st
     double a[4] = {0.0, 0.0, 0.0, 0.0};
     if (g < G) {
       for (int l = 1; l <= kappa; ++l) {
-        const int R = s_R[l];
-        const int64_t mX = s_mX[l];
-        const double* __restrict__ p = lp.U[l] + s_base[l] + rp + il + (int64_t)g * mX;
-        const double* tx = tX + s_off[l];
+        const int sh = 2 * (kappa - l);
+        const int64_t X = L >> sh;
+        const int32_t cb = lp.ucolbase[l][X];
+        const int R = lp.ucolbase[l][X + 1] - cb;
+        const int64_t bx0 = leaf_start[X << sh];
+        const int64_t mX = leaf_start[(X + 1) << sh] - bx0;
+        const double* __restrict__ p = lp.U[l] + lp.upan_off[l][X] + (s0 - bx0) + rp + il +
+                                       (int64_t)g * mX;
+        const double* __restrict__ tx = lp.tu[l] + cb;
         const int64_t step = (int64_t)G * mX;
         int q = g;
         for (; q + (kBUnroll - 1) * G < R; q += kBUnroll * G, p += kBUnroll * step) {
-          double u[kBUnroll];
+          double u[kBUnroll], tv[kBUnroll];
 #pragma unroll
           for (int k = 0; k < kBUnroll; ++k) u[k] = __ldcs(p + k * step);
 #pragma unroll
-          for (int k = 0; k < kBUnroll; ++k) a[k & 3] = fma(u[k], tx[q + k * G], a[k & 3]);
+          for (int k = 0; k < kBUnroll; ++k) tv[k] = __ldg(tx + q + k * G);
+#pragma unroll
+          for (int k = 0; k < kBUnroll; ++k) a[k & 3] = fma(u[k], tv[k], a[k & 3]);
         }
-        for (; q < R; q += G, p += step) a[0] = fma(__ldcs(p), tx[q], a[0]);
+        for (; q < R; q += G, p += step) a[0] = fma(__ldcs(p), __ldg(tx + q), a[0]);
       }
     }
+    const double acc = (a[0] + a[1]) + (a[2] + a[3]);
+    if (G == 1) {
+      if (tid < RT) {
+        const int64_t r = s0 + rp + tid;
+        const double s = acc + ynear[r];
+        if (order_out == H2D_ORDER_ORIGINAL) y[perm[r]] = s;
+        else y[r - y_row0] = s;
+      }
+      continue;
+    }
     __syncthreads();
-    red[tid] = (a[0] + a[1]) + (a[2] + a[3]);
+    red[tid] = acc;
     __syncthreads();
     if (tid < RT) {
       double s = 0.0;
@@ -392,53 +382,49 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
   H2D_CUDA(cudaStreamSynchronize(s));
 }
 
-// Widest t gather of stage B: max over served leaves of sum_l R_{X_l(L)}.
-static int max_gather_width(const Handle& h) {
-  int64_t best = 1;
-  for (int64_t L = h.leaf_begin; L < h.leaf_end; ++L) {
-    int64_t tot = 0;
-    for (int l = 1; l <= h.kappa; ++l) {
-      const Level& Lv = h.levels[(size_t)l];
-      const int64_t X = L >> (2 * (h.kappa - l));
-      tot += Lv.ucolbase[(size_t)X + 1] - Lv.ucolbase[(size_t)X];
-    }
-    best = std::max(best, tot);
-  }
-  return (int)best;
-}
-
-// Build the stage-A / reduce schedule, t layout and the per-level device tables.
+// Build the stage-A / reduce schedule, the t layout (U-panel order) and the per-level
+// device tables.
 void finalize_schedule(Handle& h) {
   cudaStream_t s = h.stream;
   int64_t t_len = 0, tpart_len = 0;
   std::vector<AItem> aitems;
   std::vector<RItem> ritems;
+  // t layout: level by level, U-panel column order (ucolbase) -> tu_base per level
+  for (int l = 1; l <= h.kappa; ++l) {
+    Level& L = h.levels[(size_t)l];
+    L.tu_base = t_len;
+    t_len += L.ucolbase[(size_t)L.nbox];
+  }
+  if (t_len > INT32_MAX) throw Error{H2D_EINVAL, "t vector exceeds 2^31 entries"};
+  // vdst: V-panel columns in column-box order (per level, box, column) -> t index
+  std::vector<int32_t> vdst((size_t)std::max<int64_t>(1, t_len));
+  int64_t vpos = 0;
   for (int l = 1; l <= h.kappa; ++l) {
     Level& L = h.levels[(size_t)l];
     L.t_off.assign((size_t)L.nbox, 0);
     for (int64_t Y = 0; Y < L.nbox; ++Y) {
-      L.t_off[(size_t)Y] = t_len;
-      t_len += L.vR[(size_t)Y];
+      L.t_off[(size_t)Y] = vpos;       // first vdst entry of the V panel of Y
+      for (int32_t e2 = L.off[(size_t)Y]; e2 < L.off[(size_t)Y + 1]; ++e2) {
+        const int32_t b = L.trans[(size_t)e2];           // block (X, Y)
+        const int r = std::max<int32_t>(0, L.rank[(size_t)b]);
+        if (r == 0) continue;
+        const int64_t X = L.col[(size_t)e2];
+        for (int q = 0; q < r; ++q)
+          vdst[(size_t)(vpos + L.vcol[(size_t)b] + q)] =
+              (int32_t)(L.tu_base + L.ucolbase[(size_t)X] + L.ucol[(size_t)b] + q);
+      }
+      vpos += L.vR[(size_t)Y];
     }
   }
-  if (t_len > INT32_MAX) throw Error{H2D_EINVAL, "t vector exceeds 2^31 entries"};
+  if (vpos != t_len) throw Error{H2D_ECUDA, "t layout mismatch"};
+  h.t_len = t_len;
+  h.d_t = h.alloc<double>(t_len);
+  h.d_vdst = h.alloc<int32_t>(vdst.size());
+  H2D_CUDA(cudaMemcpyAsync(h.d_vdst, vdst.data(), vdst.size() * 4, cudaMemcpyHostToDevice, s));
   for (int l = 1; l <= h.kappa; ++l) {
     Level& L = h.levels[(size_t)l];
-    // t index of every U-panel column
-    std::vector<int32_t> tidx((size_t)L.ucolbase[(size_t)L.nbox]);
-    for (int64_t X = 0; X < L.nbox; ++X)
-      for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
-        const int r = std::max<int32_t>(0, L.rank[(size_t)e]);
-        const int64_t Y = L.col[(size_t)e];
-        for (int q = 0; q < r; ++q)
-          tidx[(size_t)(L.ucolbase[(size_t)X] + L.ucol[(size_t)e] + q)] =
-              (int32_t)(L.t_off[(size_t)Y] + L.vcol[(size_t)e] + q);
-      }
-    L.d_tidx = h.alloc<int32_t>(tidx.size());
     L.d_ucolbase = h.alloc<int32_t>(L.ucolbase.size());
     L.d_upan_off = h.alloc<int64_t>(L.upan_off.size());
-    if (!tidx.empty())
-      H2D_CUDA(cudaMemcpyAsync(L.d_tidx, tidx.data(), tidx.size() * 4, cudaMemcpyHostToDevice, s));
     H2D_CUDA(cudaMemcpyAsync(L.d_ucolbase, L.ucolbase.data(), L.ucolbase.size() * 4,
                              cudaMemcpyHostToDevice, s));
     H2D_CUDA(cudaMemcpyAsync(L.d_upan_off, L.upan_off.data(), L.upan_off.size() * 8,
@@ -448,7 +434,7 @@ void finalize_schedule(Handle& h) {
     h.lp.V[l] = L.V;
     h.lp.ucolbase[l] = L.d_ucolbase;
     h.lp.upan_off[l] = L.d_upan_off;
-    h.lp.tidx[l] = L.d_tidx;
+    h.lp.tu[l] = h.d_t + L.tu_base;
     // stage-A items: chunks of <= kATarget elements and <= kAMaxRows rows
     for (int64_t Y = 0; Y < L.nbox; ++Y) {
       const int R = L.vR[(size_t)Y];
@@ -459,11 +445,12 @@ void finalize_schedule(Handle& h) {
       nch = std::min<int64_t>(nY, std::max<int64_t>(1, nch));
       const int64_t rows = (nY + nch - 1) / nch;
       nch = (nY + rows - 1) / rows;
+      const int32_t vp = (int32_t)L.t_off[(size_t)Y];
       if (nch == 1) {
-        aitems.push_back(AItem{L.vpan_off[(size_t)Y], y0, (int32_t)nY, R, (int32_t)L.t_off[(size_t)Y], l});
+        aitems.push_back(AItem{L.vpan_off[(size_t)Y], y0, (int32_t)nY, R, vp, l});
       } else {
         if (tpart_len + nch * R > INT32_MAX) throw Error{H2D_EINVAL, "partial buffer too large"};
-        ritems.push_back(RItem{(int32_t)L.t_off[(size_t)Y], (int32_t)tpart_len, R, (int32_t)nch});
+        ritems.push_back(RItem{vp, (int32_t)tpart_len, R, (int32_t)nch});
         for (int64_t c = 0; c < nch; ++c) {
           const int64_t r0 = c * rows, nr = std::min(rows, nY - r0);
           aitems.push_back(AItem{L.vpan_off[(size_t)Y] + r0 * R, y0 + r0, (int32_t)nr, R,
@@ -473,12 +460,7 @@ void finalize_schedule(Handle& h) {
       }
     }
   }
-  h.t_len = t_len;
   h.tpart_len = tpart_len;
-  h.rmax_panel = max_gather_width(h);
-  h.max_ritem_R = 1;
-  for (auto& r : ritems) h.max_ritem_R = std::max(h.max_ritem_R, (int)r.R);
-  h.d_t = h.alloc<double>(t_len);
   h.d_tpart = h.alloc<double>(tpart_len);
   h.n_aitems = (int64_t)aitems.size();
   h.n_ritems = (int64_t)ritems.size();
@@ -496,11 +478,6 @@ void finalize_schedule(Handle& h) {
     H2D_CUDA(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
     H2D_CUDA(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
   }
-  const size_t smem = (size_t)h.rmax_panel * sizeof(double);
-  if (smem > 40 * 1024)
-    H2D_CUDA(cudaFuncSetAttribute(stageB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)std::min<size_t>(smem, 200 * 1024)));
-  if (smem > 200 * 1024) throw Error{H2D_EINVAL, "U panels too wide for stage B shared memory"};
   H2D_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -547,23 +524,21 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
   record(h, 7, a);
   H2D_CUDA(cudaEventRecord(h.ev_join, a));
   if (h.n_aitems > 0) {
-    stageA_kernel<<<(int)h.n_aitems, kAThreads, 0, s>>>(h.d_aitems, h.lp, d_xtree, h.d_t, h.d_tpart);
+    stageA_kernel<<<(int)h.n_aitems, kAThreads, 0, s>>>(h.d_aitems, h.lp, d_xtree, h.d_vdst, h.d_t,
+                                                        h.d_tpart);
     H2D_LAUNCH_CHECK();
   }
   record(h, 2, s);
   if (h.n_ritems > 0) {
-    dim3 grid((unsigned)h.n_ritems, (unsigned)std::max(1, (h.max_ritem_R + 7) / 8));
-    reduce_kernel<<<grid, 256, 0, s>>>(h.d_ritems, h.d_tpart, h.d_t);
+    reduce_kernel<<<(int)h.n_ritems, 256, 0, s>>>(h.d_ritems, h.d_tpart, h.d_vdst, h.d_t);
     H2D_LAUNCH_CHECK();
   }
   record(h, 3, s);
   H2D_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
   record(h, 4, s);
   if (nleaves > 0) {
-    const size_t smem = (size_t)h.rmax_panel * sizeof(double);
-    stageB_kernel<<<(int)nleaves, kBThreads, smem, s>>>(h.kappa, h.leaf_begin, h.d_leaf_start, h.lp,
-                                                         h.d_t, h.d_ynear, d_y, h.d_perm, order_out,
-                                                         y_row0);
+    stageB_kernel<<<(int)nleaves, kBThreads, 0, s>>>(h.kappa, h.leaf_begin, h.d_leaf_start, h.lp,
+                                                      h.d_ynear, d_y, h.d_perm, order_out, y_row0);
     H2D_LAUNCH_CHECK();
   }
   record(h, 5, s);

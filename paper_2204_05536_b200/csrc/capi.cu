@@ -63,13 +63,13 @@ static void clear_factors(Handle& h) {
     Level& L = h.levels[(size_t)l];
     h.release(L.U); L.U = nullptr;
     h.release(L.V); L.V = nullptr;
-    h.release(L.d_tidx); L.d_tidx = nullptr;
     h.release(L.d_ucolbase); L.d_ucolbase = nullptr;
     h.release(L.d_upan_off); L.d_upan_off = nullptr;
   }
   h.release(h.d_aitems); h.d_aitems = nullptr;
   h.release(h.d_ritems); h.d_ritems = nullptr;
   h.release(h.d_t); h.d_t = nullptr;
+  h.release(h.d_vdst); h.d_vdst = nullptr;
   h.release(h.d_tpart); h.d_tpart = nullptr;
   h.n_aitems = h.n_ritems = 0;
 }
@@ -469,12 +469,10 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   // algorithmic bytes: stage A reads V + x per chunk and writes t;
   // stage B reads U + t (+ tidx) + near-field points/x and writes y.
   const int64_t served = h.row_end - h.row_begin;
-  // stage A: V panels once, x once, t written once.  stage B: U panels once, t + its
-  // index read once, ynear read once, y written once.  P2P: points + x + ynear.
-  int64_t tidx_len = 0;
-  for (int l = 1; l <= h.kappa; ++l) tidx_len += h.levels[(size_t)l].ucolbase.empty() ? 0 : h.levels[(size_t)l].ucolbase.back();
-  info->stageA_bytes = 8 * vv + 8 * (int64_t)h.n + 8 * h.t_len;
-  info->stageB_bytes = 8 * uv + 8 * h.t_len + 4 * tidx_len + 16 * served;
+  // stage A: V panels once, x once, t (+ its destination index) written once.  stage B:
+  // U panels once, t read once, ynear read once, y written once.  P2P: points + x + ynear.
+  info->stageA_bytes = 8 * vv + 8 * (int64_t)h.n + 12 * h.t_len;
+  info->stageB_bytes = 8 * uv + 8 * h.t_len + 16 * served;
   info->p2p_bytes = 24 * served + 8 * served;
   info->matvec_bytes = info->stageA_bytes + info->stageB_bytes + info->p2p_bytes;
   info->device_bytes = (int64_t)h.device_bytes;

@@ -86,21 +86,22 @@ struct Level {
   std::vector<int64_t> t_off;               // per box: t of column box Y (global t index)
   int32_t* d_ucolbase = nullptr;            // [nbox + 1]
   int64_t* d_upan_off = nullptr;            // [nbox]
-  int32_t* d_tidx = nullptr;                // [sum R_X]: t index of every U-panel column
+  int64_t tu_base = 0;                      // first t entry of the level (U-panel order)
 };
 
-// Stage-A work item: one row chunk of one V panel.
+// Stage-A work item: one row chunk of one V panel.  Outputs go to t (U-panel order)
+// through vdst[out + q] when out >= 0, or to the partial buffer at -out-1 + q.
 struct AItem {
   int64_t v_off;   // element offset of the chunk's first row inside the level V array
   int64_t x_off;   // TREE index of the chunk's first row
   int32_t nrows;
   int32_t R;       // panel width RV_Y
-  int32_t out;     // output index (into t or the partial buffer)
+  int32_t out;
   int32_t level;
 };
-// Reduction of multi-chunk partials: t[t_off + q] = sum_c part[p_off + c*R + q]
+// Reduction of multi-chunk partials: t[vdst[vpos + q]] = sum_c part[p_off + c*R + q]
 struct RItem {
-  int32_t t_off;
+  int32_t vpos;
   int32_t p_off;
   int32_t R;
   int32_t nchunks;
@@ -111,7 +112,7 @@ struct LevelPtrs {
   const double* V[H2D_MAX_LEVELS + 1];
   const int32_t* ucolbase[H2D_MAX_LEVELS + 1];
   const int64_t* upan_off[H2D_MAX_LEVELS + 1];
-  const int32_t* tidx[H2D_MAX_LEVELS + 1];
+  const double* tu[H2D_MAX_LEVELS + 1];   // t of the level in U-panel column order
 };
 
 struct Handle {
@@ -147,7 +148,8 @@ struct Handle {
   int64_t n_aitems = 0;
   RItem* d_ritems = nullptr;
   int64_t n_ritems = 0;
-  double* d_t = nullptr;                  // all t values
+  double* d_t = nullptr;                  // all t values, U-panel column order
+  int32_t* d_vdst = nullptr;              // V-panel column (column-box order) -> t index
   int64_t t_len = 0;
   double* d_tpart = nullptr;              // multi-chunk partials
   int64_t tpart_len = 0;
