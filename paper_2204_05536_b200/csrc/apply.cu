@@ -29,7 +29,7 @@ constexpr int kBThreads = 256;
 constexpr int kTile = 512;           // near-field points staged in smem per tile
 constexpr int64_t kATarget = 32768;  // stage-A elements per CTA
 constexpr int kAUnroll = 8;
-constexpr int kAMaxRows = 2048;      // rows per stage-A chunk (x staged in smem)
+constexpr int kAMaxRows = 4096;      // rows per stage-A chunk (x staged in smem)
 constexpr int kBUnroll = 8;
 
 struct CopyItem {
@@ -73,9 +73,11 @@ T* upload_tmp(const std::vector<T>& v, cudaStream_t s) {
 __global__ void __launch_bounds__(kAThreads, 6)
 stageA_kernel(const AItem* __restrict__ items, LevelPtrs lp, const double* __restrict__ x,
               const int32_t* __restrict__ vdst, double* __restrict__ t,
-              double* __restrict__ tpart) {
+              double* __restrict__ tpart, const RItem* __restrict__ ritems,
+              int32_t* __restrict__ rcount) {
   __shared__ double red[kAThreads];
   __shared__ double xs[kAMaxRows];
+  __shared__ int s_last;
   const AItem it = items[blockIdx.x];
   const double* __restrict__ V = lp.V[it.level] + it.v_off;
   const int R = it.R, nrows = it.nrows, tid = threadIdx.x;
@@ -116,26 +118,40 @@ stageA_kernel(const AItem* __restrict__ items, LevelPtrs lp, const double* __res
       else tpart[(-(int64_t)it.out - 1) + q0 + tid] = acc;
     }
   }
-}
-
-// t[vdst[vpos + q]] = sum_c tpart[p_off + c*R + q]: one CTA per item, one warp per q,
-// lanes over chunks, fixed shuffle tree (deterministic).
-__global__ void reduce_kernel(const RItem* __restrict__ items, const double* __restrict__ tpart,
-                              const int32_t* __restrict__ vdst, double* __restrict__ t) {
-  const RItem it = items[blockIdx.x];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int q = w; q < it.R; q += nw) {
-    double s = 0.0;
-    for (int c = lane; c < it.nchunks; c += 32) s += tpart[it.p_off + (int64_t)c * it.R + q];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) t[vdst[it.vpos + q]] = s;
+  if (it.ritem < 0) return;
+  // Multi-chunk box: the last chunk CTA to finish sums the partials in chunk order
+  // (deterministic) and resets the counter for the next matvec.
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const RItem ri = ritems[it.ritem];
+    s_last = atomicAdd(rcount + it.ritem, 1) == ri.nchunks - 1;
   }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const RItem ri = ritems[it.ritem];
+  for (int q = tid; q < ri.R; q += kAThreads) {
+    const double* __restrict__ pp = tpart + ri.p_off + q;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int c = 0;
+    for (; c + 3 < ri.nchunks; c += 4) {
+      a0 += __ldcg(pp + (int64_t)c * ri.R);
+      a1 += __ldcg(pp + (int64_t)(c + 1) * ri.R);
+      a2 += __ldcg(pp + (int64_t)(c + 2) * ri.R);
+      a3 += __ldcg(pp + (int64_t)(c + 3) * ri.R);
+    }
+    for (; c < ri.nchunks; ++c) a0 += __ldcg(pp + (int64_t)c * ri.R);
+    t[vdst[ri.vpos + q]] = (a0 + a1) + (a2 + a3);
+  }
+  if (tid == 0) rcount[it.ritem] = 0;
 }
 
 // ---------------------------------------------------------------- near-field P2P
 // ynear_L = shift x_L + scale * sum_{Y in {L} u E_L} K(L, Y) x_Y   (Alg. 2 l.4, l.7)
 // One CTA per leaf; the <= 5 near leaves' points and x are staged in shared-memory tiles,
 // thread (g, i) owns row i and columns j = g, g+G, ...; entries are evaluated on the fly.
+template <int KID>
 __global__ void __launch_bounds__(kBThreads)
 p2p_kernel(int64_t leaf_begin, const int32_t* __restrict__ leaf_start,
            const int32_t* __restrict__ nf_off, const int32_t* __restrict__ nf_col,
@@ -188,10 +204,10 @@ p2p_kernel(int64_t leaf_begin, const int32_t* __restrict__ leaf_start,
         double b0 = 0.0, b1 = 0.0;
         int j = g;
         for (; j + G < tn; j += 2 * G) {
-          b0 = fma(kernel_eval(kp, pxi, pyi, tpx[j], tpy[j]), txv[j], b0);
-          b1 = fma(kernel_eval(kp, pxi, pyi, tpx[j + G], tpy[j + G]), txv[j + G], b1);
+          b0 = fma(kernel_eval_t<KID>(kp, pxi, pyi, tpx[j], tpy[j]), txv[j], b0);
+          b1 = fma(kernel_eval_t<KID>(kp, pxi, pyi, tpx[j + G], tpy[j + G]), txv[j + G], b1);
         }
-        for (; j < tn; j += G) b0 = fma(kernel_eval(kp, pxi, pyi, tpx[j], tpy[j]), txv[j], b0);
+        for (; j < tn; j += G) b0 = fma(kernel_eval_t<KID>(kp, pxi, pyi, tpx[j], tpy[j]), txv[j], b0);
         near += b0 + b1;
       }
     }
@@ -208,67 +224,92 @@ p2p_kernel(int64_t leaf_begin, const int32_t* __restrict__ leaf_start,
 }
 
 // ---------------------------------------------------------------- stage B: y = ynear + U t
-// One CTA per leaf L.  Thread (g, i) owns row i of the leaf and columns q = g, g+G, ... of
-// every ancestor U panel: it streams the contiguous row segment of each column (8 loads in
-// flight) and reads the matching t entries straight from L1/L2 (t is contiguous per row
-// box and shared by all rows), so there is no barrier until the final row reduction.
+// One CTA (8 warps) per leaf L.  Lane i owns rows i, i+32, ... (RPL rows) of the leaf;
+// warp w owns columns q = w, w+8, ... of every ancestor U panel.  For a column, the
+// warp's loads are 256 B contiguous row segments at constant offsets (no per-load
+// address math); t for 32 of the warp's columns is fetched with one coalesced load and
+// broadcast by shuffles.  8 loads in flight per thread, one barrier (final row sum).
+template <int RPL, int CU>
+__device__ __forceinline__ void stageB_rows(int kappa, int rows_here, int64_t rowoff,
+                                            const int* s_R, const int* s_cb,
+                                            const int64_t* s_base, const int64_t* s_mX,
+                                            const LevelPtrs& lp, double (&acc)[4]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  bool valid[RPL];
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) valid[r] = lane + 32 * r < rows_here;
+  for (int l = 1; l <= kappa; ++l) {
+    const int R = s_R[l];
+    const int64_t mX = s_mX[l];
+    const double* __restrict__ base = lp.U[l] + s_base[l] + rowoff + lane;
+    const double* __restrict__ tl = lp.tu[l] + s_cb[l];
+    const int64_t stepc = 8 * mX;                    // this warp's next column
+    for (int q0 = w; q0 < R; q0 += 8 * 32) {
+      const int qq = q0 + 8 * lane;
+      const double tq = qq < R ? __ldg(tl + qq) : 0.0;
+      const int ncol = min(32, (R - q0 + 7) >> 3);
+      const double* __restrict__ p = base + (int64_t)q0 * mX;
+      int k = 0;
+      for (; k + CU <= ncol; k += CU, p += CU * stepc) {
+        double u[CU][RPL];
+#pragma unroll
+        for (int c = 0; c < CU; ++c)
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) u[c][r] = valid[r] ? __ldcs(p + c * stepc + 32 * r) : 0.0;
+#pragma unroll
+        for (int c = 0; c < CU; ++c) {
+          const double tv = __shfl_sync(0xffffffffu, tq, k + c);
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) acc[r] = fma(u[c][r], tv, acc[r]);
+        }
+      }
+      for (; k < ncol; ++k, p += stepc) {
+        const double tv = __shfl_sync(0xffffffffu, tq, k);
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) acc[r] = fma(valid[r] ? __ldcs(p + 32 * r) : 0.0, tv, acc[r]);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kBThreads, 4)
 stageB_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_start, LevelPtrs lp,
               const double* __restrict__ ynear, double* __restrict__ y,
               const int32_t* __restrict__ perm, int order_out, int64_t y_row0) {
-  __shared__ double red[kBThreads];
+  __shared__ double red[8][128];
+  __shared__ int s_R[H2D_MAX_LEVELS + 1], s_cb[H2D_MAX_LEVELS + 1];
+  __shared__ int64_t s_base[H2D_MAX_LEVELS + 1], s_mX[H2D_MAX_LEVELS + 1];
   const int64_t L = leaf_begin + blockIdx.x;
   const int64_t s0 = leaf_start[L];
   const int mL = leaf_start[L + 1] - (int)s0;
   if (mL <= 0) return;
-  const int tid = threadIdx.x;
-  for (int rp = 0; rp < mL; rp += kBThreads) {
-    const int RT = min(mL - rp, kBThreads);
-    const int G = kBThreads / RT;
-    const int g = tid / RT;
-    const int il = tid - g * RT;
-    double a[4] = {0.0, 0.0, 0.0, 0.0};
-    if (g < G) {
-      for (int l = 1; l <= kappa; ++l) {
-        const int sh = 2 * (kappa - l);
-        const int64_t X = L >> sh;
-        const int32_t cb = lp.ucolbase[l][X];
-        const int R = lp.ucolbase[l][X + 1] - cb;
-        const int64_t bx0 = leaf_start[X << sh];
-        const int64_t mX = leaf_start[(X + 1) << sh] - bx0;
-        const double* __restrict__ p = lp.U[l] + lp.upan_off[l][X] + (s0 - bx0) + rp + il +
-                                       (int64_t)g * mX;
-        const double* __restrict__ tx = lp.tu[l] + cb;
-        const int64_t step = (int64_t)G * mX;
-        int q = g;
-        for (; q + (kBUnroll - 1) * G < R; q += kBUnroll * G, p += kBUnroll * step) {
-          double u[kBUnroll], tv[kBUnroll];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid >= 1 && tid <= kappa) {           // per-level metadata, fetched in parallel once
+    const int l = tid, sh = 2 * (kappa - l);
+    const int64_t X = L >> sh;
+    const int32_t cb = lp.ucolbase[l][X];
+    const int64_t bx0 = leaf_start[X << sh];
+    s_R[l] = lp.ucolbase[l][X + 1] - cb;
+    s_cb[l] = cb;
+    s_mX[l] = leaf_start[(X + 1) << sh] - bx0;
+    s_base[l] = lp.upan_off[l][X] + (s0 - bx0);
+  }
+  __syncthreads();
+  for (int rp = 0; rp < mL; rp += 128) {
+    const int rows = min(mL - rp, 128);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (rows <= 32) stageB_rows<1, 8>(kappa, rows, rp, s_R, s_cb, s_base, s_mX, lp, acc);
+    else if (rows <= 64) stageB_rows<2, 4>(kappa, rows, rp, s_R, s_cb, s_base, s_mX, lp, acc);
+    else if (rows <= 96) stageB_rows<3, 2>(kappa, rows, rp, s_R, s_cb, s_base, s_mX, lp, acc);
+    else stageB_rows<4, 2>(kappa, rows, rp, s_R, s_cb, s_base, s_mX, lp, acc);
+    if (rp > 0) __syncthreads();
 #pragma unroll
-          for (int k = 0; k < kBUnroll; ++k) u[k] = __ldcs(p + k * step);
-#pragma unroll
-          for (int k = 0; k < kBUnroll; ++k) tv[k] = __ldg(tx + q + k * G);
-#pragma unroll
-          for (int k = 0; k < kBUnroll; ++k) a[k & 3] = fma(u[k], tv[k], a[k & 3]);
-        }
-        for (; q < R; q += G, p += step) a[0] = fma(__ldcs(p), __ldg(tx + q), a[0]);
-      }
-    }
-    const double acc = (a[0] + a[1]) + (a[2] + a[3]);
-    if (G == 1) {
-      if (tid < RT) {
-        const int64_t r = s0 + rp + tid;
-        const double s = acc + ynear[r];
-        if (order_out == H2D_ORDER_ORIGINAL) y[perm[r]] = s;
-        else y[r - y_row0] = s;
-      }
-      continue;
-    }
+    for (int r = 0; r < 4; ++r) red[w][lane + 32 * r] = acc[r];
     __syncthreads();
-    red[tid] = acc;
-    __syncthreads();
-    if (tid < RT) {
+    if (tid < rows) {
       double s = 0.0;
-      for (int gg = 0; gg < G; ++gg) s += red[gg * RT + tid];
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) s += red[ww][tid];
       const int64_t r = s0 + rp + tid;
       s += ynear[r];
       if (order_out == H2D_ORDER_ORIGINAL) y[perm[r]] = s;
@@ -447,14 +488,15 @@ void finalize_schedule(Handle& h) {
       nch = (nY + rows - 1) / rows;
       const int32_t vp = (int32_t)L.t_off[(size_t)Y];
       if (nch == 1) {
-        aitems.push_back(AItem{L.vpan_off[(size_t)Y], y0, (int32_t)nY, R, vp, l});
+        aitems.push_back(AItem{L.vpan_off[(size_t)Y], y0, (int32_t)nY, R, vp, l, -1, 0});
       } else {
         if (tpart_len + nch * R > INT32_MAX) throw Error{H2D_EINVAL, "partial buffer too large"};
         ritems.push_back(RItem{vp, (int32_t)tpart_len, R, (int32_t)nch});
         for (int64_t c = 0; c < nch; ++c) {
           const int64_t r0 = c * rows, nr = std::min(rows, nY - r0);
           aitems.push_back(AItem{L.vpan_off[(size_t)Y] + r0 * R, y0 + r0, (int32_t)nr, R,
-                                 (int32_t)(-(tpart_len + c * R) - 1), l});
+                                 (int32_t)(-(tpart_len + c * R) - 1), l,
+                                 (int32_t)(ritems.size() - 1), 0});
         }
         tpart_len += nch * R;
       }
@@ -466,6 +508,8 @@ void finalize_schedule(Handle& h) {
   h.n_ritems = (int64_t)ritems.size();
   h.d_aitems = h.alloc<AItem>(aitems.size());
   h.d_ritems = h.alloc<RItem>(ritems.size());
+  h.d_rcount = h.alloc<int32_t>(ritems.size());
+  H2D_CUDA(cudaMemsetAsync(h.d_rcount, 0, std::max<size_t>(1, ritems.size()) * sizeof(int32_t), s));
   if (!aitems.empty())
     H2D_CUDA(cudaMemcpyAsync(h.d_aitems, aitems.data(), aitems.size() * sizeof(AItem),
                              cudaMemcpyHostToDevice, s));
@@ -473,6 +517,8 @@ void finalize_schedule(Handle& h) {
     H2D_CUDA(cudaMemcpyAsync(h.d_ritems, ritems.data(), ritems.size() * sizeof(RItem),
                              cudaMemcpyHostToDevice, s));
   if (!h.d_ynear) h.d_ynear = h.alloc<double>(h.n);
+  H2D_CUDA(cudaFuncSetAttribute(stageA_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                cudaSharedmemCarveoutMaxShared));
   if (!h.aux_stream) {
     H2D_CUDA(cudaStreamCreateWithFlags(&h.aux_stream, cudaStreamNonBlocking));
     H2D_CUDA(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
@@ -516,23 +562,22 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
   H2D_CUDA(cudaStreamWaitEvent(a, h.ev_fork, 0));
   record(h, 6, a);
   if (nleaves > 0) {
-    p2p_kernel<<<(int)nleaves, kBThreads, 0, a>>>(h.leaf_begin, h.d_leaf_start, h.d_nf_off,
-                                                   h.d_nf_col, h.d_px, h.d_py, d_xtree, h.kp,
-                                                   h.d_ynear);
+    auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_kernel<H2D_KERNEL_LOG>
+              : h.kp.id == H2D_KERNEL_IMQ ? p2p_kernel<H2D_KERNEL_IMQ>
+              : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_kernel<H2D_KERNEL_ONE_OVER_R>
+                                                 : p2p_kernel<H2D_KERNEL_TEST_LOWRANK>;
+    kfn<<<(int)nleaves, kBThreads, 0, a>>>(h.leaf_begin, h.d_leaf_start, h.d_nf_off, h.d_nf_col,
+                                           h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear);
     H2D_LAUNCH_CHECK();
   }
   record(h, 7, a);
   H2D_CUDA(cudaEventRecord(h.ev_join, a));
   if (h.n_aitems > 0) {
     stageA_kernel<<<(int)h.n_aitems, kAThreads, 0, s>>>(h.d_aitems, h.lp, d_xtree, h.d_vdst, h.d_t,
-                                                        h.d_tpart);
+                                                        h.d_tpart, h.d_ritems, h.d_rcount);
     H2D_LAUNCH_CHECK();
   }
   record(h, 2, s);
-  if (h.n_ritems > 0) {
-    reduce_kernel<<<(int)h.n_ritems, 256, 0, s>>>(h.d_ritems, h.d_tpart, h.d_vdst, h.d_t);
-    H2D_LAUNCH_CHECK();
-  }
   record(h, 3, s);
   H2D_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
   record(h, 4, s);

@@ -68,6 +68,7 @@ static void clear_factors(Handle& h) {
   }
   h.release(h.d_aitems); h.d_aitems = nullptr;
   h.release(h.d_ritems); h.d_ritems = nullptr;
+  h.release(h.d_rcount); h.d_rcount = nullptr;
   h.release(h.d_t); h.d_t = nullptr;
   h.release(h.d_vdst); h.d_vdst = nullptr;
   h.release(h.d_tpart); h.d_tpart = nullptr;

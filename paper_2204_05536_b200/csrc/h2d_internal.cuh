@@ -36,6 +36,26 @@ struct KernelParams {
   int test_rank;
 };
 
+// K(p, q) specialised at compile time (hot P2P loop: no per-pair dispatch).
+template <int KID>
+__device__ __forceinline__ double kernel_eval_t(const KernelParams& k, double px, double py,
+                                                double qx, double qy) {
+  const double dx = px - qx, dy = py - qy;
+  const double r2 = fma(dx, dx, dy * dy);
+  if (KID == H2D_KERNEL_LOG) {
+    return r2 > 0.0 ? 0.5 * log(r2) : 0.0;
+  } else if (KID == H2D_KERNEL_IMQ) {
+    return rsqrt(fma(r2, k.inv_c2, 1.0));
+  } else if (KID == H2D_KERNEL_ONE_OVER_R) {
+    return r2 > 0.0 ? rsqrt(r2) : 0.0;
+  } else {
+    double acc = 0.0;
+    for (int s = 0; s < k.test_rank; ++s)
+      acc = fma(cos((s + 1) * px + 0.5 * s * py), cos((s + 1) * qx + 0.5 * s * qy), acc);
+    return acc;
+  }
+}
+
 // K(p, q) for r^2 = |p - q|^2; K(r = 0) := K0 (R8) by distance, not by index.
 __device__ __forceinline__ double kernel_eval(const KernelParams& k, double px, double py,
                                               double qx, double qy) {
@@ -98,6 +118,8 @@ struct AItem {
   int32_t R;       // panel width RV_Y
   int32_t out;
   int32_t level;
+  int32_t ritem;   // >= 0: multi-chunk box (RItem index); the last chunk CTA reduces
+  int32_t pad;
 };
 // Reduction of multi-chunk partials: t[vdst[vpos + q]] = sum_c part[p_off + c*R + q]
 struct RItem {
@@ -148,6 +170,7 @@ struct Handle {
   int64_t n_aitems = 0;
   RItem* d_ritems = nullptr;
   int64_t n_ritems = 0;
+  int32_t* d_rcount = nullptr;            // per RItem: chunk CTAs finished (self-resetting)
   double* d_t = nullptr;                  // all t values, U-panel column order
   int32_t* d_vdst = nullptr;              // V-panel column (column-box order) -> t index
   int64_t t_len = 0;
