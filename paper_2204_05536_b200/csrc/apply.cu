@@ -26,7 +26,6 @@ namespace {
 
 constexpr int kAThreads = 256;
 constexpr int kBThreads = 256;
-constexpr int kTile = 512;           // near-field points staged in smem per tile
 constexpr int64_t kATarget = 32768;  // stage-A elements per CTA
 constexpr int kAUnroll = 8;
 constexpr int kAMaxRows = 4096;      // rows per stage-A chunk (x staged in smem)
@@ -70,7 +69,7 @@ T* upload_tmp(const std::vector<T>& v, cudaStream_t s) {
 // The chunk is a contiguous row-major block nrows x R of the V panel; thread (g, q) owns
 // panel column q and rows g, g+G, ..., so each CTA step reads G*R consecutive doubles,
 // 8 rows in flight per thread; x_chunk is staged once in shared memory.
-__global__ void __launch_bounds__(kAThreads, 6)
+__global__ void __launch_bounds__(kAThreads, 4)
 stageA_kernel(const AItem* __restrict__ items, LevelPtrs lp, const double* __restrict__ x,
               const int32_t* __restrict__ vdst, double* __restrict__ t,
               double* __restrict__ tpart, const RItem* __restrict__ ritems,
@@ -147,79 +146,174 @@ stageA_kernel(const AItem* __restrict__ items, LevelPtrs lp, const double* __res
   if (tid == 0) rcount[it.ritem] = 0;
 }
 
-// ---------------------------------------------------------------- near-field P2P
-// ynear_L = shift x_L + scale * sum_{Y in {L} u E_L} K(L, Y) x_Y   (Alg. 2 l.4, l.7)
-// One CTA per leaf; the <= 5 near leaves' points and x are staged in shared-memory tiles,
-// thread (g, i) owns row i and columns j = g, g+G, ...; entries are evaluated on the fly.
+// ---------------------------------------------------------------- near-field P2P (symmetric)
+// Alg. 2 l.4 and l.7: y_X += K(X, X) x_X + sum_{Y in E_X} K(X, Y) x_Y.
+// Every configured kernel is symmetric, so each unordered leaf pair is evaluated
+// once: the CTA of leaf X evaluates its self block (i < j, plus the diagonal) and the
+// blocks with its +x and +y edge neighbours (Morton codes grow with each coordinate, so
+// those are the higher-numbered sharers).  Contributions land in three slots per row,
+// each row slot having exactly one writer CTA (deterministic, no atomics):
+//   s0[r] : row r's own CTA (self block + its +x/+y blocks, both orientations of self)
+//   sL[r] : written by the -x neighbour's CTA (K(X_left, X)^T x_left)
+//   sD[r] : written by the -y neighbour's CTA
+// Stage B adds shift x + scale (s0 + sL + sD).  Neighbours outside the rank's served
+// leaves are evaluated one-sidedly by the served leaf (rows only).
+// Thread (ti, tj) of a 16 x 16 grid owns the 4 x 4 micro-tile rows ti + 16a, columns
+// tj + 16b of a 64 x 64 super-tile: 16 independent kernel evaluations per super-tile with
+// the 8 point coordinates and x values held in registers.
+constexpr int kSymRowsOnly = 0, kSymBoth = 1, kSymSelf = 2;
+
 template <int KID>
-__global__ void __launch_bounds__(kBThreads)
-p2p_kernel(int64_t leaf_begin, const int32_t* __restrict__ leaf_start,
-           const int32_t* __restrict__ nf_off, const int32_t* __restrict__ nf_col,
-           const double* __restrict__ px, const double* __restrict__ py,
-           const double* __restrict__ x, KernelParams kp, double* __restrict__ ynear) {
-  __shared__ double tpx[kTile], tpy[kTile], txv[kTile];
-  __shared__ double red[kBThreads];
-  __shared__ int seg_s[5], seg_n[5];
-  const int64_t L = leaf_begin + blockIdx.x;
-  const int64_t s0 = leaf_start[L];
-  const int mL = leaf_start[L + 1] - (int)s0;
-  if (mL <= 0) return;
-  const int tid = threadIdx.x;
-  if (tid < 5) {
-    const int nf0 = nf_off[L], nfn = nf_off[L + 1] - nf0;
-    int a = 0, n = 0;
-    if (tid < nfn) {
-      const int Y = nf_col[nf0 + tid];
-      a = leaf_start[Y];
-      n = leaf_start[Y + 1] - a;
-    }
-    seg_s[tid] = a;
-    seg_n[tid] = n;
-  }
-  __syncthreads();
-  const int tot_near = seg_n[0] + seg_n[1] + seg_n[2] + seg_n[3] + seg_n[4];
-  for (int rp = 0; rp < mL; rp += kBThreads) {
-    const int RT = min(mL - rp, kBThreads);
-    const int G = kBThreads / RT;
-    const int g = tid / RT;
-    const int il = tid - g * RT;
-    const bool act = g < G;
-    const int64_t row = s0 + rp + il;
-    double pxi = 0.0, pyi = 0.0;
-    if (act) { pxi = px[row]; pyi = py[row]; }
-    double near = 0.0;
-    for (int t0 = 0; t0 < tot_near; t0 += kTile) {
-      const int tn = min(kTile, tot_near - t0);
+__device__ void sym_block(int mode, int64_t a0, int m, int64_t b0, int n, double* row_dst,
+                          double* col_dst, const double* __restrict__ px,
+                          const double* __restrict__ py, const double* __restrict__ x,
+                          const KernelParams& kp, double* s_a, double* s_b,
+                          double (*scol)[65], double* srow) {
+  const int tid = threadIdx.x, ti = tid >> 4, tj = tid & 15;
+  for (int ra = 0; ra < m; ra += 64) {
+    const int mt = min(64, m - ra);
+    const int cstart = mode == kSymSelf ? ra : 0;
+    for (int cb = cstart; cb < n; cb += 64) {
+      const int nt = min(64, n - cb);
       __syncthreads();
-      for (int e = tid; e < tn; e += kBThreads) {
-        int idx = t0 + e, k = 0;
-        while (idx >= seg_n[k]) { idx -= seg_n[k]; ++k; }
-        const int64_t src = seg_s[k] + idx;
-        tpx[e] = px[src];
-        tpy[e] = py[src];
-        txv[e] = x[src];
+      if (tid < mt) {
+        s_a[tid] = px[a0 + ra + tid];
+        s_a[64 + tid] = py[a0 + ra + tid];
+        s_a[128 + tid] = x[a0 + ra + tid];
+      } else if (tid >= 64 && tid < 64 + nt) {
+        const int j = tid - 64;
+        s_b[j] = px[b0 + cb + j];
+        s_b[64 + j] = py[b0 + cb + j];
+        s_b[128 + j] = x[b0 + cb + j];
       }
       __syncthreads();
-      if (act) {
-        double b0 = 0.0, b1 = 0.0;
-        int j = g;
-        for (; j + G < tn; j += 2 * G) {
-          b0 = fma(kernel_eval_t<KID>(kp, pxi, pyi, tpx[j], tpy[j]), txv[j], b0);
-          b1 = fma(kernel_eval_t<KID>(kp, pxi, pyi, tpx[j + G], tpy[j + G]), txv[j + G], b1);
+      const bool diag_tile = mode == kSymSelf && cb == ra;
+      double rpx[4], rpy[4], rx[4], cpx[4], cpy[4], cx[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int i = ti + 16 * a;
+        rpx[a] = s_a[i]; rpy[a] = s_a[64 + i]; rx[a] = i < mt ? s_a[128 + i] : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int j = tj + 16 * b;
+        cpx[b] = s_b[j]; cpy[b] = s_b[64 + j]; cx[b] = j < nt ? s_b[128 + j] : 0.0;
+      }
+      double racc[4] = {0.0, 0.0, 0.0, 0.0}, cacc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = ti + 16 * a, j = tj + 16 * b;
+          bool ok = i < mt && j < nt;
+          if (diag_tile) ok = ok && i <= j;
+          if (ok) {
+            const double k = kernel_eval_t<KID>(kp, rpx[a], rpy[a], cpx[b], cpy[b]);
+            racc[a] = fma(k, cx[b], racc[a]);
+            if (!(diag_tile && i == j)) cacc[b] = fma(k, rx[a], cacc[b]);
+          }
         }
-        for (; j < tn; j += G) b0 = fma(kernel_eval_t<KID>(kp, pxi, pyi, tpx[j], tpy[j]), txv[j], b0);
-        near += b0 + b1;
+      }
+      // rows: reduce over tj (16 lanes of a half-warp)
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        double v = racc[a];
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        if (tj == 0) srow[ti + 16 * a] = v;
+      }
+      if (mode != kSymRowsOnly) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) scol[ti][tj + 16 * b] = cacc[b];
+      }
+      __syncthreads();
+      if (tid < mt) row_dst[ra + tid] += srow[tid];
+      if (mode != kSymRowsOnly) {
+        __syncthreads();   // self blocks: row and column targets may coincide
+        if (tid < nt) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) s += scol[k][tid];
+          col_dst[cb + tid] += s;
+        }
       }
     }
-    __syncthreads();
-    red[tid] = near;
-    __syncthreads();
-    if (tid < RT) {
-      double s = 0.0;
-      for (int gg = 0; gg < G; ++gg) s += red[gg * RT + tid];
-      const int64_t r = s0 + rp + tid;
-      ynear[r] = fma(kp.shift, x[r], kp.scale * s);
-    }
+  }
+}
+
+__device__ __forceinline__ uint32_t p2p_spread(uint32_t v) {
+  v &= 0xFFFFu;
+  v = (v | (v << 8)) & 0x00FF00FFu;
+  v = (v | (v << 4)) & 0x0F0F0F0Fu;
+  v = (v | (v << 2)) & 0x33333333u;
+  v = (v | (v << 1)) & 0x55555555u;
+  return v;
+}
+__device__ __forceinline__ uint32_t p2p_compact(uint32_t v) {
+  v &= 0x55555555u;
+  v = (v | (v >> 1)) & 0x33333333u;
+  v = (v | (v >> 2)) & 0x0F0F0F0Fu;
+  v = (v | (v >> 4)) & 0x00FF00FFu;
+  v = (v | (v >> 8)) & 0x0000FFFFu;
+  return v;
+}
+
+template <int KID>
+__global__ void __launch_bounds__(256, 2)
+p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end,
+               const int32_t* __restrict__ leaf_start, const double* __restrict__ px,
+               const double* __restrict__ py, const double* __restrict__ x, KernelParams kp,
+               double* __restrict__ s0, double* __restrict__ sL, double* __restrict__ sD) {
+  __shared__ double s_a[192], s_b[192], srow[64];
+  __shared__ double scol[16][65];
+  const int64_t X = leaf_begin + blockIdx.x;
+  const int tid = threadIdx.x;
+  const uint32_t cx = p2p_compact((uint32_t)X), cy = p2p_compact((uint32_t)X >> 1);
+  const uint32_t side = 1u << kappa;
+  const int64_t xs = leaf_start[X];
+  const int m = leaf_start[X + 1] - (int)xs;
+  auto served = [&](int64_t Y) { return Y >= leaf_begin && Y < leaf_end; };
+  const bool has_r = cx + 1 < side, has_u = cy + 1 < side, has_l = cx > 0, has_d = cy > 0;
+  const int64_t Rn = has_r ? (int64_t)(p2p_spread(cx + 1) | (p2p_spread(cy) << 1)) : -1;
+  const int64_t Un = has_u ? (int64_t)(p2p_spread(cx) | (p2p_spread(cy + 1) << 1)) : -1;
+  const int64_t Ln = has_l ? (int64_t)(p2p_spread(cx - 1) | (p2p_spread(cy) << 1)) : -1;
+  const int64_t Dn = has_d ? (int64_t)(p2p_spread(cx) | (p2p_spread(cy - 1) << 1)) : -1;
+  const bool do_r = has_r && served(Rn), do_u = has_u && served(Un);
+  const bool own_l = !has_l || !served(Ln), own_d = !has_d || !served(Dn);
+  int64_t rs = 0, us = 0;
+  int rn = 0, un = 0;
+  if (has_r) { rs = leaf_start[Rn]; rn = leaf_start[Rn + 1] - (int)rs; }
+  if (has_u) { us = leaf_start[Un]; un = leaf_start[Un + 1] - (int)us; }
+  // phase 0: zero every slot row this CTA is the writer of
+  for (int i = tid; i < m; i += 256) {
+    s0[xs + i] = 0.0;
+    if (own_l) sL[xs + i] = 0.0;
+    if (own_d) sD[xs + i] = 0.0;
+  }
+  if (do_r)
+    for (int i = tid; i < rn; i += 256) sL[rs + i] = 0.0;
+  if (do_u)
+    for (int i = tid; i < un; i += 256) sD[us + i] = 0.0;
+  if (m == 0) return;
+  // phase 1: blocks in a fixed order
+  sym_block<KID>(kSymSelf, xs, m, xs, m, s0 + xs, s0 + xs, px, py, x, kp, s_a, s_b, scol, srow);
+  if (has_r)
+    sym_block<KID>(do_r ? kSymBoth : kSymRowsOnly, xs, m, rs, rn, s0 + xs, sL + rs, px, py, x, kp,
+                   s_a, s_b, scol, srow);
+  if (has_u)
+    sym_block<KID>(do_u ? kSymBoth : kSymRowsOnly, xs, m, us, un, s0 + xs, sD + us, px, py, x, kp,
+                   s_a, s_b, scol, srow);
+  if (has_l && own_l) {
+    const int64_t ls = leaf_start[Ln];
+    sym_block<KID>(kSymRowsOnly, xs, m, ls, leaf_start[Ln + 1] - (int)ls, sL + xs, nullptr, px, py,
+                   x, kp, s_a, s_b, scol, srow);
+  }
+  if (has_d && own_d) {
+    const int64_t ds = leaf_start[Dn];
+    sym_block<KID>(kSymRowsOnly, xs, m, ds, leaf_start[Dn + 1] - (int)ds, sD + xs, nullptr, px, py,
+                   x, kp, s_a, s_b, scol, srow);
   }
 }
 
@@ -274,7 +368,8 @@ __device__ __forceinline__ void stageB_rows(int kappa, int rows_here, int64_t ro
 
 __global__ void __launch_bounds__(kBThreads, 4)
 stageB_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_start, LevelPtrs lp,
-              const double* __restrict__ ynear, double* __restrict__ y,
+              const double* __restrict__ ynear, int64_t n, const double* __restrict__ x,
+              double scale, double shift, double* __restrict__ y,
               const int32_t* __restrict__ perm, int order_out, int64_t y_row0) {
   __shared__ double red[8][128];
   __shared__ int s_R[H2D_MAX_LEVELS + 1], s_cb[H2D_MAX_LEVELS + 1];
@@ -311,7 +406,8 @@ stageB_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_st
 #pragma unroll
       for (int ww = 0; ww < 8; ++ww) s += red[ww][tid];
       const int64_t r = s0 + rp + tid;
-      s += ynear[r];
+      // near field (three symmetric-P2P slots) + shift x
+      s += fma(scale, (ynear[r] + ynear[n + r]) + ynear[2 * n + r], shift * x[r]);
       if (order_out == H2D_ORDER_ORIGINAL) y[perm[r]] = s;
       else y[r - y_row0] = s;
     }
@@ -516,7 +612,7 @@ void finalize_schedule(Handle& h) {
   if (!ritems.empty())
     H2D_CUDA(cudaMemcpyAsync(h.d_ritems, ritems.data(), ritems.size() * sizeof(RItem),
                              cudaMemcpyHostToDevice, s));
-  if (!h.d_ynear) h.d_ynear = h.alloc<double>(h.n);
+  if (!h.d_ynear) h.d_ynear = h.alloc<double>(3 * h.n);   // three P2P slots (p2p_sym_kernel)
   H2D_CUDA(cudaFuncSetAttribute(stageA_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                 cudaSharedmemCarveoutMaxShared));
   if (!h.aux_stream) {
@@ -562,12 +658,13 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
   H2D_CUDA(cudaStreamWaitEvent(a, h.ev_fork, 0));
   record(h, 6, a);
   if (nleaves > 0) {
-    auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_kernel<H2D_KERNEL_LOG>
-              : h.kp.id == H2D_KERNEL_IMQ ? p2p_kernel<H2D_KERNEL_IMQ>
-              : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_kernel<H2D_KERNEL_ONE_OVER_R>
-                                                 : p2p_kernel<H2D_KERNEL_TEST_LOWRANK>;
-    kfn<<<(int)nleaves, kBThreads, 0, a>>>(h.leaf_begin, h.d_leaf_start, h.d_nf_off, h.d_nf_col,
-                                           h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear);
+    auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_sym_kernel<H2D_KERNEL_LOG>
+              : h.kp.id == H2D_KERNEL_IMQ ? p2p_sym_kernel<H2D_KERNEL_IMQ>
+              : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_sym_kernel<H2D_KERNEL_ONE_OVER_R>
+                                                 : p2p_sym_kernel<H2D_KERNEL_TEST_LOWRANK>;
+    kfn<<<(int)nleaves, 256, 0, a>>>(h.kappa, h.leaf_begin, h.leaf_end, h.d_leaf_start, h.d_px,
+                                     h.d_py, d_xtree, h.kp, h.d_ynear, h.d_ynear + h.n,
+                                     h.d_ynear + 2 * h.n);
     H2D_LAUNCH_CHECK();
   }
   record(h, 7, a);
@@ -583,7 +680,8 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
   record(h, 4, s);
   if (nleaves > 0) {
     stageB_kernel<<<(int)nleaves, kBThreads, 0, s>>>(h.kappa, h.leaf_begin, h.d_leaf_start, h.lp,
-                                                      h.d_ynear, d_y, h.d_perm, order_out, y_row0);
+                                                      h.d_ynear, h.n, d_xtree, h.kp.scale,
+                                                      h.kp.shift, d_y, h.d_perm, order_out, y_row0);
     H2D_LAUNCH_CHECK();
   }
   record(h, 5, s);
