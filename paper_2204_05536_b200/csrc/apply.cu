@@ -26,9 +26,8 @@ namespace {
 
 constexpr int kAThreads = 256;
 constexpr int kBThreads = 256;
-constexpr int64_t kATarget = 32768;  // stage-A elements per CTA
-constexpr int kAUnroll = 8;
-constexpr int kAMaxRows = 4096;      // rows per stage-A chunk (x staged in smem)
+constexpr int64_t kATarget = 65536;  // stage-A elements per CTA
+constexpr int kAMaxRows = 16384;     // rows per stage-A chunk
 constexpr int kBUnroll = 8;
 
 struct CopyItem {
@@ -66,55 +65,70 @@ T* upload_tmp(const std::vector<T>& v, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- stage A: t = V^T x
-// The chunk is a contiguous row-major block nrows x R of the V panel; thread (g, q) owns
-// panel column q and rows g, g+G, ..., so each CTA step reads G*R consecutive doubles,
-// 8 rows in flight per thread; x_chunk is staged once in shared memory.
+// The chunk is a contiguous row-major block nrows x R of the V panel.  Lane l owns the
+// panel columns q0 + l + 32c (c < CPL) and warp w the rows w, w+8, ...: each row is one
+// coalesced 32*CPL-double read at constant offsets, x_i is a warp-uniform broadcast load,
+// 8 loads in flight per thread, partial sums reduced over the 8 warps in shared memory.
+template <int CPL>
+__device__ __forceinline__ void stageA_cols(const double* __restrict__ V, int R, int nrows, int q0,
+                                            int W, const double* __restrict__ xx,
+                                            double (&acc)[8]) {
+  constexpr int RU = 8 / CPL;   // rows per unrolled step
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  bool valid[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) valid[c] = lane + 32 * c < W;
+  const double* __restrict__ p = V + (int64_t)w * R + q0 + lane;
+  const int64_t rstep = (int64_t)8 * R;
+  int i = w;
+  for (; i + 8 * (RU - 1) < nrows; i += 8 * RU, p += RU * rstep) {
+    double v[RU][CPL], xv[RU];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+      xv[u] = __ldg(xx + i + 8 * u);
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) v[u][c] = valid[c] ? __ldcs(p + u * rstep + 32 * c) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < RU; ++u)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) acc[c] = fma(v[u][c], xv[u], acc[c]);
+  }
+  for (; i < nrows; i += 8, p += rstep) {
+    const double xv = __ldg(xx + i);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) acc[c] = fma(valid[c] ? __ldcs(p + 32 * c) : 0.0, xv, acc[c]);
+  }
+}
+
 __global__ void __launch_bounds__(kAThreads, 4)
 stageA_kernel(const AItem* __restrict__ items, LevelPtrs lp, const double* __restrict__ x,
               const int32_t* __restrict__ vdst, double* __restrict__ t,
               double* __restrict__ tpart, const RItem* __restrict__ ritems,
               int32_t* __restrict__ rcount) {
-  __shared__ double red[kAThreads];
-  __shared__ double xs[kAMaxRows];
+  __shared__ double red[8][256];
   __shared__ int s_last;
   const AItem it = items[blockIdx.x];
   const double* __restrict__ V = lp.V[it.level] + it.v_off;
-  const int R = it.R, nrows = it.nrows, tid = threadIdx.x;
-  for (int i = tid; i < nrows; i += kAThreads) xs[i] = __ldg(x + it.x_off + i);
-  __syncthreads();
-  for (int q0 = 0; q0 < R; q0 += kAThreads) {
-    const int W = min(R - q0, kAThreads);      // columns handled in this pass
-    const int G = kAThreads / W;               // row groups
-    const int g = tid / W, q = tid - g * W;
-    double acc = 0.0;
-    if (g < G) {
-      const double* __restrict__ p = V + (int64_t)g * R + q0 + q;
-      const int64_t step = (int64_t)G * R;
-      int i = g;
-      double a[4] = {0.0, 0.0, 0.0, 0.0};
-      for (; i + (kAUnroll - 1) * G < nrows; i += kAUnroll * G, p += kAUnroll * step) {
-        double v[kAUnroll];
+  const double* __restrict__ xx = x + it.x_off;
+  const int R = it.R, nrows = it.nrows, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int q0 = 0; q0 < R; q0 += 256) {
+    const int W = min(R - q0, 256);
+    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (W <= 32) stageA_cols<1>(V, R, nrows, q0, W, xx, acc);
+    else if (W <= 64) stageA_cols<2>(V, R, nrows, q0, W, xx, acc);
+    else if (W <= 128) stageA_cols<4>(V, R, nrows, q0, W, xx, acc);
+    else stageA_cols<8>(V, R, nrows, q0, W, xx, acc);
+    if (q0 > 0) __syncthreads();
 #pragma unroll
-        for (int u = 0; u < kAUnroll; ++u) v[u] = __ldcs(p + u * step);
-#pragma unroll
-        for (int u = 0; u < kAUnroll; ++u) a[u & 3] = fma(v[u], xs[i + u * G], a[u & 3]);
-      }
-      for (; i < nrows; i += G, p += step) a[0] = fma(__ldcs(p), xs[i], a[0]);
-      acc = (a[0] + a[1]) + (a[2] + a[3]);
-    }
-    if (G > 1) {
-      __syncthreads();
-      red[tid] = acc;
-      __syncthreads();
-      if (tid < W) {
-        double s = 0.0;
-        for (int gg = 0; gg < G; ++gg) s += red[gg * W + tid];
-        acc = s;
-      }
-    }
+    for (int c = 0; c < 8; ++c) red[w][lane + 32 * c] = acc[c];
+    __syncthreads();
     if (tid < W) {
-      if (it.out >= 0) t[vdst[it.out + q0 + tid]] = acc;
-      else tpart[(-(int64_t)it.out - 1) + q0 + tid] = acc;
+      double s = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < 8; ++ww) s += red[ww][tid];
+      if (it.out >= 0) t[vdst[it.out + q0 + tid]] = s;
+      else tpart[(-(int64_t)it.out - 1) + q0 + tid] = s;
     }
   }
   if (it.ritem < 0) return;
@@ -164,7 +178,7 @@ stageA_kernel(const AItem* __restrict__ items, LevelPtrs lp, const double* __res
 constexpr int kSymRowsOnly = 0, kSymBoth = 1, kSymSelf = 2;
 
 template <int KID>
-__device__ void sym_block(int mode, int64_t a0, int m, int64_t b0, int n, double* row_dst,
+__device__ __noinline__ void sym_block(int mode, int64_t a0, int m, int64_t b0, int n, double* row_dst,
                           double* col_dst, const double* __restrict__ px,
                           const double* __restrict__ py, const double* __restrict__ x,
                           const KernelParams& kp, double* s_a, double* s_b,
@@ -297,23 +311,26 @@ p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end,
   if (do_u)
     for (int i = tid; i < un; i += 256) sD[us + i] = 0.0;
   if (m == 0) return;
-  // phase 1: blocks in a fixed order
-  sym_block<KID>(kSymSelf, xs, m, xs, m, s0 + xs, s0 + xs, px, py, x, kp, s_a, s_b, scol, srow);
-  if (has_r)
-    sym_block<KID>(do_r ? kSymBoth : kSymRowsOnly, xs, m, rs, rn, s0 + xs, sL + rs, px, py, x, kp,
-                   s_a, s_b, scol, srow);
-  if (has_u)
-    sym_block<KID>(do_u ? kSymBoth : kSymRowsOnly, xs, m, us, un, s0 + xs, sD + us, px, py, x, kp,
-                   s_a, s_b, scol, srow);
-  if (has_l && own_l) {
-    const int64_t ls = leaf_start[Ln];
-    sym_block<KID>(kSymRowsOnly, xs, m, ls, leaf_start[Ln + 1] - (int)ls, sL + xs, nullptr, px, py,
-                   x, kp, s_a, s_b, scol, srow);
-  }
-  if (has_d && own_d) {
-    const int64_t ds = leaf_start[Dn];
-    sym_block<KID>(kSymRowsOnly, xs, m, ds, leaf_start[Dn + 1] - (int)ds, sD + xs, nullptr, px, py,
-                   x, kp, s_a, s_b, scol, srow);
+  // phase 1: blocks in a fixed order (one code instance: keeps the I-cache footprint small)
+  for (int task = 0; task < 5; ++task) {
+    int mode = kSymRowsOnly, n = 0;
+    int64_t b0 = 0;
+    double *rdst = s0 + xs, *cdst = nullptr;
+    if (task == 0) { mode = kSymSelf; b0 = xs; n = m; cdst = s0 + xs; }
+    else if (task == 1) {
+      if (!has_r) continue;
+      mode = do_r ? kSymBoth : kSymRowsOnly; b0 = rs; n = rn; cdst = sL + rs;
+    } else if (task == 2) {
+      if (!has_u) continue;
+      mode = do_u ? kSymBoth : kSymRowsOnly; b0 = us; n = un; cdst = sD + us;
+    } else if (task == 3) {
+      if (!(has_l && own_l)) continue;
+      b0 = leaf_start[Ln]; n = leaf_start[Ln + 1] - (int)b0; rdst = sL + xs;
+    } else {
+      if (!(has_d && own_d)) continue;
+      b0 = leaf_start[Dn]; n = leaf_start[Dn + 1] - (int)b0; rdst = sD + xs;
+    }
+    sym_block<KID>(mode, xs, m, b0, n, rdst, cdst, px, py, x, kp, s_a, s_b, scol, srow);
   }
 }
 
