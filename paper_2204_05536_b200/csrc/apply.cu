@@ -73,31 +73,38 @@ template <int CPL>
 __device__ __forceinline__ void stageA_cols(const double* __restrict__ V, int R, int nrows, int q0,
                                             int W, const double* __restrict__ xx,
                                             double (&acc)[8]) {
-  constexpr int RU = 8 / CPL;   // rows per unrolled step
+  constexpr int RU = CPL >= 5 ? 1 : CPL >= 3 ? 2 : CPL == 2 ? 4 : 8;   // rows per step
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   bool valid[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) valid[c] = lane + 32 * c < W;
-  const double* __restrict__ p = V + (int64_t)w * R + q0 + lane;
   const int64_t rstep = (int64_t)8 * R;
-  int i = w;
-  for (; i + 8 * (RU - 1) < nrows; i += 8 * RU, p += RU * rstep) {
-    double v[RU][CPL], xv[RU];
+  // rows of this warp: w + 8k.  x for 32 of them is fetched by one coalesced load and
+  // broadcast by shuffles.
+  for (int k0 = 0; w + 8 * k0 < nrows; k0 += 32) {
+    const int ib = w + 8 * k0;
+    const int nk = min(32, (nrows - ib + 7) >> 3);
+    const double xl = lane < nk ? __ldg(xx + ib + 8 * lane) : 0.0;
+    const double* __restrict__ p = V + (int64_t)ib * R + q0 + lane;
+    int k = 0;
+    for (; k + RU <= nk; k += RU, p += RU * rstep) {
+      double v[RU][CPL];
 #pragma unroll
-    for (int u = 0; u < RU; ++u) {
-      xv[u] = __ldg(xx + i + 8 * u);
+      for (int u = 0; u < RU; ++u)
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) v[u][c] = valid[c] ? __ldcs(p + u * rstep + 32 * c) : 0.0;
+        for (int c = 0; c < CPL; ++c) v[u][c] = valid[c] ? __ldcs(p + u * rstep + 32 * c) : 0.0;
+#pragma unroll
+      for (int u = 0; u < RU; ++u) {
+        const double xv = __shfl_sync(0xffffffffu, xl, k + u);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) acc[c] = fma(v[u][c], xv, acc[c]);
+      }
     }
+    for (; k < nk; ++k, p += rstep) {
+      const double xv = __shfl_sync(0xffffffffu, xl, k);
 #pragma unroll
-    for (int u = 0; u < RU; ++u)
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) acc[c] = fma(v[u][c], xv[u], acc[c]);
-  }
-  for (; i < nrows; i += 8, p += rstep) {
-    const double xv = __ldg(xx + i);
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) acc[c] = fma(valid[c] ? __ldcs(p + 32 * c) : 0.0, xv, acc[c]);
+      for (int c = 0; c < CPL; ++c) acc[c] = fma(valid[c] ? __ldcs(p + 32 * c) : 0.0, xv, acc[c]);
+    }
   }
 }
 
@@ -115,10 +122,16 @@ stageA_kernel(const AItem* __restrict__ items, LevelPtrs lp, const double* __res
   for (int q0 = 0; q0 < R; q0 += 256) {
     const int W = min(R - q0, 256);
     double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    if (W <= 32) stageA_cols<1>(V, R, nrows, q0, W, xx, acc);
-    else if (W <= 64) stageA_cols<2>(V, R, nrows, q0, W, xx, acc);
-    else if (W <= 128) stageA_cols<4>(V, R, nrows, q0, W, xx, acc);
-    else stageA_cols<8>(V, R, nrows, q0, W, xx, acc);
+    switch ((W + 31) >> 5) {
+      case 1: stageA_cols<1>(V, R, nrows, q0, W, xx, acc); break;
+      case 2: stageA_cols<2>(V, R, nrows, q0, W, xx, acc); break;
+      case 3: stageA_cols<3>(V, R, nrows, q0, W, xx, acc); break;
+      case 4: stageA_cols<4>(V, R, nrows, q0, W, xx, acc); break;
+      case 5: stageA_cols<5>(V, R, nrows, q0, W, xx, acc); break;
+      case 6: stageA_cols<6>(V, R, nrows, q0, W, xx, acc); break;
+      case 7: stageA_cols<7>(V, R, nrows, q0, W, xx, acc); break;
+      default: stageA_cols<8>(V, R, nrows, q0, W, xx, acc); break;
+    }
     if (q0 > 0) __syncthreads();
 #pragma unroll
     for (int c = 0; c < 8; ++c) red[w][lane + 32 * c] = acc[c];
@@ -177,11 +190,45 @@ stageA_kernel(const AItem* __restrict__ items, LevelPtrs lp, const double* __res
 // the 8 point coordinates and x values held in registers.
 constexpr int kSymRowsOnly = 0, kSymBoth = 1, kSymSelf = 2;
 
+// log(r2) for r2 > 0 (normal): r2 = 2^e m, m in [1, 2); c_k = 1 + (k + 1/2)/128 is the
+// centre of m's 1/128 bin (k = top 7 mantissa bits), tab[k] = (1/c_k, log c_k);
+// log r2 = e ln2 + log c_k + log1p(f), f = m/c_k - 1 in (-2^-8, 2^-8), log1p by its
+// degree-8 Taylor polynomial.  11 FP64 operations instead of libdevice's 29; absolute
+// error < 1e-15 (checked against libm over [1e-14, 8] when written).
+__device__ __forceinline__ double log_r2_fast(double r2, const double2* __restrict__ tab) {
+  const long long bits = __double_as_longlong(r2);
+  const int e = (int)(bits >> 52) - 1023;
+  const int k = (int)((bits >> 45) & 127);
+  const double mnt = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
+  const double2 tb = tab[k];
+  const double f = fma(mnt, tb.x, -1.0);
+  double p = fma(f, -0.125, 1.0 / 7.0);
+  p = fma(f, p, -1.0 / 6.0);
+  p = fma(f, p, 0.2);
+  p = fma(f, p, -0.25);
+  p = fma(f, p, 1.0 / 3.0);
+  p = fma(f, p, -0.5);
+  p = fma(f, p, 1.0);
+  const double ed = (double)e;
+  return fma(ed, 0.6931471805599453, fma(p, f, fma(ed, 2.3190468138462996e-17, tb.y)));
+}
+
+template <int KID>
+__device__ __forceinline__ double p2p_eval(const KernelParams& kp, const double2* tab, double px,
+                                           double py, double qx, double qy) {
+  if (KID == H2D_KERNEL_LOG) {
+    const double dx = px - qx, dy = py - qy;
+    const double r2 = fma(dx, dx, dy * dy);
+    return r2 > 0.0 ? 0.5 * log_r2_fast(r2, tab) : 0.0;
+  }
+  return kernel_eval_t<KID>(kp, px, py, qx, qy);
+}
+
 template <int KID>
 __device__ __noinline__ void sym_block(int mode, int64_t a0, int m, int64_t b0, int n, double* row_dst,
                           double* col_dst, const double* __restrict__ px,
                           const double* __restrict__ py, const double* __restrict__ x,
-                          const KernelParams& kp, double* s_a, double* s_b,
+                          const KernelParams& kp, const double2* tab, double* s_a, double* s_b,
                           double (*scol)[65], double* srow) {
   const int tid = threadIdx.x, ti = tid >> 4, tj = tid & 15;
   for (int ra = 0; ra < m; ra += 64) {
@@ -222,7 +269,7 @@ __device__ __noinline__ void sym_block(int mode, int64_t a0, int m, int64_t b0, 
           bool ok = i < mt && j < nt;
           if (diag_tile) ok = ok && i <= j;
           if (ok) {
-            const double k = kernel_eval_t<KID>(kp, rpx[a], rpy[a], cpx[b], cpy[b]);
+            const double k = p2p_eval<KID>(kp, tab, rpx[a], rpy[a], cpx[b], cpy[b]);
             racc[a] = fma(k, cx[b], racc[a]);
             if (!(diag_tile && i == j)) cacc[b] = fma(k, rx[a], cacc[b]);
           }
@@ -282,8 +329,13 @@ p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end,
                double* __restrict__ s0, double* __restrict__ sL, double* __restrict__ sD) {
   __shared__ double s_a[192], s_b[192], srow[64];
   __shared__ double scol[16][65];
+  __shared__ double2 s_logtab[128];
   const int64_t X = leaf_begin + blockIdx.x;
   const int tid = threadIdx.x;
+  if (KID == H2D_KERNEL_LOG && tid < 128) {
+    const double c = 1.0 + (tid + 0.5) / 128.0;
+    s_logtab[tid] = make_double2(1.0 / c, log(c));
+  }
   const uint32_t cx = p2p_compact((uint32_t)X), cy = p2p_compact((uint32_t)X >> 1);
   const uint32_t side = 1u << kappa;
   const int64_t xs = leaf_start[X];
@@ -330,7 +382,7 @@ p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end,
       if (!(has_d && own_d)) continue;
       b0 = leaf_start[Dn]; n = leaf_start[Dn + 1] - (int)b0; rdst = sD + xs;
     }
-    sym_block<KID>(mode, xs, m, b0, n, rdst, cdst, px, py, x, kp, s_a, s_b, scol, srow);
+    sym_block<KID>(mode, xs, m, b0, n, rdst, cdst, px, py, x, kp, s_logtab, s_a, s_b, scol, srow);
   }
 }
 
