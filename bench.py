@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: functional check of the multi-rank path (host-staged gather)")
     return ap.parse_args()
 
 
@@ -187,11 +189,15 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    dev = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
     stream = torch.cuda.current_stream()
     pts = W.config_points(cfg)
     d_pts = torch.from_numpy(pts).cuda()
@@ -214,7 +220,7 @@ def run_ours(args, cfg):
     else:
         perm, _ = op.tree()
         rb, re_ = inf["row_begin"], inf["row_end"]
-        cnt = torch.tensor([re_ - rb], device="cuda")
+        cnt = torch.tensor([re_ - rb], device="cuda" if args.dist_backend == "nccl" else "cpu")
         allc = [torch.zeros_like(cnt) for _ in range(world)]
         dist.all_gather(allc, cnt)
         cmax = int(max(int(c.item()) for c in allc))
@@ -228,8 +234,15 @@ def run_ours(args, cfg):
         y = torch.empty(re_ - rb, dtype=torch.float64, device="cuda")
         assert cmax == inf["gather_stride"], (cmax, inf["gather_stride"])
 
+        if args.dist_backend == "gloo":
+            xg_h = torch.empty(world * cmax, dtype=torch.float64)
+
         def step(k):
-            dist.all_gather_into_tensor(xg, xs[k % nx])
+            if args.dist_backend == "gloo":      # functional check only (host-staged)
+                dist.all_gather_into_tensor(xg_h, xs[k % nx].cpu())
+                xg.copy_(xg_h)
+            else:
+                dist.all_gather_into_tensor(xg, xs[k % nx])
             op.matvec_raw(xg.data_ptr(), y.data_ptr(), h2d.ORDER_GATHERED)
 
     for k in range(args.warmup):
@@ -240,7 +253,7 @@ def run_ours(args, cfg):
     op.stage_times(reset=True)
     op.set_timing(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
@@ -255,7 +268,7 @@ def run_ours(args, cfg):
     ms = ev0.elapsed_time(ev1)
     stages, cnt = op.stage_times(reset=True)
     if dist:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda" if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps

@@ -224,70 +224,70 @@ __device__ __forceinline__ double p2p_eval(const KernelParams& kp, const double2
   return kernel_eval_t<KID>(kp, px, py, qx, qy);
 }
 
+// One leaf-pair block on a 16 x 16 thread grid: thread (ti, tj) owns rows ti + 16a
+// (a < A = ceil(m/16)) and columns tj + 16b (b < B = ceil(n/16)) of a super-tile of up to
+// 96 x 96 points (a leaf of the configs fits one super-tile; larger blocks loop).  Row
+// points live in registers one row at a time, column points are read from shared memory,
+// column sums stay in registers (cacc[b]), row sums are reduced over tj by shuffles.
+constexpr int kSymTile = 96, kSymMaxB = kSymTile / 16;
 template <int KID>
 __device__ __noinline__ void sym_block(int mode, int64_t a0, int m, int64_t b0, int n, double* row_dst,
                           double* col_dst, const double* __restrict__ px,
                           const double* __restrict__ py, const double* __restrict__ x,
                           const KernelParams& kp, const double2* tab, double* s_a, double* s_b,
-                          double (*scol)[65], double* srow) {
+                          double (*scol)[kSymTile + 1], double* srow) {
   const int tid = threadIdx.x, ti = tid >> 4, tj = tid & 15;
-  for (int ra = 0; ra < m; ra += 64) {
-    const int mt = min(64, m - ra);
+  for (int ra = 0; ra < m; ra += kSymTile) {
+    const int mt = min(kSymTile, m - ra);
+    const int A = (mt + 15) >> 4;
     const int cstart = mode == kSymSelf ? ra : 0;
-    for (int cb = cstart; cb < n; cb += 64) {
-      const int nt = min(64, n - cb);
+    for (int cb = cstart; cb < n; cb += kSymTile) {
+      const int nt = min(kSymTile, n - cb);
+      const int B = (nt + 15) >> 4;
       __syncthreads();
-      if (tid < mt) {
-        s_a[tid] = px[a0 + ra + tid];
-        s_a[64 + tid] = py[a0 + ra + tid];
-        s_a[128 + tid] = x[a0 + ra + tid];
-      } else if (tid >= 64 && tid < 64 + nt) {
-        const int j = tid - 64;
-        s_b[j] = px[b0 + cb + j];
-        s_b[64 + j] = py[b0 + cb + j];
-        s_b[128 + j] = x[b0 + cb + j];
+      for (int e = tid; e < mt; e += 256) {
+        s_a[e] = px[a0 + ra + e];
+        s_a[kSymTile + e] = py[a0 + ra + e];
+        s_a[2 * kSymTile + e] = x[a0 + ra + e];
+      }
+      for (int e = tid; e < nt; e += 256) {
+        s_b[e] = px[b0 + cb + e];
+        s_b[kSymTile + e] = py[b0 + cb + e];
+        s_b[2 * kSymTile + e] = x[b0 + cb + e];
       }
       __syncthreads();
       const bool diag_tile = mode == kSymSelf && cb == ra;
-      double rpx[4], rpy[4], rx[4], cpx[4], cpy[4], cx[4];
+      double cacc[kSymMaxB];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int i = ti + 16 * a;
-        rpx[a] = s_a[i]; rpy[a] = s_a[64 + i]; rx[a] = i < mt ? s_a[128 + i] : 0.0;
-      }
+      for (int bb = 0; bb < kSymMaxB; ++bb) cacc[bb] = 0.0;
+      for (int aa = 0; aa < A; ++aa) {
+        const int i = ti + 16 * aa;
+        const bool vi = i < mt;
+        const double rpx = s_a[i], rpy = s_a[kSymTile + i], rx = vi ? s_a[2 * kSymTile + i] : 0.0;
+        double racc = 0.0;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int j = tj + 16 * b;
-        cpx[b] = s_b[j]; cpy[b] = s_b[64 + j]; cx[b] = j < nt ? s_b[128 + j] : 0.0;
-      }
-      double racc[4] = {0.0, 0.0, 0.0, 0.0}, cacc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int i = ti + 16 * a, j = tj + 16 * b;
-          bool ok = i < mt && j < nt;
-          if (diag_tile) ok = ok && i <= j;
-          if (ok) {
-            const double k = p2p_eval<KID>(kp, tab, rpx[a], rpy[a], cpx[b], cpy[b]);
-            racc[a] = fma(k, cx[b], racc[a]);
-            if (!(diag_tile && i == j)) cacc[b] = fma(k, rx[a], cacc[b]);
+        for (int bb = 0; bb < kSymMaxB; ++bb) {
+          const int j = tj + 16 * bb;
+          if (bb < B) {
+            bool ok = vi && j < nt;
+            if (diag_tile) ok = ok && i <= j;
+            if (ok) {
+              const double k = p2p_eval<KID>(kp, tab, rpx, rpy, s_b[j], s_b[kSymTile + j]);
+              racc = fma(k, s_b[2 * kSymTile + j], racc);
+              if (!(diag_tile && i == j)) cacc[bb] = fma(k, rx, cacc[bb]);
+            }
           }
         }
-      }
-      // rows: reduce over tj (16 lanes of a half-warp)
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        double v = racc[a];
-        v += __shfl_xor_sync(0xffffffffu, v, 8);
-        v += __shfl_xor_sync(0xffffffffu, v, 4);
-        v += __shfl_xor_sync(0xffffffffu, v, 2);
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
-        if (tj == 0) srow[ti + 16 * a] = v;
+        racc += __shfl_xor_sync(0xffffffffu, racc, 8);
+        racc += __shfl_xor_sync(0xffffffffu, racc, 4);
+        racc += __shfl_xor_sync(0xffffffffu, racc, 2);
+        racc += __shfl_xor_sync(0xffffffffu, racc, 1);
+        if (tj == 0 && vi) srow[i] = racc;
       }
       if (mode != kSymRowsOnly) {
 #pragma unroll
-        for (int b = 0; b < 4; ++b) scol[ti][tj + 16 * b] = cacc[b];
+        for (int bb = 0; bb < kSymMaxB; ++bb)
+          if (bb < B) scol[ti][tj + 16 * bb] = cacc[bb];
       }
       __syncthreads();
       if (tid < mt) row_dst[ra + tid] += srow[tid];
@@ -322,13 +322,13 @@ __device__ __forceinline__ uint32_t p2p_compact(uint32_t v) {
 }
 
 template <int KID>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, 3)
 p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end,
                const int32_t* __restrict__ leaf_start, const double* __restrict__ px,
                const double* __restrict__ py, const double* __restrict__ x, KernelParams kp,
                double* __restrict__ s0, double* __restrict__ sL, double* __restrict__ sD) {
-  __shared__ double s_a[192], s_b[192], srow[64];
-  __shared__ double scol[16][65];
+  __shared__ double s_a[3 * kSymTile], s_b[3 * kSymTile], srow[kSymTile];
+  __shared__ double scol[16][kSymTile + 1];
   __shared__ double2 s_logtab[128];
   const int64_t X = leaf_begin + blockIdx.x;
   const int tid = threadIdx.x;

@@ -1,0 +1,74 @@
+#!/usr/bin/env python
+"""Summarise an ncu report (or a launch-list CSV) into the markdown kept under profiles/.
+
+    python tools/ncu_summary.py gpurun_out/prof.ncu-rep  > profiles/rNN_ncu_full.md
+    python tools/ncu_summary.py --launches gpurun_out/launches.csv > profiles/rNN_launches.md
+"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+METRICS = [
+    ("gpu__time_duration.sum", "time (ms)"),
+    ("dram__bytes_read.sum", "DRAM read (GB)"),
+    ("dram__bytes_write.sum", "DRAM write (MB)"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % peak"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe % active"),
+    ("smsp__inst_executed_pipe_fp64.sum", "FP64 warp-instr"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue % active"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("launch__registers_per_thread", "regs"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit %"),
+]
+
+
+def full(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    print(f"# ncu --set full summary: `{path}`\n")
+    print("| kernel | grid | " + " | ".join(n for _, n in METRICS) + " | top stalls |")
+    print("|---" * (len(METRICS) + 3) + "|")
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")]
+        name = name.split("::")[-1].split("(")[0] if "::" in name else name.split("(")[0]
+        vals = []
+        for m, _ in METRICS:
+            v = r[hdr.index(m)] if m in hdr else ""
+            vals.append(v)
+        st = []
+        for h, v in zip(hdr, r):
+            if "average_warps_issue_stalled" in h and h.endswith("per_issue_active.ratio"):
+                try:
+                    st.append((float(v), h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", "")))
+                except ValueError:
+                    pass
+        st.sort(reverse=True)
+        stalls = ", ".join(f"{n} {v:.1f}" for v, n in st[:3])
+        print(f"| {name} | {r[hdr.index('Grid Size')]} | " + " | ".join(vals) + f" | {stalls} |")
+    print("\nUnits as reported by ncu: " + ", ".join(f"{m}={units[hdr.index(m)]}" for m, _ in METRICS if m in hdr))
+
+
+def launches(path):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    hdr = rows[0]
+    k, v = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    agg = defaultdict(list)
+    for r in rows[1:]:
+        name = r[k].split("::")[-1].split("(")[0]
+        agg[name].append(float(r[v]))
+    tot = sum(sum(x) for x in agg.values())
+    print(f"# ncu launch list (gpu__time_duration.sum, --clock-control none): `{path}`\n")
+    print("| kernel | launches | mean (us) | share of listed time |")
+    print("|---|---|---|---|")
+    for name, xs in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        print(f"| {name} | {len(xs)} | {sum(xs) / len(xs) / 1e3:.1f} | {100 * sum(xs) / tot:.1f} % |")
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "--launches":
+        launches(sys.argv[2])
+    else:
+        full(sys.argv[1])
