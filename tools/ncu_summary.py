@@ -32,8 +32,7 @@ def full(path):
     print("| kernel | grid | " + " | ".join(n for _, n in METRICS) + " | top stalls |")
     print("|---" * (len(METRICS) + 3) + "|")
     for r in rows[2:]:
-        name = r[hdr.index("Kernel Name")]
-        name = name.split("::")[-1].split("(")[0] if "::" in name else name.split("(")[0]
+        name = short(r[hdr.index("Kernel Name")])
         vals = []
         for m, _ in METRICS:
             v = r[hdr.index(m)] if m in hdr else ""
@@ -51,20 +50,59 @@ def full(path):
     print("\nUnits as reported by ncu: " + ", ".join(f"{m}={units[hdr.index(m)]}" for m, _ in METRICS if m in hdr))
 
 
+def short(n):
+    """Kernel name without return type, namespaces or argument list (template args kept)."""
+    depth, cut = 0, len(n)
+    for i, ch in enumerate(n):
+        if ch == "<":
+            depth += 1
+        elif ch == ">":
+            depth -= 1
+        elif ch == "(" and depth == 0:
+            cut = i
+            break
+    head = n[:cut].strip()
+    parts, depth, cur = [], 0, ""
+    for i, ch in enumerate(head):
+        if ch == "<":
+            depth += 1
+        elif ch == ">":
+            depth -= 1
+        if depth == 0 and head.startswith("::", i):
+            parts.append(cur)
+            cur = ""
+            continue
+        if depth == 0 and ch == ":" and i > 0 and head[i - 1] == ":":
+            continue
+        cur += ch
+    parts.append(cur)
+    return parts[-1].split(" ")[-1] if "<" not in parts[-1] else parts[-1].strip()
+
+
+MATVEC = ("stageA", "stageB", "p2p", "permute_in", "unpad", "reduce_kernel")
+
+
 def launches(path):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     hdr = rows[0]
     k, v = hdr.index("Kernel Name"), hdr.index("Metric Value")
     agg = defaultdict(list)
     for r in rows[1:]:
-        name = r[k].split("::")[-1].split("(")[0]
-        agg[name].append(float(r[v]))
+        agg[short(r[k])].append(float(r[v]))
     tot = sum(sum(x) for x in agg.values())
     print(f"# ncu launch list (gpu__time_duration.sum, --clock-control none): `{path}`\n")
     print("| kernel | launches | mean (us) | share of listed time |")
     print("|---|---|---|---|")
     for name, xs in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         print(f"| {name} | {len(xs)} | {sum(xs) / len(xs) / 1e3:.1f} | {100 * sum(xs) / tot:.1f} % |")
+    mv = {n: xs for n, xs in agg.items() if n.startswith(MATVEC)}
+    mtot = sum(sum(x) for x in mv.values())
+    if mtot:
+        print("\nMatvec kernels only (one matvec = one launch of each; serialised, cold-cache):\n")
+        print("| kernel | launches | mean (us) | share of the matvec |")
+        print("|---|---|---|---|")
+        for name, xs in sorted(mv.items(), key=lambda kv: -sum(kv[1])):
+            print(f"| {name} | {len(xs)} | {sum(xs) / len(xs) / 1e3:.1f} | {100 * sum(xs) / mtot:.1f} % |")
 
 
 if __name__ == "__main__":
