@@ -92,10 +92,11 @@ typedef struct {
 } hodlr2d_options;
 
 #define H2D_MAX_LEVELS 16
-#define H2D_NUM_STAGES 6 /* 0 input permute / unpad, 1 stage A (t = V^T x), 2 t-partial
-                            reduce, 3 wait for the near-field P2P, 4 stage B (y = ynear +
-                            U t), 5 near-field P2P (ynear = shift x + scale K_near x; runs on
-                            a second stream concurrently with stages 1-2)               */
+#define H2D_NUM_STAGES 6 /* 0 input permute / unpad, 1 stage A (t = V^T x, incl. the
+                            multi-chunk t reduction), 2 stage B (yfar = U t), 3 wait for
+                            the near-field P2P after stage B, 4 combine (y = yfar + scale
+                            K_near x + shift x, output permutation), 5 near-field P2P (runs
+                            on a low-priority stream concurrently with stages 1-2)     */
 
 typedef struct {
   int64_t n;                 /* N                                                     */

@@ -32,7 +32,7 @@ ORDER_ORIGINAL, ORDER_TREE, ORDER_GATHERED = 0, 1, 2
 ORDERS = {"original": 0, "tree": 1, "gathered": 2}
 MAX_LEVELS = 16
 NUM_STAGES = 6
-STAGE_NAMES = ("input_permute", "stageA_VTx", "t_reduce", "p2p_join_wait", "stageB_Ut", "p2p_near")
+STAGE_NAMES = ("input_permute", "stageA_VTx", "stageB_Ut", "p2p_join_wait", "combine", "p2p_near")
 
 # Every function declared in include/hodlr2d.h (checked by tests/test_abi.py).
 ABI_FUNCTIONS = (

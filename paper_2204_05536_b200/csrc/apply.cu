@@ -1,43 +1,90 @@
 // Factor packing (G7) and the matvec hot path (S7-S10).
 //
 // HBM layout:
-//   U panel of row box X at level l : column-major m_X x R_X, the concatenation
-//                                     [U_b1 | U_b2 | ...] of the blocks (X, Y), Y in I_X
-//                                     ascending.  A leaf L inside X owns the contiguous
-//                                     row segment [a, a + |L|) of every column.
-//   V panel of column box Y         : row-major n_Y x RV_Y, the columns of the blocks
-//                                     (X, Y), X in I_Y ascending.  Row i of the panel is the
-//                                     RV_Y values that multiply x_i.
-//   t                               : one value per (block, rank index) in U-panel column
-//                                     order, so a row box's t is contiguous; stage A writes
-//                                     it through vdst (V-panel column -> t position).
+//   U leaf panel (level l, served leaf L, level-l ancestor X): column-major mLp x R_X, the
+//                                     rows of L of [U_b1 | U_b2 | ...] over the blocks (X, Y),
+//                                     Y in I_X ascending; mLp = |L| rounded up to even.  One
+//                                     contiguous 16-byte aligned range per (leaf, level).
+//   V panel of column box Y         : row-major n_Y x RVp_Y, the columns of the blocks
+//                                     (X, Y), X in I_Y ascending (RVp_Y = RV_Y rounded up to
+//                                     even).  Row i holds the RV_Y values that multiply x_i.
+//   t                               : one value per (block, rank index) in U-column order
+//                                     (a row box's t is contiguous); stage A writes it through
+//                                     vdst (V-panel column -> t position).
 // Matvec (Alg. 2; stage order is free, R18):
-//   p2p      ynear = shift x + scale K_near x  (second stream, overlaps stage A)
-//   stage A  t = V^T x          one CTA per (column box, row chunk)
-//   reduce   t = sum of chunk partials (boxes split over several CTAs only)
-//   stage B  per leaf L: y_L = ynear_L + sum_l U_{X_l}[rows of L, :] t_{X_l}
-//                               one CTA per leaf, one y write per row, no atomics.
+//   stage A  t = V^T x          persistent, bulk-TMA pipelined, one work item per
+//                               (column box, row chunk), multi-chunk boxes reduced by the
+//                               last chunk to finish                  (high-priority stream)
+//   stage B  yfar_L = sum_l U_{X_l}[rows of L, :] t_{X_l}
+//                               persistent, bulk-TMA pipelined, one item per leaf (row block)
+//   p2p      ynear = K_near x   three deterministic slots             (low-priority stream,
+//                               co-resident with A and B: they leave it registers and smem)
+//   combine  y = yfar + scale * ynear + shift * x, permuted to the caller's order.
 #include <algorithm>
+#include <numeric>
 
 #include "h2d_internal.cuh"
+#include "tma.cuh"
 
 namespace h2d {
 namespace {
 
-constexpr int kAThreads = 256;
-constexpr int kBThreads = 256;
-constexpr int64_t kATarget = 65536;  // stage-A elements per CTA
-constexpr int kAMaxRows = 16384;     // rows per stage-A chunk
-constexpr int kBUnroll = 8;
+constexpr int64_t kATarget = 32768;  // stage-A elements per work item (256 KB)
+constexpr int kAMaxRows = 16384;     // rows per stage-A item
+constexpr int kBRows = 256;          // rows per stage-B item (leaf row block)
 
-struct CopyItem {
-  const double* src;
-  double* dst;
-  int64_t count;
+// ---------------------------------------------------------------- pipeline layout
+// One producer warp (bulk TMA of the factor stream + 8-byte cp.async of the x / t values
+// a stage needs) and 8 consumer warps per CTA, kNS-deep ring of 16 KB stages.  With
+// 2 CTAs per SM (grid = 2 x SMs, ~95 KB smem, <= 72 registers) a third CTA of the P2P
+// kernel still fits on every SM, so the FP64-bound near field runs under the HBM stream.
+constexpr int kNS = 5;
+constexpr int kStageDbl = 2048;      // factor doubles per stage (16 KB)
+constexpr int kStageVec = 256;       // x (stage A) / t (stage B) values per stage
+constexpr int kCons = 256;           // consumer threads
+constexpr int kPipeThreads = kCons + 32;
+constexpr int kFirst = 1, kLast = 2;
+
+struct StageHdr {
+  int32_t item;    // work item index; < 0: no more work (terminator)
+  int32_t cnt;     // rows (stage A) / columns (stage B) held by this stage
+  int32_t flags;   // kFirst / kLast stage of the item
+  int32_t a, b, c, d, pad;   // item fields for the consumers (see the producers)
 };
-__global__ void copy_items_kernel(const CopyItem* __restrict__ items) {
-  const CopyItem it = items[blockIdx.x];
-  for (int64_t i = threadIdx.x; i < it.count; i += blockDim.x) it.dst[i] = it.src[i];
+
+struct PipeSmem {
+  double ring[kNS][kStageDbl];
+  double vec[kNS][kStageVec];
+  double red[kCons];
+  StageHdr hdr[kNS];
+  uint64_t full[kNS];    // 1 producer arrival (+ tx bytes) + 32 cp.async arrivals
+  uint64_t empty[kNS];   // 8 consumer-warp arrivals
+  int flag;
+};
+
+__device__ __forceinline__ void pipe_init(PipeSmem& S) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kNS; ++s) {
+      mbar_init(&S.full[s], 1 + 32);
+      mbar_init(&S.empty[s], kCons / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+}
+
+struct UCopyItem {
+  const double* src;   // column-major, leading dimension ld_src
+  double* dst;         // column-major, leading dimension ld_dst
+  int32_t ld_src, ld_dst, rows, cols;
+};
+__global__ void ucopy_kernel(const UCopyItem* __restrict__ items) {
+  const UCopyItem it = items[blockIdx.x];
+  const int64_t tot = (int64_t)it.rows * it.cols;
+  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int64_t c = e / it.rows, i = e - c * it.rows;
+    it.dst[c * it.ld_dst + i] = it.src[c * it.ld_src + i];
+  }
 }
 
 struct VPackItem {
@@ -65,112 +112,185 @@ T* upload_tmp(const std::vector<T>& v, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- stage A: t = V^T x
-// The chunk is a contiguous row-major block nrows x R of the V panel.  Lane l owns the
-// panel columns q0 + l + 32c (c < CPL) and warp w the rows w, w+8, ...: each row is one
-// coalesced 32*CPL-double read at constant offsets, x_i is a warp-uniform broadcast load,
-// 8 loads in flight per thread, partial sums reduced over the 8 warps in shared memory.
-template <int CPL>
-__device__ __forceinline__ void stageA_cols(const double* __restrict__ V, int R, int nrows, int q0,
-                                            int W, const double* __restrict__ xx,
-                                            double (&acc)[8]) {
-  constexpr int RU = CPL >= 5 ? 1 : CPL >= 3 ? 2 : CPL == 2 ? 4 : 8;   // rows per step
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  bool valid[CPL];
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) valid[c] = lane + 32 * c < W;
-  const int64_t rstep = (int64_t)8 * R;
-  // rows of this warp: w + 8k.  x for 32 of them is fetched by one coalesced load and
-  // broadcast by shuffles.
-  for (int k0 = 0; w + 8 * k0 < nrows; k0 += 32) {
-    const int ib = w + 8 * k0;
-    const int nk = min(32, (nrows - ib + 7) >> 3);
-    const double xl = lane < nk ? __ldg(xx + ib + 8 * lane) : 0.0;
-    const double* __restrict__ p = V + (int64_t)ib * R + q0 + lane;
-    int k = 0;
-    for (; k + RU <= nk; k += RU, p += RU * rstep) {
-      double v[RU][CPL];
-#pragma unroll
-      for (int u = 0; u < RU; ++u)
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) v[u][c] = valid[c] ? __ldcs(p + u * rstep + 32 * c) : 0.0;
-#pragma unroll
-      for (int u = 0; u < RU; ++u) {
-        const double xv = __shfl_sync(0xffffffffu, xl, k + u);
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) acc[c] = fma(v[u][c], xv, acc[c]);
+// Item = rows [0, nrows) of a row-major V panel chunk (stride Rp).  A stage holds
+// rows_s = min(256, 2048 / Rp) whole rows (one bulk copy) and their x values.  Consumers:
+// R <= 256 -> thread (g, q) = (tid / R, tid % R) owns panel column q and rows g, g + G, ...
+// (G = 256 / R groups, reduced in smem at the end of the item); R > 256 -> thread owns
+// columns tid + 256 c (c < CPL) over all rows.  Stage header: a = R, b = Rp, c = out,
+// d = ritem.
+__device__ void stageA_producer(PipeSmem& S, const AItem* __restrict__ items, int n_items,
+                                int32_t* counter, const LevelPtrs& lp, const double* __restrict__ x) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = l2_evict_first_policy();
+  int stage = 0;
+  uint32_t phase = 0;
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(counter, 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    const bool done = idx >= n_items;
+    AItem it{};
+    if (!done) it = items[idx];
+    const int rows_s = done ? 1 : min(kStageVec, kStageDbl / it.Rp);
+    const double* V = done ? nullptr : lp.V[it.level] + it.v_off;
+    int r0 = 0;
+    do {
+      const int rows = done ? 0 : min(rows_s, it.nrows - r0);
+      mbar_wait(&S.empty[stage], phase ^ 1);
+      if (lane == 0) {
+        StageHdr& h = S.hdr[stage];
+        h.item = done ? -1 : idx;
+        h.cnt = rows;
+        h.flags = (r0 == 0 ? kFirst : 0) | (r0 + rows >= it.nrows ? kLast : 0);
+        h.a = it.R;
+        h.b = it.Rp;
+        h.c = it.out;
+        h.d = it.ritem;
+        const uint32_t bytes = (uint32_t)rows * (uint32_t)it.Rp * 8u;
+        mbar_arrive_expect_tx(&S.full[stage], bytes);
+        if (bytes) bulk_g2s(S.ring[stage], V + (int64_t)r0 * it.Rp, bytes, &S.full[stage], pol);
       }
+      for (int j = lane; j < rows; j += 32) cp_async8(&S.vec[stage][j], x + it.x_off + r0 + j);
+      cp_async_arrive_noinc(&S.full[stage]);
+      if (++stage == kNS) { stage = 0; phase ^= 1; }
+      r0 += rows;
+    } while (!done && r0 < it.nrows);
+    if (done) break;
+  }
+}
+
+template <int CPL>
+__device__ __forceinline__ void stageA_consume(const double* __restrict__ sv, const double* __restrict__ sx,
+                                               int rows, int Rp, int R, int q, int g, int G,
+                                               double (&acc)[8]) {
+  if (CPL == 1) {
+    if (g >= G) return;
+    const double* p = sv + q;
+    int j = g;
+    for (; j + 3 * G < rows; j += 4 * G) {
+      const double v0 = p[j * Rp], v1 = p[(j + G) * Rp], v2 = p[(j + 2 * G) * Rp], v3 = p[(j + 3 * G) * Rp];
+      acc[0] = fma(v0, sx[j], acc[0]);
+      acc[1] = fma(v1, sx[j + G], acc[1]);
+      acc[2] = fma(v2, sx[j + 2 * G], acc[2]);
+      acc[3] = fma(v3, sx[j + 3 * G], acc[3]);
     }
-    for (; k < nk; ++k, p += rstep) {
-      const double xv = __shfl_sync(0xffffffffu, xl, k);
+    for (; j < rows; j += G) acc[0] = fma(p[j * Rp], sx[j], acc[0]);
+  } else {
+    bool valid[CPL];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) acc[c] = fma(valid[c] ? __ldcs(p + 32 * c) : 0.0, xv, acc[c]);
+    for (int c = 0; c < CPL; ++c) valid[c] = q + 256 * c < R;
+    const double* p = sv + q;
+    for (int j = 0; j < rows; ++j, p += Rp) {
+      const double xv = sx[j];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c)
+        if (valid[c]) acc[c] = fma(p[256 * c], xv, acc[c]);
     }
   }
 }
 
-__global__ void __launch_bounds__(kAThreads, 4)
-stageA_kernel(const AItem* __restrict__ items, LevelPtrs lp, const double* __restrict__ x,
-              const int32_t* __restrict__ vdst, double* __restrict__ t,
-              double* __restrict__ tpart, const RItem* __restrict__ ritems,
-              int32_t* __restrict__ rcount) {
-  __shared__ double red[8][256];
-  __shared__ int s_last;
-  const AItem it = items[blockIdx.x];
-  const double* __restrict__ V = lp.V[it.level] + it.v_off;
-  const double* __restrict__ xx = x + it.x_off;
-  const int R = it.R, nrows = it.nrows, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int q0 = 0; q0 < R; q0 += 256) {
-    const int W = min(R - q0, 256);
-    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    switch ((W + 31) >> 5) {
-      case 1: stageA_cols<1>(V, R, nrows, q0, W, xx, acc); break;
-      case 2: stageA_cols<2>(V, R, nrows, q0, W, xx, acc); break;
-      case 3: stageA_cols<3>(V, R, nrows, q0, W, xx, acc); break;
-      case 4: stageA_cols<4>(V, R, nrows, q0, W, xx, acc); break;
-      case 5: stageA_cols<5>(V, R, nrows, q0, W, xx, acc); break;
-      case 6: stageA_cols<6>(V, R, nrows, q0, W, xx, acc); break;
-      case 7: stageA_cols<7>(V, R, nrows, q0, W, xx, acc); break;
-      default: stageA_cols<8>(V, R, nrows, q0, W, xx, acc); break;
-    }
-    if (q0 > 0) __syncthreads();
+__device__ void stageA_consumers(PipeSmem& S, const int32_t* __restrict__ vdst, double* __restrict__ t,
+                                 double* __restrict__ tpart, const RItem* __restrict__ ritems,
+                                 int32_t* __restrict__ rcount) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  int stage = 0;
+  uint32_t phase = 0;
+  int R = 1, Rp = 2, CPL = 1, G = 1, g = 0, q = 0;
+  double acc[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) red[w][lane + 32 * c] = acc[c];
-    __syncthreads();
-    if (tid < W) {
-      double s = 0.0;
+  for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+  for (;;) {
+    mbar_wait(&S.full[stage], phase);
+    const StageHdr h = S.hdr[stage];
+    if (h.item < 0) break;
+    if (h.flags & kFirst) {
+      R = h.a;
+      Rp = h.b;
+      CPL = (R + 255) >> 8;
+      if (CPL == 1) { G = kCons / R; g = tid / R; q = tid - g * R; }
+      else { G = 1; g = 0; q = tid; }
 #pragma unroll
-      for (int ww = 0; ww < 8; ++ww) s += red[ww][tid];
-      if (it.out >= 0) t[vdst[it.out + q0 + tid]] = s;
-      else tpart[(-(int64_t)it.out - 1) + q0 + tid] = s;
+      for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+    }
+    const double* sv = S.ring[stage];
+    const double* sx = S.vec[stage];
+    switch (CPL) {
+      case 1: stageA_consume<1>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
+      case 2: stageA_consume<2>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
+      case 3: stageA_consume<3>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
+      case 4: stageA_consume<4>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
+      case 5: stageA_consume<5>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
+      case 6: stageA_consume<6>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
+      case 7: stageA_consume<7>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
+      default: stageA_consume<8>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[stage]);
+    if (++stage == kNS) { stage = 0; phase ^= 1; }
+    if (!(h.flags & kLast)) continue;
+    // ---- end of item: column sums -> t (or this chunk's partials)
+    auto put = [&](int qq, double v) {
+      if (h.c >= 0) t[vdst[h.c + qq]] = v;
+      else tpart[(int64_t)(-h.c - 1) + qq] = v;
+    };
+    if (CPL == 1) {
+      const double s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      if (G > 1) {
+        S.red[tid] = g < G ? s : 0.0;
+        named_bar_sync(1, kCons);
+        if (tid < R) {
+          double u = 0.0;
+          for (int gg = 0; gg < G; ++gg) u += S.red[tid + gg * R];
+          put(tid, u);
+        }
+        named_bar_sync(1, kCons);
+      } else if (tid < R) {
+        put(tid, s);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < CPL && tid + 256 * c < R) put(tid + 256 * c, acc[c]);
+    }
+    if (h.d >= 0) {
+      // Multi-chunk box: the last chunk to finish sums the partials in chunk order
+      // (deterministic) and resets the counter for the next matvec.
+      __threadfence();
+      named_bar_sync(1, kCons);
+      if (tid == 0) S.flag = atomicAdd(rcount + h.d, 1) == ritems[h.d].nchunks - 1;
+      named_bar_sync(1, kCons);
+      if (S.flag) {
+        __threadfence();
+        const RItem ri = ritems[h.d];
+        for (int qq = tid; qq < ri.R; qq += kCons) {
+          const double* __restrict__ pp = tpart + ri.p_off + qq;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int c = 0;
+          for (; c + 3 < ri.nchunks; c += 4) {
+            a0 += __ldcg(pp + (int64_t)c * ri.R);
+            a1 += __ldcg(pp + (int64_t)(c + 1) * ri.R);
+            a2 += __ldcg(pp + (int64_t)(c + 2) * ri.R);
+            a3 += __ldcg(pp + (int64_t)(c + 3) * ri.R);
+          }
+          for (; c < ri.nchunks; ++c) a0 += __ldcg(pp + (int64_t)c * ri.R);
+          t[vdst[ri.vpos + qq]] = (a0 + a1) + (a2 + a3);
+        }
+        if (tid == 0) rcount[h.d] = 0;
+      }
     }
   }
-  if (it.ritem < 0) return;
-  // Multi-chunk box: the last chunk CTA to finish sums the partials in chunk order
-  // (deterministic) and resets the counter for the next matvec.
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    const RItem ri = ritems[it.ritem];
-    s_last = atomicAdd(rcount + it.ritem, 1) == ri.nchunks - 1;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const RItem ri = ritems[it.ritem];
-  for (int q = tid; q < ri.R; q += kAThreads) {
-    const double* __restrict__ pp = tpart + ri.p_off + q;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int c = 0;
-    for (; c + 3 < ri.nchunks; c += 4) {
-      a0 += __ldcg(pp + (int64_t)c * ri.R);
-      a1 += __ldcg(pp + (int64_t)(c + 1) * ri.R);
-      a2 += __ldcg(pp + (int64_t)(c + 2) * ri.R);
-      a3 += __ldcg(pp + (int64_t)(c + 3) * ri.R);
-    }
-    for (; c < ri.nchunks; ++c) a0 += __ldcg(pp + (int64_t)c * ri.R);
-    t[vdst[ri.vpos + q]] = (a0 + a1) + (a2 + a3);
-  }
-  if (tid == 0) rcount[it.ritem] = 0;
+}
+
+__global__ void __launch_bounds__(kPipeThreads, 3)
+stageA_tma_kernel(const AItem* __restrict__ items, int n_items, int32_t* counter, LevelPtrs lp,
+                  const double* __restrict__ x, const int32_t* __restrict__ vdst, double* __restrict__ t,
+                  double* __restrict__ tpart, const RItem* __restrict__ ritems,
+                  int32_t* __restrict__ rcount) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  PipeSmem& S = *reinterpret_cast<PipeSmem*>(smem_raw);
+  pipe_init(S);
+  if (threadIdx.x >= kCons) stageA_producer(S, items, n_items, counter, lp, x);
+  else stageA_consumers(S, vdst, t, tpart, ritems, rcount);
 }
 
 // ---------------------------------------------------------------- near-field P2P (symmetric)
@@ -386,100 +506,177 @@ p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end,
   }
 }
 
-// ---------------------------------------------------------------- stage B: y = ynear + U t
-// One CTA (8 warps) per leaf L.  Lane i owns rows i, i+32, ... (RPL rows) of the leaf;
-// warp w owns columns q = w, w+8, ... of every ancestor U panel.  For a column, the
-// warp's loads are 256 B contiguous row segments at constant offsets (no per-load
-// address math); t for 32 of the warp's columns is fetched with one coalesced load and
-// broadcast by shuffles.  8 loads in flight per thread, one barrier (final row sum).
-template <int RPL, int CU>
-__device__ __forceinline__ void stageB_rows(int kappa, int rows_here, int64_t rowoff,
-                                            const int* s_R, const int* s_cb,
-                                            const int64_t* s_base, const int64_t* s_mX,
-                                            const LevelPtrs& lp, double (&acc)[4]) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  bool valid[RPL];
-#pragma unroll
-  for (int r = 0; r < RPL; ++r) valid[r] = lane + 32 * r < rows_here;
-  for (int l = 1; l <= kappa; ++l) {
-    const int R = s_R[l];
-    const int64_t mX = s_mX[l];
-    const double* __restrict__ base = lp.U[l] + s_base[l] + rowoff + lane;
-    const double* __restrict__ tl = lp.tu[l] + s_cb[l];
-    const int64_t stepc = 8 * mX;                    // this warp's next column
-    for (int q0 = w; q0 < R; q0 += 8 * 32) {
-      const int qq = q0 + 8 * lane;
-      const double tq = qq < R ? __ldg(tl + qq) : 0.0;
-      const int ncol = min(32, (R - q0 + 7) >> 3);
-      const double* __restrict__ p = base + (int64_t)q0 * mX;
-      int k = 0;
-      for (; k + CU <= ncol; k += CU, p += CU * stepc) {
-        double u[CU][RPL];
-#pragma unroll
-        for (int c = 0; c < CU; ++c)
-#pragma unroll
-          for (int r = 0; r < RPL; ++r) u[c][r] = valid[r] ? __ldcs(p + c * stepc + 32 * r) : 0.0;
-#pragma unroll
-        for (int c = 0; c < CU; ++c) {
-          const double tv = __shfl_sync(0xffffffffu, tq, k + c);
-#pragma unroll
-          for (int r = 0; r < RPL; ++r) acc[r] = fma(u[c][r], tv, acc[r]);
-        }
+// ---------------------------------------------------------------- stage B: yfar = U t
+// Item = rows [r0, r0 + rows) (rows <= 256) of served leaf L.  For every ancestor level l
+// the leaf's U columns form one contiguous column-major range (stride mLp); a stage holds
+// cols_s = min(256, 2048 / rowsp) columns (one bulk copy for whole leaves, one per column
+// for row blocks of a leaf > 256 rows) plus their t values (cp.async gather).  Thread
+// (g, i) = (tid / rows, tid % rows) owns row i and columns g, g + G, ... (G = 256 / rows),
+// reduced in smem at the end of the item: one yfar write per row, no atomics.
+// Stage header: a = rows, b = rowsp (row stride inside the stage), c = output row.
+__device__ void stageB_producer(PipeSmem& S, const BItem* __restrict__ items, int n_items,
+                                int32_t* counter, int kappa, int64_t leaf_begin, int64_t row_begin,
+                                const int32_t* __restrict__ leaf_start, const LevelPtrs& lp) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = l2_evict_first_policy();
+  int stage = 0;
+  uint32_t phase = 0;
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(counter, 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    const bool done = idx >= n_items;
+    BItem it{};
+    int64_t s0 = 0;
+    int mL = 0;
+    if (!done) {
+      it = items[idx];
+      s0 = leaf_start[it.leaf];
+      mL = leaf_start[it.leaf + 1] - (int)s0;
+    }
+    const int mLp = (mL + 1) & ~1, rowsp = (it.rows + 1) & ~1;
+    const bool whole = !done && it.rows == mL;
+    // per-level metadata, lane l - 1 <-> level l
+    int R = 0, cb = 0;
+    int64_t ub = 0;
+    if (!done && lane < kappa) {
+      const int l = lane + 1;
+      const int64_t X = (int64_t)it.leaf >> (2 * (kappa - l));
+      cb = lp.ucolbase[l][X];
+      R = lp.ucolbase[l][X + 1] - cb;
+      ub = lp.uoff[l][it.leaf - leaf_begin];
+    }
+    const unsigned nz = __ballot_sync(0xffffffffu, R > 0);
+    const int lastl = nz ? 32 - __clz(nz) : 0;
+    const int yrow = (int)(s0 + it.r0 - row_begin);
+    if (done || nz == 0) {
+      // terminator, or an item without low-rank columns (kappa = 0 / zero ranks): one
+      // empty stage so the consumers still write the item's rows
+      mbar_wait(&S.empty[stage], phase ^ 1);
+      if (lane == 0) {
+        StageHdr& h = S.hdr[stage];
+        h.item = done ? -1 : idx;
+        h.cnt = 0;
+        h.flags = kFirst | kLast;
+        h.a = it.rows;
+        h.b = rowsp;
+        h.c = yrow;
+        mbar_arrive_expect_tx(&S.full[stage], 0);
       }
-      for (; k < ncol; ++k, p += stepc) {
-        const double tv = __shfl_sync(0xffffffffu, tq, k);
-#pragma unroll
-        for (int r = 0; r < RPL; ++r) acc[r] = fma(valid[r] ? __ldcs(p + 32 * r) : 0.0, tv, acc[r]);
+      cp_async_arrive_noinc(&S.full[stage]);
+      if (++stage == kNS) { stage = 0; phase ^= 1; }
+      if (done) break;
+      continue;
+    }
+    const int cols_s = min(kStageVec, kStageDbl / rowsp);
+    bool first = true;
+    for (int li = 0; li < lastl; ++li) {
+      const int Rl = __shfl_sync(0xffffffffu, R, li);
+      const int cbl = __shfl_sync(0xffffffffu, cb, li);
+      const int64_t ubl = __shfl_sync(0xffffffffu, ub, li);
+      if (Rl == 0) continue;
+      const double* Ub = lp.U[li + 1] + ubl;
+      const double* tb = lp.tu[li + 1] + cbl;
+      for (int c0 = 0; c0 < Rl; c0 += cols_s) {
+        const int cols = min(cols_s, Rl - c0);
+        const bool last = li == lastl - 1 && c0 + cols >= Rl;
+        mbar_wait(&S.empty[stage], phase ^ 1);
+        if (lane == 0) {
+          StageHdr& h = S.hdr[stage];
+          h.item = idx;
+          h.cnt = cols;
+          h.flags = (first ? kFirst : 0) | (last ? kLast : 0);
+          h.a = it.rows;
+          h.b = rowsp;
+          h.c = yrow;
+          mbar_arrive_expect_tx(&S.full[stage], (uint32_t)cols * (uint32_t)rowsp * 8u);
+          if (whole)
+            bulk_g2s(S.ring[stage], Ub + (int64_t)c0 * mLp, (uint32_t)cols * (uint32_t)mLp * 8u,
+                     &S.full[stage], pol);
+        }
+        if (!whole)
+          for (int c = lane; c < cols; c += 32)
+            bulk_g2s(S.ring[stage] + c * rowsp, Ub + (int64_t)(c0 + c) * mLp + it.r0,
+                     (uint32_t)rowsp * 8u, &S.full[stage], pol);
+        for (int c = lane; c < cols; c += 32) cp_async8(&S.vec[stage][c], tb + c0 + c);
+        cp_async_arrive_noinc(&S.full[stage]);
+        if (++stage == kNS) { stage = 0; phase ^= 1; }
+        first = false;
       }
     }
   }
 }
 
-__global__ void __launch_bounds__(kBThreads, 4)
-stageB_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_start, LevelPtrs lp,
-              const double* __restrict__ ynear, int64_t n, const double* __restrict__ x,
-              double scale, double shift, double* __restrict__ y,
-              const int32_t* __restrict__ perm, int order_out, int64_t y_row0) {
-  __shared__ double red[8][128];
-  __shared__ int s_R[H2D_MAX_LEVELS + 1], s_cb[H2D_MAX_LEVELS + 1];
-  __shared__ int64_t s_base[H2D_MAX_LEVELS + 1], s_mX[H2D_MAX_LEVELS + 1];
-  const int64_t L = leaf_begin + blockIdx.x;
-  const int64_t s0 = leaf_start[L];
-  const int mL = leaf_start[L + 1] - (int)s0;
-  if (mL <= 0) return;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid >= 1 && tid <= kappa) {           // per-level metadata, fetched in parallel once
-    const int l = tid, sh = 2 * (kappa - l);
-    const int64_t X = L >> sh;
-    const int32_t cb = lp.ucolbase[l][X];
-    const int64_t bx0 = leaf_start[X << sh];
-    s_R[l] = lp.ucolbase[l][X + 1] - cb;
-    s_cb[l] = cb;
-    s_mX[l] = leaf_start[(X + 1) << sh] - bx0;
-    s_base[l] = lp.upan_off[l][X] + (s0 - bx0);
-  }
-  __syncthreads();
-  for (int rp = 0; rp < mL; rp += 128) {
-    const int rows = min(mL - rp, 128);
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    if (rows <= 32) stageB_rows<1, 8>(kappa, rows, rp, s_R, s_cb, s_base, s_mX, lp, acc);
-    else if (rows <= 64) stageB_rows<2, 4>(kappa, rows, rp, s_R, s_cb, s_base, s_mX, lp, acc);
-    else if (rows <= 96) stageB_rows<3, 2>(kappa, rows, rp, s_R, s_cb, s_base, s_mX, lp, acc);
-    else stageB_rows<4, 2>(kappa, rows, rp, s_R, s_cb, s_base, s_mX, lp, acc);
-    if (rp > 0) __syncthreads();
-#pragma unroll
-    for (int r = 0; r < 4; ++r) red[w][lane + 32 * r] = acc[r];
-    __syncthreads();
-    if (tid < rows) {
-      double s = 0.0;
-#pragma unroll
-      for (int ww = 0; ww < 8; ++ww) s += red[ww][tid];
-      const int64_t r = s0 + rp + tid;
-      // near field (three symmetric-P2P slots) + shift x
-      s += fma(scale, (ynear[r] + ynear[n + r]) + ynear[2 * n + r], shift * x[r]);
-      if (order_out == H2D_ORDER_ORIGINAL) y[perm[r]] = s;
-      else y[r - y_row0] = s;
+__device__ void stageB_consumers(PipeSmem& S, double* __restrict__ yfar) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  int stage = 0;
+  uint32_t phase = 0;
+  int rows = 1, rowsp = 2, G = 1, g = 0, i = 0;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (;;) {
+    mbar_wait(&S.full[stage], phase);
+    const StageHdr h = S.hdr[stage];
+    if (h.item < 0) break;
+    if (h.flags & kFirst) {
+      rows = h.a;
+      rowsp = h.b;
+      G = kCons / rows;
+      g = tid / rows;
+      i = tid - g * rows;
+      a0 = a1 = a2 = a3 = 0.0;
     }
+    if (g < G) {
+      const double* __restrict__ p = S.ring[stage] + i;
+      const double* __restrict__ tv = S.vec[stage];
+      const int cols = h.cnt;
+      int c = g;
+      for (; c + 3 * G < cols; c += 4 * G) {
+        const double u0 = p[c * rowsp], u1 = p[(c + G) * rowsp], u2 = p[(c + 2 * G) * rowsp],
+                     u3 = p[(c + 3 * G) * rowsp];
+        a0 = fma(u0, tv[c], a0);
+        a1 = fma(u1, tv[c + G], a1);
+        a2 = fma(u2, tv[c + 2 * G], a2);
+        a3 = fma(u3, tv[c + 3 * G], a3);
+      }
+      for (; c < cols; c += G) a0 = fma(p[c * rowsp], tv[c], a0);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[stage]);
+    if (++stage == kNS) { stage = 0; phase ^= 1; }
+    if (!(h.flags & kLast)) continue;
+    S.red[tid] = g < G ? (a0 + a1) + (a2 + a3) : 0.0;
+    named_bar_sync(1, kCons);
+    if (tid < rows) {
+      double u = 0.0;
+      for (int gg = 0; gg < G; ++gg) u += S.red[tid + gg * rows];
+      yfar[h.c + tid] = u;
+    }
+    named_bar_sync(1, kCons);
+  }
+}
+
+__global__ void __launch_bounds__(kPipeThreads, 3)
+stageB_tma_kernel(const BItem* __restrict__ items, int n_items, int32_t* counter, int kappa,
+                  int64_t leaf_begin, int64_t row_begin, const int32_t* __restrict__ leaf_start,
+                  LevelPtrs lp, double* __restrict__ yfar) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  PipeSmem& S = *reinterpret_cast<PipeSmem*>(smem_raw);
+  pipe_init(S);
+  if (threadIdx.x >= kCons) stageB_producer(S, items, n_items, counter, kappa, leaf_begin, row_begin, leaf_start, lp);
+  else stageB_consumers(S, yfar);
+}
+
+// y = yfar + scale (s0 + sL + sD) + shift x over the served rows, in the caller's order.
+__global__ void combine_kernel(int64_t row_begin, int64_t rows, const double* __restrict__ yfar,
+                               const double* __restrict__ ynear, int64_t n, const double* __restrict__ x,
+                               double scale, double shift, double* __restrict__ y,
+                               const int32_t* __restrict__ perm, int order_out, int64_t y_row0) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < rows;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = row_begin + k;
+    const double s = yfar[k] + fma(scale, (ynear[r] + ynear[n + r]) + ynear[2 * n + r], shift * x[r]);
+    if (order_out == H2D_ORDER_ORIGINAL) y[perm[r]] = s;
+    else y[r - y_row0] = s;
   }
 }
 
@@ -511,20 +708,21 @@ void unpad_gathered(Handle& h, const double* d_xg, double* d_xtree) {
 }
 
 // Pack one level's factors (per-block sources, column-major U_b m x r and V_b n x r) into
-// the U / V panels and fill the level's panel metadata.
+// the U leaf panels and V panels and fill the level's panel metadata.
 void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
                 const std::vector<const double*>& srcV) {
   cudaStream_t s = h.stream;
   const int l = L.l;
   const int64_t nbox = L.nbox;
+  const int sh = 2 * (h.kappa - l);
   auto rank_of = [&](int64_t e) { return std::max<int32_t>(0, L.rank[(size_t)e]); };
+  auto up16 = [](int64_t v) { return (v + 15) & ~(int64_t)15; };
   L.ucol.assign((size_t)L.nblocks, 0);
   L.vcol.assign((size_t)L.nblocks, 0);
-  L.upan_off.assign((size_t)nbox, 0);
   L.vpan_off.assign((size_t)nbox, 0);
   L.ucolbase.assign((size_t)nbox + 1, 0);
   L.vR.assign((size_t)nbox, 0);
-  int64_t uo = 0, vo = 0;
+  int64_t vo = 0, vvals = 0;
   int32_t cb = 0;
   for (int64_t X = 0; X < nbox; ++X) {
     const int64_t m = h.box_end(l, X) - h.box_begin(l, X);
@@ -535,8 +733,6 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
     }
     L.ucolbase[(size_t)X] = cb;
     cb += R;
-    L.upan_off[(size_t)X] = uo;
-    uo += m * R;
     // V panel of column box X: blocks (Z, X) for Z in I_X ascending
     int32_t RV = 0;
     for (int32_t e2 = L.off[(size_t)X]; e2 < L.off[(size_t)X + 1]; ++e2) {
@@ -544,37 +740,65 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
       L.vcol[(size_t)b] = RV;
       RV += rank_of(b);
     }
+    if (RV > 2048) throw Error{H2D_EINVAL, "V panel wider than 2048 columns (lower max_rank)"};
     L.vR[(size_t)X] = RV;
     L.vpan_off[(size_t)X] = vo;
-    vo += m * RV;
+    vo = up16(vo + m * ((RV + 1) & ~1));
+    vvals += m * RV;
   }
   L.ucolbase[(size_t)nbox] = cb;
-  L.u_values = uo;
-  L.v_values = vo;
+  // U leaf panels of the served leaves
+  const int64_t nserved = h.leaf_end - h.leaf_begin;
+  L.uoff.assign((size_t)std::max<int64_t>(nserved, 0), 0);
+  int64_t uo = 0, uvals = 0;
+  for (int64_t lf = h.leaf_begin; lf < h.leaf_end; ++lf) {
+    const int64_t X = lf >> sh;
+    const int64_t R = L.ucolbase[(size_t)X + 1] - L.ucolbase[(size_t)X];
+    const int64_t mL = h.leaf_start[(size_t)lf + 1] - h.leaf_start[(size_t)lf];
+    L.uoff[(size_t)(lf - h.leaf_begin)] = uo;
+    uo = up16(uo + ((mL + 1) & ~1) * R);
+    uvals += mL * R;
+  }
+  L.u_values = uvals;
+  L.v_values = vvals;
+  L.u_alloc = uo;
+  L.v_alloc = vo;
   L.U = h.alloc<double>(uo);
   L.V = h.alloc<double>(vo);
-  std::vector<CopyItem> citems;
+  H2D_CUDA(cudaMemsetAsync(L.U, 0, std::max<int64_t>(1, uo) * sizeof(double), s));
+  H2D_CUDA(cudaMemsetAsync(L.V, 0, std::max<int64_t>(1, vo) * sizeof(double), s));
+  std::vector<UCopyItem> uitems;
   std::vector<VPackItem> vitems;
+  for (int64_t lf = h.leaf_begin; lf < h.leaf_end; ++lf) {
+    const int64_t X = lf >> sh;
+    const int64_t bx0 = h.box_begin(l, X), mX = h.box_end(l, X) - bx0;
+    const int64_t s0 = h.leaf_start[(size_t)lf];
+    const int32_t mL = h.leaf_start[(size_t)lf + 1] - (int32_t)s0;
+    if (mL == 0) continue;
+    double* base = L.U + L.uoff[(size_t)(lf - h.leaf_begin)];
+    for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
+      const int r = rank_of(e);
+      if (r == 0) continue;
+      uitems.push_back(UCopyItem{srcU[(size_t)e] + (s0 - bx0), base + (int64_t)L.ucol[(size_t)e] * ((mL + 1) & ~1),
+                                 (int32_t)mX, (mL + 1) & ~1, mL, r});
+    }
+  }
   for (int64_t X = 0; X < nbox; ++X) {
-    const int64_t mX = h.box_end(l, X) - h.box_begin(l, X);
     for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
       const int r = rank_of(e);
       if (r == 0) continue;
       const int64_t Y = L.col[(size_t)e];
       const int64_t nY = h.box_end(l, Y) - h.box_begin(l, Y);
-      if (mX * r > 0)
-        citems.push_back(CopyItem{srcU[(size_t)e], L.U + L.upan_off[(size_t)X] + (int64_t)L.ucol[(size_t)e] * mX,
-                                  mX * r});
       if (nY * r > 0)
         vitems.push_back(VPackItem{srcV[(size_t)e], L.V + L.vpan_off[(size_t)Y] + L.vcol[(size_t)e],
-                                   (int32_t)nY, r, L.vR[(size_t)Y], 0});
+                                   (int32_t)nY, r, (L.vR[(size_t)Y] + 1) & ~1, 0});
     }
   }
   const size_t CH = 1 << 20;
-  for (size_t c0 = 0; c0 < citems.size(); c0 += CH) {
-    std::vector<CopyItem> part(citems.begin() + c0, citems.begin() + std::min(citems.size(), c0 + CH));
-    CopyItem* d = upload_tmp(part, s);
-    copy_items_kernel<<<(int)part.size(), 256, 0, s>>>(d);
+  for (size_t c0 = 0; c0 < uitems.size(); c0 += CH) {
+    std::vector<UCopyItem> part(uitems.begin() + c0, uitems.begin() + std::min(uitems.size(), c0 + CH));
+    UCopyItem* d = upload_tmp(part, s);
+    ucopy_kernel<<<(int)part.size(), 256, 0, s>>>(d);
     H2D_LAUNCH_CHECK();
     H2D_CUDA(cudaFreeAsync(d, s));
   }
@@ -588,14 +812,51 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
   H2D_CUDA(cudaStreamSynchronize(s));
 }
 
-// Build the stage-A / reduce schedule, the t layout (U-panel order) and the per-level
-// device tables.
+// Copy block e of level l out of the panels: U (m x r col-major), V (n x r col-major),
+// host arrays.  U needs every leaf of the row box to be served by this handle.
+void unpack_block(Handle& h, int l, int64_t e, int* m, int* n, int* r, double* U, double* V) {
+  Level& L = h.levels[(size_t)l];
+  const int64_t X = (int64_t)(std::upper_bound(L.off.begin(), L.off.end(), (int32_t)e) - L.off.begin()) - 1;
+  const int64_t Y = L.col[(size_t)e];
+  const int64_t bx0 = h.box_begin(l, X);
+  const int64_t mm = h.box_end(l, X) - bx0;
+  const int64_t nn = h.box_end(l, Y) - h.box_begin(l, Y);
+  const int rr = std::max<int32_t>(0, L.rank[(size_t)e]);
+  *m = (int)mm; *n = (int)nn; *r = rr;
+  if (rr == 0) return;
+  if (U) {
+    const int sh = 2 * (h.kappa - l);
+    const int64_t lf0 = X << sh, lf1 = (X + 1) << sh;
+    if (lf0 < h.leaf_begin || lf1 > h.leaf_end)
+      throw Error{H2D_EINVAL, "block row box not fully served by this handle"};
+    for (int64_t lf = lf0; lf < lf1; ++lf) {
+      const int64_t s0 = h.leaf_start[(size_t)lf];
+      const int64_t mL = h.leaf_start[(size_t)lf + 1] - s0;
+      if (mL == 0) continue;
+      const int64_t mLp = (mL + 1) & ~1;
+      H2D_CUDA(cudaMemcpy2D(U + (s0 - bx0), mm * 8,
+                            L.U + L.uoff[(size_t)(lf - h.leaf_begin)] + (int64_t)L.ucol[(size_t)e] * mLp,
+                            mLp * 8, mL * 8, rr, cudaMemcpyDeviceToHost));
+    }
+  }
+  if (V) {
+    const int64_t Rp = (L.vR[(size_t)Y] + 1) & ~1;
+    std::vector<double> rm((size_t)(nn * rr));
+    if (nn > 0)
+      H2D_CUDA(cudaMemcpy2D(rm.data(), rr * 8, L.V + L.vpan_off[(size_t)Y] + L.vcol[(size_t)e],
+                            (size_t)Rp * 8, rr * 8, nn, cudaMemcpyDeviceToHost));
+    for (int64_t j = 0; j < nn; ++j)
+      for (int q = 0; q < rr; ++q) V[j + (int64_t)q * nn] = rm[(size_t)(j * rr + q)];
+  }
+}
+
+// Build the stage-A / reduce schedule, the t layout (U-column order), the stage-B items
+// and the per-level device tables.
 void finalize_schedule(Handle& h) {
   cudaStream_t s = h.stream;
   int64_t t_len = 0, tpart_len = 0;
   std::vector<AItem> aitems;
   std::vector<RItem> ritems;
-  // t layout: level by level, U-panel column order (ucolbase) -> tu_base per level
   for (int l = 1; l <= h.kappa; ++l) {
     Level& L = h.levels[(size_t)l];
     L.tu_base = t_len;
@@ -609,7 +870,7 @@ void finalize_schedule(Handle& h) {
     Level& L = h.levels[(size_t)l];
     L.t_off.assign((size_t)L.nbox, 0);
     for (int64_t Y = 0; Y < L.nbox; ++Y) {
-      L.t_off[(size_t)Y] = vpos;       // first vdst entry of the V panel of Y
+      L.t_off[(size_t)Y] = vpos;
       for (int32_t e2 = L.off[(size_t)Y]; e2 < L.off[(size_t)Y + 1]; ++e2) {
         const int32_t b = L.trans[(size_t)e2];           // block (X, Y)
         const int r = std::max<int32_t>(0, L.rank[(size_t)b]);
@@ -630,50 +891,79 @@ void finalize_schedule(Handle& h) {
   for (int l = 1; l <= h.kappa; ++l) {
     Level& L = h.levels[(size_t)l];
     L.d_ucolbase = h.alloc<int32_t>(L.ucolbase.size());
-    L.d_upan_off = h.alloc<int64_t>(L.upan_off.size());
+    L.d_uoff = h.alloc<int64_t>(L.uoff.size());
     H2D_CUDA(cudaMemcpyAsync(L.d_ucolbase, L.ucolbase.data(), L.ucolbase.size() * 4,
                              cudaMemcpyHostToDevice, s));
-    H2D_CUDA(cudaMemcpyAsync(L.d_upan_off, L.upan_off.data(), L.upan_off.size() * 8,
-                             cudaMemcpyHostToDevice, s));
+    if (!L.uoff.empty())
+      H2D_CUDA(cudaMemcpyAsync(L.d_uoff, L.uoff.data(), L.uoff.size() * 8, cudaMemcpyHostToDevice, s));
     H2D_CUDA(cudaStreamSynchronize(s));
     h.lp.U[l] = L.U;
     h.lp.V[l] = L.V;
     h.lp.ucolbase[l] = L.d_ucolbase;
-    h.lp.upan_off[l] = L.d_upan_off;
+    h.lp.uoff[l] = L.d_uoff;
     h.lp.tu[l] = h.d_t + L.tu_base;
     // stage-A items: chunks of <= kATarget elements and <= kAMaxRows rows
     for (int64_t Y = 0; Y < L.nbox; ++Y) {
-      const int R = L.vR[(size_t)Y];
+      const int R = L.vR[(size_t)Y], Rp = (R + 1) & ~1;
       const int64_t y0 = h.box_begin(l, Y);
       const int64_t nY = h.box_end(l, Y) - y0;
       if (R == 0 || nY == 0) continue;
-      int64_t nch = std::max<int64_t>((nY * R + kATarget - 1) / kATarget, (nY + kAMaxRows - 1) / kAMaxRows);
+      int64_t nch = std::max<int64_t>((nY * Rp + kATarget - 1) / kATarget, (nY + kAMaxRows - 1) / kAMaxRows);
       nch = std::min<int64_t>(nY, std::max<int64_t>(1, nch));
       const int64_t rows = (nY + nch - 1) / nch;
       nch = (nY + rows - 1) / rows;
       const int32_t vp = (int32_t)L.t_off[(size_t)Y];
       if (nch == 1) {
-        aitems.push_back(AItem{L.vpan_off[(size_t)Y], y0, (int32_t)nY, R, vp, l, -1, 0});
+        aitems.push_back(AItem{L.vpan_off[(size_t)Y], y0, (int32_t)nY, R, vp, l, -1, Rp});
       } else {
         if (tpart_len + nch * R > INT32_MAX) throw Error{H2D_EINVAL, "partial buffer too large"};
         ritems.push_back(RItem{vp, (int32_t)tpart_len, R, (int32_t)nch});
         for (int64_t c = 0; c < nch; ++c) {
           const int64_t r0 = c * rows, nr = std::min(rows, nY - r0);
-          aitems.push_back(AItem{L.vpan_off[(size_t)Y] + r0 * R, y0 + r0, (int32_t)nr, R,
+          aitems.push_back(AItem{L.vpan_off[(size_t)Y] + r0 * Rp, y0 + r0, (int32_t)nr, R,
                                  (int32_t)(-(tpart_len + c * R) - 1), l,
-                                 (int32_t)(ritems.size() - 1), 0});
+                                 (int32_t)(ritems.size() - 1), Rp});
         }
         tpart_len += nch * R;
       }
     }
   }
+  // largest items first: the dynamic (atomic-counter) schedule then ends with small items
+  std::stable_sort(aitems.begin(), aitems.end(), [](const AItem& a, const AItem& b) {
+    return (int64_t)a.nrows * a.Rp > (int64_t)b.nrows * b.Rp;
+  });
+  // stage-B items: served leaves in row blocks of <= kBRows rows, largest cost first
+  std::vector<BItem> bitems;
+  std::vector<int64_t> bcost;
+  for (int64_t lf = h.leaf_begin; lf < h.leaf_end; ++lf) {
+    const int32_t mL = h.leaf_start[(size_t)lf + 1] - h.leaf_start[(size_t)lf];
+    int64_t RL = 0;
+    for (int l = 1; l <= h.kappa; ++l) {
+      const Level& L = h.levels[(size_t)l];
+      const int64_t X = lf >> (2 * (h.kappa - l));
+      RL += L.ucolbase[(size_t)X + 1] - L.ucolbase[(size_t)X];
+    }
+    for (int32_t r0 = 0; r0 < mL; r0 += kBRows) {
+      const int32_t rows = std::min(kBRows, mL - r0);
+      bitems.push_back(BItem{(int32_t)lf, r0, rows, 0});
+      bcost.push_back((int64_t)((rows + 1) & ~1) * RL + 512);
+    }
+  }
+  std::vector<size_t> ord(bitems.size());
+  std::iota(ord.begin(), ord.end(), 0);
+  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return bcost[a] > bcost[b]; });
+  std::vector<BItem> bsorted;
+  bsorted.reserve(bitems.size());
+  for (size_t k : ord) bsorted.push_back(bitems[k]);
   h.tpart_len = tpart_len;
   h.d_tpart = h.alloc<double>(tpart_len);
   h.n_aitems = (int64_t)aitems.size();
   h.n_ritems = (int64_t)ritems.size();
+  h.n_bitems = (int64_t)bsorted.size();
   h.d_aitems = h.alloc<AItem>(aitems.size());
   h.d_ritems = h.alloc<RItem>(ritems.size());
   h.d_rcount = h.alloc<int32_t>(ritems.size());
+  h.d_bitems = h.alloc<BItem>(bsorted.size());
   H2D_CUDA(cudaMemsetAsync(h.d_rcount, 0, std::max<size_t>(1, ritems.size()) * sizeof(int32_t), s));
   if (!aitems.empty())
     H2D_CUDA(cudaMemcpyAsync(h.d_aitems, aitems.data(), aitems.size() * sizeof(AItem),
@@ -681,14 +971,35 @@ void finalize_schedule(Handle& h) {
   if (!ritems.empty())
     H2D_CUDA(cudaMemcpyAsync(h.d_ritems, ritems.data(), ritems.size() * sizeof(RItem),
                              cudaMemcpyHostToDevice, s));
+  if (!bsorted.empty())
+    H2D_CUDA(cudaMemcpyAsync(h.d_bitems, bsorted.data(), bsorted.size() * sizeof(BItem),
+                             cudaMemcpyHostToDevice, s));
   if (!h.d_ynear) h.d_ynear = h.alloc<double>(3 * h.n);   // three P2P slots (p2p_sym_kernel)
-  H2D_CUDA(cudaFuncSetAttribute(stageA_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                cudaSharedmemCarveoutMaxShared));
-  if (!h.aux_stream) {
-    H2D_CUDA(cudaStreamCreateWithFlags(&h.aux_stream, cudaStreamNonBlocking));
+  if (!h.d_yfar) h.d_yfar = h.alloc<double>(std::max<int64_t>(1, h.row_end - h.row_begin));
+  if (!h.d_counters) h.d_counters = h.alloc<int32_t>(2);
+  if (!h.hi_stream) {
+    int sm = 0, lo_prio = 0, hi_prio = 0;
+    H2D_CUDA(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, h.device));
+    h.persist_ctas = 2 * sm;
+    H2D_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    H2D_CUDA(cudaStreamCreateWithPriority(&h.hi_stream, cudaStreamNonBlocking, hi_prio));
+    H2D_CUDA(cudaStreamCreateWithPriority(&h.aux_stream, cudaStreamNonBlocking, lo_prio));
     H2D_CUDA(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
     H2D_CUDA(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
+    H2D_CUDA(cudaEventCreateWithFlags(&h.ev_far, cudaEventDisableTiming));
+    const int smem = (int)sizeof(PipeSmem);
+    H2D_CUDA(cudaFuncSetAttribute(stageA_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    H2D_CUDA(cudaFuncSetAttribute(stageB_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    H2D_CUDA(cudaFuncSetAttribute(stageA_tma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+    H2D_CUDA(cudaFuncSetAttribute(stageB_tma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+    for (auto* f : {p2p_sym_kernel<H2D_KERNEL_LOG>, p2p_sym_kernel<H2D_KERNEL_IMQ>,
+                    p2p_sym_kernel<H2D_KERNEL_ONE_OVER_R>, p2p_sym_kernel<H2D_KERNEL_TEST_LOWRANK>})
+      H2D_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    cudaSharedmemCarveoutMaxShared));
   }
+  H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 2 * sizeof(int32_t), s));
   H2D_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -718,13 +1029,32 @@ void begin_matvec_timing(Handle& h) {
 
 void mark_after_input(Handle& h) { record(h, 1, h.stream); }
 
-// Matvec on TREE-order x (S7-S9).  The near-field P2P (compute-bound) runs on the aux
-// stream concurrently with stage A (HBM-bound); stage B joins both.
+// Matvec on TREE-order x (S7-S9).  Stages A and B (HBM-bound) run on the high-priority
+// stream, the near-field P2P (FP64-bound) concurrently on the low-priority stream; the
+// combine epilogue on the caller's stream joins them.
 void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, int64_t y_row0) {
-  cudaStream_t s = h.stream, a = h.aux_stream;
+  cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
   const int64_t nleaves = h.leaf_end - h.leaf_begin;
   H2D_CUDA(cudaEventRecord(h.ev_fork, s));
+  H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_fork, 0));
   H2D_CUDA(cudaStreamWaitEvent(a, h.ev_fork, 0));
+  const size_t smem = sizeof(PipeSmem);
+  H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 2 * sizeof(int32_t), hi));
+  if (h.n_aitems > 0) {
+    stageA_tma_kernel<<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+        h.d_aitems, (int)h.n_aitems, h.d_counters, h.lp, d_xtree, h.d_vdst, h.d_t, h.d_tpart,
+        h.d_ritems, h.d_rcount);
+    H2D_LAUNCH_CHECK();
+  }
+  record(h, 2, hi);
+  if (h.n_bitems > 0) {
+    stageB_tma_kernel<<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+        h.d_bitems, (int)h.n_bitems, h.d_counters + 1, h.kappa, h.leaf_begin, h.row_begin,
+        h.d_leaf_start, h.lp, h.d_yfar);
+    H2D_LAUNCH_CHECK();
+  }
+  record(h, 3, hi);
+  H2D_CUDA(cudaEventRecord(h.ev_far, hi));
   record(h, 6, a);
   if (nleaves > 0) {
     auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_sym_kernel<H2D_KERNEL_LOG>
@@ -738,19 +1068,14 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
   }
   record(h, 7, a);
   H2D_CUDA(cudaEventRecord(h.ev_join, a));
-  if (h.n_aitems > 0) {
-    stageA_kernel<<<(int)h.n_aitems, kAThreads, 0, s>>>(h.d_aitems, h.lp, d_xtree, h.d_vdst, h.d_t,
-                                                        h.d_tpart, h.d_ritems, h.d_rcount);
-    H2D_LAUNCH_CHECK();
-  }
-  record(h, 2, s);
-  record(h, 3, s);
+  H2D_CUDA(cudaStreamWaitEvent(s, h.ev_far, 0));
   H2D_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
   record(h, 4, s);
-  if (nleaves > 0) {
-    stageB_kernel<<<(int)nleaves, kBThreads, 0, s>>>(h.kappa, h.leaf_begin, h.d_leaf_start, h.lp,
-                                                      h.d_ynear, h.n, d_xtree, h.kp.scale,
-                                                      h.kp.shift, d_y, h.d_perm, order_out, y_row0);
+  const int64_t rows = h.row_end - h.row_begin;
+  if (rows > 0) {
+    const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 148 * 8);
+    combine_kernel<<<blocks, 256, 0, s>>>(h.row_begin, rows, h.d_yfar, h.d_ynear, h.n, d_xtree,
+                                          h.kp.scale, h.kp.shift, d_y, h.d_perm, order_out, y_row0);
     H2D_LAUNCH_CHECK();
   }
   record(h, 5, s);

@@ -35,7 +35,9 @@ Handle::~Handle() {
   for (auto e : ev_pool) cudaEventDestroy(e);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
+  if (ev_far) cudaEventDestroy(ev_far);
   if (aux_stream) cudaStreamDestroy(aux_stream);
+  if (hi_stream) cudaStreamDestroy(hi_stream);
 }
 
 static double now_s() {
@@ -64,8 +66,10 @@ static void clear_factors(Handle& h) {
     h.release(L.U); L.U = nullptr;
     h.release(L.V); L.V = nullptr;
     h.release(L.d_ucolbase); L.d_ucolbase = nullptr;
-    h.release(L.d_upan_off); L.d_upan_off = nullptr;
+    h.release(L.d_uoff); L.d_uoff = nullptr;
   }
+  h.release(h.d_bitems); h.d_bitems = nullptr;
+  h.n_bitems = 0;
   h.release(h.d_aitems); h.d_aitems = nullptr;
   h.release(h.d_ritems); h.d_ritems = nullptr;
   h.release(h.d_rcount); h.d_rcount = nullptr;
@@ -251,27 +255,8 @@ static void load_factors(Handle& h, const char* path) {
   finalize_schedule(h);
 }
 
-// Extract block e of level l from the panels: U (m x r col-major), V (n x r col-major).
 static void extract_block(Handle& h, int l, int64_t e, int* m, int* n, int* r, double* U, double* V) {
-  Level& L = h.levels[(size_t)l];
-  const int64_t X = (int64_t)(std::upper_bound(L.off.begin(), L.off.end(), (int32_t)e) - L.off.begin()) - 1;
-  const int64_t Y = L.col[(size_t)e];
-  const int64_t mm = h.box_end(l, X) - h.box_begin(l, X);
-  const int64_t nn = h.box_end(l, Y) - h.box_begin(l, Y);
-  const int rr = std::max<int32_t>(0, L.rank[(size_t)e]);
-  *m = (int)mm; *n = (int)nn; *r = rr;
-  if (rr == 0) return;
-  if (U)
-    H2D_CUDA(cudaMemcpy(U, L.U + L.upan_off[(size_t)X] + (int64_t)L.ucol[(size_t)e] * mm,
-                        mm * rr * 8, cudaMemcpyDeviceToHost));
-  if (V) {
-    std::vector<double> rm((size_t)(nn * rr));
-    if (nn > 0)
-      H2D_CUDA(cudaMemcpy2D(rm.data(), rr * 8, L.V + L.vpan_off[(size_t)Y] + L.vcol[(size_t)e],
-                            (size_t)L.vR[(size_t)Y] * 8, rr * 8, nn, cudaMemcpyDeviceToHost));
-    for (int64_t j = 0; j < nn; ++j)
-      for (int q = 0; q < rr; ++q) V[j + (int64_t)q * nn] = rm[(size_t)(j * rr + q)];
-  }
+  unpack_block(h, l, e, m, n, r, U, V);
 }
 
 }  // namespace h2d

@@ -93,20 +93,26 @@ struct Level {
   // per block (host): rank, built flag, panel columns
   std::vector<int32_t> rank;   // -1 = not built on this rank
   std::vector<uint8_t> truncated;
-  std::vector<int32_t> ucol;   // first column inside the U panel of the row box
+  std::vector<int32_t> ucol;   // first column of the block among the U columns of its row box
   std::vector<int32_t> vcol;   // first column inside the V panel of the column box
-  // panels (device): U panel of row box X: col-major m_X x R_X at U + upan_off[X];
-  // V panel of column box Y: row-major n_Y x RV_Y at V + vpan_off[Y].
+  // U leaf panels (device): for every served leaf L with level-l ancestor X, the rows of L
+  // of all U columns of X ([U_b1 | U_b2 | ...], blocks (X, Y), Y in I_X ascending):
+  // column-major mLp x R_X at U + uoff[L - leaf_begin], mLp = |L| rounded up to even, so a
+  // leaf's level-l factors are one contiguous, 16-byte aligned range (bulk-TMA source).
+  // V panel of column box Y: row-major n_Y x RVp_Y at V + vpan_off[Y], RVp_Y = RV_Y
+  // rounded up to even (every row chunk is a 16-byte aligned range).
   double* U = nullptr;
   double* V = nullptr;
-  int64_t u_values = 0, v_values = 0;
-  std::vector<int64_t> upan_off, vpan_off;  // per box
+  int64_t u_values = 0, v_values = 0;       // stored factor values (without padding)
+  int64_t u_alloc = 0, v_alloc = 0;         // allocated doubles (with padding)
+  std::vector<int64_t> uoff;                // per served leaf
+  std::vector<int64_t> vpan_off;            // per box
   std::vector<int32_t> ucolbase;            // per box + 1 (prefix of R_X)
   std::vector<int32_t> vR;                  // per box RV_Y
-  std::vector<int64_t> t_off;               // per box: t of column box Y (global t index)
+  std::vector<int64_t> t_off;               // per box: first vdst entry of column box Y
   int32_t* d_ucolbase = nullptr;            // [nbox + 1]
-  int64_t* d_upan_off = nullptr;            // [nbox]
-  int64_t tu_base = 0;                      // first t entry of the level (U-panel order)
+  int64_t* d_uoff = nullptr;                // [served leaves]
+  int64_t tu_base = 0;                      // first t entry of the level (U-column order)
 };
 
 // Stage-A work item: one row chunk of one V panel.  Outputs go to t (U-panel order)
@@ -119,6 +125,13 @@ struct AItem {
   int32_t out;
   int32_t level;
   int32_t ritem;   // >= 0: multi-chunk box (RItem index); the last chunk CTA reduces
+  int32_t Rp;      // row stride of the panel (R rounded up to even)
+};
+// Stage-B work item: rows [r0, r0 + rows) (rows <= 256) of served leaf `leaf`.
+struct BItem {
+  int32_t leaf;
+  int32_t r0;
+  int32_t rows;
   int32_t pad;
 };
 // Reduction of multi-chunk partials: t[vdst[vpos + q]] = sum_c part[p_off + c*R + q]
@@ -133,8 +146,8 @@ struct LevelPtrs {
   const double* U[H2D_MAX_LEVELS + 1];
   const double* V[H2D_MAX_LEVELS + 1];
   const int32_t* ucolbase[H2D_MAX_LEVELS + 1];
-  const int64_t* upan_off[H2D_MAX_LEVELS + 1];
-  const double* tu[H2D_MAX_LEVELS + 1];   // t of the level in U-panel column order
+  const int64_t* uoff[H2D_MAX_LEVELS + 1];  // U leaf-panel offsets (served leaves)
+  const double* tu[H2D_MAX_LEVELS + 1];   // t of the level in U-column order
 };
 
 struct Handle {
@@ -179,9 +192,15 @@ struct Handle {
   LevelPtrs lp{};
   int rmax_panel = 1;                     // widest per-leaf t gather (smem of stage B)
   int max_ritem_R = 1;
-  double* d_ynear = nullptr;              // [n] near field + shift x (P2P output)
-  cudaStream_t aux_stream = nullptr;      // P2P runs here, concurrent with stage A
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  BItem* d_bitems = nullptr;              // stage-B items, largest first
+  int64_t n_bitems = 0;
+  int32_t* d_counters = nullptr;          // [2] dynamic work counters of stage A / B
+  int persist_ctas = 0;                   // CTAs of the persistent stage-A/B kernels
+  double* d_ynear = nullptr;              // [3n] near-field P2P slots (p2p_sym_kernel)
+  double* d_yfar = nullptr;               // [served] low-rank part (stage B output)
+  cudaStream_t hi_stream = nullptr;       // stages A, B (high priority)
+  cudaStream_t aux_stream = nullptr;      // P2P (low priority), concurrent with A and B
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_far = nullptr;
   // matvec work buffers
   double* d_xtree = nullptr;              // [n]
   double* d_ybuf = nullptr;               // [n] staging for host y
@@ -230,11 +249,14 @@ void run_aca(Handle& h);                                          // aca.cu (G6)
 void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
                 const std::vector<const double*>& srcV);
 void finalize_schedule(Handle& h);                                // apply.cu
+// Copy block e of level l out of the panels to host arrays (U m x r, V n x r, col-major).
+void unpack_block(Handle& h, int l, int64_t e, int* m, int* n, int* r, double* U, double* V);
 void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out,
                  int64_t y_row0);                                 // apply.cu (S7-S9)
 void permute_in(Handle& h, const double* d_x, double* d_xtree);   // apply.cu (S10)
-// per-matvec CUDA events (timing mode): 0 start, 1 after input permute/unpad, 2 after
-// stage A, 3 after t-reduce, 4 after joining P2P, 5 end (main stream); 6/7 P2P (aux)
+// per-matvec CUDA events (timing mode): 0 start, 1 after input permute/unpad (caller
+// stream); 2 after stage A, 3 after stage B (high-priority stream); 4 after joining the
+// P2P, 5 end = after the combine epilogue (caller stream); 6/7 P2P (aux stream)
 constexpr int kEventsPerMatvec = 8;
 void begin_matvec_timing(Handle& h);
 void mark_after_input(Handle& h);
