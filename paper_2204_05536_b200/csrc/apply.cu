@@ -21,6 +21,7 @@
 //                               co-resident with A and B: they leave it registers and smem)
 //   combine  y = yfar + scale * ynear + shift * x, permuted to the caller's order.
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 #include "h2d_internal.cuh"
@@ -29,20 +30,23 @@
 namespace h2d {
 namespace {
 
-constexpr int64_t kATarget = 32768;  // stage-A elements per work item (256 KB)
+constexpr int64_t kATargetDefault = 1048576;  // stage-A elements per work item (8 MB)
 constexpr int kAMaxRows = 16384;     // rows per stage-A item
-constexpr int kBRows = 256;          // rows per stage-B item (leaf row block)
+constexpr int kBRows = 224;          // rows per stage-B item (leaf row block) <= kCons
 
 // ---------------------------------------------------------------- pipeline layout
 // One producer warp (bulk TMA of the factor stream + 8-byte cp.async of the x / t values
-// a stage needs) and 8 consumer warps per CTA, kNS-deep ring of 16 KB stages.  With
+// a stage needs) and 8 consumer warps per CTA, NS-deep ring of 16 KB stages.  With
 // 2 CTAs per SM (grid = 2 x SMs, ~95 KB smem, <= 72 registers) a third CTA of the P2P
 // kernel still fits on every SM, so the FP64-bound near field runs under the HBM stream.
-constexpr int kNS = 5;
+constexpr int kNSShallow = 5, kNSDeep = 9;   // ring depth at 2 / 1 CTAs per SM
+constexpr int kDefaultCtasPerSm = 2;
 constexpr int kStageDbl = 2048;      // factor doubles per stage (16 KB)
 constexpr int kStageVec = 256;       // x (stage A) / t (stage B) values per stage
-constexpr int kCons = 256;           // consumer threads
+constexpr int kCons = 224;           // consumer threads (7 warps: 8-warp CTAs spread evenly
+                                     // over the 4 SM sub-partitions' register files)
 constexpr int kPipeThreads = kCons + 32;
+
 constexpr int kFirst = 1, kLast = 2;
 
 struct StageHdr {
@@ -52,19 +56,21 @@ struct StageHdr {
   int32_t a, b, c, d, pad;   // item fields for the consumers (see the producers)
 };
 
+template <int NS>
 struct PipeSmem {
-  double ring[kNS][kStageDbl];
-  double vec[kNS][kStageVec];
-  double red[kCons];
-  StageHdr hdr[kNS];
-  uint64_t full[kNS];    // 1 producer arrival (+ tx bytes) + 32 cp.async arrivals
-  uint64_t empty[kNS];   // 8 consumer-warp arrivals
+  double ring[NS][kStageDbl];
+  double vec[NS][kStageVec];
+  double red[2 * kCons];
+  StageHdr hdr[NS];
+  uint64_t full[NS];    // 1 producer arrival (+ tx bytes) + 32 cp.async arrivals
+  uint64_t empty[NS];   // 8 consumer-warp arrivals
   int flag;
 };
 
-__device__ __forceinline__ void pipe_init(PipeSmem& S) {
+template <int NS>
+__device__ __forceinline__ void pipe_init(PipeSmem<NS>& S) {
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kNS; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&S.full[s], 1 + 32);
       mbar_init(&S.empty[s], kCons / 32);
     }
@@ -118,19 +124,28 @@ T* upload_tmp(const std::vector<T>& v, cudaStream_t s) {
 // (G = 256 / R groups, reduced in smem at the end of the item); R > 256 -> thread owns
 // columns tid + 256 c (c < CPL) over all rows.  Stage header: a = R, b = Rp, c = out,
 // d = ritem.
-__device__ void stageA_producer(PipeSmem& S, const AItem* __restrict__ items, int n_items,
+template <int NS>
+__device__ void stageA_producer(PipeSmem<NS>& S, const AItem* __restrict__ items, int n_items,
                                 int32_t* counter, const LevelPtrs& lp, const double* __restrict__ x) {
   const int lane = threadIdx.x & 31;
   const uint64_t pol = l2_evict_first_policy();
   int stage = 0;
   uint32_t phase = 0;
+  // one-item lookahead: the next item's index (atomic) and descriptor (load) are in flight
+  // while the current item streams, so item boundaries cost no memory latency
+  int idx = 0, nidx = 0;
+  if (lane == 0) idx = atomicAdd(counter, 1);
+  idx = __shfl_sync(0xffffffffu, idx, 0);
+  if (lane == 0) nidx = atomicAdd(counter, 1);
+  AItem nit{};
+  if (idx < n_items) nit = items[idx];
   for (;;) {
-    int idx = 0;
-    if (lane == 0) idx = atomicAdd(counter, 1);
-    idx = __shfl_sync(0xffffffffu, idx, 0);
     const bool done = idx >= n_items;
-    AItem it{};
-    if (!done) it = items[idx];
+    const AItem it = nit;
+    const int cur = idx;
+    idx = __shfl_sync(0xffffffffu, nidx, 0);       // issued one item ago
+    if (!done && lane == 0) nidx = atomicAdd(counter, 1);
+    if (!done && idx < n_items) nit = items[idx];
     const int rows_s = done ? 1 : min(kStageVec, kStageDbl / it.Rp);
     const double* V = done ? nullptr : lp.V[it.level] + it.v_off;
     int r0 = 0;
@@ -139,7 +154,7 @@ __device__ void stageA_producer(PipeSmem& S, const AItem* __restrict__ items, in
       mbar_wait(&S.empty[stage], phase ^ 1);
       if (lane == 0) {
         StageHdr& h = S.hdr[stage];
-        h.item = done ? -1 : idx;
+        h.item = done ? -1 : cur;
         h.cnt = rows;
         h.flags = (r0 == 0 ? kFirst : 0) | (r0 + rows >= it.nrows ? kLast : 0);
         h.a = it.R;
@@ -152,53 +167,73 @@ __device__ void stageA_producer(PipeSmem& S, const AItem* __restrict__ items, in
       }
       for (int j = lane; j < rows; j += 32) cp_async8(&S.vec[stage][j], x + it.x_off + r0 + j);
       cp_async_arrive_noinc(&S.full[stage]);
-      if (++stage == kNS) { stage = 0; phase ^= 1; }
+      if (++stage == NS) { stage = 0; phase ^= 1; }
       r0 += rows;
     } while (!done && r0 < it.nrows);
     if (done) break;
   }
 }
 
-template <int CPL>
+// Consumers work on column pairs (one 16-byte smem load = 2 panel elements; Rp is even
+// and the padding column is zero, so a pair never straddles a row).  P = Rp / 2 pairs per
+// row.  P <= kCons: thread (g, p) = (tid / P, tid % P) owns pair p, rows g, g + G, ...
+// (G = kCons / P groups, reduced in smem at the end of the item).  P > kCons: thread owns
+// pairs tid + kCons c (c < CP) over all rows.
+constexpr int kMaxCP = (kStageDbl / 2 + kCons - 1) / kCons;
+
+template <int CP>
 __device__ __forceinline__ void stageA_consume(const double* __restrict__ sv, const double* __restrict__ sx,
-                                               int rows, int Rp, int R, int q, int g, int G,
-                                               double (&acc)[8]) {
-  if (CPL == 1) {
+                                               int rows, int Rp, int P, int p, int g, int G,
+                                               double (&acc)[2 * kMaxCP]) {
+  if (CP == 1) {
     if (g >= G) return;
-    const double* p = sv + q;
+    const double* __restrict__ v = sv + (size_t)g * Rp + 2 * p;
+    const int step = G * Rp;
     int j = g;
-    for (; j + 3 * G < rows; j += 4 * G) {
-      const double v0 = p[j * Rp], v1 = p[(j + G) * Rp], v2 = p[(j + 2 * G) * Rp], v3 = p[(j + 3 * G) * Rp];
-      acc[0] = fma(v0, sx[j], acc[0]);
-      acc[1] = fma(v1, sx[j + G], acc[1]);
-      acc[2] = fma(v2, sx[j + 2 * G], acc[2]);
-      acc[3] = fma(v3, sx[j + 3 * G], acc[3]);
+    for (; j + G < rows; j += 2 * G, v += 2 * step) {
+      const double2 a = *reinterpret_cast<const double2*>(v);
+      const double2 b = *reinterpret_cast<const double2*>(v + step);
+      const double xa = sx[j], xb = sx[j + G];
+      acc[0] = fma(a.x, xa, acc[0]);
+      acc[1] = fma(a.y, xa, acc[1]);
+      acc[2] = fma(b.x, xb, acc[2]);
+      acc[3] = fma(b.y, xb, acc[3]);
     }
-    for (; j < rows; j += G) acc[0] = fma(p[j * Rp], sx[j], acc[0]);
+    if (j < rows) {
+      const double2 a = *reinterpret_cast<const double2*>(v);
+      const double xa = sx[j];
+      acc[0] = fma(a.x, xa, acc[0]);
+      acc[1] = fma(a.y, xa, acc[1]);
+    }
   } else {
-    bool valid[CPL];
+    bool valid[CP];
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) valid[c] = q + 256 * c < R;
-    const double* p = sv + q;
-    for (int j = 0; j < rows; ++j, p += Rp) {
+    for (int c = 0; c < CP; ++c) valid[c] = p + kCons * c < P;
+    const double* __restrict__ v = sv + 2 * p;
+    for (int j = 0; j < rows; ++j, v += Rp) {
       const double xv = sx[j];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c)
-        if (valid[c]) acc[c] = fma(p[256 * c], xv, acc[c]);
+      for (int c = 0; c < CP; ++c)
+        if (valid[c]) {
+          const double2 a = *reinterpret_cast<const double2*>(v + 2 * kCons * c);
+          acc[2 * c] = fma(a.x, xv, acc[2 * c]);
+          acc[2 * c + 1] = fma(a.y, xv, acc[2 * c + 1]);
+        }
     }
   }
 }
 
-__device__ void stageA_consumers(PipeSmem& S, const int32_t* __restrict__ vdst, double* __restrict__ t,
+template <int NS>
+__device__ void stageA_consumers(PipeSmem<NS>& S, const int32_t* __restrict__ vdst, double* __restrict__ t,
                                  double* __restrict__ tpart, const RItem* __restrict__ ritems,
                                  int32_t* __restrict__ rcount) {
   const int tid = threadIdx.x, lane = tid & 31;
   int stage = 0;
   uint32_t phase = 0;
-  int R = 1, Rp = 2, CPL = 1, G = 1, g = 0, q = 0;
-  double acc[8];
+  int R = 1, Rp = 2, P = 1, CP = 1, G = 1, g = 0, p = 0;
+  double acc[2 * kMaxCP];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+  for (int c = 0; c < 2 * kMaxCP; ++c) acc[c] = 0.0;
   for (;;) {
     mbar_wait(&S.full[stage], phase);
     const StageHdr h = S.hdr[stage];
@@ -206,61 +241,75 @@ __device__ void stageA_consumers(PipeSmem& S, const int32_t* __restrict__ vdst, 
     if (h.flags & kFirst) {
       R = h.a;
       Rp = h.b;
-      CPL = (R + 255) >> 8;
-      if (CPL == 1) { G = kCons / R; g = tid / R; q = tid - g * R; }
-      else { G = 1; g = 0; q = tid; }
+      P = Rp >> 1;
+      CP = (P + kCons - 1) / kCons;
+      if (CP == 1) { G = kCons / P; g = tid / P; p = tid - g * P; }
+      else { G = 1; g = 0; p = tid; }
 #pragma unroll
-      for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+      for (int c = 0; c < 2 * kMaxCP; ++c) acc[c] = 0.0;
     }
     const double* sv = S.ring[stage];
     const double* sx = S.vec[stage];
-    switch (CPL) {
-      case 1: stageA_consume<1>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
-      case 2: stageA_consume<2>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
-      case 3: stageA_consume<3>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
-      case 4: stageA_consume<4>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
-      case 5: stageA_consume<5>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
-      case 6: stageA_consume<6>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
-      case 7: stageA_consume<7>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
-      default: stageA_consume<8>(sv, sx, h.cnt, Rp, R, q, g, G, acc); break;
+    switch (CP) {
+      case 1: stageA_consume<1>(sv, sx, h.cnt, Rp, P, p, g, G, acc); break;
+      case 2: stageA_consume<2>(sv, sx, h.cnt, Rp, P, p, g, G, acc); break;
+      case 3: stageA_consume<3>(sv, sx, h.cnt, Rp, P, p, g, G, acc); break;
+      case 4: stageA_consume<4>(sv, sx, h.cnt, Rp, P, p, g, G, acc); break;
+      default: stageA_consume<kMaxCP>(sv, sx, h.cnt, Rp, P, p, g, G, acc); break;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.empty[stage]);
-    if (++stage == kNS) { stage = 0; phase ^= 1; }
+    if (++stage == NS) { stage = 0; phase ^= 1; }
     if (!(h.flags & kLast)) continue;
     // ---- end of item: column sums -> t (or this chunk's partials)
     auto put = [&](int qq, double v) {
+      if (qq >= R) return;
       if (h.c >= 0) t[vdst[h.c + qq]] = v;
       else tpart[(int64_t)(-h.c - 1) + qq] = v;
     };
-    if (CPL == 1) {
-      const double s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    if (CP == 1) {
+      const double s0 = acc[0] + acc[2], s1 = acc[1] + acc[3];
       if (G > 1) {
-        S.red[tid] = g < G ? s : 0.0;
+        S.red[2 * tid] = g < G ? s0 : 0.0;
+        S.red[2 * tid + 1] = g < G ? s1 : 0.0;
         named_bar_sync(1, kCons);
-        if (tid < R) {
-          double u = 0.0;
-          for (int gg = 0; gg < G; ++gg) u += S.red[tid + gg * R];
-          put(tid, u);
+        if (tid < P) {
+          double u0 = 0.0, u1 = 0.0;
+          for (int gg = 0; gg < G; ++gg) {
+            u0 += S.red[2 * (tid + gg * P)];
+            u1 += S.red[2 * (tid + gg * P) + 1];
+          }
+          put(2 * tid, u0);
+          put(2 * tid + 1, u1);
         }
         named_bar_sync(1, kCons);
-      } else if (tid < R) {
-        put(tid, s);
+      } else if (tid < P) {
+        put(2 * tid, s0);
+        put(2 * tid + 1, s1);
       }
     } else {
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < CPL && tid + 256 * c < R) put(tid + 256 * c, acc[c]);
+      for (int c = 0; c < kMaxCP; ++c)
+        if (c < CP && tid + kCons * c < P) {
+          put(2 * (tid + kCons * c), acc[2 * c]);
+          put(2 * (tid + kCons * c) + 1, acc[2 * c + 1]);
+        }
     }
     if (h.d >= 0) {
       // Multi-chunk box: the last chunk to finish sums the partials in chunk order
       // (deterministic) and resets the counter for the next matvec.
-      __threadfence();
+      // (the barrier orders every consumer's partial writes before thread 0's gpu-scope
+      // fence + atomic; the last arriver's fence orders the other chunks' partials before
+      // its consumers' L2 reads)
       named_bar_sync(1, kCons);
-      if (tid == 0) S.flag = atomicAdd(rcount + h.d, 1) == ritems[h.d].nchunks - 1;
+      if (tid == 0) {
+        __threadfence();
+        const int last = atomicAdd(rcount + h.d, 1) == ritems[h.d].nchunks - 1;
+        if (last) __threadfence();
+        S.flag = last;
+      }
       named_bar_sync(1, kCons);
       if (S.flag) {
-        __threadfence();
         const RItem ri = ritems[h.d];
         for (int qq = tid; qq < ri.R; qq += kCons) {
           const double* __restrict__ pp = tpart + ri.p_off + qq;
@@ -281,13 +330,14 @@ __device__ void stageA_consumers(PipeSmem& S, const int32_t* __restrict__ vdst, 
   }
 }
 
+template <int NS>
 __global__ void __launch_bounds__(kPipeThreads, 3)
 stageA_tma_kernel(const AItem* __restrict__ items, int n_items, int32_t* counter, LevelPtrs lp,
                   const double* __restrict__ x, const int32_t* __restrict__ vdst, double* __restrict__ t,
                   double* __restrict__ tpart, const RItem* __restrict__ ritems,
                   int32_t* __restrict__ rcount) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  PipeSmem& S = *reinterpret_cast<PipeSmem*>(smem_raw);
+  PipeSmem<NS>& S = *reinterpret_cast<PipeSmem<NS>*>(smem_raw);
   pipe_init(S);
   if (threadIdx.x >= kCons) stageA_producer(S, items, n_items, counter, lp, x);
   else stageA_consumers(S, vdst, t, tpart, ritems, rcount);
@@ -310,27 +360,52 @@ stageA_tma_kernel(const AItem* __restrict__ items, int n_items, int32_t* counter
 // the 8 point coordinates and x values held in registers.
 constexpr int kSymRowsOnly = 0, kSymBoth = 1, kSymSelf = 2;
 
-// log(r2) for r2 > 0 (normal): r2 = 2^e m, m in [1, 2); c_k = 1 + (k + 1/2)/128 is the
-// centre of m's 1/128 bin (k = top 7 mantissa bits), tab[k] = (1/c_k, log c_k);
-// log r2 = e ln2 + log c_k + log1p(f), f = m/c_k - 1 in (-2^-8, 2^-8), log1p by its
-// degree-8 Taylor polynomial.  11 FP64 operations instead of libdevice's 29; absolute
-// error < 1e-15 (checked against libm over [1e-14, 8] when written).
-__device__ __forceinline__ double log_r2_fast(double r2, const double2* __restrict__ tab) {
+constexpr int kSymTile = 96, kSymMaxB = kSymTile / 16;
+
+// 0.5 log(r2) for normal r2 > 0: r2 = 2^e m, m in [1, 2); c_k = 1 + (k + 1/2)/128 is the
+// centre of m's 1/128 bin (k = top 7 mantissa bits), tab[k] = (1/c_k, 0.5 log c_k);
+// 0.5 log r2 = e ln2/2 + 0.5 log c_k + 0.5 log1p(f), f = m/c_k - 1, |f| <= 2^-8, with
+// 0.5 log1p(f) = f p(f), p the degree-5 Taylor polynomial (truncation f^7/7 <= 2e-18).
+// 9 DFMA; the coefficients are constant-bank operands (no register materialisation).
+__constant__ double c_hlog[8] = {0.34657359027997264,   // ln2 / 2 (high part)
+                                 1.1595234069231498e-17, // ln2 / 2 (low part)
+                                 0.5, -0.25, 1.0 / 6.0, -0.125, 0.1, -1.0 / 12.0};
+
+__device__ __forceinline__ double hlog_r2(double r2, const double2* __restrict__ tab) {
   const long long bits = __double_as_longlong(r2);
   const int e = (int)(bits >> 52) - 1023;
-  const int k = (int)((bits >> 45) & 127);
+  const int k = (int)(bits >> 45) & 127;
   const double mnt = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
   const double2 tb = tab[k];
   const double f = fma(mnt, tb.x, -1.0);
-  double p = fma(f, -0.125, 1.0 / 7.0);
-  p = fma(f, p, -1.0 / 6.0);
-  p = fma(f, p, 0.2);
-  p = fma(f, p, -0.25);
-  p = fma(f, p, 1.0 / 3.0);
-  p = fma(f, p, -0.5);
-  p = fma(f, p, 1.0);
+  double p = fma(f, c_hlog[7], c_hlog[6]);
+  p = fma(f, p, c_hlog[5]);
+  p = fma(f, p, c_hlog[4]);
+  p = fma(f, p, c_hlog[3]);
+  p = fma(f, p, c_hlog[2]);
   const double ed = (double)e;
-  return fma(ed, 0.6931471805599453, fma(p, f, fma(ed, 2.3190468138462996e-17, tb.y)));
+  return fma(ed, c_hlog[0], fma(p, f, fma(ed, c_hlog[1], tb.y)));
+}
+
+__device__ __forceinline__ void hlog_table(double2* tab) {
+  if (threadIdx.x < 128) {
+    const double c = 1.0 + (threadIdx.x + 0.5) / 128.0;
+    tab[threadIdx.x] = make_double2(1.0 / c, 0.5 * log(c));
+  }
+}
+
+// K(r) from r^2 with K(0) := K0 by a select (no branch); distance kernels only.
+template <int KID>
+__device__ __forceinline__ double kfast(double r2, const double2* __restrict__ tab, double inv_c2) {
+  if (KID == H2D_KERNEL_LOG) {
+    const double v = hlog_r2(r2, tab);
+    return r2 > 0.0 ? v : 0.0;
+  } else if (KID == H2D_KERNEL_IMQ) {
+    return rsqrt(fma(r2, inv_c2, 1.0));
+  } else {
+    const double v = rsqrt(r2);
+    return r2 > 0.0 ? v : 0.0;
+  }
 }
 
 template <int KID>
@@ -339,9 +414,74 @@ __device__ __forceinline__ double p2p_eval(const KernelParams& kp, const double2
   if (KID == H2D_KERNEL_LOG) {
     const double dx = px - qx, dy = py - qy;
     const double r2 = fma(dx, dx, dy * dy);
-    return r2 > 0.0 ? 0.5 * log_r2_fast(r2, tab) : 0.0;
+    return r2 > 0.0 ? hlog_r2(r2, tab) : 0.0;
   }
   return kernel_eval_t<KID>(kp, px, py, qx, qy);
+}
+
+// Fast tile (distance kernels, both tiles <= 96 points, already in shared memory as
+// [px | py | x] x 96): thread (ti, tj) of the 16 x 16 grid owns rows ti + 16 a and columns
+// tj + 16 b; its columns live in registers, rows are read from smem once per row.  Every
+// pair is evaluated branch-free; rows / columns beyond the tile carry zero weights.  DIAG:
+// the self block, pairs i < j only (both orientations) plus K0 x_i on the diagonal.
+template <int KID, bool DIAG>
+__device__ __forceinline__ void tile_fast(int mt, int nt, const double* __restrict__ sa,
+                                          const double* __restrict__ sb, const double2* __restrict__ tab,
+                                          double inv_c2, double k0, double* srow,
+                                          double (*scol)[kSymTile + 1]) {
+  const int tid = threadIdx.x, ti = tid >> 4, tj = tid & 15;
+  const int A = (mt + 15) >> 4, B = (nt + 15) >> 4;
+  double cpx[kSymMaxB], cpy[kSymMaxB], cxv[kSymMaxB], cacc[kSymMaxB];
+#pragma unroll
+  for (int bb = 0; bb < kSymMaxB; ++bb) {
+    const int j = tj + 16 * bb;
+    const bool vj = j < nt;
+    cpx[bb] = vj ? sb[j] : 0.0;
+    cpy[bb] = vj ? sb[kSymTile + j] : 0.0;
+    cxv[bb] = vj ? sb[2 * kSymTile + j] : 0.0;
+    cacc[bb] = 0.0;
+  }
+  for (int aa = 0; aa < A; ++aa) {
+    const int i = ti + 16 * aa;
+    const bool vi = i < mt;
+    const double rpx = vi ? sa[i] : 0.0, rpy = vi ? sa[kSymTile + i] : 0.0;
+    const double rx = vi ? sa[2 * kSymTile + i] : 0.0;
+    double racc = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < kSymMaxB; ++bb) {
+      if (bb < B) {
+        const double dx = rpx - cpx[bb], dy = rpy - cpy[bb];
+        double k = kfast<KID>(fma(dx, dx, dy * dy), tab, inv_c2);
+        if (DIAG) k = i < tj + 16 * bb ? k : 0.0;
+        racc = fma(k, cxv[bb], racc);
+        cacc[bb] = fma(k, rx, cacc[bb]);
+      }
+    }
+    if (DIAG && tj == 0) racc = fma(k0, rx, racc);
+    racc += __shfl_xor_sync(0xffffffffu, racc, 8);
+    racc += __shfl_xor_sync(0xffffffffu, racc, 4);
+    racc += __shfl_xor_sync(0xffffffffu, racc, 2);
+    racc += __shfl_xor_sync(0xffffffffu, racc, 1);
+    if (tj == 0 && vi) srow[i] = racc;
+  }
+#pragma unroll
+  for (int bb = 0; bb < kSymMaxB; ++bb)
+    if (bb < B) scol[ti][tj + 16 * bb] = cacc[bb];
+}
+
+// Fold a fast tile's row sums into row_dst and (unless null) its column sums into col_dst.
+__device__ __forceinline__ void tile_flush(int mt, int nt, double* row_dst, double* col_dst,
+                                           const double* srow, double (*scol)[kSymTile + 1]) {
+  const int tid = threadIdx.x;
+  __syncthreads();
+  if (tid < mt) row_dst[tid] += srow[tid];
+  if (col_dst && tid < nt) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s += scol[k][tid];
+    col_dst[tid] += s;
+  }
+  __syncthreads();
 }
 
 // One leaf-pair block on a 16 x 16 thread grid: thread (ti, tj) owns rows ti + 16a
@@ -349,7 +489,6 @@ __device__ __forceinline__ double p2p_eval(const KernelParams& kp, const double2
 // 96 x 96 points (a leaf of the configs fits one super-tile; larger blocks loop).  Row
 // points live in registers one row at a time, column points are read from shared memory,
 // column sums stay in registers (cacc[b]), row sums are reduced over tj by shuffles.
-constexpr int kSymTile = 96, kSymMaxB = kSymTile / 16;
 template <int KID>
 __device__ __noinline__ void sym_block(int mode, int64_t a0, int m, int64_t b0, int n, double* row_dst,
                           double* col_dst, const double* __restrict__ px,
@@ -377,9 +516,17 @@ __device__ __noinline__ void sym_block(int mode, int64_t a0, int m, int64_t b0, 
       }
       __syncthreads();
       const bool diag_tile = mode == kSymSelf && cb == ra;
-      double cacc[kSymMaxB];
+      // this thread's columns tj + 16 bb live in registers for the whole tile
+      double cpx[kSymMaxB], cpy[kSymMaxB], cxv[kSymMaxB], cacc[kSymMaxB];
 #pragma unroll
-      for (int bb = 0; bb < kSymMaxB; ++bb) cacc[bb] = 0.0;
+      for (int bb = 0; bb < kSymMaxB; ++bb) {
+        const int j = tj + 16 * bb;
+        const bool vj = bb < B && j < nt;
+        cpx[bb] = vj ? s_b[j] : 0.0;
+        cpy[bb] = vj ? s_b[kSymTile + j] : 0.0;
+        cxv[bb] = vj ? s_b[2 * kSymTile + j] : 0.0;
+        cacc[bb] = 0.0;
+      }
       for (int aa = 0; aa < A; ++aa) {
         const int i = ti + 16 * aa;
         const bool vi = i < mt;
@@ -392,8 +539,8 @@ __device__ __noinline__ void sym_block(int mode, int64_t a0, int m, int64_t b0, 
             bool ok = vi && j < nt;
             if (diag_tile) ok = ok && i <= j;
             if (ok) {
-              const double k = p2p_eval<KID>(kp, tab, rpx, rpy, s_b[j], s_b[kSymTile + j]);
-              racc = fma(k, s_b[2 * kSymTile + j], racc);
+              const double k = p2p_eval<KID>(kp, tab, rpx, rpy, cpx[bb], cpy[bb]);
+              racc = fma(k, cxv[bb], racc);
               if (!(diag_tile && i == j)) cacc[bb] = fma(k, rx, cacc[bb]);
             }
           }
@@ -443,19 +590,16 @@ __device__ __forceinline__ uint32_t p2p_compact(uint32_t v) {
 
 template <int KID>
 __global__ void __launch_bounds__(256, 3)
-p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end,
+p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end, const int32_t* __restrict__ leaves,
                const int32_t* __restrict__ leaf_start, const double* __restrict__ px,
                const double* __restrict__ py, const double* __restrict__ x, KernelParams kp,
                double* __restrict__ s0, double* __restrict__ sL, double* __restrict__ sD) {
-  __shared__ double s_a[3 * kSymTile], s_b[3 * kSymTile], srow[kSymTile];
+  __shared__ double s_a[3 * kSymTile], s_b[3 * kSymTile], s_c[3 * kSymTile], srow[kSymTile];
   __shared__ double scol[16][kSymTile + 1];
   __shared__ double2 s_logtab[128];
-  const int64_t X = leaf_begin + blockIdx.x;
+  const int64_t X = leaves[blockIdx.x];
   const int tid = threadIdx.x;
-  if (KID == H2D_KERNEL_LOG && tid < 128) {
-    const double c = 1.0 + (tid + 0.5) / 128.0;
-    s_logtab[tid] = make_double2(1.0 / c, log(c));
-  }
+  if (KID == H2D_KERNEL_LOG) hlog_table(s_logtab);
   const uint32_t cx = p2p_compact((uint32_t)X), cy = p2p_compact((uint32_t)X >> 1);
   const uint32_t side = 1u << kappa;
   const int64_t xs = leaf_start[X];
@@ -483,8 +627,34 @@ p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end,
   if (do_u)
     for (int i = tid; i < un; i += 256) sD[us + i] = 0.0;
   if (m == 0) return;
-  // phase 1: blocks in a fixed order (one code instance: keeps the I-cache footprint small)
-  for (int task = 0; task < 5; ++task) {
+  constexpr bool kDist = KID == H2D_KERNEL_LOG || KID == H2D_KERNEL_IMQ || KID == H2D_KERNEL_ONE_OVER_R;
+  int first_task = 0;
+  if (kDist && m <= kSymTile && rn <= kSymTile && un <= kSymTile) {
+    // fast path: the self, +x and +y tiles are loaded together (one memory latency), then
+    // evaluated branch-free; only rows-only partners (rank boundaries) take the generic path
+    for (int e = tid; e < 3 * kSymTile; e += 256) {
+      const int a = e / kSymTile, i = e - a * kSymTile;
+      const double* src = a == 0 ? px : a == 1 ? py : x;
+      if (i < m) s_a[e] = src[xs + i];
+      if (i < rn) s_b[e] = src[rs + i];
+      if (i < un) s_c[e] = src[us + i];
+    }
+    __syncthreads();
+    const double k0 = KID == H2D_KERNEL_IMQ ? 1.0 : 0.0;
+    tile_fast<KID, true>(m, m, s_a, s_a, s_logtab, kp.inv_c2, k0, srow, scol);
+    tile_flush(m, m, s0 + xs, s0 + xs, srow, scol);
+    if (has_r) {
+      tile_fast<KID, false>(m, rn, s_a, s_b, s_logtab, kp.inv_c2, k0, srow, scol);
+      tile_flush(m, rn, s0 + xs, do_r ? sL + rs : nullptr, srow, scol);
+    }
+    if (has_u) {
+      tile_fast<KID, false>(m, un, s_a, s_c, s_logtab, kp.inv_c2, k0, srow, scol);
+      tile_flush(m, un, s0 + xs, do_u ? sD + us : nullptr, srow, scol);
+    }
+    first_task = 3;
+  }
+  // generic path: blocks in a fixed order (one code instance: keeps the I-cache small)
+  for (int task = first_task; task < 5; ++task) {
     int mode = kSymRowsOnly, n = 0;
     int64_t b0 = 0;
     double *rdst = s0 + xs, *cdst = nullptr;
@@ -506,6 +676,181 @@ p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end,
   }
 }
 
+// ---------------------------------------------------------------- persistent fast P2P
+// The same slot protocol as p2p_sym_kernel for the leaves whose whole near field is served
+// by this handle and fits the fast tile (self, +x and +y neighbour <= 96 points; distance
+// kernels).  One CTA per SM loops over its leaves (atomic counter); the next leaf's three
+// tiles are prefetched with cp.async while the current one is evaluated, the leaf's own
+// rows are accumulated in shared memory and every slot row is written exactly once (no
+// global read-modify-write): s0[X] = self + (+x rows) + (+y rows), sL[R] and sD[U] = the
+// neighbour columns, sL[X] / sD[X] = 0 on the domain boundary.
+struct P2PMeta {
+  int64_t xs, rs, us;
+  int m, rn, un;
+  int has_r, has_u, has_l, has_d;
+};
+
+__device__ __forceinline__ P2PMeta p2p_meta(int kappa, int64_t X, const int32_t* __restrict__ leaf_start) {
+  P2PMeta M{};
+  const uint32_t cx = p2p_compact((uint32_t)X), cy = p2p_compact((uint32_t)X >> 1);
+  const uint32_t side = 1u << kappa;
+  M.has_r = cx + 1 < side;
+  M.has_u = cy + 1 < side;
+  M.has_l = cx > 0;
+  M.has_d = cy > 0;
+  M.xs = leaf_start[X];
+  M.m = leaf_start[X + 1] - (int)M.xs;
+  if (M.has_r) {
+    const int64_t Rn = (int64_t)(p2p_spread(cx + 1) | (p2p_spread(cy) << 1));
+    M.rs = leaf_start[Rn];
+    M.rn = leaf_start[Rn + 1] - (int)M.rs;
+  }
+  if (M.has_u) {
+    const int64_t Un = (int64_t)(p2p_spread(cx) | (p2p_spread(cy + 1) << 1));
+    M.us = leaf_start[Un];
+    M.un = leaf_start[Un + 1] - (int)M.us;
+  }
+  return M;
+}
+
+__device__ __forceinline__ void p2p_prefetch(const P2PMeta& M, double (*T)[3 * kSymTile],
+                                             const double* __restrict__ px, const double* __restrict__ py,
+                                             const double* __restrict__ x) {
+  for (int e = threadIdx.x; e < 3 * kSymTile; e += blockDim.x) {
+    const int a = e / kSymTile, i = e - a * kSymTile;
+    const double* src = a == 0 ? px : a == 1 ? py : x;
+    if (i < M.m) cp_async8(&T[0][e], src + M.xs + i);
+    if (i < M.rn) cp_async8(&T[1][e], src + M.rs + i);
+    if (i < M.un) cp_async8(&T[2][e], src + M.us + i);
+  }
+}
+
+// tile_fast with the column sums reduced over the warp's two thread rows by a shuffle and
+// stored per warp: scol8[w][j].
+template <int KID, bool DIAG>
+__device__ __forceinline__ void tile_fast8(int mt, int nt, const double* __restrict__ sa,
+                                           const double* __restrict__ sb, const double2* __restrict__ tab,
+                                           double inv_c2, double k0, double* srow,
+                                           double (*scol8)[kSymTile + 1]) {
+  const int tid = threadIdx.x, ti = tid >> 4, tj = tid & 15;
+  const int A = (mt + 15) >> 4, B = (nt + 15) >> 4;
+  double cpx[kSymMaxB], cpy[kSymMaxB], cxv[kSymMaxB], cacc[kSymMaxB];
+#pragma unroll
+  for (int bb = 0; bb < kSymMaxB; ++bb) {
+    const int j = tj + 16 * bb;
+    const bool vj = j < nt;
+    cpx[bb] = vj ? sb[j] : 0.0;
+    cpy[bb] = vj ? sb[kSymTile + j] : 0.0;
+    cxv[bb] = vj ? sb[2 * kSymTile + j] : 0.0;
+    cacc[bb] = 0.0;
+  }
+  for (int aa = 0; aa < A; ++aa) {
+    const int i = ti + 16 * aa;
+    const bool vi = i < mt;
+    const double rpx = vi ? sa[i] : 0.0, rpy = vi ? sa[kSymTile + i] : 0.0;
+    const double rx = vi ? sa[2 * kSymTile + i] : 0.0;
+    double racc = 0.0;
+#pragma unroll
+    for (int bb = 0; bb < kSymMaxB; ++bb) {
+      if (bb < B) {
+        const double dx = rpx - cpx[bb], dy = rpy - cpy[bb];
+        double k = kfast<KID>(fma(dx, dx, dy * dy), tab, inv_c2);
+        if (DIAG) k = i < tj + 16 * bb ? k : 0.0;
+        racc = fma(k, cxv[bb], racc);
+        cacc[bb] = fma(k, rx, cacc[bb]);
+      }
+    }
+    if (DIAG && tj == 0) racc = fma(k0, rx, racc);
+    racc += __shfl_xor_sync(0xffffffffu, racc, 8);
+    racc += __shfl_xor_sync(0xffffffffu, racc, 4);
+    racc += __shfl_xor_sync(0xffffffffu, racc, 2);
+    racc += __shfl_xor_sync(0xffffffffu, racc, 1);
+    if (tj == 0 && vi) srow[i] = racc;
+  }
+  const int w = tid >> 5;
+#pragma unroll
+  for (int bb = 0; bb < kSymMaxB; ++bb) {
+    if (bb < B) {
+      const double v = cacc[bb] + __shfl_xor_sync(0xffffffffu, cacc[bb], 16);
+      if ((tid & 16) == 0) scol8[w][tj + 16 * bb] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ double colsum8(double (*scol8)[kSymTile + 1], int j) {
+  return ((scol8[0][j] + scol8[1][j]) + (scol8[2][j] + scol8[3][j])) +
+         ((scol8[4][j] + scol8[5][j]) + (scol8[6][j] + scol8[7][j]));
+}
+
+template <int KID>
+__global__ void __launch_bounds__(256, 3)
+p2p_fast_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int32_t* counter,
+                const int32_t* __restrict__ leaf_start, const double* __restrict__ px,
+                const double* __restrict__ py, const double* __restrict__ x, KernelParams kp,
+                double* __restrict__ s0, double* __restrict__ sL, double* __restrict__ sD) {
+  __shared__ double tiles[2][3][3 * kSymTile];   // [buffer][X, +x, +y][px | py | x]
+  __shared__ double acc[kSymTile], srow[kSymTile];
+  __shared__ double scol8[8][kSymTile + 1];
+  __shared__ double2 tab[128];
+  __shared__ int s_next;
+  const int tid = threadIdx.x;
+  const double k0 = KID == H2D_KERNEL_IMQ ? 1.0 : 0.0;
+  if (KID == H2D_KERNEL_LOG) hlog_table(tab);
+  if (tid == 0) s_next = atomicAdd(counter, 1);
+  __syncthreads();
+  int cur = s_next;
+  P2PMeta Mc{};
+  if (cur < n_leaves) {
+    Mc = p2p_meta(kappa, leaves[cur], leaf_start);
+    p2p_prefetch(Mc, tiles[0], px, py, x);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  int b = 0;
+  while (cur < n_leaves) {
+    __syncthreads();                      // s_next consumed, buffer b ^ 1 free
+    if (tid == 0) s_next = atomicAdd(counter, 1);
+    __syncthreads();
+    const int nxt = s_next;
+    P2PMeta Mn{};
+    if (nxt < n_leaves) {
+      Mn = p2p_meta(kappa, leaves[nxt], leaf_start);
+      p2p_prefetch(Mn, tiles[b ^ 1], px, py, x);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");   // this leaf's tiles have landed
+    __syncthreads();
+    const double* TX = tiles[b][0];
+    const int m = Mc.m;
+    // self block
+    tile_fast8<KID, true>(m, m, TX, TX, tab, kp.inv_c2, k0, srow, scol8);
+    __syncthreads();
+    if (tid < m) acc[tid] = srow[tid] + colsum8(scol8, tid);
+    __syncthreads();
+    if (Mc.has_r) {
+      tile_fast8<KID, false>(m, Mc.rn, TX, tiles[b][1], tab, kp.inv_c2, k0, srow, scol8);
+      __syncthreads();
+      if (tid < m) acc[tid] += srow[tid];
+      if (tid < Mc.rn) sL[Mc.rs + tid] = colsum8(scol8, tid);
+      __syncthreads();
+    }
+    if (Mc.has_u) {
+      tile_fast8<KID, false>(m, Mc.un, TX, tiles[b][2], tab, kp.inv_c2, k0, srow, scol8);
+      __syncthreads();
+      if (tid < m) acc[tid] += srow[tid];
+      if (tid < Mc.un) sD[Mc.us + tid] = colsum8(scol8, tid);
+    }
+    if (tid < m) {
+      s0[Mc.xs + tid] = acc[tid];
+      if (!Mc.has_l) sL[Mc.xs + tid] = 0.0;
+      if (!Mc.has_d) sD[Mc.xs + tid] = 0.0;
+    }
+    Mc = Mn;
+    cur = nxt;
+    b ^= 1;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- stage B: yfar = U t
 // Item = rows [r0, r0 + rows) (rows <= 256) of served leaf L.  For every ancestor level l
 // the leaf's U columns form one contiguous column-major range (stride mLp); a stage holds
@@ -514,48 +859,53 @@ p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end,
 // (g, i) = (tid / rows, tid % rows) owns row i and columns g, g + G, ... (G = 256 / rows),
 // reduced in smem at the end of the item: one yfar write per row, no atomics.
 // Stage header: a = rows, b = rowsp (row stride inside the stage), c = output row.
-__device__ void stageB_producer(PipeSmem& S, const BItem* __restrict__ items, int n_items,
-                                int32_t* counter, int kappa, int64_t leaf_begin, int64_t row_begin,
-                                const int32_t* __restrict__ leaf_start, const LevelPtrs& lp) {
+template <int NS>
+__device__ void stageB_producer(PipeSmem<NS>& S, const BItem* __restrict__ items,
+                                const BLevel* __restrict__ blev, int n_items, int32_t* counter,
+                                int kappa, const LevelPtrs& lp) {
   const int lane = threadIdx.x & 31;
   const uint64_t pol = l2_evict_first_policy();
   int stage = 0;
   uint32_t phase = 0;
+  // one-item lookahead (index + descriptor + per-level metadata in flight, see stage A)
+  int idx = 0, nidx = 0;
+  if (lane == 0) idx = atomicAdd(counter, 1);
+  idx = __shfl_sync(0xffffffffu, idx, 0);
+  if (lane == 0) nidx = atomicAdd(counter, 1);
+  BItem nit{};
+  BLevel nlv{0, 0, 0};
+  if (idx < n_items) {
+    nit = items[idx];
+    if (lane < kappa) nlv = blev[(int64_t)idx * kappa + lane];
+  }
   for (;;) {
-    int idx = 0;
-    if (lane == 0) idx = atomicAdd(counter, 1);
-    idx = __shfl_sync(0xffffffffu, idx, 0);
     const bool done = idx >= n_items;
-    BItem it{};
-    int64_t s0 = 0;
-    int mL = 0;
-    if (!done) {
-      it = items[idx];
-      s0 = leaf_start[it.leaf];
-      mL = leaf_start[it.leaf + 1] - (int)s0;
+    const BItem it = nit;
+    const BLevel lv = nlv;
+    const int cur = idx;
+    idx = __shfl_sync(0xffffffffu, nidx, 0);
+    if (!done && lane == 0) nidx = atomicAdd(counter, 1);
+    if (!done && idx < n_items) {
+      nit = items[idx];
+      if (lane < kappa) nlv = blev[(int64_t)idx * kappa + lane];
     }
+    const int mL = it.mL;
     const int mLp = (mL + 1) & ~1, rowsp = (it.rows + 1) & ~1;
     const bool whole = !done && it.rows == mL;
     // per-level metadata, lane l - 1 <-> level l
-    int R = 0, cb = 0;
-    int64_t ub = 0;
-    if (!done && lane < kappa) {
-      const int l = lane + 1;
-      const int64_t X = (int64_t)it.leaf >> (2 * (kappa - l));
-      cb = lp.ucolbase[l][X];
-      R = lp.ucolbase[l][X + 1] - cb;
-      ub = lp.uoff[l][it.leaf - leaf_begin];
-    }
+    const int R = done || lane >= kappa ? 0 : lv.R;
+    const int cb = lv.tcol;
+    const int64_t ub = lv.uoff;
     const unsigned nz = __ballot_sync(0xffffffffu, R > 0);
     const int lastl = nz ? 32 - __clz(nz) : 0;
-    const int yrow = (int)(s0 + it.r0 - row_begin);
+    const int yrow = it.yrow;
     if (done || nz == 0) {
       // terminator, or an item without low-rank columns (kappa = 0 / zero ranks): one
       // empty stage so the consumers still write the item's rows
       mbar_wait(&S.empty[stage], phase ^ 1);
       if (lane == 0) {
         StageHdr& h = S.hdr[stage];
-        h.item = done ? -1 : idx;
+        h.item = done ? -1 : cur;
         h.cnt = 0;
         h.flags = kFirst | kLast;
         h.a = it.rows;
@@ -564,7 +914,7 @@ __device__ void stageB_producer(PipeSmem& S, const BItem* __restrict__ items, in
         mbar_arrive_expect_tx(&S.full[stage], 0);
       }
       cp_async_arrive_noinc(&S.full[stage]);
-      if (++stage == kNS) { stage = 0; phase ^= 1; }
+      if (++stage == NS) { stage = 0; phase ^= 1; }
       if (done) break;
       continue;
     }
@@ -583,7 +933,7 @@ __device__ void stageB_producer(PipeSmem& S, const BItem* __restrict__ items, in
         mbar_wait(&S.empty[stage], phase ^ 1);
         if (lane == 0) {
           StageHdr& h = S.hdr[stage];
-          h.item = idx;
+          h.item = cur;
           h.cnt = cols;
           h.flags = (first ? kFirst : 0) | (last ? kLast : 0);
           h.a = it.rows;
@@ -600,19 +950,23 @@ __device__ void stageB_producer(PipeSmem& S, const BItem* __restrict__ items, in
                      (uint32_t)rowsp * 8u, &S.full[stage], pol);
         for (int c = lane; c < cols; c += 32) cp_async8(&S.vec[stage][c], tb + c0 + c);
         cp_async_arrive_noinc(&S.full[stage]);
-        if (++stage == kNS) { stage = 0; phase ^= 1; }
+        if (++stage == NS) { stage = 0; phase ^= 1; }
         first = false;
       }
     }
   }
 }
 
-__device__ void stageB_consumers(PipeSmem& S, double* __restrict__ yfar) {
+// Consumers work on row pairs (one 16-byte smem load = rows 2i, 2i+1 of a column; rowsp is
+// even and the padding row is zero): thread (g, i) = (tid / RP, tid % RP), RP = rowsp / 2,
+// owns row pair i and columns g, g + G, ... (G = kCons / RP), reduced in smem per item.
+template <int NS>
+__device__ void stageB_consumers(PipeSmem<NS>& S, double* __restrict__ yfar) {
   const int tid = threadIdx.x, lane = tid & 31;
   int stage = 0;
   uint32_t phase = 0;
-  int rows = 1, rowsp = 2, G = 1, g = 0, i = 0;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int rows = 1, rowsp = 2, G = 1, g = 0, i = 0, RP = 1;
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
   for (;;) {
     mbar_wait(&S.full[stage], phase);
     const StageHdr h = S.hdr[stage];
@@ -620,49 +974,58 @@ __device__ void stageB_consumers(PipeSmem& S, double* __restrict__ yfar) {
     if (h.flags & kFirst) {
       rows = h.a;
       rowsp = h.b;
-      G = kCons / rows;
-      g = tid / rows;
-      i = tid - g * rows;
-      a0 = a1 = a2 = a3 = 0.0;
+      RP = rowsp >> 1;
+      G = kCons / RP;
+      g = tid / RP;
+      i = tid - g * RP;
+      a0 = a1 = b0 = b1 = 0.0;
     }
     if (g < G) {
-      const double* __restrict__ p = S.ring[stage] + i;
+      const double* __restrict__ u = S.ring[stage] + (size_t)g * rowsp + 2 * i;
       const double* __restrict__ tv = S.vec[stage];
-      const int cols = h.cnt;
+      const int cols = h.cnt, step = G * rowsp;
       int c = g;
-      for (; c + 3 * G < cols; c += 4 * G) {
-        const double u0 = p[c * rowsp], u1 = p[(c + G) * rowsp], u2 = p[(c + 2 * G) * rowsp],
-                     u3 = p[(c + 3 * G) * rowsp];
-        a0 = fma(u0, tv[c], a0);
-        a1 = fma(u1, tv[c + G], a1);
-        a2 = fma(u2, tv[c + 2 * G], a2);
-        a3 = fma(u3, tv[c + 3 * G], a3);
+      for (; c + G < cols; c += 2 * G, u += 2 * step) {
+        const double2 ua = *reinterpret_cast<const double2*>(u);
+        const double2 ub = *reinterpret_cast<const double2*>(u + step);
+        const double ta = tv[c], tb = tv[c + G];
+        a0 = fma(ua.x, ta, a0);
+        a1 = fma(ua.y, ta, a1);
+        b0 = fma(ub.x, tb, b0);
+        b1 = fma(ub.y, tb, b1);
       }
-      for (; c < cols; c += G) a0 = fma(p[c * rowsp], tv[c], a0);
+      if (c < cols) {
+        const double2 ua = *reinterpret_cast<const double2*>(u);
+        const double ta = tv[c];
+        a0 = fma(ua.x, ta, a0);
+        a1 = fma(ua.y, ta, a1);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.empty[stage]);
-    if (++stage == kNS) { stage = 0; phase ^= 1; }
+    if (++stage == NS) { stage = 0; phase ^= 1; }
     if (!(h.flags & kLast)) continue;
-    S.red[tid] = g < G ? (a0 + a1) + (a2 + a3) : 0.0;
+    S.red[2 * tid] = g < G ? a0 + b0 : 0.0;
+    S.red[2 * tid + 1] = g < G ? a1 + b1 : 0.0;
     named_bar_sync(1, kCons);
     if (tid < rows) {
+      const int ip = tid >> 1, e = tid & 1;
       double u = 0.0;
-      for (int gg = 0; gg < G; ++gg) u += S.red[tid + gg * rows];
+      for (int gg = 0; gg < G; ++gg) u += S.red[2 * (ip + gg * RP) + e];
       yfar[h.c + tid] = u;
     }
     named_bar_sync(1, kCons);
   }
 }
 
+template <int NS>
 __global__ void __launch_bounds__(kPipeThreads, 3)
-stageB_tma_kernel(const BItem* __restrict__ items, int n_items, int32_t* counter, int kappa,
-                  int64_t leaf_begin, int64_t row_begin, const int32_t* __restrict__ leaf_start,
-                  LevelPtrs lp, double* __restrict__ yfar) {
+stageB_tma_kernel(const BItem* __restrict__ items, const BLevel* __restrict__ blev, int n_items,
+                  int32_t* counter, int kappa, LevelPtrs lp, double* __restrict__ yfar) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  PipeSmem& S = *reinterpret_cast<PipeSmem*>(smem_raw);
+  PipeSmem<NS>& S = *reinterpret_cast<PipeSmem<NS>*>(smem_raw);
   pipe_init(S);
-  if (threadIdx.x >= kCons) stageB_producer(S, items, n_items, counter, kappa, leaf_begin, row_begin, leaf_start, lp);
+  if (threadIdx.x >= kCons) stageB_producer(S, items, blev, n_items, counter, kappa, lp);
   else stageB_consumers(S, yfar);
 }
 
@@ -850,11 +1213,24 @@ void unpack_block(Handle& h, int l, int64_t e, int* m, int* n, int* r, double* U
   }
 }
 
+template <int NS>
+static void set_pipe_attrs() {
+  const int smem = (int)sizeof(PipeSmem<NS>);
+  H2D_CUDA(cudaFuncSetAttribute(stageA_tma_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  H2D_CUDA(cudaFuncSetAttribute(stageB_tma_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  H2D_CUDA(cudaFuncSetAttribute(stageA_tma_kernel<NS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                cudaSharedmemCarveoutMaxShared));
+  H2D_CUDA(cudaFuncSetAttribute(stageB_tma_kernel<NS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                cudaSharedmemCarveoutMaxShared));
+}
+
 // Build the stage-A / reduce schedule, the t layout (U-column order), the stage-B items
 // and the per-level device tables.
 void finalize_schedule(Handle& h) {
   cudaStream_t s = h.stream;
   int64_t t_len = 0, tpart_len = 0;
+  const char* env_at = getenv("H2D_A_TARGET");    // diagnostics: stage-A item size (elements)
+  const int64_t kATarget = env_at && atoll(env_at) >= 2048 ? atoll(env_at) : kATargetDefault;
   std::vector<AItem> aitems;
   std::vector<RItem> ritems;
   for (int l = 1; l <= h.kappa; ++l) {
@@ -932,11 +1308,13 @@ void finalize_schedule(Handle& h) {
   std::stable_sort(aitems.begin(), aitems.end(), [](const AItem& a, const AItem& b) {
     return (int64_t)a.nrows * a.Rp > (int64_t)b.nrows * b.Rp;
   });
-  // stage-B items: served leaves in row blocks of <= kBRows rows, largest cost first
+  // stage-B items: served leaves in row blocks of <= kBRows rows, largest cost first, with
+  // the per-level metadata of each item precomputed (one dependent load in the producer)
   std::vector<BItem> bitems;
-  std::vector<int64_t> bcost;
+  std::vector<int64_t> bcost, bleaf;
   for (int64_t lf = h.leaf_begin; lf < h.leaf_end; ++lf) {
-    const int32_t mL = h.leaf_start[(size_t)lf + 1] - h.leaf_start[(size_t)lf];
+    const int32_t s0 = h.leaf_start[(size_t)lf];
+    const int32_t mL = h.leaf_start[(size_t)lf + 1] - s0;
     int64_t RL = 0;
     for (int l = 1; l <= h.kappa; ++l) {
       const Level& L = h.levels[(size_t)l];
@@ -945,16 +1323,77 @@ void finalize_schedule(Handle& h) {
     }
     for (int32_t r0 = 0; r0 < mL; r0 += kBRows) {
       const int32_t rows = std::min(kBRows, mL - r0);
-      bitems.push_back(BItem{(int32_t)lf, r0, rows, 0});
+      bitems.push_back(BItem{r0, rows, mL, (int32_t)(s0 + r0 - h.row_begin)});
       bcost.push_back((int64_t)((rows + 1) & ~1) * RL + 512);
+      bleaf.push_back(lf);
     }
   }
   std::vector<size_t> ord(bitems.size());
   std::iota(ord.begin(), ord.end(), 0);
   std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return bcost[a] > bcost[b]; });
   std::vector<BItem> bsorted;
+  std::vector<BLevel> blev;
   bsorted.reserve(bitems.size());
-  for (size_t k : ord) bsorted.push_back(bitems[k]);
+  blev.reserve(bitems.size() * (size_t)std::max(1, h.kappa));
+  for (size_t k : ord) {
+    bsorted.push_back(bitems[k]);
+    const int64_t lf = bleaf[k];
+    for (int l = 1; l <= h.kappa; ++l) {
+      const Level& L = h.levels[(size_t)l];
+      const int64_t X = lf >> (2 * (h.kappa - l));
+      blev.push_back(BLevel{L.uoff[(size_t)(lf - h.leaf_begin)], L.ucolbase[(size_t)X],
+                            L.ucolbase[(size_t)X + 1] - L.ucolbase[(size_t)X]});
+    }
+  }
+  // near-field P2P: leaves the persistent fast kernel handles (whole near field served, all
+  // three tiles <= kSymTile points, distance kernel) and the rest (generic kernel)
+  {
+    auto compact = [](uint32_t v) {
+      v &= 0x55555555u;
+      v = (v | (v >> 1)) & 0x33333333u;
+      v = (v | (v >> 2)) & 0x0F0F0F0Fu;
+      v = (v | (v >> 4)) & 0x00FF00FFu;
+      v = (v | (v >> 8)) & 0x0000FFFFu;
+      return v;
+    };
+    auto spread = [](uint32_t v) {
+      v &= 0xFFFFu;
+      v = (v | (v << 8)) & 0x00FF00FFu;
+      v = (v | (v << 4)) & 0x0F0F0F0Fu;
+      v = (v | (v << 2)) & 0x33333333u;
+      v = (v | (v << 1)) & 0x55555555u;
+      return v;
+    };
+    const bool dist = h.kp.id == H2D_KERNEL_LOG || h.kp.id == H2D_KERNEL_IMQ || h.kp.id == H2D_KERNEL_ONE_OVER_R;
+    const uint32_t side = 1u << h.kappa;
+    auto size_of = [&](int64_t lf) { return h.leaf_start[(size_t)lf + 1] - h.leaf_start[(size_t)lf]; };
+    auto served = [&](int64_t lf) { return lf >= h.leaf_begin && lf < h.leaf_end; };
+    std::vector<int32_t> fast, gen;
+    for (int64_t lf = h.leaf_begin; lf < h.leaf_end; ++lf) {
+      const uint32_t cx = compact((uint32_t)lf), cy = compact((uint32_t)lf >> 1);
+      bool ok = dist && size_of(lf) <= kSymTile;
+      auto nb = [&](bool exists, uint32_t nx, uint32_t ny, bool check_size) {
+        if (!exists) return;
+        const int64_t Y = (int64_t)(spread(nx) | (spread(ny) << 1));
+        ok = ok && served(Y) && (!check_size || size_of(Y) <= kSymTile);
+      };
+      nb(cx + 1 < side, cx + 1, cy, true);
+      nb(cy + 1 < side, cx, cy + 1, true);
+      nb(cx > 0, cx - 1, cy, false);
+      nb(cy > 0, cx, cy - 1, false);
+      (ok ? fast : gen).push_back((int32_t)lf);
+    }
+    h.n_p2p_fast = (int64_t)fast.size();
+    h.n_p2p_gen = (int64_t)gen.size();
+    h.release(h.d_p2p_fast);
+    h.release(h.d_p2p_gen);
+    h.d_p2p_fast = h.alloc<int32_t>(fast.size());
+    h.d_p2p_gen = h.alloc<int32_t>(gen.size());
+    if (!fast.empty())
+      H2D_CUDA(cudaMemcpyAsync(h.d_p2p_fast, fast.data(), fast.size() * 4, cudaMemcpyHostToDevice, s));
+    if (!gen.empty())
+      H2D_CUDA(cudaMemcpyAsync(h.d_p2p_gen, gen.data(), gen.size() * 4, cudaMemcpyHostToDevice, s));
+  }
   h.tpart_len = tpart_len;
   h.d_tpart = h.alloc<double>(tpart_len);
   h.n_aitems = (int64_t)aitems.size();
@@ -964,6 +1403,9 @@ void finalize_schedule(Handle& h) {
   h.d_ritems = h.alloc<RItem>(ritems.size());
   h.d_rcount = h.alloc<int32_t>(ritems.size());
   h.d_bitems = h.alloc<BItem>(bsorted.size());
+  h.d_blev = h.alloc<BLevel>(blev.size());
+  if (!blev.empty())
+    H2D_CUDA(cudaMemcpyAsync(h.d_blev, blev.data(), blev.size() * sizeof(BLevel), cudaMemcpyHostToDevice, s));
   H2D_CUDA(cudaMemsetAsync(h.d_rcount, 0, std::max<size_t>(1, ritems.size()) * sizeof(int32_t), s));
   if (!aitems.empty())
     H2D_CUDA(cudaMemcpyAsync(h.d_aitems, aitems.data(), aitems.size() * sizeof(AItem),
@@ -976,30 +1418,34 @@ void finalize_schedule(Handle& h) {
                              cudaMemcpyHostToDevice, s));
   if (!h.d_ynear) h.d_ynear = h.alloc<double>(3 * h.n);   // three P2P slots (p2p_sym_kernel)
   if (!h.d_yfar) h.d_yfar = h.alloc<double>(std::max<int64_t>(1, h.row_end - h.row_begin));
-  if (!h.d_counters) h.d_counters = h.alloc<int32_t>(2);
+  if (!h.d_counters) h.d_counters = h.alloc<int32_t>(3);
   if (!h.hi_stream) {
     int sm = 0, lo_prio = 0, hi_prio = 0;
     H2D_CUDA(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, h.device));
-    h.persist_ctas = 2 * sm;
     H2D_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
     H2D_CUDA(cudaStreamCreateWithPriority(&h.hi_stream, cudaStreamNonBlocking, hi_prio));
     H2D_CUDA(cudaStreamCreateWithPriority(&h.aux_stream, cudaStreamNonBlocking, lo_prio));
     H2D_CUDA(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
     H2D_CUDA(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
     H2D_CUDA(cudaEventCreateWithFlags(&h.ev_far, cudaEventDisableTiming));
-    const int smem = (int)sizeof(PipeSmem);
-    H2D_CUDA(cudaFuncSetAttribute(stageA_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    H2D_CUDA(cudaFuncSetAttribute(stageB_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    H2D_CUDA(cudaFuncSetAttribute(stageA_tma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                  cudaSharedmemCarveoutMaxShared));
-    H2D_CUDA(cudaFuncSetAttribute(stageB_tma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                  cudaSharedmemCarveoutMaxShared));
-    for (auto* f : {p2p_sym_kernel<H2D_KERNEL_LOG>, p2p_sym_kernel<H2D_KERNEL_IMQ>,
-                    p2p_sym_kernel<H2D_KERNEL_ONE_OVER_R>, p2p_sym_kernel<H2D_KERNEL_TEST_LOWRANK>})
+    // pipeline shape: 2 CTAs/SM with a 5-stage ring, or 1 CTA/SM with a 9-stage ring
+    // (leaves room for two P2P CTAs per SM); H2D_PIPE_CTAS_PER_SM overrides the default.
+    const char* env = getenv("H2D_PIPE_CTAS_PER_SM");
+    const int per_sm = env && atoi(env) == 2 ? 2 : env && atoi(env) == 1 ? 1 : kDefaultCtasPerSm;
+    h.pipe_ns = per_sm == 2 ? kNSShallow : kNSDeep;
+    h.persist_ctas = per_sm * sm;
+    set_pipe_attrs<kNSShallow>();
+    set_pipe_attrs<kNSDeep>();
+    for (const void* f : {(const void*)p2p_sym_kernel<H2D_KERNEL_LOG>, (const void*)p2p_sym_kernel<H2D_KERNEL_IMQ>,
+                          (const void*)p2p_sym_kernel<H2D_KERNEL_ONE_OVER_R>,
+                          (const void*)p2p_sym_kernel<H2D_KERNEL_TEST_LOWRANK>,
+                          (const void*)p2p_fast_kernel<H2D_KERNEL_LOG>, (const void*)p2p_fast_kernel<H2D_KERNEL_IMQ>,
+                          (const void*)p2p_fast_kernel<H2D_KERNEL_ONE_OVER_R>})
       H2D_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                     cudaSharedmemCarveoutMaxShared));
+    h.num_sms = sm;
   }
-  H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 2 * sizeof(int32_t), s));
+  H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 3 * sizeof(int32_t), s));
   H2D_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -1029,45 +1475,70 @@ void begin_matvec_timing(Handle& h) {
 
 void mark_after_input(Handle& h) { record(h, 1, h.stream); }
 
-// Matvec on TREE-order x (S7-S9).  Stages A and B (HBM-bound) run on the high-priority
-// stream, the near-field P2P (FP64-bound) concurrently on the low-priority stream; the
-// combine epilogue on the caller's stream joins them.
-void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, int64_t y_row0) {
-  cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
-  const int64_t nleaves = h.leaf_end - h.leaf_begin;
-  H2D_CUDA(cudaEventRecord(h.ev_fork, s));
-  H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_fork, 0));
-  H2D_CUDA(cudaStreamWaitEvent(a, h.ev_fork, 0));
-  const size_t smem = sizeof(PipeSmem);
-  H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 2 * sizeof(int32_t), hi));
+template <int NS>
+static void launch_stages(Handle& h, const double* d_xtree, cudaStream_t hi) {
+  const size_t smem = sizeof(PipeSmem<NS>);
   if (h.n_aitems > 0) {
-    stageA_tma_kernel<<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+    stageA_tma_kernel<NS><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
         h.d_aitems, (int)h.n_aitems, h.d_counters, h.lp, d_xtree, h.d_vdst, h.d_t, h.d_tpart,
         h.d_ritems, h.d_rcount);
     H2D_LAUNCH_CHECK();
   }
   record(h, 2, hi);
   if (h.n_bitems > 0) {
-    stageB_tma_kernel<<<h.persist_ctas, kPipeThreads, smem, hi>>>(
-        h.d_bitems, (int)h.n_bitems, h.d_counters + 1, h.kappa, h.leaf_begin, h.row_begin,
-        h.d_leaf_start, h.lp, h.d_yfar);
+    stageB_tma_kernel<NS><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+        h.d_bitems, h.d_blev, (int)h.n_bitems, h.d_counters + 1, h.kappa, h.lp, h.d_yfar);
     H2D_LAUNCH_CHECK();
   }
+}
+
+// Matvec on TREE-order x (S7-S9).  Stages A and B (HBM-bound) run on the high-priority
+// stream, the near-field P2P (FP64-bound) concurrently on the low-priority stream; the
+// combine epilogue on the caller's stream joins them.
+void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, int64_t y_row0) {
+  cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
+  const int64_t nleaves = h.leaf_end - h.leaf_begin;
+  // H2D_P2P_SERIAL=1 (diagnostics only): the P2P runs alone, before stage A
+  static const bool p2p_serial = getenv("H2D_P2P_SERIAL") && atoi(getenv("H2D_P2P_SERIAL")) == 1;
+  H2D_CUDA(cudaEventRecord(h.ev_fork, s));
+  H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_fork, 0));
+  H2D_CUDA(cudaStreamWaitEvent(a, h.ev_fork, 0));
+  auto p2p = [&]() {
+    record(h, 6, a);
+    if (h.n_p2p_gen > 0) {
+      auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_sym_kernel<H2D_KERNEL_LOG>
+                : h.kp.id == H2D_KERNEL_IMQ ? p2p_sym_kernel<H2D_KERNEL_IMQ>
+                : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_sym_kernel<H2D_KERNEL_ONE_OVER_R>
+                                                   : p2p_sym_kernel<H2D_KERNEL_TEST_LOWRANK>;
+      kfn<<<(int)h.n_p2p_gen, 256, 0, a>>>(h.kappa, h.leaf_begin, h.leaf_end, h.d_p2p_gen,
+                                           h.d_leaf_start, h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear,
+                                           h.d_ynear + h.n, h.d_ynear + 2 * h.n);
+      H2D_LAUNCH_CHECK();
+    }
+    if (h.n_p2p_fast > 0) {
+      auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_fast_kernel<H2D_KERNEL_LOG>
+                : h.kp.id == H2D_KERNEL_IMQ ? p2p_fast_kernel<H2D_KERNEL_IMQ>
+                                            : p2p_fast_kernel<H2D_KERNEL_ONE_OVER_R>;
+      H2D_CUDA(cudaMemsetAsync(h.d_counters + 2, 0, sizeof(int32_t), a));
+      const int grid = (int)std::min<int64_t>(h.num_sms, h.n_p2p_fast);
+      kfn<<<grid, 256, 0, a>>>(h.kappa, h.d_p2p_fast, (int)h.n_p2p_fast, h.d_counters + 2,
+                               h.d_leaf_start, h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear,
+                               h.d_ynear + h.n, h.d_ynear + 2 * h.n);
+      H2D_LAUNCH_CHECK();
+    }
+    record(h, 7, a);
+    H2D_CUDA(cudaEventRecord(h.ev_join, a));
+  };
+  if (p2p_serial) {
+    p2p();
+    H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_join, 0));
+  }
+  H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 2 * sizeof(int32_t), hi));
+  if (h.pipe_ns == kNSShallow) launch_stages<kNSShallow>(h, d_xtree, hi);
+  else launch_stages<kNSDeep>(h, d_xtree, hi);
   record(h, 3, hi);
   H2D_CUDA(cudaEventRecord(h.ev_far, hi));
-  record(h, 6, a);
-  if (nleaves > 0) {
-    auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_sym_kernel<H2D_KERNEL_LOG>
-              : h.kp.id == H2D_KERNEL_IMQ ? p2p_sym_kernel<H2D_KERNEL_IMQ>
-              : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_sym_kernel<H2D_KERNEL_ONE_OVER_R>
-                                                 : p2p_sym_kernel<H2D_KERNEL_TEST_LOWRANK>;
-    kfn<<<(int)nleaves, 256, 0, a>>>(h.kappa, h.leaf_begin, h.leaf_end, h.d_leaf_start, h.d_px,
-                                     h.d_py, d_xtree, h.kp, h.d_ynear, h.d_ynear + h.n,
-                                     h.d_ynear + 2 * h.n);
-    H2D_LAUNCH_CHECK();
-  }
-  record(h, 7, a);
-  H2D_CUDA(cudaEventRecord(h.ev_join, a));
+  if (!p2p_serial) p2p();   // after stage A's launch: its CTAs are placed first
   H2D_CUDA(cudaStreamWaitEvent(s, h.ev_far, 0));
   H2D_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
   record(h, 4, s);

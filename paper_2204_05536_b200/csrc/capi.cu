@@ -69,6 +69,7 @@ static void clear_factors(Handle& h) {
     h.release(L.d_uoff); L.d_uoff = nullptr;
   }
   h.release(h.d_bitems); h.d_bitems = nullptr;
+  h.release(h.d_blev); h.d_blev = nullptr;
   h.n_bitems = 0;
   h.release(h.d_aitems); h.d_aitems = nullptr;
   h.release(h.d_ritems); h.d_ritems = nullptr;

@@ -127,12 +127,19 @@ struct AItem {
   int32_t ritem;   // >= 0: multi-chunk box (RItem index); the last chunk CTA reduces
   int32_t Rp;      // row stride of the panel (R rounded up to even)
 };
-// Stage-B work item: rows [r0, r0 + rows) (rows <= 256) of served leaf `leaf`.
+// Stage-B work item: rows [r0, r0 + rows) (rows <= 224) of a served leaf of mL points whose
+// first output row is yrow (index into the served rows); its per-level metadata is
+// BLevel[item * kappa + l - 1].
 struct BItem {
-  int32_t leaf;
   int32_t r0;
   int32_t rows;
-  int32_t pad;
+  int32_t mL;
+  int32_t yrow;
+};
+struct BLevel {
+  int64_t uoff;    // leaf-panel offset inside the level's U array
+  int32_t tcol;    // first t entry of the level-l ancestor box (U-column order)
+  int32_t R;       // U columns of that box
 };
 // Reduction of multi-chunk partials: t[vdst[vpos + q]] = sum_c part[p_off + c*R + q]
 struct RItem {
@@ -193,9 +200,15 @@ struct Handle {
   int rmax_panel = 1;                     // widest per-leaf t gather (smem of stage B)
   int max_ritem_R = 1;
   BItem* d_bitems = nullptr;              // stage-B items, largest first
+  BLevel* d_blev = nullptr;               // [n_bitems * kappa]
   int64_t n_bitems = 0;
   int32_t* d_counters = nullptr;          // [2] dynamic work counters of stage A / B
   int persist_ctas = 0;                   // CTAs of the persistent stage-A/B kernels
+  int pipe_ns = 0;                        // their ring depth (template instance)
+  int num_sms = 0;
+  int32_t* d_p2p_fast = nullptr;          // leaves of the persistent fast P2P kernel
+  int32_t* d_p2p_gen = nullptr;           // leaves of the generic P2P kernel
+  int64_t n_p2p_fast = 0, n_p2p_gen = 0;
   double* d_ynear = nullptr;              // [3n] near-field P2P slots (p2p_sym_kernel)
   double* d_yfar = nullptr;               // [served] low-rank part (stage B output)
   cudaStream_t hi_stream = nullptr;       // stages A, B (high priority)
