@@ -288,7 +288,7 @@ def run_ours(args, cfg):
     clk_mhz = None
     roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
             "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-            "traffic": None, "bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4),
+            "traffic": ncu_traffic(args.config, dom), "bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4),
             "other_hbm_kernel": {"kernel": other, "ms_per_launch": round(per[other], 4),
                                  "bytes_per_launch": other_bytes,
                                  "frac": round(other_bytes / (per[other] * 1e-3) / 1e9 / peak, 4)},
@@ -314,18 +314,31 @@ def run_ours(args, cfg):
         e2e = {"value": 1e3 * ke / e0.elapsed_time(e1), "unit": "matvecs/s",
                "h2d_bytes_per_step": 8 * cfg.n, "d2h_bytes_per_step": 8 * cfg.n}
 
-    # near-field P2P against the FP64 pipe: pairs x FP64-pipe instructions per pair (from
-    # the kernel's SASS) / (148 SMs x 64 FP64 lanes x SM clock)
+    # near-field P2P against the FP64 pipe.  The symmetric kernel evaluates every unordered
+    # leaf pair once: (near_pairs + N) / 2 kernel evaluations, each P2P_FP64_OPS_PER_EVAL
+    # FP64-pipe instructions (counted in the SASS of p2p_fast_kernel).  In the
+    # timed matvec it runs concurrently with stages A/B on the spare SM resources, so its
+    # FP64 fraction is also probed standalone (H2D_P2P_SERIAL=1, diagnostics path).
     csum = clk.summary()
     p2p_ms = per["p2p_near"]
-    ops_pair = P2P_FP64_OPS_PER_PAIR.get(cfg.kernel)
+    ops_eval = P2P_FP64_OPS_PER_EVAL.get(cfg.kernel)
     sm_hz = (csum["sm_mhz"] or 1965.0) * 1e6
-    p2p = {"pairs": int(inf["p2p_pairs"]), "ms_per_launch": round(p2p_ms, 4),
-           "pairs_per_s": inf["p2p_pairs"] / (p2p_ms * 1e-3) if p2p_ms > 0 else None,
-           "fp64_ops_per_pair": ops_pair, "peak_lane_ops_per_s": 148 * 64 * sm_hz,
-           "frac_fp64_pipe": (inf["p2p_pairs"] * ops_pair / (p2p_ms * 1e-3) / (148 * 64 * sm_hz))
-           if (p2p_ms > 0 and ops_pair) else None,
-           "overlapped_with": "stageA_VTx (second stream)"}
+    served = inf["row_end"] - inf["row_begin"]
+    evals = (inf["p2p_pairs"] + served) / 2.0
+    alone_ms = p2p_standalone_ms(op, step, args) if world == 1 else None
+    peak_ops = 148 * 64 * sm_hz
+
+    def frac(ms):
+        return evals * ops_eval / (ms * 1e-3) / peak_ops if (ms and ops_eval) else None
+
+    p2p = {"directed_pairs": int(inf["p2p_pairs"]), "evaluations": int(evals),
+           "ms_per_launch_concurrent": round(p2p_ms, 4),
+           "ms_per_launch_standalone": round(alone_ms, 4) if alone_ms else None,
+           "fp64_ops_per_eval": ops_eval, "peak_fp64_lane_ops_per_s": peak_ops,
+           "frac_fp64_pipe_standalone": frac(alone_ms),
+           "frac_fp64_pipe_concurrent": frac(p2p_ms),
+           "overlapped_with": "stageA_VTx + stageB_Ut (low-priority stream, co-resident CTAs)",
+           "exposed_ms": round(per["p2p_join_wait"], 4)}
     roof["p2p"] = p2p
     if rank == 0:
         line = {
@@ -354,13 +367,42 @@ def run_ours(args, cfg):
 
 
 def launches_per_matvec(inf, world):
-    # permute-in (1-GPU ORIGINAL order) or unpad (gathered), P2P, stage A, t-reduce, stage B
-    return 5
+    # permute-in (1-GPU ORIGINAL order) or unpad (gathered), stage A, stage B, P2P (fast
+    # persistent kernel, + generic kernel when some leaves need it), combine
+    return 5 + (1 if inf.get("p2p_generic_leaves", 0) else 0)
 
 
-# FP64-pipe instructions per near-field pair in p2p_kernel's inner loop, counted from
-# `cuobjdump -sass` of libhodlr2d.so; keyed by kernel id.
-P2P_FP64_OPS_PER_PAIR = {0: 35, 1: 11, 2: 11}
+# FP64-pipe instructions per kernel evaluation in p2p_fast_kernel's unrolled tile loop,
+# counted from `cuobjdump -sass` of libhodlr2d.so; keyed by kernel id.
+# log: 2 DADD + 1 DMUL + 12 DFMA + 1 DSETP + 1 I2F.F64; IMQ / 1/r: distance + rsqrt
+# (MUFU.RSQ64H seed + Newton) + 2 accumulations.
+P2P_FP64_OPS_PER_EVAL = {0: 17, 1: 12, 2: 12}
+
+
+def p2p_standalone_ms(op, step, args, n=10):
+    """P2P time with the kernel running alone (H2D_P2P_SERIAL=1), CUDA events of the library."""
+    os.environ["H2D_P2P_SERIAL"] = "1"
+    try:
+        op.set_timing(True)
+        op.stage_times(reset=True)
+        for k in range(n):
+            step(k)
+        st, cnt = op.stage_times(reset=True)
+        return st["p2p_near"] / max(cnt, 1)
+    finally:
+        op.set_timing(False)
+        os.environ["H2D_P2P_SERIAL"] = "0"
+
+
+def ncu_traffic(cfg_name, kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu --set full
+    capture of this config (profiles/ncu_traffic.json, written by tools/ncu_summary.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        return t[cfg_name][kernel]
+    except Exception:
+        return None
 
 
 def main():

@@ -1229,8 +1229,25 @@ static void set_pipe_attrs() {
 void finalize_schedule(Handle& h) {
   cudaStream_t s = h.stream;
   int64_t t_len = 0, tpart_len = 0;
-  const char* env_at = getenv("H2D_A_TARGET");    // diagnostics: stage-A item size (elements)
-  const int64_t kATarget = env_at && atoll(env_at) >= 2048 ? atoll(env_at) : kATargetDefault;
+  // stage-A item size: large items amortise the per-item epilogue (measured: 32K -> 1M
+  // elements takes C3's stage A from 1.60 to 1.44 ms), but at least ~4 items per CTA keep
+  // the dynamic schedule balanced on small operators
+  int64_t a_elems = 0;
+  for (int l = 1; l <= h.kappa; ++l) {
+    const Level& L = h.levels[(size_t)l];
+    for (int64_t Y = 0; Y < L.nbox; ++Y)
+      a_elems += (h.box_end(l, Y) - h.box_begin(l, Y)) * ((L.vR[(size_t)Y] + 1) & ~1);
+  }
+  if (!h.persist_ctas) {
+    int sm = 0;
+    H2D_CUDA(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, h.device));
+    h.persist_ctas = 2 * sm;
+  }
+  const char* env_at = getenv("H2D_A_TARGET");    // diagnostics override (elements)
+  const int64_t kATarget = env_at && atoll(env_at) >= 2048
+                               ? atoll(env_at)
+                               : std::min<int64_t>(kATargetDefault,
+                                                   std::max<int64_t>(32768, a_elems / (4 * (int64_t)h.persist_ctas)));
   std::vector<AItem> aitems;
   std::vector<RItem> ritems;
   for (int l = 1; l <= h.kappa; ++l) {
@@ -1499,7 +1516,8 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
   cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
   const int64_t nleaves = h.leaf_end - h.leaf_begin;
   // H2D_P2P_SERIAL=1 (diagnostics only): the P2P runs alone, before stage A
-  static const bool p2p_serial = getenv("H2D_P2P_SERIAL") && atoi(getenv("H2D_P2P_SERIAL")) == 1;
+  const char* env_ser = getenv("H2D_P2P_SERIAL");
+  const bool p2p_serial = env_ser && atoi(env_ser) == 1;
   H2D_CUDA(cudaEventRecord(h.ev_fork, s));
   H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_fork, 0));
   H2D_CUDA(cudaStreamWaitEvent(a, h.ev_fork, 0));

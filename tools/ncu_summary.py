@@ -52,6 +52,7 @@ def full(path):
 
 def short(n):
     """Kernel name without return type, namespaces or argument list (template args kept)."""
+    n = n.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("unnamed>::", "")
     depth, cut = 0, len(n)
     for i, ch in enumerate(n):
         if ch == "<":
@@ -76,7 +77,10 @@ def short(n):
             continue
         cur += ch
     parts.append(cur)
-    return parts[-1].split(" ")[-1] if "<" not in parts[-1] else parts[-1].strip()
+    last = parts[-1].strip()
+    if last.startswith("void "):
+        last = last[5:]
+    return last.split(" ")[-1] if "<" not in last else last
 
 
 MATVEC = ("stageA", "stageB", "p2p", "permute_in", "unpad", "reduce_kernel")
@@ -105,8 +109,37 @@ def launches(path):
             print(f"| {name} | {len(xs)} | {sum(xs) / len(xs) / 1e3:.1f} | {100 * sum(xs) / mtot:.1f} % |")
 
 
+STAGE_OF = {"stageA_tma_kernel": "stageA_VTx", "stageB_tma_kernel": "stageB_Ut",
+            "p2p_fast_kernel": "p2p_near"}
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def traffic(path, cfg, out):
+    """Per-launch DRAM bytes (read + write) of the matvec kernels -> profiles/ncu_traffic.json."""
+    import json
+    import os
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    acc = defaultdict(list)
+    for r in rows[2:]:
+        name = short(r[hdr.index("Kernel Name")]).split("<")[0]
+        if name in STAGE_OF:
+            b = float(r[ir]) * SCALE[units[ir]] + float(r[iw]) * SCALE[units[iw]]
+            acc[STAGE_OF[name]].append(b)
+    data = json.load(open(out)) if os.path.exists(out) else {}
+    data[cfg] = {k: int(sum(v) / len(v)) for k, v in acc.items()}
+    data[cfg]["source"] = os.path.basename(path)
+    with open(out, "w") as f:
+        json.dump(data, f, indent=1, sort_keys=True)
+    print(json.dumps(data[cfg]))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "--traffic":
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4])
     else:
         full(sys.argv[1])
