@@ -43,6 +43,7 @@ typedef struct hodlr2d_s* hodlr2d_t; /* opaque handle */
 enum {
   H2D_OK = 0,
   H2D_WTRUNC = 1,        /* warning: some ACA block hit max_rank (see info.truncated)      */
+  H2D_WNOCONV = 2,       /* warning: hodlr2d_gmres stopped at max_iter above the tolerance  */
   H2D_EINVAL = -1,       /* bad argument: n < 1, leaf_size < 1, tol not in (0,1), NaN/Inf  */
   H2D_EOUTOFBOX = -2,    /* a point lies outside the explicit root box (message: index)    */
   H2D_ECOINCIDENT = -3,  /* reserved (coincident points are legal: K(r=0) := K0, R8)      */
@@ -56,6 +57,10 @@ enum {
   H2D_KERNEL_LOG = 0,           /* K(r) = log r, K(0) = 0          */
   H2D_KERNEL_IMQ = 1,           /* K(r) = 1/sqrt(1 + (r/c)^2), K(0)=1 (BASELINE configs 2,5) */
   H2D_KERNEL_ONE_OVER_R = 2,    /* K(r) = 1/r, K(0) = 0             (Eq. eq:1byr)  */
+  H2D_KERNEL_RBF_PHI1 = 3,      /* phi_1(r) = log r / log a (r >= a), (r log r - 1)/(a log a - 1)
+                                   (r < a), K(0) = 0; a = options.c   (Kernel 1) */
+  H2D_KERNEL_RBF_PHI2 = 4,      /* phi_2(r) = a / r (r >= a), r / a (r < a), K(0) = 0; a = c
+                                                                      (Kernel 2) */
   H2D_KERNEL_TEST_LOWRANK = 100 /* test-only: K(p,q) = sum_{s<test_rank} phi_s(p) phi_s(q),
                                    phi_s(p) = cos((s+1) p.x + 0.5 s p.y) (exact rank)     */
 };
@@ -71,7 +76,7 @@ enum { H2D_ORDER_ORIGINAL = 0, H2D_ORDER_TREE = 1, H2D_ORDER_GATHERED = 2 };
 
 /* Options of hodlr2d_build_ex.  Always start from hodlr2d_default_options(). */
 typedef struct {
-  double c;               /* IMQ shape parameter, c > 0                        (default 1)  */
+  double c;               /* IMQ shape c > 0; RBF phi_1/phi_2 parameter a > 0  (default 1)  */
   double scale;           /* A = shift*I + scale*K                             (default 1)  */
   double shift;           /*                                                   (default 0)  */
   double box_lo[2];       /* root square lower-left corner                                  */
@@ -146,6 +151,19 @@ int hodlr2d_matvec(hodlr2d_t h, const double* x, double* y);
  * unpads it into its TREE-order x inside the matvec.  order = H2D_ORDER_ORIGINAL: as
  * hodlr2d_matvec (single-rank handles only). */
 int hodlr2d_matvec_ex(hodlr2d_t h, const double* x, double* y, int order);
+
+/* Solve A x = b with restarted GMRES(restart) accelerated by the HODLR2D matvec — the
+ * iterative solver of the paper's applications (§5: ACA tolerance 1e-12 and GMRES residual
+ * 1e-10; RBF interpolation with phi_1 / phi_2; R20).
+ * b, x: length N in ORIGINAL order, host or device pointers; x0 = 0 and x is overwritten.
+ * Arnoldi with classical Gram-Schmidt + one reorthogonalisation, Givens rotations; stops
+ * when the estimated relative residual ||b - A x|| / ||b|| < tol (checked against the true
+ * residual at every restart) or after max_iter Arnoldi steps.  *iters (may be NULL)
+ * receives the Arnoldi steps (= matvecs excluding restarts), *rel_residual (may be NULL)
+ * the TRUE relative residual of the returned x.  Single-rank handles only.  Returns
+ * H2D_OK, H2D_WNOCONV if tol was not reached, or an error. */
+int hodlr2d_gmres(hodlr2d_t h, const double* b, double* x, double tol, int restart, int max_iter,
+                  int* iters, double* rel_residual);
 
 /* Statistics of the built operator (host struct). */
 int hodlr2d_get_info(hodlr2d_t h, hodlr2d_info* info);

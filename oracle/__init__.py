@@ -18,7 +18,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
-KERNELS = {"log": 0, "imq": 1, "one_over_r": 2, "test_lowrank": 100}
+KERNELS = {"log": 0, "imq": 1, "one_over_r": 2, "rbf_phi1": 3, "rbf_phi2": 4, "test_lowrank": 100}
 
 
 def compile_oracle(force: bool = False) -> str:
@@ -232,3 +232,62 @@ class Operator:
         rc = lib().oracle_save_factors(self._h, str(path).encode())
         if rc != 0:
             raise ValueError(last_error())
+
+
+def gmres(matvec, b, tol=1e-10, restart=30, max_iter=1000):
+    """Restarted GMRES(m) on x -> matvec(x), x0 = 0, stopping when the true (restart) or the
+    Givens-estimated (inner) relative residual ||b - A x|| / ||b|| < tol.
+
+    The paper's solver (§5.2: "stopping criteria for GMRES is
+    residual less than 1e-10 with restart after each iterations"; restart length and
+    orthogonalisation unstated -> DESIGN.md R20: GMRES(30), relative residual, x0 = 0).
+    Plain textbook algorithm (Saad, Iterative Methods, Alg. 6.9): Arnoldi with modified
+    Gram-Schmidt, Givens rotations on the Hessenberg matrix, back substitution.
+    Returns (x, total inner iterations, final relative residual ||b - A x|| / ||b||)."""
+    b = np.asarray(b, dtype=np.float64)
+    n = b.shape[0]
+    bnorm = float(np.linalg.norm(b))
+    x = np.zeros(n)
+    if bnorm == 0.0:
+        return x, 0, 0.0
+    its = 0
+    while True:
+        r = b - matvec(x)
+        beta = float(np.linalg.norm(r))
+        if beta / bnorm < tol or its >= max_iter:
+            return x, its, beta / bnorm
+        m = restart
+        V = np.zeros((m + 1, n))
+        H = np.zeros((m + 1, m))
+        cs = np.zeros(m)
+        sn = np.zeros(m)
+        g = np.zeros(m + 1)
+        g[0] = beta
+        V[0] = r / beta
+        k = 0
+        for j in range(m):
+            w = matvec(V[j])
+            for i in range(j + 1):                      # modified Gram-Schmidt
+                H[i, j] = float(np.dot(w, V[i]))
+                w = w - H[i, j] * V[i]
+            H[j + 1, j] = float(np.linalg.norm(w))
+            if H[j + 1, j] > 0.0:
+                V[j + 1] = w / H[j + 1, j]
+            for i in range(j):                          # previous rotations
+                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t
+            d = float(np.hypot(H[j, j], H[j + 1, j]))    # new rotation zeroing H[j+1, j]
+            cs[j], sn[j] = (H[j, j] / d, H[j + 1, j] / d) if d > 0.0 else (1.0, 0.0)
+            H[j, j] = d
+            H[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            k = j + 1
+            its += 1
+            if abs(g[j + 1]) / bnorm < tol or its >= max_iter:
+                break
+        y = np.zeros(k)                                 # back substitution H[:k,:k] y = g[:k]
+        for i in range(k - 1, -1, -1):
+            y[i] = (g[i] - float(np.dot(H[i, i + 1:k], y[i + 1:k]))) / H[i, i]
+        x = x + V[:k].T @ y

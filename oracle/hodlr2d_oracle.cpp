@@ -13,6 +13,7 @@
 //
 //  Contents (each follows the paper's statement or a DESIGN.md reading):
 //    kernel entry          A(i,j) = shift*[i==j] + scale*K(|p_i-p_j|)   P:218-224, R8
+//                          (log, IMQ, 1/r Eq. eq:1byr, RBF phi_1 / phi_2 P:1035-1046)
 //    depth rule            R1 (nominal leaf size; P:878 contradicts config 1)
 //    quadtree + Morton     P:583-666 (Fig. sdomain01), R2-R4
 //    relations E/V/W/clan  Defs 4.1-4.4, literal classification on integer
@@ -42,11 +43,11 @@
 
 namespace {
 
-enum { K_LOG = 0, K_IMQ = 1, K_ONE_OVER_R = 2, K_TEST_LOWRANK = 100 };
+enum { K_LOG = 0, K_IMQ = 1, K_ONE_OVER_R = 2, K_RBF_PHI1 = 3, K_RBF_PHI2 = 4, K_TEST_LOWRANK = 100 };
 
 struct KernelSpec {
     int id = K_LOG;
-    double c = 1.0;      // IMQ shape
+    double c = 1.0;      // IMQ shape c; RBF phi_1 / phi_2 parameter a
     double scale = 1.0;  // A = shift*I + scale*K
     double shift = 0.0;
     int test_rank = 1;   // TEST_LOWRANK only
@@ -70,6 +71,18 @@ double kernel_value(const KernelSpec& k, double px, double py, double qx, double
     if (k.id == K_ONE_OVER_R) {                               // Eq. eq:1byr, paper anchor
         if (r == 0.0) return 0.0;
         return 1.0 / r;
+    }
+    if (k.id == K_RBF_PHI1) {                                 // Kernel 1 phi_1
+        if (r == 0.0) return 0.0;                             // Eq. eq:ker sums j != i (R20)
+        const double a = k.c;
+        if (r >= a) return std::log(r) / std::log(a);
+        return (r * std::log(r) - 1.0) / (a * std::log(a) - 1.0);
+    }
+    if (k.id == K_RBF_PHI2) {                                 // Kernel 2 phi_2
+        if (r == 0.0) return 0.0;
+        const double a = k.c;
+        if (r >= a) return a / r;
+        return r / a;
     }
     // inverse multiquadric 1/sqrt(1 + (r/c)^2)  (BASELINE.json configs 2 and 5)
     double rc = r / k.c;

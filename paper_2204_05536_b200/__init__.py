@@ -24,10 +24,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhodlr2d.so")
 
-H2D_OK, H2D_WTRUNC = 0, 1
+H2D_OK, H2D_WTRUNC, H2D_WNOCONV = 0, 1, 2
 H2D_EINVAL, H2D_EOUTOFBOX, H2D_ECOINCIDENT, H2D_ENOMEM = -1, -2, -3, -4
 H2D_ECUDA, H2D_ENCCL, H2D_EFACTORS = -5, -6, -7
-KERNELS = {"log": 0, "imq": 1, "one_over_r": 2, "test_lowrank": 100}
+KERNELS = {"log": 0, "imq": 1, "one_over_r": 2, "rbf_phi1": 3, "rbf_phi2": 4, "test_lowrank": 100}
 ORDER_ORIGINAL, ORDER_TREE, ORDER_GATHERED = 0, 1, 2
 ORDERS = {"original": 0, "tree": 1, "gathered": 2}
 MAX_LEVELS = 16
@@ -40,7 +40,7 @@ ABI_FUNCTIONS = (
     "hodlr2d_matvec_ex", "hodlr2d_get_info", "hodlr2d_copy_tree", "hodlr2d_copy_lists",
     "hodlr2d_num_blocks", "hodlr2d_copy_ranks", "hodlr2d_copy_block", "hodlr2d_load_factors",
     "hodlr2d_save_factors", "hodlr2d_stage_times", "hodlr2d_set_timing", "hodlr2d_destroy",
-    "hodlr2d_last_error", "hodlr2d_partition",
+    "hodlr2d_last_error", "hodlr2d_partition", "hodlr2d_gmres",
 )
 
 
@@ -121,6 +121,7 @@ def lib() -> C.CDLL:
             L.hodlr2d_destroy.argtypes = [vp]
             L.hodlr2d_last_error.restype = C.c_char_p
             L.hodlr2d_partition.argtypes = [vp, i, i, i, C.POINTER(i64), C.POINTER(i64)]
+            L.hodlr2d_gmres.argtypes = [vp, vp, vp, d, i, i, C.POINTER(i), C.POINTER(d)]
             _lib = L
     return _lib
 
@@ -252,6 +253,21 @@ class Hodlr2d:
         else:
             _check(lib().hodlr2d_matvec_ex(self._h, _ptr(x), _ptr(out), o))
         return out
+
+    def gmres(self, b, x=None, tol=1e-10, restart=30, max_iter=1000):
+        """hodlr2d_gmres: solve A x = b (x0 = 0) with restarted GMRES on the HODLR2D matvec.
+        Returns (x, iterations, true relative residual); ``converged`` is the rc == H2D_OK."""
+        if x is None:
+            if isinstance(b, np.ndarray):
+                x = np.empty_like(b)
+            else:
+                import torch
+                x = torch.empty_like(b)
+        its, rr = C.c_int(), C.c_double()
+        rc = _check(lib().hodlr2d_gmres(self._h, _ptr(b), _ptr(x), tol, restart, max_iter,
+                                        C.byref(its), C.byref(rr)))
+        self.gmres_converged = rc == H2D_OK
+        return x, its.value, rr.value
 
     def matvec_raw(self, x_ptr: int, y_ptr: int, order: int = ORDER_ORIGINAL):
         _check(lib().hodlr2d_matvec_ex(self._h, x_ptr, y_ptr, order))

@@ -394,19 +394,36 @@ __device__ __forceinline__ void hlog_table(double2* tab) {
   }
 }
 
-// K(r) from r^2 with K(0) := K0 by a select (no branch); distance kernels only.
+// K(r) from r^2 with K(0) := K0 by a select (no branch; phi_1 / phi_2 branch only for
+// the rare pairs closer than a); distance kernels only.
 template <int KID>
-__device__ __forceinline__ double kfast(double r2, const double2* __restrict__ tab, double inv_c2) {
+__device__ __forceinline__ double kfast(double r2, const double2* __restrict__ tab, const KernelParams& kp) {
   if (KID == H2D_KERNEL_LOG) {
     const double v = hlog_r2(r2, tab);
     return r2 > 0.0 ? v : 0.0;
   } else if (KID == H2D_KERNEL_IMQ) {
-    return rsqrt(fma(r2, inv_c2, 1.0));
-  } else {
+    return rsqrt(fma(r2, kp.inv_c2, 1.0));
+  } else if (KID == H2D_KERNEL_ONE_OVER_R) {
     const double v = rsqrt(r2);
     return r2 > 0.0 ? v : 0.0;
+  } else if (KID == H2D_KERNEL_RBF_PHI1) {
+    double v = hlog_r2(r2, tab) * kp.inv_log_a;          // log r / log a
+    if (r2 < kp.a2) {
+      const double r = sqrt(r2);
+      v = r2 > 0.0 ? fma(r, log(r), -1.0) * kp.inv_phi1_den : 0.0;
+    }
+    return v;
+  } else {   // H2D_KERNEL_RBF_PHI2
+    const double v = kp.a * rsqrt(r2);
+    return r2 >= kp.a2 ? v : sqrt(r2) / kp.a;
   }
 }
+
+template <int KID>
+constexpr bool kDistKernel = KID == H2D_KERNEL_LOG || KID == H2D_KERNEL_IMQ || KID == H2D_KERNEL_ONE_OVER_R ||
+                             KID == H2D_KERNEL_RBF_PHI1 || KID == H2D_KERNEL_RBF_PHI2;
+template <int KID>
+constexpr bool kNeedsLogTable = KID == H2D_KERNEL_LOG || KID == H2D_KERNEL_RBF_PHI1;
 
 template <int KID>
 __device__ __forceinline__ double p2p_eval(const KernelParams& kp, const double2* tab, double px,
@@ -427,7 +444,7 @@ __device__ __forceinline__ double p2p_eval(const KernelParams& kp, const double2
 template <int KID, bool DIAG>
 __device__ __forceinline__ void tile_fast(int mt, int nt, const double* __restrict__ sa,
                                           const double* __restrict__ sb, const double2* __restrict__ tab,
-                                          double inv_c2, double k0, double* srow,
+                                          const KernelParams& kp, double k0, double* srow,
                                           double (*scol)[kSymTile + 1]) {
   const int tid = threadIdx.x, ti = tid >> 4, tj = tid & 15;
   const int A = (mt + 15) >> 4, B = (nt + 15) >> 4;
@@ -451,7 +468,7 @@ __device__ __forceinline__ void tile_fast(int mt, int nt, const double* __restri
     for (int bb = 0; bb < kSymMaxB; ++bb) {
       if (bb < B) {
         const double dx = rpx - cpx[bb], dy = rpy - cpy[bb];
-        double k = kfast<KID>(fma(dx, dx, dy * dy), tab, inv_c2);
+        double k = kfast<KID>(fma(dx, dx, dy * dy), tab, kp);
         if (DIAG) k = i < tj + 16 * bb ? k : 0.0;
         racc = fma(k, cxv[bb], racc);
         cacc[bb] = fma(k, rx, cacc[bb]);
@@ -599,7 +616,7 @@ p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end, const int32_t* _
   __shared__ double2 s_logtab[128];
   const int64_t X = leaves[blockIdx.x];
   const int tid = threadIdx.x;
-  if (KID == H2D_KERNEL_LOG) hlog_table(s_logtab);
+  if (kNeedsLogTable<KID>) hlog_table(s_logtab);
   const uint32_t cx = p2p_compact((uint32_t)X), cy = p2p_compact((uint32_t)X >> 1);
   const uint32_t side = 1u << kappa;
   const int64_t xs = leaf_start[X];
@@ -627,7 +644,7 @@ p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end, const int32_t* _
   if (do_u)
     for (int i = tid; i < un; i += 256) sD[us + i] = 0.0;
   if (m == 0) return;
-  constexpr bool kDist = KID == H2D_KERNEL_LOG || KID == H2D_KERNEL_IMQ || KID == H2D_KERNEL_ONE_OVER_R;
+  constexpr bool kDist = kDistKernel<KID>;
   int first_task = 0;
   if (kDist && m <= kSymTile && rn <= kSymTile && un <= kSymTile) {
     // fast path: the self, +x and +y tiles are loaded together (one memory latency), then
@@ -641,14 +658,14 @@ p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end, const int32_t* _
     }
     __syncthreads();
     const double k0 = KID == H2D_KERNEL_IMQ ? 1.0 : 0.0;
-    tile_fast<KID, true>(m, m, s_a, s_a, s_logtab, kp.inv_c2, k0, srow, scol);
+    tile_fast<KID, true>(m, m, s_a, s_a, s_logtab, kp, k0, srow, scol);
     tile_flush(m, m, s0 + xs, s0 + xs, srow, scol);
     if (has_r) {
-      tile_fast<KID, false>(m, rn, s_a, s_b, s_logtab, kp.inv_c2, k0, srow, scol);
+      tile_fast<KID, false>(m, rn, s_a, s_b, s_logtab, kp, k0, srow, scol);
       tile_flush(m, rn, s0 + xs, do_r ? sL + rs : nullptr, srow, scol);
     }
     if (has_u) {
-      tile_fast<KID, false>(m, un, s_a, s_c, s_logtab, kp.inv_c2, k0, srow, scol);
+      tile_fast<KID, false>(m, un, s_a, s_c, s_logtab, kp, k0, srow, scol);
       tile_flush(m, un, s0 + xs, do_u ? sD + us : nullptr, srow, scol);
     }
     first_task = 3;
@@ -730,7 +747,7 @@ __device__ __forceinline__ void p2p_prefetch(const P2PMeta& M, double (*T)[3 * k
 template <int KID, bool DIAG>
 __device__ __forceinline__ void tile_fast8(int mt, int nt, const double* __restrict__ sa,
                                            const double* __restrict__ sb, const double2* __restrict__ tab,
-                                           double inv_c2, double k0, double* srow,
+                                           const KernelParams& kp, double k0, double* srow,
                                            double (*scol8)[kSymTile + 1]) {
   const int tid = threadIdx.x, ti = tid >> 4, tj = tid & 15;
   const int A = (mt + 15) >> 4, B = (nt + 15) >> 4;
@@ -754,7 +771,7 @@ __device__ __forceinline__ void tile_fast8(int mt, int nt, const double* __restr
     for (int bb = 0; bb < kSymMaxB; ++bb) {
       if (bb < B) {
         const double dx = rpx - cpx[bb], dy = rpy - cpy[bb];
-        double k = kfast<KID>(fma(dx, dx, dy * dy), tab, inv_c2);
+        double k = kfast<KID>(fma(dx, dx, dy * dy), tab, kp);
         if (DIAG) k = i < tj + 16 * bb ? k : 0.0;
         racc = fma(k, cxv[bb], racc);
         cacc[bb] = fma(k, rx, cacc[bb]);
@@ -795,7 +812,7 @@ p2p_fast_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int
   __shared__ int s_next;
   const int tid = threadIdx.x;
   const double k0 = KID == H2D_KERNEL_IMQ ? 1.0 : 0.0;
-  if (KID == H2D_KERNEL_LOG) hlog_table(tab);
+  if (kNeedsLogTable<KID>) hlog_table(tab);
   if (tid == 0) s_next = atomicAdd(counter, 1);
   __syncthreads();
   int cur = s_next;
@@ -822,19 +839,19 @@ p2p_fast_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int
     const double* TX = tiles[b][0];
     const int m = Mc.m;
     // self block
-    tile_fast8<KID, true>(m, m, TX, TX, tab, kp.inv_c2, k0, srow, scol8);
+    tile_fast8<KID, true>(m, m, TX, TX, tab, kp, k0, srow, scol8);
     __syncthreads();
     if (tid < m) acc[tid] = srow[tid] + colsum8(scol8, tid);
     __syncthreads();
     if (Mc.has_r) {
-      tile_fast8<KID, false>(m, Mc.rn, TX, tiles[b][1], tab, kp.inv_c2, k0, srow, scol8);
+      tile_fast8<KID, false>(m, Mc.rn, TX, tiles[b][1], tab, kp, k0, srow, scol8);
       __syncthreads();
       if (tid < m) acc[tid] += srow[tid];
       if (tid < Mc.rn) sL[Mc.rs + tid] = colsum8(scol8, tid);
       __syncthreads();
     }
     if (Mc.has_u) {
-      tile_fast8<KID, false>(m, Mc.un, TX, tiles[b][2], tab, kp.inv_c2, k0, srow, scol8);
+      tile_fast8<KID, false>(m, Mc.un, TX, tiles[b][2], tab, kp, k0, srow, scol8);
       __syncthreads();
       if (tid < m) acc[tid] += srow[tid];
       if (tid < Mc.un) sD[Mc.us + tid] = colsum8(scol8, tid);
@@ -1381,7 +1398,8 @@ void finalize_schedule(Handle& h) {
       v = (v | (v << 1)) & 0x55555555u;
       return v;
     };
-    const bool dist = h.kp.id == H2D_KERNEL_LOG || h.kp.id == H2D_KERNEL_IMQ || h.kp.id == H2D_KERNEL_ONE_OVER_R;
+    const bool dist = h.kp.id == H2D_KERNEL_LOG || h.kp.id == H2D_KERNEL_IMQ || h.kp.id == H2D_KERNEL_ONE_OVER_R ||
+                      h.kp.id == H2D_KERNEL_RBF_PHI1 || h.kp.id == H2D_KERNEL_RBF_PHI2;
     const uint32_t side = 1u << h.kappa;
     auto size_of = [&](int64_t lf) { return h.leaf_start[(size_t)lf + 1] - h.leaf_start[(size_t)lf]; };
     auto served = [&](int64_t lf) { return lf >= h.leaf_begin && lf < h.leaf_end; };
@@ -1456,8 +1474,12 @@ void finalize_schedule(Handle& h) {
     for (const void* f : {(const void*)p2p_sym_kernel<H2D_KERNEL_LOG>, (const void*)p2p_sym_kernel<H2D_KERNEL_IMQ>,
                           (const void*)p2p_sym_kernel<H2D_KERNEL_ONE_OVER_R>,
                           (const void*)p2p_sym_kernel<H2D_KERNEL_TEST_LOWRANK>,
+                          (const void*)p2p_sym_kernel<H2D_KERNEL_RBF_PHI1>,
+                          (const void*)p2p_sym_kernel<H2D_KERNEL_RBF_PHI2>,
                           (const void*)p2p_fast_kernel<H2D_KERNEL_LOG>, (const void*)p2p_fast_kernel<H2D_KERNEL_IMQ>,
-                          (const void*)p2p_fast_kernel<H2D_KERNEL_ONE_OVER_R>})
+                          (const void*)p2p_fast_kernel<H2D_KERNEL_ONE_OVER_R>,
+                          (const void*)p2p_fast_kernel<H2D_KERNEL_RBF_PHI1>,
+                          (const void*)p2p_fast_kernel<H2D_KERNEL_RBF_PHI2>})
       H2D_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                     cudaSharedmemCarveoutMaxShared));
     h.num_sms = sm;
@@ -1527,6 +1549,8 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
       auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_sym_kernel<H2D_KERNEL_LOG>
                 : h.kp.id == H2D_KERNEL_IMQ ? p2p_sym_kernel<H2D_KERNEL_IMQ>
                 : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_sym_kernel<H2D_KERNEL_ONE_OVER_R>
+                : h.kp.id == H2D_KERNEL_RBF_PHI1 ? p2p_sym_kernel<H2D_KERNEL_RBF_PHI1>
+                : h.kp.id == H2D_KERNEL_RBF_PHI2 ? p2p_sym_kernel<H2D_KERNEL_RBF_PHI2>
                                                    : p2p_sym_kernel<H2D_KERNEL_TEST_LOWRANK>;
       kfn<<<(int)h.n_p2p_gen, 256, 0, a>>>(h.kappa, h.leaf_begin, h.leaf_end, h.d_p2p_gen,
                                            h.d_leaf_start, h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear,
@@ -1536,7 +1560,9 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
     if (h.n_p2p_fast > 0) {
       auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_fast_kernel<H2D_KERNEL_LOG>
                 : h.kp.id == H2D_KERNEL_IMQ ? p2p_fast_kernel<H2D_KERNEL_IMQ>
-                                            : p2p_fast_kernel<H2D_KERNEL_ONE_OVER_R>;
+                : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_fast_kernel<H2D_KERNEL_ONE_OVER_R>
+                : h.kp.id == H2D_KERNEL_RBF_PHI1 ? p2p_fast_kernel<H2D_KERNEL_RBF_PHI1>
+                                                 : p2p_fast_kernel<H2D_KERNEL_RBF_PHI2>;
       H2D_CUDA(cudaMemsetAsync(h.d_counters + 2, 0, sizeof(int32_t), a));
       const int grid = (int)std::min<int64_t>(h.num_sms, h.n_p2p_fast);
       kfn<<<grid, 256, 0, a>>>(h.kappa, h.d_p2p_fast, (int)h.n_p2p_fast, h.d_counters + 2,

@@ -326,9 +326,14 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
   if (leaf_size < 1) throw Error{H2D_EINVAL, "leaf_size < 1"};
   if (!(aca_tol > 0.0 && aca_tol < 1.0)) throw Error{H2D_EINVAL, "aca_tol not in (0, 1)"};
   if (kernel_id != H2D_KERNEL_LOG && kernel_id != H2D_KERNEL_IMQ && kernel_id != H2D_KERNEL_ONE_OVER_R &&
+      kernel_id != H2D_KERNEL_RBF_PHI1 && kernel_id != H2D_KERNEL_RBF_PHI2 &&
       kernel_id != H2D_KERNEL_TEST_LOWRANK)
     throw Error{H2D_EINVAL, "unknown kernel_id"};
   if (kernel_id == H2D_KERNEL_IMQ && !(opts->c > 0.0)) throw Error{H2D_EINVAL, "IMQ needs c > 0"};
+  if ((kernel_id == H2D_KERNEL_RBF_PHI1 || kernel_id == H2D_KERNEL_RBF_PHI2) && !(opts->c > 0.0))
+    throw Error{H2D_EINVAL, "RBF kernels need a = c > 0"};
+  if (kernel_id == H2D_KERNEL_RBF_PHI1 && opts->c == 1.0)
+    throw Error{H2D_EINVAL, "phi_1 needs a != 1 (log a = 0)"};
   if (opts->max_rank < 1 || opts->aca_consecutive < 1 || opts->aca_trim < 0 ||
       opts->aca_trim > opts->aca_consecutive)
     throw Error{H2D_EINVAL, "bad ACA options"};
@@ -347,6 +352,10 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
   h.n = n;
   h.kp.id = kernel_id;
   h.kp.inv_c2 = kernel_id == H2D_KERNEL_IMQ ? 1.0 / (opts->c * opts->c) : 0.0;
+  h.kp.a = opts->c;
+  h.kp.a2 = opts->c * opts->c;
+  h.kp.inv_log_a = kernel_id == H2D_KERNEL_RBF_PHI1 ? 1.0 / std::log(opts->c) : 0.0;
+  h.kp.inv_phi1_den = kernel_id == H2D_KERNEL_RBF_PHI1 ? 1.0 / (opts->c * std::log(opts->c) - 1.0) : 0.0;
   h.kp.scale = opts->scale;
   h.kp.shift = opts->shift;
   h.kp.test_rank = opts->test_rank;
@@ -399,6 +408,44 @@ int hodlr2d_matvec_ex(hodlr2d_t H, const double* x, double* y, int order) {
   if (!H) throw Error{H2D_EINVAL, "null handle"};
   do_matvec(H->h, x, y, order);
   return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_gmres(hodlr2d_t H, const double* b, double* x, double tol, int restart, int max_iter,
+                  int* iters, double* rel_residual) {
+  H2D_TRY
+  if (!H || !b || !x) throw Error{H2D_EINVAL, "null argument"};
+  Handle& h = H->h;
+  cudaStream_t s = h.stream;
+  const bool bdev = is_device_ptr(b), xdev = is_device_ptr(x);
+  const double* db = b;
+  double* dx = x;
+  double *tb = nullptr, *tx = nullptr;
+  if (!bdev) {
+    H2D_CUDA(cudaMallocAsync(&tb, h.n * sizeof(double), s));
+    H2D_CUDA(cudaMemcpyAsync(tb, b, h.n * sizeof(double), cudaMemcpyHostToDevice, s));
+    db = tb;
+  }
+  if (!xdev) {
+    H2D_CUDA(cudaMallocAsync(&tx, h.n * sizeof(double), s));
+    dx = tx;
+  }
+  int its = 0;
+  double rr = 0.0;
+  try {
+    gmres_solve(h, db, dx, tol, restart, max_iter, &its, &rr);
+  } catch (...) {
+    if (tb) cudaFreeAsync(tb, s);
+    if (tx) cudaFreeAsync(tx, s);
+    throw;
+  }
+  if (!xdev) H2D_CUDA(cudaMemcpyAsync(x, dx, h.n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (tb) H2D_CUDA(cudaFreeAsync(tb, s));
+  if (tx) H2D_CUDA(cudaFreeAsync(tx, s));
+  H2D_CUDA(cudaStreamSynchronize(s));
+  if (iters) *iters = its;
+  if (rel_residual) *rel_residual = rr;
+  return rr < tol ? H2D_OK : H2D_WNOCONV;
   H2D_CATCH
 }
 

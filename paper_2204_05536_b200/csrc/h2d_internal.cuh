@@ -31,6 +31,9 @@ void set_error(int code, const std::string& msg);
 struct KernelParams {
   int id;          // H2D_KERNEL_*
   double inv_c2;   // 1 / c^2 (IMQ)
+  double a, a2;    // RBF parameter a and a^2 (phi_1, phi_2)
+  double inv_log_a;      // 1 / log a                 (phi_1, r >= a)
+  double inv_phi1_den;   // 1 / (a log a - 1)         (phi_1, r < a)
   double scale;    // A = shift I + scale K
   double shift;
   int test_rank;
@@ -48,6 +51,14 @@ __device__ __forceinline__ double kernel_eval_t(const KernelParams& k, double px
     return rsqrt(fma(r2, k.inv_c2, 1.0));
   } else if (KID == H2D_KERNEL_ONE_OVER_R) {
     return r2 > 0.0 ? rsqrt(r2) : 0.0;
+  } else if (KID == H2D_KERNEL_RBF_PHI1) {
+    if (r2 == 0.0) return 0.0;
+    if (r2 >= k.a2) return 0.5 * log(r2) * k.inv_log_a;
+    const double r = sqrt(r2);
+    return fma(r, log(r), -1.0) * k.inv_phi1_den;
+  } else if (KID == H2D_KERNEL_RBF_PHI2) {
+    if (r2 >= k.a2) return k.a * rsqrt(r2);
+    return sqrt(r2) / k.a;
   } else {
     double acc = 0.0;
     for (int s = 0; s < k.test_rank; ++s)
@@ -67,6 +78,10 @@ __device__ __forceinline__ double kernel_eval(const KernelParams& k, double px, 
     return rsqrt(fma(r2, k.inv_c2, 1.0));
   } else if (k.id == H2D_KERNEL_ONE_OVER_R) {
     return r2 > 0.0 ? rsqrt(r2) : 0.0;
+  } else if (k.id == H2D_KERNEL_RBF_PHI1) {
+    return kernel_eval_t<H2D_KERNEL_RBF_PHI1>(k, px, py, qx, qy);
+  } else if (k.id == H2D_KERNEL_RBF_PHI2) {
+    return kernel_eval_t<H2D_KERNEL_RBF_PHI2>(k, px, py, qx, qy);
   } else {
     double acc = 0.0;
     for (int s = 0; s < k.test_rank; ++s)
@@ -274,5 +289,7 @@ constexpr int kEventsPerMatvec = 8;
 void begin_matvec_timing(Handle& h);
 void mark_after_input(Handle& h);
 void unpad_gathered(Handle& h, const double* d_xg, double* d_xtree);  // apply.cu (S11 epilogue)
+void gmres_solve(Handle& h, const double* d_b, double* d_x, double tol, int restart, int max_iter,
+                 int* iters, double* relres);                             // gmres.cu
 
 }  // namespace h2d
