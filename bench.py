@@ -39,6 +39,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--rank-slice", type=int, default=None,
+                    help="informational: build and time rank G's slice of a --slice-world partition "
+                         "on this one GPU, full x resident (per-GPU compute of the multi-GPU run)")
+    ap.add_argument("--slice-world", type=int, default=8)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: functional check of the multi-rank path (host-staged gather)")
     return ap.parse_args()
@@ -405,9 +409,64 @@ def ncu_traffic(cfg_name, kernel):
         return None
 
 
+def run_rank_slice(args, cfg):
+    """One rank's slice of the Morton-range partition on this GPU: the per-GPU
+    compute time of the --slice-world run.  The x all-gather is not run (one process); its
+    NVLink time is estimated from the measured peer bandwidth (B200_PROFILING.md, 770 GB/s
+    per direction).  Prints one informational JSON line (not the driver's bench line)."""
+    import torch
+    import paper_2204_05536_b200 as h2d
+    torch.cuda.set_device(0)
+    P, g = args.slice_world, args.rank_slice
+    stream = torch.cuda.current_stream()
+    pts = W.config_points(cfg)
+    t0 = time.time()
+    op = h2d.Hodlr2d.build(torch.from_numpy(pts).cuda(), cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c,
+                           scale=cfg.scale, shift=cfg.shift, box_lo=cfg.box_lo, box_side=cfg.box_side,
+                           world=P, rank=g, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    inf = op.info()
+    perm, _ = op.tree()
+    nx = min(args.steps + args.warmup, 8)
+    xs = [torch.from_numpy(np.ascontiguousarray(W.config_x(cfg, k)[perm])).cuda() for k in range(nx)]
+    y = torch.empty(inf["row_end"] - inf["row_begin"], dtype=torch.float64, device="cuda")
+    for k in range(args.warmup):
+        op.matvec_raw(xs[k % nx].data_ptr(), y.data_ptr(), h2d.ORDER_TREE)
+    op.set_timing(True)
+    op.stage_times(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for k in range(args.steps):
+            op.matvec_raw(xs[k % nx].data_ptr(), y.data_ptr(), h2d.ORDER_TREE)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    op.set_timing(False)
+    ms = e0.elapsed_time(e1) / args.steps
+    st, cnt = op.stage_times(reset=True)
+    peak, peak_kind = peaks()
+    gather_ms = 8.0 * cfg.n * (P - 1) / P / 770e9 * 1e3
+    line = {"mode": "rank_slice", "config": config_dict(cfg, P), "slice_world": P, "rank": g,
+            "rows": [inf["row_begin"], inf["row_end"]], "build_seconds": round(build_s, 2),
+            "ms_per_matvec_compute": ms, "steps": args.steps, "warmup": args.warmup,
+            "stage_ms_per_matvec": {k: round(v / max(cnt, 1), 4) for k, v in st.items()},
+            "matvec_bytes": inf["matvec_bytes"],
+            "hbm_frac_of_measured": inf["matvec_bytes"] / (ms * 1e-3) / 1e9 / peak,
+            "allgather_ms_estimate": gather_ms,
+            "projected_matvecs_per_s_at_world": 1e3 / (ms + gather_ms),
+            "device_gb": inf["device_bytes"] / 1e9, "rank_max": inf["rank_max"],
+            "clocks": clk.summary(), "dtype": "f64", "data": "synthetic"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     cfg = W.CONFIGS[args.config]
+    if args.rank_slice is not None:
+        run_rank_slice(args, cfg)
+        return
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
