@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--multi-rhs", type=int, default=8,
+                    help="also time hodlr2d_matvec_multi with this many vectors per call (0: skip)")
     ap.add_argument("--rank-slice", type=int, default=None,
                     help="informational: build and time rank G's slice of a --slice-world partition "
                          "on this one GPU, full x resident (per-GPU compute of the multi-GPU run)")
@@ -318,6 +320,29 @@ def run_ours(args, cfg):
         e2e = {"value": 1e3 * ke / e0.elapsed_time(e1), "unit": "matvecs/s",
                "h2d_bytes_per_step": 8 * cfg.n, "d2h_bytes_per_step": 8 * cfg.n}
 
+    # multi-RHS (NEXT N2): the same fresh vectors, nrhs per call; reported beside the
+    # single-vector headline, never in place of it
+    multi = None
+    if world == 1 and args.multi_rhs > 1 and nx >= args.multi_rhs:
+        K = args.multi_rhs
+        Ym = torch.empty(K, cfg.n, dtype=torch.float64, device="cuda")
+        nb = max(3, min(20, args.steps // K))
+        for _ in range(2):
+            op.matvec_multi_raw(xs[:K].data_ptr(), Ym.data_ptr(), K, h2d.ORDER_ORIGINAL)
+        torch.cuda.synchronize()
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record(stream)
+        for b in range(nb):
+            k0 = (b * K) % (nx - K + 1)
+            op.matvec_multi_raw(xs[k0:k0 + K].data_ptr(), Ym.data_ptr(), K, h2d.ORDER_ORIGINAL)
+        m1.record(stream)
+        torch.cuda.synchronize()
+        ms_b = m0.elapsed_time(m1) / nb
+        multi = {"nrhs": K, "matvecs_per_s": 1e3 * K / ms_b, "ms_per_call": ms_b, "calls": nb,
+                 "factor_bytes_per_call": inf["stageA_bytes"] + inf["stageB_bytes"],
+                 "note": "hodlr2d_matvec_multi: factor panels streamed once per call of nrhs "
+                         "vectors; a batched-throughput figure, not the per-vector headline"}
+
     # near-field P2P against the FP64 pipe.  The symmetric kernel evaluates every unordered
     # leaf pair once: (near_pairs + N) / 2 kernel evaluations, each P2P_FP64_OPS_PER_EVAL
     # FP64-pipe instructions (counted in the SASS of p2p_fast_kernel).  In the
@@ -355,7 +380,7 @@ def run_ours(args, cfg):
             "operator": {k: inf[k] for k in ("kappa", "rank_max", "u_values", "v_values", "near_pairs",
                                                "compression_ratio", "truncated", "matvec_bytes",
                                                "tree_seconds", "aca_seconds", "pack_seconds")},
-            "roofline": roof, "e2e": e2e,
+            "roofline": roof, "e2e": e2e, "multi_rhs": multi,
             "gpu_launches": args.steps * launches_per_matvec(inf, world),
             "clocks": csum,
         }

@@ -40,7 +40,7 @@ ABI_FUNCTIONS = (
     "hodlr2d_matvec_ex", "hodlr2d_get_info", "hodlr2d_copy_tree", "hodlr2d_copy_lists",
     "hodlr2d_num_blocks", "hodlr2d_copy_ranks", "hodlr2d_copy_block", "hodlr2d_load_factors",
     "hodlr2d_save_factors", "hodlr2d_stage_times", "hodlr2d_set_timing", "hodlr2d_destroy",
-    "hodlr2d_last_error", "hodlr2d_partition", "hodlr2d_gmres",
+    "hodlr2d_last_error", "hodlr2d_partition", "hodlr2d_gmres", "hodlr2d_matvec_multi",
 )
 
 
@@ -122,6 +122,7 @@ def lib() -> C.CDLL:
             L.hodlr2d_last_error.restype = C.c_char_p
             L.hodlr2d_partition.argtypes = [vp, i, i, i, C.POINTER(i64), C.POINTER(i64)]
             L.hodlr2d_gmres.argtypes = [vp, vp, vp, d, i, i, C.POINTER(i), C.POINTER(d)]
+            L.hodlr2d_matvec_multi.argtypes = [vp, vp, vp, i, i]
             _lib = L
     return _lib
 
@@ -268,6 +269,27 @@ class Hodlr2d:
                                         C.byref(its), C.byref(rr)))
         self.gmres_converged = rc == H2D_OK
         return x, its.value, rr.value
+
+    def matvec_multi(self, X, out=None, order="original"):
+        """hodlr2d_matvec_multi: ``X`` is (nrhs, N) (one vector per row, C-contiguous);
+        returns ``out`` of shape (nrhs, len_y)."""
+        o = ORDERS[order]
+        nrhs = X.shape[0]
+        if out is None:
+            m = self.n
+            if o != ORDER_ORIGINAL:
+                inf = self.info()
+                m = inf["row_end"] - inf["row_begin"]
+            if isinstance(X, np.ndarray):
+                out = np.empty((nrhs, m), dtype=np.float64)
+            else:
+                import torch
+                out = torch.empty((nrhs, m), dtype=torch.float64, device=X.device)
+        _check(lib().hodlr2d_matvec_multi(self._h, _ptr(X), _ptr(out), nrhs, o))
+        return out
+
+    def matvec_multi_raw(self, x_ptr: int, y_ptr: int, nrhs: int, order: int = ORDER_ORIGINAL):
+        _check(lib().hodlr2d_matvec_multi(self._h, x_ptr, y_ptr, nrhs, order))
 
     def matvec_raw(self, x_ptr: int, y_ptr: int, order: int = ORDER_ORIGINAL):
         _check(lib().hodlr2d_matvec_ex(self._h, x_ptr, y_ptr, order))

@@ -539,6 +539,7 @@ void run_big(Handle& h, std::vector<AcaBlock>& blk, const std::vector<int32_t>& 
   while (true) {
     for (int rep = 0; rep < 4; ++rep, ++step) {
       H2D_CUDA(cudaMemsetAsync(d_active, 0, sizeof(int), s));
+      if (row_items.empty() || all_items.empty()) throw Error{H2D_ECUDA, "ACA big path: empty block"};
       big_row_kernel<<<(int)row_items.size(), kBigThreads, smem, s>>>(
           d_blk, d_st, d_row, d_scr, d_pv, d_pi, h.d_px, h.d_py, h.kp, ap.max_rank);
       big_pivot_kernel<<<nb, 256, 0, s>>>(d_blk, d_st, nb, d_pv, d_pi, d_scr, d_used);
@@ -576,9 +577,15 @@ void run_aca(Handle& h) {
     L.truncated.assign((size_t)nbk, 0);
     // blocks served by this rank (row box intersects the served rows)
     std::vector<int64_t> todo;
-    for (int64_t X = 0; X < L.nbox; ++X)
-      if (h.row_box_active(l, X))
-        for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) todo.push_back(e);
+    for (int64_t X = 0; X < L.nbox; ++X) {
+      if (!h.row_box_active(l, X)) continue;
+      const bool mz = h.box_end(l, X) == h.box_begin(l, X);
+      for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
+        const int64_t Y = L.col[(size_t)e];
+        if (mz || h.box_end(l, Y) == h.box_begin(l, Y)) L.rank[(size_t)e] = 0;   // empty side (R5)
+        else todo.push_back(e);
+      }
+    }
     std::vector<const double*> srcU((size_t)nbk, nullptr), srcV((size_t)nbk, nullptr);
     if (todo.empty()) {
       pack_level(h, L, srcU, srcV);

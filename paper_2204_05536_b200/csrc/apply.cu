@@ -25,7 +25,7 @@
 #include <numeric>
 
 #include "h2d_internal.cuh"
-#include "tma.cuh"
+#include "pipe.cuh"
 
 namespace h2d {
 namespace {
@@ -33,51 +33,6 @@ namespace {
 constexpr int64_t kATargetDefault = 1048576;  // stage-A elements per work item (8 MB)
 constexpr int kAMaxRows = 16384;     // rows per stage-A item
 constexpr int kBRows = 224;          // rows per stage-B item (leaf row block) <= kCons
-
-// ---------------------------------------------------------------- pipeline layout
-// One producer warp (bulk TMA of the factor stream + 8-byte cp.async of the x / t values
-// a stage needs) and 8 consumer warps per CTA, NS-deep ring of 16 KB stages.  With
-// 2 CTAs per SM (grid = 2 x SMs, ~95 KB smem, <= 72 registers) a third CTA of the P2P
-// kernel still fits on every SM, so the FP64-bound near field runs under the HBM stream.
-constexpr int kNSShallow = 5, kNSDeep = 9;   // ring depth at 2 / 1 CTAs per SM
-constexpr int kDefaultCtasPerSm = 2;
-constexpr int kStageDbl = 2048;      // factor doubles per stage (16 KB)
-constexpr int kStageVec = 256;       // x (stage A) / t (stage B) values per stage
-constexpr int kCons = 224;           // consumer threads (7 warps: 8-warp CTAs spread evenly
-                                     // over the 4 SM sub-partitions' register files)
-constexpr int kPipeThreads = kCons + 32;
-
-constexpr int kFirst = 1, kLast = 2;
-
-struct StageHdr {
-  int32_t item;    // work item index; < 0: no more work (terminator)
-  int32_t cnt;     // rows (stage A) / columns (stage B) held by this stage
-  int32_t flags;   // kFirst / kLast stage of the item
-  int32_t a, b, c, d, pad;   // item fields for the consumers (see the producers)
-};
-
-template <int NS>
-struct PipeSmem {
-  double ring[NS][kStageDbl];
-  double vec[NS][kStageVec];
-  double red[2 * kCons];
-  StageHdr hdr[NS];
-  uint64_t full[NS];    // 1 producer arrival (+ tx bytes) + 32 cp.async arrivals
-  uint64_t empty[NS];   // 8 consumer-warp arrivals
-  int flag;
-};
-
-template <int NS>
-__device__ __forceinline__ void pipe_init(PipeSmem<NS>& S) {
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&S.full[s], 1 + 32);
-      mbar_init(&S.empty[s], kCons / 32);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-}
 
 struct UCopyItem {
   const double* src;   // column-major, leading dimension ld_src
@@ -360,71 +315,6 @@ stageA_tma_kernel(const AItem* __restrict__ items, int n_items, int32_t* counter
 // the 8 point coordinates and x values held in registers.
 constexpr int kSymRowsOnly = 0, kSymBoth = 1, kSymSelf = 2;
 
-constexpr int kSymTile = 96, kSymMaxB = kSymTile / 16;
-
-// 0.5 log(r2) for normal r2 > 0: r2 = 2^e m, m in [1, 2); c_k = 1 + (k + 1/2)/128 is the
-// centre of m's 1/128 bin (k = top 7 mantissa bits), tab[k] = (1/c_k, 0.5 log c_k);
-// 0.5 log r2 = e ln2/2 + 0.5 log c_k + 0.5 log1p(f), f = m/c_k - 1, |f| <= 2^-8, with
-// 0.5 log1p(f) = f p(f), p the degree-5 Taylor polynomial (truncation f^7/7 <= 2e-18).
-// 9 DFMA; the coefficients are constant-bank operands (no register materialisation).
-__constant__ double c_hlog[8] = {0.34657359027997264,   // ln2 / 2 (high part)
-                                 1.1595234069231498e-17, // ln2 / 2 (low part)
-                                 0.5, -0.25, 1.0 / 6.0, -0.125, 0.1, -1.0 / 12.0};
-
-__device__ __forceinline__ double hlog_r2(double r2, const double2* __restrict__ tab) {
-  const long long bits = __double_as_longlong(r2);
-  const int e = (int)(bits >> 52) - 1023;
-  const int k = (int)(bits >> 45) & 127;
-  const double mnt = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
-  const double2 tb = tab[k];
-  const double f = fma(mnt, tb.x, -1.0);
-  double p = fma(f, c_hlog[7], c_hlog[6]);
-  p = fma(f, p, c_hlog[5]);
-  p = fma(f, p, c_hlog[4]);
-  p = fma(f, p, c_hlog[3]);
-  p = fma(f, p, c_hlog[2]);
-  const double ed = (double)e;
-  return fma(ed, c_hlog[0], fma(p, f, fma(ed, c_hlog[1], tb.y)));
-}
-
-__device__ __forceinline__ void hlog_table(double2* tab) {
-  if (threadIdx.x < 128) {
-    const double c = 1.0 + (threadIdx.x + 0.5) / 128.0;
-    tab[threadIdx.x] = make_double2(1.0 / c, 0.5 * log(c));
-  }
-}
-
-// K(r) from r^2 with K(0) := K0 by a select (no branch; phi_1 / phi_2 branch only for
-// the rare pairs closer than a); distance kernels only.
-template <int KID>
-__device__ __forceinline__ double kfast(double r2, const double2* __restrict__ tab, const KernelParams& kp) {
-  if (KID == H2D_KERNEL_LOG) {
-    const double v = hlog_r2(r2, tab);
-    return r2 > 0.0 ? v : 0.0;
-  } else if (KID == H2D_KERNEL_IMQ) {
-    return rsqrt(fma(r2, kp.inv_c2, 1.0));
-  } else if (KID == H2D_KERNEL_ONE_OVER_R) {
-    const double v = rsqrt(r2);
-    return r2 > 0.0 ? v : 0.0;
-  } else if (KID == H2D_KERNEL_RBF_PHI1) {
-    double v = hlog_r2(r2, tab) * kp.inv_log_a;          // log r / log a
-    if (r2 < kp.a2) {
-      const double r = sqrt(r2);
-      v = r2 > 0.0 ? fma(r, log(r), -1.0) * kp.inv_phi1_den : 0.0;
-    }
-    return v;
-  } else {   // H2D_KERNEL_RBF_PHI2
-    const double v = kp.a * rsqrt(r2);
-    return r2 >= kp.a2 ? v : sqrt(r2) / kp.a;
-  }
-}
-
-template <int KID>
-constexpr bool kDistKernel = KID == H2D_KERNEL_LOG || KID == H2D_KERNEL_IMQ || KID == H2D_KERNEL_ONE_OVER_R ||
-                             KID == H2D_KERNEL_RBF_PHI1 || KID == H2D_KERNEL_RBF_PHI2;
-template <int KID>
-constexpr bool kNeedsLogTable = KID == H2D_KERNEL_LOG || KID == H2D_KERNEL_RBF_PHI1;
-
 template <int KID>
 __device__ __forceinline__ double p2p_eval(const KernelParams& kp, const double2* tab, double px,
                                            double py, double qx, double qy) {
@@ -586,23 +476,6 @@ __device__ __noinline__ void sym_block(int mode, int64_t a0, int m, int64_t b0, 
       }
     }
   }
-}
-
-__device__ __forceinline__ uint32_t p2p_spread(uint32_t v) {
-  v &= 0xFFFFu;
-  v = (v | (v << 8)) & 0x00FF00FFu;
-  v = (v | (v << 4)) & 0x0F0F0F0Fu;
-  v = (v | (v << 2)) & 0x33333333u;
-  v = (v | (v << 1)) & 0x55555555u;
-  return v;
-}
-__device__ __forceinline__ uint32_t p2p_compact(uint32_t v) {
-  v &= 0x55555555u;
-  v = (v | (v >> 1)) & 0x33333333u;
-  v = (v | (v >> 2)) & 0x0F0F0F0Fu;
-  v = (v | (v >> 4)) & 0x00FF00FFu;
-  v = (v | (v >> 8)) & 0x0000FFFFu;
-  return v;
 }
 
 template <int KID>

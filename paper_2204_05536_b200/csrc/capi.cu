@@ -68,6 +68,13 @@ static void clear_factors(Handle& h) {
     h.release(L.d_ucolbase); L.d_ucolbase = nullptr;
     h.release(L.d_uoff); L.d_uoff = nullptr;
   }
+  for (void* q : {(void*)h.m_aitems, (void*)h.m_ritems, (void*)h.m_rcount, (void*)h.m_tpart, (void*)h.m_xm,
+                  (void*)h.m_xcols, (void*)h.m_t, (void*)h.m_yfar, (void*)h.m_ynear})
+    h.release(q);
+  h.m_aitems = nullptr; h.m_ritems = nullptr; h.m_rcount = nullptr; h.m_tpart = nullptr;
+  h.m_xm = h.m_xcols = h.m_t = h.m_yfar = h.m_ynear = nullptr;
+  h.m_n_aitems = 0;
+  h.multi_ready = false;
   h.release(h.d_bitems); h.d_bitems = nullptr;
   h.release(h.d_blev); h.d_blev = nullptr;
   h.n_bitems = 0;
@@ -407,6 +414,43 @@ int hodlr2d_matvec_ex(hodlr2d_t H, const double* x, double* y, int order) {
   H2D_TRY
   if (!H) throw Error{H2D_EINVAL, "null handle"};
   do_matvec(H->h, x, y, order);
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_matvec_multi(hodlr2d_t H, const double* X, double* Y, int nrhs, int order) {
+  H2D_TRY
+  if (!H || !X || !Y) throw Error{H2D_EINVAL, "null argument"};
+  if (nrhs < 1) throw Error{H2D_EINVAL, "nrhs < 1"};
+  Handle& h = H->h;
+  if (order != H2D_ORDER_ORIGINAL && order != H2D_ORDER_TREE) throw Error{H2D_EINVAL, "bad order"};
+  cudaStream_t s = h.stream;
+  const int64_t xlen = h.n;
+  const int64_t ylen = order == H2D_ORDER_ORIGINAL ? h.n : h.row_end - h.row_begin;
+  const bool xdev = is_device_ptr(X), ydev = is_device_ptr(Y);
+  const double* dX = X;
+  double* dY = Y;
+  double *tx = nullptr, *ty = nullptr;
+  if (!xdev) {
+    H2D_CUDA(cudaMallocAsync(&tx, (size_t)nrhs * xlen * sizeof(double), s));
+    H2D_CUDA(cudaMemcpyAsync(tx, X, (size_t)nrhs * xlen * sizeof(double), cudaMemcpyHostToDevice, s));
+    dX = tx;
+  }
+  if (!ydev) {
+    H2D_CUDA(cudaMallocAsync(&ty, (size_t)nrhs * ylen * sizeof(double), s));
+    dY = ty;
+  }
+  try {
+    matvec_multi(h, dX, dY, nrhs, order);
+  } catch (...) {
+    if (tx) cudaFreeAsync(tx, s);
+    if (ty) cudaFreeAsync(ty, s);
+    throw;
+  }
+  if (!ydev) H2D_CUDA(cudaMemcpyAsync(Y, dY, (size_t)nrhs * ylen * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (tx) H2D_CUDA(cudaFreeAsync(tx, s));
+  if (ty) H2D_CUDA(cudaFreeAsync(ty, s));
+  if (!ydev || !xdev) H2D_CUDA(cudaStreamSynchronize(s));
   return H2D_OK;
   H2D_CATCH
 }

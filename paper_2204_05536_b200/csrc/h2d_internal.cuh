@@ -224,6 +224,14 @@ struct Handle {
   int32_t* d_p2p_fast = nullptr;          // leaves of the persistent fast P2P kernel
   int32_t* d_p2p_gen = nullptr;           // leaves of the generic P2P kernel
   int64_t n_p2p_fast = 0, n_p2p_gen = 0;
+  // multi-RHS (multi.cu): tiled stage-A schedule and per-chunk buffers (<= 8 vectors)
+  bool multi_ready = false;
+  AItem* m_aitems = nullptr;
+  int64_t m_n_aitems = 0;
+  RItem* m_ritems = nullptr;
+  int32_t* m_rcount = nullptr;
+  double *m_tpart = nullptr, *m_xm = nullptr, *m_xcols = nullptr, *m_t = nullptr;
+  double *m_yfar = nullptr, *m_ynear = nullptr;
   double* d_ynear = nullptr;              // [3n] near-field P2P slots (p2p_sym_kernel)
   double* d_yfar = nullptr;               // [served] low-rank part (stage B output)
   cudaStream_t hi_stream = nullptr;       // stages A, B (high priority)
@@ -289,6 +297,7 @@ constexpr int kEventsPerMatvec = 8;
 void begin_matvec_timing(Handle& h);
 void mark_after_input(Handle& h);
 void unpad_gathered(Handle& h, const double* d_xg, double* d_xtree);  // apply.cu (S11 epilogue)
+void matvec_multi(Handle& h, const double* d_X, double* d_Y, int nrhs, int order);  // multi.cu
 void gmres_solve(Handle& h, const double* d_b, double* d_x, double tol, int restart, int max_iter,
                  int* iters, double* relres);                             // gmres.cu
 

@@ -1,0 +1,867 @@
+// Multi-RHS HODLR2D matvec (NEXT N2): Y = A X for a batch of vectors, every factor panel
+// streamed once per chunk of NR <= 8 vectors (the paper applies its matvec to "ten
+// different input vectors psi").  Same operator, same three stages as apply.cu; the
+// low-rank stages do NR FMAs per factor element loaded and the near field NR FMAs per
+// kernel evaluation, so the HBM-bound matvec becomes NR times more arithmetic-intense.
+//
+// Layouts (TREE order): x_m[s * NR + j] and t_m[q * NR + j], yfar_m[r * NR + j] interleave
+// the vectors so a stage's vector data is one contiguous run; x_cols[j * N + s] and
+// ynear_m[j * N + s] keep one vector per column for the near field.
+//
+// Stage A items are tiled to <= 2 * kCons columns so a consumer thread owns one column
+// pair x NR accumulators; the near field is evaluated per leaf in both directions
+// (row sums only: one writer per output row, no column reduction; twice the kernel
+// evaluations of the symmetric single-vector kernel, amortised over NR vectors).
+#include <algorithm>
+#include <cstdlib>
+#include <numeric>
+
+#include "pipe.cuh"
+
+namespace h2d {
+namespace {
+
+constexpr int kTileW = 2 * kCons;    // stage-A column tile (<= kCons pairs)
+constexpr int kMaxNR = 8;            // vectors per chunk
+constexpr int kBRowsMax = 224;       // stage-B item rows (apply.cu kBRows)
+
+// ---------------------------------------------------------------- stage A (multi)
+// Stage header: a = W (tile width), b = Wp (row stride of the stage, W rounded up to even),
+// c = out, d = ritem.
+template <int NS, int NR>
+__device__ void mA_producer(PipeSmem<NS>& S, const AItem* __restrict__ items, int n_items, int32_t* counter,
+                            const LevelPtrs& lp, const double* __restrict__ xm) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = l2_evict_first_policy();
+  int stage = 0;
+  uint32_t phase = 0;
+  int idx = 0, nidx = 0;
+  if (lane == 0) idx = atomicAdd(counter, 1);
+  idx = __shfl_sync(0xffffffffu, idx, 0);
+  if (lane == 0) nidx = atomicAdd(counter, 1);
+  AItem nit{};
+  if (idx < n_items) nit = items[idx];
+  for (;;) {
+    const bool done = idx >= n_items;
+    const AItem it = nit;
+    const int cur = idx;
+    idx = __shfl_sync(0xffffffffu, nidx, 0);
+    if (!done && lane == 0) nidx = atomicAdd(counter, 1);
+    if (!done && idx < n_items) nit = items[idx];
+    const int Wp = (it.R + 1) & ~1;
+    const bool contiguous = Wp == it.Rp;
+    const int rows_s = done ? 1 : min(kStageVec / NR, kStageDbl / max(Wp, 2));
+    const double* V = done ? nullptr : lp.V[it.level] + it.v_off;
+    int r0 = 0;
+    do {
+      const int rows = done ? 0 : min(rows_s, it.nrows - r0);
+      mbar_wait(&S.empty[stage], phase ^ 1);
+      if (lane == 0) {
+        StageHdr& h = S.hdr[stage];
+        h.item = done ? -1 : cur;
+        h.cnt = rows;
+        h.flags = (r0 == 0 ? kFirst : 0) | (r0 + rows >= it.nrows ? kLast : 0);
+        h.a = it.R;
+        h.b = Wp;
+        h.c = it.out;
+        h.d = it.ritem;
+        const uint32_t bytes = (uint32_t)rows * (uint32_t)Wp * 8u;
+        mbar_arrive_expect_tx(&S.full[stage], bytes);
+        if (bytes && contiguous) bulk_g2s(S.ring[stage], V + (int64_t)r0 * it.Rp, bytes, &S.full[stage], pol);
+      }
+      if (!contiguous)
+        for (int r = lane; r < rows; r += 32)
+          bulk_g2s(S.ring[stage] + r * Wp, V + (int64_t)(r0 + r) * it.Rp, (uint32_t)Wp * 8u, &S.full[stage], pol);
+      const double* xs = xm + (it.x_off + r0) * NR;
+      for (int e = lane; e < rows * NR; e += 32) cp_async8(&S.vec[stage][e], xs + e);
+      cp_async_arrive_noinc(&S.full[stage]);
+      if (++stage == NS) { stage = 0; phase ^= 1; }
+      r0 += rows;
+    } while (!done && r0 < it.nrows);
+    if (done) break;
+  }
+}
+
+template <int NS, int NR>
+__device__ void mA_consumers(PipeSmem<NS>& S, const int32_t* __restrict__ vdst, double* __restrict__ tm,
+                             double* __restrict__ tpartm, const RItem* __restrict__ ritems,
+                             int32_t* __restrict__ rcount) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  int stage = 0;
+  uint32_t phase = 0;
+  int W = 1, Wp = 2, P = 1, G = 1, g = 0, p = 0;
+  double acc[2 * NR];
+#pragma unroll
+  for (int c = 0; c < 2 * NR; ++c) acc[c] = 0.0;
+  for (;;) {
+    mbar_wait(&S.full[stage], phase);
+    const StageHdr h = S.hdr[stage];
+    if (h.item < 0) break;
+    if (h.flags & kFirst) {
+      W = h.a;
+      Wp = h.b;
+      P = Wp >> 1;
+      G = kCons / P;
+      g = tid / P;
+      p = tid - g * P;
+#pragma unroll
+      for (int c = 0; c < 2 * NR; ++c) acc[c] = 0.0;
+    }
+    if (g < G) {
+      const double* __restrict__ v = S.ring[stage] + (size_t)g * Wp + 2 * p;
+      const double* __restrict__ sx = S.vec[stage] + (size_t)g * NR;
+      const int step = G * Wp;
+      for (int j = g; j < h.cnt; j += G, v += step, sx += G * NR) {
+        const double2 a = *reinterpret_cast<const double2*>(v);
+#pragma unroll
+        for (int k = 0; k < NR; k += 2) {
+          const double2 xv = *reinterpret_cast<const double2*>(sx + k);
+          acc[k] = fma(a.x, xv.x, acc[k]);
+          acc[NR + k] = fma(a.y, xv.x, acc[NR + k]);
+          if (k + 1 < NR) {
+            acc[k + 1] = fma(a.x, xv.y, acc[k + 1]);
+            acc[NR + k + 1] = fma(a.y, xv.y, acc[NR + k + 1]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[stage]);
+    if (++stage == NS) { stage = 0; phase ^= 1; }
+    if (!(h.flags & kLast)) continue;
+    // ---- end of item: per vector, sum the G groups of each column pair
+    auto put = [&](int q, int k, double v) {
+      if (q >= W) return;
+      if (h.c >= 0) tm[(int64_t)vdst[h.c + q] * NR + k] = v;
+      else tpartm[((int64_t)(-h.c - 1) + q) * NR + k] = v;
+    };
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      if (G > 1) {
+        S.red[2 * tid] = g < G ? acc[k] : 0.0;
+        S.red[2 * tid + 1] = g < G ? acc[NR + k] : 0.0;
+        named_bar_sync(1, kCons);
+        if (tid < P) {
+          double u0 = 0.0, u1 = 0.0;
+          for (int gg = 0; gg < G; ++gg) {
+            u0 += S.red[2 * (tid + gg * P)];
+            u1 += S.red[2 * (tid + gg * P) + 1];
+          }
+          put(2 * tid, k, u0);
+          put(2 * tid + 1, k, u1);
+        }
+        named_bar_sync(1, kCons);
+      } else if (tid < P) {
+        put(2 * tid, k, acc[k]);
+        put(2 * tid + 1, k, acc[NR + k]);
+      }
+    }
+    if (h.d >= 0) {
+      named_bar_sync(1, kCons);
+      if (tid == 0) {
+        __threadfence();
+        const int last = atomicAdd(rcount + h.d, 1) == ritems[h.d].nchunks - 1;
+        if (last) __threadfence();
+        S.flag = last;
+      }
+      named_bar_sync(1, kCons);
+      if (S.flag) {
+        const RItem ri = ritems[h.d];
+        for (int e = tid; e < ri.R * NR; e += kCons) {
+          const int q = e / NR, k = e - q * NR;
+          const double* __restrict__ pp = tpartm + ((int64_t)ri.p_off + q) * NR + k;
+          const int64_t cs = (int64_t)ri.R * NR;
+          double a0 = 0.0, a1 = 0.0;
+          int c = 0;
+          for (; c + 1 < ri.nchunks; c += 2) {
+            a0 += __ldcg(pp + c * cs);
+            a1 += __ldcg(pp + (c + 1) * cs);
+          }
+          if (c < ri.nchunks) a0 += __ldcg(pp + c * cs);
+          tm[(int64_t)vdst[ri.vpos + q] * NR + k] = a0 + a1;
+        }
+        if (tid == 0) rcount[h.d] = 0;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- FP64 tensor cores (NR = 8)
+// With 8 vectors both low-rank stages are small dense fp64 contractions, T = V^T X and
+// Y = U T with N = 8 = the vector count, so they run on the FP64 tensor cores (DMMA,
+// mma.sync m8n8k4 f64 — tcgen05 has no f64 kind): 256 FMAs per warp instruction instead of
+// 32, which takes the consumers off the issue limit.  Fragments (PTX m8n8k4 .f64): lane t
+// holds A[t/4][t%4], B[t%4][t/4] and D[t/4][2(t%4) + {0,1}].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int kConsWarps = kCons / 32;
+constexpr int kMaxMTA = (kTileW / 8 + kConsWarps - 1) / kConsWarps;   // m-tiles per warp, stage A
+constexpr int kMaxMTB = (kBRowsMax / 8 + kConsWarps - 1) / kConsWarps; // m-tiles per warp, stage B
+
+// Stage A: M = tile columns (m-tile i of the item owned by warp i % 7, all rows), N = the 8
+// vectors, K = rows, 4 per DMMA.  No cross-warp reduction: every T entry has one owner.
+template <int NS>
+__device__ void mA_consumers_dmma(PipeSmem<NS>& S, const int32_t* __restrict__ vdst, double* __restrict__ tm,
+                                  double* __restrict__ tpartm, const RItem* __restrict__ ritems,
+                                  int32_t* __restrict__ rcount) {
+  constexpr int NR = 8;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  int stage = 0;
+  uint32_t phase = 0;
+  int W = 1, Wp = 2, MT = 1;
+  double d[kMaxMTA][2];
+#pragma unroll
+  for (int i = 0; i < kMaxMTA; ++i) d[i][0] = d[i][1] = 0.0;
+  for (;;) {
+    mbar_wait(&S.full[stage], phase);
+    const StageHdr h = S.hdr[stage];
+    if (h.item < 0) break;
+    if (h.flags & kFirst) {
+      W = h.a;
+      Wp = h.b;
+      MT = (W + 7) >> 3;
+#pragma unroll
+      for (int i = 0; i < kMaxMTA; ++i) d[i][0] = d[i][1] = 0.0;
+    }
+    const double* __restrict__ sv = S.ring[stage];
+    const double* __restrict__ sx = S.vec[stage];
+    const int rows = h.cnt;
+    for (int k0 = 0; k0 < rows; k0 += 4) {
+      const int r = k0 + tq;
+      const bool rv = r < rows;
+      const double b = rv ? sx[r * NR + gq] : 0.0;
+#pragma unroll
+      for (int i = 0; i < kMaxMTA; ++i) {
+        const int mt = w + kConsWarps * i;
+        if (mt < MT) {
+          const int c = mt * 8 + gq;
+          const double a = (rv && c < Wp) ? sv[r * Wp + c] : 0.0;
+          dmma884(d[i][0], d[i][1], a, b);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[stage]);
+    if (++stage == NS) { stage = 0; phase ^= 1; }
+    if (!(h.flags & kLast)) continue;
+#pragma unroll
+    for (int i = 0; i < kMaxMTA; ++i) {
+      const int mt = w + kConsWarps * i;
+      const int q = mt * 8 + gq;
+      if (mt < MT && q < W) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int k = 2 * tq + e;
+          if (h.c >= 0) tm[(int64_t)vdst[h.c + q] * NR + k] = d[i][e];
+          else tpartm[((int64_t)(-h.c - 1) + q) * NR + k] = d[i][e];
+        }
+      }
+    }
+    if (h.d >= 0) {
+      named_bar_sync(1, kCons);
+      if (tid == 0) {
+        __threadfence();
+        const int last = atomicAdd(rcount + h.d, 1) == ritems[h.d].nchunks - 1;
+        if (last) __threadfence();
+        S.flag = last;
+      }
+      named_bar_sync(1, kCons);
+      if (S.flag) {
+        const RItem ri = ritems[h.d];
+        for (int e = tid; e < ri.R * NR; e += kCons) {
+          const int q = e / NR, k = e - q * NR;
+          const double* __restrict__ pp = tpartm + ((int64_t)ri.p_off + q) * NR + k;
+          const int64_t cs = (int64_t)ri.R * NR;
+          double a0 = 0.0, a1 = 0.0;
+          int c = 0;
+          for (; c + 1 < ri.nchunks; c += 2) {
+            a0 += __ldcg(pp + c * cs);
+            a1 += __ldcg(pp + (c + 1) * cs);
+          }
+          if (c < ri.nchunks) a0 += __ldcg(pp + c * cs);
+          tm[(int64_t)vdst[ri.vpos + q] * NR + k] = a0 + a1;
+        }
+        if (tid == 0) rcount[h.d] = 0;
+      }
+    }
+  }
+}
+
+// Stage B: M = leaf rows, N = the 8 vectors, K = U columns.  Leaves of <= 64 rows (<= 8
+// m-tiles, the configs' case) split K over the 7 warps (every warp all m-tiles, K steps
+// 4w, 4w + 28, ...) and reduce the 7 partials per m-tile in smem at the end of the item;
+// taller row blocks give m-tile i to warp i % 7.
+constexpr int kMaxMTK = 8;
+template <int NS>
+__device__ void mB_consumers_dmma(PipeSmem<NS>& S, double* __restrict__ yfarm) {
+  constexpr int NR = 8;
+  constexpr int kD = kMaxMTK > kMaxMTB ? kMaxMTK : kMaxMTB;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  int stage = 0;
+  uint32_t phase = 0;
+  int rows = 1, rowsp = 2, MT = 1;
+  bool ksplit = true;
+  double d[kD][2];
+#pragma unroll
+  for (int i = 0; i < kD; ++i) d[i][0] = d[i][1] = 0.0;
+  for (;;) {
+    mbar_wait(&S.full[stage], phase);
+    const StageHdr h = S.hdr[stage];
+    if (h.item < 0) break;
+    if (h.flags & kFirst) {
+      rows = h.a;
+      rowsp = h.b;
+      MT = (rows + 7) >> 3;
+      ksplit = MT <= kMaxMTK;
+#pragma unroll
+      for (int i = 0; i < kD; ++i) d[i][0] = d[i][1] = 0.0;
+    }
+    const double* __restrict__ su = S.ring[stage];
+    const double* __restrict__ tv = S.vec[stage];
+    const int cols = h.cnt;
+    if (ksplit) {
+      for (int k0 = 4 * w; k0 < cols; k0 += 4 * kConsWarps) {
+        const int c = k0 + tq;
+        const bool cv = c < cols;
+        const double b = cv ? tv[c * NR + gq] : 0.0;
+        const double* __restrict__ col = su + c * rowsp + gq;
+#pragma unroll
+        for (int i = 0; i < kMaxMTK; ++i) {
+          if (i < MT) {
+            const int r = i * 8 + gq;
+            const double a = (cv && r < rowsp) ? col[i * 8] : 0.0;
+            dmma884(d[i][0], d[i][1], a, b);
+          }
+        }
+      }
+    } else {
+      for (int k0 = 0; k0 < cols; k0 += 4) {
+        const int c = k0 + tq;
+        const bool cv = c < cols;
+        const double b = cv ? tv[c * NR + gq] : 0.0;
+#pragma unroll
+        for (int i = 0; i < kMaxMTB; ++i) {
+          const int mt = w + kConsWarps * i;
+          if (mt < MT) {
+            const int r = mt * 8 + gq;
+            const double a = (cv && r < rowsp) ? su[c * rowsp + r] : 0.0;
+            dmma884(d[i][0], d[i][1], a, b);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[stage]);
+    if (++stage == NS) { stage = 0; phase ^= 1; }
+    if (!(h.flags & kLast)) continue;
+    if (ksplit) {
+#pragma unroll
+      for (int i = 0; i < kMaxMTK; ++i) {
+        if (i < MT) {
+          S.red[w * 64 + gq * 8 + 2 * tq] = d[i][0];
+          S.red[w * 64 + gq * 8 + 2 * tq + 1] = d[i][1];
+          named_bar_sync(1, kCons);
+          if (tid < 64) {
+            const int r = i * 8 + (tid >> 3);
+            double u = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < kConsWarps; ++ww) u += S.red[ww * 64 + tid];
+            if (r < rows) yfarm[(int64_t)(h.c + r) * NR + (tid & 7)] = u;
+          }
+          named_bar_sync(1, kCons);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kMaxMTB; ++i) {
+        const int mt = w + kConsWarps * i;
+        const int r = mt * 8 + gq;
+        if (mt < MT && r < rows) {
+          double2* dst = reinterpret_cast<double2*>(yfarm + (int64_t)(h.c + r) * NR + 2 * tq);
+          *dst = make_double2(d[i][0], d[i][1]);
+        }
+      }
+    }
+  }
+}
+
+template <int NR>
+constexpr int kMultiMinBlocks = 3;
+
+template <int NS, int NR>
+__global__ void __launch_bounds__(kPipeThreads, kMultiMinBlocks<NR>)
+stageA_multi_kernel(const AItem* __restrict__ items, int n_items, int32_t* counter, LevelPtrs lp,
+                    const double* __restrict__ xm, const int32_t* __restrict__ vdst, double* __restrict__ tm,
+                    double* __restrict__ tpartm, const RItem* __restrict__ ritems, int32_t* __restrict__ rcount) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  PipeSmem<NS>& S = *reinterpret_cast<PipeSmem<NS>*>(smem_raw);
+  pipe_init(S);
+  if (threadIdx.x >= kCons) mA_producer<NS, NR>(S, items, n_items, counter, lp, xm);
+  else if constexpr (NR == 8) mA_consumers_dmma<NS>(S, vdst, tm, tpartm, ritems, rcount);
+  else mA_consumers<NS, NR>(S, vdst, tm, tpartm, ritems, rcount);
+}
+
+// ---------------------------------------------------------------- stage B (multi)
+template <int NS, int NR>
+__device__ void mB_producer(PipeSmem<NS>& S, const BItem* __restrict__ items, const BLevel* __restrict__ blev,
+                            int n_items, int32_t* counter, int kappa, const LevelPtrs& lp,
+                            const double* const* __restrict__ tml) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = l2_evict_first_policy();
+  int stage = 0;
+  uint32_t phase = 0;
+  int idx = 0, nidx = 0;
+  if (lane == 0) idx = atomicAdd(counter, 1);
+  idx = __shfl_sync(0xffffffffu, idx, 0);
+  if (lane == 0) nidx = atomicAdd(counter, 1);
+  BItem nit{};
+  BLevel nlv{0, 0, 0};
+  if (idx < n_items) {
+    nit = items[idx];
+    if (lane < kappa) nlv = blev[(int64_t)idx * kappa + lane];
+  }
+  for (;;) {
+    const bool done = idx >= n_items;
+    const BItem it = nit;
+    const BLevel lv = nlv;
+    const int cur = idx;
+    idx = __shfl_sync(0xffffffffu, nidx, 0);
+    if (!done && lane == 0) nidx = atomicAdd(counter, 1);
+    if (!done && idx < n_items) {
+      nit = items[idx];
+      if (lane < kappa) nlv = blev[(int64_t)idx * kappa + lane];
+    }
+    const int mL = it.mL;
+    const int mLp = (mL + 1) & ~1, rowsp = (it.rows + 1) & ~1;
+    const bool whole = !done && it.rows == mL;
+    const int R = done || lane >= kappa ? 0 : lv.R;
+    const unsigned nz = __ballot_sync(0xffffffffu, R > 0);
+    const int lastl = nz ? 32 - __clz(nz) : 0;
+    if (done || nz == 0) {
+      mbar_wait(&S.empty[stage], phase ^ 1);
+      if (lane == 0) {
+        StageHdr& h = S.hdr[stage];
+        h.item = done ? -1 : cur;
+        h.cnt = 0;
+        h.flags = kFirst | kLast;
+        h.a = it.rows;
+        h.b = rowsp;
+        h.c = it.yrow;
+        mbar_arrive_expect_tx(&S.full[stage], 0);
+      }
+      cp_async_arrive_noinc(&S.full[stage]);
+      if (++stage == NS) { stage = 0; phase ^= 1; }
+      if (done) break;
+      continue;
+    }
+    const int cols_s = min(kStageVec / NR, kStageDbl / rowsp);
+    bool first = true;
+    for (int li = 0; li < lastl; ++li) {
+      const int Rl = __shfl_sync(0xffffffffu, R, li);
+      const int cbl = __shfl_sync(0xffffffffu, lv.tcol, li);
+      const int64_t ubl = __shfl_sync(0xffffffffu, lv.uoff, li);
+      if (Rl == 0) continue;
+      const double* Ub = lp.U[li + 1] + ubl;
+      const double* tb = tml[li + 1] + (int64_t)cbl * NR;
+      for (int c0 = 0; c0 < Rl; c0 += cols_s) {
+        const int cols = min(cols_s, Rl - c0);
+        const bool last = li == lastl - 1 && c0 + cols >= Rl;
+        mbar_wait(&S.empty[stage], phase ^ 1);
+        if (lane == 0) {
+          StageHdr& h = S.hdr[stage];
+          h.item = cur;
+          h.cnt = cols;
+          h.flags = (first ? kFirst : 0) | (last ? kLast : 0);
+          h.a = it.rows;
+          h.b = rowsp;
+          h.c = it.yrow;
+          mbar_arrive_expect_tx(&S.full[stage], (uint32_t)cols * (uint32_t)rowsp * 8u);
+          if (whole)
+            bulk_g2s(S.ring[stage], Ub + (int64_t)c0 * mLp, (uint32_t)cols * (uint32_t)mLp * 8u, &S.full[stage], pol);
+        }
+        if (!whole)
+          for (int c = lane; c < cols; c += 32)
+            bulk_g2s(S.ring[stage] + c * rowsp, Ub + (int64_t)(c0 + c) * mLp + it.r0, (uint32_t)rowsp * 8u,
+                     &S.full[stage], pol);
+        const double* ts = tb + (int64_t)c0 * NR;
+        for (int e = lane; e < cols * NR; e += 32) cp_async8(&S.vec[stage][e], ts + e);
+        cp_async_arrive_noinc(&S.full[stage]);
+        if (++stage == NS) { stage = 0; phase ^= 1; }
+        first = false;
+      }
+    }
+  }
+}
+
+template <int NS, int NR>
+__device__ void mB_consumers(PipeSmem<NS>& S, double* __restrict__ yfarm) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  int stage = 0;
+  uint32_t phase = 0;
+  int rows = 1, rowsp = 2, G = 1, g = 0, i = 0, RP = 1;
+  double acc[2 * NR];
+#pragma unroll
+  for (int c = 0; c < 2 * NR; ++c) acc[c] = 0.0;
+  for (;;) {
+    mbar_wait(&S.full[stage], phase);
+    const StageHdr h = S.hdr[stage];
+    if (h.item < 0) break;
+    if (h.flags & kFirst) {
+      rows = h.a;
+      rowsp = h.b;
+      RP = rowsp >> 1;
+      G = kCons / RP;
+      g = tid / RP;
+      i = tid - g * RP;
+#pragma unroll
+      for (int c = 0; c < 2 * NR; ++c) acc[c] = 0.0;
+    }
+    if (g < G) {
+      const double* __restrict__ u = S.ring[stage] + (size_t)g * rowsp + 2 * i;
+      const double* __restrict__ tv = S.vec[stage] + (size_t)g * NR;
+      const int step = G * rowsp;
+      for (int c = g; c < h.cnt; c += G, u += step, tv += G * NR) {
+        const double2 a = *reinterpret_cast<const double2*>(u);
+#pragma unroll
+        for (int k = 0; k < NR; k += 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(tv + k);
+          acc[k] = fma(a.x, t2.x, acc[k]);
+          acc[NR + k] = fma(a.y, t2.x, acc[NR + k]);
+          if (k + 1 < NR) {
+            acc[k + 1] = fma(a.x, t2.y, acc[k + 1]);
+            acc[NR + k + 1] = fma(a.y, t2.y, acc[NR + k + 1]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[stage]);
+    if (++stage == NS) { stage = 0; phase ^= 1; }
+    if (!(h.flags & kLast)) continue;
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      S.red[2 * tid] = g < G ? acc[k] : 0.0;
+      S.red[2 * tid + 1] = g < G ? acc[NR + k] : 0.0;
+      named_bar_sync(1, kCons);
+      if (tid < rows) {
+        const int ip = tid >> 1, e = tid & 1;
+        double u = 0.0;
+        for (int gg = 0; gg < G; ++gg) u += S.red[2 * (ip + gg * RP) + e];
+        yfarm[(int64_t)(h.c + tid) * NR + k] = u;
+      }
+      named_bar_sync(1, kCons);
+    }
+  }
+}
+
+struct TmPtrs {
+  const double* p[H2D_MAX_LEVELS + 1];
+};
+
+template <int NS, int NR>
+__global__ void __launch_bounds__(kPipeThreads, kMultiMinBlocks<NR>)
+stageB_multi_kernel(const BItem* __restrict__ items, const BLevel* __restrict__ blev, int n_items,
+                    int32_t* counter, int kappa, LevelPtrs lp, TmPtrs tml, double* __restrict__ yfarm) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  PipeSmem<NS>& S = *reinterpret_cast<PipeSmem<NS>*>(smem_raw);
+  pipe_init(S);
+  if (threadIdx.x >= kCons) mB_producer<NS, NR>(S, items, blev, n_items, counter, kappa, lp, tml.p);
+  else if constexpr (NR == 8) mB_consumers_dmma<NS>(S, yfarm);
+  else mB_consumers<NS, NR>(S, yfarm);
+}
+
+// ---------------------------------------------------------------- near field (multi)
+// One CTA per served leaf X; rows of X in blocks of <= 128, thread (g, i) = (tid / RB,
+// tid % RB) owns row i and the tile columns g, g + G, ...; every column tile (<= 96
+// points of {X} u E_X) is staged in smem with its NR x values; K(r) is evaluated once
+// per (row, column) and applied to the NR vectors.  ynear_m[k * n + row] = sum_Y K x_Y.
+constexpr int kMTile = 96, kMRows = 128;
+
+template <int KID>
+__device__ __forceinline__ double keval_m(const KernelParams& kp, const double2* tab, double px, double py,
+                                          double qx, double qy) {
+  if constexpr (kDistKernel<KID>) {
+    const double dx = px - qx, dy = py - qy;
+    return kfast<KID>(fma(dx, dx, dy * dy), tab, kp);
+  }
+  return kernel_eval_t<KID>(kp, px, py, qx, qy);
+}
+
+template <int KID, int NR>
+__global__ void __launch_bounds__(256, 3)
+p2p_multi_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_start,
+                 const double* __restrict__ px, const double* __restrict__ py,
+                 const double* __restrict__ xcols, int64_t n, KernelParams kp, double* __restrict__ ynearm) {
+  __shared__ double tpx[kMTile], tpy[kMTile], tx[NR][kMTile];
+  __shared__ double red[256];
+  __shared__ double2 tab[128];
+  const int tid = threadIdx.x;
+  if (kNeedsLogTable<KID>) hlog_table(tab);
+  const int64_t X = leaf_begin + blockIdx.x;
+  const uint32_t cx = p2p_compact((uint32_t)X), cy = p2p_compact((uint32_t)X >> 1);
+  const uint32_t side = 1u << kappa;
+  int64_t nb[5];
+  int nn = 0;
+  nb[nn++] = X;
+  if (cx + 1 < side) nb[nn++] = (int64_t)(p2p_spread(cx + 1) | (p2p_spread(cy) << 1));
+  if (cy + 1 < side) nb[nn++] = (int64_t)(p2p_spread(cx) | (p2p_spread(cy + 1) << 1));
+  if (cx > 0) nb[nn++] = (int64_t)(p2p_spread(cx - 1) | (p2p_spread(cy) << 1));
+  if (cy > 0) nb[nn++] = (int64_t)(p2p_spread(cx) | (p2p_spread(cy - 1) << 1));
+  const int64_t xs = leaf_start[X];
+  const int m = leaf_start[X + 1] - (int)xs;
+  for (int rb = 0; rb < m; rb += kMRows) {
+    const int RB = min(kMRows, m - rb), G = 256 / RB;
+    const int g = tid / RB, i = tid - g * RB;
+    const bool act = g < G;
+    const double rpx = act ? px[xs + rb + i] : 0.0, rpy = act ? py[xs + rb + i] : 0.0;
+    double racc[NR];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) racc[k] = 0.0;
+    for (int a = 0; a < nn; ++a) {
+      const int64_t ys = leaf_start[nb[a]];
+      const int ny = leaf_start[nb[a] + 1] - (int)ys;
+      for (int cb = 0; cb < ny; cb += kMTile) {
+        const int nt = min(kMTile, ny - cb);
+        __syncthreads();
+        for (int e = tid; e < nt; e += 256) {
+          tpx[e] = px[ys + cb + e];
+          tpy[e] = py[ys + cb + e];
+#pragma unroll
+          for (int k = 0; k < NR; ++k) tx[k][e] = xcols[(int64_t)k * n + ys + cb + e];
+        }
+        __syncthreads();
+        if (act) {
+          int j = g;
+          for (; j + G < nt; j += 2 * G) {
+            const double k0v = keval_m<KID>(kp, tab, rpx, rpy, tpx[j], tpy[j]);
+            const double k1v = keval_m<KID>(kp, tab, rpx, rpy, tpx[j + G], tpy[j + G]);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) racc[k] = fma(k1v, tx[k][j + G], fma(k0v, tx[k][j], racc[k]));
+          }
+          if (j < nt) {
+            const double k0v = keval_m<KID>(kp, tab, rpx, rpy, tpx[j], tpy[j]);
+#pragma unroll
+            for (int k = 0; k < NR; ++k) racc[k] = fma(k0v, tx[k][j], racc[k]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      __syncthreads();
+      red[tid] = act ? racc[k] : 0.0;
+      __syncthreads();
+      if (tid < RB) {
+        double u = 0.0;
+        for (int gg = 0; gg < G; ++gg) u += red[gg * RB + tid];
+        ynearm[(int64_t)k * n + xs + rb + tid] = u;
+      }
+    }
+  }
+}
+
+// x_m[s * NR + k] and x_cols[k * n + s] from NR vectors of length xlen (TREE: X[k*xlen + s],
+// ORIGINAL: X[k*xlen + perm[s]]).
+__global__ void permute_multi_kernel(int NR, const double* __restrict__ X, int64_t xlen,
+                                     const int32_t* __restrict__ perm, int64_t n, double* __restrict__ xm,
+                                     double* __restrict__ xcols) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t src = perm ? perm[s] : s;
+    for (int k = 0; k < NR; ++k) {
+      const double v = X[(int64_t)k * xlen + src];
+      xm[s * NR + k] = v;
+      xcols[(int64_t)k * n + s] = v;
+    }
+  }
+}
+
+// Y[k * ylen + out(r)] = yfar_m[(r - row_begin) * NR + k] + scale ynear_m[k n + r] + shift x
+__global__ void combine_multi_kernel(int NR, int64_t row_begin, int64_t rows, const double* __restrict__ yfarm,
+                                     const double* __restrict__ ynearm, int64_t n, const double* __restrict__ xcols,
+                                     double scale, double shift, double* __restrict__ Y, int64_t ylen,
+                                     const int32_t* __restrict__ perm, int order_out, int64_t y_row0) {
+  for (int64_t kk = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; kk < rows; kk += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = row_begin + kk;
+    const int64_t o = order_out == H2D_ORDER_ORIGINAL ? perm[r] : r - y_row0;
+    for (int k = 0; k < NR; ++k)
+      Y[(int64_t)k * ylen + o] = yfarm[kk * NR + k] + fma(scale, ynearm[(int64_t)k * n + r], shift * xcols[(int64_t)k * n + r]);
+  }
+}
+
+}  // namespace
+
+// Tiled stage-A schedule for the multi-RHS kernels (columns in tiles of <= kTileW).
+static void build_multi_schedule(Handle& h) {
+  std::vector<AItem> items;
+  std::vector<RItem> ritems;
+  int64_t p_len = 0, elems = 0;
+  for (int l = 1; l <= h.kappa; ++l) {
+    const Level& L = h.levels[(size_t)l];
+    for (int64_t Y = 0; Y < L.nbox; ++Y)
+      elems += (h.box_end(l, Y) - h.box_begin(l, Y)) * ((L.vR[(size_t)Y] + 1) & ~1);
+  }
+  const int64_t target = std::min<int64_t>(262144, std::max<int64_t>(16384, elems / (4 * (int64_t)h.persist_ctas)));
+  for (int l = 1; l <= h.kappa; ++l) {
+    const Level& L = h.levels[(size_t)l];
+    for (int64_t Y = 0; Y < L.nbox; ++Y) {
+      const int R = L.vR[(size_t)Y], Rp = (R + 1) & ~1;
+      const int64_t y0 = h.box_begin(l, Y), nY = h.box_end(l, Y) - y0;
+      if (R == 0 || nY == 0) continue;
+      const int32_t vp = (int32_t)L.t_off[(size_t)Y];
+      for (int q0 = 0; q0 < R; q0 += kTileW) {
+        const int Wt = std::min(kTileW, R - q0), Wp = (Wt + 1) & ~1;
+        int64_t nch = std::max<int64_t>(1, (nY * Wp + target - 1) / target);
+        nch = std::min<int64_t>(nY, nch);
+        const int64_t rows = (nY + nch - 1) / nch;
+        nch = (nY + rows - 1) / rows;
+        const int64_t base = L.vpan_off[(size_t)Y] + q0;
+        if (nch == 1) {
+          items.push_back(AItem{base, y0, (int32_t)nY, Wt, vp + q0, l, -1, Rp});
+        } else {
+          if (p_len + nch * Wt > INT32_MAX / kMaxNR) throw Error{H2D_EINVAL, "multi partial buffer too large"};
+          ritems.push_back(RItem{vp + q0, (int32_t)p_len, Wt, (int32_t)nch});
+          for (int64_t c = 0; c < nch; ++c) {
+            const int64_t r0 = c * rows, nr = std::min(rows, nY - r0);
+            items.push_back(AItem{base + r0 * Rp, y0 + r0, (int32_t)nr, Wt, (int32_t)(-(p_len + c * Wt) - 1), l,
+                                  (int32_t)(ritems.size() - 1), Rp});
+          }
+          p_len += nch * Wt;
+        }
+      }
+    }
+  }
+  std::stable_sort(items.begin(), items.end(), [](const AItem& a, const AItem& b) {
+    return (int64_t)a.nrows * a.R > (int64_t)b.nrows * b.R;
+  });
+  cudaStream_t s = h.stream;
+  h.m_n_aitems = (int64_t)items.size();
+  h.m_aitems = h.alloc<AItem>(items.size());
+  h.m_ritems = h.alloc<RItem>(ritems.size());
+  h.m_rcount = h.alloc<int32_t>(ritems.size());
+  h.m_tpart = h.alloc<double>((size_t)std::max<int64_t>(1, p_len) * kMaxNR);
+  H2D_CUDA(cudaMemsetAsync(h.m_rcount, 0, std::max<size_t>(1, ritems.size()) * 4, s));
+  if (!items.empty())
+    H2D_CUDA(cudaMemcpyAsync(h.m_aitems, items.data(), items.size() * sizeof(AItem), cudaMemcpyHostToDevice, s));
+  if (!ritems.empty())
+    H2D_CUDA(cudaMemcpyAsync(h.m_ritems, ritems.data(), ritems.size() * sizeof(RItem), cudaMemcpyHostToDevice, s));
+  const int64_t served = h.row_end - h.row_begin;
+  h.m_xm = h.alloc<double>((size_t)h.n * kMaxNR);
+  h.m_xcols = h.alloc<double>((size_t)h.n * kMaxNR);
+  h.m_t = h.alloc<double>((size_t)std::max<int64_t>(1, h.t_len) * kMaxNR);
+  h.m_yfar = h.alloc<double>((size_t)std::max<int64_t>(1, served) * kMaxNR);
+  h.m_ynear = h.alloc<double>((size_t)h.n * kMaxNR);
+  H2D_CUDA(cudaStreamSynchronize(s));
+  h.multi_ready = true;
+}
+
+template <int NR>
+static void set_multi_attrs() {
+  const int smem = (int)sizeof(PipeSmem<kNSShallow>);
+  H2D_CUDA(cudaFuncSetAttribute(stageA_multi_kernel<kNSShallow, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  H2D_CUDA(cudaFuncSetAttribute(stageB_multi_kernel<kNSShallow, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  H2D_CUDA(cudaFuncSetAttribute(stageA_multi_kernel<kNSShallow, NR>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                cudaSharedmemCarveoutMaxShared));
+  H2D_CUDA(cudaFuncSetAttribute(stageB_multi_kernel<kNSShallow, NR>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                cudaSharedmemCarveoutMaxShared));
+}
+
+template <int KID, int NR>
+static void launch_p2p_multi(Handle& h, cudaStream_t a) {
+  const int64_t nleaves = h.leaf_end - h.leaf_begin;
+  if (nleaves <= 0) return;
+  p2p_multi_kernel<KID, NR><<<(int)nleaves, 256, 0, a>>>(h.kappa, h.leaf_begin, h.d_leaf_start, h.d_px, h.d_py,
+                                                         h.m_xcols, h.n, h.kp, h.m_ynear);
+  H2D_LAUNCH_CHECK();
+}
+
+template <int NR>
+static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, int64_t ylen, int order) {
+  cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
+  const int grid = (int)std::min<int64_t>((h.n + 255) / 256, 148 * 16);
+  permute_multi_kernel<<<grid, 256, 0, s>>>(NR, dX, xlen, order == H2D_ORDER_ORIGINAL ? h.d_perm : nullptr, h.n,
+                                            h.m_xm, h.m_xcols);
+  H2D_LAUNCH_CHECK();
+  H2D_CUDA(cudaEventRecord(h.ev_fork, s));
+  H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_fork, 0));
+  H2D_CUDA(cudaStreamWaitEvent(a, h.ev_fork, 0));
+  H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 2 * sizeof(int32_t), hi));
+  const size_t smem = sizeof(PipeSmem<kNSShallow>);
+  if (h.m_n_aitems > 0) {
+    stageA_multi_kernel<kNSShallow, NR><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+        h.m_aitems, (int)h.m_n_aitems, h.d_counters, h.lp, h.m_xm, h.d_vdst, h.m_t, h.m_tpart, h.m_ritems,
+        h.m_rcount);
+    H2D_LAUNCH_CHECK();
+  }
+  if (h.n_bitems > 0) {
+    TmPtrs tml{};
+    for (int l = 1; l <= h.kappa; ++l) tml.p[l] = h.m_t + h.levels[(size_t)l].tu_base * NR;
+    stageB_multi_kernel<kNSShallow, NR><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+        h.d_bitems, h.d_blev, (int)h.n_bitems, h.d_counters + 1, h.kappa, h.lp, tml, h.m_yfar);
+    H2D_LAUNCH_CHECK();
+  }
+  H2D_CUDA(cudaEventRecord(h.ev_far, hi));
+  switch (h.kp.id) {
+    case H2D_KERNEL_LOG: launch_p2p_multi<H2D_KERNEL_LOG, NR>(h, a); break;
+    case H2D_KERNEL_IMQ: launch_p2p_multi<H2D_KERNEL_IMQ, NR>(h, a); break;
+    case H2D_KERNEL_ONE_OVER_R: launch_p2p_multi<H2D_KERNEL_ONE_OVER_R, NR>(h, a); break;
+    case H2D_KERNEL_RBF_PHI1: launch_p2p_multi<H2D_KERNEL_RBF_PHI1, NR>(h, a); break;
+    case H2D_KERNEL_RBF_PHI2: launch_p2p_multi<H2D_KERNEL_RBF_PHI2, NR>(h, a); break;
+    default: launch_p2p_multi<H2D_KERNEL_TEST_LOWRANK, NR>(h, a); break;
+  }
+  H2D_CUDA(cudaEventRecord(h.ev_join, a));
+  H2D_CUDA(cudaStreamWaitEvent(s, h.ev_far, 0));
+  H2D_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
+  const int64_t rows = h.row_end - h.row_begin;
+  if (rows > 0) {
+    const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 148 * 8);
+    combine_multi_kernel<<<blocks, 256, 0, s>>>(NR, h.row_begin, rows, h.m_yfar, h.m_ynear, h.n, h.m_xcols,
+                                                h.kp.scale, h.kp.shift, dY, ylen, h.d_perm,
+                                                order == H2D_ORDER_ORIGINAL ? H2D_ORDER_ORIGINAL : H2D_ORDER_TREE,
+                                                h.row_begin);
+    H2D_LAUNCH_CHECK();
+  }
+}
+
+// Y = A X for nrhs vectors (device pointers; vector k at X + k * xlen, Y + k * ylen).
+void matvec_multi(Handle& h, const double* dX, double* dY, int nrhs, int order) {
+  if (order != H2D_ORDER_ORIGINAL && order != H2D_ORDER_TREE)
+    throw Error{H2D_EINVAL, "multi-RHS matvec supports ORIGINAL and TREE orders"};
+  const bool part = h.row_begin != 0 || h.row_end != h.n;
+  if (order == H2D_ORDER_ORIGINAL && part)
+    throw Error{H2D_EINVAL, "ORIGINAL order needs a single-rank (full-range) handle"};
+  if (!h.multi_ready) {
+    build_multi_schedule(h);
+    set_multi_attrs<2>();
+    set_multi_attrs<4>();
+    set_multi_attrs<8>();
+  }
+  const int64_t xlen = h.n;
+  const int64_t ylen = order == H2D_ORDER_ORIGINAL ? h.n : h.row_end - h.row_begin;
+  int k0 = 0;
+  while (k0 < nrhs) {
+    const int left = nrhs - k0;
+    const double* X = dX + (int64_t)k0 * xlen;
+    double* Y = dY + (int64_t)k0 * ylen;
+    if (left >= 8) { multi_chunk<8>(h, X, xlen, Y, ylen, order); k0 += 8; }
+    else if (left >= 4) { multi_chunk<4>(h, X, xlen, Y, ylen, order); k0 += 4; }
+    else if (left >= 2) { multi_chunk<2>(h, X, xlen, Y, ylen, order); k0 += 2; }
+    else {
+      // one vector: the single-vector path (symmetric P2P)
+      if (order == H2D_ORDER_ORIGINAL) {
+        permute_in(h, X, h.d_xtree);
+        matvec_tree(h, h.d_xtree, Y, H2D_ORDER_ORIGINAL, h.row_begin);
+      } else {
+        matvec_tree(h, X, Y, H2D_ORDER_TREE, h.row_begin);
+      }
+      k0 += 1;
+    }
+  }
+}
+
+}  // namespace h2d
