@@ -81,7 +81,9 @@ typedef struct {
   double shift;           /*                                                   (default 0)  */
   double box_lo[2];       /* root square lower-left corner                                  */
   double box_side;        /* root square side; <= 0 -> bounding square of the points (R2)   */
-  int depth;              /* kappa; < 0 -> R1 depth rule from leaf_size        (default -1) */
+  int depth;              /* kappa >= 0; -1 -> R1 depth rule (nominal leaf size); -2 -> the
+                             paper's rule (Alg. 1 l.3): smallest kappa with no leaf
+                             holding more than leaf_size points (R22)      (default -1) */
   int max_rank;           /* ACA rank cap per block; hitting it sets H2D_WTRUNC (def. 128)  */
   int aca_consecutive;    /* tolerance hits in a row that stop ACA (R7)        (default 3)  */
   int aca_trim;           /* streak terms dropped on a tolerance stop (R7)     (default 3)  */

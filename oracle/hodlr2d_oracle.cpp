@@ -482,7 +482,8 @@ int oracle_dense_rows(const double* pts, int64_t n, int kernel_id, double c, dou
     return 0;
 }
 
-// Alg. 1 InitializeHODLR2D.  box_side <= 0 -> bounding square (R2); depth < 0 -> R1.
+// Alg. 1 InitializeHODLR2D.  box_side <= 0 -> bounding square (R2); depth -1 -> R1,
+// -2 -> the paper's max-occupancy rule (R22).
 // [row_lo, row_hi) restricts the operator to the rows (tree order) one partition serves
 // (row_hi <= 0 -> all rows): only blocks whose row box intersects it are built.
 void* oracle_build(const double* pts, int64_t n, int kernel_id, double c, double scale,
@@ -513,14 +514,26 @@ void* oracle_build(const double* pts, int64_t n, int kernel_id, double c, double
         o->side = std::max(mxx - mnx, mxy - mny);
         if (o->side == 0.0) o->side = 1.0;
     }
+    // depth >= 0: given; -1: R1 (nominal leaf size); -2: the paper's rule, Alg. 1 l.3
+    // (P:878): the smallest kappa at which no leaf holds more than N_max = leaf_size points
+    // (R22), searched upwards from the R1 depth, which is a lower bound.
     o->kappa = depth >= 0 ? depth : oracle_depth(n, leaf_size);
     int kappa = o->kappa;
-    int64_t nleaf = (int64_t)1 << (2 * kappa);
-    o->perm.resize((size_t)n);
-    o->leaf_start.resize((size_t)nleaf + 1);
-    int rc = oracle_tree(pts, n, o->lo[0], o->lo[1], o->side, kappa, nullptr, o->perm.data(),
-                         o->leaf_start.data());
-    if (rc != 0) { delete o; return nullptr; }
+    for (;;) {
+        int64_t nleaf = (int64_t)1 << (2 * kappa);
+        o->perm.resize((size_t)n);
+        o->leaf_start.assign((size_t)nleaf + 1, 0);
+        int rc = oracle_tree(pts, n, o->lo[0], o->lo[1], o->side, kappa, nullptr, o->perm.data(),
+                             o->leaf_start.data());
+        if (rc != 0) { delete o; return nullptr; }
+        if (depth != -2) break;
+        int64_t mx = 0;
+        for (int64_t b = 0; b < nleaf; ++b) mx = std::max<int64_t>(mx, o->leaf_start[(size_t)b + 1] - o->leaf_start[(size_t)b]);
+        if (mx <= leaf_size) break;
+        if (++kappa > 15) { set_err(-1, "no depth <= 15 keeps every leaf <= N_max"); delete o; return nullptr; }
+    }
+    o->kappa = kappa;
+    const int64_t nleaf = (int64_t)1 << (2 * kappa);
     o->px.resize((size_t)n); o->py.resize((size_t)n);
     for (int64_t s = 0; s < n; ++s) {
         o->px[(size_t)s] = pts[2 * (int64_t)o->perm[(size_t)s]];

@@ -341,6 +341,7 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
     throw Error{H2D_EINVAL, "RBF kernels need a = c > 0"};
   if (kernel_id == H2D_KERNEL_RBF_PHI1 && opts->c == 1.0)
     throw Error{H2D_EINVAL, "phi_1 needs a != 1 (log a = 0)"};
+  if (opts->depth < -2) throw Error{H2D_EINVAL, "depth < -2"};
   if (opts->max_rank < 1 || opts->aca_consecutive < 1 || opts->aca_trim < 0 ||
       opts->aca_trim > opts->aca_consecutive)
     throw Error{H2D_EINVAL, "bad ACA options"};
@@ -378,6 +379,19 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
     d_pts = tmp;
   }
   build_tree(h, d_pts);
+  if (opts->depth == -2) {
+    // the paper's rule (Alg. 1 l.3; R22): deepen until no leaf holds more than
+    // N_max = leaf_size points (the R1 depth is a lower bound)
+    for (;;) {
+      int32_t mx = 0;
+      for (size_t b = 0; b + 1 < h.leaf_start.size(); ++b) mx = std::max(mx, h.leaf_start[b + 1] - h.leaf_start[b]);
+      if (mx <= leaf_size) break;
+      if (h.kappa >= 15) throw Error{H2D_EINVAL, "no depth <= 15 keeps every leaf <= N_max"};
+      for (void* q : {(void*)h.d_perm, (void*)h.d_px, (void*)h.d_py, (void*)h.d_leaf_start}) h.release(q);
+      ++h.kappa;
+      build_tree(h, d_pts);
+    }
+  }
   if (tmp) H2D_CUDA(cudaFreeAsync(tmp, h.stream));
   build_lists(h);
   set_partition(h);

@@ -116,3 +116,17 @@ def test_gpu_gmres_host_pointers_restart_and_edges(h2d):
     # not converged -> warning status, residual still reported
     x2, its2, rr2 = gpu.gmres(dev(f), tol=1e-14, restart=3, max_iter=2)
     assert its2 == 2 and not gpu.gmres_converged and rr2 > 1e-14
+
+
+def test_paper_depth_rule_gpu_matches_oracle(h2d):
+    """depth = -2 (the paper's max-occupancy rule, R22): same depth and bit-identical tree."""
+    for pts, n_max in ((W.chebyshev_grid(100), 500), (W.uniform_points(3000, 4, (-1.0, -1.0), 0.3), 100)):
+        orc = oracle.Operator(pts, 0, n_max, 1e-8, box_lo=(-1, -1), box_side=2.0, depth=-2)
+        gpu = h2d.Hodlr2d.build(dev(pts), "log", n_max, 1e-8, box_lo=(-1, -1), box_side=2.0, depth=-2)
+        assert gpu.info()["kappa"] == orc.kappa
+        p_g, ls_g = gpu.tree()
+        p_o, ls_o = orc.tree()
+        assert np.array_equal(p_g, p_o) and np.array_equal(ls_g, ls_o)
+        x = W.random_vector(pts.shape[0], 9)
+        yd = oracle.dense_matvec(pts, x, 0)
+        assert rel(gpu.matvec(dev(x)).cpu().numpy(), yd) <= 1e-7

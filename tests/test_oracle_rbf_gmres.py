@@ -133,3 +133,40 @@ def test_paper_rbf_solution_error(kernel_name):
     err = np.linalg.norm(lam - lam_hat) / np.linalg.norm(lam)
     assert err < 1e-9, err                                 # "of the order of 1e-10"
     assert its < 60
+
+
+# ---------------------------------------------------------------- the paper's depth rule (R22)
+
+def test_paper_depth_rule_definition():
+    """depth = -2: the smallest kappa whose fullest leaf holds <= N_max points."""
+    for pts, n_max in ((W.chebyshev_grid(100), 500), (W.uniform_points(5000, 3), 64),
+                       (W.uniform_points(3000, 4, (-1.0, -1.0), 0.3), 100)):
+        op = oracle.Operator(pts, 0, n_max, 1e-6, box_lo=(-1, -1), box_side=2.0, depth=-2)
+        k = op.kappa
+        _, _, ls = oracle.tree(pts, (-1, -1), 2.0, k)
+        assert int(np.diff(ls).max()) <= n_max
+        if k > 0:
+            _, _, ls1 = oracle.tree(pts, (-1, -1), 2.0, k - 1)
+            assert int(np.diff(ls1).max()) > n_max
+
+
+def test_paper_depth_rule_reproduces_tables():
+    """With the paper's own depth rule the N = 10000 rows are reproduced closely: kappa = 4
+    (R1 gives 3); phi_1 CR 0.1536 vs 0.154 and r_m 41 vs 42 (Table tab:ker1_init, P:1054);
+    1/r memory 0.215 vs 0.23 GB and r_m 103 vs 113 (Table tab:1byr_init)."""
+    g = load_golden("paper_tab_rbf_phi1_n10000.txt")
+    pts = W.chebyshev_grid(int(g["grid_m"]))
+    n = pts.shape[0]
+    op = oracle.Operator(pts, oracle.KERNELS["rbf_phi1"], int(g["n_max"]), float(g["tol"]), c=A_RBF,
+                         scale=1.0, shift=float(n), box_lo=(-1, -1), box_side=2.0, depth=-2)
+    assert op.kappa == 4
+    r_m = max(int(op.ranks(l)[0].max()) for l in range(1, op.kappa + 1))
+    assert abs(r_m - int(g["r_m"])) <= 2, r_m
+    assert abs(cr_of(op, n) - float(g["cr"])) <= 0.03 * float(g["cr"]), cr_of(op, n)
+    g1 = load_golden("paper_tab_1byr_n10000.txt")
+    op1 = oracle.Operator(pts, oracle.KERNELS["one_over_r"], int(g1["n_max"]), float(g1["tol"]),
+                          box_lo=(-1, -1), box_side=2.0, depth=-2)
+    r_m1 = max(int(op1.ranks(l)[0].max()) for l in range(1, op1.kappa + 1))
+    mem = cr_of(op1, n) * n * n * 8 / 1e9
+    assert abs(r_m1 - int(g1["r_m"])) <= 0.1 * int(g1["r_m"]), r_m1
+    assert abs(mem - float(g1["memory_gb"])) <= 0.1 * float(g1["memory_gb"]), mem
