@@ -216,11 +216,11 @@ int hodlr2d_stage_times(hodlr2d_t h, double* ms, int64_t* count, int reset);
 int hodlr2d_set_timing(hodlr2d_t h, int on);
 
 /* Host-only helper (no device work; callable without a GPU): the Morton-range partition
- * every rank of a world uses.  leaf_start: the tree's 4^kappa + 1 leaf offsets (see
- * hodlr2d_copy_tree); n = leaf_start[4^kappa].  Rank r serves leaves
- * [*leaf_begin, *leaf_end): contiguous Morton ranges cut at the leaf boundary nearest to
- * r * n / world points (equal point shares; Eq. eq:par's per-node load, is
- * proportional to the points for the balanced trees of the configs). */
+ * every rank of a world uses.  leaf_start: the tree's 4^kappa + 1 leaf
+ * offsets (see hodlr2d_copy_tree); n = leaf_start[4^kappa].  Rank r serves leaves
+ * [*leaf_begin, *leaf_end): contiguous Morton ranges cut at the quantiles r / world of the
+ * per-leaf load w(L) = |L| (1 + sum over L's ancestors X of |I_X|) — rows times the blocks
+ * they meet, the geometric part of Eq. eq:par's per-node load. */
 int hodlr2d_partition(const int32_t* leaf_start, int kappa, int world, int rank,
                       int64_t* leaf_begin, int64_t* leaf_end);
 

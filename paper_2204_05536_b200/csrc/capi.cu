@@ -87,17 +87,57 @@ static void clear_factors(Handle& h) {
   h.n_aitems = h.n_ritems = 0;
 }
 
-// Contiguous Morton ranges of leaves with equal point shares: the cut before rank r is the
-// first leaf whose start is >= r * n / world (rounded).
+// |I_X| of box (cx, cy) at level l: children of the parent and its edge sharers (inside the
+// domain) that are not edge or vertex neighbours of X (Eq. eq:ilist closed form, R5).
+static int ilist_count(int l, int cx, int cy) {
+  const int px = cx >> 1, py = cy >> 1, pside = 1 << (l - 1);
+  const int dxs[5] = {0, -1, 1, 0, 0}, dys[5] = {0, 0, 0, -1, 1};
+  int cnt = 0;
+  for (int k = 0; k < 5; ++k) {
+    const int qx = px + dxs[k], qy = py + dys[k];
+    if (qx < 0 || qy < 0 || qx >= pside || qy >= pside) continue;
+    for (int c = 0; c < 4; ++c)
+      if (std::abs(2 * qx + (c & 1) - cx) + std::abs(2 * qy + (c >> 1) - cy) >= 2) ++cnt;
+  }
+  return cnt;
+}
+
+static uint32_t compact_host(uint32_t v) {
+  v &= 0x55555555u;
+  v = (v | (v >> 1)) & 0x33333333u;
+  v = (v | (v >> 2)) & 0x0F0F0F0Fu;
+  v = (v | (v >> 4)) & 0x00FF00FFu;
+  v = (v | (v >> 8)) & 0x0000FFFFu;
+  return v;
+}
+
+// Contiguous Morton ranges of leaves cut at the quantiles of a per-leaf load (SURVEY §8(e),
+// in the spirit of Eq. eq:par): w(L) = |L| (1 + sum_l |I_{X_l}|) over L's
+// ancestors X_l — the rows of L times the blocks each of them meets, a geometric proxy of
+// the factor bytes (ranks are unknown before ACA).  Boxes near the domain boundary have
+// fewer partners, so equal point shares left the centre-facing ranks ~12 % heavier (C5).
+// The cut before rank r is the first leaf whose load prefix reaches r / world of the total.
 static void partition_leaves(const int32_t* ls, int kappa, int world, int rank, int64_t* lb,
                              int64_t* le) {
   const int64_t nleaf = (int64_t)1 << (2 * kappa);
-  const int64_t n = ls[nleaf];
+  std::vector<std::vector<uint8_t>> cnt((size_t)kappa + 1);
+  for (int l = 1; l <= kappa; ++l) {
+    const int64_t nbox = (int64_t)1 << (2 * l);
+    cnt[(size_t)l].resize((size_t)nbox);
+    for (int64_t b = 0; b < nbox; ++b)
+      cnt[(size_t)l][(size_t)b] = (uint8_t)ilist_count(l, (int)compact_host((uint32_t)b), (int)compact_host((uint32_t)b >> 1));
+  }
+  std::vector<double> pre((size_t)nleaf + 1, 0.0);
+  for (int64_t L = 0; L < nleaf; ++L) {
+    int s = 1;
+    for (int l = 1; l <= kappa; ++l) s += cnt[(size_t)l][(size_t)(L >> (2 * (kappa - l)))];
+    pre[(size_t)L + 1] = pre[(size_t)L] + (double)(ls[L + 1] - ls[L]) * s;
+  }
   auto cut = [&](int r) {
     if (r <= 0) return (int64_t)0;
     if (r >= world) return nleaf;
-    const int64_t target = (n * r + world / 2) / world;
-    return (int64_t)(std::lower_bound(ls, ls + nleaf + 1, (int32_t)target) - ls);
+    const double target = pre[(size_t)nleaf] * r / world;
+    return (int64_t)(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
   };
   *lb = std::min(cut(rank), nleaf);
   *le = std::min(cut(rank + 1), nleaf);
