@@ -355,7 +355,13 @@ def run_ours(args, cfg):
     served = inf["row_end"] - inf["row_begin"]
     evals = (inf["p2p_pairs"] + served) / 2.0
     alone_ms = p2p_standalone_ms(op, step, args) if world == 1 else None
-    peak_ops = 148 * 64 * sm_hz
+    peak_ops, peak_ops_kind = 148 * 64 * sm_hz, "nominal: 148 SMs x 64 FP64 lanes x SM clock"
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peaks_measured.json")) as f:
+            peak_ops = json.load(f)["fp64_dfma_tflops"] * 1e12 / 2.0   # FP64-pipe instr/s
+        peak_ops_kind = "measured: tools/fp64_peak.cu sustained DFMA (profiles/fp64_peaks_measured.json)"
+    except Exception:
+        pass
 
     def frac(ms):
         return evals * ops_eval / (ms * 1e-3) / peak_ops if (ms and ops_eval) else None
@@ -364,6 +370,7 @@ def run_ours(args, cfg):
            "ms_per_launch_concurrent": round(p2p_ms, 4),
            "ms_per_launch_standalone": round(alone_ms, 4) if alone_ms else None,
            "fp64_ops_per_eval": ops_eval, "peak_fp64_lane_ops_per_s": peak_ops,
+           "peak_kind": peak_ops_kind,
            "frac_fp64_pipe_standalone": frac(alone_ms),
            "frac_fp64_pipe_concurrent": frac(p2p_ms),
            "overlapped_with": "stageA_VTx + stageB_Ut (low-priority stream, co-resident CTAs)",
