@@ -45,6 +45,11 @@ def parse():
                     help="informational: build and time rank G's slice of a --slice-world partition "
                          "on this one GPU, full x resident (per-GPU compute of the multi-GPU run)")
     ap.add_argument("--slice-world", type=int, default=8)
+    ap.add_argument("--mode", default="matvec", choices=["matvec", "gmres"],
+                    help="gmres: the paper's RBF application (P:1020-1048) at --grid-m^2 Chebyshev "
+                         "points, informational line with T_I / T_G (paper values as context)")
+    ap.add_argument("--grid-m", type=int, default=500)
+    ap.add_argument("--rbf-kernel", default="rbf_phi1", choices=["rbf_phi1", "rbf_phi2"])
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: functional check of the multi-rank path (host-staged gather)")
     return ap.parse_args()
@@ -493,9 +498,53 @@ def run_rank_slice(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+# The paper's T_I / T_G for the largest RBF rows (N = 250000, one laptop core):
+# Table tab:ker1_init / tab:k1_sol (phi_1) and tab:ker2_init / tab:ker2_sol (phi_2).
+PAPER_RBF_250000 = {"rbf_phi1": {"T_I_s": 105.4, "T_G_s": 12.2752, "r_m": 59, "CR": 0.013},
+                    "rbf_phi2": {"T_I_s": 147.6, "T_G_s": 8.93127, "r_m": 118, "CR": 0.021}}
+
+
+def run_gmres(args):
+    """The paper's application (§5.2): A lambda = f, A = N I + phi(|x_i - x_j|), a = 0.001,
+    on the m x m Chebyshev grid, ACA 1e-12, N_max 500 with the paper's depth rule (R22),
+    GMRES residual 1e-10.  f = A lambda with the HODLR2D operator itself (a
+    dense product at N = 250000 is beyond this run); prints one informational line."""
+    import torch
+    import paper_2204_05536_b200 as h2d
+    torch.cuda.set_device(0)
+    pts = W.chebyshev_grid(args.grid_m)
+    n = pts.shape[0]
+    t0 = time.time()
+    op = h2d.Hodlr2d.build(torch.from_numpy(pts).cuda(), args.rbf_kernel, 500, 1e-12, c=1e-3, scale=1.0,
+                           shift=float(n), box_lo=(-1, -1), box_side=2.0, depth=-2)
+    torch.cuda.synchronize()
+    t_i = time.time() - t0
+    inf = op.info()
+    lam = torch.from_numpy(np.random.default_rng(1048).uniform(-1.0, 1.0, n)).cuda()
+    f = op.matvec(lam)
+    op.gmres(f, tol=1e-10)                      # warm-up (allocations, schedules)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    lam_hat, its, rr = op.gmres(f, tol=1e-10)
+    torch.cuda.synchronize()
+    t_g = time.time() - t0
+    err = float(torch.linalg.norm(lam_hat - lam) / torch.linalg.norm(lam))
+    line = {"mode": "gmres", "workload": f"{args.rbf_kernel}, {args.grid_m}^2 Chebyshev grid, a = 0.001, "
+                                         f"beta = N, ACA 1e-12, N_max 500 (paper depth rule)",
+            "n": n, "kappa": inf["kappa"], "rank_max": inf["rank_max"],
+            "compression_ratio": inf["compression_ratio"], "T_I_s": round(t_i, 3), "T_G_s": round(t_g, 4),
+            "iterations": its, "rel_residual": rr, "solution_rel_error": err,
+            "paper_context": PAPER_RBF_250000.get(args.rbf_kernel) if n == 250000 else None,
+            "note": "paper numbers: one laptop core (P:1022), context only"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     cfg = W.CONFIGS[args.config]
+    if args.mode == "gmres":
+        run_gmres(args)
+        return
     if args.rank_slice is not None:
         run_rank_slice(args, cfg)
         return
