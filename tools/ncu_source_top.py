@@ -24,7 +24,14 @@ def main():
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
     i_s, i_e, i_w = hdr.index("Source"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
+    i_x = hdr.index("L1 Wavefronts Shared Excessive") if "L1 Wavefronts Shared Excessive" in hdr else None
     data = [(r[i_s].strip(), num(r[i_e]), num(r[i_w])) for r in rows[2:] if len(r) > i_e and r[0] != "Address"]
+    if i_x is not None:
+        ex = [(r[i_s].strip(), num(r[i_x])) for r in rows[2:] if len(r) > i_x and r[0] != "Address"]
+        tx = sum(e for _, e in ex) or 1
+        print(f"-- by excessive shared wavefronts (bank conflicts), total {tx}")
+        for src, e in sorted(ex, key=lambda d: -d[1])[:10]:
+            print(f"{e:>11} {100 * e / tx:5.1f}%  {src[:80]}")
     tot = sum(d[1] for d in data) or 1
     totw = sum(d[2] for d in data) or 1
     print(f"{kern}: {tot} warp-instructions executed, {totw} stall samples")
