@@ -96,6 +96,9 @@ typedef struct {
   size_t aca_scratch_bytes; /* ACA scratch budget; 0 -> 40 % of free device memory         */
   int timing;             /* 1 -> record per-stage CUDA events in every matvec (default 0)  */
   int skip_aca;           /* 1 -> build tree + lists only (factors via load_factors)        */
+  int symmetric;          /* 1 -> one ACA per unordered pair {X, Y}, X < Y in Morton order;
+                             block (Y, X) := V U^T (the paper's symmetric setting, P:61;
+                             halves the ACA work, exactly symmetric operator, R23)  (def 0) */
 } hodlr2d_options;
 
 #define H2D_MAX_LEVELS 16

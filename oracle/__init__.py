@@ -53,7 +53,7 @@ def lib():
             L.oracle_aca_dense.argtypes = [vp, i, i, d, i, i, i, vp, vp, vp, vp]
             L.oracle_dense_matvec.argtypes = [vp, i64, i, d, d, d, i, vp, vp]
             L.oracle_dense_rows.argtypes = [vp, i64, i, d, d, d, i, vp, vp, i64, vp]
-            L.oracle_build.argtypes = [vp, i64, i, d, d, d, i, i, d, d, d, d, i, i, i, i, i64, i64]
+            L.oracle_build.argtypes = [vp, i64, i, d, d, d, i, i, d, d, d, d, i, i, i, i, i64, i64, i]
             L.oracle_build.restype = vp
             L.oracle_destroy.argtypes = [vp]
             L.oracle_kappa.argtypes = [vp]
@@ -173,13 +173,13 @@ class Operator:
 
     def __init__(self, points, kernel_id=0, leaf_size=64, tol=1e-10, c=1.0, scale=1.0, shift=0.0,
                  test_rank=1, box_lo=(0.0, 0.0), box_side=0.0, depth=-1, max_rank=128,
-                 consecutive=3, trim=3, row_range=None):
+                 consecutive=3, trim=3, row_range=None, symmetric=False):
         self.points = np.ascontiguousarray(points, dtype=np.float64)
         self.n = self.points.shape[0]
         lo, hi = row_range if row_range is not None else (0, 0)
         self._h = lib().oracle_build(_p(self.points), self.n, kernel_id, c, scale, shift, test_rank,
                                      leaf_size, tol, box_lo[0], box_lo[1], box_side, depth, max_rank,
-                                     consecutive, trim, lo, hi)
+                                     consecutive, trim, lo, hi, int(bool(symmetric)))
         if not self._h:
             raise ValueError(f"oracle_build failed: {last_error()}")
         self.kappa = int(lib().oracle_kappa(self._h))

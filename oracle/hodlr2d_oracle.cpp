@@ -489,7 +489,7 @@ int oracle_dense_rows(const double* pts, int64_t n, int kernel_id, double c, dou
 void* oracle_build(const double* pts, int64_t n, int kernel_id, double c, double scale,
                    double shift, int test_rank, int leaf_size, double tol, double box_lo_x,
                    double box_lo_y, double box_side, int depth, int max_rank, int consecutive,
-                   int trim, int64_t row_lo, int64_t row_hi) {
+                   int trim, int64_t row_lo, int64_t row_hi, int symmetric) {
     if (n < 1) { set_err(-1, "n < 1"); return nullptr; }
     if (leaf_size < 1) { set_err(-1, "leaf_size < 1"); return nullptr; }
     if (!(tol > 0.0 && tol < 1.0)) { set_err(-1, "aca_tol not in (0,1)"); return nullptr; }
@@ -582,16 +582,36 @@ void* oracle_build(const double* pts, int64_t n, int kernel_id, double c, double
                 for (int64_t j = 0; j < nn; ++j) D[(size_t)(i * nn + j)] = o->entry(r0 + i, c0 + j);
         }
     }
-    // Alg. 1 l.6: ACA for every member of every interaction list, l = kappa..1
+    // Alg. 1 l.6: ACA for every member of every interaction list, l = kappa..1.
+    // symmetric = 1 (NEXT N1, R23; the paper assumes a symmetric matrix):
+    // one ACA per unordered pair, on K(X, Y) with X < Y (Morton); the block (Y, X) is
+    // K(X, Y)^T ~ V U^T, i.e. its factors are the swapped (U, V).
     for (int l = kappa; l >= 1; --l) {
         auto& BL = o->blocks[l];
 #pragma omp parallel for schedule(dynamic, 1)
         for (int64_t e = 0; e < (int64_t)BL.size(); ++e) {
             Block& B = BL[(size_t)e];
-            if (!o->row_box_active(l, B.X)) continue;
+            const bool need = o->row_box_active(l, B.X) || (symmetric && o->row_box_active(l, B.Y));
+            if (!need || (symmetric && B.X > B.Y)) continue;
             const Oracle* oc = o;
             int64_t r0 = B.r0, c0 = B.c0;
             B.f = aca([oc, r0, c0](int i, int j) { return oc->entry(r0 + i, c0 + j); }, B.m, B.n, o->aca);
+            B.built = true;
+        }
+        if (!symmetric) continue;
+        for (int64_t e = 0; e < (int64_t)BL.size(); ++e) {
+            Block& B = BL[(size_t)e];
+            if (B.X < B.Y || !o->row_box_active(l, B.X)) continue;
+            const auto& off = o->il_off[l];
+            const auto& col = o->il_col[l];
+            const auto* first = col.data() + off[(size_t)B.Y];
+            const auto* last = col.data() + off[(size_t)B.Y + 1];
+            const int64_t t = (int64_t)(std::lower_bound(first, last, B.X) - col.data());
+            const Block& T = BL[(size_t)t];
+            B.f.rank = T.f.rank;
+            B.f.truncated = T.f.truncated;
+            B.f.U = T.f.V;
+            B.f.V = T.f.U;
             B.built = true;
         }
     }

@@ -54,6 +54,7 @@ class Options(C.Structure):
         ("stream", C.c_void_p), ("world", C.c_int), ("rank", C.c_int),
         ("row_begin", C.c_int64), ("row_end", C.c_int64),
         ("aca_scratch_bytes", C.c_size_t), ("timing", C.c_int), ("skip_aca", C.c_int),
+        ("symmetric", C.c_int),
     ]
 
 
@@ -178,7 +179,7 @@ class Hodlr2d:
     def build(cls, points, kernel="log", leaf_size=64, aca_tol=1e-10, *, c=1.0, scale=1.0,
               shift=0.0, box_lo=(0.0, 0.0), box_side=0.0, depth=-1, max_rank=128,
               aca_consecutive=3, aca_trim=3, test_rank=1, stream=None, world=1, rank=0,
-              row_range=None, aca_scratch_bytes=0, timing=False, skip_aca=False):
+              row_range=None, aca_scratch_bytes=0, timing=False, skip_aca=False, symmetric=False):
         """hodlr2d_build_ex.  ``points``: (N, 2) float64 torch tensor (CUDA or CPU) or numpy array."""
         kid = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
         o = default_options()
@@ -201,6 +202,7 @@ class Hodlr2d:
         o.aca_scratch_bytes = aca_scratch_bytes
         o.timing = int(bool(timing))
         o.skip_aca = int(bool(skip_aca))
+        o.symmetric = int(bool(symmetric))
         n = points.shape[0]
         h = C.c_void_p()
         rc = _check(lib().hodlr2d_build_ex(_ptr(points), n, kid, leaf_size, aca_tol, C.byref(o), C.byref(h)))

@@ -576,18 +576,38 @@ void run_aca(Handle& h) {
     L.rank.assign((size_t)nbk, -1);
     L.truncated.assign((size_t)nbk, 0);
     // blocks served by this rank (row box intersects the served rows)
+    // symmetric (R23): one ACA per unordered pair, on K(X, Y) with X < Y; the block (Y, X)
+    // takes the swapped factors after the level's ACA
+    const bool sym = h.opts.symmetric != 0;
     std::vector<int64_t> todo;
     for (int64_t X = 0; X < L.nbox; ++X) {
-      if (!h.row_box_active(l, X)) continue;
       const bool mz = h.box_end(l, X) == h.box_begin(l, X);
       for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
         const int64_t Y = L.col[(size_t)e];
+        const bool need = sym ? X < Y && (h.row_box_active(l, X) || h.row_box_active(l, Y))
+                              : h.row_box_active(l, X);
+        if (!need) continue;
         if (mz || h.box_end(l, Y) == h.box_begin(l, Y)) L.rank[(size_t)e] = 0;   // empty side (R5)
         else todo.push_back(e);
       }
     }
     std::vector<const double*> srcU((size_t)nbk, nullptr), srcV((size_t)nbk, nullptr);
+    auto mirror = [&]() {   // symmetric: block (X, Y), X > Y, from block (Y, X)
+      if (!sym) return;
+      for (int64_t X = 0; X < L.nbox; ++X) {
+        if (!h.row_box_active(l, X)) continue;
+        for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
+          if (L.col[(size_t)e] > X) continue;
+          const int32_t t = L.trans[(size_t)e];
+          L.rank[(size_t)e] = L.rank[(size_t)t];
+          L.truncated[(size_t)e] = L.truncated[(size_t)t];
+          srcU[(size_t)e] = srcV[(size_t)t];
+          srcV[(size_t)e] = srcU[(size_t)t];
+        }
+      }
+    };
     if (todo.empty()) {
+      mirror();
       pack_level(h, L, srcU, srcV);
       continue;
     }
@@ -743,6 +763,7 @@ void run_aca(Handle& h) {
     H2D_CUDA(cudaStreamSynchronize(s));
     h.aca_seconds += now_s() - t0;
     for (int64_t e : todo) h.truncated += L.truncated[(size_t)e];
+    mirror();
     double t1 = now_s();
     pack_level(h, L, srcU, srcV);
     H2D_CUDA(cudaStreamSynchronize(s));

@@ -306,3 +306,45 @@ def test_paper_table_1byr_row_10000():
         b = oracle.dense_matvec(pts, x, 2)
         eps_r = max(eps_r, float(np.max(np.abs(op.matvec(x) - b) / np.abs(b))))
     assert eps_r <= 10 * float(g["eps_r"])
+
+
+# ---------------------------------------------------------------- symmetric mode (NEXT N1, R23)
+
+def test_symmetric_mode_oracle():
+    """One ACA per unordered pair: (Y, X) holds exactly the swapped factors of (X, Y); the
+    operator is then symmetric to rounding (the directed one only to O(tol)); accuracy vs
+    the dense product stays within the 10 tol bar; row-restricted symmetric operators union
+    bitwise to the full one."""
+    cfg = W.CONFIGS["c1"]
+    pts = W.config_points(cfg)
+    kw = dict(box_lo=cfg.box_lo, box_side=cfg.box_side)
+    op = oracle.Operator(pts, cfg.kernel, cfg.leaf_size, cfg.tol, symmetric=True, **kw)
+    for l in range(1, op.kappa + 1):
+        off, col = oracle.level_lists(l)
+        for X in range(len(off) - 1):
+            for e in range(off[X], off[X + 1]):
+                Y = col[e]
+                t = off[Y] + int(np.searchsorted(col[off[Y]:off[Y + 1]], X))
+                U, V = op.block(l, e)
+                U2, V2 = op.block(l, t)
+                assert np.array_equal(U, V2) and np.array_equal(V, U2)
+    x, y = W.config_x(cfg, 0), W.random_vector(cfg.n, 17)
+    Ax, Ay = op.matvec(x), op.matvec(y)
+    norm_a = np.linalg.norm(Ax) / np.linalg.norm(x)
+    asym = abs(y @ Ax - x @ Ay) / (np.linalg.norm(x) * np.linalg.norm(y) * norm_a)
+    assert asym < 1e-14
+    assert rel(Ax, oracle.dense_matvec(pts, x, cfg.kernel)) <= 10 * cfg.tol
+    # IMQ on the C2 grid geometry (smaller)
+    g = W.grid_points(64)
+    op2 = oracle.Operator(g, 1, 64, 1e-10, c=0.1, box_lo=(-1, -1), box_side=2.0, symmetric=True)
+    xg = W.random_vector(g.shape[0], 3)
+    assert rel(op2.matvec(xg), oracle.dense_matvec(g, xg, 1, c=0.1)) <= 1e-9
+    # row-restricted symmetric operators (two halves) union bitwise to the full operator
+    perm, ls = op.tree()
+    half = int(ls[len(ls) // 2])
+    y_full = op.matvec(x[perm], order="tree")
+    parts = [oracle.Operator(pts, cfg.kernel, cfg.leaf_size, cfg.tol, symmetric=True, row_range=r, **kw)
+             for r in ((0, half), (half, cfg.n))]
+    y0 = parts[0].matvec(x[perm], order="tree")
+    y1 = parts[1].matvec(x[perm], order="tree")
+    assert np.array_equal(np.concatenate([y0[:half], y1[half:]]), y_full)
