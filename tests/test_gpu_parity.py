@@ -358,3 +358,22 @@ def test_c4_full_size_sampled_rows(h2d):
     assert e <= 10 * cfg.tol
     # the I + h^2 K check is weak on A x; also bound the error of the kernel part
     assert e_kernel <= 10 * cfg.tol
+
+
+def test_c5_rank_slice_full_size_sampled_rows(h2d):
+    """BASELINE config 5 at full size (N = 2^24, IMQ c = 0.05, leaf 128 -> kappa 9, tol 1e-6):
+    rank 0 of the 8-way partition (the launch configuration of the 8-GPU run; ~47 GB on one
+    B200), 48 seeded rows of its range vs the dense product summed over all 2^24 columns."""
+    cfg = W.CONFIGS["c5"]
+    pts = W.config_points(cfg)
+    op = h2d.Hodlr2d.build(dev(pts), cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c, scale=cfg.scale,
+                           shift=cfg.shift, box_lo=cfg.box_lo, box_side=cfg.box_side, world=8, rank=0)
+    inf = op.info()
+    assert inf["kappa"] == 9 and inf["truncated"] == 0
+    perm, _ = op.tree()
+    x = W.config_x(cfg, 0)
+    y = op.matvec(dev(x[perm]), order="tree").cpu().numpy()
+    rows_local = np.sort(np.random.default_rng(55).choice(inf["row_end"] - inf["row_begin"], 48, replace=False))
+    rows_orig = perm[inf["row_begin"] + rows_local]
+    yd = oracle.dense_rows(pts, x, rows_orig, cfg.kernel, cfg.c, cfg.scale, cfg.shift)
+    assert rel(y[rows_local], yd) <= 10 * cfg.tol

@@ -83,7 +83,7 @@ def short(n):
     return last.split(" ")[-1] if "<" not in last else last
 
 
-MATVEC = ("stageA", "stageB", "p2p", "permute_in", "unpad", "reduce_kernel")
+MATVEC = ("stageA", "stageB", "p2p", "permute_in", "unpad", "combine")
 
 
 def launches(path):
