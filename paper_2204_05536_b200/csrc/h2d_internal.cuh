@@ -236,6 +236,8 @@ struct Handle {
   double* d_yfar = nullptr;               // [served] low-rank part (stage B output)
   cudaStream_t hi_stream = nullptr;       // stages A, B (high priority)
   cudaStream_t aux_stream = nullptr;      // P2P (low priority), concurrent with A and B
+  cudaStream_t copy_stream = nullptr;     // host <-> device copies of host-pointer calls
+  cudaEvent_t ev_copy0 = nullptr, ev_copy1 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_far = nullptr;
   // matvec work buffers
   double* d_xtree = nullptr;              // [n]
