@@ -39,6 +39,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--symmetric", action="store_true",
+                    help="symmetric build + apply (one ACA per unordered pair, DESIGN.md R23)")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the symmetric-storage (NEXT N1) variant measured beside the headline")
     ap.add_argument("--multi-rhs", type=int, default=8,
                     help="also time hodlr2d_matvec_multi with this many vectors per call (0: skip)")
     ap.add_argument("--rank-slice", type=int, default=None,
@@ -215,7 +219,7 @@ def run_ours(args, cfg):
     t0 = time.time()
     op = h2d.Hodlr2d.build(d_pts, cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c, scale=cfg.scale,
                            shift=cfg.shift, box_lo=cfg.box_lo, box_side=cfg.box_side,
-                           world=world, rank=rank, stream=stream.cuda_stream)
+                           world=world, rank=rank, stream=stream.cuda_stream, symmetric=args.symmetric)
     torch.cuda.synchronize()
     build_s = time.time() - t0
     del d_pts
@@ -297,12 +301,19 @@ def run_ours(args, cfg):
     other = "stageA_VTx" if dom == "stageB_Ut" else "stageB_Ut"
     other_bytes = inf["stageA_bytes"] if dom == "stageB_Ut" else inf["stageB_bytes"]
     clk_mhz = None
+    other_ms = per[other]
+    if inf.get("symmetric_apply"):   # slot 1 = A' + B' (two kernels), slot 2 = C'
+        dom = {"stageA_VTx": "symmetric A'+B' (stageA_tma + stageA_dual)",
+               "stageB_Ut": "symmetric C' (stageB_tma)"}[dom]
+        other = {"stageA_VTx": "symmetric A'+B' (stageA_tma + stageA_dual)",
+                 "stageB_Ut": "symmetric C' (stageB_tma)"}[other]
+        per = {"symA+B" if k == "stageA_VTx" else "symC" if k == "stageB_Ut" else k: v for k, v in per.items()}
     roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
             "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
             "traffic": ncu_traffic(args.config, dom), "bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4),
-            "other_hbm_kernel": {"kernel": other, "ms_per_launch": round(per[other], 4),
+            "other_hbm_kernel": {"kernel": other, "ms_per_launch": round(other_ms, 4),
                                  "bytes_per_launch": other_bytes,
-                                 "frac": round(other_bytes / (per[other] * 1e-3) / 1e9 / peak, 4)},
+                                 "frac": round(other_bytes / (other_ms * 1e-3) / 1e9 / peak, 4)},
             "stage_ms_per_matvec": {k: round(v, 4) for k, v in per.items()},
             "whole_matvec_frac": round(inf["matvec_bytes"] / (ms_step * 1e-3) / 1e9 / peak, 4)}
 
@@ -348,6 +359,13 @@ def run_ours(args, cfg):
                  "note": "hodlr2d_matvec_multi: factor panels streamed once per call of nrhs "
                          "vectors; a batched-throughput figure, not the per-vector headline"}
 
+    # symmetric block storage (NEXT N1, R23): the same workload built with one ACA
+    # per unordered pair and applied by the three-pass symmetric apply; reported beside the
+    # directed (paper's) headline, never in place of it
+    variants = None
+    if world == 1 and not args.symmetric and not args.no_variants:
+        variants = {"symmetric_N1": symmetric_variant(h2d, op, cfg, xs, nx, y, stream, args)}
+
     # near-field P2P against the FP64 pipe.  The symmetric kernel evaluates every unordered
     # leaf pair once: (near_pairs + N) / 2 kernel evaluations, each P2P_FP64_OPS_PER_EVAL
     # FP64-pipe instructions (counted in the SASS of p2p_fast_kernel).  In the
@@ -392,7 +410,7 @@ def run_ours(args, cfg):
             "operator": {k: inf[k] for k in ("kappa", "rank_max", "u_values", "v_values", "near_pairs",
                                                "compression_ratio", "truncated", "matvec_bytes",
                                                "tree_seconds", "aca_seconds", "pack_seconds")},
-            "roofline": roof, "e2e": e2e, "multi_rhs": multi,
+            "roofline": roof, "e2e": e2e, "multi_rhs": multi, "variants": variants,
             "gpu_launches": args.steps * launches_per_matvec(inf, world),
             "clocks": csum,
         }
@@ -407,10 +425,56 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def symmetric_variant(h2d, op_dir, cfg, xs, nx, y, stream, args):
+    """Device-timed matvecs/s of the symmetric build (options.symmetric = 1) on the same
+    fresh x vectors, with its relative difference from the directed operator on x_0 (both
+    approximate A to aca_tol, so the difference is O(tol))."""
+    import torch
+    pts = torch.from_numpy(W.config_points(cfg)).cuda()
+    t0 = time.time()
+    op = h2d.Hodlr2d.build(pts, cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c, scale=cfg.scale, shift=cfg.shift,
+                           box_lo=cfg.box_lo, box_side=cfg.box_side, stream=stream.cuda_stream, symmetric=True)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    del pts
+    inf = op.info()
+    ys = torch.empty_like(y)
+    for k in range(max(3, args.warmup)):
+        op.matvec_raw(xs[k % nx].data_ptr(), ys.data_ptr(), h2d.ORDER_ORIGINAL)
+    torch.cuda.synchronize()
+    op.stage_times(reset=True)
+    op.set_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(args.steps):
+        op.matvec_raw(xs[(args.warmup + k) % nx].data_ptr(), ys.data_ptr(), h2d.ORDER_ORIGINAL)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    op.set_timing(False)
+    ms = e0.elapsed_time(e1) / args.steps
+    st, cnt = op.stage_times(reset=True)
+    op.matvec_raw(xs[0].data_ptr(), ys.data_ptr(), h2d.ORDER_ORIGINAL)
+    yd = torch.empty_like(y)
+    op_dir.matvec_raw(xs[0].data_ptr(), yd.data_ptr(), h2d.ORDER_ORIGINAL)
+    torch.cuda.synchronize()
+    rel = float(torch.linalg.norm(ys - yd) / torch.linalg.norm(yd))
+    dev_bytes = inf["device_bytes"]
+    op.close()
+    del ys, yd
+    return {"value": 1e3 / ms, "unit": "matvecs/s", "ms_per_step": ms, "steps": args.steps,
+            "build_seconds": round(build_s, 3), "aca_seconds": inf["aca_seconds"],
+            "symmetric_apply": bool(inf["symmetric_apply"]), "matvec_bytes": inf["matvec_bytes"],
+            "frac_hbm_whole_matvec": round(inf["matvec_bytes"] / (ms * 1e-3) / 1e9 / peaks()[0], 4),
+            "stage_ms_per_matvec": {("symA+B" if k == "stageA_VTx" else "symC" if k == "stageB_Ut" else k):
+                                    round(v / max(cnt, 1), 4) for k, v in st.items()},
+            "device_bytes": dev_bytes, "rel_diff_vs_directed_x0": rel}
+
+
 def launches_per_matvec(inf, world):
     # permute-in (1-GPU ORIGINAL order) or unpad (gathered), stage A, stage B, P2P (fast
-    # persistent kernel, + generic kernel when some leaves need it), combine
-    return 5 + (1 if inf.get("p2p_generic_leaves", 0) else 0)
+    # persistent kernel, + generic kernel when some leaves need it), combine; the symmetric
+    # apply adds stage B' (A', B', C' in place of A, B)
+    return 5 + (1 if inf.get("p2p_generic_leaves", 0) else 0) + (1 if inf.get("symmetric_apply") else 0)
 
 
 # FP64-pipe instructions per kernel evaluation in p2p_fast_kernel's unrolled tile loop,

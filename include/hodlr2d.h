@@ -130,6 +130,9 @@ typedef struct {
   int64_t device_bytes;      /* device memory held by the handle                      */
   int64_t gather_stride;     /* max rows over ranks (slot size of H2D_ORDER_GATHERED) */
   int64_t p2p_bytes;         /* algorithmic bytes of the near-field P2P kernel        */
+  int symmetric_apply;       /* 1 -> matvecs run the symmetric three-pass apply (R23):
+                                stage slot 1 = A' + B', slot 2 = C'; stageA_bytes /
+                                stageB_bytes then count those passes                  */
 } hodlr2d_info;
 
 /* Fill *opts with the defaults listed above. */

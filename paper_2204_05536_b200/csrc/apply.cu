@@ -25,7 +25,7 @@
 #include <numeric>
 
 #include "h2d_internal.cuh"
-#include "pipe.cuh"
+#include "stages.cuh"
 
 namespace h2d {
 namespace {
@@ -33,6 +33,11 @@ namespace {
 constexpr int64_t kATargetDefault = 1048576;  // stage-A elements per work item (8 MB)
 constexpr int kAMaxRows = 16384;     // rows per stage-A item
 constexpr int kBRows = 224;          // rows per stage-B item (leaf row block) <= kCons
+constexpr int kT1Max = kT1Smem;      // symmetric stage B': t1 values of one row box in smem
+// stage B' ring: 2 x 44 KB slots.  The fused column-sum + row-dot pass is issue-bound, not
+// latency-bound (the second CTA on the SM hides the copy latency), so fewer, larger stages
+// win by amortising the per-stage overhead: A'+B' 2.20 ms (5 x 16 KB) -> 1.76 ms (C3).
+constexpr int kNSDual = 2, kSDDual = 5632;
 
 struct UCopyItem {
   const double* src;   // column-major, leading dimension ld_src
@@ -70,232 +75,6 @@ T* upload_tmp(const std::vector<T>& v, cudaStream_t s) {
   if (!v.empty())
     H2D_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
   return p;
-}
-
-// ---------------------------------------------------------------- stage A: t = V^T x
-// Item = rows [0, nrows) of a row-major V panel chunk (stride Rp).  A stage holds
-// rows_s = min(256, 2048 / Rp) whole rows (one bulk copy) and their x values.  Consumers:
-// R <= 256 -> thread (g, q) = (tid / R, tid % R) owns panel column q and rows g, g + G, ...
-// (G = 256 / R groups, reduced in smem at the end of the item); R > 256 -> thread owns
-// columns tid + 256 c (c < CPL) over all rows.  Stage header: a = R, b = Rp, c = out,
-// d = ritem.
-template <int NS>
-__device__ void stageA_producer(PipeSmem<NS>& S, const AItem* __restrict__ items, int n_items,
-                                int32_t* counter, const LevelPtrs& lp, const double* __restrict__ x) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t pol = l2_evict_first_policy();
-  int stage = 0;
-  uint32_t phase = 0;
-  // one-item lookahead: the next item's index (atomic) and descriptor (load) are in flight
-  // while the current item streams, so item boundaries cost no memory latency
-  int idx = 0, nidx = 0;
-  if (lane == 0) idx = atomicAdd(counter, 1);
-  idx = __shfl_sync(0xffffffffu, idx, 0);
-  if (lane == 0) nidx = atomicAdd(counter, 1);
-  AItem nit{};
-  if (idx < n_items) nit = items[idx];
-  for (;;) {
-    const bool done = idx >= n_items;
-    const AItem it = nit;
-    const int cur = idx;
-    idx = __shfl_sync(0xffffffffu, nidx, 0);       // issued one item ago
-    if (!done && lane == 0) nidx = atomicAdd(counter, 1);
-    if (!done && idx < n_items) nit = items[idx];
-    const int rows_s = done ? 1 : min(kStageVec, kStageDbl / it.Rp);
-    const double* V = done ? nullptr : lp.V[it.level] + it.v_off;
-    int r0 = 0;
-    do {
-      const int rows = done ? 0 : min(rows_s, it.nrows - r0);
-      mbar_wait(&S.empty[stage], phase ^ 1);
-      if (lane == 0) {
-        StageHdr& h = S.hdr[stage];
-        h.item = done ? -1 : cur;
-        h.cnt = rows;
-        h.flags = (r0 == 0 ? kFirst : 0) | (r0 + rows >= it.nrows ? kLast : 0);
-        h.a = it.R;
-        h.b = it.Rp;
-        h.c = it.out;
-        h.d = it.ritem;
-        const uint32_t bytes = (uint32_t)rows * (uint32_t)it.Rp * 8u;
-        mbar_arrive_expect_tx(&S.full[stage], bytes);
-        if (bytes) bulk_g2s(S.ring[stage], V + (int64_t)r0 * it.Rp, bytes, &S.full[stage], pol);
-      }
-      for (int j = lane; j < rows; j += 32) cp_async8(&S.vec[stage][j], x + it.x_off + r0 + j);
-      cp_async_arrive_noinc(&S.full[stage]);
-      if (++stage == NS) { stage = 0; phase ^= 1; }
-      r0 += rows;
-    } while (!done && r0 < it.nrows);
-    if (done) break;
-  }
-}
-
-// Consumers work on column pairs (one 16-byte smem load = 2 panel elements; Rp is even
-// and the padding column is zero, so a pair never straddles a row).  P = Rp / 2 pairs per
-// row.  P <= kCons: thread (g, p) = (tid / P, tid % P) owns pair p, rows g, g + G, ...
-// (G = kCons / P groups, reduced in smem at the end of the item).  P > kCons: thread owns
-// pairs tid + kCons c (c < CP) over all rows.
-constexpr int kMaxCP = (kStageDbl / 2 + kCons - 1) / kCons;
-
-template <int CP>
-__device__ __forceinline__ void stageA_consume(const double* __restrict__ sv, const double* __restrict__ sx,
-                                               int rows, int Rp, int P, int p, int g, int G,
-                                               double (&acc)[2 * kMaxCP]) {
-  if (CP == 1) {
-    if (g >= G) return;
-    const double* __restrict__ v = sv + (size_t)g * Rp + 2 * p;
-    const int step = G * Rp;
-    int j = g;
-    for (; j + G < rows; j += 2 * G, v += 2 * step) {
-      const double2 a = *reinterpret_cast<const double2*>(v);
-      const double2 b = *reinterpret_cast<const double2*>(v + step);
-      const double xa = sx[j], xb = sx[j + G];
-      acc[0] = fma(a.x, xa, acc[0]);
-      acc[1] = fma(a.y, xa, acc[1]);
-      acc[2] = fma(b.x, xb, acc[2]);
-      acc[3] = fma(b.y, xb, acc[3]);
-    }
-    if (j < rows) {
-      const double2 a = *reinterpret_cast<const double2*>(v);
-      const double xa = sx[j];
-      acc[0] = fma(a.x, xa, acc[0]);
-      acc[1] = fma(a.y, xa, acc[1]);
-    }
-  } else {
-    bool valid[CP];
-#pragma unroll
-    for (int c = 0; c < CP; ++c) valid[c] = p + kCons * c < P;
-    const double* __restrict__ v = sv + 2 * p;
-    for (int j = 0; j < rows; ++j, v += Rp) {
-      const double xv = sx[j];
-#pragma unroll
-      for (int c = 0; c < CP; ++c)
-        if (valid[c]) {
-          const double2 a = *reinterpret_cast<const double2*>(v + 2 * kCons * c);
-          acc[2 * c] = fma(a.x, xv, acc[2 * c]);
-          acc[2 * c + 1] = fma(a.y, xv, acc[2 * c + 1]);
-        }
-    }
-  }
-}
-
-template <int NS>
-__device__ void stageA_consumers(PipeSmem<NS>& S, const int32_t* __restrict__ vdst, double* __restrict__ t,
-                                 double* __restrict__ tpart, const RItem* __restrict__ ritems,
-                                 int32_t* __restrict__ rcount) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  int stage = 0;
-  uint32_t phase = 0;
-  int R = 1, Rp = 2, P = 1, CP = 1, G = 1, g = 0, p = 0;
-  double acc[2 * kMaxCP];
-#pragma unroll
-  for (int c = 0; c < 2 * kMaxCP; ++c) acc[c] = 0.0;
-  for (;;) {
-    mbar_wait(&S.full[stage], phase);
-    const StageHdr h = S.hdr[stage];
-    if (h.item < 0) break;
-    if (h.flags & kFirst) {
-      R = h.a;
-      Rp = h.b;
-      P = Rp >> 1;
-      CP = (P + kCons - 1) / kCons;
-      if (CP == 1) { G = kCons / P; g = tid / P; p = tid - g * P; }
-      else { G = 1; g = 0; p = tid; }
-#pragma unroll
-      for (int c = 0; c < 2 * kMaxCP; ++c) acc[c] = 0.0;
-    }
-    const double* sv = S.ring[stage];
-    const double* sx = S.vec[stage];
-    switch (CP) {
-      case 1: stageA_consume<1>(sv, sx, h.cnt, Rp, P, p, g, G, acc); break;
-      case 2: stageA_consume<2>(sv, sx, h.cnt, Rp, P, p, g, G, acc); break;
-      case 3: stageA_consume<3>(sv, sx, h.cnt, Rp, P, p, g, G, acc); break;
-      case 4: stageA_consume<4>(sv, sx, h.cnt, Rp, P, p, g, G, acc); break;
-      default: stageA_consume<kMaxCP>(sv, sx, h.cnt, Rp, P, p, g, G, acc); break;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&S.empty[stage]);
-    if (++stage == NS) { stage = 0; phase ^= 1; }
-    if (!(h.flags & kLast)) continue;
-    // ---- end of item: column sums -> t (or this chunk's partials)
-    auto put = [&](int qq, double v) {
-      if (qq >= R) return;
-      if (h.c >= 0) t[vdst[h.c + qq]] = v;
-      else tpart[(int64_t)(-h.c - 1) + qq] = v;
-    };
-    if (CP == 1) {
-      const double s0 = acc[0] + acc[2], s1 = acc[1] + acc[3];
-      if (G > 1) {
-        S.red[2 * tid] = g < G ? s0 : 0.0;
-        S.red[2 * tid + 1] = g < G ? s1 : 0.0;
-        named_bar_sync(1, kCons);
-        if (tid < P) {
-          double u0 = 0.0, u1 = 0.0;
-          for (int gg = 0; gg < G; ++gg) {
-            u0 += S.red[2 * (tid + gg * P)];
-            u1 += S.red[2 * (tid + gg * P) + 1];
-          }
-          put(2 * tid, u0);
-          put(2 * tid + 1, u1);
-        }
-        named_bar_sync(1, kCons);
-      } else if (tid < P) {
-        put(2 * tid, s0);
-        put(2 * tid + 1, s1);
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < kMaxCP; ++c)
-        if (c < CP && tid + kCons * c < P) {
-          put(2 * (tid + kCons * c), acc[2 * c]);
-          put(2 * (tid + kCons * c) + 1, acc[2 * c + 1]);
-        }
-    }
-    if (h.d >= 0) {
-      // Multi-chunk box: the last chunk to finish sums the partials in chunk order
-      // (deterministic) and resets the counter for the next matvec.
-      // (the barrier orders every consumer's partial writes before thread 0's gpu-scope
-      // fence + atomic; the last arriver's fence orders the other chunks' partials before
-      // its consumers' L2 reads)
-      named_bar_sync(1, kCons);
-      if (tid == 0) {
-        __threadfence();
-        const int last = atomicAdd(rcount + h.d, 1) == ritems[h.d].nchunks - 1;
-        if (last) __threadfence();
-        S.flag = last;
-      }
-      named_bar_sync(1, kCons);
-      if (S.flag) {
-        const RItem ri = ritems[h.d];
-        for (int qq = tid; qq < ri.R; qq += kCons) {
-          const double* __restrict__ pp = tpart + ri.p_off + qq;
-          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-          int c = 0;
-          for (; c + 3 < ri.nchunks; c += 4) {
-            a0 += __ldcg(pp + (int64_t)c * ri.R);
-            a1 += __ldcg(pp + (int64_t)(c + 1) * ri.R);
-            a2 += __ldcg(pp + (int64_t)(c + 2) * ri.R);
-            a3 += __ldcg(pp + (int64_t)(c + 3) * ri.R);
-          }
-          for (; c < ri.nchunks; ++c) a0 += __ldcg(pp + (int64_t)c * ri.R);
-          t[vdst[ri.vpos + qq]] = (a0 + a1) + (a2 + a3);
-        }
-        if (tid == 0) rcount[h.d] = 0;
-      }
-    }
-  }
-}
-
-template <int NS>
-__global__ void __launch_bounds__(kPipeThreads, 3)
-stageA_tma_kernel(const AItem* __restrict__ items, int n_items, int32_t* counter, LevelPtrs lp,
-                  const double* __restrict__ x, const int32_t* __restrict__ vdst, double* __restrict__ t,
-                  double* __restrict__ tpart, const RItem* __restrict__ ritems,
-                  int32_t* __restrict__ rcount) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  PipeSmem<NS>& S = *reinterpret_cast<PipeSmem<NS>*>(smem_raw);
-  pipe_init(S);
-  if (threadIdx.x >= kCons) stageA_producer(S, items, n_items, counter, lp, x);
-  else stageA_consumers(S, vdst, t, tpart, ritems, rcount);
 }
 
 // ---------------------------------------------------------------- near-field P2P (symmetric)
@@ -741,184 +520,6 @@ p2p_fast_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-// ---------------------------------------------------------------- stage B: yfar = U t
-// Item = rows [r0, r0 + rows) (rows <= 256) of served leaf L.  For every ancestor level l
-// the leaf's U columns form one contiguous column-major range (stride mLp); a stage holds
-// cols_s = min(256, 2048 / rowsp) columns (one bulk copy for whole leaves, one per column
-// for row blocks of a leaf > 256 rows) plus their t values (cp.async gather).  Thread
-// (g, i) = (tid / rows, tid % rows) owns row i and columns g, g + G, ... (G = 256 / rows),
-// reduced in smem at the end of the item: one yfar write per row, no atomics.
-// Stage header: a = rows, b = rowsp (row stride inside the stage), c = output row.
-template <int NS>
-__device__ void stageB_producer(PipeSmem<NS>& S, const BItem* __restrict__ items,
-                                const BLevel* __restrict__ blev, int n_items, int32_t* counter,
-                                int kappa, const LevelPtrs& lp) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t pol = l2_evict_first_policy();
-  int stage = 0;
-  uint32_t phase = 0;
-  // one-item lookahead (index + descriptor + per-level metadata in flight, see stage A)
-  int idx = 0, nidx = 0;
-  if (lane == 0) idx = atomicAdd(counter, 1);
-  idx = __shfl_sync(0xffffffffu, idx, 0);
-  if (lane == 0) nidx = atomicAdd(counter, 1);
-  BItem nit{};
-  BLevel nlv{0, 0, 0};
-  if (idx < n_items) {
-    nit = items[idx];
-    if (lane < kappa) nlv = blev[(int64_t)idx * kappa + lane];
-  }
-  for (;;) {
-    const bool done = idx >= n_items;
-    const BItem it = nit;
-    const BLevel lv = nlv;
-    const int cur = idx;
-    idx = __shfl_sync(0xffffffffu, nidx, 0);
-    if (!done && lane == 0) nidx = atomicAdd(counter, 1);
-    if (!done && idx < n_items) {
-      nit = items[idx];
-      if (lane < kappa) nlv = blev[(int64_t)idx * kappa + lane];
-    }
-    const int mL = it.mL;
-    const int mLp = (mL + 1) & ~1, rowsp = (it.rows + 1) & ~1;
-    const bool whole = !done && it.rows == mL;
-    // per-level metadata, lane l - 1 <-> level l
-    const int R = done || lane >= kappa ? 0 : lv.R;
-    const int cb = lv.tcol;
-    const int64_t ub = lv.uoff;
-    const unsigned nz = __ballot_sync(0xffffffffu, R > 0);
-    const int lastl = nz ? 32 - __clz(nz) : 0;
-    const int yrow = it.yrow;
-    if (done || nz == 0) {
-      // terminator, or an item without low-rank columns (kappa = 0 / zero ranks): one
-      // empty stage so the consumers still write the item's rows
-      mbar_wait(&S.empty[stage], phase ^ 1);
-      if (lane == 0) {
-        StageHdr& h = S.hdr[stage];
-        h.item = done ? -1 : cur;
-        h.cnt = 0;
-        h.flags = kFirst | kLast;
-        h.a = it.rows;
-        h.b = rowsp;
-        h.c = yrow;
-        mbar_arrive_expect_tx(&S.full[stage], 0);
-      }
-      cp_async_arrive_noinc(&S.full[stage]);
-      if (++stage == NS) { stage = 0; phase ^= 1; }
-      if (done) break;
-      continue;
-    }
-    const int cols_s = min(kStageVec, kStageDbl / rowsp);
-    bool first = true;
-    for (int li = 0; li < lastl; ++li) {
-      const int Rl = __shfl_sync(0xffffffffu, R, li);
-      const int cbl = __shfl_sync(0xffffffffu, cb, li);
-      const int64_t ubl = __shfl_sync(0xffffffffu, ub, li);
-      if (Rl == 0) continue;
-      const double* Ub = lp.U[li + 1] + ubl;
-      const double* tb = lp.tu[li + 1] + cbl;
-      for (int c0 = 0; c0 < Rl; c0 += cols_s) {
-        const int cols = min(cols_s, Rl - c0);
-        const bool last = li == lastl - 1 && c0 + cols >= Rl;
-        mbar_wait(&S.empty[stage], phase ^ 1);
-        if (lane == 0) {
-          StageHdr& h = S.hdr[stage];
-          h.item = cur;
-          h.cnt = cols;
-          h.flags = (first ? kFirst : 0) | (last ? kLast : 0);
-          h.a = it.rows;
-          h.b = rowsp;
-          h.c = yrow;
-          mbar_arrive_expect_tx(&S.full[stage], (uint32_t)cols * (uint32_t)rowsp * 8u);
-          if (whole)
-            bulk_g2s(S.ring[stage], Ub + (int64_t)c0 * mLp, (uint32_t)cols * (uint32_t)mLp * 8u,
-                     &S.full[stage], pol);
-        }
-        if (!whole)
-          for (int c = lane; c < cols; c += 32)
-            bulk_g2s(S.ring[stage] + c * rowsp, Ub + (int64_t)(c0 + c) * mLp + it.r0,
-                     (uint32_t)rowsp * 8u, &S.full[stage], pol);
-        for (int c = lane; c < cols; c += 32) cp_async8(&S.vec[stage][c], tb + c0 + c);
-        cp_async_arrive_noinc(&S.full[stage]);
-        if (++stage == NS) { stage = 0; phase ^= 1; }
-        first = false;
-      }
-    }
-  }
-}
-
-// Consumers work on row pairs (one 16-byte smem load = rows 2i, 2i+1 of a column; rowsp is
-// even and the padding row is zero): thread (g, i) = (tid / RP, tid % RP), RP = rowsp / 2,
-// owns row pair i and columns g, g + G, ... (G = kCons / RP), reduced in smem per item.
-template <int NS>
-__device__ void stageB_consumers(PipeSmem<NS>& S, double* __restrict__ yfar) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  int stage = 0;
-  uint32_t phase = 0;
-  int rows = 1, rowsp = 2, G = 1, g = 0, i = 0, RP = 1;
-  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-  for (;;) {
-    mbar_wait(&S.full[stage], phase);
-    const StageHdr h = S.hdr[stage];
-    if (h.item < 0) break;
-    if (h.flags & kFirst) {
-      rows = h.a;
-      rowsp = h.b;
-      RP = rowsp >> 1;
-      G = kCons / RP;
-      g = tid / RP;
-      i = tid - g * RP;
-      a0 = a1 = b0 = b1 = 0.0;
-    }
-    if (g < G) {
-      const double* __restrict__ u = S.ring[stage] + (size_t)g * rowsp + 2 * i;
-      const double* __restrict__ tv = S.vec[stage];
-      const int cols = h.cnt, step = G * rowsp;
-      int c = g;
-      for (; c + G < cols; c += 2 * G, u += 2 * step) {
-        const double2 ua = *reinterpret_cast<const double2*>(u);
-        const double2 ub = *reinterpret_cast<const double2*>(u + step);
-        const double ta = tv[c], tb = tv[c + G];
-        a0 = fma(ua.x, ta, a0);
-        a1 = fma(ua.y, ta, a1);
-        b0 = fma(ub.x, tb, b0);
-        b1 = fma(ub.y, tb, b1);
-      }
-      if (c < cols) {
-        const double2 ua = *reinterpret_cast<const double2*>(u);
-        const double ta = tv[c];
-        a0 = fma(ua.x, ta, a0);
-        a1 = fma(ua.y, ta, a1);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&S.empty[stage]);
-    if (++stage == NS) { stage = 0; phase ^= 1; }
-    if (!(h.flags & kLast)) continue;
-    S.red[2 * tid] = g < G ? a0 + b0 : 0.0;
-    S.red[2 * tid + 1] = g < G ? a1 + b1 : 0.0;
-    named_bar_sync(1, kCons);
-    if (tid < rows) {
-      const int ip = tid >> 1, e = tid & 1;
-      double u = 0.0;
-      for (int gg = 0; gg < G; ++gg) u += S.red[2 * (ip + gg * RP) + e];
-      yfar[h.c + tid] = u;
-    }
-    named_bar_sync(1, kCons);
-  }
-}
-
-template <int NS>
-__global__ void __launch_bounds__(kPipeThreads, 3)
-stageB_tma_kernel(const BItem* __restrict__ items, const BLevel* __restrict__ blev, int n_items,
-                  int32_t* counter, int kappa, LevelPtrs lp, double* __restrict__ yfar) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  PipeSmem<NS>& S = *reinterpret_cast<PipeSmem<NS>*>(smem_raw);
-  pipe_init(S);
-  if (threadIdx.x >= kCons) stageB_producer(S, items, blev, n_items, counter, kappa, lp);
-  else stageB_consumers(S, yfar);
-}
-
 // y = yfar + scale (s0 + sL + sD) + shift x over the served rows, in the caller's order.
 __global__ void combine_kernel(int64_t row_begin, int64_t rows, const double* __restrict__ yfar,
                                const double* __restrict__ ynear, int64_t n, const double* __restrict__ x,
@@ -930,6 +531,20 @@ __global__ void combine_kernel(int64_t row_begin, int64_t rows, const double* __
     const double s = yfar[k] + fma(scale, (ynear[r] + ynear[n + r]) + ynear[2 * n + r], shift * x[r]);
     if (order_out == H2D_ORDER_ORIGINAL) y[perm[r]] = s;
     else y[r - y_row0] = s;
+  }
+}
+
+// symmetric apply: y = yfar (C') + sum_l y1[l] (B') + scale ynear + shift x
+__global__ void combine_sym_kernel(int64_t rows, int kappa, const double* __restrict__ yfar,
+                                   const double* __restrict__ y1, const double* __restrict__ ynear, int64_t n,
+                                   const double* __restrict__ x, double scale, double shift, double* __restrict__ y,
+                                   const int32_t* __restrict__ perm, int order_out, int64_t y_row0) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    double v = yfar[r];
+    for (int l = 0; l < kappa; ++l) v += y1[(int64_t)l * n + r];
+    v += fma(scale, (ynear[r] + ynear[n + r]) + ynear[2 * n + r], shift * x[r]);
+    if (order_out == H2D_ORDER_ORIGINAL) y[perm[r]] = v;
+    else y[r - y_row0] = v;
   }
 }
 
@@ -968,7 +583,19 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
   const int l = L.l;
   const int64_t nbox = L.nbox;
   const int sh = 2 * (h.kappa - l);
-  auto rank_of = [&](int64_t e) { return std::max<int32_t>(0, L.rank[(size_t)e]); };
+  // symmetric apply: U leaf panels hold the second-side blocks (row > column box), V box
+  // panels the first-side blocks (row < column box); the first-side U factors go to the
+  // row-major U box panels Ub below
+  const bool sym = h.symapply;
+  std::vector<int32_t> rowbox;
+  if (sym) {
+    rowbox.resize((size_t)L.nblocks);
+    for (int64_t X = 0; X < nbox; ++X)
+      for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) rowbox[(size_t)e] = (int32_t)X;
+  }
+  auto rank_all = [&](int64_t e) { return std::max<int32_t>(0, L.rank[(size_t)e]); };
+  auto rankU = [&](int64_t e) { return sym && rowbox[(size_t)e] < L.col[(size_t)e] ? 0 : rank_all(e); };
+  auto rankV = [&](int64_t e) { return sym && rowbox[(size_t)e] > L.col[(size_t)e] ? 0 : rank_all(e); };
   auto up16 = [](int64_t v) { return (v + 15) & ~(int64_t)15; };
   L.ucol.assign((size_t)L.nblocks, 0);
   L.vcol.assign((size_t)L.nblocks, 0);
@@ -982,7 +609,7 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
     int32_t R = 0;
     for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
       L.ucol[(size_t)e] = R;
-      R += rank_of(e);
+      R += rankU(e);
     }
     L.ucolbase[(size_t)X] = cb;
     cb += R;
@@ -991,7 +618,7 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
     for (int32_t e2 = L.off[(size_t)X]; e2 < L.off[(size_t)X + 1]; ++e2) {
       const int32_t b = L.trans[(size_t)e2];
       L.vcol[(size_t)b] = RV;
-      RV += rank_of(b);
+      RV += rankV(b);
     }
     if (RV > 2048) throw Error{H2D_EINVAL, "V panel wider than 2048 columns (lower max_rank)"};
     L.vR[(size_t)X] = RV;
@@ -1030,7 +657,7 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
     if (mL == 0) continue;
     double* base = L.U + L.uoff[(size_t)(lf - h.leaf_begin)];
     for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
-      const int r = rank_of(e);
+      const int r = rankU(e);
       if (r == 0) continue;
       uitems.push_back(UCopyItem{srcU[(size_t)e] + (s0 - bx0), base + (int64_t)L.ucol[(size_t)e] * ((mL + 1) & ~1),
                                  (int32_t)mX, (mL + 1) & ~1, mL, r});
@@ -1038,13 +665,52 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
   }
   for (int64_t X = 0; X < nbox; ++X) {
     for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
-      const int r = rank_of(e);
+      const int r = rankV(e);
       if (r == 0) continue;
       const int64_t Y = L.col[(size_t)e];
       const int64_t nY = h.box_end(l, Y) - h.box_begin(l, Y);
       if (nY * r > 0)
         vitems.push_back(VPackItem{srcV[(size_t)e], L.V + L.vpan_off[(size_t)Y] + L.vcol[(size_t)e],
                                    (int32_t)nY, r, (L.vR[(size_t)Y] + 1) & ~1, 0});
+    }
+  }
+  if (sym) {
+    // first-side U factors (X, Y), X < Y, as row-major box panels of X (stage B'); t1 layout
+    L.ub_off.assign((size_t)nbox, 0);
+    L.ubR.assign((size_t)nbox, 0);
+    L.ubcol.assign((size_t)L.nblocks, 0);
+    L.t1base.assign((size_t)nbox + 1, 0);
+    int64_t bo = 0, bvals = 0;
+    int32_t tb = 0;
+    for (int64_t X = 0; X < nbox; ++X) {
+      const int64_t m = h.box_end(l, X) - h.box_begin(l, X);
+      int32_t R = 0;
+      for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
+        if (L.col[(size_t)e] < X) continue;
+        L.ubcol[(size_t)e] = R;
+        R += rank_all(e);
+      }
+      if (R > kT1Max) throw Error{H2D_EINVAL, "symmetric apply: first-side panel wider than 1024 columns"};
+      L.ubR[(size_t)X] = R;
+      L.t1base[(size_t)X] = tb;
+      tb += R;
+      L.ub_off[(size_t)X] = bo;
+      bo = up16(bo + m * ((R + 1) & ~1));
+      bvals += m * R;
+    }
+    L.t1base[(size_t)nbox] = tb;
+    L.ub_values = bvals;
+    L.ub_alloc = bo;
+    L.Ub = h.alloc<double>(bo);
+    H2D_CUDA(cudaMemsetAsync(L.Ub, 0, std::max<int64_t>(1, bo) * sizeof(double), s));
+    for (int64_t X = 0; X < nbox; ++X) {
+      const int64_t m = h.box_end(l, X) - h.box_begin(l, X);
+      for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
+        const int r = rank_all(e);
+        if (L.col[(size_t)e] < X || r == 0 || m == 0) continue;
+        vitems.push_back(VPackItem{srcU[(size_t)e], L.Ub + L.ub_off[(size_t)X] + L.ubcol[(size_t)e], (int32_t)m, r,
+                                   (L.ubR[(size_t)X] + 1) & ~1, 0});
+      }
     }
   }
   const size_t CH = 1 << 20;
@@ -1077,6 +743,28 @@ void unpack_block(Handle& h, int l, int64_t e, int* m, int* n, int* r, double* U
   const int rr = std::max<int32_t>(0, L.rank[(size_t)e]);
   *m = (int)mm; *n = (int)nn; *r = rr;
   if (rr == 0) return;
+  // a row-major box panel (ld doubles per row, first column c0) -> column-major rows x rr
+  auto from_rowmajor = [&](double* dst, const double* panel, int64_t ld, int64_t c0, int64_t rows) {
+    std::vector<double> rm((size_t)(rows * rr));
+    if (rows > 0)
+      H2D_CUDA(cudaMemcpy2D(rm.data(), rr * 8, panel + c0, (size_t)ld * 8, rr * 8, rows, cudaMemcpyDeviceToHost));
+    for (int64_t j = 0; j < rows; ++j)
+      for (int q = 0; q < rr; ++q) dst[j + (int64_t)q * rows] = rm[(size_t)(j * rr + q)];
+  };
+  if (h.symapply) {
+    // first side (X < Y): U in the Ub box panel of X, V in the V box panel of Y;
+    // second side (X > Y): U in the leaf panels (handled below), V = U of the pair (Y, X)
+    if (X < Y) {
+      if (U) from_rowmajor(U, L.Ub + L.ub_off[(size_t)X], (L.ubR[(size_t)X] + 1) & ~1, L.ubcol[(size_t)e], mm);
+      if (V) from_rowmajor(V, L.V + L.vpan_off[(size_t)Y], (L.vR[(size_t)Y] + 1) & ~1, L.vcol[(size_t)e], nn);
+      return;
+    }
+    if (V) {
+      const int32_t t = L.trans[(size_t)e];
+      from_rowmajor(V, L.Ub + L.ub_off[(size_t)Y], (L.ubR[(size_t)Y] + 1) & ~1, L.ubcol[(size_t)t], nn);
+      V = nullptr;
+    }
+  }
   if (U) {
     const int sh = 2 * (h.kappa - l);
     const int64_t lf0 = X << sh, lf1 = (X + 1) << sh;
@@ -1146,7 +834,17 @@ void finalize_schedule(Handle& h) {
     t_len += L.ucolbase[(size_t)L.nbox];
   }
   if (t_len > INT32_MAX) throw Error{H2D_EINVAL, "t vector exceeds 2^31 entries"};
-  // vdst: V-panel columns in column-box order (per level, box, column) -> t index
+  // symmetric apply: stage A' writes t1 (first-side blocks, U-box column order), the
+  // directed t above is t2 (second-side blocks, U-leaf column order)
+  const bool sym = h.symapply;
+  int64_t t1_len = 0;
+  if (sym)
+    for (int l = 1; l <= h.kappa; ++l) {
+      Level& L = h.levels[(size_t)l];
+      L.t1_base = t1_len;
+      t1_len += L.t1base[(size_t)L.nbox];
+    }
+  // vdst: V-panel columns in column-box order (per level, box, column) -> t (t1) index
   std::vector<int32_t> vdst((size_t)std::max<int64_t>(1, t_len));
   int64_t vpos = 0;
   for (int l = 1; l <= h.kappa; ++l) {
@@ -1156,17 +854,17 @@ void finalize_schedule(Handle& h) {
       L.t_off[(size_t)Y] = vpos;
       for (int32_t e2 = L.off[(size_t)Y]; e2 < L.off[(size_t)Y + 1]; ++e2) {
         const int32_t b = L.trans[(size_t)e2];           // block (X, Y)
-        const int r = std::max<int32_t>(0, L.rank[(size_t)b]);
-        if (r == 0) continue;
         const int64_t X = L.col[(size_t)e2];
-        for (int q = 0; q < r; ++q)
-          vdst[(size_t)(vpos + L.vcol[(size_t)b] + q)] =
-              (int32_t)(L.tu_base + L.ucolbase[(size_t)X] + L.ucol[(size_t)b] + q);
+        const int r = sym && X > Y ? 0 : std::max<int32_t>(0, L.rank[(size_t)b]);
+        if (r == 0) continue;
+        const int64_t base = sym ? L.t1_base + L.t1base[(size_t)X] + L.ubcol[(size_t)b]
+                                 : L.tu_base + L.ucolbase[(size_t)X] + L.ucol[(size_t)b];
+        for (int q = 0; q < r; ++q) vdst[(size_t)(vpos + L.vcol[(size_t)b] + q)] = (int32_t)(base + q);
       }
       vpos += L.vR[(size_t)Y];
     }
   }
-  if (vpos != t_len) throw Error{H2D_ECUDA, "t layout mismatch"};
+  if (vpos != (sym ? t1_len : t_len)) throw Error{H2D_ECUDA, "t layout mismatch"};
   h.t_len = t_len;
   h.d_t = h.alloc<double>(t_len);
   h.d_vdst = h.alloc<int32_t>(vdst.size());
@@ -1185,6 +883,7 @@ void finalize_schedule(Handle& h) {
     h.lp.ucolbase[l] = L.d_ucolbase;
     h.lp.uoff[l] = L.d_uoff;
     h.lp.tu[l] = h.d_t + L.tu_base;
+    h.lp.Ub[l] = L.Ub;
     // stage-A items: chunks of <= kATarget elements and <= kAMaxRows rows
     for (int64_t Y = 0; Y < L.nbox; ++Y) {
       const int R = L.vR[(size_t)Y], Rp = (R + 1) & ~1;
@@ -1215,6 +914,97 @@ void finalize_schedule(Handle& h) {
   std::stable_sort(aitems.begin(), aitems.end(), [](const AItem& a, const AItem& b) {
     return (int64_t)a.nrows * a.Rp > (int64_t)b.nrows * b.Rp;
   });
+  // symmetric stage B' items over the first-side U box panels (same chunking as stage A);
+  // udst maps a U-box column (block (X, Y), X < Y, column q) to the t2 index of (Y, X)
+  std::vector<AItem> b1items;
+  std::vector<RItem> b1ritems;
+  int64_t b1part_len = 0;
+  if (sym) {
+    std::vector<int32_t> udst((size_t)std::max<int64_t>(1, t1_len));
+    int64_t upos = 0;
+    for (int l = 1; l <= h.kappa; ++l) {
+      Level& L = h.levels[(size_t)l];
+      for (int64_t X = 0; X < L.nbox; ++X) {
+        const int R = L.ubR[(size_t)X], Rp = (R + 1) & ~1;
+        for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
+          const int64_t Y = L.col[(size_t)e];
+          const int r = std::max<int32_t>(0, L.rank[(size_t)e]);
+          if (Y < X || r == 0) continue;
+          const int32_t t = L.trans[(size_t)e];
+          for (int q = 0; q < r; ++q)
+            udst[(size_t)(upos + L.ubcol[(size_t)e] + q)] =
+                (int32_t)(L.tu_base + L.ucolbase[(size_t)Y] + L.ucol[(size_t)t] + q);
+        }
+        const int64_t x0 = h.box_begin(l, X), nX = h.box_end(l, X) - x0;
+        if (R > 0 && nX > 0) {
+          const int64_t t1o = L.t1_base + L.t1base[(size_t)X];
+          int64_t nch = std::max<int64_t>((nX * Rp + kATarget - 1) / kATarget, (nX + kAMaxRows - 1) / kAMaxRows);
+          nch = std::min<int64_t>(nX, std::max<int64_t>(1, nch));
+          const int64_t rows = (nX + nch - 1) / nch;
+          nch = (nX + rows - 1) / rows;
+          if (nch == 1) {
+            b1items.push_back(AItem{L.ub_off[(size_t)X], x0, (int32_t)nX, R, (int32_t)upos, l, -1, Rp, t1o});
+          } else {
+            if (b1part_len + nch * R > INT32_MAX) throw Error{H2D_EINVAL, "partial buffer too large"};
+            b1ritems.push_back(RItem{(int32_t)upos, (int32_t)b1part_len, R, (int32_t)nch});
+            for (int64_t c = 0; c < nch; ++c) {
+              const int64_t r0 = c * rows, nr = std::min(rows, nX - r0);
+              b1items.push_back(AItem{L.ub_off[(size_t)X] + r0 * Rp, x0 + r0, (int32_t)nr, R,
+                                      (int32_t)(-(b1part_len + c * R) - 1), l, (int32_t)(b1ritems.size() - 1),
+                                      Rp, t1o});
+            }
+            b1part_len += nch * R;
+          }
+        }
+        upos += R;
+      }
+    }
+    if (upos != t1_len) throw Error{H2D_ECUDA, "symmetric U-box layout mismatch"};
+    std::stable_sort(b1items.begin(), b1items.end(), [](const AItem& a, const AItem& b) {
+      return (int64_t)a.nrows * a.Rp > (int64_t)b.nrows * b.Rp;
+    });
+    if (getenv("H2D_VERBOSE")) {   // diagnostics: share of B' elements on the two-pass (wide) path
+      double tot = 0, wide = 0;
+      for (const AItem& it : b1items) {
+        const double e = (double)it.nrows * it.Rp;
+        tot += e;
+        if (it.Rp / 2 > 32 * kDualMaxC) wide += e;
+      }
+      fprintf(stderr, "[h2d] B' items %zu, elements %.0f, wide (R > %d) share %.4f\n", b1items.size(), tot,
+              64 * kDualMaxC, tot > 0 ? wide / tot : 0.0);
+      for (int sd : {2048, 3072, 4096}) {   // stages per slot size (doubles)
+        double st = 0;
+        for (const AItem& it : b1items) {
+          const int rs = std::min(kStageVec, (sd - ((it.R + 1) & ~1)) / it.Rp);
+          st += (it.nrows + rs - 1) / rs;
+        }
+        fprintf(stderr, "[h2d]   slot %d doubles: %.0f stages, fill %.3f\n", sd, st, tot / (st * sd));
+      }
+      double sa = 0, ea = 0;
+      for (const AItem& it : aitems) {
+        const int rs = std::min(kStageVec, kStageDbl / it.Rp);
+        sa += (it.nrows + rs - 1) / rs;
+        ea += (double)it.nrows * it.Rp;
+      }
+      fprintf(stderr, "[h2d] A' items %zu: %.0f stages, fill %.3f\n", aitems.size(), sa, ea / (sa * kStageDbl));
+    }
+    h.t1_len = t1_len;
+    h.d_t1 = h.alloc<double>(t1_len);
+    h.d_udst = h.alloc<int32_t>(udst.size());
+    H2D_CUDA(cudaMemcpyAsync(h.d_udst, udst.data(), udst.size() * 4, cudaMemcpyHostToDevice, s));
+    h.n_b1items = (int64_t)b1items.size();
+    h.d_b1items = h.alloc<AItem>(b1items.size());
+    h.d_b1ritems = h.alloc<RItem>(b1ritems.size());
+    h.d_b1rcount = h.alloc<int32_t>(b1ritems.size());
+    h.d_b1tpart = h.alloc<double>(b1part_len);
+    H2D_CUDA(cudaMemsetAsync(h.d_b1rcount, 0, std::max<size_t>(1, b1ritems.size()) * sizeof(int32_t), s));
+    if (!b1items.empty())
+      H2D_CUDA(cudaMemcpyAsync(h.d_b1items, b1items.data(), b1items.size() * sizeof(AItem), cudaMemcpyHostToDevice, s));
+    if (!b1ritems.empty())
+      H2D_CUDA(cudaMemcpyAsync(h.d_b1ritems, b1ritems.data(), b1ritems.size() * sizeof(RItem),
+                               cudaMemcpyHostToDevice, s));
+    if (!h.d_y1) h.d_y1 = h.alloc<double>((size_t)h.kappa * h.n);
+  }
   // stage-B items: served leaves in row blocks of <= kBRows rows, largest cost first, with
   // the per-level metadata of each item precomputed (one dependent load in the producer)
   std::vector<BItem> bitems;
@@ -1326,7 +1116,7 @@ void finalize_schedule(Handle& h) {
                              cudaMemcpyHostToDevice, s));
   if (!h.d_ynear) h.d_ynear = h.alloc<double>(3 * h.n);   // three P2P slots (p2p_sym_kernel)
   if (!h.d_yfar) h.d_yfar = h.alloc<double>(std::max<int64_t>(1, h.row_end - h.row_begin));
-  if (!h.d_counters) h.d_counters = h.alloc<int32_t>(3);
+  if (!h.d_counters) h.d_counters = h.alloc<int32_t>(4);
   if (!h.hi_stream) {
     int sm = 0, lo_prio = 0, hi_prio = 0;
     H2D_CUDA(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, h.device));
@@ -1344,6 +1134,12 @@ void finalize_schedule(Handle& h) {
     h.persist_ctas = per_sm * sm;
     set_pipe_attrs<kNSShallow>();
     set_pipe_attrs<kNSDeep>();
+    {
+      const int dsm = (int)sizeof(PipeSmem<kNSDual, kSDDual>);
+      H2D_CUDA(cudaFuncSetAttribute(stageA_dual_kernel<kNSDual, kSDDual>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm));
+      H2D_CUDA(cudaFuncSetAttribute(stageA_dual_kernel<kNSDual, kSDDual>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    cudaSharedmemCarveoutMaxShared));
+    }
     for (const void* f : {(const void*)p2p_sym_kernel<H2D_KERNEL_LOG>, (const void*)p2p_sym_kernel<H2D_KERNEL_IMQ>,
                           (const void*)p2p_sym_kernel<H2D_KERNEL_ONE_OVER_R>,
                           (const void*)p2p_sym_kernel<H2D_KERNEL_TEST_LOWRANK>,
@@ -1357,7 +1153,7 @@ void finalize_schedule(Handle& h) {
                                     cudaSharedmemCarveoutMaxShared));
     h.num_sms = sm;
   }
-  H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 3 * sizeof(int32_t), s));
+  H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 4 * sizeof(int32_t), s));
   H2D_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -1450,9 +1246,35 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
     p2p();
     H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_join, 0));
   }
-  H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 2 * sizeof(int32_t), hi));
-  if (h.pipe_ns == kNSShallow) launch_stages<kNSShallow>(h, d_xtree, hi);
-  else launch_stages<kNSDeep>(h, d_xtree, hi);
+  if (h.symapply) {
+    // symmetric apply (R23): A' t1 = V^T x; B' t2 = U^T x and y1 = U t1; C' yfar = V t2
+    const size_t smem = sizeof(PipeSmem<kNSShallow>);
+    H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 4 * sizeof(int32_t), hi));
+    H2D_CUDA(cudaMemsetAsync(h.d_y1, 0, (size_t)h.kappa * h.n * sizeof(double), hi));
+    if (h.n_aitems > 0) {
+      stageA_tma_kernel<kNSShallow><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+          h.d_aitems, (int)h.n_aitems, h.d_counters, h.lp, d_xtree, h.d_vdst, h.d_t1, h.d_tpart, h.d_ritems,
+          h.d_rcount);
+      H2D_LAUNCH_CHECK();
+    }
+    if (h.n_b1items > 0) {
+      stageA_dual_kernel<kNSDual, kSDDual><<<h.persist_ctas, kPipeThreads, sizeof(PipeSmem<kNSDual, kSDDual>), hi>>>(
+          h.d_b1items, (int)h.n_b1items, h.d_counters + 3, h.lp, d_xtree, h.d_udst, h.d_t, h.d_b1tpart,
+          h.d_b1ritems, h.d_b1rcount, h.d_t1, h.d_y1,
+          getenv("H2D_DUAL_NOROW") ? (int64_t)-1 : h.n);   // diagnostics: skip the row dots
+      H2D_LAUNCH_CHECK();
+    }
+    record(h, 2, hi);
+    if (h.n_bitems > 0) {
+      stageB_tma_kernel<kNSShallow><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+          h.d_bitems, h.d_blev, (int)h.n_bitems, h.d_counters + 1, h.kappa, h.lp, h.d_yfar);
+      H2D_LAUNCH_CHECK();
+    }
+  } else {
+    H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 2 * sizeof(int32_t), hi));
+    if (h.pipe_ns == kNSShallow) launch_stages<kNSShallow>(h, d_xtree, hi);
+    else launch_stages<kNSDeep>(h, d_xtree, hi);
+  }
   record(h, 3, hi);
   H2D_CUDA(cudaEventRecord(h.ev_far, hi));
   if (!p2p_serial) p2p();   // after stage A's launch: its CTAs are placed first
@@ -1462,8 +1284,12 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
   const int64_t rows = h.row_end - h.row_begin;
   if (rows > 0) {
     const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 148 * 8);
-    combine_kernel<<<blocks, 256, 0, s>>>(h.row_begin, rows, h.d_yfar, h.d_ynear, h.n, d_xtree,
-                                          h.kp.scale, h.kp.shift, d_y, h.d_perm, order_out, y_row0);
+    if (h.symapply)
+      combine_sym_kernel<<<blocks, 256, 0, s>>>(rows, h.kappa, h.d_yfar, h.d_y1, h.d_ynear, h.n, d_xtree, h.kp.scale,
+                                                h.kp.shift, d_y, h.d_perm, order_out, y_row0);
+    else
+      combine_kernel<<<blocks, 256, 0, s>>>(h.row_begin, rows, h.d_yfar, h.d_ynear, h.n, d_xtree,
+                                            h.kp.scale, h.kp.shift, d_y, h.d_perm, order_out, y_row0);
     H2D_LAUNCH_CHECK();
   }
   record(h, 5, s);

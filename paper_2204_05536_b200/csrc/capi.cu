@@ -115,7 +115,16 @@ static void clear_factors(Handle& h) {
     h.release(L.V); L.V = nullptr;
     h.release(L.d_ucolbase); L.d_ucolbase = nullptr;
     h.release(L.d_uoff); L.d_uoff = nullptr;
+    h.release(L.Ub); L.Ub = nullptr;
   }
+  for (void* q : {(void*)h.d_t1, (void*)h.d_udst, (void*)h.d_b1items, (void*)h.d_b1ritems, (void*)h.d_b1rcount,
+                  (void*)h.d_b1tpart})
+    h.release(q);
+  h.d_t1 = h.d_b1tpart = nullptr;
+  h.d_udst = h.d_b1rcount = nullptr;
+  h.d_b1items = nullptr;
+  h.d_b1ritems = nullptr;
+  h.n_b1items = 0;
   for (void* q : {(void*)h.m_aitems, (void*)h.m_ritems, (void*)h.m_rcount, (void*)h.m_tpart, (void*)h.m_xm,
                   (void*)h.m_xcols, (void*)h.m_t, (void*)h.m_yfar, (void*)h.m_ynear})
     h.release(q);
@@ -483,6 +492,10 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
   if (tmp) H2D_CUDA(cudaFreeAsync(tmp, h.stream));
   build_lists(h);
   set_partition(h);
+  // symmetric apply (R23): symmetric build on a single-rank handle (the multi-rank row
+  // partitions keep the directed panels; stage B' needs every row of a row box)
+  h.symapply = opts->symmetric && h.row_begin == 0 && h.row_end == h.n && h.kappa >= 1 &&
+               !(getenv("H2D_SYMAPPLY") && atoi(getenv("H2D_SYMAPPLY")) == 0);
   h.tree_seconds = now_s() - t0;
   if (opts->skip_aca) skip_factors(h); else run_aca(h);
   finalize_schedule(h);
@@ -653,10 +666,22 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   // U panels once, t read once, ynear read once, y written once.  P2P: points + x + ynear.
   info->stageA_bytes = 8 * vv + 8 * (int64_t)h.n + 12 * h.t_len;
   info->stageB_bytes = 8 * uv + 8 * h.t_len + 16 * served;
+  if (h.symapply) {
+    // symmetric apply (R23): "stage A" = A' (first-side V box panels, x, t1 + its
+    // destination index written) + B' (first-side U box panels, x, t1 read, t2 + udst, the
+    // kappa y1 rows written); "stage B" = C' (second-side U leaf panels, t2) + the combine's
+    // y1 / ynear / y traffic
+    int64_t ub = 0;
+    for (int l = 1; l <= h.kappa; ++l) ub += h.levels[(size_t)l].ub_values;
+    info->stageA_bytes = 8 * vv + 8 * ub + 16 * (int64_t)h.n + 20 * h.t1_len + 12 * h.t_len +
+                         8 * (int64_t)h.kappa * h.n;
+    info->stageB_bytes = 8 * uv + 8 * h.t_len + 16 * served + 8 * (int64_t)h.kappa * served;
+  }
   info->p2p_bytes = 24 * served + 8 * served;
   info->matvec_bytes = info->stageA_bytes + info->stageB_bytes + info->p2p_bytes;
   info->device_bytes = (int64_t)h.device_bytes;
   info->gather_stride = h.gather_stride;
+  info->symmetric_apply = h.symapply ? 1 : 0;
   (void)rsum;
   return H2D_OK;
   H2D_CATCH

@@ -128,6 +128,17 @@ struct Level {
   int32_t* d_ucolbase = nullptr;            // [nbox + 1]
   int64_t* d_uoff = nullptr;                // [served leaves]
   int64_t tu_base = 0;                      // first t entry of the level (U-column order)
+  // symmetric apply (Handle::symapply): the U leaf / V box panels above then hold the
+  // second-side blocks (Y, X), Y > X (U leaf panels, = V of the pair) and the first-side
+  // blocks (Z, Y), Z < Y (V box panels); the first-side U factors (X, Y), X < Y, are kept
+  // as row-major box panels Ub (m_X x ubRp_X) for stage B' of the symmetric matvec.
+  double* Ub = nullptr;
+  int64_t ub_values = 0, ub_alloc = 0;
+  std::vector<int64_t> ub_off;              // per box
+  std::vector<int32_t> ubR;                 // per box: first-side columns R^F_X
+  std::vector<int32_t> ubcol;               // per block (first side): column in the Ub panel of X
+  std::vector<int32_t> t1base;              // per box + 1: prefix of R^F (t1 layout)
+  int64_t t1_base = 0;                      // first t1 entry of the level
 };
 
 // Stage-A work item: one row chunk of one V panel.  Outputs go to t (U-panel order)
@@ -141,6 +152,7 @@ struct AItem {
   int32_t level;
   int32_t ritem;   // >= 0: multi-chunk box (RItem index); the last chunk CTA reduces
   int32_t Rp;      // row stride of the panel (R rounded up to even)
+  int64_t t1_off;  // symmetric stage B': first t1 entry of the item's row box (else 0)
 };
 // Stage-B work item: rows [r0, r0 + rows) (rows <= 224) of a served leaf of mL points whose
 // first output row is yrow (index into the served rows); its per-level metadata is
@@ -170,6 +182,7 @@ struct LevelPtrs {
   const int32_t* ucolbase[H2D_MAX_LEVELS + 1];
   const int64_t* uoff[H2D_MAX_LEVELS + 1];  // U leaf-panel offsets (served leaves)
   const double* tu[H2D_MAX_LEVELS + 1];   // t of the level in U-column order
+  const double* Ub[H2D_MAX_LEVELS + 1];   // symmetric apply: first-side U box panels
 };
 
 struct Handle {
@@ -224,6 +237,19 @@ struct Handle {
   int32_t* d_p2p_fast = nullptr;          // leaves of the persistent fast P2P kernel
   int32_t* d_p2p_gen = nullptr;           // leaves of the generic P2P kernel
   int64_t n_p2p_fast = 0, n_p2p_gen = 0;
+  // symmetric apply (symmetric build on a single-rank handle, R23): A' over the
+  // first-side V box panels -> t1; B' over the first-side U box panels -> t2 (= t) and the
+  // per-level row dots y1 = U t1; C' = stage B over the second-side leaf panels with t2
+  bool symapply = false;
+  double* d_t1 = nullptr;                 // [t1_len]
+  int64_t t1_len = 0;
+  int32_t* d_udst = nullptr;              // U-box column -> t2 index
+  AItem* d_b1items = nullptr;             // stage B' items
+  int64_t n_b1items = 0;
+  RItem* d_b1ritems = nullptr;
+  int32_t* d_b1rcount = nullptr;
+  double* d_b1tpart = nullptr;
+  double* d_y1 = nullptr;                 // [kappa][n] per-level row dots of B'
   // multi-RHS (multi.cu): tiled stage-A schedule and per-chunk buffers (<= 8 vectors)
   bool multi_ready = false;
   AItem* m_aitems = nullptr;

@@ -835,6 +835,21 @@ void matvec_multi(Handle& h, const double* dX, double* dY, int nrhs, int order) 
   const bool part = h.row_begin != 0 || h.row_end != h.n;
   if (order == H2D_ORDER_ORIGINAL && part)
     throw Error{H2D_EINVAL, "ORIGINAL order needs a single-rank (full-range) handle"};
+  if (h.symapply) {
+    // the symmetric apply keeps no directed panels: one vector at a time
+    const int64_t ylen1 = order == H2D_ORDER_ORIGINAL ? h.n : h.row_end - h.row_begin;
+    for (int k = 0; k < nrhs; ++k) {
+      const double* X = dX + (int64_t)k * h.n;
+      double* Y = dY + (int64_t)k * ylen1;
+      if (order == H2D_ORDER_ORIGINAL) {
+        permute_in(h, X, h.d_xtree);
+        matvec_tree(h, h.d_xtree, Y, H2D_ORDER_ORIGINAL, h.row_begin);
+      } else {
+        matvec_tree(h, X, Y, H2D_ORDER_TREE, h.row_begin);
+      }
+    }
+    return;
+  }
   if (!h.multi_ready) {
     build_multi_schedule(h);
     set_multi_attrs<2>();

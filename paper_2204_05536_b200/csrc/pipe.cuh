@@ -29,11 +29,12 @@ struct StageHdr {
   int32_t cnt;     // rows (stage A) / columns (stage B) held by this stage
   int32_t flags;   // kFirst / kLast stage of the item
   int32_t a, b, c, d, pad;   // item fields for the consumers (see the producers)
+  int32_t e, f;
 };
 
-template <int NS>
+template <int NS, int SD = kStageDbl>
 struct PipeSmem {
-  double ring[NS][kStageDbl];
+  double ring[NS][SD];
   double vec[NS][kStageVec];
   double red[2 * kCons];
   StageHdr hdr[NS];
@@ -42,8 +43,8 @@ struct PipeSmem {
   int flag;
 };
 
-template <int NS>
-__device__ __forceinline__ void pipe_init(PipeSmem<NS>& S) {
+template <int NS, int SD>
+__device__ __forceinline__ void pipe_init(PipeSmem<NS, SD>& S) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&S.full[s], 1 + 32);
