@@ -114,3 +114,72 @@ def test_symmetric_apply_matches_directed_panels(h2d, name):
     Y = op.matvec_multi(dev(X)).cpu().numpy()
     for k in range(3):
         assert np.array_equal(Y[k], op.matvec(dev(X[k])).cpu().numpy())
+
+
+def _sym_pair(h2d, pts, kernel, leaf, tol, **kw):
+    """(symmetric-apply handle, directed-panel handle) of the same symmetric build."""
+    import os
+    args = dict(box_lo=(-1, -1), box_side=2.0, symmetric=True)
+    args.update(kw)
+    op = h2d.Hodlr2d.build(dev(pts), kernel, leaf, tol, **args)
+    os.environ["H2D_SYMAPPLY"] = "0"
+    try:
+        ref = h2d.Hodlr2d.build(dev(pts), kernel, leaf, tol, **args)
+    finally:
+        os.environ.pop("H2D_SYMAPPLY")
+    assert op.info()["symmetric_apply"] == 1 and ref.info()["symmetric_apply"] == 0
+    return op, ref
+
+
+def test_symmetric_apply_multichunk_items(h2d):
+    """N = 2^18: level-1 boxes hold ~65K rows > 16384, so stage A' and B' split them into
+    row chunks whose partial column sums are reduced by the last chunk (RItem path)."""
+    n = 1 << 18
+    pts = W.uniform_points(n, 4242)
+    op, ref = _sym_pair(h2d, pts, "log", 64, 1e-8)
+    for k in range(2):
+        x = W.random_vector(n, 900 + k)
+        assert rel(op.matvec(dev(x)).cpu().numpy(), ref.matvec(dev(x)).cpu().numpy()) <= 1e-13
+
+
+def test_symmetric_apply_wide_panels(h2d, capfd):
+    """IMQ with c = 0.05, 256-point leaves and tol 1e-13 makes first-side panels up to ~500
+    columns wide (tools/probe_first_side_R.py): B' takes its two-pass (column pass +
+    row-dot pass) path for those wider than 256 (share reported by H2D_VERBOSE).  Ranks hit
+    the cap there, so the bar is the directed-panel apply of the same factors."""
+    import os
+    import re
+    n = 1 << 14
+    pts = W.uniform_points(n, 4343)
+    os.environ["H2D_VERBOSE"] = "1"
+    try:
+        op, ref = _sym_pair(h2d, pts, "imq", 256, 1e-13, c=0.05)
+    finally:
+        os.environ.pop("H2D_VERBOSE")
+    err = capfd.readouterr().err
+    share = [float(m) for m in re.findall(r"wide \(R > \d+\) share ([0-9.]+)", err)]
+    assert share and share[0] > 0.0, err
+    for k in range(2):
+        x = W.random_vector(n, 910 + k)
+        y = op.matvec(dev(x)).cpu().numpy()
+        assert rel(y, ref.matvec(dev(x)).cpu().numpy()) <= 1e-13
+
+
+@pytest.mark.parametrize("case", ["clustered_empty_leaves", "chebyshev_big_leaves", "rbf_phi1", "imq_depth_rule"])
+def test_symmetric_apply_cases(h2d, case):
+    if case == "clustered_empty_leaves":
+        pts, kernel, leaf, kw = W.uniform_points(6000, 77, (-1.0, -1.0), 0.9), "log", 64, {}
+    elif case == "chebyshev_big_leaves":
+        pts, kernel, leaf, kw = W.chebyshev_grid(70), "log", 500, {}
+    elif case == "rbf_phi1":
+        pts, kernel, leaf, kw = W.chebyshev_grid(60), "rbf_phi1", 100, {"c": 1e-3, "shift": 3600.0}
+    else:
+        pts, kernel, leaf, kw = W.uniform_points(9000, 79), "imq", 50, {"c": 0.1, "depth": -2}
+    n = pts.shape[0]
+    op, ref = _sym_pair(h2d, pts, kernel, leaf, 1e-10, **kw)
+    x = W.random_vector(n, 920)
+    y = op.matvec(dev(x)).cpu().numpy()
+    assert rel(y, ref.matvec(dev(x)).cpu().numpy()) <= 1e-13
+    kid = {"log": 0, "imq": 1, "rbf_phi1": 3}[kernel]
+    yd = oracle.dense_matvec(pts, x, kid, kw.get("c", 1.0), 1.0, kw.get("shift", 0.0))
+    assert rel(y, yd) <= 1e-8
