@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <numeric>
+#include <type_traits>
 
 #include "pipe.cuh"
 
@@ -24,12 +25,13 @@ namespace {
 constexpr int kTileW = 2 * kCons;    // stage-A column tile (<= kCons pairs)
 constexpr int kMaxNR = 8;            // vectors per chunk
 constexpr int kBRowsMax = 224;       // stage-B item rows (apply.cu kBRows)
+constexpr int kNSMulti = 2, kSDMulti = 5632, kSVMulti = 704;   // ring: stages, doubles, vector values
 
 // ---------------------------------------------------------------- stage A (multi)
 // Stage header: a = W (tile width), b = Wp (row stride of the stage, W rounded up to even),
 // c = out, d = ritem.
-template <int NS, int NR>
-__device__ void mA_producer(PipeSmem<NS>& S, const AItem* __restrict__ items, int n_items, int32_t* counter,
+template <int NS, int NR, int SD, int SV>
+__device__ void mA_producer(PipeSmem<NS, SD, SV>& S, const AItem* __restrict__ items, int n_items, int32_t* counter,
                             const LevelPtrs& lp, const double* __restrict__ xm) {
   const int lane = threadIdx.x & 31;
   const uint64_t pol = l2_evict_first_policy();
@@ -50,7 +52,7 @@ __device__ void mA_producer(PipeSmem<NS>& S, const AItem* __restrict__ items, in
     if (!done && idx < n_items) nit = items[idx];
     const int Wp = (it.R + 1) & ~1;
     const bool contiguous = Wp == it.Rp;
-    const int rows_s = done ? 1 : min(kStageVec / NR, kStageDbl / max(Wp, 2));
+    const int rows_s = done ? 1 : min(SV / NR, SD / max(Wp, 2));
     const double* V = done ? nullptr : lp.V[it.level] + it.v_off;
     int r0 = 0;
     do {
@@ -82,8 +84,8 @@ __device__ void mA_producer(PipeSmem<NS>& S, const AItem* __restrict__ items, in
   }
 }
 
-template <int NS, int NR>
-__device__ void mA_consumers(PipeSmem<NS>& S, const int32_t* __restrict__ vdst, double* __restrict__ tm,
+template <int NS, int NR, int SD, int SV>
+__device__ void mA_consumers(PipeSmem<NS, SD, SV>& S, const int32_t* __restrict__ vdst, double* __restrict__ tm,
                              double* __restrict__ tpartm, const RItem* __restrict__ ritems,
                              int32_t* __restrict__ rcount) {
   const int tid = threadIdx.x, lane = tid & 31;
@@ -204,8 +206,8 @@ constexpr int kMaxMTB = (kBRowsMax / 8 + kConsWarps - 1) / kConsWarps; // m-tile
 
 // Stage A: M = tile columns (m-tile i of the item owned by warp i % 7, all rows), N = the 8
 // vectors, K = rows, 4 per DMMA.  No cross-warp reduction: every T entry has one owner.
-template <int NS>
-__device__ void mA_consumers_dmma(PipeSmem<NS>& S, const int32_t* __restrict__ vdst, double* __restrict__ tm,
+template <int NS, int SD, int SV>
+__device__ void mA_consumers_dmma(PipeSmem<NS, SD, SV>& S, const int32_t* __restrict__ vdst, double* __restrict__ tm,
                                   double* __restrict__ tpartm, const RItem* __restrict__ ritems,
                                   int32_t* __restrict__ rcount) {
   constexpr int NR = 8;
@@ -297,8 +299,8 @@ __device__ void mA_consumers_dmma(PipeSmem<NS>& S, const int32_t* __restrict__ v
 // 4w, 4w + 28, ...) and reduce the 7 partials per m-tile in smem at the end of the item;
 // taller row blocks give m-tile i to warp i % 7.
 constexpr int kMaxMTK = 8;
-template <int NS>
-__device__ void mB_consumers_dmma(PipeSmem<NS>& S, double* __restrict__ yfarm) {
+template <int NS, int SD, int SV>
+__device__ void mB_consumers_dmma(PipeSmem<NS, SD, SV>& S, double* __restrict__ yfarm) {
   constexpr int NR = 8;
   constexpr int kD = kMaxMTK > kMaxMTB ? kMaxMTK : kMaxMTB;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -394,22 +396,22 @@ __device__ void mB_consumers_dmma(PipeSmem<NS>& S, double* __restrict__ yfarm) {
 template <int NR>
 constexpr int kMultiMinBlocks = 3;
 
-template <int NS, int NR>
+template <int NS, int NR, int SD, int SV>
 __global__ void __launch_bounds__(kPipeThreads, kMultiMinBlocks<NR>)
 stageA_multi_kernel(const AItem* __restrict__ items, int n_items, int32_t* counter, LevelPtrs lp,
                     const double* __restrict__ xm, const int32_t* __restrict__ vdst, double* __restrict__ tm,
                     double* __restrict__ tpartm, const RItem* __restrict__ ritems, int32_t* __restrict__ rcount) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  PipeSmem<NS>& S = *reinterpret_cast<PipeSmem<NS>*>(smem_raw);
+  PipeSmem<NS, SD, SV>& S = *reinterpret_cast<PipeSmem<NS, SD, SV>*>(smem_raw);
   pipe_init(S);
-  if (threadIdx.x >= kCons) mA_producer<NS, NR>(S, items, n_items, counter, lp, xm);
-  else if constexpr (NR == 8) mA_consumers_dmma<NS>(S, vdst, tm, tpartm, ritems, rcount);
-  else mA_consumers<NS, NR>(S, vdst, tm, tpartm, ritems, rcount);
+  if (threadIdx.x >= kCons) mA_producer<NS, NR, SD, SV>(S, items, n_items, counter, lp, xm);
+  else if constexpr (NR == 8) mA_consumers_dmma<NS, SD, SV>(S, vdst, tm, tpartm, ritems, rcount);
+  else mA_consumers<NS, NR, SD, SV>(S, vdst, tm, tpartm, ritems, rcount);
 }
 
 // ---------------------------------------------------------------- stage B (multi)
-template <int NS, int NR>
-__device__ void mB_producer(PipeSmem<NS>& S, const BItem* __restrict__ items, const BLevel* __restrict__ blev,
+template <int NS, int NR, int SD, int SV>
+__device__ void mB_producer(PipeSmem<NS, SD, SV>& S, const BItem* __restrict__ items, const BLevel* __restrict__ blev,
                             int n_items, int32_t* counter, int kappa, const LevelPtrs& lp,
                             const double* const* __restrict__ tml) {
   const int lane = threadIdx.x & 31;
@@ -460,7 +462,7 @@ __device__ void mB_producer(PipeSmem<NS>& S, const BItem* __restrict__ items, co
       if (done) break;
       continue;
     }
-    const int cols_s = min(kStageVec / NR, kStageDbl / rowsp);
+    const int cols_s = min(SV / NR, SD / rowsp);
     bool first = true;
     for (int li = 0; li < lastl; ++li) {
       const int Rl = __shfl_sync(0xffffffffu, R, li);
@@ -499,8 +501,8 @@ __device__ void mB_producer(PipeSmem<NS>& S, const BItem* __restrict__ items, co
   }
 }
 
-template <int NS, int NR>
-__device__ void mB_consumers(PipeSmem<NS>& S, double* __restrict__ yfarm) {
+template <int NS, int NR, int SD, int SV>
+__device__ void mB_consumers(PipeSmem<NS, SD, SV>& S, double* __restrict__ yfarm) {
   const int tid = threadIdx.x, lane = tid & 31;
   int stage = 0;
   uint32_t phase = 0;
@@ -564,16 +566,16 @@ struct TmPtrs {
   const double* p[H2D_MAX_LEVELS + 1];
 };
 
-template <int NS, int NR>
+template <int NS, int NR, int SD, int SV>
 __global__ void __launch_bounds__(kPipeThreads, kMultiMinBlocks<NR>)
 stageB_multi_kernel(const BItem* __restrict__ items, const BLevel* __restrict__ blev, int n_items,
                     int32_t* counter, int kappa, LevelPtrs lp, TmPtrs tml, double* __restrict__ yfarm) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  PipeSmem<NS>& S = *reinterpret_cast<PipeSmem<NS>*>(smem_raw);
+  PipeSmem<NS, SD, SV>& S = *reinterpret_cast<PipeSmem<NS, SD, SV>*>(smem_raw);
   pipe_init(S);
-  if (threadIdx.x >= kCons) mB_producer<NS, NR>(S, items, blev, n_items, counter, kappa, lp, tml.p);
-  else if constexpr (NR == 8) mB_consumers_dmma<NS>(S, yfarm);
-  else mB_consumers<NS, NR>(S, yfarm);
+  if (threadIdx.x >= kCons) mB_producer<NS, NR, SD, SV>(S, items, blev, n_items, counter, kappa, lp, tml.p);
+  else if constexpr (NR == 8) mB_consumers_dmma<NS, SD, SV>(S, yfarm);
+  else mB_consumers<NS, NR, SD, SV>(S, yfarm);
 }
 
 // ---------------------------------------------------------------- near field (multi)
@@ -760,15 +762,18 @@ static void build_multi_schedule(Handle& h) {
   h.multi_ready = true;
 }
 
-template <int NR>
+template <int NR, int NS, int SD, int SV>
 static void set_multi_attrs() {
-  const int smem = (int)sizeof(PipeSmem<kNSShallow>);
-  H2D_CUDA(cudaFuncSetAttribute(stageA_multi_kernel<kNSShallow, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  H2D_CUDA(cudaFuncSetAttribute(stageB_multi_kernel<kNSShallow, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  H2D_CUDA(cudaFuncSetAttribute(stageA_multi_kernel<kNSShallow, NR>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  static bool done = false;   // per instantiation, per process (attributes are per function)
+  if (done) return;
+  const int smem = (int)sizeof(PipeSmem<NS, SD, SV>);
+  H2D_CUDA(cudaFuncSetAttribute(stageA_multi_kernel<NS, NR, SD, SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  H2D_CUDA(cudaFuncSetAttribute(stageB_multi_kernel<NS, NR, SD, SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  H2D_CUDA(cudaFuncSetAttribute(stageA_multi_kernel<NS, NR, SD, SV>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                 cudaSharedmemCarveoutMaxShared));
-  H2D_CUDA(cudaFuncSetAttribute(stageB_multi_kernel<kNSShallow, NR>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  H2D_CUDA(cudaFuncSetAttribute(stageB_multi_kernel<NS, NR, SD, SV>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                 cudaSharedmemCarveoutMaxShared));
+  done = true;
 }
 
 template <int KID, int NR>
@@ -780,8 +785,9 @@ static void launch_p2p_multi(Handle& h, cudaStream_t a) {
   H2D_LAUNCH_CHECK();
 }
 
-template <int NR>
+template <int NR, int NS, int SD, int SV>
 static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, int64_t ylen, int order) {
+  set_multi_attrs<NR, NS, SD, SV>();
   cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
   const int grid = (int)std::min<int64_t>((h.n + 255) / 256, 148 * 16);
   permute_multi_kernel<<<grid, 256, 0, s>>>(NR, dX, xlen, order == H2D_ORDER_ORIGINAL ? h.d_perm : nullptr, h.n,
@@ -791,9 +797,9 @@ static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, i
   H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_fork, 0));
   H2D_CUDA(cudaStreamWaitEvent(a, h.ev_fork, 0));
   H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 2 * sizeof(int32_t), hi));
-  const size_t smem = sizeof(PipeSmem<kNSShallow>);
+  const size_t smem = sizeof(PipeSmem<NS, SD, SV>);
   if (h.m_n_aitems > 0) {
-    stageA_multi_kernel<kNSShallow, NR><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+    stageA_multi_kernel<NS, NR, SD, SV><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
         h.m_aitems, (int)h.m_n_aitems, h.d_counters, h.lp, h.m_xm, h.d_vdst, h.m_t, h.m_tpart, h.m_ritems,
         h.m_rcount);
     H2D_LAUNCH_CHECK();
@@ -801,7 +807,7 @@ static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, i
   if (h.n_bitems > 0) {
     TmPtrs tml{};
     for (int l = 1; l <= h.kappa; ++l) tml.p[l] = h.m_t + h.levels[(size_t)l].tu_base * NR;
-    stageB_multi_kernel<kNSShallow, NR><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+    stageB_multi_kernel<NS, NR, SD, SV><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
         h.d_bitems, h.d_blev, (int)h.n_bitems, h.d_counters + 1, h.kappa, h.lp, tml, h.m_yfar);
     H2D_LAUNCH_CHECK();
   }
@@ -850,22 +856,23 @@ void matvec_multi(Handle& h, const double* dX, double* dY, int nrhs, int order) 
     }
     return;
   }
-  if (!h.multi_ready) {
-    build_multi_schedule(h);
-    set_multi_attrs<2>();
-    set_multi_attrs<4>();
-    set_multi_attrs<8>();
-  }
+  if (!h.multi_ready) build_multi_schedule(h);
   const int64_t xlen = h.n;
   const int64_t ylen = order == H2D_ORDER_ORIGINAL ? h.n : h.row_end - h.row_begin;
+  // ring geometry: 2 x 44 KB slots (+ 8 x 88 vector values each) -- the DMMA consumers are
+  // issue- / chain-bound per stage, so fewer, larger stages amortise the per-stage overhead:
+  // C3 8 vectors 4.43 -> 3.88 ms per call, 4 vectors +9 % (5 x 16 KB measured alongside)
+  auto chunk = [&](auto nr, const double* X, double* Y) {
+    multi_chunk<decltype(nr)::value, kNSMulti, kSDMulti, kSVMulti>(h, X, xlen, Y, ylen, order);
+  };
   int k0 = 0;
   while (k0 < nrhs) {
     const int left = nrhs - k0;
     const double* X = dX + (int64_t)k0 * xlen;
     double* Y = dY + (int64_t)k0 * ylen;
-    if (left >= 8) { multi_chunk<8>(h, X, xlen, Y, ylen, order); k0 += 8; }
-    else if (left >= 4) { multi_chunk<4>(h, X, xlen, Y, ylen, order); k0 += 4; }
-    else if (left >= 2) { multi_chunk<2>(h, X, xlen, Y, ylen, order); k0 += 2; }
+    if (left >= 8) { chunk(std::integral_constant<int, 8>{}, X, Y); k0 += 8; }
+    else if (left >= 4) { chunk(std::integral_constant<int, 4>{}, X, Y); k0 += 4; }
+    else if (left >= 2) { chunk(std::integral_constant<int, 2>{}, X, Y); k0 += 2; }
     else {
       // one vector: the single-vector path (symmetric P2P)
       if (order == H2D_ORDER_ORIGINAL) {

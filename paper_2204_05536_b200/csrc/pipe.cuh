@@ -32,10 +32,10 @@ struct StageHdr {
   int32_t e, f;
 };
 
-template <int NS, int SD = kStageDbl>
+template <int NS, int SD = kStageDbl, int SV = kStageVec>
 struct PipeSmem {
   double ring[NS][SD];
-  double vec[NS][kStageVec];
+  double vec[NS][SV];
   double red[2 * kCons];
   StageHdr hdr[NS];
   uint64_t full[NS];    // 1 producer arrival (+ tx bytes) + 32 cp.async arrivals
@@ -43,8 +43,8 @@ struct PipeSmem {
   int flag;
 };
 
-template <int NS, int SD>
-__device__ __forceinline__ void pipe_init(PipeSmem<NS, SD>& S) {
+template <int NS, int SD, int SV>
+__device__ __forceinline__ void pipe_init(PipeSmem<NS, SD, SV>& S) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&S.full[s], 1 + 32);
