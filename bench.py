@@ -302,7 +302,13 @@ def run_ours(args, cfg):
     other_bytes = inf["stageA_bytes"] if dom == "stageB_Ut" else inf["stageB_bytes"]
     clk_mhz = None
     other_ms = per[other]
-    if inf.get("symmetric_apply"):   # slot 1 = A' + B' (two kernels), slot 2 = C'
+    dom_traffic = ncu_traffic(args.config, dom)
+    if inf.get("symmetric_apply"):
+        # the capture of the symmetric run is keyed "<config>_symmetric": A'+B' = stageA_tma +
+        # stageA_dual, C' = stageB_tma
+        parts = ["stageA_VTx", "stageA_dual"] if dom == "stageA_VTx" else ["stageB_Ut"]
+        tr = [ncu_traffic(args.config + "_symmetric", k) for k in parts]
+        dom_traffic = sum(tr) if all(t is not None for t in tr) else None   # slot 1 = A' + B' (two kernels), slot 2 = C'
         dom = {"stageA_VTx": "symmetric A'+B' (stageA_tma + stageA_dual)",
                "stageB_Ut": "symmetric C' (stageB_tma)"}[dom]
         other = {"stageA_VTx": "symmetric A'+B' (stageA_tma + stageA_dual)",
@@ -310,7 +316,7 @@ def run_ours(args, cfg):
         per = {"symA+B" if k == "stageA_VTx" else "symC" if k == "stageB_Ut" else k: v for k, v in per.items()}
     roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
             "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-            "traffic": ncu_traffic(args.config, dom), "bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4),
+            "traffic": dom_traffic, "bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4),
             "other_hbm_kernel": {"kernel": other, "ms_per_launch": round(other_ms, 4),
                                  "bytes_per_launch": other_bytes,
                                  "frac": round(other_bytes / (other_ms * 1e-3) / 1e9 / peak, 4)},

@@ -110,7 +110,7 @@ def launches(path):
 
 
 STAGE_OF = {"stageA_tma_kernel": "stageA_VTx", "stageB_tma_kernel": "stageB_Ut",
-            "p2p_fast_kernel": "p2p_near"}
+            "p2p_fast_kernel": "p2p_near", "stageA_dual_kernel": "stageA_dual"}
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
