@@ -133,6 +133,9 @@ typedef struct {
   int symmetric_apply;       /* 1 -> matvecs run the symmetric three-pass apply (R23):
                                 stage slot 1 = A' + B', slot 2 = C'; stageA_bytes /
                                 stageB_bytes then count those passes                  */
+  int p2p_launches;          /* near-field kernels per matvec: warp-per-leaf (<= 32-point
+                                leaves), CTA fast path, generic (1..3)                 */
+  int64_t p2p_leaves[3];     /* leaves on the warp / fast / generic P2P paths          */
 } hodlr2d_info;
 
 /* Fill *opts with the defaults listed above. */

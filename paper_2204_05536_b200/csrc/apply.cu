@@ -520,6 +520,110 @@ p2p_fast_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+// Small-leaf near field: leaves of <= 32 points (clustered inputs such as the paper's
+// Chebyshev grids put a handful of points in most leaves at the depth-rule kappa, where one
+// CTA and six barriers per leaf cost more than the pairs).  One warp per leaf (atomic
+// counter), lane i = row i; the leaf's and the neighbour's points are staged in the warp's
+// smem.  Self block: row sums over all m x m pairs.  +x / +y neighbour (any size, 32-point
+// chunks, 8 columns at a time): row sums in registers, the 8 column sums of the group by a
+// transposed butterfly (9 double shuffles; lane 4t ends up holding column t).  Same slots
+// as p2p_fast_kernel: s0 (own rows), sL / sD (the neighbour's rows), one writer per value.
+constexpr int kWarpLeaf = 32;
+
+template <int KID>
+__device__ __forceinline__ void warp_nbr(int lane, double pi, double qi, double xi, bool vi, int n, int64_t nb0,
+                                         const double* __restrict__ px, const double* __restrict__ py,
+                                         const double* __restrict__ x, double2* __restrict__ spq,
+                                         double* __restrict__ sx, const double2* __restrict__ tab,
+                                         const KernelParams& kp, double& acc, double* __restrict__ out) {
+  for (int cb = 0; cb < n; cb += 32) {
+    const int nc = min(32, n - cb);
+    __syncwarp();
+    if (lane < nc) {
+      spq[lane] = make_double2(px[nb0 + cb + lane], py[nb0 + cb + lane]);
+      sx[lane] = x[nb0 + cb + lane];
+    }
+    __syncwarp();
+    for (int g = 0; g < nc; g += 8) {
+      double c[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int j = g + t;
+        double v = 0.0, xj = 0.0;
+        if (j < nc) {
+          const double2 q = spq[j];
+          xj = sx[j];
+          const double dx = pi - q.x, dy = qi - q.y;
+          v = kfast<KID>(fma(dx, dx, dy * dy), tab, kp);
+        }
+        acc = fma(v, xj, acc);
+        c[t] = vi ? v * xi : 0.0;
+      }
+      const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
+      double a[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        a[k] = (b16 ? c[k + 4] : c[k]) + __shfl_xor_sync(0xffffffffu, b16 ? c[k] : c[k + 4], 16);
+      double b[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        b[k] = (b8 ? a[k + 2] : a[k]) + __shfl_xor_sync(0xffffffffu, b8 ? a[k] : a[k + 2], 8);
+      double v = (b4 ? b[1] : b[0]) + __shfl_xor_sync(0xffffffffu, b4 ? b[0] : b[1], 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      const int col = g + (lane >> 2);
+      if ((lane & 3) == 0 && col < nc) out[cb + col] = v;
+    }
+  }
+}
+
+template <int KID>
+__global__ void __launch_bounds__(256, 3)
+p2p_warp_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int32_t* counter,
+                const int32_t* __restrict__ leaf_start, const double* __restrict__ px,
+                const double* __restrict__ py, const double* __restrict__ x, KernelParams kp,
+                double* __restrict__ s0, double* __restrict__ sL, double* __restrict__ sD) {
+  __shared__ double2 spq[8][2][32];
+  __shared__ double sxv[8][2][32];
+  __shared__ double2 tab[128];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (kNeedsLogTable<KID>) hlog_table(tab);
+  __syncthreads();
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(counter, 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= n_leaves) break;
+    const P2PMeta M = p2p_meta(kappa, leaves[idx], leaf_start);
+    const bool vi = lane < M.m;
+    double pi = 0.0, qi = 0.0, xi = 0.0;
+    if (vi) {
+      pi = px[M.xs + lane];
+      qi = py[M.xs + lane];
+      xi = x[M.xs + lane];
+    }
+    __syncwarp();
+    spq[w][0][lane] = make_double2(pi, qi);
+    sxv[w][0][lane] = xi;
+    __syncwarp();
+    double acc = 0.0;
+    for (int j = 0; j < M.m; ++j) {   // self block (K(0) by kfast's r2 = 0 branch)
+      const double2 q = spq[w][0][j];
+      const double dx = pi - q.x, dy = qi - q.y;
+      acc = fma(kfast<KID>(fma(dx, dx, dy * dy), tab, kp), sxv[w][0][j], acc);
+    }
+    if (M.has_r)
+      warp_nbr<KID>(lane, pi, qi, xi, vi, M.rn, M.rs, px, py, x, spq[w][1], sxv[w][1], tab, kp, acc, sL + M.rs);
+    if (M.has_u)
+      warp_nbr<KID>(lane, pi, qi, xi, vi, M.un, M.us, px, py, x, spq[w][1], sxv[w][1], tab, kp, acc, sD + M.us);
+    if (vi) {
+      s0[M.xs + lane] = acc;
+      if (!M.has_l) sL[M.xs + lane] = 0.0;
+      if (!M.has_d) sD[M.xs + lane] = 0.0;
+    }
+  }
+}
+
 // y = yfar + scale (s0 + sL + sD) + shift x over the served rows, in the caller's order.
 __global__ void combine_kernel(int64_t row_begin, int64_t rows, const double* __restrict__ yfar,
                                const double* __restrict__ ynear, int64_t n, const double* __restrict__ x,
@@ -1066,21 +1170,44 @@ void finalize_schedule(Handle& h) {
     const uint32_t side = 1u << h.kappa;
     auto size_of = [&](int64_t lf) { return h.leaf_start[(size_t)lf + 1] - h.leaf_start[(size_t)lf]; };
     auto served = [&](int64_t lf) { return lf >= h.leaf_begin && lf < h.leaf_end; };
-    std::vector<int32_t> fast, gen;
+    std::vector<int32_t> fast, gen, wlist;
     for (int64_t lf = h.leaf_begin; lf < h.leaf_end; ++lf) {
       const uint32_t cx = compact((uint32_t)lf), cy = compact((uint32_t)lf >> 1);
-      bool ok = dist && size_of(lf) <= kSymTile;
+      bool served_all = true, small_nbrs = true;
       auto nb = [&](bool exists, uint32_t nx, uint32_t ny, bool check_size) {
         if (!exists) return;
         const int64_t Y = (int64_t)(spread(nx) | (spread(ny) << 1));
-        ok = ok && served(Y) && (!check_size || size_of(Y) <= kSymTile);
+        served_all = served_all && served(Y);
+        small_nbrs = small_nbrs && (!check_size || size_of(Y) <= kSymTile);
       };
       nb(cx + 1 < side, cx + 1, cy, true);
       nb(cy + 1 < side, cx, cy + 1, true);
       nb(cx > 0, cx - 1, cy, false);
       nb(cy > 0, cx, cy - 1, false);
-      (ok ? fast : gen).push_back((int32_t)lf);
+      // warp path: <= 32-point leaves (any neighbour size); CTA fast path: three tiles
+      // <= kSymTile points; both need a distance kernel and the whole near field served
+      if (dist && served_all && size_of(lf) <= kWarpLeaf) wlist.push_back((int32_t)lf);
+      else if (dist && served_all && small_nbrs && size_of(lf) <= kSymTile) fast.push_back((int32_t)lf);
+      else gen.push_back((int32_t)lf);
     }
+    if (getenv("H2D_P2P_NOWARP")) {   // diagnostics: small leaves on the CTA paths
+      for (int32_t lf : wlist) {
+        const uint32_t cx = compact((uint32_t)lf), cy = compact((uint32_t)lf >> 1);
+        bool small = true;
+        auto chk = [&](bool e, uint32_t nx, uint32_t ny) {
+          if (e) small = small && size_of((int64_t)(spread(nx) | (spread(ny) << 1))) <= kSymTile;
+        };
+        chk(cx + 1 < side, cx + 1, cy);
+        chk(cy + 1 < side, cx, cy + 1);
+        (small ? fast : gen).push_back(lf);
+      }
+      wlist.clear();
+    }
+    h.n_p2p_warp = (int64_t)wlist.size();
+    h.release(h.d_p2p_warp);
+    h.d_p2p_warp = h.alloc<int32_t>(wlist.size());
+    if (!wlist.empty())
+      H2D_CUDA(cudaMemcpyAsync(h.d_p2p_warp, wlist.data(), wlist.size() * 4, cudaMemcpyHostToDevice, s));
     h.n_p2p_fast = (int64_t)fast.size();
     h.n_p2p_gen = (int64_t)gen.size();
     h.release(h.d_p2p_fast);
@@ -1116,7 +1243,7 @@ void finalize_schedule(Handle& h) {
                              cudaMemcpyHostToDevice, s));
   if (!h.d_ynear) h.d_ynear = h.alloc<double>(3 * h.n);   // three P2P slots (p2p_sym_kernel)
   if (!h.d_yfar) h.d_yfar = h.alloc<double>(std::max<int64_t>(1, h.row_end - h.row_begin));
-  if (!h.d_counters) h.d_counters = h.alloc<int32_t>(4);
+  if (!h.d_counters) h.d_counters = h.alloc<int32_t>(8);
   if (!h.hi_stream) {
     int sm = 0, lo_prio = 0, hi_prio = 0;
     H2D_CUDA(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, h.device));
@@ -1237,6 +1364,18 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
       kfn<<<grid, 256, 0, a>>>(h.kappa, h.d_p2p_fast, (int)h.n_p2p_fast, h.d_counters + 2,
                                h.d_leaf_start, h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear,
                                h.d_ynear + h.n, h.d_ynear + 2 * h.n);
+      H2D_LAUNCH_CHECK();
+    }
+    if (h.n_p2p_warp > 0) {
+      auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_warp_kernel<H2D_KERNEL_LOG>
+                : h.kp.id == H2D_KERNEL_IMQ ? p2p_warp_kernel<H2D_KERNEL_IMQ>
+                : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_warp_kernel<H2D_KERNEL_ONE_OVER_R>
+                : h.kp.id == H2D_KERNEL_RBF_PHI1 ? p2p_warp_kernel<H2D_KERNEL_RBF_PHI1>
+                                                 : p2p_warp_kernel<H2D_KERNEL_RBF_PHI2>;
+      H2D_CUDA(cudaMemsetAsync(h.d_counters + 4, 0, sizeof(int32_t), a));
+      const int grid = (int)std::min<int64_t>(h.num_sms, (h.n_p2p_warp + 7) / 8);
+      kfn<<<grid, 256, 0, a>>>(h.kappa, h.d_p2p_warp, (int)h.n_p2p_warp, h.d_counters + 4, h.d_leaf_start,
+                               h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear, h.d_ynear + h.n, h.d_ynear + 2 * h.n);
       H2D_LAUNCH_CHECK();
     }
     record(h, 7, a);

@@ -682,6 +682,10 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   info->device_bytes = (int64_t)h.device_bytes;
   info->gather_stride = h.gather_stride;
   info->symmetric_apply = h.symapply ? 1 : 0;
+  info->p2p_leaves[0] = h.n_p2p_warp;
+  info->p2p_leaves[1] = h.n_p2p_fast;
+  info->p2p_leaves[2] = h.n_p2p_gen;
+  info->p2p_launches = (h.n_p2p_warp > 0) + (h.n_p2p_fast > 0) + (h.n_p2p_gen > 0);
   (void)rsum;
   return H2D_OK;
   H2D_CATCH

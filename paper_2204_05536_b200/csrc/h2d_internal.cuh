@@ -230,13 +230,15 @@ struct Handle {
   BItem* d_bitems = nullptr;              // stage-B items, largest first
   BLevel* d_blev = nullptr;               // [n_bitems * kappa]
   int64_t n_bitems = 0;
-  int32_t* d_counters = nullptr;          // [2] dynamic work counters of stage A / B
+  int32_t* d_counters = nullptr;          // dynamic work counters: stage A, B, P2P fast, B', P2P warp
   int persist_ctas = 0;                   // CTAs of the persistent stage-A/B kernels
   int pipe_ns = 0;                        // their ring depth (template instance)
   int num_sms = 0;
   int32_t* d_p2p_fast = nullptr;          // leaves of the persistent fast P2P kernel
   int32_t* d_p2p_gen = nullptr;           // leaves of the generic P2P kernel
   int64_t n_p2p_fast = 0, n_p2p_gen = 0;
+  int32_t* d_p2p_warp = nullptr;          // <= 32-point leaves of the warp-per-leaf P2P kernel
+  int64_t n_p2p_warp = 0;
   // symmetric apply (symmetric build on a single-rank handle, R23): A' over the
   // first-side V box panels -> t1; B' over the first-side U box panels -> t2 (= t) and the
   // per-level row dots y1 = U t1; C' = stage B over the second-side leaf panels with t2

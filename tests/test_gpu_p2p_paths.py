@@ -1,0 +1,103 @@
+"""GPU parity of the near-field paths (S9): the warp-per-leaf kernel for <= 32-point leaves,
+the CTA fast kernel and the generic kernel (info p2p_leaves = [warp, fast, generic]).
+
+Bars: the matvec vs the dense product <= 10 tol-level bounds; with the warp path disabled
+(H2D_P2P_NOWARP=1: the same leaves on the CTA paths, different summation order) equal to
+1e-14; a world-2 partition (leaves next to the cut go generic) reassembles the full matvec.
+Inputs: the paper's Chebyshev grids at the depth rule (most interior leaves hold a few
+points, the corner leaves hundreds), tiny uniform leaves, every distance kernel.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+KID = {"log": 0, "imq": 1, "one_over_r": 2, "rbf_phi1": 3, "rbf_phi2": 4}
+
+
+@pytest.fixture(scope="module")
+def h2d():
+    import paper_2204_05536_b200 as m
+    m.lib()
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def build(h2d, pts, kernel, leaf, tol, nowarp=False, **kw):
+    args = dict(box_lo=(-1, -1), box_side=2.0)
+    args.update(kw)
+    if nowarp:
+        os.environ["H2D_P2P_NOWARP"] = "1"
+    try:
+        return h2d.Hodlr2d.build(dev(pts), kernel, leaf, tol, **args)
+    finally:
+        os.environ.pop("H2D_P2P_NOWARP", None)
+
+
+CASES = [
+    ("cheb_phi1", lambda: W.chebyshev_grid(120), "rbf_phi1", 500, 1e-12, {"c": 1e-3, "shift": 14400.0, "depth": -2}),
+    ("cheb_phi2", lambda: W.chebyshev_grid(100), "rbf_phi2", 300, 1e-12, {"c": 1e-3, "shift": 10000.0, "depth": -2}),
+    ("cheb_log", lambda: W.chebyshev_grid(90), "log", 200, 1e-12, {"depth": -2}),
+    ("tiny_uniform_imq", lambda: W.uniform_points(6000, 5150), "imq", 12, 1e-10, {"c": 0.1}),
+    ("tiny_uniform_1r", lambda: W.uniform_points(6000, 5151), "one_over_r", 20, 1e-10, {}),
+]
+
+
+@pytest.mark.parametrize("name,gen,kernel,leaf,tol,kw", CASES, ids=[c[0] for c in CASES])
+def test_warp_path_vs_dense_and_cta_paths(h2d, name, gen, kernel, leaf, tol, kw):
+    pts = gen()
+    n = pts.shape[0]
+    op = build(h2d, pts, kernel, leaf, tol, **kw)
+    ref = build(h2d, pts, kernel, leaf, tol, nowarp=True, **kw)
+    pw, pf, pg = op.info()["p2p_leaves"]
+    assert pw > 0, (pw, pf, pg)
+    assert ref.info()["p2p_leaves"][0] == 0 and sum(ref.info()["p2p_leaves"]) == pw + pf + pg
+    x = W.random_vector(n, 5200)
+    y = op.matvec(dev(x)).cpu().numpy()
+    assert rel(y, ref.matvec(dev(x)).cpu().numpy()) <= 1e-14
+    yd = oracle.dense_matvec(pts, x, KID[kernel], kw.get("c", 1.0), 1.0, kw.get("shift", 0.0))
+    assert rel(y, yd) <= max(10 * tol, 1e-12)
+
+
+def test_warp_path_oracle_factors(h2d, tmp_path):
+    """With the oracle's factors loaded the whole matvec (near field included) matches the
+    oracle matvec to 1e-12 on a Chebyshev grid whose interior leaves go to the warp path."""
+    pts = W.chebyshev_grid(64)
+    kw = dict(c=1e-3, scale=1.0, shift=4096.0, box_lo=(-1, -1), box_side=2.0, depth=-2)
+    orc = oracle.Operator(pts, KID["rbf_phi1"], 100, 1e-12, **kw)
+    path = str(tmp_path / "f.bin")
+    orc.save_factors(path)
+    op = h2d.Hodlr2d.build(dev(pts), "rbf_phi1", 100, 1e-12, **kw)
+    assert op.info()["p2p_leaves"][0] > 0
+    op.load_factors(path)
+    x = W.random_vector(pts.shape[0], 5300)
+    assert rel(op.matvec(dev(x)).cpu().numpy(), orc.matvec(x)) <= 1e-12
+
+
+def test_warp_path_partition_union(h2d):
+    pts = W.chebyshev_grid(80)
+    kw = dict(depth=-2)
+    full = build(h2d, pts, "log", 150, 1e-12, **kw)
+    perm, _ = full.tree()
+    x = W.random_vector(pts.shape[0], 5400)[perm]
+    yfull = full.matvec(dev(x), order="tree").cpu().numpy()
+    parts = []
+    for rank in range(2):
+        p = build(h2d, pts, "log", 150, 1e-12, world=2, rank=rank, **kw)
+        assert p.info()["p2p_leaves"][0] > 0
+        parts.append(p.matvec(dev(x), order="tree").cpu().numpy())
+    assert rel(np.concatenate(parts), yfull) <= 1e-14
