@@ -477,10 +477,10 @@ def symmetric_variant(h2d, op_dir, cfg, xs, nx, y, stream, args):
 
 
 def launches_per_matvec(inf, world):
-    # permute-in (1-GPU ORIGINAL order) or unpad (gathered), stage A, stage B, the P2P
-    # kernels (warp-per-leaf / CTA fast / generic, those with leaves), combine; the
-    # symmetric apply adds stage B' (A', B', C' in place of A, B)
-    return 4 + inf.get("p2p_launches", 1) + (1 if inf.get("symmetric_apply") else 0)
+    # permute-in (1-GPU ORIGINAL order) or unpad (gathered), the low-rank apply kernels
+    # (stage A / B rings + small-item kernels; symmetric: A', B', C'), the P2P kernels
+    # (warp-per-leaf / CTA fast / generic, those with leaves), combine
+    return 2 + inf.get("apply_launches", 2) + inf.get("p2p_launches", 1)
 
 
 # FP64-pipe instructions per kernel evaluation in p2p_fast_kernel's unrolled tile loop,

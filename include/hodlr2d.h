@@ -136,6 +136,9 @@ typedef struct {
   int p2p_launches;          /* near-field kernels per matvec: warp-per-leaf (<= 32-point
                                 leaves), CTA fast path, generic (1..3)                 */
   int64_t p2p_leaves[3];     /* leaves on the warp / fast / generic P2P paths          */
+  int apply_launches;        /* low-rank apply kernels per matvec: stage A / B rings and
+                                their small-item (warp-per-item) kernels, B' (symmetric) */
+  int64_t small_items[2];    /* stage A boxes / stage B leaves on the small-item kernels */
 } hodlr2d_info;
 
 /* Fill *opts with the defaults listed above. */

@@ -74,6 +74,7 @@ class Info(C.Structure):
         ("stageA_bytes", C.c_int64), ("stageB_bytes", C.c_int64), ("p2p_pairs", C.c_double),
         ("device_bytes", C.c_int64), ("gather_stride", C.c_int64), ("p2p_bytes", C.c_int64),
         ("symmetric_apply", C.c_int), ("p2p_launches", C.c_int), ("p2p_leaves", C.c_int64 * 3),
+        ("apply_launches", C.c_int), ("small_items", C.c_int64 * 2),
     ]
 
     def as_dict(self) -> dict:

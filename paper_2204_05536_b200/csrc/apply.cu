@@ -559,18 +559,7 @@ __device__ __forceinline__ void warp_nbr(int lane, double pi, double qi, double 
         acc = fma(v, xj, acc);
         c[t] = vi ? v * xi : 0.0;
       }
-      const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
-      double a[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        a[k] = (b16 ? c[k + 4] : c[k]) + __shfl_xor_sync(0xffffffffu, b16 ? c[k] : c[k + 4], 16);
-      double b[2];
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-        b[k] = (b8 ? a[k + 2] : a[k]) + __shfl_xor_sync(0xffffffffu, b8 ? a[k] : a[k + 2], 8);
-      double v = (b4 ? b[1] : b[0]) + __shfl_xor_sync(0xffffffffu, b4 ? b[0] : b[1], 4);
-      v += __shfl_xor_sync(0xffffffffu, v, 2);
-      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      const double v = warp_transpose_sum8(c, lane);
       const int col = g + (lane >> 2);
       if ((lane & 3) == 0 && col < nc) out[cb + col] = v;
     }
@@ -899,10 +888,7 @@ template <int NS>
 static void set_pipe_attrs() {
   const int smem = (int)sizeof(PipeSmem<NS>);
   H2D_CUDA(cudaFuncSetAttribute(stageA_tma_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  H2D_CUDA(cudaFuncSetAttribute(stageB_tma_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   H2D_CUDA(cudaFuncSetAttribute(stageA_tma_kernel<NS>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                cudaSharedmemCarveoutMaxShared));
-  H2D_CUDA(cudaFuncSetAttribute(stageB_tma_kernel<NS>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                 cudaSharedmemCarveoutMaxShared));
 }
 
@@ -920,11 +906,8 @@ void finalize_schedule(Handle& h) {
     for (int64_t Y = 0; Y < L.nbox; ++Y)
       a_elems += (h.box_end(l, Y) - h.box_begin(l, Y)) * ((L.vR[(size_t)Y] + 1) & ~1);
   }
-  if (!h.persist_ctas) {
-    int sm = 0;
-    H2D_CUDA(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, h.device));
-    h.persist_ctas = 2 * sm;
-  }
+  if (!h.num_sms) H2D_CUDA(cudaDeviceGetAttribute(&h.num_sms, cudaDevAttrMultiProcessorCount, h.device));
+  if (!h.persist_ctas) h.persist_ctas = 2 * h.num_sms;
   const char* env_at = getenv("H2D_A_TARGET");    // diagnostics override (elements)
   const int64_t kATarget = env_at && atoll(env_at) >= 2048
                                ? atoll(env_at)
@@ -1014,8 +997,19 @@ void finalize_schedule(Handle& h) {
       }
     }
   }
-  // largest items first: the dynamic (atomic-counter) schedule then ends with small items
-  std::stable_sort(aitems.begin(), aitems.end(), [](const AItem& a, const AItem& b) {
+  // single-chunk boxes of <= kSmallARows rows go to the warp-per-item kernel (tail of the
+  // list, H2D_SMALL_ITEMS=0 keeps them in the ring); the ring's items largest first: the
+  // dynamic (atomic-counter) schedule then ends with small items
+  // (only when there are enough of them to fill the GPU: a handful stay in the ring)
+  const bool small_items = !(getenv("H2D_SMALL_ITEMS") && atoi(getenv("H2D_SMALL_ITEMS")) == 0);
+  // H2D_SMALL_MIN (tests): the minimum count (default 4 per SM)
+  const int64_t small_min = getenv("H2D_SMALL_MIN") ? atoll(getenv("H2D_SMALL_MIN")) : 4 * (int64_t)h.num_sms;
+  auto a_small = [](const AItem& a) { return a.nrows <= kSmallARows && a.ritem < 0 && a.out >= 0; };
+  const bool a_split = small_items && std::count_if(aitems.begin(), aitems.end(), a_small) >= small_min;
+  const auto amid = std::stable_partition(aitems.begin(), aitems.end(),
+                                          [&](const AItem& a) { return !(a_split && a_small(a)); });
+  h.n_abig = amid - aitems.begin();
+  std::stable_sort(aitems.begin(), amid, [](const AItem& a, const AItem& b) {
     return (int64_t)a.nrows * a.Rp > (int64_t)b.nrows * b.Rp;
   });
   // symmetric stage B' items over the first-side U box panels (same chunking as stage A);
@@ -1129,9 +1123,49 @@ void finalize_schedule(Handle& h) {
       bleaf.push_back(lf);
     }
   }
+  if (getenv("H2D_VERBOSE")) {   // diagnostics: stage A / B items, stages and bytes by size
+    const int edges[6] = {0, 8, 32, 96, 224, 1 << 30};
+    double cnt[5] = {0}, el[5] = {0}, st[5] = {0};
+    for (size_t k = 0; k < bitems.size(); ++k) {
+      const int rows = bitems[k].rows, rowsp = (rows + 1) & ~1;
+      int b = 0;
+      while (rows > edges[b + 1]) ++b;
+      const int64_t lf = bleaf[k];
+      const int cols_s = std::min(kStageVec, kStageDbl / rowsp);
+      for (int l = 1; l <= h.kappa; ++l) {
+        const Level& L = h.levels[(size_t)l];
+        const int64_t X = lf >> (2 * (h.kappa - l));
+        const int R = L.ucolbase[(size_t)X + 1] - L.ucolbase[(size_t)X];
+        el[b] += (double)rowsp * R;
+        st[b] += (R + cols_s - 1) / cols_s;
+      }
+      cnt[b] += 1;
+    }
+    for (int b = 0; b < 5; ++b)
+      fprintf(stderr, "[h2d] B items rows (%d, %d]: %.0f items, %.0f stages, %.3f GB\n", edges[b], edges[b + 1],
+              cnt[b], st[b], el[b] * 8e-9);
+    double ac[5] = {0}, ae[5] = {0}, as[5] = {0};
+    for (const AItem& it : aitems) {
+      int b = 0;
+      while (it.nrows > edges[b + 1]) ++b;
+      const int rs = std::min(kStageVec, kStageDbl / it.Rp);
+      ac[b] += 1;
+      ae[b] += (double)it.nrows * it.Rp;
+      as[b] += (it.nrows + rs - 1) / rs;
+    }
+    for (int b = 0; b < 5; ++b)
+      fprintf(stderr, "[h2d] A items rows (%d, %d]: %.0f items, %.0f stages, %.3f GB\n", edges[b], edges[b + 1],
+              ac[b], as[b], ae[b] * 8e-9);
+  }
   std::vector<size_t> ord(bitems.size());
   std::iota(ord.begin(), ord.end(), 0);
   std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return bcost[a] > bcost[b]; });
+  // whole leaves of <= kSmallBRows rows: warp-per-item kernel (tail of the list; the
+  // multi-RHS kernels still take the whole list)
+  auto b_small = [&](size_t k) { return bitems[k].rows <= kSmallBRows && bitems[k].rows == bitems[k].mL; };
+  const bool b_split = small_items && std::count_if(ord.begin(), ord.end(), b_small) >= small_min;
+  h.n_bbig = std::stable_partition(ord.begin(), ord.end(), [&](size_t k) { return !(b_split && b_small(k)); }) -
+             ord.begin();
   std::vector<BItem> bsorted;
   std::vector<BLevel> blev;
   bsorted.reserve(bitems.size());
@@ -1310,21 +1344,55 @@ void begin_matvec_timing(Handle& h) {
 
 void mark_after_input(Handle& h) { record(h, 1, h.stream); }
 
+template <int NS, int SD, int SV>
+static void launch_stageB_geom(Handle& h, cudaStream_t hi) {
+  static bool set = false;
+  const size_t smem = sizeof(PipeSmem<NS, SD, SV>);
+  if (!set) {
+    H2D_CUDA(cudaFuncSetAttribute(stageB_tma_kernel<NS, SD, SV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    H2D_CUDA(cudaFuncSetAttribute(stageB_tma_kernel<NS, SD, SV>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+    set = true;
+  }
+  stageB_tma_kernel<NS, SD, SV><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+      h.d_bitems, h.d_blev, (int)h.n_bbig, h.d_counters + 1, h.kappa, h.lp, h.d_yfar);
+  H2D_LAUNCH_CHECK();
+}
+
+static void launch_small(Handle& h, bool stage_a, const double* d_xtree, double* t, cudaStream_t hi) {
+  const int64_t n = stage_a ? h.n_aitems - h.n_abig : h.n_bitems - h.n_bbig;
+  if (n <= 0) return;
+  // 16 CTAs x 8 warps per SM requested: the warps are latency-bound on their own loads
+  const int grid = (int)std::min<int64_t>((int64_t)h.num_sms * 16, (n + 7) / 8);
+  if (stage_a)
+    stageA_small_kernel<<<grid, 256, 0, hi>>>(h.d_aitems + h.n_abig, (int)n, h.lp, d_xtree, h.d_vdst, t);
+  else
+    stageB_small_kernel<<<grid, 256, 0, hi>>>(h.d_bitems + h.n_bbig, h.d_blev + h.n_bbig * h.kappa, (int)n,
+                                              h.kappa, h.lp, h.d_yfar);
+  H2D_LAUNCH_CHECK();
+}
+
+static void launch_stageB(Handle& h, cudaStream_t hi) {
+  launch_small(h, false, nullptr, nullptr, hi);
+  if (h.n_bbig <= 0) return;
+  // (a 2 x 44 KB ring measured 1 % slower on C3; 5 x 16 KB stays)
+  if (h.pipe_ns == kNSDeep) launch_stageB_geom<kNSDeep, kStageDbl, kStageVec>(h, hi);
+  else launch_stageB_geom<kNSShallow, kStageDbl, kStageVec>(h, hi);
+}
+
 template <int NS>
 static void launch_stages(Handle& h, const double* d_xtree, cudaStream_t hi) {
   const size_t smem = sizeof(PipeSmem<NS>);
-  if (h.n_aitems > 0) {
+  launch_small(h, true, d_xtree, h.d_t, hi);
+  if (h.n_abig > 0) {
     stageA_tma_kernel<NS><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
-        h.d_aitems, (int)h.n_aitems, h.d_counters, h.lp, d_xtree, h.d_vdst, h.d_t, h.d_tpart,
+        h.d_aitems, (int)h.n_abig, h.d_counters, h.lp, d_xtree, h.d_vdst, h.d_t, h.d_tpart,
         h.d_ritems, h.d_rcount);
     H2D_LAUNCH_CHECK();
   }
   record(h, 2, hi);
-  if (h.n_bitems > 0) {
-    stageB_tma_kernel<NS><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
-        h.d_bitems, h.d_blev, (int)h.n_bitems, h.d_counters + 1, h.kappa, h.lp, h.d_yfar);
-    H2D_LAUNCH_CHECK();
-  }
+  launch_stageB(h, hi);
 }
 
 // Matvec on TREE-order x (S7-S9).  Stages A and B (HBM-bound) run on the high-priority
@@ -1390,9 +1458,10 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
     const size_t smem = sizeof(PipeSmem<kNSShallow>);
     H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 4 * sizeof(int32_t), hi));
     H2D_CUDA(cudaMemsetAsync(h.d_y1, 0, (size_t)h.kappa * h.n * sizeof(double), hi));
-    if (h.n_aitems > 0) {
+    launch_small(h, true, d_xtree, h.d_t1, hi);
+    if (h.n_abig > 0) {
       stageA_tma_kernel<kNSShallow><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
-          h.d_aitems, (int)h.n_aitems, h.d_counters, h.lp, d_xtree, h.d_vdst, h.d_t1, h.d_tpart, h.d_ritems,
+          h.d_aitems, (int)h.n_abig, h.d_counters, h.lp, d_xtree, h.d_vdst, h.d_t1, h.d_tpart, h.d_ritems,
           h.d_rcount);
       H2D_LAUNCH_CHECK();
     }
@@ -1404,11 +1473,7 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
       H2D_LAUNCH_CHECK();
     }
     record(h, 2, hi);
-    if (h.n_bitems > 0) {
-      stageB_tma_kernel<kNSShallow><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
-          h.d_bitems, h.d_blev, (int)h.n_bitems, h.d_counters + 1, h.kappa, h.lp, h.d_yfar);
-      H2D_LAUNCH_CHECK();
-    }
+    launch_stageB(h, hi);
   } else {
     H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 2 * sizeof(int32_t), hi));
     if (h.pipe_ns == kNSShallow) launch_stages<kNSShallow>(h, d_xtree, hi);

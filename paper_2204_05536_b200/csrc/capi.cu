@@ -142,6 +142,7 @@ static void clear_factors(Handle& h) {
   h.release(h.d_vdst); h.d_vdst = nullptr;
   h.release(h.d_tpart); h.d_tpart = nullptr;
   h.n_aitems = h.n_ritems = 0;
+  h.n_abig = h.n_bbig = 0;
 }
 
 // |I_X| of box (cx, cy) at level l: children of the parent and its edge sharers (inside the
@@ -686,6 +687,10 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   info->p2p_leaves[1] = h.n_p2p_fast;
   info->p2p_leaves[2] = h.n_p2p_gen;
   info->p2p_launches = (h.n_p2p_warp > 0) + (h.n_p2p_fast > 0) + (h.n_p2p_gen > 0);
+  info->small_items[0] = h.n_aitems - h.n_abig;
+  info->small_items[1] = h.n_bitems - h.n_bbig;
+  info->apply_launches = (h.n_abig > 0) + (h.n_aitems > h.n_abig) + (h.n_bbig > 0) + (h.n_bitems > h.n_bbig) +
+                         (h.symapply && h.n_b1items > 0);
   (void)rsum;
   return H2D_OK;
   H2D_CATCH

@@ -237,6 +237,7 @@ struct Handle {
   int32_t* d_p2p_fast = nullptr;          // leaves of the persistent fast P2P kernel
   int32_t* d_p2p_gen = nullptr;           // leaves of the generic P2P kernel
   int64_t n_p2p_fast = 0, n_p2p_gen = 0;
+  int64_t n_abig = 0, n_bbig = 0;         // stage A / B items on the ring (the rest: small-item kernels)
   int32_t* d_p2p_warp = nullptr;          // <= 32-point leaves of the warp-per-leaf P2P kernel
   int64_t n_p2p_warp = 0;
   // symmetric apply (symmetric build on a single-rank handle, R23): A' over the

@@ -55,6 +55,25 @@ __device__ __forceinline__ void pipe_init(PipeSmem<NS, SD, SV>& S) {
   __syncthreads();
 }
 
+// Sum 8 per-lane values c[0..7] over the 32 lanes of a warp (a transposed butterfly: 9
+// double shuffles instead of 8 x 5).  Lane 4 t + (0..3) ends up holding the sum of c[t];
+// read it from lane 4 t.  Fixed order, deterministic.
+__device__ __forceinline__ double warp_transpose_sum8(const double (&c)[8], int lane) {
+  const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
+  double a[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    a[k] = (b16 ? c[k + 4] : c[k]) + __shfl_xor_sync(0xffffffffu, b16 ? c[k] : c[k + 4], 16);
+  double b[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    b[k] = (b8 ? a[k + 2] : a[k]) + __shfl_xor_sync(0xffffffffu, b8 ? a[k] : a[k + 2], 8);
+  double v = (b4 ? b[1] : b[0]) + __shfl_xor_sync(0xffffffffu, b4 ? b[0] : b[1], 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v;
+}
+
 constexpr int kSymTile = 96, kSymMaxB = kSymTile / 16;
 
 // 0.5 log(r2) for normal r2 > 0: r2 = 2^e m, m in [1, 2); c_k = 1 + (k + 1/2)/128 is the

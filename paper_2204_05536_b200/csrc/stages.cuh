@@ -85,6 +85,38 @@ __device__ void stageA_producer(PipeSmem<NS, SD>& S, const AItem* __restrict__ i
   }
 }
 
+// Sum the G group partials of the consumer threads (thread g W + i holds pair i of group g
+// in red[2 (g W + i) .. + 1]) into group 0: serially for G <= 8, else by a fixed pairwise
+// tree (ceil(log2 G) barrier steps instead of a G-long dependent chain per output: narrow
+// panels / short rows have G up to 224).  Deterministic; ends with a barrier, so group 0's
+// values are visible to all consumers.
+__device__ __forceinline__ void group_tree_sum(double* red, int G, int W, int g) {
+  const int tid = threadIdx.x;
+  named_bar_sync(1, kCons);
+  if (G <= 8) {   // few groups (the common wide-panel case): one serial pass, one barrier
+    if (g == 0) {
+      double u0 = red[2 * tid], u1 = red[2 * tid + 1];
+      for (int gg = 1; gg < G; ++gg) {
+        u0 += red[2 * (tid + gg * W)];
+        u1 += red[2 * (tid + gg * W) + 1];
+      }
+      red[2 * tid] = u0;
+      red[2 * tid + 1] = u1;
+    }
+    named_bar_sync(1, kCons);
+    return;
+  }
+  for (int span = G; span > 1;) {
+    const int half = (span + 1) >> 1;
+    if (g < span - half) {
+      red[2 * tid] += red[2 * (tid + half * W)];
+      red[2 * tid + 1] += red[2 * (tid + half * W) + 1];
+    }
+    named_bar_sync(1, kCons);
+    span = half;
+  }
+}
+
 // Consumers work on column pairs (one 16-byte smem load = 2 panel elements; Rp is even
 // and the padding column is zero, so a pair never straddles a row).  P = Rp / 2 pairs per
 // row.  P <= kCons: thread (g, p) = (tid / P, tid % P) owns pair p, rows g, g + G, ...
@@ -328,15 +360,10 @@ __device__ void stageA_consumers(PipeSmem<NS, SD>& S, const int32_t* __restrict_
       if (G > 1) {
         S.red[2 * tid] = g < G ? s0 : 0.0;
         S.red[2 * tid + 1] = g < G ? s1 : 0.0;
-        named_bar_sync(1, kCons);
+        group_tree_sum(S.red, G, P, g);
         if (tid < P) {
-          double u0 = 0.0, u1 = 0.0;
-          for (int gg = 0; gg < G; ++gg) {
-            u0 += S.red[2 * (tid + gg * P)];
-            u1 += S.red[2 * (tid + gg * P) + 1];
-          }
-          put(2 * tid, u0);
-          put(2 * tid + 1, u1);
+          put(2 * tid, S.red[2 * tid]);
+          put(2 * tid + 1, S.red[2 * tid + 1]);
         }
         named_bar_sync(1, kCons);
       } else if (tid < P) {
@@ -415,6 +442,87 @@ stageA_dual_kernel(const AItem* __restrict__ items, int n_items, int32_t* counte
   else stageA_consumers<NS, true, SD>(S, udst, t2, tpart, ritems, rcount, dc);
 }
 
+// ---------------------------------------------------------------- small items
+// Items too small for the bulk-copy ring (its per-stage and per-item overhead exceeds their
+// bytes; clustered inputs such as the paper's Chebyshev grids put most boxes / leaves here)
+// run one warp per item on direct, coalesced 16-byte loads instead.
+constexpr int kSmallARows = 32, kSmallBRows = 8;
+
+// Stage A, boxes of <= kSmallARows rows in one chunk: lane owns column pairs pb + lane and
+// pb + 32 + lane of a 64-pair block, rows in order; t through vdst (no reduction: the warp
+// owns the whole box).
+__global__ void __launch_bounds__(256)
+stageA_small_kernel(const AItem* __restrict__ items, int n_items, LevelPtrs lp, const double* __restrict__ x,
+                    const int32_t* __restrict__ vdst, double* __restrict__ t) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_items; k += nw) {
+    const AItem it = items[k];
+    const double* __restrict__ V = lp.V[it.level] + it.v_off;
+    const double* __restrict__ xr = x + it.x_off;
+    const int P = it.Rp >> 1;
+    for (int pb = 0; pb < P; pb += 64) {
+      const int p0 = pb + lane, p1 = pb + 32 + lane;
+      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+      for (int j = 0; j < it.nrows; ++j) {
+        const double xj = __ldg(xr + j);
+        const double2* __restrict__ row = reinterpret_cast<const double2*>(V + (int64_t)j * it.Rp);
+        if (p0 < P) {
+          const double2 v = __ldcs(row + p0);
+          a0 = fma(v.x, xj, a0);
+          a1 = fma(v.y, xj, a1);
+        }
+        if (p1 < P) {
+          const double2 v = __ldcs(row + p1);
+          b0 = fma(v.x, xj, b0);
+          b1 = fma(v.y, xj, b1);
+        }
+      }
+      if (2 * p0 < it.R) t[vdst[it.out + 2 * p0]] = a0;
+      if (2 * p0 + 1 < it.R) t[vdst[it.out + 2 * p0 + 1]] = a1;
+      if (2 * p1 < it.R) t[vdst[it.out + 2 * p1]] = b0;
+      if (2 * p1 + 1 < it.R) t[vdst[it.out + 2 * p1 + 1]] = b1;
+    }
+  }
+}
+// Stage B, whole leaves of <= kSmallBRows rows: lane owns columns c = lane + 32 k of every
+// level's (leaf, level) panel (column-major, mLp <= 8 rows: one to four 16-byte loads per
+// column), 8 row accumulators, reduced over the warp by one transposed butterfly.  (Loading
+// 2-8 columns per lane ahead of use measured 5-10 % slower: tiny items waste the predicated
+// loads.)
+__global__ void __launch_bounds__(256)
+stageB_small_kernel(const BItem* __restrict__ items, const BLevel* __restrict__ blev, int n_items, int kappa,
+                    LevelPtrs lp, double* __restrict__ yfar) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_items; k += nw) {
+    const BItem it = items[k];
+    const int mLp = (it.mL + 1) & ~1;
+    double acc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) acc[r] = 0.0;
+    for (int l = 1; l <= kappa; ++l) {
+      const BLevel lv = blev[(int64_t)k * kappa + l - 1];
+      if (lv.R <= 0) continue;
+      const double* __restrict__ U = lp.U[l] + lv.uoff;
+      const double* __restrict__ tb = lp.tu[l] + lv.tcol;
+      for (int c = lane; c < lv.R; c += 32) {
+        const double tc = __ldg(tb + c);
+        const double2* __restrict__ col = reinterpret_cast<const double2*>(U + (int64_t)c * mLp);
+#pragma unroll
+        for (int r2 = 0; r2 < 4; ++r2)
+          if (2 * r2 < mLp) {
+            const double2 u = __ldcs(col + r2);
+            acc[2 * r2] = fma(u.x, tc, acc[2 * r2]);
+            acc[2 * r2 + 1] = fma(u.y, tc, acc[2 * r2 + 1]);
+          }
+      }
+    }
+    const double v = warp_transpose_sum8(acc, lane);
+    const int r = lane >> 2;
+    if ((lane & 3) == 0 && r < it.rows) yfar[it.yrow + r] = v;
+  }
+}
 // ---------------------------------------------------------------- stage B: yfar = U t
 // Item = rows [r0, r0 + rows) (rows <= 256) of served leaf L.  For every ancestor level l
 // the leaf's U columns form one contiguous column-major range (stride mLp); a stage holds
@@ -423,8 +531,8 @@ stageA_dual_kernel(const AItem* __restrict__ items, int n_items, int32_t* counte
 // (g, i) = (tid / rows, tid % rows) owns row i and columns g, g + G, ... (G = 256 / rows),
 // reduced in smem at the end of the item: one yfar write per row, no atomics.
 // Stage header: a = rows, b = rowsp (row stride inside the stage), c = output row.
-template <int NS>
-__device__ void stageB_producer(PipeSmem<NS>& S, const BItem* __restrict__ items,
+template <int NS, int SD = kStageDbl, int SV = kStageVec>
+__device__ void stageB_producer(PipeSmem<NS, SD, SV>& S, const BItem* __restrict__ items,
                                 const BLevel* __restrict__ blev, int n_items, int32_t* counter,
                                 int kappa, const LevelPtrs& lp) {
   const int lane = threadIdx.x & 31;
@@ -482,8 +590,12 @@ __device__ void stageB_producer(PipeSmem<NS>& S, const BItem* __restrict__ items
       if (done) break;
       continue;
     }
-    const int cols_s = min(kStageVec, kStageDbl / rowsp);
+    // a stage packs consecutive column ranges of successive levels: the (leaf, level)
+    // panels share the row stride, so their concatenation is one column-major block and the
+    // consumers never see level boundaries (small leaves: one stage per leaf, not per level)
+    const int cols_s = min(SV, SD / rowsp);
     bool first = true;
+    int fill = 0;
     for (int li = 0; li < lastl; ++li) {
       const int Rl = __shfl_sync(0xffffffffu, R, li);
       const int cbl = __shfl_sync(0xffffffffu, cb, li);
@@ -491,31 +603,39 @@ __device__ void stageB_producer(PipeSmem<NS>& S, const BItem* __restrict__ items
       if (Rl == 0) continue;
       const double* Ub = lp.U[li + 1] + ubl;
       const double* tb = lp.tu[li + 1] + cbl;
-      for (int c0 = 0; c0 < Rl; c0 += cols_s) {
-        const int cols = min(cols_s, Rl - c0);
+      for (int c0 = 0; c0 < Rl;) {
+        if (fill == 0) mbar_wait(&S.empty[stage], phase ^ 1);
+        const int cols = min(cols_s - fill, Rl - c0);
         const bool last = li == lastl - 1 && c0 + cols >= Rl;
-        mbar_wait(&S.empty[stage], phase ^ 1);
+        double* dst = S.ring[stage] + fill * rowsp;
         if (lane == 0) {
-          StageHdr& h = S.hdr[stage];
-          h.item = cur;
-          h.cnt = cols;
-          h.flags = (first ? kFirst : 0) | (last ? kLast : 0);
-          h.a = it.rows;
-          h.b = rowsp;
-          h.c = yrow;
-          mbar_arrive_expect_tx(&S.full[stage], (uint32_t)cols * (uint32_t)rowsp * 8u);
-          if (whole)
-            bulk_g2s(S.ring[stage], Ub + (int64_t)c0 * mLp, (uint32_t)cols * (uint32_t)mLp * 8u,
-                     &S.full[stage], pol);
+          mbar_expect_tx(&S.full[stage], (uint32_t)cols * (uint32_t)rowsp * 8u);
+          if (whole) bulk_g2s(dst, Ub + (int64_t)c0 * mLp, (uint32_t)cols * (uint32_t)mLp * 8u, &S.full[stage], pol);
         }
+        __syncwarp();
         if (!whole)
           for (int c = lane; c < cols; c += 32)
-            bulk_g2s(S.ring[stage] + c * rowsp, Ub + (int64_t)(c0 + c) * mLp + it.r0,
-                     (uint32_t)rowsp * 8u, &S.full[stage], pol);
-        for (int c = lane; c < cols; c += 32) cp_async8(&S.vec[stage][c], tb + c0 + c);
-        cp_async_arrive_noinc(&S.full[stage]);
-        if (++stage == NS) { stage = 0; phase ^= 1; }
-        first = false;
+            bulk_g2s(dst + c * rowsp, Ub + (int64_t)(c0 + c) * mLp + it.r0, (uint32_t)rowsp * 8u, &S.full[stage],
+                     pol);
+        for (int c = lane; c < cols; c += 32) cp_async8(&S.vec[stage][fill + c], tb + c0 + c);
+        fill += cols;
+        c0 += cols;
+        if (fill == cols_s || last) {
+          if (lane == 0) {
+            StageHdr& h = S.hdr[stage];
+            h.item = cur;
+            h.cnt = fill;
+            h.flags = (first ? kFirst : 0) | (last ? kLast : 0);
+            h.a = it.rows;
+            h.b = rowsp;
+            h.c = yrow;
+            mbar_arrive(&S.full[stage]);
+          }
+          cp_async_arrive_noinc(&S.full[stage]);
+          if (++stage == NS) { stage = 0; phase ^= 1; }
+          first = false;
+          fill = 0;
+        }
       }
     }
   }
@@ -524,8 +644,8 @@ __device__ void stageB_producer(PipeSmem<NS>& S, const BItem* __restrict__ items
 // Consumers work on row pairs (one 16-byte smem load = rows 2i, 2i+1 of a column; rowsp is
 // even and the padding row is zero): thread (g, i) = (tid / RP, tid % RP), RP = rowsp / 2,
 // owns row pair i and columns g, g + G, ... (G = kCons / RP), reduced in smem per item.
-template <int NS>
-__device__ void stageB_consumers(PipeSmem<NS>& S, double* __restrict__ yfar) {
+template <int NS, int SD = kStageDbl, int SV = kStageVec>
+__device__ void stageB_consumers(PipeSmem<NS, SD, SV>& S, double* __restrict__ yfar) {
   const int tid = threadIdx.x, lane = tid & 31;
   int stage = 0;
   uint32_t phase = 0;
@@ -571,23 +691,18 @@ __device__ void stageB_consumers(PipeSmem<NS>& S, double* __restrict__ yfar) {
     if (!(h.flags & kLast)) continue;
     S.red[2 * tid] = g < G ? a0 + b0 : 0.0;
     S.red[2 * tid + 1] = g < G ? a1 + b1 : 0.0;
-    named_bar_sync(1, kCons);
-    if (tid < rows) {
-      const int ip = tid >> 1, e = tid & 1;
-      double u = 0.0;
-      for (int gg = 0; gg < G; ++gg) u += S.red[2 * (ip + gg * RP) + e];
-      yfar[h.c + tid] = u;
-    }
+    group_tree_sum(S.red, G, RP, g);
+    if (tid < rows) yfar[h.c + tid] = S.red[tid];   // group 0: red[2 i + e] = row 2 i + e
     named_bar_sync(1, kCons);
   }
 }
 
-template <int NS>
+template <int NS, int SD = kStageDbl, int SV = kStageVec>
 __global__ void __launch_bounds__(kPipeThreads, 3)
 stageB_tma_kernel(const BItem* __restrict__ items, const BLevel* __restrict__ blev, int n_items,
                   int32_t* counter, int kappa, LevelPtrs lp, double* __restrict__ yfar) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  PipeSmem<NS>& S = *reinterpret_cast<PipeSmem<NS>*>(smem_raw);
+  PipeSmem<NS, SD, SV>& S = *reinterpret_cast<PipeSmem<NS, SD, SV>*>(smem_raw);
   pipe_init(S);
   if (threadIdx.x >= kCons) stageB_producer(S, items, blev, n_items, counter, kappa, lp);
   else stageB_consumers(S, yfar);

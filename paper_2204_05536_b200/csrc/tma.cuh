@@ -31,6 +31,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+// `bytes` more expected transaction count for the current phase, no arrival (several bulk
+// copies into one stage, the stage closed by one mbar_arrive after the last of them).
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+
 // The waiting thread is suspended (suspend-time hint ~10 ms, woken at phase completion)
 // instead of spinning, so idle pipeline warps leave issue slots to co-resident kernels.
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {

@@ -101,3 +101,32 @@ def test_warp_path_partition_union(h2d):
         assert p.info()["p2p_leaves"][0] > 0
         parts.append(p.matvec(dev(x), order="tree").cpu().numpy())
     assert rel(np.concatenate(parts), yfull) <= 1e-14
+
+
+@pytest.mark.parametrize("symmetric", [False, True])
+def test_small_item_kernels(h2d, symmetric):
+    """Clustered Chebyshev grid at the depth rule: hundreds of boxes <= 32 rows and leaves
+    <= 8 rows run on the warp-per-item stage A / B kernels (info small_items; the default
+    threshold of 4 per SM lowered to 1 by H2D_SMALL_MIN).  Equal to the
+    all-ring build (H2D_SMALL_ITEMS=0) to 1e-13 and to the dense product to 1e-10;
+    symmetric builds route A' / C' the same way."""
+    pts = W.chebyshev_grid(150)
+    kw = dict(c=1e-3, shift=22500.0, depth=-2, symmetric=symmetric)
+    os.environ["H2D_SMALL_MIN"] = "1"   # this size has fewer than 4 per SM of them
+    try:
+        op = build(h2d, pts, "rbf_phi1", 100, 1e-12, **kw)
+    finally:
+        os.environ.pop("H2D_SMALL_MIN")
+    sa, sb = op.info()["small_items"]
+    assert sa > 0 and sb > 0, (sa, sb)
+    os.environ["H2D_SMALL_ITEMS"] = "0"
+    try:
+        ref = build(h2d, pts, "rbf_phi1", 100, 1e-12, **kw)
+    finally:
+        os.environ.pop("H2D_SMALL_ITEMS")
+    assert ref.info()["small_items"] == [0, 0]
+    x = W.random_vector(pts.shape[0], 5500)
+    y = op.matvec(dev(x)).cpu().numpy()
+    assert rel(y, ref.matvec(dev(x)).cpu().numpy()) <= 1e-13
+    yd = oracle.dense_matvec(pts, x, KID["rbf_phi1"], 1e-3, 1.0, 22500.0)
+    assert rel(y, yd) <= 1e-10
