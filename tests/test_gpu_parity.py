@@ -377,3 +377,34 @@ def test_c5_rank_slice_full_size_sampled_rows(h2d):
     rows_orig = perm[inf["row_begin"] + rows_local]
     yd = oracle.dense_rows(pts, x, rows_orig, cfg.kernel, cfg.c, cfg.scale, cfg.shift)
     assert rel(y[rows_local], yd) <= 10 * cfg.tol
+
+
+# ------------------------------------------------------------------ configuration variants
+
+@pytest.mark.parametrize("env", [{"H2D_PIPE_CTAS_PER_SM": "1"}, {"H2D_P2P_SERIAL": "1"},
+                                 {"H2D_COPY_STREAM": "0"}, {"H2D_SMALL_ITEMS": "0"}])
+def test_runtime_variants_same_result(h2d, env):
+    """The alternative pipeline shapes and scheduling switches compute the same matvec:
+    1 CTA/SM with the 9-stage ring, the P2P serialised before the streams, host copies on
+    the caller's stream, small items kept in the ring (C2, and a clustered grid with small
+    items).  Host pointers exercise the copy paths."""
+    cases = [(W.config_points(W.CONFIGS["c2"]), "imq", 64, 1e-10, dict(c=0.1)),
+             (W.chebyshev_grid(120), "rbf_phi1", 100, 1e-12, dict(c=1e-3, shift=14400.0, depth=-2))]
+    for pts, kernel, leaf, tol, kw in cases:
+        ref = h2d.Hodlr2d.build(dev(pts), kernel, leaf, tol, box_lo=(-1, -1), box_side=2.0, **kw)
+        saved = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            op = h2d.Hodlr2d.build(dev(pts), kernel, leaf, tol, box_lo=(-1, -1), box_side=2.0, **kw)
+            x = W.random_vector(pts.shape[0], 77)
+            y = op.matvec(x.copy())                      # host pointers: copy paths
+            yd = op.matvec(dev(x)).cpu().numpy()
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        yr = ref.matvec(dev(x)).cpu().numpy()
+        assert np.array_equal(y, yd)
+        assert rel(y, yr) <= 1e-14
