@@ -131,6 +131,13 @@ static void clear_factors(Handle& h) {
   h.m_aitems = nullptr; h.m_ritems = nullptr; h.m_rcount = nullptr; h.m_tpart = nullptr;
   h.m_xm = h.m_xcols = h.m_t = h.m_yfar = h.m_ynear = nullptr;
   h.m_n_aitems = 0;
+  for (void* q : {(void*)h.m_b1items, (void*)h.m_b1ritems, (void*)h.m_b1rcount, (void*)h.m_b1tpart, (void*)h.m_t1,
+                  (void*)h.m_y1})
+    h.release(q);
+  h.m_b1items = nullptr; h.m_b1ritems = nullptr; h.m_b1rcount = nullptr;
+  h.m_b1tpart = h.m_t1 = h.m_y1 = nullptr;
+  h.m_n_b1items = 0;
+  h.m_sym_ok = false;
   h.multi_ready = false;
   h.release(h.d_bitems); h.d_bitems = nullptr;
   h.release(h.d_blev); h.d_blev = nullptr;

@@ -261,6 +261,13 @@ struct Handle {
   int32_t* m_rcount = nullptr;
   double *m_tpart = nullptr, *m_xm = nullptr, *m_xcols = nullptr, *m_t = nullptr;
   double *m_yfar = nullptr, *m_ynear = nullptr;
+  // symmetric multi-RHS (8-vector chunks): B' items over the U box panels, T1 / Y1
+  bool m_sym_ok = false;
+  AItem* m_b1items = nullptr;
+  int64_t m_n_b1items = 0;
+  RItem* m_b1ritems = nullptr;
+  int32_t* m_b1rcount = nullptr;
+  double *m_b1tpart = nullptr, *m_t1 = nullptr, *m_y1 = nullptr;
   double* d_ynear = nullptr;              // [3n] near-field P2P slots (p2p_sym_kernel)
   double* d_yfar = nullptr;               // [served] low-rank part (stage B output)
   cudaStream_t hi_stream = nullptr;       // stages A, B (high priority)

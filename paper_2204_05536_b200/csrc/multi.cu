@@ -204,6 +204,68 @@ constexpr int kConsWarps = kCons / 32;
 constexpr int kMaxMTA = (kTileW / 8 + kConsWarps - 1) / kConsWarps;   // m-tiles per warp, stage A
 constexpr int kMaxMTB = (kBRowsMax / 8 + kConsWarps - 1) / kConsWarps; // m-tiles per warp, stage B
 
+// Column sums of one stage for the CNT m-tiles warp w owns (w + 7 i, i < CNT): M = panel
+// columns, N = 8 vectors, K = rows (4 per DMMA).  Dispatched on the exact count so narrow
+// panels (1-2 m-tiles per warp) do not issue the predicates of all kMaxMTA slots; whole
+// k-steps run without bounds checks.
+template <int CNT>
+__device__ __forceinline__ void colsum_mtiles(double (&d)[kMaxMTA][2], const double* __restrict__ sv,
+                                              const double* __restrict__ sx, int rows, int Wp, int w, int gq, int tq) {
+  int cidx[CNT];
+#pragma unroll
+  for (int i = 0; i < CNT; ++i) cidx[i] = (w + kConsWarps * i) * 8 + gq;
+  int k0 = 0;
+  if constexpr (CNT <= 2) {   // few m-tiles: a second accumulator per m-tile (more DMMA chains in flight)
+    double e[CNT][2];
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) e[i][0] = e[i][1] = 0.0;
+    for (; k0 + 8 <= rows; k0 += 8) {
+      const int r = k0 + tq;
+      const double b = sx[r * 8 + gq], b2 = sx[(r + 4) * 8 + gq];
+#pragma unroll
+      for (int i = 0; i < CNT; ++i) {
+        dmma884(d[i][0], d[i][1], cidx[i] < Wp ? sv[r * Wp + cidx[i]] : 0.0, b);
+        dmma884(e[i][0], e[i][1], cidx[i] < Wp ? sv[(r + 4) * Wp + cidx[i]] : 0.0, b2);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) {
+      d[i][0] += e[i][0];
+      d[i][1] += e[i][1];
+    }
+  }
+  for (; k0 + 4 <= rows; k0 += 4) {
+    const int r = k0 + tq;
+    const double b = sx[r * 8 + gq];
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) dmma884(d[i][0], d[i][1], cidx[i] < Wp ? sv[r * Wp + cidx[i]] : 0.0, b);
+  }
+  if (k0 < rows) {
+    const int r = k0 + tq;
+    const bool rv = r < rows;
+    const double b = rv ? sx[r * 8 + gq] : 0.0;
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) dmma884(d[i][0], d[i][1], (rv && cidx[i] < Wp) ? sv[r * Wp + cidx[i]] : 0.0, b);
+  }
+}
+
+__device__ __forceinline__ void colsum_dispatch(double (&d)[kMaxMTA][2], const double* __restrict__ sv,
+                                                const double* __restrict__ sx, int rows, int Wp, int MT, int w, int gq,
+                                                int tq) {
+  const int cnt = MT > w ? (MT - w + kConsWarps - 1) / kConsWarps : 0;
+  switch (cnt) {
+    case 0: break;
+    case 1: colsum_mtiles<1>(d, sv, sx, rows, Wp, w, gq, tq); break;
+    case 2: colsum_mtiles<2>(d, sv, sx, rows, Wp, w, gq, tq); break;
+    case 3: colsum_mtiles<3>(d, sv, sx, rows, Wp, w, gq, tq); break;
+    case 4: colsum_mtiles<4>(d, sv, sx, rows, Wp, w, gq, tq); break;
+    case 5: colsum_mtiles<5>(d, sv, sx, rows, Wp, w, gq, tq); break;
+    case 6: colsum_mtiles<6>(d, sv, sx, rows, Wp, w, gq, tq); break;
+    case 7: colsum_mtiles<7>(d, sv, sx, rows, Wp, w, gq, tq); break;
+    default: colsum_mtiles<kMaxMTA>(d, sv, sx, rows, Wp, w, gq, tq); break;
+  }
+}
+
 // Stage A: M = tile columns (m-tile i of the item owned by warp i % 7, all rows), N = the 8
 // vectors, K = rows, 4 per DMMA.  No cross-warp reduction: every T entry has one owner.
 template <int NS, int SD, int SV>
@@ -232,21 +294,7 @@ __device__ void mA_consumers_dmma(PipeSmem<NS, SD, SV>& S, const int32_t* __rest
     }
     const double* __restrict__ sv = S.ring[stage];
     const double* __restrict__ sx = S.vec[stage];
-    const int rows = h.cnt;
-    for (int k0 = 0; k0 < rows; k0 += 4) {
-      const int r = k0 + tq;
-      const bool rv = r < rows;
-      const double b = rv ? sx[r * NR + gq] : 0.0;
-#pragma unroll
-      for (int i = 0; i < kMaxMTA; ++i) {
-        const int mt = w + kConsWarps * i;
-        if (mt < MT) {
-          const int c = mt * 8 + gq;
-          const double a = (rv && c < Wp) ? sv[r * Wp + c] : 0.0;
-          dmma884(d[i][0], d[i][1], a, b);
-        }
-      }
-    }
+    colsum_dispatch(d, sv, sx, h.cnt, Wp, MT, w, gq, tq);
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.empty[stage]);
     if (++stage == NS) { stage = 0; phase ^= 1; }
@@ -407,6 +455,191 @@ stageA_multi_kernel(const AItem* __restrict__ items, int n_items, int32_t* count
   if (threadIdx.x >= kCons) mA_producer<NS, NR, SD, SV>(S, items, n_items, counter, lp, xm);
   else if constexpr (NR == 8) mA_consumers_dmma<NS, SD, SV>(S, vdst, tm, tpartm, ritems, rcount);
   else mA_consumers<NS, NR, SD, SV>(S, vdst, tm, tpartm, ritems, rcount);
+}
+
+// ---------------------------------------------------------------- symmetric stage B' (multi)
+// Eight vectors through the first-side U box panels of the symmetric apply (R23): the
+// column sums T2 = U^T X (written through udst into the second-side t layout) and the row
+// products Y1 = U T1 (per level, [kappa][n][8]) from one read of U.  Items are whole panels
+// (R <= kTileW) in row chunks; a stage holds rows x Wp of U and, after them, the item's
+// Wp x 8 T1 tile (one more bulk copy: T1 is contiguous per row box, 64-byte aligned).
+// Stage header: a = R, b = Wp, c = out, d = ritem, pad = level, e = first TREE row.
+template <int NS, int SD, int SV>
+__device__ void mD_producer(PipeSmem<NS, SD, SV>& S, const AItem* __restrict__ items, int n_items, int32_t* counter,
+                            const LevelPtrs& lp, const double* __restrict__ xm, const double* __restrict__ t1m) {
+  constexpr int NR = 8;
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = l2_evict_first_policy();
+  int stage = 0;
+  uint32_t phase = 0;
+  int idx = 0, nidx = 0;
+  if (lane == 0) idx = atomicAdd(counter, 1);
+  idx = __shfl_sync(0xffffffffu, idx, 0);
+  if (lane == 0) nidx = atomicAdd(counter, 1);
+  AItem nit{};
+  if (idx < n_items) nit = items[idx];
+  for (;;) {
+    const bool done = idx >= n_items;
+    const AItem it = nit;
+    const int cur = idx;
+    idx = __shfl_sync(0xffffffffu, nidx, 0);
+    if (!done && lane == 0) nidx = atomicAdd(counter, 1);
+    if (!done && idx < n_items) nit = items[idx];
+    const int Wp = it.Rp;
+    const int rows_s = done ? 1 : min(SV / NR, (SD - Wp * NR) / max(Wp, 2));
+    const double* U = done ? nullptr : lp.Ub[it.level] + it.v_off;
+    int r0 = 0;
+    do {
+      const int rows = done ? 0 : min(rows_s, it.nrows - r0);
+      mbar_wait(&S.empty[stage], phase ^ 1);
+      if (lane == 0) {
+        StageHdr& h = S.hdr[stage];
+        h.item = done ? -1 : cur;
+        h.cnt = rows;
+        h.flags = (r0 == 0 ? kFirst : 0) | (r0 + rows >= it.nrows ? kLast : 0);
+        h.a = it.R;
+        h.b = Wp;
+        h.c = it.out;
+        h.d = it.ritem;
+        h.pad = it.level;
+        h.e = (int32_t)(it.x_off + r0);
+        const uint32_t ub = (uint32_t)rows * (uint32_t)Wp * 8u, tb = done ? 0u : (uint32_t)Wp * NR * 8u;
+        mbar_arrive_expect_tx(&S.full[stage], ub + tb);
+        if (ub) bulk_g2s(S.ring[stage], U + (int64_t)r0 * Wp, ub, &S.full[stage], pol);
+        if (tb) bulk_g2s(S.ring[stage] + rows * Wp, t1m + it.t1_off * NR, tb, &S.full[stage], pol);
+      }
+      const double* xs = xm + (it.x_off + r0) * NR;
+      for (int e = lane; e < rows * NR; e += 32) cp_async8(&S.vec[stage][e], xs + e);
+      cp_async_arrive_noinc(&S.full[stage]);
+      if (++stage == NS) { stage = 0; phase ^= 1; }
+      r0 += rows;
+    } while (!done && r0 < it.nrows);
+    if (done) break;
+  }
+}
+
+// Consumers: column sums as mA_consumers_dmma (M = panel columns, K = rows); row products
+// M = the stage's rows (row m-tile i of warp w: w + 7 i), N = 8 vectors, K = columns, two
+// accumulator chains per m-tile.
+template <int NS, int SD, int SV>
+__device__ void mD_consumers(PipeSmem<NS, SD, SV>& S, const int32_t* __restrict__ udst, double* __restrict__ t2m,
+                             double* __restrict__ tpartm, const RItem* __restrict__ ritems,
+                             int32_t* __restrict__ rcount, double* __restrict__ y1m, int64_t n) {
+  constexpr int NR = 8;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  int stage = 0;
+  uint32_t phase = 0;
+  int W = 1, Wp = 2, MT = 1;
+  double d[kMaxMTA][2];
+#pragma unroll
+  for (int i = 0; i < kMaxMTA; ++i) d[i][0] = d[i][1] = 0.0;
+  for (;;) {
+    mbar_wait(&S.full[stage], phase);
+    const StageHdr h = S.hdr[stage];
+    if (h.item < 0) break;
+    if (h.flags & kFirst) {
+      W = h.a;
+      Wp = h.b;
+      MT = (W + 7) >> 3;
+#pragma unroll
+      for (int i = 0; i < kMaxMTA; ++i) d[i][0] = d[i][1] = 0.0;
+    }
+    const double* __restrict__ sv = S.ring[stage];
+    const double* __restrict__ sx = S.vec[stage];
+    const int rows = h.cnt;
+    const double* __restrict__ t1s = sv + rows * Wp;
+    colsum_dispatch(d, sv, sx, rows, Wp, MT, w, gq, tq);   // column sums
+    const int RT = (rows + 7) >> 3;   // row products
+    for (int rt = w; rt < RT; rt += kConsWarps) {
+      const int r = rt * 8 + gq;
+      const bool rv = r < rows;
+      const double* __restrict__ urow = sv + (rv ? r : 0) * Wp;   // rows past the stage read row 0, masked
+      double e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0, g0 = 0.0, g1 = 0.0, q0 = 0.0, q1 = 0.0;
+      int k0 = 0;
+      for (; k0 + 16 <= Wp; k0 += 16) {   // four accumulator chains
+        const int c = k0 + tq;
+        dmma884(e0, e1, rv ? urow[c] : 0.0, t1s[c * NR + gq]);
+        dmma884(f0, f1, rv ? urow[c + 4] : 0.0, t1s[(c + 4) * NR + gq]);
+        dmma884(g0, g1, rv ? urow[c + 8] : 0.0, t1s[(c + 8) * NR + gq]);
+        dmma884(q0, q1, rv ? urow[c + 12] : 0.0, t1s[(c + 12) * NR + gq]);
+      }
+      e0 += g0;
+      e1 += g1;
+      f0 += q0;
+      f1 += q1;
+      for (; k0 + 8 <= Wp; k0 += 8) {
+        const int c = k0 + tq;
+        dmma884(e0, e1, rv ? urow[c] : 0.0, t1s[c * NR + gq]);
+        dmma884(f0, f1, rv ? urow[c + 4] : 0.0, t1s[(c + 4) * NR + gq]);
+      }
+      for (; k0 < Wp; k0 += 4) {
+        const int c = k0 + tq;
+        dmma884(e0, e1, (rv && c < Wp) ? urow[c] : 0.0, c < Wp ? t1s[c * NR + gq] : 0.0);
+      }
+      if (rv) {
+        double2* dst = reinterpret_cast<double2*>(y1m + ((int64_t)(h.pad - 1) * n + h.e + r) * NR + 2 * tq);
+        *dst = make_double2(e0 + f0, e1 + f1);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[stage]);
+    if (++stage == NS) { stage = 0; phase ^= 1; }
+    if (!(h.flags & kLast)) continue;
+#pragma unroll
+    for (int i = 0; i < kMaxMTA; ++i) {
+      const int mt = w + kConsWarps * i;
+      const int q = mt * 8 + gq;
+      if (mt < MT && q < W) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int k = 2 * tq + e;
+          if (h.c >= 0) t2m[(int64_t)udst[h.c + q] * NR + k] = d[i][e];
+          else tpartm[((int64_t)(-h.c - 1) + q) * NR + k] = d[i][e];
+        }
+      }
+    }
+    if (h.d >= 0) {
+      named_bar_sync(1, kCons);
+      if (tid == 0) {
+        __threadfence();
+        const int last = atomicAdd(rcount + h.d, 1) == ritems[h.d].nchunks - 1;
+        if (last) __threadfence();
+        S.flag = last;
+      }
+      named_bar_sync(1, kCons);
+      if (S.flag) {
+        const RItem ri = ritems[h.d];
+        for (int e = tid; e < ri.R * NR; e += kCons) {
+          const int q = e / NR, k = e - q * NR;
+          const double* __restrict__ pp = tpartm + ((int64_t)ri.p_off + q) * NR + k;
+          const int64_t cs = (int64_t)ri.R * NR;
+          double a0 = 0.0, a1 = 0.0;
+          int c = 0;
+          for (; c + 1 < ri.nchunks; c += 2) {
+            a0 += __ldcg(pp + c * cs);
+            a1 += __ldcg(pp + (c + 1) * cs);
+          }
+          if (c < ri.nchunks) a0 += __ldcg(pp + c * cs);
+          t2m[(int64_t)udst[ri.vpos + q] * NR + k] = a0 + a1;
+        }
+        if (tid == 0) rcount[h.d] = 0;
+      }
+    }
+  }
+}
+
+template <int NS, int SD, int SV>
+__global__ void __launch_bounds__(kPipeThreads, 3)
+stageA_dual_multi_kernel(const AItem* __restrict__ items, int n_items, int32_t* counter, LevelPtrs lp,
+                         const double* __restrict__ xm, const int32_t* __restrict__ udst, double* __restrict__ t2m,
+                         double* __restrict__ tpartm, const RItem* __restrict__ ritems, int32_t* __restrict__ rcount,
+                         const double* __restrict__ t1m, double* __restrict__ y1m, int64_t n) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  PipeSmem<NS, SD, SV>& S = *reinterpret_cast<PipeSmem<NS, SD, SV>*>(smem_raw);
+  pipe_init(S);
+  if (threadIdx.x >= kCons) mD_producer<NS, SD, SV>(S, items, n_items, counter, lp, xm, t1m);
+  else mD_consumers<NS, SD, SV>(S, udst, t2m, tpartm, ritems, rcount, y1m, n);
 }
 
 // ---------------------------------------------------------------- stage B (multi)
@@ -696,6 +929,39 @@ __global__ void combine_multi_kernel(int NR, int64_t row_begin, int64_t rows, co
   }
 }
 
+// symmetric apply: + the kappa per-level row products Y1 of B'
+__global__ void combine_multi_sym_kernel(int64_t rows, int kappa, const double* __restrict__ yfarm,
+                                         const double* __restrict__ y1m, const double* __restrict__ ynearm, int64_t n,
+                                         const double* __restrict__ xcols, double scale, double shift,
+                                         double* __restrict__ Y, int64_t ylen, const int32_t* __restrict__ perm,
+                                         int order_out, int64_t y_row0) {
+  // NR = 8: a row's 8 values are one 64-byte record in yfar and in every level of Y1 (four
+  // 16-byte loads each, levels outer, 8 register accumulators)
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = order_out == H2D_ORDER_ORIGINAL ? perm[r] : r - y_row0;
+    double v[8];
+    const double2* __restrict__ yf = reinterpret_cast<const double2*>(yfarm + r * 8);
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+      const double2 a = yf[k2];
+      v[2 * k2] = a.x;
+      v[2 * k2 + 1] = a.y;
+    }
+    for (int l = 0; l < kappa; ++l) {
+      const double2* __restrict__ y1 = reinterpret_cast<const double2*>(y1m + ((int64_t)l * n + r) * 8);
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) {
+        const double2 a = __ldcs(y1 + k2);
+        v[2 * k2] += a.x;
+        v[2 * k2 + 1] += a.y;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      Y[(int64_t)k * ylen + o] = v[k] + fma(scale, ynearm[(int64_t)k * n + r], shift * xcols[(int64_t)k * n + r]);
+  }
+}
+
 }  // namespace
 
 // Tiled stage-A schedule for the multi-RHS kernels (columns in tiles of <= kTileW).
@@ -752,6 +1018,64 @@ static void build_multi_schedule(Handle& h) {
     H2D_CUDA(cudaMemcpyAsync(h.m_aitems, items.data(), items.size() * sizeof(AItem), cudaMemcpyHostToDevice, s));
   if (!ritems.empty())
     H2D_CUDA(cudaMemcpyAsync(h.m_ritems, ritems.data(), ritems.size() * sizeof(RItem), cudaMemcpyHostToDevice, s));
+  if (h.symapply) {
+    // symmetric B' for 8 vectors: whole first-side U box panels (R <= kTileW, else the
+    // symmetric handle keeps one vector at a time) in row chunks of <= target elements
+    std::vector<AItem> bitems;
+    std::vector<RItem> britems;
+    int64_t bp_len = 0, upos = 0;
+    bool ok = true;
+    for (int l = 1; l <= h.kappa && ok; ++l) {
+      const Level& L = h.levels[(size_t)l];
+      for (int64_t X = 0; X < L.nbox; ++X) {
+        const int R = L.ubR[(size_t)X], Rp = (R + 1) & ~1;
+        if (R > kTileW) { ok = false; break; }
+        const int64_t x0 = h.box_begin(l, X), nX = h.box_end(l, X) - x0;
+        if (R > 0 && nX > 0) {
+          const int64_t t1o = L.t1_base + L.t1base[(size_t)X];
+          int64_t nch = std::max<int64_t>(1, (nX * Rp + target - 1) / target);
+          nch = std::min<int64_t>(nX, nch);
+          const int64_t rows = (nX + nch - 1) / nch;
+          nch = (nX + rows - 1) / rows;
+          if (nch == 1) {
+            bitems.push_back(AItem{L.ub_off[(size_t)X], x0, (int32_t)nX, R, (int32_t)upos, l, -1, Rp, t1o});
+          } else {
+            if (bp_len + nch * R > INT32_MAX / kMaxNR) throw Error{H2D_EINVAL, "multi partial buffer too large"};
+            britems.push_back(RItem{(int32_t)upos, (int32_t)bp_len, R, (int32_t)nch});
+            for (int64_t c = 0; c < nch; ++c) {
+              const int64_t r0 = c * rows, nr = std::min(rows, nX - r0);
+              bitems.push_back(AItem{L.ub_off[(size_t)X] + r0 * Rp, x0 + r0, (int32_t)nr, R,
+                                     (int32_t)(-(bp_len + c * R) - 1), l, (int32_t)(britems.size() - 1), Rp, t1o});
+            }
+            bp_len += nch * R;
+          }
+        }
+        upos += R;
+      }
+    }
+    h.m_sym_ok = ok;
+    if (ok) {
+      std::stable_sort(bitems.begin(), bitems.end(), [](const AItem& a, const AItem& b) {
+        return (int64_t)a.nrows * a.R > (int64_t)b.nrows * b.R;
+      });
+      h.m_n_b1items = (int64_t)bitems.size();
+      h.m_b1items = h.alloc<AItem>(bitems.size());
+      h.m_b1ritems = h.alloc<RItem>(britems.size());
+      h.m_b1rcount = h.alloc<int32_t>(britems.size());
+      h.m_b1tpart = h.alloc<double>((size_t)std::max<int64_t>(1, bp_len) * kMaxNR);
+      h.m_t1 = h.alloc<double>((size_t)std::max<int64_t>(1, h.t1_len) * kMaxNR + 16);   // + tile over-read
+      h.m_y1 = h.alloc<double>((size_t)h.kappa * h.n * kMaxNR);
+      // rows without a first-side panel at a level are never written: zero once
+      H2D_CUDA(cudaMemsetAsync(h.m_y1, 0, (size_t)h.kappa * h.n * kMaxNR * sizeof(double), s));
+      H2D_CUDA(cudaMemsetAsync(h.m_t1, 0, ((size_t)std::max<int64_t>(1, h.t1_len) * kMaxNR + 16) * sizeof(double), s));
+      H2D_CUDA(cudaMemsetAsync(h.m_b1rcount, 0, std::max<size_t>(1, britems.size()) * 4, s));
+      if (!bitems.empty())
+        H2D_CUDA(cudaMemcpyAsync(h.m_b1items, bitems.data(), bitems.size() * sizeof(AItem), cudaMemcpyHostToDevice, s));
+      if (!britems.empty())
+        H2D_CUDA(cudaMemcpyAsync(h.m_b1ritems, britems.data(), britems.size() * sizeof(RItem), cudaMemcpyHostToDevice,
+                                 s));
+    }
+  }
   const int64_t served = h.row_end - h.row_begin;
   h.m_xm = h.alloc<double>((size_t)h.n * kMaxNR);
   h.m_xcols = h.alloc<double>((size_t)h.n * kMaxNR);
@@ -834,6 +1158,72 @@ static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, i
   }
 }
 
+// Symmetric apply, 8 vectors: A' (stage A multi over the first-side V box panels -> T1),
+// B' (T2 = U^T X and Y1 = U T1 over the first-side U box panels), C' (stage B multi over
+// the second-side leaf panels with T2), P2P, combine with the kappa Y1 rows.
+static void multi_chunk_sym(Handle& h, const double* dX, int64_t xlen, double* dY, int64_t ylen, int order) {
+  constexpr int NR = 8;
+  set_multi_attrs<NR, kNSMulti, kSDMulti, kSVMulti>();
+  static bool dual_set = false;
+  const size_t smem = sizeof(PipeSmem<kNSMulti, kSDMulti, kSVMulti>);
+  if (!dual_set) {
+    H2D_CUDA(cudaFuncSetAttribute(stageA_dual_multi_kernel<kNSMulti, kSDMulti, kSVMulti>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    H2D_CUDA(cudaFuncSetAttribute(stageA_dual_multi_kernel<kNSMulti, kSDMulti, kSVMulti>,
+                                  cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    dual_set = true;
+  }
+  cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
+  const int grid = (int)std::min<int64_t>((h.n + 255) / 256, 148 * 16);
+  permute_multi_kernel<<<grid, 256, 0, s>>>(NR, dX, xlen, order == H2D_ORDER_ORIGINAL ? h.d_perm : nullptr, h.n,
+                                            h.m_xm, h.m_xcols);
+  H2D_LAUNCH_CHECK();
+  H2D_CUDA(cudaEventRecord(h.ev_fork, s));
+  H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_fork, 0));
+  H2D_CUDA(cudaStreamWaitEvent(a, h.ev_fork, 0));
+  H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 4 * sizeof(int32_t), hi));
+  if (h.m_n_aitems > 0) {
+    stageA_multi_kernel<kNSMulti, NR, kSDMulti, kSVMulti><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+        h.m_aitems, (int)h.m_n_aitems, h.d_counters, h.lp, h.m_xm, h.d_vdst, h.m_t1, h.m_tpart, h.m_ritems,
+        h.m_rcount);
+    H2D_LAUNCH_CHECK();
+  }
+  if (h.m_n_b1items > 0) {
+    stageA_dual_multi_kernel<kNSMulti, kSDMulti, kSVMulti><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+        h.m_b1items, (int)h.m_n_b1items, h.d_counters + 3, h.lp, h.m_xm, h.d_udst, h.m_t, h.m_b1tpart,
+        h.m_b1ritems, h.m_b1rcount, h.m_t1, h.m_y1, h.n);
+    H2D_LAUNCH_CHECK();
+  }
+  if (h.n_bitems > 0) {
+    TmPtrs tml{};
+    for (int l = 1; l <= h.kappa; ++l) tml.p[l] = h.m_t + h.levels[(size_t)l].tu_base * NR;
+    stageB_multi_kernel<kNSMulti, NR, kSDMulti, kSVMulti><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+        h.d_bitems, h.d_blev, (int)h.n_bitems, h.d_counters + 1, h.kappa, h.lp, tml, h.m_yfar);
+    H2D_LAUNCH_CHECK();
+  }
+  H2D_CUDA(cudaEventRecord(h.ev_far, hi));
+  switch (h.kp.id) {
+    case H2D_KERNEL_LOG: launch_p2p_multi<H2D_KERNEL_LOG, NR>(h, a); break;
+    case H2D_KERNEL_IMQ: launch_p2p_multi<H2D_KERNEL_IMQ, NR>(h, a); break;
+    case H2D_KERNEL_ONE_OVER_R: launch_p2p_multi<H2D_KERNEL_ONE_OVER_R, NR>(h, a); break;
+    case H2D_KERNEL_RBF_PHI1: launch_p2p_multi<H2D_KERNEL_RBF_PHI1, NR>(h, a); break;
+    case H2D_KERNEL_RBF_PHI2: launch_p2p_multi<H2D_KERNEL_RBF_PHI2, NR>(h, a); break;
+    default: launch_p2p_multi<H2D_KERNEL_TEST_LOWRANK, NR>(h, a); break;
+  }
+  H2D_CUDA(cudaEventRecord(h.ev_join, a));
+  H2D_CUDA(cudaStreamWaitEvent(s, h.ev_far, 0));
+  H2D_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));
+  const int64_t rows = h.row_end - h.row_begin;   // symmetric apply: single-rank handles
+  if (rows > 0) {
+    const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 148 * 8);
+    combine_multi_sym_kernel<<<blocks, 256, 0, s>>>(rows, h.kappa, h.m_yfar, h.m_y1, h.m_ynear, h.n, h.m_xcols,
+                                                    h.kp.scale, h.kp.shift, dY, ylen, h.d_perm,
+                                                    order == H2D_ORDER_ORIGINAL ? H2D_ORDER_ORIGINAL : H2D_ORDER_TREE,
+                                                    h.row_begin);
+    H2D_LAUNCH_CHECK();
+  }
+}
+
 // Y = A X for nrhs vectors (device pointers; vector k at X + k * xlen, Y + k * ylen).
 void matvec_multi(Handle& h, const double* dX, double* dY, int nrhs, int order) {
   if (order != H2D_ORDER_ORIGINAL && order != H2D_ORDER_TREE)
@@ -842,9 +1232,14 @@ void matvec_multi(Handle& h, const double* dX, double* dY, int nrhs, int order) 
   if (order == H2D_ORDER_ORIGINAL && part)
     throw Error{H2D_EINVAL, "ORIGINAL order needs a single-rank (full-range) handle"};
   if (h.symapply) {
-    // the symmetric apply keeps no directed panels: one vector at a time
+    // the symmetric apply keeps no directed panels: chunks of 8 through A' / B' / C' multi
+    // (when every first-side panel fits one tile), the rest one vector at a time
+    if (!h.multi_ready) build_multi_schedule(h);
     const int64_t ylen1 = order == H2D_ORDER_ORIGINAL ? h.n : h.row_end - h.row_begin;
-    for (int k = 0; k < nrhs; ++k) {
+    int k0 = 0;
+    if (h.m_sym_ok)
+      for (; k0 + 8 <= nrhs; k0 += 8) multi_chunk_sym(h, dX + (int64_t)k0 * h.n, h.n, dY + (int64_t)k0 * ylen1, ylen1, order);
+    for (int k = k0; k < nrhs; ++k) {
       const double* X = dX + (int64_t)k * h.n;
       double* Y = dY + (int64_t)k * ylen1;
       if (order == H2D_ORDER_ORIGINAL) {

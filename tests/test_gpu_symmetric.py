@@ -183,3 +183,49 @@ def test_symmetric_apply_cases(h2d, case):
     kid = {"log": 0, "imq": 1, "rbf_phi1": 3}[kernel]
     yd = oracle.dense_matvec(pts, x, kid, kw.get("c", 1.0), 1.0, kw.get("shift", 0.0))
     assert rel(y, yd) <= 1e-8
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+@pytest.mark.parametrize("nrhs", [8, 11, 16])
+def test_symmetric_multi_rhs(h2d, name, nrhs):
+    """Symmetric handles run 8-vector chunks through A' / B' / C' multi (DMMA B' fusing
+    T2 = U^T X with Y1 = U T1) and the remainder one vector at a time: every column equals
+    its single-vector matvec to 1e-13, in ORIGINAL and TREE order."""
+    cfg = W.CONFIGS[name]
+    pts = W.config_points(cfg)
+    op = build(h2d, cfg, pts)
+    X = np.stack([W.config_x(cfg, k) for k in range(nrhs)])
+    Y = op.matvec_multi(dev(X)).cpu().numpy()
+    for k in range(nrhs):
+        assert rel(Y[k], op.matvec(dev(X[k])).cpu().numpy()) <= 1e-13, k
+    perm, _ = op.tree()
+    Xt = np.ascontiguousarray(X[:, perm])
+    Yt = op.matvec_multi(dev(Xt), order="tree").cpu().numpy()
+    assert rel(Yt, Y[:, perm]) <= 1e-13
+
+
+def test_symmetric_multi_rhs_oracle_factors(h2d, tmp_path):
+    cfg = W.CONFIGS["c1"]
+    pts = W.config_points(cfg)
+    orc = oracle.Operator(pts, cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c, scale=cfg.scale, shift=cfg.shift,
+                          box_lo=cfg.box_lo, box_side=cfg.box_side, symmetric=True)
+    path = str(tmp_path / "f.bin")
+    orc.save_factors(path)
+    op = build(h2d, cfg, pts)
+    op.load_factors(path)
+    X = np.stack([W.config_x(cfg, k) for k in range(8)])
+    Y = op.matvec_multi(dev(X)).cpu().numpy()
+    for k in range(8):
+        assert rel(Y[k], orc.matvec(X[k])) <= 1e-12, k
+
+
+def test_symmetric_multi_rhs_wide_panels_fallback(h2d):
+    """First-side panels wider than one 448-column tile (IMQ c = 0.05, 256-point leaves,
+    tol 1e-13): the handle keeps one vector at a time; results still equal."""
+    n = 1 << 14
+    pts = W.uniform_points(n, 4343)
+    op = h2d.Hodlr2d.build(dev(pts), "imq", 256, 1e-13, c=0.05, box_lo=(-1, -1), box_side=2.0, symmetric=True)
+    X = np.stack([W.random_vector(n, 950 + k) for k in range(8)])
+    Y = op.matvec_multi(dev(X)).cpu().numpy()
+    for k in range(8):
+        assert np.array_equal(Y[k], op.matvec(dev(X[k])).cpu().numpy())

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Build C3 and run hodlr2d_matvec_multi (nrhs vectors) a few times: a target for ncu.
 
-    ncu --metrics gpu__time_duration.sum -k regex:multi python tools/multi_probe.py 8
+    ncu --metrics gpu__time_duration.sum -k regex:multi python tools/multi_probe.py 8 [c3 [sym]]
 """
 import os
 import sys
@@ -17,9 +17,10 @@ import workloads as W  # noqa: E402
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 cfg = W.CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "c3"]
+sym = len(sys.argv) > 3 and sys.argv[3] == "sym"
 pts = W.config_points(cfg)
 op = h2d.Hodlr2d.build(torch.from_numpy(pts).cuda(), cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c,
-                       scale=cfg.scale, shift=cfg.shift, box_lo=cfg.box_lo, box_side=cfg.box_side)
+                       scale=cfg.scale, shift=cfg.shift, box_lo=cfg.box_lo, box_side=cfg.box_side, symmetric=sym)
 X = torch.from_numpy(np.stack([W.config_x(cfg, k) for k in range(K)])).cuda()
 Y = torch.empty_like(X)
 for _ in range(3):
