@@ -246,6 +246,19 @@ def test_edge_cases(h2d):
     op = h2d.Hodlr2d.build(dev(pts), "log", 64, 1e-9, box_lo=(-1, -1), box_side=2.0, depth=6)
     assert op.info()["kappa"] == 6
     assert rel(gpu_matvec(op, x), oracle.dense_matvec(pts, x)) <= 1e-8
+    # degenerate geometries: every point identical (all pairs at r = 0, one occupied leaf
+    # per level), and points on a line (most boxes empty; warp P2P and small-item paths)
+    same = np.tile(np.array([[0.25, -0.5]]), (700, 1))
+    xs = W.random_vector(700, 4)
+    for kernel, kid in (("log", 0), ("imq", 1)):
+        op = h2d.Hodlr2d.build(dev(same), kernel, 16, 1e-10, c=0.3, shift=1.5, box_lo=(-1, -1), box_side=2.0,
+                               depth=4)
+        assert rel(gpu_matvec(op, xs), oracle.dense_matvec(same, xs, kid, 0.3, 1.0, 1.5)) <= 1e-13
+    t = np.linspace(-0.9, 0.9, 6000)
+    line = np.ascontiguousarray(np.stack([t, 0.3 * t + 0.1], axis=1))
+    xl = W.random_vector(6000, 5)
+    op = h2d.Hodlr2d.build(dev(line), "log", 8, 1e-10, box_lo=(-1, -1), box_side=2.0)
+    assert rel(gpu_matvec(op, xl), oracle.dense_matvec(line, xl)) <= 1e-9
     # errors
     with pytest.raises(h2d.Hodlr2dError) as e:
         h2d.Hodlr2d.build(dev(np.array([[0.0, 0.0], [3.0, 0.0]])), "log", 1, 1e-8, box_lo=(-1, -1), box_side=2.0)
