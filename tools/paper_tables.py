@@ -8,6 +8,7 @@ Prints one JSON line per (kernel, N)."""
 import json
 import os
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -43,5 +44,31 @@ for kernel in ("one_over_r", "rbf_phi1", "rbf_phi2"):
                 b = oracle.dense_rows(pts, x, rows, KID[kernel])
                 eps = max(eps, float(np.max(np.abs(y[rows] - b) / np.abs(b))))
             line["eps_r_sampled"] = eps
+        # matvec time (CUDA events, device pointers) and, for the RBF systems, the GMRES solve
+        # time T_G to residual 1e-10 (median of 3) — the paper's single-core times are context
+        x = torch.from_numpy(np.random.default_rng(7).uniform(0.0, 1.0, n)).cuda()
+        y = torch.empty_like(x)
+        for _ in range(3):
+            op.matvec_raw(x.data_ptr(), y.data_ptr(), h2d.ORDER_ORIGINAL)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            op.matvec_raw(x.data_ptr(), y.data_ptr(), h2d.ORDER_ORIGINAL)
+        e1.record()
+        torch.cuda.synchronize()
+        line["matvec_s"] = e0.elapsed_time(e1) / 20 / 1e3
+        if kernel != "one_over_r":
+            f = op.matvec(x)
+            op.gmres(f, tol=1e-10)
+            tg = []
+            for _ in range(3):
+                torch.cuda.synchronize()
+                t0 = time.time()
+                _, its, rr = op.gmres(f, tol=1e-10)
+                torch.cuda.synchronize()
+                tg.append(time.time() - t0)
+            line["T_G_s"] = float(np.median(tg))
+            line["gmres_iterations"] = its
         print(json.dumps(line), flush=True)
         op.close()
