@@ -1101,7 +1101,10 @@ void finalize_schedule(Handle& h) {
     if (!b1ritems.empty())
       H2D_CUDA(cudaMemcpyAsync(h.d_b1ritems, b1ritems.data(), b1ritems.size() * sizeof(RItem),
                                cudaMemcpyHostToDevice, s));
+    // entries of rows without a first-side panel at a level are never written by B': zeroed
+    // here, at every (re)schedule, not per matvec
     if (!h.d_y1) h.d_y1 = h.alloc<double>((size_t)h.kappa * h.n);
+    H2D_CUDA(cudaMemsetAsync(h.d_y1, 0, (size_t)h.kappa * h.n * sizeof(double), s));
   }
   // stage-B items: served leaves in row blocks of <= kBRows rows, largest cost first, with
   // the per-level metadata of each item precomputed (one dependent load in the producer)
@@ -1457,7 +1460,6 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
     // symmetric apply (R23): A' t1 = V^T x; B' t2 = U^T x and y1 = U t1; C' yfar = V t2
     const size_t smem = sizeof(PipeSmem<kNSShallow>);
     H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 4 * sizeof(int32_t), hi));
-    H2D_CUDA(cudaMemsetAsync(h.d_y1, 0, (size_t)h.kappa * h.n * sizeof(double), hi));
     launch_small(h, true, d_xtree, h.d_t1, hi);
     if (h.n_abig > 0) {
       stageA_tma_kernel<kNSShallow><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
