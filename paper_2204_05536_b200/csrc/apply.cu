@@ -413,28 +413,42 @@ __device__ __forceinline__ void tile_fast8(int mt, int nt, const double* __restr
     cxv[bb] = vj ? sb[2 * kSymTile + j] : 0.0;
     cacc[bb] = 0.0;
   }
-  for (int aa = 0; aa < A; ++aa) {
-    const int i = ti + 16 * aa;
-    const bool vi = i < mt;
-    const double rpx = vi ? sa[i] : 0.0, rpy = vi ? sa[kSymTile + i] : 0.0;
-    const double rx = vi ? sa[2 * kSymTile + i] : 0.0;
-    double racc = 0.0;
+  // two rows (i, i + 16) per pass: 2 B independent evaluations in flight per thread (the
+  // kernel runs at 8 warps per SM beside the streaming CTAs, so ILP is its latency cover)
+  for (int aa = 0; aa < A; aa += 2) {
+    const int i0 = ti + 16 * aa, i1 = i0 + 16;
+    const bool v0 = i0 < mt, v1 = i1 < mt && aa + 1 < A;
+    const double px0 = v0 ? sa[i0] : 0.0, py0 = v0 ? sa[kSymTile + i0] : 0.0, x0 = v0 ? sa[2 * kSymTile + i0] : 0.0;
+    const double px1 = v1 ? sa[i1] : 0.0, py1 = v1 ? sa[kSymTile + i1] : 0.0, x1 = v1 ? sa[2 * kSymTile + i1] : 0.0;
+    double r0 = 0.0, r1 = 0.0;
 #pragma unroll
     for (int bb = 0; bb < kSymMaxB; ++bb) {
       if (bb < B) {
-        const double dx = rpx - cpx[bb], dy = rpy - cpy[bb];
-        double k = kfast<KID>(fma(dx, dx, dy * dy), tab, kp);
-        if (DIAG) k = i < tj + 16 * bb ? k : 0.0;
-        racc = fma(k, cxv[bb], racc);
-        cacc[bb] = fma(k, rx, cacc[bb]);
+        const double dx0 = px0 - cpx[bb], dy0 = py0 - cpy[bb];
+        const double dx1 = px1 - cpx[bb], dy1 = py1 - cpy[bb];
+        double k0v = kfast<KID>(fma(dx0, dx0, dy0 * dy0), tab, kp);
+        double k1v = kfast<KID>(fma(dx1, dx1, dy1 * dy1), tab, kp);
+        if (DIAG) {
+          k0v = i0 < tj + 16 * bb ? k0v : 0.0;
+          k1v = i1 < tj + 16 * bb ? k1v : 0.0;
+        }
+        r0 = fma(k0v, cxv[bb], r0);
+        r1 = fma(k1v, cxv[bb], r1);
+        cacc[bb] = fma(k0v, x0, cacc[bb]);
+        cacc[bb] = fma(k1v, x1, cacc[bb]);
       }
     }
-    if (DIAG && tj == 0) racc = fma(k0, rx, racc);
-    racc += __shfl_xor_sync(0xffffffffu, racc, 8);
-    racc += __shfl_xor_sync(0xffffffffu, racc, 4);
-    racc += __shfl_xor_sync(0xffffffffu, racc, 2);
-    racc += __shfl_xor_sync(0xffffffffu, racc, 1);
-    if (tj == 0 && vi) srow[i] = racc;
+    if (DIAG && tj == 0) {
+      r0 = fma(k0, x0, r0);
+      r1 = fma(k0, x1, r1);
+    }
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) {
+      r0 += __shfl_xor_sync(0xffffffffu, r0, o);
+      r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+    }
+    if (tj == 0 && v0) srow[i0] = r0;
+    if (tj == 0 && v1) srow[i1] = r1;
   }
   const int w = tid >> 5;
 #pragma unroll
