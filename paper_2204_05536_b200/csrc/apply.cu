@@ -33,7 +33,7 @@ namespace {
 constexpr int64_t kATargetDefault = 1048576;  // stage-A elements per work item (8 MB)
 constexpr int kAMaxRows = 16384;     // rows per stage-A item
 constexpr int kBRows = 224;          // rows per stage-B item (leaf row block) <= kCons
-constexpr int kT1Max = kT1Smem;      // symmetric stage B': t1 values of one row box in smem
+constexpr int kT1Max = kT1Smem;      // symmetric stage B': widest first-side panel (its t1 rides in the slot)
 // stage B' ring: 2 x 44 KB slots.  The fused column-sum + row-dot pass is issue-bound, not
 // latency-bound (the second CTA on the SM hides the copy latency), so fewer, larger stages
 // win by amortising the per-stage overhead: A'+B' 2.20 ms (5 x 16 KB) -> 1.76 ms (C3).

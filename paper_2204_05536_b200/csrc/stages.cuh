@@ -1,6 +1,10 @@
-// The two factor-streaming stages of the matvec (shared by apply.cu and symapply.cu):
+// The factor-streaming stages of the single-vector matvec (apply.cu):
 //   stage A  t = V^T x  over row-major V box panels (persistent, bulk-TMA ring)
-//   stage B  yfar = U t over column-major U leaf panels (persistent, bulk-TMA ring)
+//   stage B' the symmetric apply's fused pass: t2 = U^T x and y1 = U t1 over the first-side
+//            U box panels (stage A's ring with the row dots added, DUAL)
+//   stage B  yfar = U t over column-major U leaf panels (persistent, bulk-TMA ring; several
+//            levels of a leaf per stage)
+//   small-item kernels: warp per box / leaf for items too small for the ring
 #pragma once
 #include "pipe.cuh"
 
