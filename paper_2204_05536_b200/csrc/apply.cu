@@ -1363,15 +1363,14 @@ void mark_after_input(Handle& h) { record(h, 1, h.stream); }
 
 template <int NS, int SD, int SV>
 static void launch_stageB_geom(Handle& h, cudaStream_t hi) {
-  static bool set = false;
+  static uint64_t seen = 0;
   const size_t smem = sizeof(PipeSmem<NS, SD, SV>);
-  if (!set) {
+  once_per_device(seen, [&] {
     H2D_CUDA(cudaFuncSetAttribute(stageB_tma_kernel<NS, SD, SV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     H2D_CUDA(cudaFuncSetAttribute(stageB_tma_kernel<NS, SD, SV>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));
-    set = true;
-  }
+  });
   stageB_tma_kernel<NS, SD, SV><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
       h.d_bitems, h.d_blev, (int)h.n_bbig, h.d_counters + 1, h.kappa, h.lp, h.d_yfar);
   H2D_LAUNCH_CHECK();

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -175,6 +176,22 @@ struct RItem {
   int32_t R;
   int32_t nchunks;
 };
+
+// Run f() once per (call site, current device): kernel function attributes (dynamic smem
+// size, carve-out) belong to a device's context, so a process driving several GPUs must set
+// them on each.  `seen` is the call site's device bitmask; the mutex also orders a second
+// thread after the first one's attribute calls.
+template <typename F>
+inline void once_per_device(uint64_t& seen, F&& f) {
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  std::lock_guard<std::mutex> lock(mu);
+  if (seen & bit) return;
+  f();
+  seen |= bit;
+}
 
 struct LevelPtrs {
   const double* U[H2D_MAX_LEVELS + 1];

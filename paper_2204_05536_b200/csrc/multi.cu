@@ -1088,16 +1088,16 @@ static void build_multi_schedule(Handle& h) {
 
 template <int NR, int NS, int SD, int SV>
 static void set_multi_attrs() {
-  static bool done = false;   // per instantiation, per process (attributes are per function)
-  if (done) return;
-  const int smem = (int)sizeof(PipeSmem<NS, SD, SV>);
-  H2D_CUDA(cudaFuncSetAttribute(stageA_multi_kernel<NS, NR, SD, SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  H2D_CUDA(cudaFuncSetAttribute(stageB_multi_kernel<NS, NR, SD, SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  H2D_CUDA(cudaFuncSetAttribute(stageA_multi_kernel<NS, NR, SD, SV>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                cudaSharedmemCarveoutMaxShared));
-  H2D_CUDA(cudaFuncSetAttribute(stageB_multi_kernel<NS, NR, SD, SV>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                cudaSharedmemCarveoutMaxShared));
-  done = true;
+  static uint64_t seen = 0;   // per instantiation and device (attributes live in the device's context)
+  once_per_device(seen, [] {
+    const int smem = (int)sizeof(PipeSmem<NS, SD, SV>);
+    H2D_CUDA(cudaFuncSetAttribute(stageA_multi_kernel<NS, NR, SD, SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    H2D_CUDA(cudaFuncSetAttribute(stageB_multi_kernel<NS, NR, SD, SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    H2D_CUDA(cudaFuncSetAttribute(stageA_multi_kernel<NS, NR, SD, SV>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+    H2D_CUDA(cudaFuncSetAttribute(stageB_multi_kernel<NS, NR, SD, SV>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+  });
 }
 
 template <int KID, int NR>
@@ -1164,15 +1164,14 @@ static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, i
 static void multi_chunk_sym(Handle& h, const double* dX, int64_t xlen, double* dY, int64_t ylen, int order) {
   constexpr int NR = 8;
   set_multi_attrs<NR, kNSMulti, kSDMulti, kSVMulti>();
-  static bool dual_set = false;
+  static uint64_t dual_seen = 0;
   const size_t smem = sizeof(PipeSmem<kNSMulti, kSDMulti, kSVMulti>);
-  if (!dual_set) {
+  once_per_device(dual_seen, [&] {
     H2D_CUDA(cudaFuncSetAttribute(stageA_dual_multi_kernel<kNSMulti, kSDMulti, kSVMulti>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     H2D_CUDA(cudaFuncSetAttribute(stageA_dual_multi_kernel<kNSMulti, kSDMulti, kSVMulti>,
                                   cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
-    dual_set = true;
-  }
+  });
   cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
   const int grid = (int)std::min<int64_t>((h.n + 255) / 256, 148 * 16);
   permute_multi_kernel<<<grid, 256, 0, s>>>(NR, dX, xlen, order == H2D_ORDER_ORIGINAL ? h.d_perm : nullptr, h.n,
