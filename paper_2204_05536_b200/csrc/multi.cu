@@ -346,7 +346,25 @@ __device__ void mA_consumers_dmma(PipeSmem<NS, SD, SV>& S, const int32_t* __rest
 // m-tiles, the configs' case) split K over the 7 warps (every warp all m-tiles, K steps
 // 4w, 4w + 28, ...) and reduce the 7 partials per m-tile in smem at the end of the item;
 // taller row blocks give m-tile i to warp i % 7.
-constexpr int kMaxMTK = 8;
+constexpr int kMaxMTK = 12;
+// Stage-B DMMA k-split for CNT m-tiles (the leaf's rows / 8): warp w takes k-steps 4 w,
+// 4 w + 28, ... over all m-tiles; only the last m-tile can run past the leaf's rows.
+template <int CNT, int KD>
+__device__ __forceinline__ void bsplit_mtiles(double (&d)[KD][2], const double* __restrict__ su,
+                                              const double* __restrict__ tv, int cols, int rowsp, int w, int gq,
+                                              int tq) {
+  const bool last_ok = (CNT - 1) * 8 + gq < rowsp;
+  for (int k0 = 4 * w; k0 < cols; k0 += 4 * kConsWarps) {
+    const int c = k0 + tq;
+    const bool cv = c < cols;
+    const double b = cv ? tv[c * 8 + gq] : 0.0;
+    const double* __restrict__ col = su + c * rowsp + gq;
+#pragma unroll
+    for (int i = 0; i < CNT - 1; ++i) dmma884(d[i][0], d[i][1], cv ? col[i * 8] : 0.0, b);
+    dmma884(d[CNT - 1][0], d[CNT - 1][1], (cv && last_ok) ? col[(CNT - 1) * 8] : 0.0, b);
+  }
+}
+
 template <int NS, int SD, int SV>
 __device__ void mB_consumers_dmma(PipeSmem<NS, SD, SV>& S, double* __restrict__ yfarm) {
   constexpr int NR = 8;
@@ -376,19 +394,19 @@ __device__ void mB_consumers_dmma(PipeSmem<NS, SD, SV>& S, double* __restrict__ 
     const double* __restrict__ tv = S.vec[stage];
     const int cols = h.cnt;
     if (ksplit) {
-      for (int k0 = 4 * w; k0 < cols; k0 += 4 * kConsWarps) {
-        const int c = k0 + tq;
-        const bool cv = c < cols;
-        const double b = cv ? tv[c * NR + gq] : 0.0;
-        const double* __restrict__ col = su + c * rowsp + gq;
-#pragma unroll
-        for (int i = 0; i < kMaxMTK; ++i) {
-          if (i < MT) {
-            const int r = i * 8 + gq;
-            const double a = (cv && r < rowsp) ? col[i * 8] : 0.0;
-            dmma884(d[i][0], d[i][1], a, b);
-          }
-        }
+      switch (MT) {   // exact m-tile count: no per-slot predicates
+        case 1: bsplit_mtiles<1>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 2: bsplit_mtiles<2>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 3: bsplit_mtiles<3>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 4: bsplit_mtiles<4>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 5: bsplit_mtiles<5>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 6: bsplit_mtiles<6>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 7: bsplit_mtiles<7>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 8: bsplit_mtiles<8>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 9: bsplit_mtiles<9>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 10: bsplit_mtiles<10>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 11: bsplit_mtiles<11>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        default: bsplit_mtiles<kMaxMTK>(d, su, tv, cols, rowsp, w, gq, tq); break;
       }
     } else {
       for (int k0 = 0; k0 < cols; k0 += 4) {
