@@ -132,8 +132,10 @@ static void clear_factors(Handle& h) {
   h.m_xm = h.m_xcols = h.m_t = h.m_yfar = h.m_ynear = nullptr;
   h.m_n_aitems = 0;
   for (void* q : {(void*)h.m_b1items, (void*)h.m_b1ritems, (void*)h.m_b1rcount, (void*)h.m_b1tpart, (void*)h.m_t1,
-                  (void*)h.m_y1})
+                  (void*)h.m_y1, (void*)h.m16_aitems, (void*)h.m16_ritems, (void*)h.m16_rcount, (void*)h.m16_tpart})
     h.release(q);
+  h.m16_aitems = nullptr; h.m16_ritems = nullptr; h.m16_rcount = nullptr; h.m16_tpart = nullptr;
+  h.m16_n_aitems = 0;
   h.m_b1items = nullptr; h.m_b1ritems = nullptr; h.m_b1rcount = nullptr;
   h.m_b1tpart = h.m_t1 = h.m_y1 = nullptr;
   h.m_n_b1items = 0;

@@ -278,6 +278,12 @@ struct Handle {
   int32_t* m_rcount = nullptr;
   double *m_tpart = nullptr, *m_xm = nullptr, *m_xcols = nullptr, *m_t = nullptr;
   double *m_yfar = nullptr, *m_ynear = nullptr;
+  // 16-vector chunks: stage-A tiles of <= 224 columns (their own schedule)
+  AItem* m16_aitems = nullptr;
+  int64_t m16_n_aitems = 0;
+  RItem* m16_ritems = nullptr;
+  int32_t* m16_rcount = nullptr;
+  double* m16_tpart = nullptr;
   // symmetric multi-RHS (8-vector chunks): B' items over the U box panels, T1 / Y1
   bool m_sym_ok = false;
   AItem* m_b1items = nullptr;

@@ -23,9 +23,12 @@ namespace h2d {
 namespace {
 
 constexpr int kTileW = 2 * kCons;    // stage-A column tile (<= kCons pairs)
-constexpr int kMaxNR = 8;            // vectors per chunk
+constexpr int kMaxNR = 16;           // vectors per chunk (16: two 8-vector DMMA groups)
+constexpr int kTileW16 = kCons;      // stage-A column tile for 16 vectors (<= 4 m-tiles per warp)
+constexpr int kSymNR = 8;            // symmetric handles: 8-vector chunks
 constexpr int kBRowsMax = 224;       // stage-B item rows (apply.cu kBRows)
 constexpr int kNSMulti = 2, kSDMulti = 5632, kSVMulti = 704;   // ring: stages, doubles, vector values
+constexpr int kSDMulti16 = 4096, kSVMulti16 = 1024;              // 16 vectors: 64 rows x 64 columns
 
 // ---------------------------------------------------------------- stage A (multi)
 // Stage header: a = W (tile width), b = Wp (row stride of the stage, W rounded up to even),
@@ -459,6 +462,261 @@ __device__ void mB_consumers_dmma(PipeSmem<NS, SD, SV>& S, double* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------- 16 vectors per chunk
+// Two 8-vector groups share every A fragment (factor values loaded once from smem, one DMMA
+// per group).  Registers (80 at 3 CTAs/SM) bound the m-tiles a warp accumulates: stage-A
+// tiles of <= kTileW16 columns (<= 4 m-tiles per warp), stage-B k-split up to 6 m-tiles.
+constexpr int kMaxMTA16 = (kTileW16 / 8 + kConsWarps - 1) / kConsWarps;
+constexpr int kMaxMTK16 = 6;   // (8: 80-register cap spills, 4.39 vs 3.32 ms)
+
+template <int CNT>
+__device__ __forceinline__ void colsum16_mtiles(double (&d)[kMaxMTA16][2][2], const double* __restrict__ sv,
+                                                const double* __restrict__ sx, int rows, int Wp, int w, int gq,
+                                                int tq) {
+  int cidx[CNT];
+#pragma unroll
+  for (int i = 0; i < CNT; ++i) cidx[i] = (w + kConsWarps * i) * 8 + gq;
+  int k0 = 0;
+  for (; k0 + 4 <= rows; k0 += 4) {
+    const int r = k0 + tq;
+    const double b0 = sx[r * 16 + gq], b1 = sx[r * 16 + 8 + gq];
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) {
+      const double a = cidx[i] < Wp ? sv[r * Wp + cidx[i]] : 0.0;
+      dmma884(d[i][0][0], d[i][0][1], a, b0);
+      dmma884(d[i][1][0], d[i][1][1], a, b1);
+    }
+  }
+  if (k0 < rows) {
+    const int r = k0 + tq;
+    const bool rv = r < rows;
+    const double b0 = rv ? sx[r * 16 + gq] : 0.0, b1 = rv ? sx[r * 16 + 8 + gq] : 0.0;
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) {
+      const double a = (rv && cidx[i] < Wp) ? sv[r * Wp + cidx[i]] : 0.0;
+      dmma884(d[i][0][0], d[i][0][1], a, b0);
+      dmma884(d[i][1][0], d[i][1][1], a, b1);
+    }
+  }
+}
+
+template <int NS, int SD, int SV>
+__device__ void mA16_consumers(PipeSmem<NS, SD, SV>& S, const int32_t* __restrict__ vdst, double* __restrict__ tm,
+                               double* __restrict__ tpartm, const RItem* __restrict__ ritems,
+                               int32_t* __restrict__ rcount) {
+  constexpr int NR = 16;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  int stage = 0;
+  uint32_t phase = 0;
+  int W = 1, Wp = 2, MT = 1;
+  double d[kMaxMTA16][2][2];
+#pragma unroll
+  for (int i = 0; i < kMaxMTA16; ++i) d[i][0][0] = d[i][0][1] = d[i][1][0] = d[i][1][1] = 0.0;
+  for (;;) {
+    mbar_wait(&S.full[stage], phase);
+    const StageHdr h = S.hdr[stage];
+    if (h.item < 0) break;
+    if (h.flags & kFirst) {
+      W = h.a;
+      Wp = h.b;
+      MT = (W + 7) >> 3;
+#pragma unroll
+      for (int i = 0; i < kMaxMTA16; ++i) d[i][0][0] = d[i][0][1] = d[i][1][0] = d[i][1][1] = 0.0;
+    }
+    const double* __restrict__ sv = S.ring[stage];
+    const double* __restrict__ sx = S.vec[stage];
+    const int cnt = MT > w ? (MT - w + kConsWarps - 1) / kConsWarps : 0;
+    switch (cnt) {
+      case 0: break;
+      case 1: colsum16_mtiles<1>(d, sv, sx, h.cnt, Wp, w, gq, tq); break;
+      case 2: colsum16_mtiles<2>(d, sv, sx, h.cnt, Wp, w, gq, tq); break;
+      case 3: colsum16_mtiles<3>(d, sv, sx, h.cnt, Wp, w, gq, tq); break;
+      default: colsum16_mtiles<kMaxMTA16>(d, sv, sx, h.cnt, Wp, w, gq, tq); break;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[stage]);
+    if (++stage == NS) { stage = 0; phase ^= 1; }
+    if (!(h.flags & kLast)) continue;
+#pragma unroll
+    for (int i = 0; i < kMaxMTA16; ++i) {
+      const int mt = w + kConsWarps * i;
+      const int q = mt * 8 + gq;
+      if (mt < MT && q < W) {
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int k = 8 * g + 2 * tq + e;
+            if (h.c >= 0) tm[(int64_t)vdst[h.c + q] * NR + k] = d[i][g][e];
+            else tpartm[((int64_t)(-h.c - 1) + q) * NR + k] = d[i][g][e];
+          }
+      }
+    }
+    if (h.d >= 0) {
+      named_bar_sync(1, kCons);
+      if (tid == 0) {
+        __threadfence();
+        const int last = atomicAdd(rcount + h.d, 1) == ritems[h.d].nchunks - 1;
+        if (last) __threadfence();
+        S.flag = last;
+      }
+      named_bar_sync(1, kCons);
+      if (S.flag) {
+        const RItem ri = ritems[h.d];
+        for (int e = tid; e < ri.R * NR; e += kCons) {
+          const int q = e / NR, k = e - q * NR;
+          const double* __restrict__ pp = tpartm + ((int64_t)ri.p_off + q) * NR + k;
+          const int64_t cs = (int64_t)ri.R * NR;
+          double a0 = 0.0, a1 = 0.0;
+          int c = 0;
+          for (; c + 1 < ri.nchunks; c += 2) {
+            a0 += __ldcg(pp + c * cs);
+            a1 += __ldcg(pp + (c + 1) * cs);
+          }
+          if (c < ri.nchunks) a0 += __ldcg(pp + c * cs);
+          tm[(int64_t)vdst[ri.vpos + q] * NR + k] = a0 + a1;
+        }
+        if (tid == 0) rcount[h.d] = 0;
+      }
+    }
+  }
+}
+
+constexpr int kAcc16 = 4 * 6;   // flat accumulators of the 16-vector stage B (both mappings)
+template <int CNT>
+__device__ __forceinline__ void bsplit16_mtiles(double (&d)[kAcc16], const double* __restrict__ su,
+                                                const double* __restrict__ tv, int cols, int rowsp, int w, int gq,
+                                                int tq) {
+  const bool last_ok = (CNT - 1) * 8 + gq < rowsp;
+  for (int k0 = 4 * w; k0 < cols; k0 += 4 * kConsWarps) {
+    const int c = k0 + tq;
+    const bool cv = c < cols;
+    const double b0 = cv ? tv[c * 16 + gq] : 0.0, b1 = cv ? tv[c * 16 + 8 + gq] : 0.0;
+    const double* __restrict__ col = su + c * rowsp + gq;
+#pragma unroll
+    for (int i = 0; i < CNT; ++i) {
+      const double a = (cv && (i < CNT - 1 || last_ok)) ? col[i * 8] : 0.0;
+      dmma884(d[4 * i], d[4 * i + 1], a, b0);
+      dmma884(d[4 * i + 2], d[4 * i + 3], a, b1);
+    }
+  }
+}
+
+// Taller leaves (> 6 m-tiles): m-tile i of warp w is w + 7 i (both vector groups, one A
+// load for two DMMAs), each warp over all k-steps of the stage, exact per-warp count.
+template <int CNT>
+__device__ __forceinline__ void bmt16(double (&d)[kAcc16], const double* __restrict__ su,
+                                      const double* __restrict__ tv, int cols, int rowsp, int w, int gq, int tq) {
+  int roff[CNT];
+  bool rok[CNT];
+#pragma unroll
+  for (int j = 0; j < CNT; ++j) {
+    roff[j] = (w + kConsWarps * j) * 8 + gq;
+    rok[j] = roff[j] < rowsp;
+  }
+  for (int k0 = 0; k0 < cols; k0 += 4) {
+    const int c = k0 + tq;
+    const bool cv = c < cols;
+    const double b0 = cv ? tv[c * 16 + gq] : 0.0, b1 = cv ? tv[c * 16 + 8 + gq] : 0.0;
+    const double* __restrict__ col = su + c * rowsp;
+#pragma unroll
+    for (int j = 0; j < CNT; ++j) {
+      const double a = (cv && rok[j]) ? col[roff[j]] : 0.0;
+      dmma884(d[4 * j], d[4 * j + 1], a, b0);
+      dmma884(d[4 * j + 2], d[4 * j + 3], a, b1);
+    }
+  }
+}
+
+template <int NS, int SD, int SV>
+__device__ void mB16_consumers(PipeSmem<NS, SD, SV>& S, double* __restrict__ yfarm) {
+  constexpr int NR = 16;
+  static_assert(4 * kMaxMTK16 <= kAcc16 && 4 * kMaxMTB <= kAcc16, "accumulator size");
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  int stage = 0;
+  uint32_t phase = 0;
+  int rows = 1, rowsp = 2, MT = 1;
+  bool ksplit = true;
+  double d[kAcc16];   // m-tile i, vector group g: d[4 i + 2 g + (0, 1)]
+#pragma unroll
+  for (int i = 0; i < kAcc16; ++i) d[i] = 0.0;
+  for (;;) {
+    mbar_wait(&S.full[stage], phase);
+    const StageHdr h = S.hdr[stage];
+    if (h.item < 0) break;
+    if (h.flags & kFirst) {
+      rows = h.a;
+      rowsp = h.b;
+      MT = (rows + 7) >> 3;
+      ksplit = MT <= kMaxMTK16;
+#pragma unroll
+      for (int i = 0; i < kAcc16; ++i) d[i] = 0.0;
+    }
+    const double* __restrict__ su = S.ring[stage];
+    const double* __restrict__ tv = S.vec[stage];
+    const int cols = h.cnt;
+    if (ksplit) {
+      switch (MT) {
+        case 1: bsplit16_mtiles<1>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 2: bsplit16_mtiles<2>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 3: bsplit16_mtiles<3>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 4: bsplit16_mtiles<4>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 5: bsplit16_mtiles<5>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        default: bsplit16_mtiles<kMaxMTK16>(d, su, tv, cols, rowsp, w, gq, tq); break;
+      }
+    } else {
+      const int cnt = MT > w ? (MT - w + kConsWarps - 1) / kConsWarps : 0;
+      switch (cnt) {
+        case 0: break;
+        case 1: bmt16<1>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 2: bmt16<2>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 3: bmt16<3>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        default: bmt16<kMaxMTB>(d, su, tv, cols, rowsp, w, gq, tq); break;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[stage]);
+    if (++stage == NS) { stage = 0; phase ^= 1; }
+    if (!(h.flags & kLast)) continue;
+    if (ksplit) {
+#pragma unroll
+      for (int i = 0; i < kMaxMTK16; ++i) {
+        if (i < MT) {
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            S.red[w * 64 + gq * 8 + 2 * tq] = d[4 * i + 2 * g];
+            S.red[w * 64 + gq * 8 + 2 * tq + 1] = d[4 * i + 2 * g + 1];
+            named_bar_sync(1, kCons);
+            if (tid < 64) {
+              const int r = i * 8 + (tid >> 3);
+              double u = 0.0;
+#pragma unroll
+              for (int ww = 0; ww < kConsWarps; ++ww) u += S.red[ww * 64 + tid];
+              if (r < rows) yfarm[(int64_t)(h.c + r) * NR + 8 * g + (tid & 7)] = u;
+            }
+            named_bar_sync(1, kCons);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kMaxMTB; ++j) {
+        const int mt = w + kConsWarps * j;
+        const int r = mt * 8 + gq;
+        if (mt < MT && r < rows) {
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            double2* dst = reinterpret_cast<double2*>(yfarm + (int64_t)(h.c + r) * NR + 8 * g + 2 * tq);
+            *dst = make_double2(d[4 * j + 2 * g], d[4 * j + 2 * g + 1]);
+          }
+        }
+      }
+    }
+  }
+}
+
 template <int NR>
 constexpr int kMultiMinBlocks = 3;
 
@@ -472,6 +730,7 @@ stageA_multi_kernel(const AItem* __restrict__ items, int n_items, int32_t* count
   pipe_init(S);
   if (threadIdx.x >= kCons) mA_producer<NS, NR, SD, SV>(S, items, n_items, counter, lp, xm);
   else if constexpr (NR == 8) mA_consumers_dmma<NS, SD, SV>(S, vdst, tm, tpartm, ritems, rcount);
+  else if constexpr (NR == 16) mA16_consumers<NS, SD, SV>(S, vdst, tm, tpartm, ritems, rcount);
   else mA_consumers<NS, NR, SD, SV>(S, vdst, tm, tpartm, ritems, rcount);
 }
 
@@ -826,6 +1085,7 @@ stageB_multi_kernel(const BItem* __restrict__ items, const BLevel* __restrict__ 
   pipe_init(S);
   if (threadIdx.x >= kCons) mB_producer<NS, NR, SD, SV>(S, items, blev, n_items, counter, kappa, lp, tml.p);
   else if constexpr (NR == 8) mB_consumers_dmma<NS, SD, SV>(S, yfarm);
+  else if constexpr (NR == 16) mB16_consumers<NS, SD, SV>(S, yfarm);
   else mB_consumers<NS, NR, SD, SV>(S, yfarm);
 }
 
@@ -984,58 +1244,67 @@ __global__ void combine_multi_sym_kernel(int64_t rows, int kappa, const double* 
 
 // Tiled stage-A schedule for the multi-RHS kernels (columns in tiles of <= kTileW).
 static void build_multi_schedule(Handle& h) {
-  std::vector<AItem> items;
-  std::vector<RItem> ritems;
-  int64_t p_len = 0, elems = 0;
+  int64_t elems = 0;
   for (int l = 1; l <= h.kappa; ++l) {
     const Level& L = h.levels[(size_t)l];
     for (int64_t Y = 0; Y < L.nbox; ++Y)
       elems += (h.box_end(l, Y) - h.box_begin(l, Y)) * ((L.vR[(size_t)Y] + 1) & ~1);
   }
   const int64_t target = std::min<int64_t>(262144, std::max<int64_t>(16384, elems / (4 * (int64_t)h.persist_ctas)));
-  for (int l = 1; l <= h.kappa; ++l) {
-    const Level& L = h.levels[(size_t)l];
-    for (int64_t Y = 0; Y < L.nbox; ++Y) {
-      const int R = L.vR[(size_t)Y], Rp = (R + 1) & ~1;
-      const int64_t y0 = h.box_begin(l, Y), nY = h.box_end(l, Y) - y0;
-      if (R == 0 || nY == 0) continue;
-      const int32_t vp = (int32_t)L.t_off[(size_t)Y];
-      for (int q0 = 0; q0 < R; q0 += kTileW) {
-        const int Wt = std::min(kTileW, R - q0), Wp = (Wt + 1) & ~1;
-        int64_t nch = std::max<int64_t>(1, (nY * Wp + target - 1) / target);
-        nch = std::min<int64_t>(nY, nch);
-        const int64_t rows = (nY + nch - 1) / nch;
-        nch = (nY + rows - 1) / rows;
-        const int64_t base = L.vpan_off[(size_t)Y] + q0;
-        if (nch == 1) {
-          items.push_back(AItem{base, y0, (int32_t)nY, Wt, vp + q0, l, -1, Rp});
-        } else {
-          if (p_len + nch * Wt > INT32_MAX / kMaxNR) throw Error{H2D_EINVAL, "multi partial buffer too large"};
-          ritems.push_back(RItem{vp + q0, (int32_t)p_len, Wt, (int32_t)nch});
-          for (int64_t c = 0; c < nch; ++c) {
-            const int64_t r0 = c * rows, nr = std::min(rows, nY - r0);
-            items.push_back(AItem{base + r0 * Rp, y0 + r0, (int32_t)nr, Wt, (int32_t)(-(p_len + c * Wt) - 1), l,
-                                  (int32_t)(ritems.size() - 1), Rp});
+  cudaStream_t s = h.stream;
+  // tiles of <= tile_w columns of every V box panel, row chunks of <= target elements (the
+  // 8- and 16-vector chunks use different tile widths: register budget of the consumers)
+  auto build_items = [&](int tile_w, AItem*& d_items, int64_t& n_items, RItem*& d_ritems, int32_t*& d_rcount,
+                         double*& d_tpart) {
+    std::vector<AItem> items;
+    std::vector<RItem> ritems;
+    int64_t p_len = 0;
+    for (int l = 1; l <= h.kappa; ++l) {
+      const Level& L = h.levels[(size_t)l];
+      for (int64_t Y = 0; Y < L.nbox; ++Y) {
+        const int R = L.vR[(size_t)Y], Rp = (R + 1) & ~1;
+        const int64_t y0 = h.box_begin(l, Y), nY = h.box_end(l, Y) - y0;
+        if (R == 0 || nY == 0) continue;
+        const int32_t vp = (int32_t)L.t_off[(size_t)Y];
+        for (int q0 = 0; q0 < R; q0 += tile_w) {
+          const int Wt = std::min(tile_w, R - q0), Wp = (Wt + 1) & ~1;
+          int64_t nch = std::max<int64_t>(1, (nY * Wp + target - 1) / target);
+          nch = std::min<int64_t>(nY, nch);
+          const int64_t rows = (nY + nch - 1) / nch;
+          nch = (nY + rows - 1) / rows;
+          const int64_t base = L.vpan_off[(size_t)Y] + q0;
+          if (nch == 1) {
+            items.push_back(AItem{base, y0, (int32_t)nY, Wt, vp + q0, l, -1, Rp});
+          } else {
+            if (p_len + nch * Wt > INT32_MAX / kMaxNR) throw Error{H2D_EINVAL, "multi partial buffer too large"};
+            ritems.push_back(RItem{vp + q0, (int32_t)p_len, Wt, (int32_t)nch});
+            for (int64_t c = 0; c < nch; ++c) {
+              const int64_t r0 = c * rows, nr = std::min(rows, nY - r0);
+              items.push_back(AItem{base + r0 * Rp, y0 + r0, (int32_t)nr, Wt, (int32_t)(-(p_len + c * Wt) - 1), l,
+                                    (int32_t)(ritems.size() - 1), Rp});
+            }
+            p_len += nch * Wt;
           }
-          p_len += nch * Wt;
         }
       }
     }
-  }
-  std::stable_sort(items.begin(), items.end(), [](const AItem& a, const AItem& b) {
-    return (int64_t)a.nrows * a.R > (int64_t)b.nrows * b.R;
-  });
-  cudaStream_t s = h.stream;
-  h.m_n_aitems = (int64_t)items.size();
-  h.m_aitems = h.alloc<AItem>(items.size());
-  h.m_ritems = h.alloc<RItem>(ritems.size());
-  h.m_rcount = h.alloc<int32_t>(ritems.size());
-  h.m_tpart = h.alloc<double>((size_t)std::max<int64_t>(1, p_len) * kMaxNR);
-  H2D_CUDA(cudaMemsetAsync(h.m_rcount, 0, std::max<size_t>(1, ritems.size()) * 4, s));
-  if (!items.empty())
-    H2D_CUDA(cudaMemcpyAsync(h.m_aitems, items.data(), items.size() * sizeof(AItem), cudaMemcpyHostToDevice, s));
-  if (!ritems.empty())
-    H2D_CUDA(cudaMemcpyAsync(h.m_ritems, ritems.data(), ritems.size() * sizeof(RItem), cudaMemcpyHostToDevice, s));
+    std::stable_sort(items.begin(), items.end(), [](const AItem& a, const AItem& b) {
+      return (int64_t)a.nrows * a.R > (int64_t)b.nrows * b.R;
+    });
+    n_items = (int64_t)items.size();
+    d_items = h.alloc<AItem>(items.size());
+    d_ritems = h.alloc<RItem>(ritems.size());
+    d_rcount = h.alloc<int32_t>(ritems.size());
+    d_tpart = h.alloc<double>((size_t)std::max<int64_t>(1, p_len) * kMaxNR);
+    H2D_CUDA(cudaMemsetAsync(d_rcount, 0, std::max<size_t>(1, ritems.size()) * 4, s));
+    if (!items.empty())
+      H2D_CUDA(cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(AItem), cudaMemcpyHostToDevice, s));
+    if (!ritems.empty())
+      H2D_CUDA(cudaMemcpyAsync(d_ritems, ritems.data(), ritems.size() * sizeof(RItem), cudaMemcpyHostToDevice, s));
+  };
+  build_items(kTileW, h.m_aitems, h.m_n_aitems, h.m_ritems, h.m_rcount, h.m_tpart);
+  if (!h.symapply)
+    build_items(kTileW16, h.m16_aitems, h.m16_n_aitems, h.m16_ritems, h.m16_rcount, h.m16_tpart);
   if (h.symapply) {
     // symmetric B' for 8 vectors: whole first-side U box panels (R <= kTileW, else the
     // symmetric handle keeps one vector at a time) in row chunks of <= target elements
@@ -1058,7 +1327,7 @@ static void build_multi_schedule(Handle& h) {
           if (nch == 1) {
             bitems.push_back(AItem{L.ub_off[(size_t)X], x0, (int32_t)nX, R, (int32_t)upos, l, -1, Rp, t1o});
           } else {
-            if (bp_len + nch * R > INT32_MAX / kMaxNR) throw Error{H2D_EINVAL, "multi partial buffer too large"};
+            if (bp_len + nch * R > INT32_MAX / kSymNR) throw Error{H2D_EINVAL, "multi partial buffer too large"};
             britems.push_back(RItem{(int32_t)upos, (int32_t)bp_len, R, (int32_t)nch});
             for (int64_t c = 0; c < nch; ++c) {
               const int64_t r0 = c * rows, nr = std::min(rows, nX - r0);
@@ -1080,12 +1349,12 @@ static void build_multi_schedule(Handle& h) {
       h.m_b1items = h.alloc<AItem>(bitems.size());
       h.m_b1ritems = h.alloc<RItem>(britems.size());
       h.m_b1rcount = h.alloc<int32_t>(britems.size());
-      h.m_b1tpart = h.alloc<double>((size_t)std::max<int64_t>(1, bp_len) * kMaxNR);
-      h.m_t1 = h.alloc<double>((size_t)std::max<int64_t>(1, h.t1_len) * kMaxNR + 16);   // + tile over-read
-      h.m_y1 = h.alloc<double>((size_t)h.kappa * h.n * kMaxNR);
+      h.m_b1tpart = h.alloc<double>((size_t)std::max<int64_t>(1, bp_len) * kSymNR);
+      h.m_t1 = h.alloc<double>((size_t)std::max<int64_t>(1, h.t1_len) * kSymNR + 16);   // + tile over-read
+      h.m_y1 = h.alloc<double>((size_t)h.kappa * h.n * kSymNR);
       // rows without a first-side panel at a level are never written: zero once
-      H2D_CUDA(cudaMemsetAsync(h.m_y1, 0, (size_t)h.kappa * h.n * kMaxNR * sizeof(double), s));
-      H2D_CUDA(cudaMemsetAsync(h.m_t1, 0, ((size_t)std::max<int64_t>(1, h.t1_len) * kMaxNR + 16) * sizeof(double), s));
+      H2D_CUDA(cudaMemsetAsync(h.m_y1, 0, (size_t)h.kappa * h.n * kSymNR * sizeof(double), s));
+      H2D_CUDA(cudaMemsetAsync(h.m_t1, 0, ((size_t)std::max<int64_t>(1, h.t1_len) * kSymNR + 16) * sizeof(double), s));
       H2D_CUDA(cudaMemsetAsync(h.m_b1rcount, 0, std::max<size_t>(1, britems.size()) * 4, s));
       if (!bitems.empty())
         H2D_CUDA(cudaMemcpyAsync(h.m_b1items, bitems.data(), bitems.size() * sizeof(AItem), cudaMemcpyHostToDevice, s));
@@ -1140,10 +1409,12 @@ static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, i
   H2D_CUDA(cudaStreamWaitEvent(a, h.ev_fork, 0));
   H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 2 * sizeof(int32_t), hi));
   const size_t smem = sizeof(PipeSmem<NS, SD, SV>);
-  if (h.m_n_aitems > 0) {
+  const bool w16 = NR == 16;   // 16 vectors: the narrower-tile schedule
+  const int64_t n_ai = w16 ? h.m16_n_aitems : h.m_n_aitems;
+  if (n_ai > 0) {
     stageA_multi_kernel<NS, NR, SD, SV><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
-        h.m_aitems, (int)h.m_n_aitems, h.d_counters, h.lp, h.m_xm, h.d_vdst, h.m_t, h.m_tpart, h.m_ritems,
-        h.m_rcount);
+        w16 ? h.m16_aitems : h.m_aitems, (int)n_ai, h.d_counters, h.lp, h.m_xm, h.d_vdst, h.m_t,
+        w16 ? h.m16_tpart : h.m_tpart, w16 ? h.m16_ritems : h.m_ritems, w16 ? h.m16_rcount : h.m_rcount);
     H2D_LAUNCH_CHECK();
   }
   if (h.n_bitems > 0) {
@@ -1275,14 +1546,17 @@ void matvec_multi(Handle& h, const double* dX, double* dY, int nrhs, int order) 
   // issue- / chain-bound per stage, so fewer, larger stages amortise the per-stage overhead:
   // C3 8 vectors 4.43 -> 3.88 ms per call, 4 vectors +9 % (5 x 16 KB measured alongside)
   auto chunk = [&](auto nr, const double* X, double* Y) {
-    multi_chunk<decltype(nr)::value, kNSMulti, kSDMulti, kSVMulti>(h, X, xlen, Y, ylen, order);
+    constexpr int R = decltype(nr)::value;
+    if constexpr (R == 16) multi_chunk<16, kNSMulti, kSDMulti16, kSVMulti16>(h, X, xlen, Y, ylen, order);
+    else multi_chunk<R, kNSMulti, kSDMulti, kSVMulti>(h, X, xlen, Y, ylen, order);
   };
   int k0 = 0;
   while (k0 < nrhs) {
     const int left = nrhs - k0;
     const double* X = dX + (int64_t)k0 * xlen;
     double* Y = dY + (int64_t)k0 * ylen;
-    if (left >= 8) { chunk(std::integral_constant<int, 8>{}, X, Y); k0 += 8; }
+    if (left >= 16) { chunk(std::integral_constant<int, 16>{}, X, Y); k0 += 16; }
+    else if (left >= 8) { chunk(std::integral_constant<int, 8>{}, X, Y); k0 += 8; }
     else if (left >= 4) { chunk(std::integral_constant<int, 4>{}, X, Y); k0 += 4; }
     else if (left >= 2) { chunk(std::integral_constant<int, 2>{}, X, Y); k0 += 2; }
     else {

@@ -3,8 +3,8 @@
 Bars: with the oracle's factors loaded, every column of Y = A X matches the oracle matvec
 of that column to rel-l2 <= 1e-12 (the single-vector bar); with GPU-built factors, every
 column matches the single-vector GPU matvec to <= 1e-13 (same operator, different
-summation order).  Chunks of 8 / 4 / 2 and a trailing single vector are all exercised
-(nrhs = 1, 2, 3, 5, 8, 11), as are TREE order on a row-restricted handle, host pointers,
+summation order).  Chunks of 16 / 8 / 4 / 2 and a trailing single vector are all exercised
+(nrhs = 1, 2, 3, 5, 8, 11, 16, 19, 31), as are TREE order on a row-restricted handle, host pointers,
 every kernel, leaves > 128 points (row blocks of the near field) and empty leaves.
 """
 import numpy as np
@@ -40,7 +40,7 @@ def cfg_build(h2d, cfg, pts=None, **kw):
     return pts, h2d.Hodlr2d.build(dev(pts), cfg.kernel, cfg.leaf_size, cfg.tol, **args)
 
 
-@pytest.mark.parametrize("nrhs", [1, 2, 3, 5, 8, 11])
+@pytest.mark.parametrize("nrhs", [1, 2, 3, 5, 8, 11, 16, 19])
 def test_multi_oracle_factors_c1(h2d, nrhs, tmp_path):
     cfg = W.CONFIGS["c1"]
     pts = W.config_points(cfg)
@@ -60,9 +60,9 @@ def test_multi_oracle_factors_c1(h2d, nrhs, tmp_path):
 def test_multi_matches_single_gpu(h2d, name):
     cfg = W.CONFIGS[name]
     pts, op = cfg_build(h2d, cfg)
-    X = np.stack([W.config_x(cfg, k) for k in range(13)])
+    X = np.stack([W.config_x(cfg, k) for k in range(31)])   # chunks of 16, 8, 4, 2, 1
     Y = op.matvec_multi(dev(X)).cpu().numpy()
-    for k in range(13):
+    for k in range(31):
         y1 = op.matvec(dev(X[k])).cpu().numpy()
         assert rel(Y[k], y1) <= 1e-13, k
     # host pointers give the same result (deterministic)
@@ -78,9 +78,9 @@ def test_multi_kernels(h2d, kernel, c, scale, shift):
     pts = W.uniform_points(4096, 91)
     op = h2d.Hodlr2d.build(dev(pts), kernel, 64, 1e-10, c=c, scale=scale, shift=shift,
                            box_lo=(-1, -1), box_side=2.0, test_rank=5)
-    X = np.stack([W.random_vector(4096, 200 + k) for k in range(4)])
+    X = np.stack([W.random_vector(4096, 200 + k) for k in range(20)])
     Y = op.matvec_multi(dev(X)).cpu().numpy()
-    for k in range(4):
+    for k in range(20):
         assert rel(Y[k], op.matvec(dev(X[k])).cpu().numpy()) <= 1e-13
 
 
@@ -90,9 +90,9 @@ def test_multi_big_and_empty_leaves(h2d):
     for pts, leaf in ((W.chebyshev_grid(60), 500), (W.uniform_points(5000, 78, (-1.0, -1.0), 0.9), 64)):
         op = h2d.Hodlr2d.build(dev(pts), "log", leaf, 1e-10, box_lo=(-1, -1), box_side=2.0)
         n = pts.shape[0]
-        X = np.stack([W.random_vector(n, 300 + k) for k in range(8)])
+        X = np.stack([W.random_vector(n, 300 + k) for k in range(16)])
         Y = op.matvec_multi(dev(X)).cpu().numpy()
-        for k in range(8):
+        for k in range(16):
             yd = oracle.dense_matvec(pts, X[k], 0)
             assert rel(Y[k], op.matvec(dev(X[k])).cpu().numpy()) <= 1e-13
             assert rel(Y[k], yd) <= 1e-9
@@ -104,11 +104,11 @@ def test_multi_tree_order_row_partition(h2d):
     full = h2d.Hodlr2d.build(dev(pts), cfg.kernel, cfg.leaf_size, cfg.tol, box_lo=cfg.box_lo,
                              box_side=cfg.box_side)
     perm, _ = full.tree()
-    X = np.stack([W.config_x(cfg, k)[perm] for k in range(6)])
+    X = np.stack([W.config_x(cfg, k)[perm] for k in range(22)])
     for rank in range(2):
         part = h2d.Hodlr2d.build(dev(pts), cfg.kernel, cfg.leaf_size, cfg.tol, box_lo=cfg.box_lo,
                                  box_side=cfg.box_side, world=2, rank=rank)
         Y = part.matvec_multi(dev(X), order="tree").cpu().numpy()
-        for k in range(6):
+        for k in range(22):
             y1 = part.matvec(dev(X[k]), order="tree").cpu().numpy()
             assert rel(Y[k], y1) <= 1e-13
