@@ -43,7 +43,7 @@ def parse():
                     help="symmetric build + apply (one ACA per unordered pair, DESIGN.md R23)")
     ap.add_argument("--no-variants", action="store_true",
                     help="skip the symmetric-storage (NEXT N1) variant measured beside the headline")
-    ap.add_argument("--multi-rhs", type=int, default=8,
+    ap.add_argument("--multi-rhs", type=int, default=16,
                     help="also time hodlr2d_matvec_multi with this many vectors per call (0: skip)")
     ap.add_argument("--rank-slice", type=int, default=None,
                     help="informational: build and time rank G's slice of a --slice-world partition "
