@@ -126,10 +126,11 @@ static void clear_factors(Handle& h) {
   h.d_b1ritems = nullptr;
   h.n_b1items = 0;
   for (void* q : {(void*)h.m_aitems, (void*)h.m_ritems, (void*)h.m_rcount, (void*)h.m_tpart, (void*)h.m_xm,
-                  (void*)h.m_xcols, (void*)h.m_t, (void*)h.m_yfar, (void*)h.m_ynear})
+                  (void*)h.m_iperm, (void*)h.m_t, (void*)h.m_yfar, (void*)h.m_ynear})
     h.release(q);
   h.m_aitems = nullptr; h.m_ritems = nullptr; h.m_rcount = nullptr; h.m_tpart = nullptr;
-  h.m_xm = h.m_xcols = h.m_t = h.m_yfar = h.m_ynear = nullptr;
+  h.m_xm = h.m_t = h.m_yfar = h.m_ynear = nullptr;
+  h.m_iperm = nullptr;
   h.m_n_aitems = 0;
   for (void* q : {(void*)h.m_b1items, (void*)h.m_b1ritems, (void*)h.m_b1rcount, (void*)h.m_b1tpart, (void*)h.m_t1,
                   (void*)h.m_y1, (void*)h.m16_aitems, (void*)h.m16_ritems, (void*)h.m16_rcount, (void*)h.m16_tpart})

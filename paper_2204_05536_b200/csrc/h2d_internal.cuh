@@ -276,7 +276,8 @@ struct Handle {
   int64_t m_n_aitems = 0;
   RItem* m_ritems = nullptr;
   int32_t* m_rcount = nullptr;
-  double *m_tpart = nullptr, *m_xm = nullptr, *m_xcols = nullptr, *m_t = nullptr;
+  double *m_tpart = nullptr, *m_xm = nullptr, *m_t = nullptr;
+  int32_t* m_iperm = nullptr;             // inverse of d_perm (ORIGINAL index -> TREE row)
   double *m_yfar = nullptr, *m_ynear = nullptr;
   // 16-vector chunks: stage-A tiles of <= 224 columns (their own schedule)
   AItem* m16_aitems = nullptr;

@@ -1110,7 +1110,7 @@ template <int KID, int NR>
 __global__ void __launch_bounds__(256, 3)
 p2p_multi_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_start,
                  const double* __restrict__ px, const double* __restrict__ py,
-                 const double* __restrict__ xcols, int64_t n, KernelParams kp, double* __restrict__ ynearm) {
+                 const double* __restrict__ xm, int64_t n, KernelParams kp, double* __restrict__ ynearm) {
   __shared__ double tpx[kMTile], tpy[kMTile], tx[NR][kMTile];
   __shared__ double red[256];
   __shared__ double2 tab[128];
@@ -1145,8 +1145,10 @@ p2p_multi_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf
         for (int e = tid; e < nt; e += 256) {
           tpx[e] = px[ys + cb + e];
           tpy[e] = py[ys + cb + e];
-#pragma unroll
-          for (int k = 0; k < NR; ++k) tx[k][e] = xcols[(int64_t)k * n + ys + cb + e];
+        }
+        for (int q = tid; q < nt * NR; q += 256) {   // x records of the tile, coalesced
+          const int e = q / NR;
+          tx[q - e * NR][e] = xm[(ys + cb) * NR + q];
         }
         __syncthreads();
         if (act) {
@@ -1173,50 +1175,60 @@ p2p_multi_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf
       if (tid < RB) {
         double u = 0.0;
         for (int gg = 0; gg < G; ++gg) u += red[gg * RB + tid];
-        ynearm[(int64_t)k * n + xs + rb + tid] = u;
+        ynearm[(xs + rb + tid) * NR + k] = u;
       }
     }
   }
 }
 
-// x_m[s * NR + k] and x_cols[k * n + s] from NR vectors of length xlen (TREE: X[k*xlen + s],
-// ORIGINAL: X[k*xlen + perm[s]]).
+// x_m[s * NR + k] (one record of the NR values per TREE row s) from NR vectors of length
+// xlen, in the caller's order: ORIGINAL -> thread per original index o, s = iperm[o] (the
+// reads of X coalesce, each thread writes one record); TREE -> s = o.
+__global__ void invert_perm_kernel(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ iperm) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
+    iperm[perm[s]] = (int32_t)s;
+}
+
 __global__ void permute_multi_kernel(int NR, const double* __restrict__ X, int64_t xlen,
-                                     const int32_t* __restrict__ perm, int64_t n, double* __restrict__ xm,
-                                     double* __restrict__ xcols) {
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t src = perm ? perm[s] : s;
-    for (int k = 0; k < NR; ++k) {
-      const double v = X[(int64_t)k * xlen + src];
-      xm[s * NR + k] = v;
-      xcols[(int64_t)k * n + s] = v;
+                                     const int32_t* __restrict__ iperm, int64_t n, double* __restrict__ xm) {
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = iperm ? iperm[o] : o;
+    double2* __restrict__ rec = reinterpret_cast<double2*>(xm + s * NR);
+    for (int k = 0; k < NR; k += 2)
+      rec[k >> 1] = make_double2(X[(int64_t)k * xlen + o], X[(int64_t)(k + 1) * xlen + o]);
+  }
+}
+
+// Y[k * ylen + o] = yfar_m[r] + scale ynear_m[r] + shift x_m[r] (records of NR values per
+// TREE row r).  ORIGINAL: thread per output index o, r = iperm[o] (coalesced Y writes,
+// record reads); TREE: r = row_begin + o' with o = r - y_row0.
+__global__ void combine_multi_kernel(int NR, int64_t row_begin, int64_t rows, const double* __restrict__ yfarm,
+                                     const double* __restrict__ ynearm, int64_t n, const double* __restrict__ xm,
+                                     double scale, double shift, double* __restrict__ Y, int64_t ylen,
+                                     const int32_t* __restrict__ iperm, int order_out, int64_t y_row0) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < rows; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = order_out == H2D_ORDER_ORIGINAL ? (int64_t)iperm[q] : row_begin + q;
+    const int64_t o = order_out == H2D_ORDER_ORIGINAL ? q : r - y_row0;
+    const double2* __restrict__ yf = reinterpret_cast<const double2*>(yfarm + (r - row_begin) * NR);
+    const double2* __restrict__ yn = reinterpret_cast<const double2*>(ynearm + r * NR);
+    const double2* __restrict__ xr = reinterpret_cast<const double2*>(xm + r * NR);
+    for (int k = 0; k < NR; k += 2) {
+      const double2 f = yf[k >> 1], e = yn[k >> 1], xv = xr[k >> 1];
+      Y[(int64_t)k * ylen + o] = f.x + fma(scale, e.x, shift * xv.x);
+      Y[(int64_t)(k + 1) * ylen + o] = f.y + fma(scale, e.y, shift * xv.y);
     }
   }
 }
 
-// Y[k * ylen + out(r)] = yfar_m[(r - row_begin) * NR + k] + scale ynear_m[k n + r] + shift x
-__global__ void combine_multi_kernel(int NR, int64_t row_begin, int64_t rows, const double* __restrict__ yfarm,
-                                     const double* __restrict__ ynearm, int64_t n, const double* __restrict__ xcols,
-                                     double scale, double shift, double* __restrict__ Y, int64_t ylen,
-                                     const int32_t* __restrict__ perm, int order_out, int64_t y_row0) {
-  for (int64_t kk = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; kk < rows; kk += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = row_begin + kk;
-    const int64_t o = order_out == H2D_ORDER_ORIGINAL ? perm[r] : r - y_row0;
-    for (int k = 0; k < NR; ++k)
-      Y[(int64_t)k * ylen + o] = yfarm[kk * NR + k] + fma(scale, ynearm[(int64_t)k * n + r], shift * xcols[(int64_t)k * n + r]);
-  }
-}
-
-// symmetric apply: + the kappa per-level row products Y1 of B'
+// symmetric apply: + the kappa per-level row products Y1 of B' (8 vectors; records of 8)
 __global__ void combine_multi_sym_kernel(int64_t rows, int kappa, const double* __restrict__ yfarm,
                                          const double* __restrict__ y1m, const double* __restrict__ ynearm, int64_t n,
-                                         const double* __restrict__ xcols, double scale, double shift,
-                                         double* __restrict__ Y, int64_t ylen, const int32_t* __restrict__ perm,
+                                         const double* __restrict__ xm, double scale, double shift,
+                                         double* __restrict__ Y, int64_t ylen, const int32_t* __restrict__ iperm,
                                          int order_out, int64_t y_row0) {
-  // NR = 8: a row's 8 values are one 64-byte record in yfar and in every level of Y1 (four
-  // 16-byte loads each, levels outer, 8 register accumulators)
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = order_out == H2D_ORDER_ORIGINAL ? perm[r] : r - y_row0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < rows; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = order_out == H2D_ORDER_ORIGINAL ? (int64_t)iperm[q] : q;
+    const int64_t o = order_out == H2D_ORDER_ORIGINAL ? q : r - y_row0;
     double v[8];
     const double2* __restrict__ yf = reinterpret_cast<const double2*>(yfarm + r * 8);
 #pragma unroll
@@ -1234,9 +1246,14 @@ __global__ void combine_multi_sym_kernel(int64_t rows, int kappa, const double* 
         v[2 * k2 + 1] += a.y;
       }
     }
+    const double2* __restrict__ yn = reinterpret_cast<const double2*>(ynearm + r * 8);
+    const double2* __restrict__ xr = reinterpret_cast<const double2*>(xm + r * 8);
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      Y[(int64_t)k * ylen + o] = v[k] + fma(scale, ynearm[(int64_t)k * n + r], shift * xcols[(int64_t)k * n + r]);
+    for (int k2 = 0; k2 < 4; ++k2) {
+      const double2 e = yn[k2], xv = xr[k2];
+      Y[(int64_t)(2 * k2) * ylen + o] = v[2 * k2] + fma(scale, e.x, shift * xv.x);
+      Y[(int64_t)(2 * k2 + 1) * ylen + o] = v[2 * k2 + 1] + fma(scale, e.y, shift * xv.y);
+    }
   }
 }
 
@@ -1365,7 +1382,9 @@ static void build_multi_schedule(Handle& h) {
   }
   const int64_t served = h.row_end - h.row_begin;
   h.m_xm = h.alloc<double>((size_t)h.n * kMaxNR);
-  h.m_xcols = h.alloc<double>((size_t)h.n * kMaxNR);
+  h.m_iperm = h.alloc<int32_t>((size_t)h.n);   // original index -> TREE row (record permutes)
+  invert_perm_kernel<<<(int)std::min<int64_t>((h.n + 255) / 256, 148 * 16), 256, 0, s>>>(h.d_perm, h.n, h.m_iperm);
+  H2D_LAUNCH_CHECK();
   h.m_t = h.alloc<double>((size_t)std::max<int64_t>(1, h.t_len) * kMaxNR);
   h.m_yfar = h.alloc<double>((size_t)std::max<int64_t>(1, served) * kMaxNR);
   h.m_ynear = h.alloc<double>((size_t)h.n * kMaxNR);
@@ -1392,7 +1411,7 @@ static void launch_p2p_multi(Handle& h, cudaStream_t a) {
   const int64_t nleaves = h.leaf_end - h.leaf_begin;
   if (nleaves <= 0) return;
   p2p_multi_kernel<KID, NR><<<(int)nleaves, 256, 0, a>>>(h.kappa, h.leaf_begin, h.d_leaf_start, h.d_px, h.d_py,
-                                                         h.m_xcols, h.n, h.kp, h.m_ynear);
+                                                         h.m_xm, h.n, h.kp, h.m_ynear);
   H2D_LAUNCH_CHECK();
 }
 
@@ -1401,8 +1420,8 @@ static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, i
   set_multi_attrs<NR, NS, SD, SV>();
   cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
   const int grid = (int)std::min<int64_t>((h.n + 255) / 256, 148 * 16);
-  permute_multi_kernel<<<grid, 256, 0, s>>>(NR, dX, xlen, order == H2D_ORDER_ORIGINAL ? h.d_perm : nullptr, h.n,
-                                            h.m_xm, h.m_xcols);
+  permute_multi_kernel<<<grid, 256, 0, s>>>(NR, dX, xlen, order == H2D_ORDER_ORIGINAL ? h.m_iperm : nullptr, h.n,
+                                            h.m_xm);
   H2D_LAUNCH_CHECK();
   H2D_CUDA(cudaEventRecord(h.ev_fork, s));
   H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_fork, 0));
@@ -1439,8 +1458,8 @@ static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, i
   const int64_t rows = h.row_end - h.row_begin;
   if (rows > 0) {
     const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 148 * 8);
-    combine_multi_kernel<<<blocks, 256, 0, s>>>(NR, h.row_begin, rows, h.m_yfar, h.m_ynear, h.n, h.m_xcols,
-                                                h.kp.scale, h.kp.shift, dY, ylen, h.d_perm,
+    combine_multi_kernel<<<blocks, 256, 0, s>>>(NR, h.row_begin, rows, h.m_yfar, h.m_ynear, h.n, h.m_xm,
+                                                h.kp.scale, h.kp.shift, dY, ylen, h.m_iperm,
                                                 order == H2D_ORDER_ORIGINAL ? H2D_ORDER_ORIGINAL : H2D_ORDER_TREE,
                                                 h.row_begin);
     H2D_LAUNCH_CHECK();
@@ -1463,8 +1482,8 @@ static void multi_chunk_sym(Handle& h, const double* dX, int64_t xlen, double* d
   });
   cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
   const int grid = (int)std::min<int64_t>((h.n + 255) / 256, 148 * 16);
-  permute_multi_kernel<<<grid, 256, 0, s>>>(NR, dX, xlen, order == H2D_ORDER_ORIGINAL ? h.d_perm : nullptr, h.n,
-                                            h.m_xm, h.m_xcols);
+  permute_multi_kernel<<<grid, 256, 0, s>>>(NR, dX, xlen, order == H2D_ORDER_ORIGINAL ? h.m_iperm : nullptr, h.n,
+                                            h.m_xm);
   H2D_LAUNCH_CHECK();
   H2D_CUDA(cudaEventRecord(h.ev_fork, s));
   H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_fork, 0));
@@ -1504,8 +1523,8 @@ static void multi_chunk_sym(Handle& h, const double* dX, int64_t xlen, double* d
   const int64_t rows = h.row_end - h.row_begin;   // symmetric apply: single-rank handles
   if (rows > 0) {
     const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 148 * 8);
-    combine_multi_sym_kernel<<<blocks, 256, 0, s>>>(rows, h.kappa, h.m_yfar, h.m_y1, h.m_ynear, h.n, h.m_xcols,
-                                                    h.kp.scale, h.kp.shift, dY, ylen, h.d_perm,
+    combine_multi_sym_kernel<<<blocks, 256, 0, s>>>(rows, h.kappa, h.m_yfar, h.m_y1, h.m_ynear, h.n, h.m_xm,
+                                                    h.kp.scale, h.kp.shift, dY, ylen, h.m_iperm,
                                                     order == H2D_ORDER_ORIGINAL ? H2D_ORDER_ORIGINAL : H2D_ORDER_TREE,
                                                     h.row_begin);
     H2D_LAUNCH_CHECK();
