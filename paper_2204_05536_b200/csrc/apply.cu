@@ -423,19 +423,21 @@ __device__ __forceinline__ void tile_fast8(int mt, int nt, const double* __restr
     double r0 = 0.0, r1 = 0.0;
 #pragma unroll
     for (int bb = 0; bb < kSymMaxB; ++bb) {
-      if (bb < B) {
+      // self block: column block bb < aa lies wholly below the diagonal (i >= 16 aa > j), as
+      // does bb = aa for the second row (warp-uniform skips, no evaluation)
+      if (bb < B && (!DIAG || bb >= aa)) {
         const double dx0 = px0 - cpx[bb], dy0 = py0 - cpy[bb];
-        const double dx1 = px1 - cpx[bb], dy1 = py1 - cpy[bb];
         double k0v = kfast<KID>(fma(dx0, dx0, dy0 * dy0), tab, kp);
-        double k1v = kfast<KID>(fma(dx1, dx1, dy1 * dy1), tab, kp);
-        if (DIAG) {
-          k0v = i0 < tj + 16 * bb ? k0v : 0.0;
-          k1v = i1 < tj + 16 * bb ? k1v : 0.0;
-        }
+        if (DIAG) k0v = i0 < tj + 16 * bb ? k0v : 0.0;
         r0 = fma(k0v, cxv[bb], r0);
-        r1 = fma(k1v, cxv[bb], r1);
         cacc[bb] = fma(k0v, x0, cacc[bb]);
-        cacc[bb] = fma(k1v, x1, cacc[bb]);
+        if (!DIAG || bb > aa) {
+          const double dx1 = px1 - cpx[bb], dy1 = py1 - cpy[bb];
+          double k1v = kfast<KID>(fma(dx1, dx1, dy1 * dy1), tab, kp);
+          if (DIAG) k1v = i1 < tj + 16 * bb ? k1v : 0.0;
+          r1 = fma(k1v, cxv[bb], r1);
+          cacc[bb] = fma(k1v, x1, cacc[bb]);
+        }
       }
     }
     if (DIAG && tj == 0) {
