@@ -1373,7 +1373,8 @@ static void launch_stageB_geom(Handle& h, cudaStream_t hi) {
     H2D_CUDA(cudaFuncSetAttribute(stageB_tma_kernel<NS, SD, SV>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));
   });
-  stageB_tma_kernel<NS, SD, SV><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+  // persistent grid, but never more CTAs than items (small operators: ring set-up per CTA)
+  stageB_tma_kernel<NS, SD, SV><<<(int)std::min<int64_t>(h.persist_ctas, h.n_bbig), kPipeThreads, smem, hi>>>(
       h.d_bitems, h.d_blev, (int)h.n_bbig, h.d_counters + 1, h.kappa, h.lp, h.d_yfar);
   H2D_LAUNCH_CHECK();
 }
@@ -1404,7 +1405,7 @@ static void launch_stages(Handle& h, const double* d_xtree, cudaStream_t hi) {
   const size_t smem = sizeof(PipeSmem<NS>);
   launch_small(h, true, d_xtree, h.d_t, hi);
   if (h.n_abig > 0) {
-    stageA_tma_kernel<NS><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+    stageA_tma_kernel<NS><<<(int)std::min<int64_t>(h.persist_ctas, h.n_abig), kPipeThreads, smem, hi>>>(
         h.d_aitems, (int)h.n_abig, h.d_counters, h.lp, d_xtree, h.d_vdst, h.d_t, h.d_tpart,
         h.d_ritems, h.d_rcount);
     H2D_LAUNCH_CHECK();
@@ -1477,13 +1478,14 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
     H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 4 * sizeof(int32_t), hi));
     launch_small(h, true, d_xtree, h.d_t1, hi);
     if (h.n_abig > 0) {
-      stageA_tma_kernel<kNSShallow><<<h.persist_ctas, kPipeThreads, smem, hi>>>(
+      stageA_tma_kernel<kNSShallow><<<(int)std::min<int64_t>(h.persist_ctas, h.n_abig), kPipeThreads, smem, hi>>>(
           h.d_aitems, (int)h.n_abig, h.d_counters, h.lp, d_xtree, h.d_vdst, h.d_t1, h.d_tpart, h.d_ritems,
           h.d_rcount);
       H2D_LAUNCH_CHECK();
     }
     if (h.n_b1items > 0) {
-      stageA_dual_kernel<kNSDual, kSDDual><<<h.persist_ctas, kPipeThreads, sizeof(PipeSmem<kNSDual, kSDDual>), hi>>>(
+      stageA_dual_kernel<kNSDual, kSDDual><<<(int)std::min<int64_t>(h.persist_ctas, h.n_b1items), kPipeThreads,
+                                             sizeof(PipeSmem<kNSDual, kSDDual>), hi>>>(
           h.d_b1items, (int)h.n_b1items, h.d_counters + 3, h.lp, d_xtree, h.d_udst, h.d_t, h.d_b1tpart,
           h.d_b1ritems, h.d_b1rcount, h.d_t1, h.d_y1,
           getenv("H2D_DUAL_NOROW") ? (int64_t)-1 : h.n);   // diagnostics: skip the row dots
