@@ -322,6 +322,13 @@ def run_ours(args, cfg):
                                  "frac": round(other_bytes / (other_ms * 1e-3) / 1e9 / peak, 4)},
             "stage_ms_per_matvec": {k: round(v, 4) for k, v in per.items()},
             "whole_matvec_frac": round(inf["matvec_bytes"] / (ms_step * 1e-3) / 1e9 / peak, 4)}
+    try:   # context: the practical ceiling of a pure-read stream (tools/read_bw.cu)
+        with open(os.path.join(ROOT, "profiles", "read_bw_measured.json")) as f:
+            rp = json.load(f)["read_gbs_best"]
+        roof["read_peak_microbench"] = {"gbs": rp, "frac": round(achieved / rp, 4),
+                                        "source": "profiles/read_bw_measured.json (tools/read_bw.cu)"}
+    except Exception:
+        pass
 
     # e2e through the public API with host (pinned) buffers, copies inside the timed region
     e2e = None
