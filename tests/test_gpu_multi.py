@@ -112,3 +112,17 @@ def test_multi_tree_order_row_partition(h2d):
         for k in range(22):
             y1 = part.matvec(dev(X[k]), order="tree").cpu().numpy()
             assert rel(Y[k], y1) <= 1e-13
+
+
+def test_multi_clustered_chebyshev(h2d):
+    """The paper's clustered workload (Chebyshev grid, depth rule, phi_1 system): the multi-RHS
+    kernels stream every item through their rings (the single-vector path routes the tiny
+    ones to warp kernels); 16 + 2 + 1 vectors equal their single-vector matvecs to 1e-13."""
+    pts = W.chebyshev_grid(120)
+    n = pts.shape[0]
+    op = h2d.Hodlr2d.build(dev(pts), "rbf_phi1", 100, 1e-12, c=1e-3, shift=float(n), box_lo=(-1, -1),
+                           box_side=2.0, depth=-2)
+    X = np.stack([W.random_vector(n, 700 + k) for k in range(19)])
+    Y = op.matvec_multi(dev(X)).cpu().numpy()
+    for k in range(19):
+        assert rel(Y[k], op.matvec(dev(X[k])).cpu().numpy()) <= 1e-13, k

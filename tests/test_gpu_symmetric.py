@@ -229,3 +229,21 @@ def test_symmetric_multi_rhs_wide_panels_fallback(h2d):
     Y = op.matvec_multi(dev(X)).cpu().numpy()
     for k in range(8):
         assert np.array_equal(Y[k], op.matvec(dev(X[k])).cpu().numpy())
+
+
+def test_symmetric_gmres(h2d):
+    """GMRES on a symmetric-apply handle (the paper's phi_1 system on a Chebyshev grid):
+    converges to 1e-10 and recovers the directed handle's solution to the ACA tolerance."""
+    pts = W.chebyshev_grid(80)
+    n = pts.shape[0]
+    kw = dict(c=1e-3, shift=float(n), box_lo=(-1, -1), box_side=2.0, depth=-2)
+    sym = h2d.Hodlr2d.build(dev(pts), "rbf_phi1", 100, 1e-12, symmetric=True, **kw)
+    dirh = h2d.Hodlr2d.build(dev(pts), "rbf_phi1", 100, 1e-12, **kw)
+    assert sym.info()["symmetric_apply"] == 1
+    lam = np.random.default_rng(5).uniform(-1.0, 1.0, n)
+    f = oracle.dense_matvec(pts, lam, 3, 1e-3, 1.0, float(n))
+    xs, its, rr = sym.gmres(dev(f), tol=1e-10)
+    xd, _, _ = dirh.gmres(dev(f), tol=1e-10)
+    assert rr <= 1e-10 and its < 40
+    assert rel(xs.cpu().numpy(), lam) <= 1e-9
+    assert rel(xs.cpu().numpy(), xd.cpu().numpy()) <= 1e-9
