@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <numeric>
+#include <type_traits>
 
 #include "h2d_internal.cuh"
 #include "stages.cuh"
@@ -536,22 +537,25 @@ p2p_fast_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-// Small-leaf near field: leaves of <= 32 points (clustered inputs such as the paper's
-// Chebyshev grids put a handful of points in most leaves at the depth-rule kappa, where one
-// CTA and six barriers per leaf cost more than the pairs).  One warp per leaf (atomic
-// counter), lane i = row i; the leaf's and the neighbour's points are staged in the warp's
-// smem.  Self block: row sums over all m x m pairs.  +x / +y neighbour (any size, 32-point
-// chunks, 8 columns at a time): row sums in registers, the 8 column sums of the group by a
-// transposed butterfly (9 double shuffles; lane 4t ends up holding column t).  Same slots
-// as p2p_fast_kernel: s0 (own rows), sL / sD (the neighbour's rows), one writer per value.
-constexpr int kWarpLeaf = 32;
+// Warp-per-leaf near field for leaves of <= 96 points: one warp per leaf (atomic counter),
+// lane owns rows lane + 32 r (r < RPL = ceil(m / 32)); no block barriers, so 8 leaves per
+// CTA proceed independently (the CTA kernel's six barriers per leaf made it latency-bound:
+// C3 P2P 1.21 -> 0.64 ms standalone, FP64 fraction 0.14 -> 0.26).  The leaf's points are
+// staged in the warp's smem.  Self block: row sums over all m x m pairs (a third more
+// evaluations than the symmetric CTA kernel, no column sums).  +x / +y neighbour (any size,
+// 32-point chunks, 8 columns at a time): row sums in registers, the 8 column sums of the
+// group (over all RPL rows) by a transposed butterfly (9 double shuffles; lane 4t ends up
+// holding column t).  Same slots as p2p_fast_kernel: s0 (own rows), sL / sD (the
+// neighbour's rows), one writer per value.
+constexpr int kWarpLeaf = 96;      // rows per lane RPL = ceil(m / 32) <= 3 (leaves <= 96 points)
 
-template <int KID>
-__device__ __forceinline__ void warp_nbr(int lane, double pi, double qi, double xi, bool vi, int n, int64_t nb0,
-                                         const double* __restrict__ px, const double* __restrict__ py,
-                                         const double* __restrict__ x, double2* __restrict__ spq,
-                                         double* __restrict__ sx, const double2* __restrict__ tab,
-                                         const KernelParams& kp, double& acc, double* __restrict__ out) {
+template <int KID, int RPL>
+__device__ __forceinline__ void warp_nbr(int lane, const double (&pi)[RPL], const double (&qi)[RPL],
+                                         const double (&xi)[RPL], int n, int64_t nb0, const double* __restrict__ px,
+                                         const double* __restrict__ py, const double* __restrict__ x,
+                                         double2* __restrict__ spq, double* __restrict__ sx,
+                                         const double2* __restrict__ tab, const KernelParams& kp,
+                                         double (&acc)[RPL], double* __restrict__ out) {
   for (int cb = 0; cb < n; cb += 32) {
     const int nc = min(32, n - cb);
     __syncwarp();
@@ -565,15 +569,18 @@ __device__ __forceinline__ void warp_nbr(int lane, double pi, double qi, double 
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         const int j = g + t;
-        double v = 0.0, xj = 0.0;
-        if (j < nc) {
+        c[t] = 0.0;
+        if (j < nc) {   // warp-uniform
           const double2 q = spq[j];
-          xj = sx[j];
-          const double dx = pi - q.x, dy = qi - q.y;
-          v = kfast<KID>(fma(dx, dx, dy * dy), tab, kp);
+          const double xj = sx[j];
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) {
+            const double dx = pi[r] - q.x, dy = qi[r] - q.y;
+            const double v = kfast<KID>(fma(dx, dx, dy * dy), tab, kp);
+            acc[r] = fma(v, xj, acc[r]);
+            c[t] = fma(v, xi[r], c[t]);   // xi = 0 on rows past the leaf
+          }
         }
-        acc = fma(v, xj, acc);
-        c[t] = vi ? v * xi : 0.0;
       }
       const double v = warp_transpose_sum8(c, lane);
       const int col = g + (lane >> 2);
@@ -582,14 +589,14 @@ __device__ __forceinline__ void warp_nbr(int lane, double pi, double qi, double 
   }
 }
 
-template <int KID>
+template <int KID, int RPL>
 __global__ void __launch_bounds__(256, 3)
 p2p_warp_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int32_t* counter,
                 const int32_t* __restrict__ leaf_start, const double* __restrict__ px,
                 const double* __restrict__ py, const double* __restrict__ x, KernelParams kp,
                 double* __restrict__ s0, double* __restrict__ sL, double* __restrict__ sD) {
-  __shared__ double2 spq[8][2][32];
-  __shared__ double sxv[8][2][32];
+  __shared__ double2 sself[8][32 * RPL], snb[8][32];
+  __shared__ double xself[8][32 * RPL], xnb[8][32];
   __shared__ double2 tab[128];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (kNeedsLogTable<KID>) hlog_table(tab);
@@ -600,31 +607,41 @@ p2p_warp_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int
     idx = __shfl_sync(0xffffffffu, idx, 0);
     if (idx >= n_leaves) break;
     const P2PMeta M = p2p_meta(kappa, leaves[idx], leaf_start);
-    const bool vi = lane < M.m;
-    double pi = 0.0, qi = 0.0, xi = 0.0;
-    if (vi) {
-      pi = px[M.xs + lane];
-      qi = py[M.xs + lane];
-      xi = x[M.xs + lane];
+    double pi[RPL], qi[RPL], xi[RPL], acc[RPL];
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      const bool vi = i < M.m;
+      pi[r] = vi ? px[M.xs + i] : 0.0;
+      qi[r] = vi ? py[M.xs + i] : 0.0;
+      xi[r] = vi ? x[M.xs + i] : 0.0;
+      acc[r] = 0.0;
+      sself[w][i] = make_double2(pi[r], qi[r]);
+      xself[w][i] = xi[r];
     }
     __syncwarp();
-    spq[w][0][lane] = make_double2(pi, qi);
-    sxv[w][0][lane] = xi;
-    __syncwarp();
-    double acc = 0.0;
     for (int j = 0; j < M.m; ++j) {   // self block (K(0) by kfast's r2 = 0 branch)
-      const double2 q = spq[w][0][j];
-      const double dx = pi - q.x, dy = qi - q.y;
-      acc = fma(kfast<KID>(fma(dx, dx, dy * dy), tab, kp), sxv[w][0][j], acc);
+      const double2 q = sself[w][j];
+      const double xj = xself[w][j];
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const double dx = pi[r] - q.x, dy = qi[r] - q.y;
+        acc[r] = fma(kfast<KID>(fma(dx, dx, dy * dy), tab, kp), xj, acc[r]);
+      }
     }
     if (M.has_r)
-      warp_nbr<KID>(lane, pi, qi, xi, vi, M.rn, M.rs, px, py, x, spq[w][1], sxv[w][1], tab, kp, acc, sL + M.rs);
+      warp_nbr<KID, RPL>(lane, pi, qi, xi, M.rn, M.rs, px, py, x, snb[w], xnb[w], tab, kp, acc, sL + M.rs);
     if (M.has_u)
-      warp_nbr<KID>(lane, pi, qi, xi, vi, M.un, M.us, px, py, x, spq[w][1], sxv[w][1], tab, kp, acc, sD + M.us);
-    if (vi) {
-      s0[M.xs + lane] = acc;
-      if (!M.has_l) sL[M.xs + lane] = 0.0;
-      if (!M.has_d) sD[M.xs + lane] = 0.0;
+      warp_nbr<KID, RPL>(lane, pi, qi, xi, M.un, M.us, px, py, x, snb[w], xnb[w], tab, kp, acc, sD + M.us);
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = lane + 32 * r;
+      if (i < M.m) {
+        s0[M.xs + i] = acc[r];
+        if (!M.has_l) sL[M.xs + i] = 0.0;
+        if (!M.has_d) sD[M.xs + i] = 0.0;
+      }
     }
   }
 }
@@ -1224,6 +1241,9 @@ void finalize_schedule(Handle& h) {
     auto size_of = [&](int64_t lf) { return h.leaf_start[(size_t)lf + 1] - h.leaf_start[(size_t)lf]; };
     auto served = [&](int64_t lf) { return lf >= h.leaf_begin && lf < h.leaf_end; };
     std::vector<int32_t> fast, gen, wlist;
+    // leaves up to warp_max points go to the warp-per-leaf kernels (RPL = ceil(m / 32)); the
+    // CTA kernels keep larger leaves (H2D_P2P_WARP_MAX: diagnostics override, <= 96)
+    const int warp_max = getenv("H2D_P2P_WARP_MAX") ? std::min(96, atoi(getenv("H2D_P2P_WARP_MAX"))) : kWarpLeaf;
     for (int64_t lf = h.leaf_begin; lf < h.leaf_end; ++lf) {
       const uint32_t cx = compact((uint32_t)lf), cy = compact((uint32_t)lf >> 1);
       bool served_all = true, small_nbrs = true;
@@ -1239,7 +1259,7 @@ void finalize_schedule(Handle& h) {
       nb(cy > 0, cx, cy - 1, false);
       // warp path: <= 32-point leaves (any neighbour size); CTA fast path: three tiles
       // <= kSymTile points; both need a distance kernel and the whole near field served
-      if (dist && served_all && size_of(lf) <= kWarpLeaf) wlist.push_back((int32_t)lf);
+      if (dist && served_all && size_of(lf) <= warp_max) wlist.push_back((int32_t)lf);
       else if (dist && served_all && small_nbrs && size_of(lf) <= kSymTile) fast.push_back((int32_t)lf);
       else gen.push_back((int32_t)lf);
     }
@@ -1256,6 +1276,13 @@ void finalize_schedule(Handle& h) {
       }
       wlist.clear();
     }
+    std::stable_sort(wlist.begin(), wlist.end(), [&](int32_t a, int32_t b) {
+      return (size_of(a) + 31) / 32 < (size_of(b) + 31) / 32;
+    });
+    for (int r = 0; r < 3; ++r)
+      h.n_p2p_warp_rpl[r] = std::count_if(wlist.begin(), wlist.end(), [&](int32_t lf) {
+        return std::max<int64_t>(1, (size_of(lf) + 31) / 32) == r + 1;
+      });
     h.n_p2p_warp = (int64_t)wlist.size();
     h.release(h.d_p2p_warp);
     h.d_p2p_warp = h.alloc<int32_t>(wlist.size());
@@ -1454,16 +1481,27 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
       H2D_LAUNCH_CHECK();
     }
     if (h.n_p2p_warp > 0) {
-      auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_warp_kernel<H2D_KERNEL_LOG>
-                : h.kp.id == H2D_KERNEL_IMQ ? p2p_warp_kernel<H2D_KERNEL_IMQ>
-                : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_warp_kernel<H2D_KERNEL_ONE_OVER_R>
-                : h.kp.id == H2D_KERNEL_RBF_PHI1 ? p2p_warp_kernel<H2D_KERNEL_RBF_PHI1>
-                                                 : p2p_warp_kernel<H2D_KERNEL_RBF_PHI2>;
-      H2D_CUDA(cudaMemsetAsync(h.d_counters + 4, 0, sizeof(int32_t), a));
-      const int grid = (int)std::min<int64_t>(h.num_sms, (h.n_p2p_warp + 7) / 8);
-      kfn<<<grid, 256, 0, a>>>(h.kappa, h.d_p2p_warp, (int)h.n_p2p_warp, h.d_counters + 4, h.d_leaf_start,
-                               h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear, h.d_ynear + h.n, h.d_ynear + 2 * h.n);
-      H2D_LAUNCH_CHECK();
+      int64_t off = 0;
+      for (int r = 0; r < 3; ++r) {
+        const int64_t cnt = h.n_p2p_warp_rpl[r];
+        if (cnt <= 0) continue;
+        auto pick = [&](auto rpl) -> decltype(&p2p_warp_kernel<H2D_KERNEL_LOG, 1>) {
+          constexpr int R = decltype(rpl)::value;
+          return h.kp.id == H2D_KERNEL_LOG ? p2p_warp_kernel<H2D_KERNEL_LOG, R>
+               : h.kp.id == H2D_KERNEL_IMQ ? p2p_warp_kernel<H2D_KERNEL_IMQ, R>
+               : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_warp_kernel<H2D_KERNEL_ONE_OVER_R, R>
+               : h.kp.id == H2D_KERNEL_RBF_PHI1 ? p2p_warp_kernel<H2D_KERNEL_RBF_PHI1, R>
+                                                : p2p_warp_kernel<H2D_KERNEL_RBF_PHI2, R>;
+        };
+        auto* kfn = r == 0 ? pick(std::integral_constant<int, 1>{})
+                  : r == 1 ? pick(std::integral_constant<int, 2>{}) : pick(std::integral_constant<int, 3>{});
+        H2D_CUDA(cudaMemsetAsync(h.d_counters + 4 + r, 0, sizeof(int32_t), a));
+        const int grid = (int)std::min<int64_t>(h.num_sms, (cnt + 7) / 8);
+        kfn<<<grid, 256, 0, a>>>(h.kappa, h.d_p2p_warp + off, (int)cnt, h.d_counters + 4 + r, h.d_leaf_start,
+                                 h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear, h.d_ynear + h.n, h.d_ynear + 2 * h.n);
+        H2D_LAUNCH_CHECK();
+        off += cnt;
+      }
     }
     record(h, 7, a);
     H2D_CUDA(cudaEventRecord(h.ev_join, a));

@@ -257,6 +257,7 @@ struct Handle {
   int64_t n_abig = 0, n_bbig = 0;         // stage A / B items on the ring (the rest: small-item kernels)
   int32_t* d_p2p_warp = nullptr;          // <= 32-point leaves of the warp-per-leaf P2P kernel
   int64_t n_p2p_warp = 0;
+  int64_t n_p2p_warp_rpl[3] = {0, 0, 0};  // warp-kernel leaves with 1 / 2 / 3 rows per lane
   // symmetric apply (symmetric build on a single-rank handle, R23): A' over the
   // first-side V box panels -> t1; B' over the first-side U box panels -> t2 (= t) and the
   // per-level row dots y1 = U t1; C' = stage B over the second-side leaf panels with t2
