@@ -49,6 +49,11 @@ def parse():
                     help="informational: build and time rank G's slice of a --slice-world partition "
                          "on this one GPU, full x resident (per-GPU compute of the multi-GPU run)")
     ap.add_argument("--slice-world", type=int, default=8)
+    ap.add_argument("--leaf-weights", default=None,
+                    help="rank-slice mode: .npy of per-leaf loads for the partition (hodlr2d_leaf_costs "
+                         "summed over the slices of a first run)")
+    ap.add_argument("--dump-leaf-costs", default=None,
+                    help="rank-slice mode: save this slice's hodlr2d_leaf_costs to this .npy")
     ap.add_argument("--mode", default="matvec", choices=["matvec", "gmres"],
                     help="gmres: the paper's RBF application (P:1020-1048) at --grid-m^2 Chebyshev "
                          "points, informational line with T_I / T_G (paper values as context)")
@@ -535,12 +540,15 @@ def run_rank_slice(args, cfg):
     stream = torch.cuda.current_stream()
     pts = W.config_points(cfg)
     t0 = time.time()
+    lw = np.load(args.leaf_weights) if args.leaf_weights else None
     op = h2d.Hodlr2d.build(torch.from_numpy(pts).cuda(), cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c,
                            scale=cfg.scale, shift=cfg.shift, box_lo=cfg.box_lo, box_side=cfg.box_side,
-                           world=P, rank=g, stream=stream.cuda_stream)
+                           world=P, rank=g, stream=stream.cuda_stream, leaf_weights=lw)
     torch.cuda.synchronize()
     build_s = time.time() - t0
     inf = op.info()
+    if args.dump_leaf_costs:
+        np.save(args.dump_leaf_costs, op.leaf_costs())
     perm, _ = op.tree()
     nx = min(args.steps + args.warmup, 8)
     xs = [torch.from_numpy(np.ascontiguousarray(W.config_x(cfg, k)[perm])).cuda() for k in range(nx)]
@@ -563,6 +571,7 @@ def run_rank_slice(args, cfg):
     peak, peak_kind = peaks()
     gather_ms = 8.0 * cfg.n * (P - 1) / P / 770e9 * 1e3
     line = {"mode": "rank_slice", "config": config_dict(cfg, P), "slice_world": P, "rank": g,
+            "partition": "measured leaf costs (--leaf-weights)" if lw is not None else "geometric weight",
             "rows": [inf["row_begin"], inf["row_end"]], "build_seconds": round(build_s, 2),
             "ms_per_matvec_compute": ms, "steps": args.steps, "warmup": args.warmup,
             "stage_ms_per_matvec": {k: round(v / max(cnt, 1), 4) for k, v in st.items()},

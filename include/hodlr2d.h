@@ -99,6 +99,10 @@ typedef struct {
   int symmetric;          /* 1 -> one ACA per unordered pair {X, Y}, X < Y in Morton order;
                              block (Y, X) := V U^T (the paper's symmetric setting, P:61;
                              halves the ACA work, exactly symmetric operator, R23)  (def 0) */
+  const double* leaf_weights; /* world > 1: host array of 4^kappa per-leaf loads (the same on
+                             every rank) replacing the geometric weight of the Morton-range
+                             partition — e.g. the sum over ranks of hodlr2d_leaf_costs from a
+                             first build; kappa must match.  Not copied.     (default NULL) */
 } hodlr2d_options;
 
 #define H2D_MAX_LEVELS 16
@@ -227,12 +231,23 @@ int hodlr2d_stage_times(hodlr2d_t h, double* ms, int64_t* count, int reset);
 /* Enable / disable stage timing after the build. */
 int hodlr2d_set_timing(hodlr2d_t h, int on);
 
+/* Measured load of the handle's served leaves, for a load-balanced re-partition: costs
+ * (host, 4^kappa entries) receives for every served leaf L the algorithmic bytes of one
+ * matvec attributable to it — 8 |L| (sum over L's ancestors X of the U columns of X plus
+ * the V columns of X's column box) + 24 |L| — and 0 for leaves the handle does not serve.
+ * Summed over the ranks of a world it is the leaf_weights option of a rebuild.  Host
+ * computation from the packed layout (no device work). */
+int hodlr2d_leaf_costs(hodlr2d_t h, double* costs);
+
 /* Host-only helper (no device work; callable without a GPU): the Morton-range partition
  * every rank of a world uses.  leaf_start: the tree's 4^kappa + 1 leaf
  * offsets (see hodlr2d_copy_tree); n = leaf_start[4^kappa].  Rank r serves leaves
  * [*leaf_begin, *leaf_end): contiguous Morton ranges cut at the quantiles r / world of the
  * per-leaf load w(L) = |L| (1 + sum over L's ancestors X of |I_X|) — rows times the blocks
- * they meet, the geometric part of Eq. eq:par's per-node load. */
+ * they meet, the geometric part of Eq. eq:par's per-node load — each cut
+ * snapped to a coarse box boundary when that shifts at most 3 % (level 1) / 4 % (level 2) /
+ * 4x less per finer level of a rank's share (a cut inside a box makes both ranks stream
+ * the V panels of all its partners). */
 int hodlr2d_partition(const int32_t* leaf_start, int kappa, int world, int rank,
                       int64_t* leaf_begin, int64_t* leaf_end);
 

@@ -40,7 +40,7 @@ ABI_FUNCTIONS = (
     "hodlr2d_matvec_ex", "hodlr2d_get_info", "hodlr2d_copy_tree", "hodlr2d_copy_lists",
     "hodlr2d_num_blocks", "hodlr2d_copy_ranks", "hodlr2d_copy_block", "hodlr2d_load_factors",
     "hodlr2d_save_factors", "hodlr2d_stage_times", "hodlr2d_set_timing", "hodlr2d_destroy",
-    "hodlr2d_last_error", "hodlr2d_partition", "hodlr2d_gmres", "hodlr2d_matvec_multi",
+    "hodlr2d_last_error", "hodlr2d_partition", "hodlr2d_gmres", "hodlr2d_matvec_multi", "hodlr2d_leaf_costs",
 )
 
 
@@ -54,7 +54,7 @@ class Options(C.Structure):
         ("stream", C.c_void_p), ("world", C.c_int), ("rank", C.c_int),
         ("row_begin", C.c_int64), ("row_end", C.c_int64),
         ("aca_scratch_bytes", C.c_size_t), ("timing", C.c_int), ("skip_aca", C.c_int),
-        ("symmetric", C.c_int),
+        ("symmetric", C.c_int), ("leaf_weights", C.c_void_p),
     ]
 
 
@@ -126,6 +126,7 @@ def lib() -> C.CDLL:
             L.hodlr2d_partition.argtypes = [vp, i, i, i, C.POINTER(i64), C.POINTER(i64)]
             L.hodlr2d_gmres.argtypes = [vp, vp, vp, d, i, i, C.POINTER(i), C.POINTER(d)]
             L.hodlr2d_matvec_multi.argtypes = [vp, vp, vp, i, i]
+            L.hodlr2d_leaf_costs.argtypes = [vp, vp]
             _lib = L
     return _lib
 
@@ -181,8 +182,11 @@ class Hodlr2d:
     def build(cls, points, kernel="log", leaf_size=64, aca_tol=1e-10, *, c=1.0, scale=1.0,
               shift=0.0, box_lo=(0.0, 0.0), box_side=0.0, depth=-1, max_rank=128,
               aca_consecutive=3, aca_trim=3, test_rank=1, stream=None, world=1, rank=0,
-              row_range=None, aca_scratch_bytes=0, timing=False, skip_aca=False, symmetric=False):
-        """hodlr2d_build_ex.  ``points``: (N, 2) float64 torch tensor (CUDA or CPU) or numpy array."""
+              row_range=None, aca_scratch_bytes=0, timing=False, skip_aca=False, symmetric=False,
+              leaf_weights=None):
+        """hodlr2d_build_ex.  ``points``: (N, 2) float64 torch tensor (CUDA or CPU) or numpy array.
+        ``leaf_weights``: host float64 array of 4^kappa per-leaf loads for the world partition
+        (e.g. the sum over ranks of ``leaf_costs()`` of a first build)."""
         kid = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
         o = default_options()
         o.c, o.scale, o.shift = c, scale, shift
@@ -205,6 +209,10 @@ class Hodlr2d:
         o.timing = int(bool(timing))
         o.skip_aca = int(bool(skip_aca))
         o.symmetric = int(bool(symmetric))
+        lw = None
+        if leaf_weights is not None:
+            lw = np.ascontiguousarray(leaf_weights, dtype=np.float64)
+            o.leaf_weights = lw.ctypes.data
         n = points.shape[0]
         h = C.c_void_p()
         rc = _check(lib().hodlr2d_build_ex(_ptr(points), n, kid, leaf_size, aca_tol, C.byref(o), C.byref(h)))
@@ -299,6 +307,14 @@ class Hodlr2d:
         _check(lib().hodlr2d_matvec_ex(self._h, x_ptr, y_ptr, order))
 
     # -------------------------------------------------------------- inspection
+    def leaf_costs(self):
+        """hodlr2d_leaf_costs: per-leaf algorithmic bytes of this handle's served leaves
+        (float64, 4^kappa entries, zero elsewhere)."""
+        kappa = self.info()["kappa"]
+        out = np.zeros(1 << (2 * kappa), dtype=np.float64)
+        _check(lib().hodlr2d_leaf_costs(self._h, out.ctypes.data))
+        return out
+
     def info(self) -> dict:
         inf = Info()
         _check(lib().hodlr2d_get_info(self._h, C.byref(inf)))

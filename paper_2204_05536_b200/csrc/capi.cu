@@ -185,30 +185,51 @@ static uint32_t compact_host(uint32_t v) {
 // the factor bytes (ranks are unknown before ACA).  Boxes near the domain boundary have
 // fewer partners, so equal point shares left the centre-facing ranks ~12 % heavier (C5).
 // The cut before rank r is the first leaf whose load prefix reaches r / world of the total.
+// Cut position of rank boundary r on the prefix sums pre[] of the per-leaf loads, snapped to
+// a coarse box boundary when that costs little balance: a cut inside a level-l box makes
+// both neighbouring ranks stream the whole V panels of that box's partners (stage A needs
+// V^T x over every row of the column box), which is ~8 % of a rank's bytes for a level-2
+// box at C5 (measured: the ranks cutting level-2 boxes read 50.5 vs 46.8 GB).  Tolerance:
+// 3 % of a share at level 1, 4 % at level 2, 4x less per finer level.
+static int64_t snapped_cut(const std::vector<double>& pre, int kappa, int world, int r) {
+  const int64_t nleaf = (int64_t)pre.size() - 1;
+  if (r <= 0) return 0;
+  if (r >= world) return nleaf;
+  const double share = pre[(size_t)nleaf] / world, target = share * r;
+  const int64_t c = (int64_t)(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
+  for (int l = 1; l <= std::min(kappa, 5); ++l) {
+    const int64_t B = (int64_t)1 << (2 * (kappa - l));
+    const double tol = (l == 1 ? 0.03 : 0.04 / (double)((int64_t)1 << (2 * (l - 2)))) * share;
+    const int64_t lo = c / B * B, hi = std::min(nleaf, lo + B);
+    const int64_t sn = std::fabs(pre[(size_t)lo] - target) <= std::fabs(pre[(size_t)hi] - target) ? lo : hi;
+    if (std::fabs(pre[(size_t)sn] - target) <= tol) return sn;
+  }
+  return std::min(c, nleaf);
+}
+
 static void partition_leaves(const int32_t* ls, int kappa, int world, int rank, int64_t* lb,
-                             int64_t* le) {
+                             int64_t* le, const double* weights = nullptr) {
   const int64_t nleaf = (int64_t)1 << (2 * kappa);
-  std::vector<std::vector<uint8_t>> cnt((size_t)kappa + 1);
-  for (int l = 1; l <= kappa; ++l) {
-    const int64_t nbox = (int64_t)1 << (2 * l);
-    cnt[(size_t)l].resize((size_t)nbox);
-    for (int64_t b = 0; b < nbox; ++b)
-      cnt[(size_t)l][(size_t)b] = (uint8_t)ilist_count(l, (int)compact_host((uint32_t)b), (int)compact_host((uint32_t)b >> 1));
-  }
   std::vector<double> pre((size_t)nleaf + 1, 0.0);
-  for (int64_t L = 0; L < nleaf; ++L) {
-    int s = 1;
-    for (int l = 1; l <= kappa; ++l) s += cnt[(size_t)l][(size_t)(L >> (2 * (kappa - l)))];
-    pre[(size_t)L + 1] = pre[(size_t)L] + (double)(ls[L + 1] - ls[L]) * s;
+  if (weights) {   // measured loads (hodlr2d_leaf_costs summed over ranks)
+    for (int64_t L = 0; L < nleaf; ++L) pre[(size_t)L + 1] = pre[(size_t)L] + std::max(0.0, weights[L]);
+  } else {
+    std::vector<std::vector<uint8_t>> cnt((size_t)kappa + 1);
+    for (int l = 1; l <= kappa; ++l) {
+      const int64_t nbox = (int64_t)1 << (2 * l);
+      cnt[(size_t)l].resize((size_t)nbox);
+      for (int64_t b = 0; b < nbox; ++b)
+        cnt[(size_t)l][(size_t)b] =
+            (uint8_t)ilist_count(l, (int)compact_host((uint32_t)b), (int)compact_host((uint32_t)b >> 1));
+    }
+    for (int64_t L = 0; L < nleaf; ++L) {
+      int s = 1;
+      for (int l = 1; l <= kappa; ++l) s += cnt[(size_t)l][(size_t)(L >> (2 * (kappa - l)))];
+      pre[(size_t)L + 1] = pre[(size_t)L] + (double)(ls[L + 1] - ls[L]) * s;
+    }
   }
-  auto cut = [&](int r) {
-    if (r <= 0) return (int64_t)0;
-    if (r >= world) return nleaf;
-    const double target = pre[(size_t)nleaf] * r / world;
-    return (int64_t)(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
-  };
-  *lb = std::min(cut(rank), nleaf);
-  *le = std::min(cut(rank + 1), nleaf);
+  *lb = snapped_cut(pre, kappa, world, rank);
+  *le = snapped_cut(pre, kappa, world, rank + 1);
 }
 
 static void set_partition(Handle& h) {
@@ -224,12 +245,12 @@ static void set_partition(Handle& h) {
     if (h.opts.row_end >= h.n) h.leaf_end = nleaf;
   } else {
     partition_leaves(h.leaf_start.data(), h.kappa, h.opts.world, h.opts.rank, &h.leaf_begin,
-                     &h.leaf_end);
+                     &h.leaf_end, h.opts.leaf_weights);
     // every rank's rows: layout of the padded all-gather (H2D_ORDER_GATHERED)
     h.rank_rows.assign((size_t)h.opts.world + 1, 0);
     for (int r = 0; r < h.opts.world; ++r) {
       int64_t lb = 0, le = 0;
-      partition_leaves(h.leaf_start.data(), h.kappa, h.opts.world, r, &lb, &le);
+      partition_leaves(h.leaf_start.data(), h.kappa, h.opts.world, r, &lb, &le, h.opts.leaf_weights);
       h.rank_rows[(size_t)r] = h.leaf_start[(size_t)lb];
       h.rank_rows[(size_t)r + 1] = h.leaf_start[(size_t)le];
       h.gather_stride = std::max<int64_t>(h.gather_stride, h.leaf_start[(size_t)le] - h.leaf_start[(size_t)lb]);
@@ -503,6 +524,7 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
   if (tmp) H2D_CUDA(cudaFreeAsync(tmp, h.stream));
   build_lists(h);
   set_partition(h);
+  h.opts.leaf_weights = nullptr;   // caller-owned, read only by the partition above
   // symmetric apply (R23): symmetric build on a single-rank handle (the multi-rank row
   // partitions keep the directed panels; stage B' needs every row of a row box)
   h.symapply = opts->symmetric && h.row_begin == 0 && h.row_end == h.n && h.kappa >= 1 &&
@@ -852,6 +874,27 @@ int hodlr2d_destroy(hodlr2d_t H) {
 }
 
 const char* hodlr2d_last_error(void) { return g_last_error.c_str(); }
+
+int hodlr2d_leaf_costs(hodlr2d_t H, double* costs) {
+  H2D_TRY
+  if (!H || !costs) throw Error{H2D_EINVAL, "null argument"};
+  Handle& h = H->h;
+  const int64_t nleaf = (int64_t)1 << (2 * h.kappa);
+  for (int64_t L = 0; L < nleaf; ++L) costs[L] = 0.0;
+  for (int64_t L = h.leaf_begin; L < h.leaf_end; ++L) {
+    const double rows = (double)(h.leaf_start[(size_t)L + 1] - h.leaf_start[(size_t)L]);
+    double cols = 0.0;
+    for (int l = 1; l <= h.kappa; ++l) {
+      const Level& Lv = h.levels[(size_t)l];
+      const int64_t X = L >> (2 * (h.kappa - l));
+      if (!Lv.ucolbase.empty()) cols += Lv.ucolbase[(size_t)X + 1] - Lv.ucolbase[(size_t)X];
+      if (!Lv.vR.empty()) cols += Lv.vR[(size_t)X];
+    }
+    costs[L] = 8.0 * rows * cols + 24.0 * rows;
+  }
+  return H2D_OK;
+  H2D_CATCH
+}
 
 int hodlr2d_partition(const int32_t* leaf_start, int kappa, int world, int rank,
                       int64_t* leaf_begin, int64_t* leaf_end) {

@@ -51,7 +51,8 @@ def test_struct_layouts_match_c(h2d, tmp_path):
 int main(void) {{
   printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(hodlr2d_options),
          sizeof(hodlr2d_info), offsetof(hodlr2d_options, stream), offsetof(hodlr2d_options, aca_scratch_bytes),
-         offsetof(hodlr2d_options, symmetric), offsetof(hodlr2d_info, rank_hist),
+         offsetof(hodlr2d_options, symmetric) + 1000000 * offsetof(hodlr2d_options, leaf_weights),
+         offsetof(hodlr2d_info, rank_hist),
          offsetof(hodlr2d_info, matvec_bytes), offsetof(hodlr2d_info, device_bytes),
          offsetof(hodlr2d_info, symmetric_apply), offsetof(hodlr2d_info, p2p_launches),
          offsetof(hodlr2d_info, p2p_leaves), offsetof(hodlr2d_info, apply_launches),
@@ -62,7 +63,8 @@ int main(void) {{
     subprocess.check_call(["gcc", "-o", str(exe), str(prog)])
     vals = list(map(int, subprocess.check_output([str(exe)]).split()))
     O, I = h2d.Options, h2d.Info
-    assert vals == [C.sizeof(O), C.sizeof(I), O.stream.offset, O.aca_scratch_bytes.offset, O.symmetric.offset,
+    assert vals == [C.sizeof(O), C.sizeof(I), O.stream.offset, O.aca_scratch_bytes.offset,
+                    O.symmetric.offset + 1000000 * O.leaf_weights.offset,
                     I.rank_hist.offset, I.matvec_bytes.offset, I.device_bytes.offset, I.symmetric_apply.offset,
                     I.p2p_launches.offset, I.p2p_leaves.offset, I.apply_launches.offset, I.small_items.offset]
 

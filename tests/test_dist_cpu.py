@@ -105,8 +105,8 @@ def test_partition_covers_all_leaves_contiguously():
         assert ranges[0][0] == 0 and ranges[-1][1] == 1 << (2 * kappa)
         assert all(ranges[r][1] == ranges[r + 1][0] for r in range(world - 1))
         # equal shares of the per-leaf load w(L) = |L| (1 + sum over L's ancestors X of |I_X|)
-        # up to one leaf; |I_X| from the oracle's literal lists (Defs 4.1-4.5), not the
-        # library's closed form
+        # up to the coarse-box snap (each cut moves by <= 4 % of a share) and one leaf;
+        # |I_X| from the oracle's literal lists (Defs 4.1-4.5), not the library's closed form
         sz = np.diff(ls).astype(np.float64)
         s = np.ones(1 << (2 * kappa))
         for l in range(1, kappa + 1):
@@ -114,6 +114,6 @@ def test_partition_covers_all_leaves_contiguously():
             s += np.repeat(np.diff(off), 1 << (2 * (kappa - l)))
         w = sz * s
         loads = [w[a:b].sum() for a, b in ranges]
-        assert max(loads) - min(loads) <= 2 * w.max()
+        assert max(loads) - min(loads) <= 0.08 * w.sum() / world + 2 * w.max()
         rows = [int(ls[b]) - int(ls[a]) for a, b in ranges]
         assert max(rows) <= 1.15 * cfg.n / world        # still close to equal point shares
