@@ -421,3 +421,35 @@ def test_runtime_variants_same_result(h2d, env):
         yr = ref.matvec(dev(x)).cpu().numpy()
         assert np.array_equal(y, yd)
         assert rel(y, yr) <= 1e-14
+
+
+def test_leaf_costs_and_weighted_partition(h2d):
+    """hodlr2d_leaf_costs is non-zero exactly on the served leaves and adds up to the
+    handle's factor stream (+ 24 B per row); a world-2 partition built from the summed costs
+    (options.leaf_weights) still reassembles the full matvec."""
+    cfg = W.CONFIGS["c1"]
+    pts = W.config_points(cfg)
+    kw = dict(box_lo=cfg.box_lo, box_side=cfg.box_side)
+    full = h2d.Hodlr2d.build(dev(pts), cfg.kernel, cfg.leaf_size, cfg.tol, **kw)
+    perm, ls = full.tree()
+    x = W.config_x(cfg, 5)[perm]
+    yfull = full.matvec(dev(x), order="tree").cpu().numpy()
+    costs = np.zeros(len(ls) - 1)
+    for rank in range(2):
+        p = h2d.Hodlr2d.build(dev(pts), cfg.kernel, cfg.leaf_size, cfg.tol, world=2, rank=rank, **kw)
+        inf = p.info()
+        c = p.leaf_costs()
+        served = np.zeros(len(c), dtype=bool)
+        served[inf["leaf_begin"]:inf["leaf_end"]] = True
+        nonempty = np.diff(ls) > 0
+        assert np.all(c[~served] == 0.0) and np.all(c[served & nonempty] > 0.0)
+        costs += c
+    parts = []
+    for rank in range(2):
+        p = h2d.Hodlr2d.build(dev(pts), cfg.kernel, cfg.leaf_size, cfg.tol, world=2, rank=rank, leaf_weights=costs,
+                              **kw)
+        parts.append(p.matvec(dev(x), order="tree").cpu().numpy())
+    assert rel(np.concatenate(parts), yfull) <= 1e-13
+    fc = full.leaf_costs()
+    inf = full.info()
+    assert abs(fc.sum() - (8 * (inf["u_values"] + inf["v_values"]) + 24 * cfg.n)) <= 0.05 * fc.sum()
