@@ -137,8 +137,9 @@ typedef struct {
   int symmetric_apply;       /* 1 -> matvecs run the symmetric three-pass apply (R23):
                                 stage slot 1 = A' + B', slot 2 = C'; stageA_bytes /
                                 stageB_bytes then count those passes                  */
-  int p2p_launches;          /* near-field kernels per matvec: warp-per-leaf (<= 32-point
-                                leaves), CTA fast path, generic (1..3)                 */
+  int p2p_launches;          /* near-field kernels per matvec: warp-per-leaf (one per rows-
+                                per-lane class 1..3, leaves <= 96 points), CTA fast path,
+                                generic (1..5)                                         */
   int64_t p2p_leaves[3];     /* leaves on the warp / fast / generic P2P paths          */
   int apply_launches;        /* low-rank apply kernels per matvec: stage A / B rings and
                                 their small-item (warp-per-item) kernels, B' (symmetric) */

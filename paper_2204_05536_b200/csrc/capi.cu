@@ -718,7 +718,8 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   info->p2p_leaves[0] = h.n_p2p_warp;
   info->p2p_leaves[1] = h.n_p2p_fast;
   info->p2p_leaves[2] = h.n_p2p_gen;
-  info->p2p_launches = (h.n_p2p_warp > 0) + (h.n_p2p_fast > 0) + (h.n_p2p_gen > 0);
+  info->p2p_launches = (h.n_p2p_warp_rpl[0] > 0) + (h.n_p2p_warp_rpl[1] > 0) + (h.n_p2p_warp_rpl[2] > 0) +
+                       (h.n_p2p_fast > 0) + (h.n_p2p_gen > 0);
   info->small_items[0] = h.n_aitems - h.n_abig;
   info->small_items[1] = h.n_bitems - h.n_bbig;
   info->apply_launches = (h.n_abig > 0) + (h.n_aitems > h.n_abig) + (h.n_bbig > 0) + (h.n_bitems > h.n_bbig) +
