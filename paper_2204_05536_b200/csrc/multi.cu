@@ -70,15 +70,16 @@ __device__ void mA_producer(PipeSmem<NS, SD, SV>& S, const AItem* __restrict__ i
         h.b = Wp;
         h.c = it.out;
         h.d = it.ritem;
-        const uint32_t bytes = (uint32_t)rows * (uint32_t)Wp * 8u;
-        mbar_arrive_expect_tx(&S.full[stage], bytes);
+        const uint32_t bytes = (uint32_t)rows * (uint32_t)Wp * 8u, xbytes = (uint32_t)rows * NR * 8u;
+        mbar_arrive_expect_tx(&S.full[stage], bytes + xbytes);
         if (bytes && contiguous) bulk_g2s(S.ring[stage], V + (int64_t)r0 * it.Rp, bytes, &S.full[stage], pol);
+        // the rows' x records are contiguous (x_m[s][NR]): one bulk copy, not rows x NR
+        // 8-byte cp.async from one producer warp (the producer was the stage's bottleneck)
+        if (xbytes) bulk_g2s_keep(S.vec[stage], xm + (it.x_off + r0) * NR, xbytes, &S.full[stage]);
       }
       if (!contiguous)
         for (int r = lane; r < rows; r += 32)
           bulk_g2s(S.ring[stage] + r * Wp, V + (int64_t)(r0 + r) * it.Rp, (uint32_t)Wp * 8u, &S.full[stage], pol);
-      const double* xs = xm + (it.x_off + r0) * NR;
-      for (int e = lane; e < rows * NR; e += 32) cp_async8(&S.vec[stage][e], xs + e);
       cp_async_arrive_noinc(&S.full[stage]);
       if (++stage == NS) { stage = 0; phase ^= 1; }
       r0 += rows;
@@ -993,16 +994,17 @@ __device__ void mB_producer(PipeSmem<NS, SD, SV>& S, const BItem* __restrict__ i
           h.a = it.rows;
           h.b = rowsp;
           h.c = it.yrow;
-          mbar_arrive_expect_tx(&S.full[stage], (uint32_t)cols * (uint32_t)rowsp * 8u);
+          const uint32_t tbytes = (uint32_t)cols * NR * 8u;
+          mbar_arrive_expect_tx(&S.full[stage], (uint32_t)cols * (uint32_t)rowsp * 8u + tbytes);
           if (whole)
             bulk_g2s(S.ring[stage], Ub + (int64_t)c0 * mLp, (uint32_t)cols * (uint32_t)mLp * 8u, &S.full[stage], pol);
+          // the columns' t records are contiguous (t[index][NR]): one bulk copy
+          bulk_g2s_keep(S.vec[stage], tb + (int64_t)c0 * NR, tbytes, &S.full[stage]);
         }
         if (!whole)
           for (int c = lane; c < cols; c += 32)
             bulk_g2s(S.ring[stage] + c * rowsp, Ub + (int64_t)(c0 + c) * mLp + it.r0, (uint32_t)rowsp * 8u,
                      &S.full[stage], pol);
-        const double* ts = tb + (int64_t)c0 * NR;
-        for (int e = lane; e < cols * NR; e += 32) cp_async8(&S.vec[stage][e], ts + e);
         cp_async_arrive_noinc(&S.full[stage]);
         if (++stage == NS) { stage = 0; phase ^= 1; }
         first = false;
