@@ -782,12 +782,12 @@ __device__ void mD_producer(PipeSmem<NS, SD, SV>& S, const AItem* __restrict__ i
         h.pad = it.level;
         h.e = (int32_t)(it.x_off + r0);
         const uint32_t ub = (uint32_t)rows * (uint32_t)Wp * 8u, tb = done ? 0u : (uint32_t)Wp * NR * 8u;
-        mbar_arrive_expect_tx(&S.full[stage], ub + tb);
+        const uint32_t xb = (uint32_t)rows * NR * 8u;
+        mbar_arrive_expect_tx(&S.full[stage], ub + tb + xb);
         if (ub) bulk_g2s(S.ring[stage], U + (int64_t)r0 * Wp, ub, &S.full[stage], pol);
         if (tb) bulk_g2s(S.ring[stage] + rows * Wp, t1m + it.t1_off * NR, tb, &S.full[stage], pol);
+        if (xb) bulk_g2s_keep(S.vec[stage], xm + (it.x_off + r0) * NR, xb, &S.full[stage]);   // x records
       }
-      const double* xs = xm + (it.x_off + r0) * NR;
-      for (int e = lane; e < rows * NR; e += 32) cp_async8(&S.vec[stage][e], xs + e);
       cp_async_arrive_noinc(&S.full[stage]);
       if (++stage == NS) { stage = 0; phase ^= 1; }
       r0 += rows;
