@@ -432,7 +432,7 @@ def run_ours(args, cfg):
             "gpu_launches": args.steps * launches_per_matvec(inf, world),
             "clocks": csum,
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:   # the contract: rank 0 at N = 1 only
             try:
                 line["cpu_baseline"] = cpu_baseline(cfg)
             except Exception as ex:  # the GPU number stands on its own
