@@ -247,3 +247,24 @@ def test_symmetric_gmres(h2d):
     assert rr <= 1e-10 and its < 40
     assert rel(xs.cpu().numpy(), lam) <= 1e-9
     assert rel(xs.cpu().numpy(), xd.cpu().numpy()) <= 1e-9
+
+
+def test_symmetric_partitioned_multi_rhs(h2d):
+    """A symmetric build on a world-2 partition keeps the directed panels (no symmetric
+    apply across ranks); its multi-RHS path (16 + 4 + 1 vectors, TREE order) equals its
+    single-vector matvecs, and the two ranks reassemble the single-rank symmetric operator."""
+    cfg = W.CONFIGS["c1"]
+    pts = W.config_points(cfg)
+    full = build(h2d, cfg, pts)
+    perm, _ = full.tree()
+    X = np.stack([W.config_x(cfg, k)[perm] for k in range(21)])
+    Yfull = full.matvec_multi(dev(X), order="tree").cpu().numpy()
+    parts = []
+    for rank in range(2):
+        p = build(h2d, cfg, pts, world=2, rank=rank)
+        assert p.info()["symmetric_apply"] == 0
+        Y = p.matvec_multi(dev(X), order="tree").cpu().numpy()
+        for k in (0, 15, 16, 20):
+            assert rel(Y[k], p.matvec(dev(X[k]), order="tree").cpu().numpy()) <= 1e-13, k
+        parts.append(Y)
+    assert rel(np.concatenate(parts, axis=1), Yfull) <= 1e-12
