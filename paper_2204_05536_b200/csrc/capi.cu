@@ -608,6 +608,9 @@ int hodlr2d_gmres(hodlr2d_t H, const double* b, double* x, double tol, int resta
   H2D_TRY
   if (!H || !b || !x) throw Error{H2D_EINVAL, "null argument"};
   Handle& h = H->h;
+  // argument checks before any staging allocation (nothing to release on these errors)
+  if (h.row_begin != 0 || h.row_end != h.n) throw Error{H2D_EINVAL, "GMRES needs a single-rank handle"};
+  if (!(tol > 0.0) || restart < 1 || max_iter < 1) throw Error{H2D_EINVAL, "bad GMRES parameters"};
   cudaStream_t s = h.stream;
   const bool bdev = is_device_ptr(b), xdev = is_device_ptr(x);
   const double* db = b;

@@ -147,3 +147,22 @@ def test_paper_table_rbf_phi1_row_250000_gpu(h2d):
     lam_hat, its, rr = op.gmres(op.matvec(lam), tol=1e-10)
     assert rr < 1e-10 and its < 30
     assert float(torch.linalg.norm(lam_hat - lam) / torch.linalg.norm(lam)) < 1e-9
+
+
+def test_gpu_gmres_argument_errors(h2d):
+    """GMRES needs a single-rank handle and positive tol / restart / max_iter: H2D_EINVAL,
+    and the handle stays usable."""
+    pts = W.uniform_points(3000, 61)
+    kw = dict(box_lo=(-1, -1), box_side=2.0, shift=3000.0)
+    part = h2d.Hodlr2d.build(dev(pts), "log", 64, 1e-10, world=2, rank=0, **kw)
+    b = dev(W.random_vector(3000, 62))
+    with pytest.raises(h2d.Hodlr2dError) as e:
+        part.gmres(b, tol=1e-10)
+    assert e.value.code == h2d.H2D_EINVAL
+    op = h2d.Hodlr2d.build(dev(pts), "log", 64, 1e-10, **kw)
+    for kwargs in (dict(tol=0.0), dict(tol=1e-10, restart=0), dict(tol=1e-10, max_iter=0)):
+        with pytest.raises(h2d.Hodlr2dError) as e:
+            op.gmres(b, **kwargs)
+        assert e.value.code == h2d.H2D_EINVAL
+    x, its, rr = op.gmres(b, tol=1e-10)
+    assert rr <= 1e-10
