@@ -172,13 +172,16 @@ int hodlr2d_matvec(hodlr2d_t h, const double* x, double* y);
 int hodlr2d_matvec_ex(hodlr2d_t h, const double* x, double* y, int order);
 
 /* Y = A X for nrhs vectors at once (NEXT N2; the paper applies its matvec to ten input
- * vectors).  Vector k is X + k * N (length N) and Y + k * len_y; order =
- * H2D_ORDER_ORIGINAL (single-rank handles, len_y = N) or H2D_ORDER_TREE (x in TREE order,
- * y = the served rows, len_y = row_end - row_begin).  The factor panels are streamed once
- * per chunk of up to 8 vectors (chunks of 8, 4, 2; a last single vector takes the
- * hodlr2d_matvec path), so throughput in matvecs/s grows with nrhs until the FP64 pipes,
- * not HBM, bound it.  Host or device pointers; Y is overwritten.  Results equal nrhs
- * separate hodlr2d_matvec_ex calls up to rounding (different summation order). */
+ * vectors).  Vector k is X + k * len_x and Y + k * len_y; order =
+ * H2D_ORDER_ORIGINAL (single-rank handles, len_x = len_y = N), H2D_ORDER_TREE (x in TREE
+ * order, len_x = N, y = the served rows, len_y = row_end - row_begin) or
+ * H2D_ORDER_GATHERED (x = one padded all-gather buffer per vector, len_x = world *
+ * info.gather_stride; y as for TREE).  The factor panels are streamed once per chunk of up
+ * to 16 vectors (chunks of 16, 8, 4, 2; a last single vector takes the hodlr2d_matvec
+ * path; symmetric-apply handles: chunks of 8), so throughput in matvecs/s grows with nrhs
+ * until the FP64 pipes, not HBM, bound it.  Host or device pointers; Y is overwritten.
+ * Results equal nrhs separate hodlr2d_matvec_ex calls up to rounding (different
+ * summation order). */
 int hodlr2d_matvec_multi(hodlr2d_t h, const double* X, double* Y, int nrhs, int order);
 
 /* Solve A x = b with restarted GMRES(restart) accelerated by the HODLR2D matvec — the

@@ -571,9 +571,13 @@ int hodlr2d_matvec_multi(hodlr2d_t H, const double* X, double* Y, int nrhs, int 
   if (!H || !X || !Y) throw Error{H2D_EINVAL, "null argument"};
   if (nrhs < 1) throw Error{H2D_EINVAL, "nrhs < 1"};
   Handle& h = H->h;
-  if (order != H2D_ORDER_ORIGINAL && order != H2D_ORDER_TREE) throw Error{H2D_EINVAL, "bad order"};
+  if (order != H2D_ORDER_ORIGINAL && order != H2D_ORDER_TREE && order != H2D_ORDER_GATHERED)
+    throw Error{H2D_EINVAL, "bad order"};
+  if (order == H2D_ORDER_GATHERED && h.rank_rows.empty())
+    throw Error{H2D_EINVAL, "GATHERED order needs a world/rank partition"};
   cudaStream_t s = h.stream;
-  const int64_t xlen = h.n;
+  const bool gathered = order == H2D_ORDER_GATHERED;
+  const int64_t xlen = gathered ? h.gather_stride * h.opts.world : h.n;
   const int64_t ylen = order == H2D_ORDER_ORIGINAL ? h.n : h.row_end - h.row_begin;
   const bool xdev = is_device_ptr(X), ydev = is_device_ptr(Y);
   const double* dX = X;
@@ -588,13 +592,22 @@ int hodlr2d_matvec_multi(hodlr2d_t H, const double* X, double* Y, int nrhs, int 
     H2D_CUDA(cudaMallocAsync(&ty, (size_t)nrhs * ylen * sizeof(double), s));
     dY = ty;
   }
+  double* tg = nullptr;   // GATHERED: the vectors unpadded into TREE order
   try {
-    matvec_multi(h, dX, dY, nrhs, order);
+    if (gathered) {
+      H2D_CUDA(cudaMallocAsync(&tg, (size_t)nrhs * h.n * sizeof(double), s));
+      for (int k = 0; k < nrhs; ++k) unpad_gathered(h, dX + (int64_t)k * xlen, tg + (int64_t)k * h.n);
+      matvec_multi(h, tg, dY, nrhs, H2D_ORDER_TREE);
+    } else {
+      matvec_multi(h, dX, dY, nrhs, order);
+    }
   } catch (...) {
     if (tx) cudaFreeAsync(tx, s);
     if (ty) cudaFreeAsync(ty, s);
+    if (tg) cudaFreeAsync(tg, s);
     throw;
   }
+  if (tg) H2D_CUDA(cudaFreeAsync(tg, s));
   if (!ydev) d2h_ordered_sync(h, Y, dY, (size_t)nrhs * ylen * sizeof(double));
   if (tx) H2D_CUDA(cudaFreeAsync(tx, s));
   if (ty) H2D_CUDA(cudaFreeAsync(ty, s));

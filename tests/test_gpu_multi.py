@@ -126,3 +126,25 @@ def test_multi_clustered_chebyshev(h2d):
     Y = op.matvec_multi(dev(X)).cpu().numpy()
     for k in range(19):
         assert rel(Y[k], op.matvec(dev(X[k])).cpu().numpy()) <= 1e-13, k
+
+
+def test_multi_gathered_order(h2d):
+    """GATHERED order (one padded all-gather buffer per vector, NaN padding never read):
+    19 vectors on each rank of a world-2 partition equal the TREE-order multi-RHS matvec."""
+    cfg = W.CONFIGS["c1"]
+    pts, full = cfg_build(h2d, cfg)
+    perm, ls = full.tree()
+    kappa = full.info()["kappa"]
+    Xt = np.stack([W.config_x(cfg, k)[perm] for k in range(19)])
+    world = 2
+    ranges = [h2d.partition(ls, kappa, world, r) for r in range(world)]
+    rows = [(int(ls[a]), int(ls[b])) for a, b in ranges]
+    stride = max(b - a for a, b in rows)
+    Xg = np.full((19, world * stride), np.nan)
+    for r, (a, b) in enumerate(rows):
+        Xg[:, r * stride: r * stride + (b - a)] = Xt[:, a:b]
+    for r in range(world):
+        _, op = cfg_build(h2d, cfg, pts, world=world, rank=r)
+        Yg = op.matvec_multi(dev(Xg), order="gathered").cpu().numpy()
+        Yt = op.matvec_multi(dev(Xt), order="tree").cpu().numpy()
+        assert np.array_equal(Yg, Yt)
