@@ -1333,6 +1333,11 @@ void finalize_schedule(Handle& h) {
     H2D_CUDA(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
     H2D_CUDA(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
     H2D_CUDA(cudaEventCreateWithFlags(&h.ev_far, cudaEventDisableTiming));
+    H2D_CUDA(cudaEventCreateWithFlags(&h.ev_p2p_fork, cudaEventDisableTiming));
+    for (int k = 0; k < 3; ++k) {
+      H2D_CUDA(cudaStreamCreateWithPriority(&h.p2p_side[k], cudaStreamNonBlocking, lo_prio));
+      H2D_CUDA(cudaEventCreateWithFlags(&h.ev_p2p_side[k], cudaEventDisableTiming));
+    }
     // pipeline shape: 2 CTAs/SM with a 5-stage ring, or 1 CTA/SM with a 9-stage ring
     // (leaves room for two P2P CTAs per SM); H2D_PIPE_CTAS_PER_SM overrides the default.
     const char* env = getenv("H2D_PIPE_CTAS_PER_SM");
@@ -1453,16 +1458,32 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
   H2D_CUDA(cudaEventRecord(h.ev_fork, s));
   H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_fork, 0));
   H2D_CUDA(cudaStreamWaitEvent(a, h.ev_fork, 0));
+  // H2D_P2P_ONESTREAM=1 (diagnostics only): every P2P class on aux_stream, one after another
+  const char* env_one = getenv("H2D_P2P_ONESTREAM");
+  const bool p2p_one = env_one && atoi(env_one) == 1;
   auto p2p = [&]() {
     record(h, 6, a);
+    // the generic CTA leaves and the 3- and 2-row warp classes run on side streams: a class
+    // with a few dozen CTAs (the big leaves of a clustered input) no longer serialises the rest
+    bool forked[3] = {false, false, false};
+    auto side = [&](int k) -> cudaStream_t {
+      if (p2p_one) return a;
+      if (!forked[k]) {
+        if (!forked[0] && !forked[1] && !forked[2]) H2D_CUDA(cudaEventRecord(h.ev_p2p_fork, a));
+        H2D_CUDA(cudaStreamWaitEvent(h.p2p_side[k], h.ev_p2p_fork, 0));
+        forked[k] = true;
+      }
+      return h.p2p_side[k];
+    };
     if (h.n_p2p_gen > 0) {
+      cudaStream_t sg = side(0);
       auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_sym_kernel<H2D_KERNEL_LOG>
                 : h.kp.id == H2D_KERNEL_IMQ ? p2p_sym_kernel<H2D_KERNEL_IMQ>
                 : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_sym_kernel<H2D_KERNEL_ONE_OVER_R>
                 : h.kp.id == H2D_KERNEL_RBF_PHI1 ? p2p_sym_kernel<H2D_KERNEL_RBF_PHI1>
                 : h.kp.id == H2D_KERNEL_RBF_PHI2 ? p2p_sym_kernel<H2D_KERNEL_RBF_PHI2>
                                                    : p2p_sym_kernel<H2D_KERNEL_TEST_LOWRANK>;
-      kfn<<<(int)h.n_p2p_gen, 256, 0, a>>>(h.kappa, h.leaf_begin, h.leaf_end, h.d_p2p_gen,
+      kfn<<<(int)h.n_p2p_gen, 256, 0, sg>>>(h.kappa, h.leaf_begin, h.leaf_end, h.d_p2p_gen,
                                            h.d_leaf_start, h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear,
                                            h.d_ynear + h.n, h.d_ynear + 2 * h.n);
       H2D_LAUNCH_CHECK();
@@ -1495,14 +1516,20 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
         };
         auto* kfn = r == 0 ? pick(std::integral_constant<int, 1>{})
                   : r == 1 ? pick(std::integral_constant<int, 2>{}) : pick(std::integral_constant<int, 3>{});
-        H2D_CUDA(cudaMemsetAsync(h.d_counters + 4 + r, 0, sizeof(int32_t), a));
+        cudaStream_t sw = r == 0 ? a : side(3 - r);
+        H2D_CUDA(cudaMemsetAsync(h.d_counters + 4 + r, 0, sizeof(int32_t), sw));
         const int grid = (int)std::min<int64_t>(h.num_sms, (cnt + 7) / 8);
-        kfn<<<grid, 256, 0, a>>>(h.kappa, h.d_p2p_warp + off, (int)cnt, h.d_counters + 4 + r, h.d_leaf_start,
+        kfn<<<grid, 256, 0, sw>>>(h.kappa, h.d_p2p_warp + off, (int)cnt, h.d_counters + 4 + r, h.d_leaf_start,
                                  h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear, h.d_ynear + h.n, h.d_ynear + 2 * h.n);
         H2D_LAUNCH_CHECK();
         off += cnt;
       }
     }
+    for (int k = 0; k < 3; ++k)
+      if (forked[k]) {
+        H2D_CUDA(cudaEventRecord(h.ev_p2p_side[k], h.p2p_side[k]));
+        H2D_CUDA(cudaStreamWaitEvent(a, h.ev_p2p_side[k], 0));
+      }
     record(h, 7, a);
     H2D_CUDA(cudaEventRecord(h.ev_join, a));
   };

@@ -38,6 +38,11 @@ Handle::~Handle() {
   if (ev_join) cudaEventDestroy(ev_join);
   if (ev_far) cudaEventDestroy(ev_far);
   if (aux_stream) cudaStreamDestroy(aux_stream);
+  for (int k = 0; k < 3; ++k) {
+    if (p2p_side[k]) cudaStreamDestroy(p2p_side[k]);
+    if (ev_p2p_side[k]) cudaEventDestroy(ev_p2p_side[k]);
+  }
+  if (ev_p2p_fork) cudaEventDestroy(ev_p2p_fork);
   if (hi_stream) cudaStreamDestroy(hi_stream);
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (ev_copy0) cudaEventDestroy(ev_copy0);

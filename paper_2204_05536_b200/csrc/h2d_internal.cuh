@@ -300,6 +300,10 @@ struct Handle {
   cudaStream_t copy_stream = nullptr;     // host <-> device copies of host-pointer calls
   cudaEvent_t ev_copy0 = nullptr, ev_copy1 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_far = nullptr;
+  // P2P classes (generic CTA leaves, warp leaves of 3 / 2 rows per lane) fork from aux_stream
+  // onto their own low-priority streams so their under-filled grids overlap
+  cudaStream_t p2p_side[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_p2p_fork = nullptr, ev_p2p_side[3] = {nullptr, nullptr, nullptr};
   // matvec work buffers
   double* d_xtree = nullptr;              // [n]
   double* d_ybuf = nullptr;               // [n] staging for host y
