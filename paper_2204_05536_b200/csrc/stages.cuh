@@ -8,6 +8,7 @@
 #pragma once
 #include "pipe.cuh"
 
+
 namespace h2d {
 namespace {
 
@@ -455,7 +456,10 @@ constexpr int kSmallARows = 32, kSmallBRows = 8;
 // Stage A, boxes of <= kSmallARows rows in one chunk: lane owns column pairs pb + lane and
 // pb + 32 + lane of a 64-pair block, rows in order; t through vdst (no reduction: the warp
 // owns the whole box).
-__global__ void __launch_bounds__(256)
+// 8 CTAs per SM (32 registers, 88 bytes spilled): more rows in flight; 4 CTAs per SM at 64
+// registers measured 6 % slower on the Chebyshev phi_1 system
+constexpr int kSmallAMinBlocks = 8;
+__global__ void __launch_bounds__(256, kSmallAMinBlocks)
 stageA_small_kernel(const AItem* __restrict__ items, int n_items, LevelPtrs lp, const double* __restrict__ x,
                     const int32_t* __restrict__ vdst, double* __restrict__ t) {
   const int lane = threadIdx.x & 31;
@@ -489,11 +493,12 @@ stageA_small_kernel(const AItem* __restrict__ items, int n_items, LevelPtrs lp, 
     }
   }
 }
-// Stage B, whole leaves of <= kSmallBRows rows: lane owns columns c = lane + 32 k of every
-// level's (leaf, level) panel (column-major, mLp <= 8 rows: one to four 16-byte loads per
-// column), 8 row accumulators, reduced over the warp by one transposed butterfly.  (Loading
-// 2-8 columns per lane ahead of use measured 5-10 % slower: tiny items waste the predicated
-// loads.)
+// Stage B, whole leaves of <= kSmallBRows rows: warp per leaf; each level's (leaf, level)
+// panel (column-major, mLp <= 8 rows) streams as flat 16-byte elements, 4 per lane in
+// flight; 8 row accumulators, reduced over the warp by one transposed butterfly.  (The
+// previous column-per-lane loop kept one to four loads per lane in flight and issued a
+// dependent descriptor load per level: Chebyshev 500^2 phi_1 matvec 1.262 -> 1.178 ms.)
+constexpr int kSmallBSteps = 4;   // flat elements in flight per lane (2: 64 regs but slower; 6, 8: slower)
 __global__ void __launch_bounds__(256)
 stageB_small_kernel(const BItem* __restrict__ items, const BLevel* __restrict__ blev, int n_items, int kappa,
                     LevelPtrs lp, double* __restrict__ yfar) {
@@ -505,20 +510,45 @@ stageB_small_kernel(const BItem* __restrict__ items, const BLevel* __restrict__ 
     double acc[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) acc[r] = 0.0;
+    // every level's descriptor in one load (lane l - 1 holds level l): the U loads of a level
+    // no longer wait behind a dependent descriptor load
+    BLevel mine{0, 0, 0};
+    if (lane < kappa) mine = blev[(int64_t)k * kappa + lane];
     for (int l = 1; l <= kappa; ++l) {
-      const BLevel lv = blev[(int64_t)k * kappa + l - 1];
-      if (lv.R <= 0) continue;
-      const double* __restrict__ U = lp.U[l] + lv.uoff;
-      const double* __restrict__ tb = lp.tu[l] + lv.tcol;
-      for (int c = lane; c < lv.R; c += 32) {
-        const double tc = __ldg(tb + c);
-        const double2* __restrict__ col = reinterpret_cast<const double2*>(U + (int64_t)c * mLp);
+      const int R = __shfl_sync(0xffffffffu, mine.R, l - 1);
+      if (R <= 0 || mLp == 0) continue;
+      const double* __restrict__ U = lp.U[l] + __shfl_sync(0xffffffffu, mine.uoff, l - 1);
+      const double* __restrict__ tb = lp.tu[l] + __shfl_sync(0xffffffffu, mine.tcol, l - 1);
+      // the panel as one flat stream of P * R 16-byte elements (P = mLp / 2 row pairs per
+      // column): lane takes elements f = lane + 32 s, kSmallBSteps per pass, so every warp
+      // load is 512 contiguous bytes whatever mLp is; element f is row pair f % P of column
+      // f / P, tracked incrementally (a step of 32 elements: +32 / P columns, +32 % P pairs)
+      const int P = mLp >> 1;
+      const int Lf = P * R;
+      const double2* __restrict__ U2 = reinterpret_cast<const double2*>(U);
+      int col = lane / P, rp = lane - (lane / P) * P;
+      const int dq = 32 / P, dr = 32 - (32 / P) * P;
+      for (int f0 = 0; f0 < Lf; f0 += 32 * kSmallBSteps) {
+        double2 u[kSmallBSteps];
+        double tc[kSmallBSteps];
+        int pr[kSmallBSteps];
 #pragma unroll
-        for (int r2 = 0; r2 < 4; ++r2)
-          if (2 * r2 < mLp) {
-            const double2 u = __ldcs(col + r2);
-            acc[2 * r2] = fma(u.x, tc, acc[2 * r2]);
-            acc[2 * r2 + 1] = fma(u.y, tc, acc[2 * r2 + 1]);
+        for (int q = 0; q < kSmallBSteps; ++q) {
+          const int f = f0 + 32 * q + lane;
+          pr[q] = rp;
+          u[q] = f < Lf ? __ldcs(U2 + f) : make_double2(0.0, 0.0);
+          tc[q] = f < Lf ? __ldg(tb + col) : 0.0;
+          rp += dr;
+          col += dq;
+          if (rp >= P) { rp -= P; ++col; }
+        }
+#pragma unroll
+        for (int q = 0; q < kSmallBSteps; ++q)
+#pragma unroll
+          for (int r2 = 0; r2 < 4; ++r2) {   // selected multiplier: no dynamic register index
+            const double w = pr[q] == r2 ? tc[q] : 0.0;
+            acc[2 * r2] = fma(u[q].x, w, acc[2 * r2]);
+            acc[2 * r2 + 1] = fma(u[q].y, w, acc[2 * r2 + 1]);
           }
       }
     }
