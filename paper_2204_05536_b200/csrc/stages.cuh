@@ -514,6 +514,7 @@ stageB_small_kernel(const BItem* __restrict__ items, const BLevel* __restrict__ 
     // no longer wait behind a dependent descriptor load
     BLevel mine{0, 0, 0};
     if (lane < kappa) mine = blev[(int64_t)k * kappa + lane];
+    double pa0 = 0.0, pa1 = 0.0;
     for (int l = 1; l <= kappa; ++l) {
       const int R = __shfl_sync(0xffffffffu, mine.R, l - 1);
       if (R <= 0 || mLp == 0) continue;
@@ -528,6 +529,26 @@ stageB_small_kernel(const BItem* __restrict__ items, const BLevel* __restrict__ 
       const double2* __restrict__ U2 = reinterpret_cast<const double2*>(U);
       int col = lane / P, rp = lane - (lane / P) * P;
       const int dq = 32 / P, dr = 32 - (32 / P) * P;
+      if (dr == 0) {
+        // P = 1, 2, 4: the lane's row pair (lane % P) never changes: two accumulators
+        for (int f0 = 0; f0 < Lf; f0 += 32 * kSmallBSteps) {
+          double2 u[kSmallBSteps];
+          double tc[kSmallBSteps];
+#pragma unroll
+          for (int q = 0; q < kSmallBSteps; ++q) {
+            const int f = f0 + 32 * q + lane;
+            u[q] = f < Lf ? __ldcs(U2 + f) : make_double2(0.0, 0.0);
+            tc[q] = f < Lf ? __ldg(tb + col + q * dq) : 0.0;
+          }
+          col += kSmallBSteps * dq;
+#pragma unroll
+          for (int q = 0; q < kSmallBSteps; ++q) {
+            pa0 = fma(u[q].x, tc[q], pa0);
+            pa1 = fma(u[q].y, tc[q], pa1);
+          }
+        }
+        continue;
+      }
       for (int f0 = 0; f0 < Lf; f0 += 32 * kSmallBSteps) {
         double2 u[kSmallBSteps];
         double tc[kSmallBSteps];
@@ -551,6 +572,16 @@ stageB_small_kernel(const BItem* __restrict__ items, const BLevel* __restrict__ 
             acc[2 * r2 + 1] = fma(u[q].y, w, acc[2 * r2 + 1]);
           }
       }
+    }
+    {   // fold the fixed-pair accumulators in (row pair lane % P; P = mLp / 2 <= 4)
+      const int P = mLp >> 1;
+      const int rp0 = P > 0 ? lane % P : 0;
+#pragma unroll
+      for (int r2 = 0; r2 < 4; ++r2)
+        if (rp0 == r2) {
+          acc[2 * r2] += pa0;
+          acc[2 * r2 + 1] += pa1;
+        }
     }
     const double v = warp_transpose_sum8(acc, lane);
     const int r = lane >> 2;
