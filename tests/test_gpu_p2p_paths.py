@@ -130,3 +130,14 @@ def test_small_item_kernels(h2d, symmetric):
     assert rel(y, ref.matvec(dev(x)).cpu().numpy()) <= 1e-13
     yd = oracle.dense_matvec(pts, x, KID["rbf_phi1"], 1e-3, 1.0, 22500.0)
     assert rel(y, yd) <= 1e-10
+    # every padded leaf height of the stage-B small kernel (2 / 4 / 8: the fixed row-pair
+    # path; 6: the selected-multiplier path) is present and correct on its own rows
+    perm, ls = op.tree()
+    sizes = np.diff(ls)
+    yt, rt = y[perm], ref.matvec(dev(x)).cpu().numpy()[perm]
+    for hp in (2, 4, 6, 8):
+        leaves = np.nonzero((sizes + 1) // 2 * 2 == hp)[0]
+        leaves = leaves[sizes[leaves] > 0]
+        assert leaves.size > 0, hp
+        rows = np.concatenate([np.arange(ls[i], ls[i + 1]) for i in leaves])
+        assert rel(yt[rows], rt[rows]) <= 1e-12, hp
