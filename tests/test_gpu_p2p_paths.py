@@ -1,5 +1,6 @@
 """GPU parity of the near-field paths (S9): the warp-per-leaf kernel for <= 32-point leaves,
-the CTA fast kernel and the generic kernel (info p2p_leaves = [warp, fast, generic]).
+the CTA fast kernel and the generic kernel (info p2p_leaves = [warp, fast, generic]); the
+side-stream schedule of the classes against the one-stream schedule (bit-identical).
 
 Bars: the matvec vs the dense product <= 10 tol-level bounds; with the warp path disabled
 (H2D_P2P_NOWARP=1: the same leaves on the CTA paths, different summation order) equal to
@@ -141,3 +142,25 @@ def test_small_item_kernels(h2d, symmetric):
         assert leaves.size > 0, hp
         rows = np.concatenate([np.arange(ls[i], ls[i + 1]) for i in leaves])
         assert rel(yt[rows], rt[rows]) <= 1e-12, hp
+
+
+def test_p2p_side_streams_bit_identical(h2d):
+    """The near-field classes (generic CTA leaves, warp leaves of 1 / 2 / 3 rows per lane) run
+    on their own low-priority streams; every slot value has one writer and a fixed summation
+    order, so the result equals the one-stream schedule (H2D_P2P_ONESTREAM=1) bit for bit.
+    Chebyshev 300^2 at the depth rule with N_max 500: corner leaves of hundreds of points
+    (generic kernel) beside thousands of small ones."""
+    pts = W.chebyshev_grid(300)
+    op = build(h2d, pts, "rbf_phi1", 500, 1e-12, c=1e-3, shift=90000.0, depth=-2)
+    warp, _, generic = op.info()["p2p_leaves"]
+    assert warp > 0 and generic > 0, op.info()["p2p_leaves"]
+    x = W.random_vector(pts.shape[0], 5600)
+    y = op.matvec(dev(x)).cpu().numpy()
+    os.environ["H2D_P2P_ONESTREAM"] = "1"
+    try:
+        y1 = op.matvec(dev(x)).cpu().numpy()
+    finally:
+        os.environ.pop("H2D_P2P_ONESTREAM")
+    assert np.array_equal(y, y1)
+    yd = oracle.dense_matvec(pts, x, KID["rbf_phi1"], 1e-3, 1.0, 90000.0)
+    assert rel(y, yd) <= 1e-10
