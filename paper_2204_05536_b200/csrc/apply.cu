@@ -1463,8 +1463,9 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
   const bool p2p_one = env_one && atoi(env_one) == 1;
   auto p2p = [&]() {
     record(h, 6, a);
-    // the generic CTA leaves and the 3- and 2-row warp classes run on side streams: a class
-    // with a few dozen CTAs (the big leaves of a clustered input) no longer serialises the rest
+    // an under-filled class (fewer CTAs than SMs: the big leaves of a clustered input) runs on
+    // a side stream and no longer serialises the rest; full-grid classes stay one after another
+    // on aux_stream (two of them at once measured 1 % slower on the C3 symmetric apply)
     bool forked[3] = {false, false, false};
     auto side = [&](int k) -> cudaStream_t {
       if (p2p_one) return a;
@@ -1476,7 +1477,7 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
       return h.p2p_side[k];
     };
     if (h.n_p2p_gen > 0) {
-      cudaStream_t sg = side(0);
+      cudaStream_t sg = h.n_p2p_gen < h.num_sms ? side(0) : a;
       auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_sym_kernel<H2D_KERNEL_LOG>
                 : h.kp.id == H2D_KERNEL_IMQ ? p2p_sym_kernel<H2D_KERNEL_IMQ>
                 : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_sym_kernel<H2D_KERNEL_ONE_OVER_R>
@@ -1516,9 +1517,9 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
         };
         auto* kfn = r == 0 ? pick(std::integral_constant<int, 1>{})
                   : r == 1 ? pick(std::integral_constant<int, 2>{}) : pick(std::integral_constant<int, 3>{});
-        cudaStream_t sw = r == 0 ? a : side(3 - r);
-        H2D_CUDA(cudaMemsetAsync(h.d_counters + 4 + r, 0, sizeof(int32_t), sw));
         const int grid = (int)std::min<int64_t>(h.num_sms, (cnt + 7) / 8);
+        cudaStream_t sw = r > 0 && grid < h.num_sms ? side(3 - r) : a;
+        H2D_CUDA(cudaMemsetAsync(h.d_counters + 4 + r, 0, sizeof(int32_t), sw));
         kfn<<<grid, 256, 0, sw>>>(h.kappa, h.d_p2p_warp + off, (int)cnt, h.d_counters + 4 + r, h.d_leaf_start,
                                  h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear, h.d_ynear + h.n, h.d_ynear + 2 * h.n);
         H2D_LAUNCH_CHECK();
