@@ -9,8 +9,8 @@ before timing (build seconds reported separately).  N = 1: the whole matvec on o
 N > 1 (torchrun): contiguous Morton row ranges per rank, one NCCL all-gather of x per
 matvec, max over ranks; total work is fixed -> "scaling": "strong".
 
-Rank 0 prints ONE JSON line.  --impl reference times the CPU oracle (oracle/) on a
-bounded Morton slice of the same workload (this tier's reference arm).
+Rank 0 prints ONE JSON line.  --impl reference times the CPU oracle (oracle/) on the same
+workload (the full operator where it fits in host RAM; this tier's reference arm).
 """
 from __future__ import annotations
 
@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c4", action="store_true",
+                    help="skip the C4 (N = 2^22) sub-result the default C3 line carries")
     ap.add_argument("--symmetric", action="store_true",
                     help="symmetric build + apply (one ACA per unordered pair, DESIGN.md R23)")
     ap.add_argument("--no-variants", action="store_true",
@@ -125,30 +127,58 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------- oracle arm
 
-def oracle_sample(cfg, threads=None):
-    """Build the oracle restricted to the rows of Morton box 0 at level 2 (1/16 of the rows)."""
+# Host RAM the oracle needs for a config (factors + dense leaf blocks + tree; survey census,
+# SURVEY §8(d)): the full operator is built when it fits in 60 % of the host's RAM.
+ORACLE_GB = {"c1": 0.05, "c2": 2.5, "c3": 24.0, "c4": 112.0, "c5": 420.0}
+
+
+def host_info():
+    """nproc, CPU model and RAM of the host the oracle runs on."""
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 1e9
+    except (ValueError, OSError):
+        ram = 0.0
+    return {"nproc": os.cpu_count(), "cpu_model": model, "ram_gb": round(ram, 1)}
+
+
+def oracle_operator(cfg, name):
+    """The oracle as it stands: the FULL operator when it fits in host RAM (C1-C3 here), else
+    the rows of Morton box 0 at level 2 (1/16 of the rows; C4 / C5), whose matvec time is
+    extrapolated by the row fraction and labelled so."""
     import oracle
-    if threads:
-        oracle.set_threads(threads)
     pts = W.config_points(cfg)
+    kw = dict(c=cfg.c, scale=cfg.scale, shift=cfg.shift, box_lo=cfg.box_lo, box_side=cfg.box_side)
+    if ORACLE_GB[name] <= 0.6 * host_info()["ram_gb"]:
+        t0 = time.time()
+        op = oracle.Operator(pts, cfg.kernel, cfg.leaf_size, cfg.tol, **kw)
+        return op, 1.0, time.time() - t0, (f"the full oracle operator (C++ -O2 -ffp-contract=off, OpenMP; "
+                                           f"Alg. 1 build + Alg. 2 matvec) on all {cfg.n} points, no extrapolation")
     kappa = oracle.depth(cfg.n, cfg.leaf_size)
     lvl = min(2, kappa)
     _, _, ls = oracle.tree(pts, cfg.box_lo, cfg.box_side, kappa)
     rows = int(ls[1 << (2 * (kappa - lvl))])
     t0 = time.time()
-    op = oracle.Operator(pts, cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c, scale=cfg.scale,
-                         shift=cfg.shift, box_lo=cfg.box_lo, box_side=cfg.box_side,
-                         row_range=(0, rows))
+    op = oracle.Operator(pts, cfg.kernel, cfg.leaf_size, cfg.tol, row_range=(0, rows), **kw)
     build_s = time.time() - t0
     frac = rows / cfg.n
-    desc = (f"oracle (C++ -O2, OpenMP) restricted to TREE rows [0, {rows}) = Morton box 0 of "
-            f"level {lvl} ({frac:.4f} of the rows); matvec time extrapolated x{1 / frac:.1f} "
-            f"(its V^T x work at levels < {lvl} is whole-block, so the extrapolation slightly "
-            f"overstates the oracle's time)")
+    desc = (f"EXTRAPOLATED: the full operator needs ~{ORACLE_GB[name]:.0f} GB of host RAM; oracle restricted "
+            f"to TREE rows [0, {rows}) = Morton box 0 of level {lvl} ({frac:.4f} of the rows), matvec time "
+            f"x{1 / frac:.1f} (its V^T x work at levels < {lvl} is whole-block, so this overstates the "
+            f"oracle's time slightly)")
     return op, frac, build_s, desc
 
 
 def time_oracle(op, cfg, frac, steps, warmup):
+    """Mean wall time of `steps` oracle matvecs (fresh seeded x each) after `warmup`."""
     xs = [W.config_x(cfg, k) for k in range(min(steps + warmup, 4))]
     for k in range(warmup):
         op.matvec(xs[k % len(xs)])
@@ -161,12 +191,24 @@ def time_oracle(op, cfg, frac, steps, warmup):
     return 1.0 / t_full, t_full
 
 
-def cpu_baseline(cfg):
+def cpu_baseline(cfg, name):
+    """The oracle timed on the host cores in the same run: build once, then
+    the mean of 10 matvecs after one warm-up on all cores, and of 2 on 1 thread."""
     import oracle
-    op, frac, build_s, desc = oracle_sample(cfg)
-    value, _ = time_oracle(op, cfg, frac, 5, 1)
-    return {"value": value, "unit": "matvecs/s", "cores": oracle.max_threads(), "kind": "oracle",
-            "sample": desc, "sample_build_seconds": round(build_s, 3)}
+    op, frac, build_s, desc = oracle_operator(cfg, name)
+    cores = oracle.max_threads()
+    value, t_all = time_oracle(op, cfg, frac, 10, 1)
+    oracle.set_threads(1)
+    try:
+        value1, t_one = time_oracle(op, cfg, frac, 2, 0)
+    finally:
+        oracle.set_threads(cores)
+    op.close()
+    return {"value": value, "unit": "matvecs/s", "cores": cores, "kind": "oracle",
+            "sample": desc + "; mean of 10 matvecs after 1 warm-up (all cores) and of 2 (1 thread)",
+            "extrapolated": frac < 1.0, "ms_per_matvec": round(t_all * 1e3, 2),
+            "value_1thread": value1, "ms_per_matvec_1thread": round(t_one * 1e3, 1),
+            "build_seconds": round(build_s, 2), "host": host_info()}
 
 
 def run_reference(args, cfg):
@@ -174,7 +216,7 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     import oracle
-    op, frac, build_s, desc = oracle_sample(cfg)
+    op, frac, build_s, desc = oracle_operator(cfg, args.config)
     value, t_full = time_oracle(op, cfg, frac, args.steps, args.warmup)
     line = {
         "impl": "reference", "metric": "HODLR2D fp64 matvecs/sec", "value": value,
@@ -183,7 +225,8 @@ def run_reference(args, cfg):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(cfg, args.gpus),
         "cpu_baseline": {"value": value, "unit": "matvecs/s", "cores": oracle.max_threads(),
-                         "kind": "oracle", "sample": desc},
+                         "kind": "oracle", "sample": desc + f"; build {build_s:.1f} s untimed",
+                         "extrapolated": frac < 1.0, "host": host_info()},
         "e2e": {"value": value, "unit": "matvecs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -222,9 +265,13 @@ def run_ours(args, cfg):
     pts = W.config_points(cfg)
     d_pts = torch.from_numpy(pts).cuda()
     t0 = time.time()
+    # N > 1: the handle owns the S11 communicator (an NCCL communicator whose unique id is
+    # broadcast over the torch.distributed group; gloo: host-staged gather) and each matvec
+    # takes only the rank's slice of x (H2D_ORDER_LOCAL): no torch collective in the loop
     op = h2d.Hodlr2d.build(d_pts, cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c, scale=cfg.scale,
                            shift=cfg.shift, box_lo=cfg.box_lo, box_side=cfg.box_side,
-                           world=world, rank=rank, stream=stream.cuda_stream, symmetric=args.symmetric)
+                           stream=stream.cuda_stream, symmetric=args.symmetric,
+                           **({"group": dist.group.WORLD} if dist else {}))
     torch.cuda.synchronize()
     build_s = time.time() - t0
     del d_pts
@@ -240,30 +287,13 @@ def run_ours(args, cfg):
     else:
         perm, _ = op.tree()
         rb, re_ = inf["row_begin"], inf["row_end"]
-        cnt = torch.tensor([re_ - rb], device="cuda" if args.dist_backend == "nccl" else "cpu")
-        allc = [torch.zeros_like(cnt) for _ in range(world)]
-        dist.all_gather(allc, cnt)
-        cmax = int(max(int(c.item()) for c in allc))
-        # each rank owns x_tree[rb:re]; the gathered [world x cmax] buffer is unpadded by the
-        # library (ORDER_GATHERED)
-        xs = torch.zeros(nx, cmax, dtype=torch.float64, device="cuda")
-        for k in range(nx):
-            xk = W.config_x(cfg, k)[perm][rb:re_]
-            xs[k, : re_ - rb] = torch.from_numpy(xk)
-        xg = torch.empty(world * cmax, dtype=torch.float64, device="cuda")
+        assert inf["comm_kind"] == (1 if args.dist_backend == "nccl" else 2), inf["comm_kind"]
+        # each rank owns x_tree[rb:re] and passes only that slice; the library gathers it
+        xs = torch.stack([torch.from_numpy(W.config_x(cfg, k)[perm][rb:re_].copy()) for k in range(nx)]).cuda()
         y = torch.empty(re_ - rb, dtype=torch.float64, device="cuda")
-        assert cmax == inf["gather_stride"], (cmax, inf["gather_stride"])
-
-        if args.dist_backend == "gloo":
-            xg_h = torch.empty(world * cmax, dtype=torch.float64)
 
         def step(k):
-            if args.dist_backend == "gloo":      # functional check only (host-staged)
-                dist.all_gather_into_tensor(xg_h, xs[k % nx].cpu())
-                xg.copy_(xg_h)
-            else:
-                dist.all_gather_into_tensor(xg, xs[k % nx])
-            op.matvec_raw(xg.data_ptr(), y.data_ptr(), h2d.ORDER_GATHERED)
+            op.matvec_raw(xs[k % nx].data_ptr(), y.data_ptr(), h2d.ORDER_LOCAL)
 
     for k in range(args.warmup):
         step(k)
@@ -432,15 +462,92 @@ def run_ours(args, cfg):
             "gpu_launches": args.steps * launches_per_matvec(inf, world),
             "clocks": csum,
         }
+        # BASELINE's metric spans N = 2^20 .. 2^24: the default (C3) line also carries C4
+        # (N = 2^22, 96 GB of factors) measured in the same run on the same GPU
+        if world == 1 and args.config == "c3" and not args.no_c4:
+            op.close()
+            del xs
+            torch.cuda.empty_cache()
+            try:
+                line["c4"] = sub_config(h2d, "c4", args, stream)
+            except Exception as ex:  # the headline stands on its own
+                line["c4"] = {"error": str(ex)}
         if not args.no_cpu_baseline and world == 1:   # the contract: rank 0 at N = 1 only
             try:
-                line["cpu_baseline"] = cpu_baseline(cfg)
+                line["cpu_baseline"] = cpu_baseline(cfg, args.config)
             except Exception as ex:  # the GPU number stands on its own
                 line["cpu_baseline"] = {"error": str(ex)}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def sub_config(h2d, name, args, stream):
+    """Another BASELINE config measured in the same run (device-timed matvecs/s after
+    warm-up, the roofline of its dominant kernel, e2e with pinned host buffers)."""
+    import torch
+    cfg = W.CONFIGS[name]
+    pts = torch.from_numpy(W.config_points(cfg)).cuda()
+    t0 = time.time()
+    op = h2d.Hodlr2d.build(pts, cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c, scale=cfg.scale, shift=cfg.shift,
+                           box_lo=cfg.box_lo, box_side=cfg.box_side, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    del pts
+    inf = op.info()
+    nx = 8
+    xs = torch.stack([torch.from_numpy(W.config_x(cfg, k)) for k in range(nx)]).cuda()
+    y = torch.empty(cfg.n, dtype=torch.float64, device="cuda")
+    for k in range(max(3, args.warmup)):
+        op.matvec_raw(xs[k % nx].data_ptr(), y.data_ptr(), h2d.ORDER_ORIGINAL)
+    torch.cuda.synchronize()
+    steps = max(10, min(args.steps, 50))
+    op.stage_times(reset=True)
+    op.set_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for k in range(steps):
+            op.matvec_raw(xs[k % nx].data_ptr(), y.data_ptr(), h2d.ORDER_ORIGINAL)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    op.set_timing(False)
+    ms = e0.elapsed_time(e1) / steps
+    st, cnt = op.stage_times(reset=True)
+    per = {k: v / max(cnt, 1) for k, v in st.items()}
+    peak, peak_kind = peaks()
+    a_ms, b_ms = per["stageA_VTx"], per["stageB_Ut"]
+    dom, dom_ms, dom_bytes = (("stageB_Ut", b_ms, inf["stageB_bytes"]) if b_ms >= a_ms
+                              else ("stageA_VTx", a_ms, inf["stageA_bytes"]))
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": ncu_traffic(name, dom),
+            "bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4),
+            "stage_ms_per_matvec": {k: round(v, 4) for k, v in per.items()},
+            "whole_matvec_frac": round(inf["matvec_bytes"] / (ms * 1e-3) / 1e9 / peak, 4)}
+    xh = torch.empty(cfg.n, dtype=torch.float64).pin_memory()
+    yh = torch.empty(cfg.n, dtype=torch.float64).pin_memory()
+    xh.copy_(xs[0].cpu())
+    op.matvec_raw(xh.data_ptr(), yh.data_ptr(), h2d.ORDER_ORIGINAL)
+    ke = 10
+    e0.record(stream)
+    for _ in range(ke):
+        op.matvec_raw(xh.data_ptr(), yh.data_ptr(), h2d.ORDER_ORIGINAL)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e = {"value": 1e3 * ke / e0.elapsed_time(e1), "unit": "matvecs/s",
+           "h2d_bytes_per_step": 8 * cfg.n, "d2h_bytes_per_step": 8 * cfg.n}
+    out = {"value": 1e3 / ms, "unit": "matvecs/s", "ms_per_step": ms, "steps": steps,
+           "config": config_dict(cfg, 1), "points_matvecs_per_s": 1e3 / ms * cfg.n,
+           "build_seconds": round(build_s, 3),
+           "operator": {k: inf[k] for k in ("kappa", "rank_max", "u_values", "v_values", "near_pairs",
+                                            "truncated", "matvec_bytes", "device_bytes")},
+           "roofline": roof, "e2e": e2e, "clocks": clk.summary(),
+           "gpu_launches": steps * launches_per_matvec(inf, 1)}
+    op.close()
+    return out
 
 
 def symmetric_variant(h2d, op_dir, cfg, xs, nx, y, stream, args):
@@ -504,7 +611,7 @@ P2P_FP64_OPS_PER_EVAL = {0: 17, 1: 12, 2: 12}
 
 def p2p_standalone_ms(op, step, args, n=10):
     """P2P time with the kernel running alone (H2D_P2P_SERIAL=1), CUDA events of the library."""
-    os.environ["H2D_P2P_SERIAL"] = "1"
+    op.set_diag("p2p_serial", 1)
     try:
         op.set_timing(True)
         op.stage_times(reset=True)
@@ -514,7 +621,7 @@ def p2p_standalone_ms(op, step, args, n=10):
         return st["p2p_near"] / max(cnt, 1)
     finally:
         op.set_timing(False)
-        os.environ["H2D_P2P_SERIAL"] = "0"
+        op.set_diag("p2p_serial", 0)
 
 
 def ncu_traffic(cfg_name, kernel):

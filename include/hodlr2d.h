@@ -72,7 +72,22 @@ enum {
  *              rows [row_begin_r, row_end_r) followed by padding — exactly the output of one
  *              equal-count all-gather (ncclAllGather / all_gather_into_tensor) of every
  *              rank's padded slice; y as for TREE. */
-enum { H2D_ORDER_ORIGINAL = 0, H2D_ORDER_TREE = 1, H2D_ORDER_GATHERED = 2 };
+enum { H2D_ORDER_ORIGINAL = 0, H2D_ORDER_TREE = 1, H2D_ORDER_GATHERED = 2, H2D_ORDER_LOCAL = 3 };
+/*   LOCAL    : x = this rank's TREE rows [row_begin, row_end) only; the library all-gathers
+ *              the slices of every rank itself (S11; the paper's distributed
+ *              matvec, §6) through the handle's communicator (options.nccl_id or
+ *              options.allgather) and overlaps it with the stage-A items whose column box is
+ *              local; y as for TREE.  Every rank of the world must call it (collective). */
+
+/* Bytes of the NCCL unique id carried by options.nccl_id (ncclUniqueId). */
+#define H2D_COMM_ID_BYTES 128
+
+/* Host all-gather callback (options.allgather): gather bytes_per_rank bytes of `send` from
+ * every rank of the world into `recv` (world * bytes_per_rank bytes, rank order), both host
+ * memory owned by the library; return 0 on success.  For worlds without NCCL between the
+ * ranks (e.g. several ranks sharing one GPU in tests); the library calls it from inside
+ * hodlr2d_matvec_ex(..., H2D_ORDER_LOCAL) on the calling thread. */
+typedef int (*hodlr2d_allgather_fn)(const void* send, void* recv, size_t bytes_per_rank, void* ctx);
 
 /* Options of hodlr2d_build_ex.  Always start from hodlr2d_default_options(). */
 typedef struct {
@@ -103,6 +118,15 @@ typedef struct {
                              every rank) replacing the geometric weight of the Morton-range
                              partition — e.g. the sum over ranks of hodlr2d_leaf_costs from a
                              first build; kappa must match.  Not copied.     (default NULL) */
+  const unsigned char* nccl_id; /* H2D_COMM_ID_BYTES-byte NCCL unique id (rank 0 calls
+                             hodlr2d_comm_unique_id, the caller broadcasts it, e.g. with
+                             torch.distributed): the handle creates and owns an NCCL
+                             communicator of `world` ranks (ncclCommInitRank, collective over
+                             the ranks) and its gather buffer (ncclMemAlloc + ncclCommRegister);
+                             enables H2D_ORDER_LOCAL.  Copied.               (default NULL) */
+  hodlr2d_allgather_fn allgather; /* host-staged alternative to nccl_id (used when nccl_id is
+                             NULL); enables H2D_ORDER_LOCAL                  (default NULL) */
+  void* allgather_ctx;    /* passed to allgather                             (default NULL) */
 } hodlr2d_options;
 
 #define H2D_MAX_LEVELS 16
@@ -144,6 +168,9 @@ typedef struct {
   int apply_launches;        /* low-rank apply kernels per matvec: stage A / B rings and
                                 their small-item (warp-per-item) kernels, B' (symmetric) */
   int64_t small_items[2];    /* stage A boxes / stage B leaves on the small-item kernels */
+  int comm_kind;             /* 0 none, 1 NCCL communicator, 2 host all-gather callback  */
+  int64_t local_items[2];    /* H2D_ORDER_LOCAL: stage-A items (ring, small) whose column box
+                                is local, run while the x all-gather is in flight        */
 } hodlr2d_info;
 
 /* Fill *opts with the defaults listed above. */
@@ -251,9 +278,22 @@ int hodlr2d_leaf_costs(hodlr2d_t h, double* costs);
  * they meet, the geometric part of Eq. eq:par's per-node load — each cut
  * snapped to a coarse box boundary when that shifts at most 3 % (level 1) / 4 % (level 2) /
  * 4x less per finer level of a rank's share (a cut inside a box makes both ranks stream
- * the V panels of all its partners). */
+ * the V panels of all its partners).  leaf_start must hold 4^kappa + 1 entries; kappa <= 15.
+ * Errors: H2D_EINVAL (bad arguments), H2D_ENOMEM (host allocation). */
 int hodlr2d_partition(const int32_t* leaf_start, int kappa, int world, int rank,
                       int64_t* leaf_begin, int64_t* leaf_end);
+
+/* Diagnostics switches of one handle's matvec (none changes results beyond
+ * rounding order, except "dual_norow", which skips the symmetric B' row dots and gives WRONG
+ * results, for timing only): "p2p_serial" (the near field alone, before stage A),
+ * "p2p_onestream" (every near-field class on one stream), "dual_norow", "copy_stream" (0:
+ * host copies on the work stream).  Defaults come from the H2D_* environment variables at
+ * build time.  H2D_EINVAL for an unknown name. */
+int hodlr2d_set_diag(hodlr2d_t h, const char* name, int value);
+
+/* Write a fresh NCCL unique id (H2D_COMM_ID_BYTES bytes) to id[] for options.nccl_id
+ * (called on one rank, then broadcast).  H2D_ENCCL if NCCL cannot be loaded. */
+int hodlr2d_comm_unique_id(unsigned char* id);
 
 /* Release every resource of the handle.  NULL is accepted. */
 int hodlr2d_destroy(hodlr2d_t h);

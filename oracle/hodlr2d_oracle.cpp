@@ -731,9 +731,11 @@ int oracle_matvec(void* h, const double* x_in, double* y_out, int order) {
 //   shift, lo_x, lo_y, side; int32 test_rank; int32 reserved;
 //   int32 perm[N]; then for l = 1..kappa: int64 nblocks; per block (CSR order):
 //   int32 rank; double U[m*rank] (col-major); double V[n*rank] (col-major).
+// A row-restricted operator (oracle_build with a row range, the rows one rank of a
+// partition serves) writes rank = -1 and no factors for the blocks it did not
+// build (R11); a loader serving only those rows never needs them.
 int oracle_save_factors(void* h, const char* path) {
     auto* o = static_cast<Oracle*>(h);
-    if (o->row_lo != 0 || o->row_hi != o->N) return set_err(-1, "row-restricted operator");
     FILE* f = std::fopen(path, "wb");
     if (!f) return set_err(-1, std::string("cannot open ") + path);
     const char magic[8] = {'H', '2', 'D', 'F', 'A', 'C', '0', '1'};
@@ -752,9 +754,9 @@ int oracle_save_factors(void* h, const char* path) {
         int64_t nbk = (int64_t)o->blocks[l].size();
         std::fwrite(&nbk, 8, 1, f);
         for (auto& B : o->blocks[l]) {
-            int32_t r = B.f.rank;
+            int32_t r = B.built ? B.f.rank : -1;
             std::fwrite(&r, 4, 1, f);
-            if (r) {
+            if (r > 0) {
                 std::fwrite(B.f.U.data(), 8, (size_t)B.m * r, f);
                 std::fwrite(B.f.V.data(), 8, (size_t)B.n * r, f);
             }

@@ -28,8 +28,10 @@ H2D_OK, H2D_WTRUNC, H2D_WNOCONV = 0, 1, 2
 H2D_EINVAL, H2D_EOUTOFBOX, H2D_ECOINCIDENT, H2D_ENOMEM = -1, -2, -3, -4
 H2D_ECUDA, H2D_ENCCL, H2D_EFACTORS = -5, -6, -7
 KERNELS = {"log": 0, "imq": 1, "one_over_r": 2, "rbf_phi1": 3, "rbf_phi2": 4, "test_lowrank": 100}
-ORDER_ORIGINAL, ORDER_TREE, ORDER_GATHERED = 0, 1, 2
-ORDERS = {"original": 0, "tree": 1, "gathered": 2}
+ORDER_ORIGINAL, ORDER_TREE, ORDER_GATHERED, ORDER_LOCAL = 0, 1, 2, 3
+ORDERS = {"original": 0, "tree": 1, "gathered": 2, "local": 3}
+COMM_ID_BYTES = 128
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 MAX_LEVELS = 16
 NUM_STAGES = 6
 STAGE_NAMES = ("input_permute", "stageA_VTx", "stageB_Ut", "p2p_join_wait", "combine", "p2p_near")
@@ -41,6 +43,7 @@ ABI_FUNCTIONS = (
     "hodlr2d_num_blocks", "hodlr2d_copy_ranks", "hodlr2d_copy_block", "hodlr2d_load_factors",
     "hodlr2d_save_factors", "hodlr2d_stage_times", "hodlr2d_set_timing", "hodlr2d_destroy",
     "hodlr2d_last_error", "hodlr2d_partition", "hodlr2d_gmres", "hodlr2d_matvec_multi", "hodlr2d_leaf_costs",
+    "hodlr2d_comm_unique_id", "hodlr2d_set_diag",
 )
 
 
@@ -55,6 +58,7 @@ class Options(C.Structure):
         ("row_begin", C.c_int64), ("row_end", C.c_int64),
         ("aca_scratch_bytes", C.c_size_t), ("timing", C.c_int), ("skip_aca", C.c_int),
         ("symmetric", C.c_int), ("leaf_weights", C.c_void_p),
+        ("nccl_id", C.c_void_p), ("allgather", ALLGATHER_FN), ("allgather_ctx", C.c_void_p),
     ]
 
 
@@ -75,6 +79,7 @@ class Info(C.Structure):
         ("device_bytes", C.c_int64), ("gather_stride", C.c_int64), ("p2p_bytes", C.c_int64),
         ("symmetric_apply", C.c_int), ("p2p_launches", C.c_int), ("p2p_leaves", C.c_int64 * 3),
         ("apply_launches", C.c_int), ("small_items", C.c_int64 * 2),
+        ("comm_kind", C.c_int), ("local_items", C.c_int64 * 2),
     ]
 
     def as_dict(self) -> dict:
@@ -127,6 +132,8 @@ def lib() -> C.CDLL:
             L.hodlr2d_gmres.argtypes = [vp, vp, vp, d, i, i, C.POINTER(i), C.POINTER(d)]
             L.hodlr2d_matvec_multi.argtypes = [vp, vp, vp, i, i]
             L.hodlr2d_leaf_costs.argtypes = [vp, vp]
+            L.hodlr2d_comm_unique_id.argtypes = [vp]
+            L.hodlr2d_set_diag.argtypes = [vp, C.c_char_p, i]
             _lib = L
     return _lib
 
@@ -162,6 +169,33 @@ def partition(leaf_start: np.ndarray, kappa: int, world: int, rank: int):
     return lb.value, le.value
 
 
+def comm_unique_id() -> bytes:
+    """hodlr2d_comm_unique_id: a fresh NCCL unique id for options.nccl_id (one rank creates
+    it, the caller broadcasts it)."""
+    buf = (C.c_ubyte * COMM_ID_BYTES)()
+    _check(lib().hodlr2d_comm_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+def _host_allgather(group):
+    """Host all-gather callback (options.allgather) over a torch.distributed CPU group (gloo):
+    argument marshalling only — the library hands over host buffers it owns."""
+    import torch
+    import torch.distributed as dist
+
+    def cb(send, recv, nbytes, ctx):
+        try:
+            world = dist.get_world_size(group)
+            n = nbytes // 8
+            st = torch.from_numpy(np.ctypeslib.as_array((C.c_double * n).from_address(send)))
+            rt = torch.from_numpy(np.ctypeslib.as_array((C.c_double * (n * world)).from_address(recv)))
+            dist.all_gather_into_tensor(rt, st, group=group)
+            return 0
+        except Exception:  # noqa: BLE001 - reported to the library as a failed collective
+            return -1
+    return ALLGATHER_FN(cb)
+
+
 def default_options() -> Options:
     o = Options()
     lib().hodlr2d_default_options(C.byref(o))
@@ -183,10 +217,15 @@ class Hodlr2d:
               shift=0.0, box_lo=(0.0, 0.0), box_side=0.0, depth=-1, max_rank=128,
               aca_consecutive=3, aca_trim=3, test_rank=1, stream=None, world=1, rank=0,
               row_range=None, aca_scratch_bytes=0, timing=False, skip_aca=False, symmetric=False,
-              leaf_weights=None):
+              leaf_weights=None, group=None, nccl_id=None):
         """hodlr2d_build_ex.  ``points``: (N, 2) float64 torch tensor (CUDA or CPU) or numpy array.
         ``leaf_weights``: host float64 array of 4^kappa per-leaf loads for the world partition
-        (e.g. the sum over ranks of ``leaf_costs()`` of a first build)."""
+        (e.g. the sum over ranks of ``leaf_costs()`` of a first build).
+        ``group``: a torch.distributed process group; world / rank are taken from it and the
+        handle gets a communicator for ``matvec(x_local, order="local")`` (S11): with an NCCL
+        group, rank 0's NCCL unique id is broadcast over it (the library then owns an NCCL
+        communicator); with a gloo group, the library's host-staged gather calls back into
+        all_gather_into_tensor.  ``nccl_id``: an id from ``comm_unique_id()`` (no group)."""
         kid = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
         o = default_options()
         o.c, o.scale, o.shift = c, scale, shift
@@ -202,6 +241,22 @@ class Hodlr2d:
             except Exception:
                 stream = None
         o.stream = stream or None
+        keep = []
+        if group is not None:
+            import torch.distributed as dist
+            world, rank = dist.get_world_size(group), dist.get_rank(group)
+            if dist.get_backend(group) == "nccl":
+                obj = [comm_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0), group=group)
+                nccl_id = obj[0]
+            else:
+                cb = _host_allgather(group)
+                keep.append(cb)
+                o.allgather = cb
+        if nccl_id is not None:
+            idbuf = (C.c_ubyte * COMM_ID_BYTES).from_buffer_copy(nccl_id)
+            keep.append(idbuf)
+            o.nccl_id = C.cast(idbuf, C.c_void_p)
         o.world, o.rank = world, rank
         if row_range is not None:
             o.row_begin, o.row_end = row_range
@@ -216,8 +271,9 @@ class Hodlr2d:
         n = points.shape[0]
         h = C.c_void_p()
         rc = _check(lib().hodlr2d_build_ex(_ptr(points), n, kid, leaf_size, aca_tol, C.byref(o), C.byref(h)))
-        op = cls(h.value, n)
+        op = cls(h.value, n, keepalive=keep)
         op.status = rc
+        op._stream = stream
         return op
 
     @classmethod
@@ -247,24 +303,69 @@ class Hodlr2d:
         self.close()
 
     # -------------------------------------------------------------- matvec
+    def _lens(self, o: int):
+        """(len_x, len_y) of one vector in order o (include/hodlr2d.h orderings)."""
+        if o == ORDER_ORIGINAL:
+            return self.n, self.n
+        inf = self.info()
+        m = inf["row_end"] - inf["row_begin"]
+        if o == ORDER_TREE:
+            return self.n, m
+        if o == ORDER_GATHERED:
+            return inf["world"] * inf["gather_stride"], m
+        return m, m
+
+    def _check_vec(self, a, length: int, what: str):
+        """The C side reads / writes exactly `length` values: refuse shorter buffers and
+        tensors on another device than the handle's stream (marshalling checks only)."""
+        numel = a.size if isinstance(a, np.ndarray) else a.numel()
+        if numel != length:
+            raise ValueError(f"{what} has {numel} values, expected {length}")
+        if not isinstance(a, np.ndarray) and a.is_cuda:
+            import torch
+            if a.device.index != torch.cuda.current_device():
+                raise ValueError(f"{what} is on {a.device}, the handle on cuda:{torch.cuda.current_device()}")
+
+    def _ordered(self, *tensors):
+        """Order the handle's stream (fixed at build) after torch's current stream when they
+        differ, and the current stream after it on exit (a context manager)."""
+        import contextlib
+        if not any(getattr(t, "is_cuda", False) for t in tensors):
+            return contextlib.nullcontext()
+        import torch
+        cur = torch.cuda.current_stream()
+        if self._stream is None or cur.cuda_stream == self._stream:
+            return contextlib.nullcontext()
+        hs = torch.cuda.ExternalStream(self._stream)
+
+        @contextlib.contextmanager
+        def ctx():
+            hs.wait_stream(cur)
+            yield
+            cur.wait_stream(hs)
+        return ctx()
+
+    _stream = None
+
     def matvec(self, x, out=None, order="original"):
-        """hodlr2d_matvec / hodlr2d_matvec_ex.  Returns ``out`` (allocated like x if None)."""
+        """hodlr2d_matvec / hodlr2d_matvec_ex.  Returns ``out`` (allocated like x if None).
+        order="local" (handles built with a group / nccl_id): x is this rank's TREE rows
+        [row_begin, row_end); every rank of the world must call it (S11 inside)."""
         o = ORDERS[order]
+        lx, ly = self._lens(o)
+        self._check_vec(x, lx, "x")
         if out is None:
-            if o != ORDER_ORIGINAL:
-                inf = self.info()
-                m = inf["row_end"] - inf["row_begin"]
-            else:
-                m = self.n
             if isinstance(x, np.ndarray):
-                out = np.empty(m, dtype=np.float64)
+                out = np.empty(ly, dtype=np.float64)
             else:
                 import torch
-                out = torch.empty(m, dtype=torch.float64, device=x.device)
-        if o == ORDER_ORIGINAL:
-            _check(lib().hodlr2d_matvec(self._h, _ptr(x), _ptr(out)))
-        else:
-            _check(lib().hodlr2d_matvec_ex(self._h, _ptr(x), _ptr(out), o))
+                out = torch.empty(ly, dtype=torch.float64, device=x.device)
+        self._check_vec(out, ly, "out")
+        with self._ordered(x, out):
+            if o == ORDER_ORIGINAL:
+                _check(lib().hodlr2d_matvec(self._h, _ptr(x), _ptr(out)))
+            else:
+                _check(lib().hodlr2d_matvec_ex(self._h, _ptr(x), _ptr(out), o))
         return out
 
     def gmres(self, b, x=None, tol=1e-10, restart=30, max_iter=1000):
@@ -276,9 +377,12 @@ class Hodlr2d:
             else:
                 import torch
                 x = torch.empty_like(b)
+        self._check_vec(b, self.n, "b")
+        self._check_vec(x, self.n, "x")
         its, rr = C.c_int(), C.c_double()
-        rc = _check(lib().hodlr2d_gmres(self._h, _ptr(b), _ptr(x), tol, restart, max_iter,
-                                        C.byref(its), C.byref(rr)))
+        with self._ordered(b, x):
+            rc = _check(lib().hodlr2d_gmres(self._h, _ptr(b), _ptr(x), tol, restart, max_iter,
+                                            C.byref(its), C.byref(rr)))
         self.gmres_converged = rc == H2D_OK
         return x, its.value, rr.value
 
@@ -287,17 +391,17 @@ class Hodlr2d:
         returns ``out`` of shape (nrhs, len_y)."""
         o = ORDERS[order]
         nrhs = X.shape[0]
+        lx, m = self._lens(o)
+        self._check_vec(X, nrhs * lx, "X")
         if out is None:
-            m = self.n
-            if o != ORDER_ORIGINAL:
-                inf = self.info()
-                m = inf["row_end"] - inf["row_begin"]
             if isinstance(X, np.ndarray):
                 out = np.empty((nrhs, m), dtype=np.float64)
             else:
                 import torch
                 out = torch.empty((nrhs, m), dtype=torch.float64, device=X.device)
-        _check(lib().hodlr2d_matvec_multi(self._h, _ptr(X), _ptr(out), nrhs, o))
+        self._check_vec(out, nrhs * m, "out")
+        with self._ordered(X, out):
+            _check(lib().hodlr2d_matvec_multi(self._h, _ptr(X), _ptr(out), nrhs, o))
         return out
 
     def matvec_multi_raw(self, x_ptr: int, y_ptr: int, nrhs: int, order: int = ORDER_ORIGINAL):
@@ -357,6 +461,10 @@ class Hodlr2d:
 
     def save_factors(self, path):
         _check(lib().hodlr2d_save_factors(self._h, str(path).encode()))
+
+    def set_diag(self, name: str, value: int):
+        """hodlr2d_set_diag: a diagnostics switch of this handle's matvec."""
+        _check(lib().hodlr2d_set_diag(self._h, name.encode(), int(value)))
 
     def set_timing(self, on: bool):
         _check(lib().hodlr2d_set_timing(self._h, int(bool(on))))

@@ -1045,6 +1045,16 @@ void finalize_schedule(Handle& h) {
   std::stable_sort(aitems.begin(), amid, [](const AItem& a, const AItem& b) {
     return (int64_t)a.nrows * a.Rp > (int64_t)b.nrows * b.Rp;
   });
+  // H2D_ORDER_LOCAL (a communicator with several ranks): items whose rows lie in the served
+  // range first (each part keeps its order), so they can run while x is being gathered
+  if (h.comm && h.opts.world > 1) {
+    auto local = [&](const AItem& a) { return a.x_off >= h.row_begin && a.x_off + a.nrows <= h.row_end; };
+    h.n_abig_loc = std::stable_partition(aitems.begin(), amid, local) - aitems.begin();
+    h.n_asmall_loc = std::stable_partition(amid, aitems.end(), local) - amid;
+  } else {
+    h.n_abig_loc = h.n_abig;
+    h.n_asmall_loc = (int64_t)aitems.size() - h.n_abig;
+  }
   // symmetric stage B' items over the first-side U box panels (same chunking as stage A);
   // udst maps a U-box column (block (X, Y), X < Y, column q) to the t2 index of (Y, X)
   std::vector<AItem> b1items;
@@ -1411,13 +1421,18 @@ static void launch_stageB_geom(Handle& h, cudaStream_t hi) {
   H2D_LAUNCH_CHECK();
 }
 
-static void launch_small(Handle& h, bool stage_a, const double* d_xtree, double* t, cudaStream_t hi) {
-  const int64_t n = stage_a ? h.n_aitems - h.n_abig : h.n_bitems - h.n_bbig;
+// part: stage A only — 0 all small items, 1 the local ones, 2 the rest (H2D_ORDER_LOCAL)
+static void launch_small(Handle& h, bool stage_a, const double* d_xtree, double* t, cudaStream_t hi,
+                         int part = 0) {
+  int64_t first = stage_a ? h.n_abig : h.n_bbig;
+  int64_t n = stage_a ? h.n_aitems - h.n_abig : h.n_bitems - h.n_bbig;
+  if (stage_a && part == 1) n = h.n_asmall_loc;
+  if (stage_a && part == 2) { first += h.n_asmall_loc; n -= h.n_asmall_loc; }
   if (n <= 0) return;
   // 16 CTAs x 8 warps per SM requested: the warps are latency-bound on their own loads
   const int grid = (int)std::min<int64_t>((int64_t)h.num_sms * 16, (n + 7) / 8);
   if (stage_a)
-    stageA_small_kernel<<<grid, 256, 0, hi>>>(h.d_aitems + h.n_abig, (int)n, h.lp, d_xtree, h.d_vdst, t);
+    stageA_small_kernel<<<grid, 256, 0, hi>>>(h.d_aitems + first, (int)n, h.lp, d_xtree, h.d_vdst, t);
   else
     stageB_small_kernel<<<grid, 256, 0, hi>>>(h.d_bitems + h.n_bbig, h.d_blev + h.n_bbig * h.kappa, (int)n,
                                               h.kappa, h.lp, h.d_yfar);
@@ -1432,15 +1447,30 @@ static void launch_stageB(Handle& h, cudaStream_t hi) {
   else launch_stageB_geom<kNSShallow, kStageDbl, kStageVec>(h, hi);
 }
 
+// Stage A then stage B on the high-priority stream.  gather (H2D_ORDER_LOCAL): only the
+// served rows of x_tree are valid at the start; the items whose column box is local run
+// first (ring items on counter 0, their own small-item launch), then the host-staged
+// exchange (if any) runs on this thread while they stream, then this stream waits for the
+// gathered slots, unpads them and runs the remaining items (counter 7) and stage B.
 template <int NS>
-static void launch_stages(Handle& h, const double* d_xtree, cudaStream_t hi) {
+static void launch_stages(Handle& h, const double* d_xtree, cudaStream_t hi, bool gather, cudaEvent_t* xready) {
   const size_t smem = sizeof(PipeSmem<NS>);
-  launch_small(h, true, d_xtree, h.d_t, hi);
-  if (h.n_abig > 0) {
-    stageA_tma_kernel<NS><<<(int)std::min<int64_t>(h.persist_ctas, h.n_abig), kPipeThreads, smem, hi>>>(
-        h.d_aitems, (int)h.n_abig, h.d_counters, h.lp, d_xtree, h.d_vdst, h.d_t, h.d_tpart,
-        h.d_ritems, h.d_rcount);
+  auto ring = [&](int64_t first, int64_t cnt, int32_t* counter) {
+    if (cnt <= 0) return;
+    stageA_tma_kernel<NS><<<(int)std::min<int64_t>(h.persist_ctas, cnt), kPipeThreads, smem, hi>>>(
+        h.d_aitems + first, (int)cnt, counter, h.lp, d_xtree, h.d_vdst, h.d_t, h.d_tpart, h.d_ritems, h.d_rcount);
     H2D_LAUNCH_CHECK();
+  };
+  if (!gather) {
+    launch_small(h, true, d_xtree, h.d_t, hi);
+    ring(0, h.n_abig, h.d_counters);
+  } else {
+    launch_small(h, true, d_xtree, h.d_t, hi, 1);
+    ring(0, h.n_abig_loc, h.d_counters);
+    comm_gather_exchange(h);
+    *xready = comm_gather_finish(h, h.d_xtree, hi);   // (gather: d_xtree == h.d_xtree)
+    launch_small(h, true, d_xtree, h.d_t, hi, 2);
+    ring(h.n_abig_loc, h.n_abig - h.n_abig_loc, h.d_counters + 7);
   }
   record(h, 2, hi);
   launch_stageB(h, hi);
@@ -1449,18 +1479,22 @@ static void launch_stages(Handle& h, const double* d_xtree, cudaStream_t hi) {
 // Matvec on TREE-order x (S7-S9).  Stages A and B (HBM-bound) run on the high-priority
 // stream, the near-field P2P (FP64-bound) concurrently on the low-priority stream; the
 // combine epilogue on the caller's stream joins them.
-void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, int64_t y_row0) {
+void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, int64_t y_row0, bool gather) {
   cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
   const int64_t nleaves = h.leaf_end - h.leaf_begin;
   // H2D_P2P_SERIAL=1 (diagnostics only): the P2P runs alone, before stage A
-  const char* env_ser = getenv("H2D_P2P_SERIAL");
-  const bool p2p_serial = env_ser && atoi(env_ser) == 1;
+  const bool p2p_serial = h.diag_p2p_serial && !gather;
+  if (gather && h.symapply) {   // (single-rank symmetric handle: gather first, no overlap)
+    comm_gather_exchange(h);
+    comm_gather_finish(h, h.d_xtree, s);
+    gather = false;
+  }
+  cudaEvent_t xready = nullptr;
   H2D_CUDA(cudaEventRecord(h.ev_fork, s));
   H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_fork, 0));
   H2D_CUDA(cudaStreamWaitEvent(a, h.ev_fork, 0));
   // H2D_P2P_ONESTREAM=1 (diagnostics only): every P2P class on aux_stream, one after another
-  const char* env_one = getenv("H2D_P2P_ONESTREAM");
-  const bool p2p_one = env_one && atoi(env_one) == 1;
+  const bool p2p_one = h.diag_p2p_onestream;
   auto p2p = [&]() {
     record(h, 6, a);
     // an under-filled class (fewer CTAs than SMs: the big leaves of a clustered input) runs on
@@ -1554,18 +1588,20 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
                                              sizeof(PipeSmem<kNSDual, kSDDual>), hi>>>(
           h.d_b1items, (int)h.n_b1items, h.d_counters + 3, h.lp, d_xtree, h.d_udst, h.d_t, h.d_b1tpart,
           h.d_b1ritems, h.d_b1rcount, h.d_t1, h.d_y1,
-          getenv("H2D_DUAL_NOROW") ? (int64_t)-1 : h.n);   // diagnostics: skip the row dots
+          h.diag_dual_norow ? (int64_t)-1 : h.n);   // diagnostics: skip the row dots
       H2D_LAUNCH_CHECK();
     }
     record(h, 2, hi);
     launch_stageB(h, hi);
   } else {
     H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 2 * sizeof(int32_t), hi));
-    if (h.pipe_ns == kNSShallow) launch_stages<kNSShallow>(h, d_xtree, hi);
-    else launch_stages<kNSDeep>(h, d_xtree, hi);
+    if (gather) H2D_CUDA(cudaMemsetAsync(h.d_counters + 7, 0, sizeof(int32_t), hi));
+    if (h.pipe_ns == kNSShallow) launch_stages<kNSShallow>(h, d_xtree, hi, gather, &xready);
+    else launch_stages<kNSDeep>(h, d_xtree, hi, gather, &xready);
   }
   record(h, 3, hi);
   H2D_CUDA(cudaEventRecord(h.ev_far, hi));
+  if (xready) H2D_CUDA(cudaStreamWaitEvent(a, xready, 0));   // the near field reads remote x
   if (!p2p_serial) p2p();   // after stage A's launch: its CTAs are placed first
   H2D_CUDA(cudaStreamWaitEvent(s, h.ev_far, 0));
   H2D_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));

@@ -32,6 +32,7 @@ void Handle::release(void* p) {
 
 Handle::~Handle() {
   cudaStreamSynchronize(stream);
+  comm_destroy(*this);
   for (void* p : allocs) cudaFree(p);
   for (auto e : ev_pool) cudaEventDestroy(e);
   if (ev_fork) cudaEventDestroy(ev_fork);
@@ -74,13 +75,8 @@ static void copy_stream_init(Handle& h) {
 
 // dst (device) <- src (host), ordered after the work already queued on the work stream and
 // before everything queued on it afterwards.
-static bool use_copy_stream() {   // H2D_COPY_STREAM=0: copies on the work stream (diagnostics)
-  const char* e = getenv("H2D_COPY_STREAM");
-  return !(e && atoi(e) == 0);
-}
-
 static void h2d_ordered(Handle& h, void* dst, const void* src, size_t bytes) {
-  if (!use_copy_stream()) {
+  if (!h.diag_copy_stream) {   // H2D_COPY_STREAM=0: copies on the work stream (diagnostics)
     H2D_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h.stream));
     return;
   }
@@ -94,7 +90,7 @@ static void h2d_ordered(Handle& h, void* dst, const void* src, size_t bytes) {
 
 // dst (host) <- src (device) after the work queued on the work stream; returns when done.
 static void d2h_ordered_sync(Handle& h, void* dst, const void* src, size_t bytes) {
-  if (!use_copy_stream()) {
+  if (!h.diag_copy_stream) {
     H2D_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h.stream));
     H2D_CUDA(cudaStreamSynchronize(h.stream));
     return;
@@ -278,15 +274,20 @@ static void skip_factors(Handle& h) {
 }
 
 static void do_matvec(Handle& h, const double* x, double* y, int order) {
-  if (order != H2D_ORDER_ORIGINAL && order != H2D_ORDER_TREE && order != H2D_ORDER_GATHERED)
+  if (order != H2D_ORDER_ORIGINAL && order != H2D_ORDER_TREE && order != H2D_ORDER_GATHERED &&
+      order != H2D_ORDER_LOCAL)
     throw Error{H2D_EINVAL, "bad order"};
+  if (order == H2D_ORDER_LOCAL && !h.comm)
+    throw Error{H2D_EINVAL, "LOCAL order needs a communicator (options.nccl_id or options.allgather)"};
   if (!x || !y) throw Error{H2D_EINVAL, "null x or y"};
   const bool part = h.row_begin != 0 || h.row_end != h.n;
   if (order == H2D_ORDER_ORIGINAL && part)
     throw Error{H2D_EINVAL, "ORIGINAL order needs a single-rank (full-range) handle"};
   if (order == H2D_ORDER_GATHERED && h.rank_rows.empty())
     throw Error{H2D_EINVAL, "GATHERED order needs a world/rank partition"};
-  const int64_t xlen = order == H2D_ORDER_GATHERED ? h.gather_stride * h.opts.world : h.n;
+  const int64_t xlen = order == H2D_ORDER_GATHERED ? h.gather_stride * h.opts.world
+                     : order == H2D_ORDER_LOCAL  ? h.row_end - h.row_begin
+                                                 : h.n;
   cudaStream_t s = h.stream;
   const bool xdev = is_device_ptr(x), ydev = is_device_ptr(y);
   const int64_t ylen = order == H2D_ORDER_ORIGINAL ? h.n : (h.row_end - h.row_begin);
@@ -309,10 +310,13 @@ static void do_matvec(Handle& h, const double* x, double* y, int order) {
   } else if (order == H2D_ORDER_GATHERED) {
     unpad_gathered(h, xin, h.d_xtree);
     xt = h.d_xtree;
+  } else if (order == H2D_ORDER_LOCAL) {   // S11: the library gathers x itself (comm.cu)
+    comm_gather_start(h, xin, h.d_xtree);
+    xt = h.d_xtree;
   }
   mark_after_input(h);
   matvec_tree(h, xt, yout, order == H2D_ORDER_ORIGINAL ? H2D_ORDER_ORIGINAL : H2D_ORDER_TREE,
-              h.row_begin);
+              h.row_begin, order == H2D_ORDER_LOCAL);
   if (h.timing) h.timed_count++;
   if (!ydev) {
     d2h_ordered_sync(h, y, yout, ylen * sizeof(double));
@@ -353,6 +357,7 @@ static void load_factors(Handle& h, const char* path) {
   if (fperm != perm) throw Error{H2D_EFACTORS, "file permutation does not match the handle's tree"};
   clear_factors(h);
   h.truncated = 0;
+  std::vector<char> discard((size_t)1 << 20);
   for (int l = 1; l <= h.kappa; ++l) {
     Level& L = h.levels[(size_t)l];
     int64_t nb = 0;
@@ -370,8 +375,12 @@ static void load_factors(Handle& h, const char* path) {
         const int64_t n = h.box_end(l, Y) - h.box_begin(l, Y);
         int32_t r = 0;
         f.read((char*)&r, 4);
-        if (!f || r < 0) throw Error{H2D_EFACTORS, "bad rank"};
-        const size_t cnt = (size_t)r * (size_t)(m + n);
+        // r = -1: block not stored by a row-restricted file (R11); fine unless served here
+        if (!f || r < -1) throw Error{H2D_EFACTORS, "bad rank"};
+        if (r == -1 && keep)
+          throw Error{H2D_EFACTORS, "file lacks block " + std::to_string(e) + " of level " + std::to_string(l) +
+                                        ", whose rows this handle serves"};
+        const size_t cnt = r > 0 ? (size_t)r * (size_t)(m + n) : 0;
         if (keep) {
           L.rank[(size_t)e] = r;
           uo[(size_t)e] = (int64_t)host.size();
@@ -379,8 +388,13 @@ static void load_factors(Handle& h, const char* path) {
           size_t o = host.size();
           host.resize(o + cnt);
           f.read((char*)(host.data() + o), cnt * 8);
-        } else {
-          f.seekg((std::streamoff)(cnt * 8), std::ios::cur);
+        } else {   // read and drop (no seek: the file may be a pipe from the producer)
+          size_t left = cnt * 8;
+          while (left > 0 && f) {
+            const size_t k = std::min(left, discard.size());
+            f.read(discard.data(), (std::streamsize)k);
+            left -= k;
+          }
         }
         if (!f) throw Error{H2D_EFACTORS, "truncated factors at level " + std::to_string(l)};
       }
@@ -505,6 +519,13 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
   if (h.kappa > 15) throw Error{H2D_EINVAL, "depth > 15"};
   if (h.kappa > H2D_MAX_LEVELS) throw Error{H2D_EINVAL, "depth > H2D_MAX_LEVELS"};
   h.timing = opts->timing;
+  {   // diagnostics switches, read once here
+    auto env_is = [](const char* name, int v) { const char* e = getenv(name); return e && atoi(e) == v; };
+    h.diag_p2p_serial = env_is("H2D_P2P_SERIAL", 1);
+    h.diag_p2p_onestream = env_is("H2D_P2P_ONESTREAM", 1);
+    h.diag_dual_norow = getenv("H2D_DUAL_NOROW") != nullptr;
+    h.diag_copy_stream = !env_is("H2D_COPY_STREAM", 0);
+  }
   const double* d_pts = points;
   double* tmp = nullptr;
   if (!is_device_ptr(points)) {
@@ -530,6 +551,8 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
   build_lists(h);
   set_partition(h);
   h.opts.leaf_weights = nullptr;   // caller-owned, read only by the partition above
+  comm_init(h);                    // S11 communicator (collective over the world's ranks)
+  h.opts.nccl_id = nullptr;        // caller-owned, read only by comm_init
   // symmetric apply (R23): symmetric build on a single-rank handle (the multi-rank row
   // partitions keep the directed panels; stage B' needs every row of a row box)
   h.symapply = opts->symmetric && h.row_begin == 0 && h.row_end == h.n && h.kappa >= 1 &&
@@ -576,8 +599,11 @@ int hodlr2d_matvec_multi(hodlr2d_t H, const double* X, double* Y, int nrhs, int 
   if (!H || !X || !Y) throw Error{H2D_EINVAL, "null argument"};
   if (nrhs < 1) throw Error{H2D_EINVAL, "nrhs < 1"};
   Handle& h = H->h;
-  if (order != H2D_ORDER_ORIGINAL && order != H2D_ORDER_TREE && order != H2D_ORDER_GATHERED)
+  if (order != H2D_ORDER_ORIGINAL && order != H2D_ORDER_TREE && order != H2D_ORDER_GATHERED &&
+      order != H2D_ORDER_LOCAL)
     throw Error{H2D_EINVAL, "bad order"};
+  if (order == H2D_ORDER_LOCAL && !h.comm)
+    throw Error{H2D_EINVAL, "LOCAL order needs a communicator (options.nccl_id or options.allgather)"};
   if (order == H2D_ORDER_GATHERED && h.rank_rows.empty())
     throw Error{H2D_EINVAL, "GATHERED order needs a world/rank partition"};
   cudaStream_t s = h.stream;
@@ -629,6 +655,7 @@ int hodlr2d_gmres(hodlr2d_t H, const double* b, double* x, double tol, int resta
   // argument checks before any staging allocation (nothing to release on these errors)
   if (h.row_begin != 0 || h.row_end != h.n) throw Error{H2D_EINVAL, "GMRES needs a single-rank handle"};
   if (!(tol > 0.0) || restart < 1 || max_iter < 1) throw Error{H2D_EINVAL, "bad GMRES parameters"};
+  if (restart > 65535) throw Error{H2D_EINVAL, "restart > 65535 (grid limit of the dot-product launch)"};
   cudaStream_t s = h.stream;
   const bool bdev = is_device_ptr(b), xdev = is_device_ptr(x);
   const double* db = b;
@@ -745,6 +772,9 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   info->small_items[1] = h.n_bitems - h.n_bbig;
   info->apply_launches = (h.n_abig > 0) + (h.n_aitems > h.n_abig) + (h.n_bbig > 0) + (h.n_bitems > h.n_bbig) +
                          (h.symapply && h.n_b1items > 0);
+  info->comm_kind = comm_kind(h);
+  info->local_items[0] = h.n_abig_loc;
+  info->local_items[1] = h.n_asmall_loc;
   (void)rsum;
   return H2D_OK;
   H2D_CATCH
@@ -897,6 +927,28 @@ int hodlr2d_destroy(hodlr2d_t H) {
 
 const char* hodlr2d_last_error(void) { return g_last_error.c_str(); }
 
+int hodlr2d_set_diag(hodlr2d_t H, const char* name, int value) {
+  H2D_TRY
+  if (!H || !name) throw Error{H2D_EINVAL, "null argument"};
+  Handle& h = H->h;
+  const std::string nm(name);
+  if (nm == "p2p_serial") h.diag_p2p_serial = value != 0;
+  else if (nm == "p2p_onestream") h.diag_p2p_onestream = value != 0;
+  else if (nm == "dual_norow") h.diag_dual_norow = value != 0;
+  else if (nm == "copy_stream") h.diag_copy_stream = value != 0;
+  else throw Error{H2D_EINVAL, "unknown diagnostics switch " + nm};
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_comm_unique_id(unsigned char* id) {
+  H2D_TRY
+  if (!id) throw Error{H2D_EINVAL, "null id"};
+  comm_unique_id(id);
+  return H2D_OK;
+  H2D_CATCH
+}
+
 int hodlr2d_leaf_costs(hodlr2d_t H, double* costs) {
   H2D_TRY
   if (!H || !costs) throw Error{H2D_EINVAL, "null argument"};
@@ -920,13 +972,14 @@ int hodlr2d_leaf_costs(hodlr2d_t H, double* costs) {
 
 int hodlr2d_partition(const int32_t* leaf_start, int kappa, int world, int rank,
                       int64_t* leaf_begin, int64_t* leaf_end) {
+  H2D_TRY
+  // the same depth cap as the build (leaf_start must hold 4^kappa + 1 entries)
   if (!leaf_start || !leaf_begin || !leaf_end || kappa < 0 || kappa > 15 || world < 1 || rank < 0 ||
-      rank >= world) {
-    set_error(H2D_EINVAL, "bad partition arguments");
-    return H2D_EINVAL;
-  }
+      rank >= world)
+    throw Error{H2D_EINVAL, "bad partition arguments"};
   partition_leaves(leaf_start, kappa, world, rank, leaf_begin, leaf_end);
   return H2D_OK;
+  H2D_CATCH
 }
 
 }  // extern "C"

@@ -208,14 +208,29 @@ void gmres_solve(Handle& h, const double* d_b, double* d_x, double tol, int rest
       ++its;
       if (std::fabs(g[(size_t)j + 1]) / bnorm < tol || its >= max_iter || d == 0.0) break;
     }
+    // a zero diagonal (d == 0 without convergence: the Krylov space stopped growing and H is
+    // singular there) would divide by zero: keep the columns before it (their least-squares
+    // solution is still exact) and stop after this update
+    bool singular = false;
+    for (int i = 0; i < k; ++i)
+      if (Hij(i, i) == 0.0) { k = i; singular = true; break; }
     for (int i = k - 1; i >= 0; --i) {   // back substitution
       double t = g[(size_t)i];
       for (int l = i + 1; l < k; ++l) t -= Hij(i, l) * y[(size_t)l];
       y[(size_t)i] = t / Hij(i, i);
     }
-    H2D_CUDA(cudaMemcpyAsync(ydev, y.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
-    vupdate_kernel<<<grid, 256, 0, s>>>(V, n, k, ydev, 1.0, xt, n);
-    H2D_LAUNCH_CHECK();
+    if (k > 0) {
+      H2D_CUDA(cudaMemcpyAsync(ydev, y.data(), k * sizeof(double), cudaMemcpyHostToDevice, s));
+      vupdate_kernel<<<grid, 256, 0, s>>>(V, n, k, ydev, 1.0, xt, n);
+      H2D_LAUNCH_CHECK();
+    }
+    if (singular) {   // true residual of the returned x, then stop (H2D_WNOCONV unless below tol)
+      G.matvec(xt, w);
+      residual_kernel<<<grid, 256, 0, s>>>(bt, w, v0, n);
+      H2D_LAUNCH_CHECK();
+      relres = std::sqrt(G.norm2_host(v0)) / bnorm;
+      break;
+    }
   }
   permute_out_kernel<<<grid, 256, 0, s>>>(xt, h.d_perm, n, d_x);
   H2D_LAUNCH_CHECK();

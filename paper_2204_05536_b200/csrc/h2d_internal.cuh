@@ -202,6 +202,8 @@ struct LevelPtrs {
   const double* Ub[H2D_MAX_LEVELS + 1];   // symmetric apply: first-side U box panels
 };
 
+struct Comm;   // comm.cu: the handle's communicator (S11)
+
 struct Handle {
   int device = 0;
   cudaStream_t stream = 0;
@@ -255,6 +257,10 @@ struct Handle {
   int32_t* d_p2p_gen = nullptr;           // leaves of the generic P2P kernel
   int64_t n_p2p_fast = 0, n_p2p_gen = 0;
   int64_t n_abig = 0, n_bbig = 0;         // stage A / B items on the ring (the rest: small-item kernels)
+  // H2D_ORDER_LOCAL (communicator): the stage-A items whose column box lies in the served
+  // rows come first in both the ring and the small-item lists; they run during the gather
+  Comm* comm = nullptr;
+  int64_t n_abig_loc = 0, n_asmall_loc = 0;
   int32_t* d_p2p_warp = nullptr;          // <= 32-point leaves of the warp-per-leaf P2P kernel
   int64_t n_p2p_warp = 0;
   int64_t n_p2p_warp_rpl[3] = {0, 0, 0};  // warp-kernel leaves with 1 / 2 / 3 rows per lane
@@ -304,6 +310,10 @@ struct Handle {
   // onto their own low-priority streams so their under-filled grids overlap
   cudaStream_t p2p_side[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_p2p_fork = nullptr, ev_p2p_side[3] = {nullptr, nullptr, nullptr};
+  // diagnostics switches of the matvec: read once from the environment at
+  // build, changeable per handle with hodlr2d_set_diag (never per call from the environment)
+  bool diag_p2p_serial = false, diag_p2p_onestream = false, diag_dual_norow = false;
+  bool diag_copy_stream = true;
   // matvec work buffers
   double* d_xtree = nullptr;              // [n]
   double* d_ybuf = nullptr;               // [n] staging for host y
@@ -354,8 +364,18 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
 void finalize_schedule(Handle& h);                                // apply.cu
 // Copy block e of level l out of the panels to host arrays (U m x r, V n x r, col-major).
 void unpack_block(Handle& h, int l, int64_t e, int* m, int* n, int* r, double* U, double* V);
+// gather: H2D_ORDER_LOCAL with a communicator — x_tree holds only the served rows when the
+// call starts; the local stage-A items run before the all-gather completes (comm.cu)
 void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out,
-                 int64_t y_row0);                                 // apply.cu (S7-S9)
+                 int64_t y_row0, bool gather = false);            // apply.cu (S7-S9)
+// comm.cu (S11 behind the ABI)
+void comm_init(Handle& h);
+void comm_destroy(Handle& h);
+void comm_unique_id(unsigned char* id);
+int comm_kind(const Handle& h);   // 0 none, 1 NCCL, 2 host callback
+void comm_gather_start(Handle& h, const double* d_xl, double* d_xtree);
+void comm_gather_exchange(Handle& h);
+cudaEvent_t comm_gather_finish(Handle& h, double* d_xtree, cudaStream_t st);
 void permute_in(Handle& h, const double* d_x, double* d_xtree);   // apply.cu (S10)
 // per-matvec CUDA events (timing mode): 0 start, 1 after input permute/unpad (caller
 // stream); 2 after stage A, 3 after stage B (high-priority stream); 4 after joining the

@@ -147,7 +147,7 @@ def test_small_item_kernels(h2d, symmetric):
 def test_p2p_side_streams_bit_identical(h2d):
     """The near-field classes (generic CTA leaves, warp leaves of 1 / 2 / 3 rows per lane) run
     on their own low-priority streams; every slot value has one writer and a fixed summation
-    order, so the result equals the one-stream schedule (H2D_P2P_ONESTREAM=1) bit for bit.
+    order, so the result equals the one-stream schedule (set_diag("p2p_onestream", 1)) bit for bit.
     Chebyshev 300^2 at the depth rule with N_max 500: corner leaves of hundreds of points
     (generic kernel) beside thousands of small ones."""
     pts = W.chebyshev_grid(300)
@@ -156,11 +156,9 @@ def test_p2p_side_streams_bit_identical(h2d):
     assert warp > 0 and generic > 0, op.info()["p2p_leaves"]
     x = W.random_vector(pts.shape[0], 5600)
     y = op.matvec(dev(x)).cpu().numpy()
-    os.environ["H2D_P2P_ONESTREAM"] = "1"
-    try:
-        y1 = op.matvec(dev(x)).cpu().numpy()
-    finally:
-        os.environ.pop("H2D_P2P_ONESTREAM")
+    op.set_diag("p2p_onestream", 1)
+    y1 = op.matvec(dev(x)).cpu().numpy()
+    op.set_diag("p2p_onestream", 0)
     assert np.array_equal(y, y1)
     yd = oracle.dense_matvec(pts, x, KID["rbf_phi1"], 1e-3, 1.0, 90000.0)
     assert rel(y, yd) <= 1e-10

@@ -124,6 +124,54 @@ def test_dense_matvec_shift_and_scale_definition():
     assert y[0] == 1.0 and y[1] == pytest.approx(1 / math.sqrt(1 + (d / 0.1) ** 2), rel=1e-15)
 
 
+@pytest.mark.parametrize("kid,c,scale,shift", [(0, 1.0, 1.0, 0.0), (1, 0.05, 1.0, 0.0), (2, 1.0, 1.0, 0.0),
+                                               (3, 1e-3, 1.0, 4096.0), (4, 1e-3, 1.0, 4096.0),
+                                               (0, 1.0, 2.0 ** -22, 1.0), (1, 0.3, -0.5, 2.0),
+                                               (100, 1.0, 1.0, 0.0)])
+def test_dense_rows_pinned_to_dense_matvec(kid, c, scale, shift):
+    """oracle_dense_rows is the reference of every full-size GPU check (sampled rows at
+    N = 2^20 .. 2^24, R10).  Pinned here to the full dense product (itself pinned to hand
+    values, the kappa = 0 operator and the shift/scale definition) at N = 4096 with coincident
+    points (K(0) := K0 by distance, R8): every row, in seeded random order and with repeats,
+    must equal the corresponding entry of dense_matvec up to summation rounding, and a few
+    rows must equal an independent numpy evaluation of A_ij = scale K(|p_i - p_j|) + shift
+    delta_ij."""
+    pts = W.uniform_points(4096, 404)
+    pts[4000:4010] = pts[100:110]                                   # coincident points
+    x = W.random_vector(4096, 405)
+    y = oracle.dense_matvec(pts, x, kid, c, scale, shift, test_rank=3)
+    rows = np.random.default_rng(406).permutation(np.concatenate([np.arange(4096), [5, 5, 4095]]))
+    yr = oracle.dense_rows(pts, x, rows, kid, c, scale, shift, test_rank=3)
+    assert np.max(np.abs(yr - y[rows])) <= 1e-13 * np.max(np.abs(y))
+    # independent evaluation of a few rows straight from the kernel definitions
+    some = np.array([0, 100, 4000, 4095, 2048])
+    d = pts[some, None, :] - pts[None, :, :]
+    r = np.hypot(d[..., 0], d[..., 1])
+    safe = np.where(r > 0, r, 1.0)
+    if kid == 0:
+        K = np.where(r > 0, np.log(safe), 0.0)
+    elif kid == 1:
+        K = 1.0 / np.sqrt(1.0 + (r / c) ** 2)
+    elif kid == 2:
+        K = np.where(r > 0, 1.0 / safe, 0.0)
+    elif kid == 3:   # phi_1 (P:1035-1040)
+        K = np.where(r >= c, np.log(safe) / math.log(c), (safe * np.log(safe) - 1) / (c * math.log(c) - 1))
+        K = np.where(r > 0, K, 0.0)
+    elif kid == 4:   # phi_2 (P:1042-1046)
+        K = np.where(r >= c, c / safe, r / c)
+        K = np.where(r > 0, K, 0.0)
+    else:            # test kernel: sum_s cos((s+1) p.x + 0.5 s p.y) cos(...) (hodlr2d.h)
+        s = np.arange(3)
+        fp = np.cos((s[None, :] + 1) * pts[some, 0:1] + 0.5 * s[None, :] * pts[some, 1:2])
+        fq = np.cos((s[None, :] + 1) * pts[:, 0:1] + 0.5 * s[None, :] * pts[:, 1:2])
+        K = fp @ fq.T
+    A = scale * K
+    A[np.arange(len(some)), some] += shift
+    ref = A @ x
+    assert np.max(np.abs(oracle.dense_rows(pts, x, some, kid, c, scale, shift, test_rank=3) - ref)) \
+        <= 1e-12 * max(1.0, np.max(np.abs(ref)))
+
+
 def test_scatter_and_linearity():
     n = 600
     pts = W.uniform_points(n, 21)
