@@ -76,7 +76,7 @@ __device__ __forceinline__ double warp_transpose_sum8(const double (&c)[8], int 
 
 constexpr int kSymTile = 96, kSymMaxB = kSymTile / 16;
 
-// 0.5 log(r2) for normal r2 > 0: r2 = 2^e m, m in [1, 2); c_k = 1 + (k + 1/2)/128 is the
+// 0.5 log(r2) for r2 > 0: r2 = 2^e m, m in [1, 2); c_k = 1 + (k + 1/2)/128 is the
 // centre of m's 1/128 bin (k = top 7 mantissa bits), tab[k] = (1/c_k, 0.5 log c_k);
 // 0.5 log r2 = e ln2/2 + 0.5 log c_k + 0.5 log1p(f), f = m/c_k - 1, |f| <= 2^-8, with
 // 0.5 log1p(f) = f p(f), p the degree-5 Taylor polynomial (truncation f^7/7 <= 2e-18).
@@ -85,9 +85,16 @@ __constant__ double c_hlog[8] = {0.34657359027997264,   // ln2 / 2 (high part)
                                  1.1595234069231498e-17, // ln2 / 2 (low part)
                                  0.5, -0.25, 1.0 / 6.0, -0.125, 0.1, -1.0 / 12.0};
 
+// Subnormal r2 (points closer than ~1.5e-154) are normalised in the integer pipe: the
+// mantissa is shifted until its leading one is the implicit bit (sh = 0 for normal r2) and
+// the exponent becomes 1 - sh - 1023.  r2 = 0 gives a finite value the callers replace by
+// K(0) = 0 (R8).
 __device__ __forceinline__ double hlog_r2(double r2, const double2* __restrict__ tab) {
-  const long long bits = __double_as_longlong(r2);
-  const int e = (int)(bits >> 52) - 1023;
+  long long bits = __double_as_longlong(r2);
+  const int E = (int)(bits >> 52);
+  const int sh = max(0, __clzll(bits) - 11);
+  bits <<= sh;
+  const int e = (E == 0 ? 1 - sh : E) - 1023;
   const int k = (int)(bits >> 45) & 127;
   const double mnt = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
   const double2 tb = tab[k];

@@ -162,3 +162,31 @@ def test_p2p_side_streams_bit_identical(h2d):
     assert np.array_equal(y, y1)
     yd = oracle.dense_matvec(pts, x, KID["rbf_phi1"], 1e-3, 1.0, 90000.0)
     assert rel(y, yd) <= 1e-10
+
+
+@pytest.mark.parametrize("path", ["warp", "cta", "generic"])
+def test_log_kernel_subnormal_distances(h2d, path):
+    """Points closer than ~1.5e-154 have a subnormal r^2; the near field's table log
+    (hlog_r2) normalises it instead of reading a zero exponent field.
+    Pairs 1e-160 apart (r^2 = 1e-320, K = 0.5 log r^2 ~ -368) inside leaves of every
+    near-field path: the warp kernel (<= 96 points), the CTA kernel (warp path off) and the
+    generic kernel (> 96 points), plus the multi-RHS near field; vs the oracle's dense
+    product (libm log)."""
+    base = W.uniform_points(3000, 4160)
+    t = np.linspace(-0.95, 0.95, 40)
+    extra = [np.stack([np.zeros(40), t], 1), np.stack([1e-160 * np.arange(1, 41), t], 1),   # |dx| <= 4e-159
+             np.stack([t[:20], np.zeros(20)], 1), np.stack([t[:20], np.full(20, 3e-155)], 1)]   # dy = 3e-155
+    pts = np.concatenate([base] + extra)
+    d = pts[3000:3040] - pts[3040:3080]
+    assert np.all((d ** 2).sum(1) < 2.2250738585072014e-308) and np.all((d ** 2).sum(1) > 0)
+    leaf = {"warp": 64, "cta": 64, "generic": 200}[path]
+    op = build(h2d, pts, "log", leaf, 1e-10, nowarp=(path == "cta"))
+    warp, fast, generic = op.info()["p2p_leaves"]
+    assert {"warp": warp, "cta": fast, "generic": generic}[path] > 0, op.info()["p2p_leaves"]
+    x = W.random_vector(pts.shape[0], 4161)
+    yd = oracle.dense_matvec(pts, x, 0)
+    assert rel(op.matvec(dev(x)).cpu().numpy(), yd) <= 1e-9
+    X = np.stack([W.random_vector(pts.shape[0], 4170 + k) for k in range(8)])
+    Y = op.matvec_multi(dev(X)).cpu().numpy()
+    for k in (0, 7):
+        assert rel(Y[k], oracle.dense_matvec(pts, X[k], 0)) <= 1e-9

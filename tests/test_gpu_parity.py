@@ -453,3 +453,32 @@ def test_leaf_costs_and_weighted_partition(h2d):
     fc = full.leaf_costs()
     inf = full.info()
     assert abs(fc.sum() - (8 * (inf["u_values"] + inf["v_values"]) + 24 * cfg.n)) <= 0.05 * fc.sum()
+
+
+# ------------------------------------------------------------------ ACA stopping rule (R7)
+
+R7_CASES = {
+    # name: (points, kernel id, c, scale, shift, leaf, tol, box)
+    "c5_geometry_16384_imq": (lambda: W.uniform_points(16384, 20220405), 1, 0.05, 1.0, 0.0, 64, 1e-6,
+                              ((-1.0, -1.0), 2.0)),
+    "c2_full_imq_1e-6": (lambda: W.config_points(W.CONFIGS["c2"]), 1, 0.1, 1.0, 0.0, 64, 1e-6, ((-1.0, -1.0), 2.0)),
+    "c4_geometry_256sq_ie": (lambda: W.grid_points(256, (0.0, 0.0), 1.0), 0, 1.0, 2.0 ** -16, 1.0, 64, 1e-8,
+                             ((0.0, 0.0), 1.0)),
+}
+
+
+@pytest.mark.parametrize("name", list(R7_CASES))
+def test_r7_stopping_rule_gpu_factors(h2d, name):
+    """GPU-built factors (the batched ACA under R7) on the geometries where weaker stopping
+    rules nearly failed: exact dense product, margin 3 x tol (bar 10 x)."""
+    gen, kid, c, scale, shift, leaf, tol, box = R7_CASES[name]
+    pts = gen()
+    op = h2d.Hodlr2d.build(dev(pts), kid, leaf, tol, c=c, scale=scale, shift=shift, box_lo=box[0], box_side=box[1])
+    worst = 0.0
+    for k in range(2):
+        x = W.random_vector(pts.shape[0], 7300 + k)
+        yd = oracle.dense_matvec(pts, x, kid, c, scale, shift)
+        y = gpu_matvec(op, x)
+        worst = max(worst, float(np.linalg.norm(y - yd) / np.linalg.norm(yd - shift * x)))
+    print(f"{name}: max rel-l2 error / tol = {worst / tol:.3f}")
+    assert worst <= 3.0 * tol, worst / tol
