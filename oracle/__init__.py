@@ -69,6 +69,12 @@ def lib():
             L.oracle_matvec.argtypes = [vp, vp, vp, i]
             L.oracle_save_factors.argtypes = [vp, C.c_char_p]
             L.oracle_set_threads.argtypes = [i]
+            L.oracle_leaves.argtypes = [vp, vp, vp]
+            L.oracle_leaves.restype = i64
+            L.oracle_op_level_lists.argtypes = [vp, i, vp, vp]
+            L.oracle_op_level_lists.restype = i64
+            L.oracle_dense_pairs.argtypes = [vp, vp, vp, vp]
+            L.oracle_dense_pairs.restype = i64
             _lib = L
     return _lib
 
@@ -227,6 +233,28 @@ class Operator:
         y = np.zeros(self.n)
         lib().oracle_matvec(self._h, _p(x), _p(y), 0 if order == "original" else 1)
         return y
+
+    def leaves(self):
+        """(level, box) of every leaf, Morton order (adaptive tree R24; balanced: level kappa)."""
+        k = int(lib().oracle_leaves(self._h, None, None))
+        lv = np.zeros(max(k, 1), np.int32); bx = np.zeros(max(k, 1), np.int32)
+        lib().oracle_leaves(self._h, _p(lv), _p(bx))
+        return lv[:k], bx[:k]
+
+    def op_lists(self, level):
+        """The operator's interaction-list CSR of a level (adaptive: existing boxes only)."""
+        tot = int(lib().oracle_op_level_lists(self._h, level, None, None))
+        off = np.zeros((1 << (2 * level)) + 1, np.int32)
+        col = np.zeros(max(tot, 1), np.int32)
+        lib().oracle_op_level_lists(self._h, level, _p(off), _p(col))
+        return off, col[:tot]
+
+    def dense_pairs(self):
+        """Dense blocks as arrays (level, X, Y), ordered by (level, X, Y)."""
+        k = int(lib().oracle_dense_pairs(self._h, None, None, None))
+        a, b, c = (np.zeros(max(k, 1), np.int32) for _ in range(3))
+        lib().oracle_dense_pairs(self._h, _p(a), _p(b), _p(c))
+        return a[:k], b[:k], c[:k]
 
     def save_factors(self, path):
         rc = lib().oracle_save_factors(self._h, str(path).encode())

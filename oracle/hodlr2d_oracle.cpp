@@ -284,9 +284,17 @@ struct Oracle {
     std::vector<int32_t> perm;           // tree position -> original index
     std::vector<int32_t> leaf_start;     // 4^kappa + 1
     std::vector<std::vector<int32_t>> il_off, il_col;  // index l = 1..kappa (0 unused)
-    std::vector<int32_t> nf_off, nf_col;
     std::vector<std::vector<Block>> blocks;              // per level, CSR order
-    std::vector<std::vector<double>> dense;              // per near-field pair, row-major |X|x|Y|
+    // Dense (near-field) blocks K(X, Y) at level l, ordered by (l, X, Y) (Alg. 1 l.5): the
+    // balanced tree's leaf pairs Y in {X} u E_X at l = kappa; the adaptive tree's pairs of
+    // existing boxes Y in {X} u E_X at any level with X or Y a leaf (R24).
+    struct DensePair { int l, X, Y; };
+    std::vector<DensePair> dpairs;
+    std::vector<std::vector<double>> dense;              // per dense pair, row-major |X|x|Y|
+    // adaptive quadtree (R24, NEXT N4; depth = -3): per level l = 0..kappa, box b exists iff
+    // its parent is subdivided; a box is subdivided iff it holds more than N_max points
+    bool adaptive = false;
+    std::vector<std::vector<uint8_t>> exists, subdiv;
     int64_t row_lo = 0, row_hi = 0;                      // rows this operator serves (tree order)
     double build_seconds = 0;
 
@@ -518,6 +526,8 @@ void* oracle_build(const double* pts, int64_t n, int kernel_id, double c, double
     // (P:878): the smallest kappa at which no leaf holds more than N_max = leaf_size points
     // (R22), searched upwards from the R1 depth, which is a lower bound.
     o->kappa = depth >= 0 ? depth : oracle_depth(n, leaf_size);
+    o->adaptive = depth == -3;
+    if (depth < -3) { set_err(-1, "depth < -3"); delete o; return nullptr; }
     int kappa = o->kappa;
     for (;;) {
         int64_t nleaf = (int64_t)1 << (2 * kappa);
@@ -526,7 +536,7 @@ void* oracle_build(const double* pts, int64_t n, int kernel_id, double c, double
         int rc = oracle_tree(pts, n, o->lo[0], o->lo[1], o->side, kappa, nullptr, o->perm.data(),
                              o->leaf_start.data());
         if (rc != 0) { delete o; return nullptr; }
-        if (depth != -2) break;
+        if (depth != -2 && depth != -3) break;   // -3: the adaptive tree's deepest level is R22's
         int64_t mx = 0;
         for (int64_t b = 0; b < nleaf; ++b) mx = std::max<int64_t>(mx, o->leaf_start[(size_t)b + 1] - o->leaf_start[(size_t)b]);
         if (mx <= leaf_size) break;
@@ -541,7 +551,24 @@ void* oracle_build(const double* pts, int64_t n, int kernel_id, double c, double
     }
     o->row_lo = 0; o->row_hi = n;
     if (row_hi > 0) { o->row_lo = std::max<int64_t>(0, row_lo); o->row_hi = std::min<int64_t>(n, row_hi); }
-    // Alg. 1 l.4: lists
+    // Adaptive quadtree (R24): top-down, a box exists iff its parent is subdivided and is
+    // subdivided iff it holds more than N_max = leaf_size points (below the deepest level,
+    // which R22's rule fixes).  Balanced tree: every box exists, all but the leaves are
+    // subdivided.
+    o->exists.assign((size_t)kappa + 1, {});
+    o->subdiv.assign((size_t)kappa + 1, {});
+    for (int l = 0; l <= kappa; ++l) {
+        int64_t nb = (int64_t)1 << (2 * l);
+        o->exists[l].assign((size_t)nb, 0);
+        o->subdiv[l].assign((size_t)nb, 0);
+        for (int64_t b = 0; b < nb; ++b) {
+            bool ex = l == 0 || o->subdiv[l - 1][(size_t)(b >> 2)];
+            o->exists[l][(size_t)b] = ex;
+            if (!ex || l == kappa) continue;
+            o->subdiv[l][(size_t)b] = o->adaptive ? (o->box_end(l, (int)b) - o->box_begin(l, (int)b) > leaf_size) : 1;
+        }
+    }
+    // Alg. 1 l.4: lists (adaptive: Eq. eq:ilist restricted to existing boxes, R24)
     o->il_off.resize((size_t)kappa + 1);
     o->il_col.resize((size_t)kappa + 1);
     o->blocks.resize((size_t)kappa + 1);
@@ -551,6 +578,19 @@ void* oracle_build(const double* pts, int64_t n, int kernel_id, double c, double
         o->il_off[l].resize((size_t)nb + 1);
         o->il_col[l].resize((size_t)tot);
         oracle_level_lists(l, o->il_off[l].data(), o->il_col[l].data());
+        if (o->adaptive) {   // keep the members of existing boxes that exist themselves
+            std::vector<int32_t> off((size_t)nb + 1, 0), col;
+            for (int64_t X = 0; X < nb; ++X) {
+                off[(size_t)X] = (int32_t)col.size();
+                if (!o->exists[l][(size_t)X]) continue;
+                for (int32_t e = o->il_off[l][X]; e < o->il_off[l][X + 1]; ++e)
+                    if (o->exists[l][(size_t)o->il_col[l][(size_t)e]]) col.push_back(o->il_col[l][(size_t)e]);
+            }
+            off[(size_t)nb] = (int32_t)col.size();
+            o->il_off[l] = off;
+            o->il_col[l] = col;
+            tot = (int64_t)col.size();
+        }
         o->blocks[l].resize((size_t)tot);
         for (int64_t X = 0; X < nb; ++X)
             for (int32_t e = o->il_off[l][X]; e < o->il_off[l][X + 1]; ++e) {
@@ -563,24 +603,34 @@ void* oracle_build(const double* pts, int64_t n, int kernel_id, double c, double
                 B.n = (int)(o->box_end(l, B.Y) - B.c0);
             }
     }
-    int64_t nnf = oracle_near_lists(kappa, nullptr, nullptr);
-    o->nf_off.resize((size_t)nleaf + 1);
-    o->nf_col.resize((size_t)nnf);
-    oracle_near_lists(kappa, o->nf_off.data(), o->nf_col.data());
-    // Alg. 1 l.5: dense self + edge blocks at the leaves (only for served rows)
-    o->dense.resize((size_t)nnf);
-#pragma omp parallel for schedule(dynamic, 16)
-    for (int64_t X = 0; X < nleaf; ++X) {
-        if (!o->row_box_active(kappa, (int)X)) continue;
-        int64_t r0 = o->box_begin(kappa, (int)X), m = o->box_end(kappa, (int)X) - r0;
-        for (int32_t e = o->nf_off[X]; e < o->nf_off[X + 1]; ++e) {
-            int Y = o->nf_col[(size_t)e];
-            int64_t c0 = o->box_begin(kappa, Y), nn = o->box_end(kappa, Y) - c0;
-            auto& D = o->dense[(size_t)e];
-            D.resize((size_t)(m * nn));
-            for (int64_t i = 0; i < m; ++i)
-                for (int64_t j = 0; j < nn; ++j) D[(size_t)(i * nn + j)] = o->entry(r0 + i, c0 + j);
+    (void)nleaf;
+    // Alg. 1 l.5: dense blocks.  Balanced: the leaves' {X} u E_X at l = kappa.  Adaptive
+    // (R24): for existing X and Y in {X} u E_X at level l, dense when X or Y is a leaf (an
+    // edge-sharing pair of two subdivided boxes recurses into its children instead).
+    for (int l = 0; l <= kappa; ++l) {
+        int64_t nb = (int64_t)1 << (2 * l);
+        for (int64_t X = 0; X < nb; ++X) {
+            if (!o->exists[l][(size_t)X]) continue;
+            auto Ys = edge_set(l, (int)X);
+            Ys.push_back((int)X);
+            std::sort(Ys.begin(), Ys.end());
+            for (int Y : Ys)
+                if (o->exists[l][(size_t)Y] && (!o->subdiv[l][(size_t)X] || !o->subdiv[l][(size_t)Y]))
+                    o->dpairs.push_back(Oracle::DensePair{l, (int)X, Y});
         }
+    }
+    // their entries (only for served rows)
+    o->dense.resize(o->dpairs.size());
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t e = 0; e < (int64_t)o->dpairs.size(); ++e) {
+        const auto& P = o->dpairs[(size_t)e];
+        if (!o->row_box_active(P.l, P.X)) continue;
+        int64_t r0 = o->box_begin(P.l, P.X), m = o->box_end(P.l, P.X) - r0;
+        int64_t c0 = o->box_begin(P.l, P.Y), nn = o->box_end(P.l, P.Y) - c0;
+        auto& D = o->dense[(size_t)e];
+        D.resize((size_t)(m * nn));
+        for (int64_t i = 0; i < m; ++i)
+            for (int64_t j = 0; j < nn; ++j) D[(size_t)(i * nn + j)] = o->entry(r0 + i, c0 + j);
     }
     // Alg. 1 l.6: ACA for every member of every interaction list, l = kappa..1.
     // symmetric = 1 (NEXT N1, R23; the paper assumes a symmetric matrix):
@@ -677,20 +727,29 @@ int oracle_matvec(void* h, const double* x_in, double* y_out, int order) {
     int kappa = o->kappa;
     std::vector<double> x((size_t)n), b((size_t)n, 0.0);
     for (int64_t s = 0; s < n; ++s) x[(size_t)s] = order == 0 ? x_in[o->perm[(size_t)s]] : x_in[s];
-    int64_t nleaf = (int64_t)1 << (2 * kappa);
-    // lines 2-9: dense self and edge-sharing blocks at the leaves
+    // lines 2-9: dense blocks (self and edge-sharing; adaptive: at every level, R24), level
+    // by level; inside a level the row boxes are disjoint, so they run in parallel (each row
+    // box's pairs in ascending Y)
+    for (int l = 0; l <= kappa; ++l) {
+        std::vector<int64_t> first;   // first pair of each row box of this level
+        for (int64_t e = 0; e < (int64_t)o->dpairs.size(); ++e)
+            if (o->dpairs[(size_t)e].l == l && (first.empty() || o->dpairs[(size_t)e].X != o->dpairs[(size_t)first.back()].X))
+                first.push_back(e);
 #pragma omp parallel for schedule(dynamic, 16)
-    for (int64_t X = 0; X < nleaf; ++X) {
-        if (!o->row_box_active(kappa, (int)X)) continue;
-        int64_t r0 = o->box_begin(kappa, (int)X), m = o->box_end(kappa, (int)X) - r0;
-        for (int32_t e = o->nf_off[X]; e < o->nf_off[X + 1]; ++e) {
-            int Y = o->nf_col[(size_t)e];
-            int64_t c0 = o->box_begin(kappa, Y), nn = o->box_end(kappa, Y) - c0;
-            const auto& D = o->dense[(size_t)e];
-            for (int64_t i = 0; i < m; ++i) {
-                double acc = 0.0;
-                for (int64_t j = 0; j < nn; ++j) acc += D[(size_t)(i * nn + j)] * x[(size_t)(c0 + j)];
-                b[(size_t)(r0 + i)] += acc;
+        for (int64_t g = 0; g < (int64_t)first.size(); ++g) {
+            for (int64_t e = first[(size_t)g]; e < (int64_t)o->dpairs.size(); ++e) {
+                const auto& P = o->dpairs[(size_t)e];
+                if (P.l != l || P.X != o->dpairs[(size_t)first[(size_t)g]].X) break;
+                if (!o->row_box_active(l, P.X)) break;
+                int64_t r0 = o->box_begin(l, P.X), m = o->box_end(l, P.X) - r0;
+                int64_t c0 = o->box_begin(l, P.Y), nn = o->box_end(l, P.Y) - c0;
+                const auto& D = o->dense[(size_t)e];
+                for (int64_t i = 0; i < m; ++i) {
+                    if (r0 + i < o->row_lo || r0 + i >= o->row_hi) continue;   // rows served
+                    double acc = 0.0;
+                    for (int64_t j = 0; j < nn; ++j) acc += D[(size_t)(i * nn + j)] * x[(size_t)(c0 + j)];
+                    b[(size_t)(r0 + i)] += acc;
+                }
             }
         }
     }
@@ -726,6 +785,43 @@ int oracle_matvec(void* h, const double* x_in, double* y_out, int order) {
     return 0;
 }
 
+// Adaptive tree structure (R24): leaves (existing, not subdivided boxes) in Morton order of
+// their first level-kappa descendant; returns the count, fills level[] / box[] if non-NULL.
+int64_t oracle_leaves(void* h, int32_t* level, int32_t* box) {
+    auto* o = static_cast<Oracle*>(h);
+    std::vector<std::pair<int64_t, std::pair<int, int>>> L;
+    for (int l = 0; l <= o->kappa; ++l)
+        for (size_t b = 0; b < o->exists[l].size(); ++b)
+            if (o->exists[l][b] && !o->subdiv[l][b])
+                L.push_back({(int64_t)b << (2 * (o->kappa - l)), {l, (int)b}});
+    std::sort(L.begin(), L.end());
+    for (size_t k = 0; k < L.size(); ++k) {
+        if (level) level[k] = L[k].second.first;
+        if (box) box[k] = L[k].second.second;
+    }
+    return (int64_t)L.size();
+}
+
+// The operator's interaction lists of level l (adaptive: restricted to existing boxes).
+int64_t oracle_op_level_lists(void* h, int level, int32_t* off, int32_t* col) {
+    auto* o = static_cast<Oracle*>(h);
+    if (level < 1 || level > o->kappa) return 0;
+    if (off) std::copy(o->il_off[level].begin(), o->il_off[level].end(), off);
+    if (col) std::copy(o->il_col[level].begin(), o->il_col[level].end(), col);
+    return (int64_t)o->il_col[level].size();
+}
+
+// The dense blocks (level, row box, column box), ordered by (level, X, Y).
+int64_t oracle_dense_pairs(void* h, int32_t* level, int32_t* X, int32_t* Y) {
+    auto* o = static_cast<Oracle*>(h);
+    for (size_t k = 0; k < o->dpairs.size(); ++k) {
+        if (level) level[k] = o->dpairs[k].l;
+        if (X) X[k] = o->dpairs[k].X;
+        if (Y) Y[k] = o->dpairs[k].Y;
+    }
+    return (int64_t)o->dpairs.size();
+}
+
 // R11 factor interchange file.
 //   char magic[8] = "H2DFAC01"; int64 N; int32 kappa; int32 kernel_id; double tol, c, scale,
 //   shift, lo_x, lo_y, side; int32 test_rank; int32 reserved;
@@ -741,7 +837,7 @@ int oracle_save_factors(void* h, const char* path) {
     const char magic[8] = {'H', '2', 'D', 'F', 'A', 'C', '0', '1'};
     std::fwrite(magic, 1, 8, f);
     int64_t N = o->N;
-    int32_t kap = o->kappa, kid = o->K.id, tr = o->K.test_rank, res = 0;
+    int32_t kap = o->kappa, kid = o->K.id, tr = o->K.test_rank, res = o->adaptive ? 1 : 0;   // R11/R24
     double d[7] = {o->aca.tol, o->K.c, o->K.scale, o->K.shift, o->lo[0], o->lo[1], o->side};
     std::fwrite(&N, 8, 1, f);
     std::fwrite(&kap, 4, 1, f);
