@@ -61,6 +61,10 @@ def parse():
                          "points, informational line with T_I / T_G (paper values as context)")
     ap.add_argument("--grid-m", type=int, default=500)
     ap.add_argument("--rbf-kernel", default="rbf_phi1", choices=["rbf_phi1", "rbf_phi2"])
+    ap.add_argument("--nmax", type=int, default=500, help="gmres mode: N_max (the paper's 500, P:921)")
+    ap.add_argument("--adaptive", action="store_true",
+                    help="gmres mode: the adaptive quadtree (depth = -3, DESIGN.md R24) instead of the "
+                         "balanced tree at the paper's depth rule (R22)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: functional check of the multi-rank path (host-staged gather)")
     return ap.parse_args()
@@ -708,8 +712,8 @@ def run_gmres(args):
     pts = W.chebyshev_grid(args.grid_m)
     n = pts.shape[0]
     t0 = time.time()
-    op = h2d.Hodlr2d.build(torch.from_numpy(pts).cuda(), args.rbf_kernel, 500, 1e-12, c=1e-3, scale=1.0,
-                           shift=float(n), box_lo=(-1, -1), box_side=2.0, depth=-2)
+    op = h2d.Hodlr2d.build(torch.from_numpy(pts).cuda(), args.rbf_kernel, args.nmax, 1e-12, c=1e-3, scale=1.0,
+                           shift=float(n), box_lo=(-1, -1), box_side=2.0, depth=-3 if args.adaptive else -2)
     torch.cuda.synchronize()
     t_i = time.time() - t0
     inf = op.info()
@@ -734,7 +738,10 @@ def run_gmres(args):
     mv_ms = e0.elapsed_time(e1) / 20
     err = float(torch.linalg.norm(lam_hat - lam) / torch.linalg.norm(lam))
     line = {"mode": "gmres", "workload": f"{args.rbf_kernel}, {args.grid_m}^2 Chebyshev grid, a = 0.001, "
-                                         f"beta = N, ACA 1e-12, N_max 500 (paper depth rule)",
+                                         f"beta = N, ACA 1e-12, N_max {args.nmax} "
+                                         + ("(adaptive quadtree, R24)" if args.adaptive else "(paper depth rule)"),
+            "n_leaves": inf["n_leaves"], "near_pairs": inf["near_pairs"],
+            "factor_gb": (inf["u_values"] + inf["v_values"]) * 8e-9,
             "n": n, "kappa": inf["kappa"], "rank_max": inf["rank_max"],
             "compression_ratio": inf["compression_ratio"], "T_I_s": round(t_i, 3), "T_G_s": round(t_g, 4),
             "T_G_runs_s": [round(v, 4) for v in tgs], "matvec_ms": round(mv_ms, 3),

@@ -98,7 +98,10 @@ typedef struct {
   double box_side;        /* root square side; <= 0 -> bounding square of the points (R2)   */
   int depth;              /* kappa >= 0; -1 -> R1 depth rule (nominal leaf size); -2 -> the
                              paper's rule (Alg. 1 l.3): smallest kappa with no leaf
-                             holding more than leaf_size points (R22)      (default -1) */
+                             holding more than leaf_size points (R22); -3 -> the adaptive
+                             (non-balanced) quadtree of P:914 (R24): a box is split iff it
+                             holds more than leaf_size points; single-rank handles, directed
+                             apply (multi-RHS calls loop over vectors)     (default -1) */
   int max_rank;           /* ACA rank cap per block; hitting it sets H2D_WTRUNC (def. 128)  */
   int aca_consecutive;    /* tolerance hits in a row that stop ACA (R7)        (default 3)  */
   int aca_trim;           /* streak terms dropped on a tolerance stop (R7)     (default 3)  */
@@ -169,6 +172,8 @@ typedef struct {
                                 their small-item (warp-per-item) kernels, B' (symmetric) */
   int64_t small_items[2];    /* stage A boxes / stage B leaves on the small-item kernels */
   int comm_kind;             /* 0 none, 1 NCCL communicator, 2 host all-gather callback  */
+  int adaptive;              /* 1: adaptive quadtree (depth = -3, R24)          */
+  int64_t n_leaves;          /* leaves (adaptive: hodlr2d_copy_leaves; else 4^kappa)      */
   int64_t local_items[2];    /* H2D_ORDER_LOCAL: stage-A items (ring, small) whose column box
                                 is local, run while the x all-gather is in flight        */
 } hodlr2d_info;
@@ -235,6 +240,12 @@ int hodlr2d_copy_tree(hodlr2d_t h, int32_t* perm, int32_t* leaf_start);
  * off[4^level + 1], col[off[4^level]] (partner Morton index, ascending).
  * level = 0 copies the leaf near field {X} u E_X (off[4^kappa + 1]). */
 int hodlr2d_copy_lists(hodlr2d_t h, int level, int32_t* off, int32_t* col);
+
+/* Leaves of the tree in Morton order: level[] and box[] (box index at that level) of each;
+ * returns their count (either array may be NULL).  Balanced trees: the 4^kappa boxes of level
+ * kappa; adaptive trees (depth = -3, R24): the unsplit boxes at their own levels.  -1 for a
+ * NULL handle. */
+int64_t hodlr2d_copy_leaves(hodlr2d_t h, int32_t* level, int32_t* box);
 
 /* Number of directed blocks of a level (CSR length); -1 if level is out of range. */
 int64_t hodlr2d_num_blocks(hodlr2d_t h, int level);

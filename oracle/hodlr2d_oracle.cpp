@@ -540,6 +540,7 @@ void* oracle_build(const double* pts, int64_t n, int kernel_id, double c, double
         int64_t mx = 0;
         for (int64_t b = 0; b < nleaf; ++b) mx = std::max<int64_t>(mx, o->leaf_start[(size_t)b + 1] - o->leaf_start[(size_t)b]);
         if (mx <= leaf_size) break;
+        if (depth == -3 && kappa >= 11) break;   // R24: the adaptive tree stops at level 11
         if (++kappa > 15) { set_err(-1, "no depth <= 15 keeps every leaf <= N_max"); delete o; return nullptr; }
     }
     o->kappa = kappa;

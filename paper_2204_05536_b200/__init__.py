@@ -43,7 +43,7 @@ ABI_FUNCTIONS = (
     "hodlr2d_num_blocks", "hodlr2d_copy_ranks", "hodlr2d_copy_block", "hodlr2d_load_factors",
     "hodlr2d_save_factors", "hodlr2d_stage_times", "hodlr2d_set_timing", "hodlr2d_destroy",
     "hodlr2d_last_error", "hodlr2d_partition", "hodlr2d_gmres", "hodlr2d_matvec_multi", "hodlr2d_leaf_costs",
-    "hodlr2d_comm_unique_id", "hodlr2d_set_diag",
+    "hodlr2d_comm_unique_id", "hodlr2d_set_diag", "hodlr2d_copy_leaves",
 )
 
 
@@ -79,7 +79,8 @@ class Info(C.Structure):
         ("device_bytes", C.c_int64), ("gather_stride", C.c_int64), ("p2p_bytes", C.c_int64),
         ("symmetric_apply", C.c_int), ("p2p_launches", C.c_int), ("p2p_leaves", C.c_int64 * 3),
         ("apply_launches", C.c_int), ("small_items", C.c_int64 * 2),
-        ("comm_kind", C.c_int), ("local_items", C.c_int64 * 2),
+        ("comm_kind", C.c_int), ("adaptive", C.c_int), ("n_leaves", C.c_int64),
+        ("local_items", C.c_int64 * 2),
     ]
 
     def as_dict(self) -> dict:
@@ -134,6 +135,8 @@ def lib() -> C.CDLL:
             L.hodlr2d_leaf_costs.argtypes = [vp, vp]
             L.hodlr2d_comm_unique_id.argtypes = [vp]
             L.hodlr2d_set_diag.argtypes = [vp, C.c_char_p, i]
+            L.hodlr2d_copy_leaves.argtypes = [vp, vp, vp]
+            L.hodlr2d_copy_leaves.restype = i64
             _lib = L
     return _lib
 
@@ -430,6 +433,14 @@ class Hodlr2d:
         ls = np.zeros((1 << (2 * inf["kappa"])) + 1, np.int32)
         _check(lib().hodlr2d_copy_tree(self._h, perm.ctypes.data, ls.ctypes.data))
         return perm, ls
+
+    def leaves(self):
+        """hodlr2d_copy_leaves: (level, box) of every leaf in Morton order."""
+        k = lib().hodlr2d_copy_leaves(self._h, None, None)
+        lv = np.zeros(max(k, 1), np.int32)
+        bx = np.zeros(max(k, 1), np.int32)
+        lib().hodlr2d_copy_leaves(self._h, lv.ctypes.data, bx.ctypes.data)
+        return lv[:k], bx[:k]
 
     def lists(self, level: int):
         kappa = self.info()["kappa"]

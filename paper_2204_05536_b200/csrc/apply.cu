@@ -547,6 +547,72 @@ p2p_fast_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int
 // group (over all RPL rows) by a transposed butterfly (9 double shuffles; lane 4t ends up
 // holding column t).  Same slots as p2p_fast_kernel: s0 (own rows), sL / sD (the
 // neighbour's rows), one writer per value.
+// Adaptive near field (R24): warp per (leaf, 64-row pass); the leaf's dense column ranges
+// (its own blocks and its subdivided ancestors' blocks against leaf neighbours) stream through
+// a per-warp shared-memory tile of 32 points; lane owns rows lane and lane + 32; one writer
+// per row (slot s0), no atomics.  item = (leaf << 8) | pass.
+template <int KID>
+__global__ void __launch_bounds__(256, 3)
+p2p_list_kernel(const int64_t* __restrict__ items, int n_items, int32_t* counter,
+                const int32_t* __restrict__ lf_start, const int64_t* __restrict__ nf_off,
+                const int64_t* __restrict__ nf_rng, const double* __restrict__ px,
+                const double* __restrict__ py, const double* __restrict__ x, KernelParams kp,
+                double* __restrict__ s0) {
+  __shared__ double2 sq[8][32];
+  __shared__ double sxv[8][32];
+  __shared__ double2 tab[128];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (kNeedsLogTable<KID>) hlog_table(tab);
+  __syncthreads();
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(counter, 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= n_items) break;
+    const int64_t it = items[idx];
+    const int64_t lf = it >> 8;
+    const int64_t xs = (int64_t)lf_start[lf] + 64 * (it & 255);
+    const int m = (int)min((int64_t)64, (int64_t)lf_start[lf + 1] - xs);
+    double pi[2], qi[2], acc[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int i = lane + 32 * r;
+      pi[r] = i < m ? px[xs + i] : 0.0;
+      qi[r] = i < m ? py[xs + i] : 0.0;
+      acc[r] = 0.0;
+    }
+    for (int64_t e = nf_off[lf]; e < nf_off[lf + 1]; ++e) {
+      const int64_t c0 = nf_rng[2 * e], cnt = nf_rng[2 * e + 1];
+      for (int64_t t = 0; t < cnt; t += 32) {
+        const int64_t j = t + lane;
+        __syncwarp();
+        sq[w][lane] = j < cnt ? make_double2(px[c0 + j], py[c0 + j]) : make_double2(0.0, 0.0);
+        sxv[w][lane] = j < cnt ? x[c0 + j] : 0.0;
+        __syncwarp();
+        const int nt = (int)min((int64_t)32, cnt - t);
+        for (int jj = 0; jj < nt; ++jj) {
+          const double2 q = sq[w][jj];
+          const double xj = sxv[w][jj];
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            double k;
+            if constexpr (kDistKernel<KID>) {
+              const double dx = pi[r] - q.x, dy = qi[r] - q.y;
+              k = kfast<KID>(fma(dx, dx, dy * dy), tab, kp);
+            } else {
+              k = kernel_eval_t<KID>(kp, pi[r], qi[r], q.x, q.y);
+            }
+            acc[r] = fma(k, xj, acc[r]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      if (lane + 32 * r < m) s0[xs + lane + 32 * r] = acc[r];
+  }
+}
+
 constexpr int kWarpLeaf = 96;      // rows per lane RPL = ceil(m / 32) <= 3 (leaves <= 96 points)
 
 template <int KID, int RPL>
@@ -758,9 +824,9 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
   L.uoff.assign((size_t)std::max<int64_t>(nserved, 0), 0);
   int64_t uo = 0, uvals = 0;
   for (int64_t lf = h.leaf_begin; lf < h.leaf_end; ++lf) {
-    const int64_t X = lf >> sh;
+    const int64_t X = h.leaf_code(lf) >> sh;   // (adaptive: levels below the leaf have no columns)
     const int64_t R = L.ucolbase[(size_t)X + 1] - L.ucolbase[(size_t)X];
-    const int64_t mL = h.leaf_start[(size_t)lf + 1] - h.leaf_start[(size_t)lf];
+    const int64_t mL = h.leaf_e(lf) - h.leaf_s(lf);
     L.uoff[(size_t)(lf - h.leaf_begin)] = uo;
     uo = up16(uo + ((mL + 1) & ~1) * R);
     uvals += mL * R;
@@ -776,10 +842,10 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
   std::vector<UCopyItem> uitems;
   std::vector<VPackItem> vitems;
   for (int64_t lf = h.leaf_begin; lf < h.leaf_end; ++lf) {
-    const int64_t X = lf >> sh;
+    const int64_t X = h.leaf_code(lf) >> sh;
     const int64_t bx0 = h.box_begin(l, X), mX = h.box_end(l, X) - bx0;
-    const int64_t s0 = h.leaf_start[(size_t)lf];
-    const int32_t mL = h.leaf_start[(size_t)lf + 1] - (int32_t)s0;
+    const int64_t s0 = h.leaf_s(lf);
+    const int32_t mL = (int32_t)(h.leaf_e(lf) - s0);
     if (mL == 0) continue;
     double* base = L.U + L.uoff[(size_t)(lf - h.leaf_begin)];
     for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
@@ -893,12 +959,16 @@ void unpack_block(Handle& h, int l, int64_t e, int* m, int* n, int* r, double* U
   }
   if (U) {
     const int sh = 2 * (h.kappa - l);
-    const int64_t lf0 = X << sh, lf1 = (X + 1) << sh;
+    int64_t lf0 = X << sh, lf1 = (X + 1) << sh;
+    if (h.adaptive) {   // the adaptive leaves inside box X (a contiguous run in Morton order)
+      lf0 = std::lower_bound(h.lf_code.begin(), h.lf_code.end(), X << sh) - h.lf_code.begin();
+      lf1 = std::lower_bound(h.lf_code.begin(), h.lf_code.end(), (X + 1) << sh) - h.lf_code.begin();
+    }
     if (lf0 < h.leaf_begin || lf1 > h.leaf_end)
       throw Error{H2D_EINVAL, "block row box not fully served by this handle"};
     for (int64_t lf = lf0; lf < lf1; ++lf) {
-      const int64_t s0 = h.leaf_start[(size_t)lf];
-      const int64_t mL = h.leaf_start[(size_t)lf + 1] - s0;
+      const int64_t s0 = h.leaf_s(lf);
+      const int64_t mL = h.leaf_e(lf) - s0;
       if (mL == 0) continue;
       const int64_t mLp = (mL + 1) & ~1;
       H2D_CUDA(cudaMemcpy2D(U + (s0 - bx0), mm * 8,
@@ -1154,12 +1224,12 @@ void finalize_schedule(Handle& h) {
   std::vector<BItem> bitems;
   std::vector<int64_t> bcost, bleaf;
   for (int64_t lf = h.leaf_begin; lf < h.leaf_end; ++lf) {
-    const int32_t s0 = h.leaf_start[(size_t)lf];
-    const int32_t mL = h.leaf_start[(size_t)lf + 1] - s0;
+    const int32_t s0 = (int32_t)h.leaf_s(lf);
+    const int32_t mL = (int32_t)h.leaf_e(lf) - s0;
     int64_t RL = 0;
     for (int l = 1; l <= h.kappa; ++l) {
       const Level& L = h.levels[(size_t)l];
-      const int64_t X = lf >> (2 * (h.kappa - l));
+      const int64_t X = h.leaf_code(lf) >> (2 * (h.kappa - l));
       RL += L.ucolbase[(size_t)X + 1] - L.ucolbase[(size_t)X];
     }
     for (int32_t r0 = 0; r0 < mL; r0 += kBRows) {
@@ -1180,7 +1250,7 @@ void finalize_schedule(Handle& h) {
       const int cols_s = std::min(kStageVec, kStageDbl / rowsp);
       for (int l = 1; l <= h.kappa; ++l) {
         const Level& L = h.levels[(size_t)l];
-        const int64_t X = lf >> (2 * (h.kappa - l));
+        const int64_t X = h.leaf_code(lf) >> (2 * (h.kappa - l));
         const int R = L.ucolbase[(size_t)X + 1] - L.ucolbase[(size_t)X];
         el[b] += (double)rowsp * R;
         st[b] += (R + cols_s - 1) / cols_s;
@@ -1221,14 +1291,35 @@ void finalize_schedule(Handle& h) {
     const int64_t lf = bleaf[k];
     for (int l = 1; l <= h.kappa; ++l) {
       const Level& L = h.levels[(size_t)l];
-      const int64_t X = lf >> (2 * (h.kappa - l));
+      const int64_t X = h.leaf_code(lf) >> (2 * (h.kappa - l));
       blev.push_back(BLevel{L.uoff[(size_t)(lf - h.leaf_begin)], L.ucolbase[(size_t)X],
                             L.ucolbase[(size_t)X + 1] - L.ucolbase[(size_t)X]});
     }
   }
   // near-field P2P: leaves the persistent fast kernel handles (whole near field served, all
-  // three tiles <= kSymTile points, distance kernel) and the rest (generic kernel)
-  {
+  // three tiles <= kSymTile points, distance kernel) and the rest (generic kernel); adaptive
+  // handles: every leaf on the column-range list kernel (R24)
+  if (h.adaptive) {
+    h.n_p2p_warp = h.n_p2p_fast = h.n_p2p_gen = 0;
+    h.n_p2p_warp_rpl[0] = h.n_p2p_warp_rpl[1] = h.n_p2p_warp_rpl[2] = 0;
+    // items (leaf, 64-row pass), most columns first (dynamic schedule ends with short items)
+    std::vector<std::pair<int64_t, int64_t>> li;
+    for (int64_t lf = h.leaf_begin; lf < h.leaf_end; ++lf) {
+      const int64_t m = h.leaf_e(lf) - h.leaf_s(lf);
+      if (m > 64 * 255) throw Error{H2D_EINVAL, "adaptive leaf larger than 16320 points"};
+      int64_t cols = 0;
+      for (int64_t e = h.ad_nf_off[(size_t)lf]; e < h.ad_nf_off[(size_t)lf + 1]; ++e) cols += h.ad_nf_rng[(size_t)(2 * e + 1)];
+      for (int64_t p = 0; 64 * p < m; ++p) li.push_back({std::min<int64_t>(64, m - 64 * p) * cols, (lf << 8) | p});
+    }
+    std::stable_sort(li.begin(), li.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+    std::vector<int64_t> items(li.size());
+    for (size_t k = 0; k < li.size(); ++k) items[k] = li[k].second;
+    h.n_p2p_list = (int64_t)items.size();
+    h.release(h.d_p2p_list);
+    h.d_p2p_list = h.alloc<int64_t>(items.size());
+    if (!items.empty())
+      H2D_CUDA(cudaMemcpyAsync(h.d_p2p_list, items.data(), items.size() * 8, cudaMemcpyHostToDevice, s));
+  } else {
     auto compact = [](uint32_t v) {
       v &= 0x55555555u;
       v = (v | (v >> 1)) & 0x33333333u;
@@ -1332,6 +1423,8 @@ void finalize_schedule(Handle& h) {
     H2D_CUDA(cudaMemcpyAsync(h.d_bitems, bsorted.data(), bsorted.size() * sizeof(BItem),
                              cudaMemcpyHostToDevice, s));
   if (!h.d_ynear) h.d_ynear = h.alloc<double>(3 * h.n);   // three P2P slots (p2p_sym_kernel)
+  if (h.adaptive)   // the list kernel writes slot 0 only; the combine reads all three
+    H2D_CUDA(cudaMemsetAsync(h.d_ynear + h.n, 0, 2 * h.n * sizeof(double), s));
   if (!h.d_yfar) h.d_yfar = h.alloc<double>(std::max<int64_t>(1, h.row_end - h.row_begin));
   if (!h.d_counters) h.d_counters = h.alloc<int32_t>(8);
   if (!h.hi_stream) {
@@ -1510,6 +1603,19 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
       }
       return h.p2p_side[k];
     };
+    if (h.n_p2p_list > 0) {   // adaptive near field (R24)
+      auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_list_kernel<H2D_KERNEL_LOG>
+                : h.kp.id == H2D_KERNEL_IMQ ? p2p_list_kernel<H2D_KERNEL_IMQ>
+                : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_list_kernel<H2D_KERNEL_ONE_OVER_R>
+                : h.kp.id == H2D_KERNEL_RBF_PHI1 ? p2p_list_kernel<H2D_KERNEL_RBF_PHI1>
+                : h.kp.id == H2D_KERNEL_RBF_PHI2 ? p2p_list_kernel<H2D_KERNEL_RBF_PHI2>
+                                                   : p2p_list_kernel<H2D_KERNEL_TEST_LOWRANK>;
+      H2D_CUDA(cudaMemsetAsync(h.d_counters + 4, 0, sizeof(int32_t), a));
+      const int grid = (int)std::min<int64_t>((int64_t)h.num_sms * 3, (h.n_p2p_list + 7) / 8);
+      kfn<<<grid, 256, 0, a>>>(h.d_p2p_list, (int)h.n_p2p_list, h.d_counters + 4, h.d_lf_start, h.d_ad_nf_off,
+                               h.d_ad_nf_rng, h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear);
+      H2D_LAUNCH_CHECK();
+    }
     if (h.n_p2p_gen > 0) {
       cudaStream_t sg = h.n_p2p_gen < h.num_sms ? side(0) : a;
       auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_sym_kernel<H2D_KERNEL_LOG>

@@ -351,6 +351,8 @@ static void load_factors(Handle& h, const char* path) {
   if (!f) throw Error{H2D_EFACTORS, "truncated header"};
   if (hd.N != h.n || hd.kappa != h.kappa)
     throw Error{H2D_EFACTORS, "file N/kappa do not match the handle"};
+  if ((hd.reserved == 1) != h.adaptive)   // R11 / R24: the adaptive tree's block lists differ
+    throw Error{H2D_EFACTORS, "file and handle disagree on the adaptive tree (depth = -3)"};
   std::vector<int32_t> fperm((size_t)hd.N), perm((size_t)h.n);
   f.read((char*)fperm.data(), hd.N * 4);
   H2D_CUDA(cudaMemcpy(perm.data(), h.d_perm, h.n * 4, cudaMemcpyDeviceToHost));
@@ -489,7 +491,9 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
     throw Error{H2D_EINVAL, "RBF kernels need a = c > 0"};
   if (kernel_id == H2D_KERNEL_RBF_PHI1 && opts->c == 1.0)
     throw Error{H2D_EINVAL, "phi_1 needs a != 1 (log a = 0)"};
-  if (opts->depth < -2) throw Error{H2D_EINVAL, "depth < -2"};
+  if (opts->depth < -3) throw Error{H2D_EINVAL, "depth < -3"};
+  if (opts->depth == -3 && (opts->world > 1 || opts->row_end > 0))
+    throw Error{H2D_EINVAL, "the adaptive tree (depth = -3) supports single-rank handles only"};
   if (opts->max_rank < 1 || opts->aca_consecutive < 1 || opts->aca_trim < 0 ||
       opts->aca_trim > opts->aca_consecutive)
     throw Error{H2D_EINVAL, "bad ACA options"};
@@ -534,13 +538,16 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
     d_pts = tmp;
   }
   build_tree(h, d_pts);
-  if (opts->depth == -2) {
+  if (opts->depth == -2 || opts->depth == -3) {
     // the paper's rule (Alg. 1 l.3; R22): deepen until no leaf holds more than
     // N_max = leaf_size points (the R1 depth is a lower bound)
     for (;;) {
       int32_t mx = 0;
       for (size_t b = 0; b + 1 < h.leaf_start.size(); ++b) mx = std::max(mx, h.leaf_start[b + 1] - h.leaf_start[b]);
       if (mx <= leaf_size) break;
+      // R24: the adaptive tree stops at level 11 (its per-level structures are indexed by
+      // the 4^l Morton grid); boxes of level 11 holding more than N_max points stay leaves
+      if (opts->depth == -3 && h.kappa >= 11) break;
       if (h.kappa >= 15) throw Error{H2D_EINVAL, "no depth <= 15 keeps every leaf <= N_max"};
       for (void* q : {(void*)h.d_perm, (void*)h.d_px, (void*)h.d_py, (void*)h.d_leaf_start}) h.release(q);
       ++h.kappa;
@@ -548,14 +555,23 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
     }
   }
   if (tmp) H2D_CUDA(cudaFreeAsync(tmp, h.stream));
+  if (opts->depth == -3) {   // adaptive quadtree (R24) below R22's deepest level
+    h.adaptive = true;
+    build_adaptive(h);
+  }
   build_lists(h);
   set_partition(h);
+  if (h.adaptive) {   // single rank: every adaptive leaf is served
+    h.leaf_begin = 0;
+    h.leaf_end = (int64_t)h.lf_code.size();
+    build_adaptive_near(h);
+  }
   h.opts.leaf_weights = nullptr;   // caller-owned, read only by the partition above
   comm_init(h);                    // S11 communicator (collective over the world's ranks)
   h.opts.nccl_id = nullptr;        // caller-owned, read only by comm_init
   // symmetric apply (R23): symmetric build on a single-rank handle (the multi-rank row
   // partitions keep the directed panels; stage B' needs every row of a row box)
-  h.symapply = opts->symmetric && h.row_begin == 0 && h.row_end == h.n && h.kappa >= 1 &&
+  h.symapply = opts->symmetric && h.row_begin == 0 && h.row_end == h.n && h.kappa >= 1 && !h.adaptive &&
                !(getenv("H2D_SYMAPPLY") && atoi(getenv("H2D_SYMAPPLY")) == 0);
   h.tree_seconds = now_s() - t0;
   if (opts->skip_aca) skip_factors(h); else run_aca(h);
@@ -606,6 +622,15 @@ int hodlr2d_matvec_multi(hodlr2d_t H, const double* X, double* Y, int nrhs, int 
     throw Error{H2D_EINVAL, "LOCAL order needs a communicator (options.nccl_id or options.allgather)"};
   if (order == H2D_ORDER_GATHERED && h.rank_rows.empty())
     throw Error{H2D_EINVAL, "GATHERED order needs a world/rank partition"};
+  if (order == H2D_ORDER_LOCAL || h.adaptive) {
+    // one vector at a time: the in-library gather (S11) and the adaptive tree (R24) run
+    // through the single-vector matvec
+    const int64_t rows = h.row_end - h.row_begin;
+    const int64_t lx = order == H2D_ORDER_LOCAL ? rows : order == H2D_ORDER_GATHERED ? h.gather_stride * h.opts.world : h.n;
+    const int64_t ly = order == H2D_ORDER_ORIGINAL ? h.n : rows;
+    for (int k = 0; k < nrhs; ++k) do_matvec(h, X + (int64_t)k * lx, Y + (int64_t)k * ly, order);
+    return H2D_OK;
+  }
   cudaStream_t s = h.stream;
   const bool gathered = order == H2D_ORDER_GATHERED;
   const int64_t xlen = gathered ? h.gather_stride * h.opts.world : h.n;
@@ -725,7 +750,12 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   info->u_values = uv;
   info->v_values = vv;
   int64_t near = 0;
-  for (int64_t X = h.leaf_begin; X < h.leaf_end; ++X) {
+  if (h.adaptive) {   // R24: every served leaf's rows times its dense column ranges
+    for (int64_t lf = h.leaf_begin; lf < h.leaf_end; ++lf)
+      for (int64_t e = h.ad_nf_off[(size_t)lf]; e < h.ad_nf_off[(size_t)lf + 1]; ++e)
+        near += (h.leaf_e(lf) - h.leaf_s(lf)) * h.ad_nf_rng[(size_t)(2 * e + 1)];
+  }
+  for (int64_t X = h.leaf_begin; X < h.leaf_end && !h.adaptive; ++X) {
     const int64_t m = h.leaf_start[(size_t)X + 1] - h.leaf_start[(size_t)X];
     for (int32_t e = h.nf_off[(size_t)X]; e < h.nf_off[(size_t)X + 1]; ++e) {
       const int32_t Y = h.nf_col[(size_t)e];
@@ -767,7 +797,9 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   info->p2p_leaves[1] = h.n_p2p_fast;
   info->p2p_leaves[2] = h.n_p2p_gen;
   info->p2p_launches = (h.n_p2p_warp_rpl[0] > 0) + (h.n_p2p_warp_rpl[1] > 0) + (h.n_p2p_warp_rpl[2] > 0) +
-                       (h.n_p2p_fast > 0) + (h.n_p2p_gen > 0);
+                       (h.n_p2p_fast > 0) + (h.n_p2p_gen > 0) + (h.n_p2p_list > 0);
+  info->adaptive = h.adaptive ? 1 : 0;
+  info->n_leaves = h.adaptive ? (int64_t)h.lf_code.size() : ((int64_t)1 << (2 * h.kappa));
   info->small_items[0] = h.n_aitems - h.n_abig;
   info->small_items[1] = h.n_bitems - h.n_bbig;
   info->apply_launches = (h.n_abig > 0) + (h.n_aitems > h.n_abig) + (h.n_bbig > 0) + (h.n_bitems > h.n_bbig) +
@@ -852,7 +884,7 @@ int hodlr2d_save_factors(hodlr2d_t H, const char* path) {
   if (!f) throw Error{H2D_EFACTORS, std::string("cannot open ") + path};
   f.write("H2DFAC01", 8);
   int64_t N = h.n;
-  int32_t kap = h.kappa, kid = h.kernel_id, tr = h.opts.test_rank, res = 0;
+  int32_t kap = h.kappa, kid = h.kernel_id, tr = h.opts.test_rank, res = h.adaptive ? 1 : 0;   // R11 / R24
   double c = h.kp.inv_c2 > 0 ? 1.0 / std::sqrt(h.kp.inv_c2) : h.opts.c;
   double d[7] = {h.tol, c, h.kp.scale, h.kp.shift, h.lo[0], h.lo[1], h.side};
   f.write((char*)&N, 8);
@@ -927,6 +959,18 @@ int hodlr2d_destroy(hodlr2d_t H) {
 
 const char* hodlr2d_last_error(void) { return g_last_error.c_str(); }
 
+int64_t hodlr2d_copy_leaves(hodlr2d_t H, int32_t* level, int32_t* box) {
+  if (!H) return -1;
+  Handle& h = H->h;
+  const int64_t n = h.adaptive ? (int64_t)h.lf_code.size() : ((int64_t)1 << (2 * h.kappa));
+  for (int64_t lf = 0; lf < n; ++lf) {
+    const int l = h.leaf_level(lf);
+    if (level) level[lf] = l;
+    if (box) box[lf] = (int32_t)(h.leaf_code(lf) >> (2 * (h.kappa - l)));
+  }
+  return n;
+}
+
 int hodlr2d_set_diag(hodlr2d_t H, const char* name, int value) {
   H2D_TRY
   if (!H || !name) throw Error{H2D_EINVAL, "null argument"};
@@ -955,6 +999,7 @@ int hodlr2d_leaf_costs(hodlr2d_t H, double* costs) {
   Handle& h = H->h;
   const int64_t nleaf = (int64_t)1 << (2 * h.kappa);
   for (int64_t L = 0; L < nleaf; ++L) costs[L] = 0.0;
+  if (h.adaptive) throw Error{H2D_EINVAL, "leaf costs are defined for the balanced tree's partition"};
   for (int64_t L = h.leaf_begin; L < h.leaf_end; ++L) {
     const double rows = (double)(h.leaf_start[(size_t)L + 1] - h.leaf_start[(size_t)L]);
     double cols = 0.0;

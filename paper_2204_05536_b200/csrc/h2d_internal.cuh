@@ -226,6 +226,30 @@ struct Handle {
   int32_t* d_perm = nullptr;
   int32_t* d_leaf_start = nullptr;
   std::vector<int32_t> leaf_start;        // host copy
+  // Adaptive quadtree (options.depth = -3, R24): a box is subdivided iff it holds
+  // more than N_max points.  The "leaves" every per-leaf structure below iterates (U leaf
+  // panels, stage-B items, the near field) are then the adaptive leaves, at various levels:
+  // lf_code = index of the leaf's first level-kappa descendant (its level-l ancestor is
+  // lf_code >> 2 (kappa - l)), lf_start = its TREE-order rows.  Balanced handles: the 4^kappa
+  // level-kappa boxes (lf_code = identity, lf_start = leaf_start).
+  bool adaptive = false;
+  std::vector<std::vector<uint8_t>> ad_sub;   // [level][box]: subdivided (exists iff parent subdivided)
+  std::vector<int64_t> lf_code;
+  std::vector<int32_t> lf_start, lf_level;
+  // the adaptive near field, per served leaf: column ranges (TREE begin, count) of every dense
+  // block whose row box contains the leaf (R24); CSR over leaves
+  std::vector<int64_t> ad_nf_off;
+  std::vector<int64_t> ad_nf_rng;   // pairs (begin, count)
+  int64_t* d_p2p_list = nullptr;   // items (leaf << 8 | 64-row pass) of the list kernel
+  int64_t n_p2p_list = 0;
+  int64_t* d_ad_nf_off = nullptr;
+  int64_t* d_ad_nf_rng = nullptr;
+  int32_t* d_lf_start = nullptr;
+  int64_t leaf_code(int64_t lf) const { return adaptive ? lf_code[(size_t)lf] : lf; }
+  int64_t leaf_s(int64_t lf) const { return adaptive ? lf_start[(size_t)lf] : leaf_start[(size_t)lf]; }
+  int64_t leaf_e(int64_t lf) const { return adaptive ? lf_start[(size_t)lf + 1] : leaf_start[(size_t)lf + 1]; }
+  int leaf_level(int64_t lf) const { return adaptive ? lf_level[(size_t)lf] : kappa; }
+  bool box_exists(int l, int64_t b) const { return !adaptive || l == 0 || ad_sub[(size_t)l - 1][(size_t)(b >> 2)]; }
   // near field (device + host)
   int32_t* d_nf_off = nullptr;
   int32_t* d_nf_col = nullptr;
@@ -357,6 +381,8 @@ struct Handle {
 // ------------------------------------------------------------------ host drivers
 void build_tree(Handle& h, const double* d_points);              // tree.cu (G1-G4)
 void build_lists(Handle& h);                                      // tree.cu (G5)
+void build_adaptive(Handle& h);                                   // tree.cu (R24 leaves)
+void build_adaptive_near(Handle& h);                              // tree.cu (R24 near field)
 void run_aca(Handle& h);                                          // aca.cu (G6) + pack (G7)
 // Pack the given per-block factor sources of one level into panels (apply.cu).
 void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,

@@ -13,6 +13,8 @@
 //                               Def. 4.4; minus self and edge sharers, Defs 4.1-4.3),
 //                               partners in ascending Morton order (R5).
 //  S5 near field              : {X} u E_X at the leaves (Alg. 1 l.5).
+#include <algorithm>
+
 #include <cub/cub.cuh>
 
 #include "h2d_internal.cuh"
@@ -20,7 +22,7 @@
 namespace h2d {
 namespace {
 
-__device__ __forceinline__ uint32_t spread_bits(uint32_t v) {
+__host__ __device__ __forceinline__ uint32_t spread_bits(uint32_t v) {
   v &= 0xFFFFu;
   v = (v | (v << 8)) & 0x00FF00FFu;
   v = (v | (v << 4)) & 0x0F0F0F0Fu;
@@ -28,7 +30,7 @@ __device__ __forceinline__ uint32_t spread_bits(uint32_t v) {
   v = (v | (v << 1)) & 0x55555555u;
   return v;
 }
-__device__ __forceinline__ uint32_t compact_bits(uint32_t v) {
+__host__ __device__ __forceinline__ uint32_t compact_bits(uint32_t v) {
   v &= 0x55555555u;
   v = (v | (v >> 1)) & 0x33333333u;
   v = (v | (v >> 2)) & 0x0F0F0F0Fu;
@@ -299,6 +301,88 @@ void build_tree(Handle& h, const double* d_points) {
   H2D_CUDA(cudaStreamSynchronize(s));
 }
 
+// Adaptive quadtree (R24): subdivided flags top-down from the box counts of the deepest
+// Morton order (the tree above is built at R22's depth, the deepest adaptive level), then the
+// leaves (existing, unsubdivided boxes) in Morton order of their first level-kappa
+// descendant.  Host work on 4^l flags per level.
+void build_adaptive(Handle& h) {
+  const int kappa = h.kappa;
+  const int nmax = h.leaf_size;
+  h.ad_sub.assign((size_t)kappa + 1, {});
+  for (int l = 0; l <= kappa; ++l) {
+    const int64_t nb = (int64_t)1 << (2 * l);
+    h.ad_sub[(size_t)l].assign((size_t)nb, 0);
+    if (l == kappa) break;
+    for (int64_t b = 0; b < nb; ++b)
+      if (h.box_exists(l, b) && h.box_end(l, b) - h.box_begin(l, b) > nmax) h.ad_sub[(size_t)l][(size_t)b] = 1;
+  }
+  h.lf_code.clear();
+  h.lf_level.clear();
+  h.lf_start.clear();
+  // depth-first in Morton order = ascending first descendant
+  std::vector<std::pair<int, int64_t>> stack{{0, 0}};
+  while (!stack.empty()) {
+    const auto [l, b] = stack.back();
+    stack.pop_back();
+    if (l < kappa && h.ad_sub[(size_t)l][(size_t)b]) {
+      for (int c = 3; c >= 0; --c) stack.push_back({l + 1, (b << 2) | c});
+      continue;
+    }
+    h.lf_code.push_back(b << (2 * (kappa - l)));
+    h.lf_level.push_back(l);
+    h.lf_start.push_back((int32_t)h.box_begin(l, b));
+  }
+  h.lf_start.push_back((int32_t)h.n);
+}
+
+// The adaptive near field (R24): dense blocks (X, Y), Y in {X} u E_X, of existing boxes at any
+// level with X or Y a leaf; every leaf collects the column ranges of the blocks whose row box
+// contains it (its own and its subdivided ancestors' mixed blocks), so each row has one
+// writer and each (i, j) of a dense block is evaluated once for row i.
+void build_adaptive_near(Handle& h) {
+  const int kappa = h.kappa;
+  const int64_t nlf = (int64_t)h.lf_code.size();
+  h.ad_nf_off.assign((size_t)nlf + 1, 0);
+  h.ad_nf_rng.clear();
+  auto leaf = [&](int l, int64_t b) { return l == kappa || !h.ad_sub[(size_t)l][(size_t)b]; };
+  for (int64_t lf = 0; lf < nlf; ++lf) {
+    h.ad_nf_off[(size_t)lf] = (int64_t)h.ad_nf_rng.size() / 2;
+    const int ll = h.lf_level[(size_t)lf];
+    const int64_t code = h.lf_code[(size_t)lf];
+    for (int l = 0; l <= ll; ++l) {
+      const int64_t X = code >> (2 * (kappa - l));
+      const uint32_t cx = compact_bits((uint32_t)X), cy = compact_bits((uint32_t)(X >> 1));
+      const int64_t side = (int64_t)1 << l;
+      // {X} u E_X in ascending Morton order
+      int64_t cand[5];
+      int nc = 0;
+      const int dxs[5] = {0, -1, 1, 0, 0}, dys[5] = {0, 0, 0, -1, 1};
+      for (int k = 0; k < 5; ++k) {
+        const int64_t qx = (int64_t)cx + dxs[k], qy = (int64_t)cy + dys[k];
+        if (qx < 0 || qy < 0 || qx >= side || qy >= side) continue;
+        cand[nc++] = (int64_t)(spread_bits((uint32_t)qx) | (spread_bits((uint32_t)qy) << 1));
+      }
+      std::sort(cand, cand + nc);
+      for (int k = 0; k < nc; ++k) {
+        const int64_t Y = cand[k];
+        if (!h.box_exists(l, Y) || (!leaf(l, X) && !leaf(l, Y))) continue;
+        const int64_t c0 = h.box_begin(l, Y), cnt = h.box_end(l, Y) - c0;
+        if (cnt == 0) continue;
+        h.ad_nf_rng.push_back(c0);
+        h.ad_nf_rng.push_back(cnt);
+      }
+    }
+  }
+  h.ad_nf_off[(size_t)nlf] = (int64_t)h.ad_nf_rng.size() / 2;
+  h.d_ad_nf_off = h.alloc<int64_t>(h.ad_nf_off.size());
+  h.d_ad_nf_rng = h.alloc<int64_t>(std::max<size_t>(1, h.ad_nf_rng.size()));
+  h.d_lf_start = h.alloc<int32_t>(h.lf_start.size());
+  H2D_CUDA(cudaMemcpy(h.d_ad_nf_off, h.ad_nf_off.data(), h.ad_nf_off.size() * 8, cudaMemcpyHostToDevice));
+  if (!h.ad_nf_rng.empty())
+    H2D_CUDA(cudaMemcpy(h.d_ad_nf_rng, h.ad_nf_rng.data(), h.ad_nf_rng.size() * 8, cudaMemcpyHostToDevice));
+  H2D_CUDA(cudaMemcpy(h.d_lf_start, h.lf_start.data(), h.lf_start.size() * 4, cudaMemcpyHostToDevice));
+}
+
 void build_lists(Handle& h) {
   h.levels.assign((size_t)h.kappa + 1, Level());
   for (int l = 1; l <= h.kappa; ++l) {
@@ -306,6 +390,23 @@ void build_lists(Handle& h) {
     L.l = l;
     L.nbox = (int64_t)1 << (2 * l);
     make_csr(h, l, 0, L.d_off, L.d_col, L.off, L.col);
+    if (h.adaptive) {   // R24: Eq. eq:ilist restricted to existing boxes
+      std::vector<int32_t> off((size_t)L.nbox + 1, 0), col;
+      col.reserve(L.col.size());
+      for (int64_t X = 0; X < L.nbox; ++X) {
+        off[(size_t)X] = (int32_t)col.size();
+        if (!h.box_exists(l, X)) continue;
+        for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e)
+          if (h.box_exists(l, L.col[(size_t)e])) col.push_back(L.col[(size_t)e]);
+      }
+      off[(size_t)L.nbox] = (int32_t)col.size();
+      L.off.swap(off);
+      L.col.swap(col);
+      h.release(L.d_col);
+      L.d_col = h.alloc<int32_t>(std::max<size_t>(1, L.col.size()));
+      H2D_CUDA(cudaMemcpy(L.d_off, L.off.data(), L.off.size() * 4, cudaMemcpyHostToDevice));
+      if (!L.col.empty()) H2D_CUDA(cudaMemcpy(L.d_col, L.col.data(), L.col.size() * 4, cudaMemcpyHostToDevice));
+    }
     L.nblocks = L.off[(size_t)L.nbox];
     // transpose map: block (X, Y) -> block (Y, X) (the relation is symmetric)
     L.trans.assign((size_t)L.nblocks, -1);

@@ -1,0 +1,146 @@
+"""GPU parity of the adaptive (non-balanced) quadtree (NEXT N4, options.depth = -3, DESIGN.md
+R24; the paper's "non-balanced or adaptive quadtree").
+
+Bars: leaves, permutation and per-level interaction lists bit-exact against the oracle; with
+the oracle's factors loaded rel-l2 <= 1e-12 against the oracle matvec; GPU-built factors
+<= 10 tol against the dense product; the balanced operator when every leaf is deepest.
+Inputs: clustered points, the paper's Chebyshev grids with small N_max, a curve.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def h2d():
+    import paper_2204_05536_b200 as m
+    m.lib()
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def clustered(n, seed):
+    rng = np.random.default_rng(seed)
+    a = np.clip(rng.normal((-0.7, -0.6), 0.03, (n // 2, 2)), -1, 1)
+    b = rng.uniform(-1, 1, (n - n // 2, 2))
+    return np.ascontiguousarray(np.concatenate([a, b]))
+
+
+CASES = {
+    "clustered_6000": (lambda: clustered(6000, 1), 48),
+    "chebyshev_120sq": (lambda: W.chebyshev_grid(120), 64),
+    "chebyshev_60sq_nmax300": (lambda: W.chebyshev_grid(60), 300),
+    "curve_5000": (lambda: np.ascontiguousarray(np.stack([np.linspace(-0.9, 0.9, 5000),
+                                                          0.3 * np.sin(3 * np.linspace(-0.9, 0.9, 5000))], 1)), 32),
+}
+
+KERNELS = [("log", 0, 1.0, 0.0), ("imq", 1, 0.1, 0.0), ("rbf_phi1", 3, 1e-3, 1.0), ("one_over_r", 2, 1.0, 0.0)]
+
+
+def gpu(h2d, pts, kernel, nmax, tol, **kw):
+    return h2d.Hodlr2d.build(dev(pts), kernel, nmax, tol, box_lo=(-1, -1), box_side=2.0, depth=-3, **kw)
+
+
+def orc(pts, kid, nmax, tol, **kw):
+    return oracle.Operator(pts, kid, nmax, tol, box_lo=(-1, -1), box_side=2.0, depth=-3, **kw)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_adaptive_structure_bit_exact(h2d, name):
+    gen, nmax = CASES[name]
+    pts = gen()
+    op = gpu(h2d, pts, "log", nmax, 1e-10, skip_aca=True)
+    o = orc(pts, 0, nmax, 1e-10)
+    inf = op.info()
+    assert inf["adaptive"] == 1 and inf["kappa"] == o.kappa
+    perm, ls = op.tree()
+    operm, ols = o.tree()
+    assert np.array_equal(perm, operm) and np.array_equal(ls, ols)
+    lv, bx = op.leaves()
+    olv, obx = o.leaves()
+    assert np.array_equal(lv, olv) and np.array_equal(bx, obx)
+    assert inf["n_leaves"] == len(olv) and len(set(lv.tolist())) > 1
+    for l in range(1, o.kappa + 1):
+        off, col = op.lists(l)
+        ooff, ocol = o.op_lists(l)
+        assert np.array_equal(off, ooff) and np.array_equal(col, ocol), l
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_adaptive_oracle_factors(h2d, name, tmp_path):
+    gen, nmax = CASES[name]
+    pts = gen()
+    o = orc(pts, 0, nmax, 1e-10)
+    path = tmp_path / "ad.h2df"
+    o.save_factors(path)
+    op = gpu(h2d, pts, "log", nmax, 1e-10, skip_aca=True)
+    op.load_factors(path)
+    for k in range(2):
+        x = W.random_vector(pts.shape[0], 300 + k)
+        assert rel(op.matvec(dev(x)).cpu().numpy(), o.matvec(x)) <= 1e-12
+    perm, _ = op.tree()
+    x = W.random_vector(pts.shape[0], 310)
+    assert rel(op.matvec(dev(x[perm]), order="tree").cpu().numpy(), o.matvec(x)[perm]) <= 1e-12
+    for l in range(1, o.kappa + 1):
+        assert np.array_equal(op.ranks(l), o.ranks(l)[0])
+    # a balanced handle refuses an adaptive factor file
+    bal = h2d.Hodlr2d.build(dev(pts), "log", nmax, 1e-10, box_lo=(-1, -1), box_side=2.0, depth=o.kappa, skip_aca=True)
+    with pytest.raises(h2d.Hodlr2dError):
+        bal.load_factors(path)
+
+
+@pytest.mark.parametrize("name", ["clustered_6000", "chebyshev_120sq", "curve_5000"])
+@pytest.mark.parametrize("kernel,kid,c,shift_per_n", KERNELS)
+def test_adaptive_gpu_factors_vs_dense(h2d, name, kernel, kid, c, shift_per_n):
+    gen, nmax = CASES[name]
+    pts = gen()
+    n = pts.shape[0]
+    tol = 1e-10
+    shift = shift_per_n * n
+    op = gpu(h2d, pts, kernel, nmax, tol, c=c, shift=shift)
+    x = W.random_vector(n, 77)
+    yd = oracle.dense_matvec(pts, x, kid, c, 1.0, shift)
+    y = op.matvec(dev(x)).cpu().numpy()
+    assert np.linalg.norm(y - yd) / np.linalg.norm(yd - shift * x) <= 10 * tol
+    # multi-RHS on an adaptive handle: one vector at a time, same result
+    X = np.stack([x, W.random_vector(n, 78)])
+    Y = op.matvec_multi(dev(X)).cpu().numpy()
+    assert np.array_equal(Y[0], y)
+
+
+def test_adaptive_equals_balanced_when_every_leaf_is_deepest(h2d):
+    pts = W.grid_points(128)             # N_max 64: every level-4 box holds 64 points
+    ad = gpu(h2d, pts, "imq", 64, 1e-10, c=0.1)
+    ba = h2d.Hodlr2d.build(dev(pts), "imq", 64, 1e-10, c=0.1, box_lo=(-1, -1), box_side=2.0, depth=-2)
+    assert ad.info()["kappa"] == ba.info()["kappa"] == 4
+    assert np.all(ad.leaves()[0] == 4)
+    for l in range(1, 5):
+        assert np.array_equal(ad.ranks(l), ba.ranks(l))
+    x = W.random_vector(pts.shape[0], 5)
+    assert rel(ad.matvec(dev(x)).cpu().numpy(), ba.matvec(dev(x)).cpu().numpy()) <= 1e-14
+
+
+def test_adaptive_gmres_rbf(h2d):
+    """The paper's RBF system on a Chebyshev grid with the adaptive tree:
+    GMRES recovers lambda to the paper's accuracy."""
+    pts = W.chebyshev_grid(150)
+    n = pts.shape[0]
+    op = gpu(h2d, pts, "rbf_phi1", 64, 1e-12, c=1e-3, shift=float(n))
+    lam = np.random.default_rng(1048).uniform(-1, 1, n)
+    f = oracle.dense_matvec(pts, lam, 3, 1e-3, 1.0, float(n))
+    x, its, rr = op.gmres(dev(f), tol=1e-10)
+    assert rr < 1e-10
+    assert rel(x.cpu().numpy(), lam) < 1e-9
