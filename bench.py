@@ -418,17 +418,26 @@ def run_ours(args, cfg):
     if world == 1 and not args.symmetric and not args.no_variants:
         variants = {"symmetric_N1": symmetric_variant(h2d, op, cfg, xs, nx, y, stream, args)}
 
-    # near-field P2P against the FP64 pipe.  The symmetric kernel evaluates every unordered
-    # leaf pair once: (near_pairs + N) / 2 kernel evaluations, each P2P_FP64_OPS_PER_EVAL
-    # FP64-pipe instructions (counted in the SASS of p2p_fast_kernel).  In the
-    # timed matvec it runs concurrently with stages A/B on the spare SM resources, so its
-    # FP64 fraction is also probed standalone (H2D_P2P_SERIAL=1, diagnostics path).
+    # near-field P2P against the FP64 pipe.  The kernel that runs on the uniform configs is
+    # p2p_warp_kernel (every leaf <= 96 points): it evaluates each leaf's self block in full
+    # (sum m^2) and each edge-neighbour leaf pair once, i.e. sum m^2 + (near_pairs - sum m^2)
+    # / 2 kernel evaluations, each P2P_FP64_OPS_PER_EVAL FP64-pipe instructions (counted in
+    # its SASS).  In the timed matvec it runs concurrently with stages A/B on
+    # the spare SM resources, so its FP64 fraction is also probed standalone (set_diag
+    # "p2p_serial": the near field alone, before stage A).
     csum = clk.summary()
     p2p_ms = per["p2p_near"]
     ops_eval = P2P_FP64_OPS_PER_EVAL.get(cfg.kernel)
     sm_hz = (csum["sm_mhz"] or 1965.0) * 1e6
     served = inf["row_end"] - inf["row_begin"]
-    evals = (inf["p2p_pairs"] + served) / 2.0
+    if inf.get("adaptive"):   # p2p_list_kernel: every directed pair of the dense blocks
+        evals = float(inf["p2p_pairs"])
+    else:
+        _, ls = op.tree()
+        msz = np.diff(ls[inf["leaf_begin"]: inf["leaf_end"] + 1]).astype(np.float64)
+        self_pairs = float((msz * msz).sum())
+        warp_only = inf["p2p_leaves"][1] == 0 and inf["p2p_leaves"][2] == 0
+        evals = self_pairs + (inf["p2p_pairs"] - self_pairs) / 2.0 if warp_only else (inf["p2p_pairs"] + served) / 2.0
     alone_ms = p2p_standalone_ms(op, step, args) if world == 1 else None
     peak_ops, peak_ops_kind = 148 * 64 * sm_hz, "nominal: 148 SMs x 64 FP64 lanes x SM clock"
     try:
@@ -606,11 +615,12 @@ def launches_per_matvec(inf, world):
     return 2 + inf.get("apply_launches", 2) + inf.get("p2p_launches", 1)
 
 
-# FP64-pipe instructions per kernel evaluation in p2p_fast_kernel's unrolled tile loop,
+# FP64-pipe instructions per kernel evaluation in p2p_warp_kernel's self-block loop,
 # counted from `cuobjdump -sass` of libhodlr2d.so; keyed by kernel id.
-# log: 2 DADD + 1 DMUL + 12 DFMA + 1 DSETP + 1 I2F.F64; IMQ / 1/r: distance + rsqrt
-# (MUFU.RSQ64H seed + Newton) + 2 accumulations.
-P2P_FP64_OPS_PER_EVAL = {0: 17, 1: 12, 2: 12}
+# log (p2p_warp_kernel<0, 2>): 44 DFMA + 8 DADD + 4 DMUL + 4 DSETP + 4 I2F.F64 per 4
+# evaluations = 16; IMQ / 1/r: distance + rsqrt (MUFU.RSQ64H seed + Newton) + the
+# accumulation, ~12 (estimate).
+P2P_FP64_OPS_PER_EVAL = {0: 16, 1: 12, 2: 12}
 
 
 def p2p_standalone_ms(op, step, args, n=10):

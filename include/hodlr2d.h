@@ -173,6 +173,9 @@ typedef struct {
   int64_t small_items[2];    /* stage A boxes / stage B leaves on the small-item kernels */
   int comm_kind;             /* 0 none, 1 NCCL communicator, 2 host all-gather callback  */
   int adaptive;              /* 1: adaptive quadtree (depth = -3, R24)          */
+  int pair_apply;            /* 1: matvecs run the pair-local symmetric apply (symmetric
+                                single-rank handles: each factor read once)
+                                and stageA_bytes counts its pass                         */
   int64_t n_leaves;          /* leaves (adaptive: hodlr2d_copy_leaves; else 4^kappa)      */
   int64_t local_items[2];    /* H2D_ORDER_LOCAL: stage-A items (ring, small) whose column box
                                 is local, run while the x all-gather is in flight        */
@@ -298,7 +301,8 @@ int hodlr2d_partition(const int32_t* leaf_start, int kappa, int world, int rank,
  * rounding order, except "dual_norow", which skips the symmetric B' row dots and gives WRONG
  * results, for timing only): "p2p_serial" (the near field alone, before stage A),
  * "p2p_onestream" (every near-field class on one stream), "dual_norow", "copy_stream" (0:
- * host copies on the work stream).  Defaults come from the H2D_* environment variables at
+ * host copies on the work stream), "pair_apply" (symmetric handles: 1 the pair-local apply,
+ * 0 the three-pass apply).  Defaults come from the H2D_* environment variables at
  * build time.  H2D_EINVAL for an unknown name. */
 int hodlr2d_set_diag(hodlr2d_t h, const char* name, int value);
 

@@ -79,7 +79,7 @@ class Info(C.Structure):
         ("device_bytes", C.c_int64), ("gather_stride", C.c_int64), ("p2p_bytes", C.c_int64),
         ("symmetric_apply", C.c_int), ("p2p_launches", C.c_int), ("p2p_leaves", C.c_int64 * 3),
         ("apply_launches", C.c_int), ("small_items", C.c_int64 * 2),
-        ("comm_kind", C.c_int), ("adaptive", C.c_int), ("n_leaves", C.c_int64),
+        ("comm_kind", C.c_int), ("adaptive", C.c_int), ("pair_apply", C.c_int), ("n_leaves", C.c_int64),
         ("local_items", C.c_int64 * 2),
     ]
 

@@ -27,6 +27,7 @@
 
 #include "h2d_internal.cuh"
 #include "stages.cuh"
+#include "pairs.cuh"
 
 namespace h2d {
 namespace {
@@ -905,6 +906,53 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
       }
     }
   }
+  if (h.pair_wanted && !h.pair_failed) {
+    for (int64_t e = 0; e < L.nblocks; ++e)
+      if (rank_all(e) > kPMaxRp - 1) h.pair_failed = true;
+    if (h.pair_failed)   // ranks above 127: the pair apply is off for these factors
+      for (auto& Lv : h.levels) { h.release(Lv.Pr); Lv.Pr = nullptr; Lv.pairs.clear(); }
+  }
+  if (h.pair_wanted && !h.pair_failed) {
+    // pair apply (pairs.cuh): per pair {X, Y}, X < Y, V_XY (n_Y x Rp) then U_XY (m_X x Rp),
+    // row-major with a zero pad column; pairs in CSR order of their first side X
+    h.release(L.Pr);
+    L.Pr = nullptr;
+    L.pairs.clear();
+    int64_t po = 0, pvals = 0;
+    for (int64_t X = 0; X < nbox; ++X) {
+      const int64_t m = h.box_end(l, X) - h.box_begin(l, X);
+      for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
+        const int64_t Y = L.col[(size_t)e];
+        const int r = rank_all(e);
+        const int64_t n = h.box_end(l, Y) - h.box_begin(l, Y);
+        if (Y < X || r == 0 || m == 0 || n == 0) continue;
+        const int Rp = (r + 1) & ~1;
+        if (Rp > kPMaxRp) throw Error{H2D_EINVAL, "pair apply: rank above 127"};
+        Level::PairDesc d{po, po + n * Rp, (int32_t)h.box_begin(l, Y), (int32_t)h.box_begin(l, X), (int32_t)n,
+                          (int32_t)m, r, Rp};
+        L.pairs.push_back(d);
+        po = up16(po + (n + m) * Rp);
+        pvals += (n + m) * r;
+      }
+    }
+    L.pr_alloc = po;
+    L.pr_values = pvals;
+    L.Pr = h.alloc<double>(po);
+    H2D_CUDA(cudaMemsetAsync(L.Pr, 0, std::max<int64_t>(1, po) * sizeof(double), s));
+    size_t k = 0;
+    for (int64_t X = 0; X < nbox; ++X) {
+      const int64_t m = h.box_end(l, X) - h.box_begin(l, X);
+      for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
+        const int64_t Y = L.col[(size_t)e];
+        const int r = rank_all(e);
+        const int64_t n = h.box_end(l, Y) - h.box_begin(l, Y);
+        if (Y < X || r == 0 || m == 0 || n == 0) continue;
+        const Level::PairDesc& d = L.pairs[k++];
+        vitems.push_back(VPackItem{srcV[(size_t)e], L.Pr + d.v_off, (int32_t)n, r, d.Rp, 0});
+        vitems.push_back(VPackItem{srcU[(size_t)e], L.Pr + d.u_off, (int32_t)m, r, d.Rp, 0});
+      }
+    }
+  }
   const size_t CH = 1 << 20;
   for (size_t c0 = 0; c0 < uitems.size(); c0 += CH) {
     std::vector<UCopyItem> part(uitems.begin() + c0, uitems.begin() + std::min(uitems.size(), c0 + CH));
@@ -1400,6 +1448,117 @@ void finalize_schedule(Handle& h) {
     if (!gen.empty())
       H2D_CUDA(cudaMemcpyAsync(h.d_p2p_gen, gen.data(), gen.size() * 4, cudaMemcpyHostToDevice, s));
   }
+  h.pairapply = h.pair_wanted && !h.pair_failed;
+  if (h.pairapply) {
+    // pair apply schedule (pairs.cuh): pairs up to kPWholeBytes are one item (one CTA, all
+    // three phases), largest first; bigger pairs are cut into row chunks of <= kPChunkDbl
+    // doubles per phase and interleaved (phase 1 of big pair k, phase 2 of k - 1, phase 3
+    // of k - 2), ahead of the whole pairs
+    std::vector<std::pair<int64_t, PItem>> whole;
+    std::vector<std::pair<int64_t, PItem>> big;
+    int64_t pvals = 0;
+    // diagnostics: H2D_PAIR_WHOLE_MAX (bytes) moves the whole-pair / chunked-pair boundary
+    const int64_t whole_max = getenv("H2D_PAIR_WHOLE_MAX") ? atoll(getenv("H2D_PAIR_WHOLE_MAX")) : kPWholeBytes;
+    int lv_lo = 1, lv_hi = h.kappa;   // diagnostics: H2D_PAIR_LEVELS=lo,hi (WRONG results; timing only)
+    if (getenv("H2D_PAIR_LEVELS")) sscanf(getenv("H2D_PAIR_LEVELS"), "%d,%d", &lv_lo, &lv_hi);
+    for (int l = std::max(1, lv_lo); l <= std::min(h.kappa, lv_hi); ++l) {
+      const Level& L = h.levels[(size_t)l];
+      for (const auto& d : L.pairs) {
+        PItem it{};
+        it.v_off = d.v_off;
+        it.u_off = d.u_off;
+        it.yv = d.yv;
+        it.yu = d.yu;
+        it.nv = d.nv;
+        it.nu = d.nu;
+        it.R = d.R;
+        it.Rp = d.Rp;
+        it.level = l;
+        it.big = -1;
+        const int64_t bytes = (int64_t)(d.nv + d.nu) * d.Rp * 8;
+        pvals += (int64_t)(d.nv + d.nu) * d.R;
+        (bytes <= whole_max ? whole : big).push_back({bytes, it});
+      }
+    }
+    h.pair_values = pvals;
+    auto by_size = [](const auto& a, const auto& b) { return a.first > b.first; };
+    std::stable_sort(whole.begin(), whole.end(), by_size);
+    std::stable_sort(big.begin(), big.end(), by_size);
+    std::vector<PItem> items;
+    std::vector<std::vector<PItem>> ph[3];
+    int64_t toff = 0, poff = 0;
+    const int64_t nbig = (int64_t)big.size();
+    for (int b = 0; b < 3; ++b) ph[b].resize((size_t)nbig);
+    for (int64_t k = 0; k < nbig; ++k) {
+      PItem base = big[(size_t)k].second;
+      base.big = (int32_t)k;
+      base.toff = toff;
+      toff += base.R;
+      for (int p = 1; p <= 3; ++p) {
+        const int n = p == 2 ? base.nu : base.nv;
+        int nch = (int)std::max<int64_t>(1, ((int64_t)n * base.Rp + kPChunkDbl - 1) / kPChunkDbl);
+        const int rows = (n + nch - 1) / nch;
+        nch = (n + rows - 1) / rows;
+        const int64_t po = poff;
+        if (p < 3) poff += (int64_t)nch * base.R;
+        for (int c = 0; c < nch; ++c) {
+          PItem it = base;
+          it.kind = p;
+          it.r0 = c * rows;
+          it.nrows = std::min(rows, n - c * rows);
+          it.chunk = c;
+          it.nchunks = nch;
+          it.poff = p < 3 ? po : 0;
+          ph[p - 1][(size_t)k].push_back(it);
+        }
+      }
+    }
+    // merge the three phase streams by byte position: a phase-2 chunk of a pair enters the
+    // queue kPLag bytes (of phase-1 traffic) after the pair's phase-1 chunks, phase 3 another
+    // kPLag later — about two rounds of chunks over every CTA, so a dependent chunk rarely
+    // waits, while the pair's V (read in phase 1) is still in L2 for phase 3
+    const double lag = getenv("H2D_PAIR_LAG") ? atof(getenv("H2D_PAIR_LAG"))
+                                              : 2.0 * (2.0 * h.num_sms) * kPChunkDbl * 8.0;
+    // (every chunk of a phase is keyed after every chunk of the pair's previous phase, so
+    // all dependencies point backwards in the queue: a producer waits only on items that
+    // were taken earlier, and the earliest unfinished item always progresses)
+    std::vector<std::pair<double, PItem>> keyed;
+    std::vector<double> prev_end((size_t)nbig, -1.0);
+    for (int p = 0; p < 3; ++p) {
+      double pos = 0.0;
+      std::vector<double> end((size_t)nbig, 0.0);
+      for (int64_t k = 0; k < nbig; ++k)
+        for (const PItem& it : ph[p][(size_t)k]) {
+          const double key = std::max(pos + p * lag, prev_end[(size_t)k] + 1.0);
+          keyed.push_back({key, it});
+          end[(size_t)k] = std::max(end[(size_t)k], key);
+          pos += (double)it.nrows * it.Rp * 8.0;
+        }
+      prev_end = end;
+    }
+    std::stable_sort(keyed.begin(), keyed.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (auto& kv : keyed) items.push_back(kv.second);
+    for (auto& w : whole) {
+      w.second.kind = kPWhole;
+      items.push_back(w.second);
+    }
+    h.n_pitems = (int64_t)items.size();
+    for (void* q : {h.d_pitems, (void*)h.d_tP1, (void*)h.d_tP2, (void*)h.d_ptpart, (void*)h.d_pcount,
+                    (void*)h.d_pflags})
+      h.release(q);
+    h.d_pitems = h.alloc<PItem>(items.size());
+    if (!items.empty())
+      H2D_CUDA(cudaMemcpyAsync(h.d_pitems, items.data(), items.size() * sizeof(PItem), cudaMemcpyHostToDevice, s));
+    h.d_tP1 = h.alloc<double>(std::max<int64_t>(2, toff + 2));
+    h.d_tP2 = h.alloc<double>(std::max<int64_t>(2, toff + 2));
+    h.d_ptpart = h.alloc<double>(std::max<int64_t>(1, poff));
+    h.d_pcount = h.alloc<int32_t>(std::max<int64_t>(2, 2 * nbig));
+    h.d_pflags = h.alloc<int32_t>(std::max<int64_t>(2, 2 * nbig));
+    H2D_CUDA(cudaMemsetAsync(h.d_pcount, 0, std::max<int64_t>(2, 2 * nbig) * 4, s));
+    H2D_CUDA(cudaMemsetAsync(h.d_pflags, 0, std::max<int64_t>(2, 2 * nbig) * 4, s));
+    h.pair_epoch = 0;
+    if (!h.d_yacc) h.d_yacc = h.alloc<double>(h.n);
+  }
   h.tpart_len = tpart_len;
   h.d_tpart = h.alloc<double>(tpart_len);
   h.n_aitems = (int64_t)aitems.size();
@@ -1426,7 +1585,7 @@ void finalize_schedule(Handle& h) {
   if (h.adaptive)   // the list kernel writes slot 0 only; the combine reads all three
     H2D_CUDA(cudaMemsetAsync(h.d_ynear + h.n, 0, 2 * h.n * sizeof(double), s));
   if (!h.d_yfar) h.d_yfar = h.alloc<double>(std::max<int64_t>(1, h.row_end - h.row_begin));
-  if (!h.d_counters) h.d_counters = h.alloc<int32_t>(8);
+  if (!h.d_counters) h.d_counters = h.alloc<int32_t>(12);   // 0 A, 1 B, 2 P2P fast, 3 B', 4-6 P2P warp, 7 A remote, 8 pairs
   if (!h.hi_stream) {
     int sm = 0, lo_prio = 0, hi_prio = 0;
     H2D_CUDA(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, h.device));
@@ -1577,7 +1736,7 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
   const int64_t nleaves = h.leaf_end - h.leaf_begin;
   // H2D_P2P_SERIAL=1 (diagnostics only): the P2P runs alone, before stage A
   const bool p2p_serial = h.diag_p2p_serial && !gather;
-  if (gather && h.symapply) {   // (single-rank symmetric handle: gather first, no overlap)
+  if (gather && (h.symapply || h.pairapply)) {   // (single-rank symmetric handle: gather first, no overlap)
     comm_gather_exchange(h);
     comm_gather_finish(h, h.d_xtree, s);
     gather = false;
@@ -1678,7 +1837,28 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
     p2p();
     H2D_CUDA(cudaStreamWaitEvent(hi, h.ev_join, 0));
   }
-  if (h.symapply) {
+  if (h.pairapply) {
+    // pair-local symmetric apply (pairs.cuh): every factor read once; dy -> yacc
+    static uint64_t seen = 0;
+    const size_t smem = sizeof(PairSmem);
+    once_per_device(seen, [&] {
+      H2D_CUDA(cudaFuncSetAttribute(pair_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      H2D_CUDA(cudaFuncSetAttribute(pair_apply_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    cudaSharedmemCarveoutMaxShared));
+    });
+    PairPtrs pp{};
+    for (int l = 1; l <= h.kappa; ++l) pp.P[l] = h.levels[(size_t)l].Pr;
+    H2D_CUDA(cudaMemsetAsync(h.d_yacc, 0, h.n * sizeof(double), hi));
+    H2D_CUDA(cudaMemsetAsync(h.d_counters + 8, 0, sizeof(int32_t), hi));
+    ++h.pair_epoch;
+    if (h.n_pitems > 0) {
+      pair_apply_kernel<<<(int)std::min<int64_t>(2 * (int64_t)h.num_sms, h.n_pitems), kPipeThreads, smem, hi>>>(
+          (const PItem*)h.d_pitems, (int)h.n_pitems, h.d_counters + 8, pp, d_xtree, h.d_yacc, h.d_tP1, h.d_tP2,
+          h.d_ptpart, h.d_pcount, h.d_pflags, h.pair_epoch);
+      H2D_LAUNCH_CHECK();
+    }
+    record(h, 2, hi);
+  } else if (h.symapply) {
     // symmetric apply (R23): A' t1 = V^T x; B' t2 = U^T x and y1 = U t1; C' yfar = V t2
     const size_t smem = sizeof(PipeSmem<kNSShallow>);
     H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 4 * sizeof(int32_t), hi));
@@ -1715,7 +1895,10 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
   const int64_t rows = h.row_end - h.row_begin;
   if (rows > 0) {
     const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 148 * 8);
-    if (h.symapply)
+    if (h.pairapply)
+      combine_kernel<<<blocks, 256, 0, s>>>(h.row_begin, rows, h.d_yacc + h.row_begin, h.d_ynear, h.n, d_xtree,
+                                            h.kp.scale, h.kp.shift, d_y, h.d_perm, order_out, y_row0);
+    else if (h.symapply)
       combine_sym_kernel<<<blocks, 256, 0, s>>>(rows, h.kappa, h.d_yfar, h.d_y1, h.d_ynear, h.n, d_xtree, h.kp.scale,
                                                 h.kp.shift, d_y, h.d_perm, order_out, y_row0);
     else

@@ -359,6 +359,8 @@ static void load_factors(Handle& h, const char* path) {
   if (fperm != perm) throw Error{H2D_EFACTORS, "file permutation does not match the handle's tree"};
   clear_factors(h);
   h.truncated = 0;
+  h.pair_failed = false;
+  for (auto& Lv : h.levels) { h.release(Lv.Pr); Lv.Pr = nullptr; Lv.pairs.clear(); }
   std::vector<char> discard((size_t)1 << 20);
   for (int l = 1; l <= h.kappa; ++l) {
     Level& L = h.levels[(size_t)l];
@@ -571,6 +573,14 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
   h.opts.nccl_id = nullptr;        // caller-owned, read only by comm_init
   // symmetric apply (R23): symmetric build on a single-rank handle (the multi-rank row
   // partitions keep the directed panels; stage B' needs every row of a row box)
+  // pair-local symmetric apply (pairs.cuh): symmetric builds on single-rank handles;
+  // adaptive symmetric handles (no three-pass apply) by default, balanced ones with
+  // H2D_PAIRAPPLY=1 (measured slower than the three-pass apply on C3 so far)
+  {
+    const char* e = getenv("H2D_PAIRAPPLY");
+    const bool want = e ? atoi(e) != 0 : (opts->depth == -3);
+    h.pair_wanted = want && opts->symmetric && h.row_begin == 0 && h.row_end == h.n && h.kappa >= 1;
+  }
   h.symapply = opts->symmetric && h.row_begin == 0 && h.row_end == h.n && h.kappa >= 1 && !h.adaptive &&
                !(getenv("H2D_SYMAPPLY") && atoi(getenv("H2D_SYMAPPLY")) == 0);
   h.tree_seconds = now_s() - t0;
@@ -788,6 +798,12 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
                          8 * (int64_t)h.kappa * h.n;
     info->stageB_bytes = 8 * uv + 8 * h.t_len + 16 * served + 8 * (int64_t)h.kappa * served;
   }
+  if (h.pairapply) {
+    // pair apply: every pair's V and U once from HBM (the phase-3 V re-read is an L2 hit),
+    // x read once, the y accumulator zeroed and reduced into (L2); "stage B" is empty
+    info->stageA_bytes = 8 * h.pair_values + 8 * (int64_t)h.n + 8 * (int64_t)h.n;
+    info->stageB_bytes = 16 * served;   // the combine's yacc read and y write
+  }
   info->p2p_bytes = 24 * served + 8 * served;
   info->matvec_bytes = info->stageA_bytes + info->stageB_bytes + info->p2p_bytes;
   info->device_bytes = (int64_t)h.device_bytes;
@@ -804,6 +820,8 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   info->small_items[1] = h.n_bitems - h.n_bbig;
   info->apply_launches = (h.n_abig > 0) + (h.n_aitems > h.n_abig) + (h.n_bbig > 0) + (h.n_bitems > h.n_bbig) +
                          (h.symapply && h.n_b1items > 0);
+  if (h.pairapply) info->apply_launches = 1;
+  info->pair_apply = h.pairapply ? 1 : 0;
   info->comm_kind = comm_kind(h);
   info->local_items[0] = h.n_abig_loc;
   info->local_items[1] = h.n_asmall_loc;
@@ -980,6 +998,11 @@ int hodlr2d_set_diag(hodlr2d_t H, const char* name, int value) {
   else if (nm == "p2p_onestream") h.diag_p2p_onestream = value != 0;
   else if (nm == "dual_norow") h.diag_dual_norow = value != 0;
   else if (nm == "copy_stream") h.diag_copy_stream = value != 0;
+  else if (nm == "pair_apply") {   // symmetric handles: pair apply (1) or the three-pass apply (0)
+    if (value && (!h.pair_wanted || h.pair_failed)) throw Error{H2D_EINVAL, "pair apply not built for this handle"};
+    if (!value && !h.symapply && h.pairapply) throw Error{H2D_EINVAL, "no three-pass apply on this handle"};
+    h.pairapply = value != 0;
+  }
   else throw Error{H2D_EINVAL, "unknown diagnostics switch " + nm};
   return H2D_OK;
   H2D_CATCH
