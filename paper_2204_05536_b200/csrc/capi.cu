@@ -573,12 +573,11 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
   h.opts.nccl_id = nullptr;        // caller-owned, read only by comm_init
   // symmetric apply (R23): symmetric build on a single-rank handle (the multi-rank row
   // partitions keep the directed panels; stage B' needs every row of a row box)
-  // pair-local symmetric apply (pairs.cuh): symmetric builds on single-rank handles;
-  // adaptive symmetric handles (no three-pass apply) by default, balanced ones with
+  // pair-local symmetric apply (pairs.cuh): symmetric builds on single-rank handles, with
   // H2D_PAIRAPPLY=1 (measured slower than the three-pass apply on C3 so far)
   {
     const char* e = getenv("H2D_PAIRAPPLY");
-    const bool want = e ? atoi(e) != 0 : (opts->depth == -3);
+    const bool want = e ? atoi(e) != 0 : false;
     h.pair_wanted = want && opts->symmetric && h.row_begin == 0 && h.row_end == h.n && h.kappa >= 1;
   }
   h.symapply = opts->symmetric && h.row_begin == 0 && h.row_end == h.n && h.kappa >= 1 && !h.adaptive &&

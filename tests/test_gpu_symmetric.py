@@ -323,10 +323,11 @@ def test_pair_apply_matches_three_pass_and_oracle(h2d, name, tmp_path, monkeypat
     assert rel(op.matvec(dev(x)).cpu().numpy(), orc.matvec(x)) <= 1e-12
 
 
-def test_pair_apply_adaptive_tree(h2d, tmp_path):
+def test_pair_apply_adaptive_tree(h2d, tmp_path, monkeypatch):
     """Symmetric adaptive handles (R24) run the pair apply too: oracle symmetric adaptive
     factors <= 1e-12, GPU factors <= 10 tol vs dense."""
     pts = W.chebyshev_grid(110)
+    monkeypatch.setenv("H2D_PAIRAPPLY", "1")
     kw = dict(box_lo=(-1, -1), box_side=2.0, depth=-3)
     op = h2d.Hodlr2d.build(dev(pts), "rbf_phi1", 48, 1e-12, c=1e-3, shift=12100.0, symmetric=True, **kw)
     assert op.info()["pair_apply"] == 1 and op.info()["adaptive"] == 1
