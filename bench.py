@@ -41,6 +41,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c4", action="store_true",
                     help="skip the C4 (N = 2^22) sub-result the default C3 line carries")
+    ap.add_argument("--c5-min-world", type=int, default=4,
+                    help="at --gpus >= this, the C3 line also carries the C5 multi-GPU sub-result "
+                         "(build + 50 matvecs, max over ranks, E_N from per-rank slice timings)")
+    ap.add_argument("--c5-config", default="c5", choices=sorted(W.CONFIGS),
+                    help="config of that sub-result (c2: functional check on one shared GPU)")
     ap.add_argument("--symmetric", action="store_true",
                     help="symmetric build + apply (one ACA per unordered pair, DESIGN.md R23)")
     ap.add_argument("--no-variants", action="store_true",
@@ -386,7 +391,19 @@ def run_ours(args, cfg):
         e1.record(stream)
         torch.cuda.synchronize()
         e2e = {"value": 1e3 * ke / e0.elapsed_time(e1), "unit": "matvecs/s",
-               "h2d_bytes_per_step": 8 * cfg.n, "d2h_bytes_per_step": 8 * cfg.n}
+               "h2d_bytes_per_step": 8 * cfg.n, "d2h_bytes_per_step": 8 * cfg.n,
+               "buffers": "pinned host (torch pin_memory)"}
+        # the same with pageable host buffers (numpy): the library stages them through its
+        # own pinned buffers (multi-threaded host copies)
+        xp = xh.numpy().copy()
+        yp = np.empty(cfg.n)
+        op.matvec_raw(xp.ctypes.data, yp.ctypes.data, h2d.ORDER_ORIGINAL)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            op.matvec_raw(xp.ctypes.data, yp.ctypes.data, h2d.ORDER_ORIGINAL)
+        e2e["pageable"] = {"value": ke / (time.perf_counter() - t0), "unit": "matvecs/s",
+                           "timing": "host wall clock (each call returns after y is written)"}
 
     # multi-RHS (NEXT N2): the same fresh vectors, nrhs per call; reported beside the
     # single-vector headline, never in place of it
@@ -460,6 +477,17 @@ def run_ours(args, cfg):
            "overlapped_with": "stageA_VTx + stageB_Ut (low-priority stream, co-resident CTAs)",
            "exposed_ms": round(per["p2p_join_wait"], 4)}
     roof["p2p"] = p2p
+    # C5 (N = 2^24) is the config BASELINE quotes on 8 GPUs: at N >= --c5-min-world ranks the
+    # line carries it too (every rank takes part: the all-gather is collective)
+    c5 = None
+    if dist and world >= args.c5_min_world and args.config == "c3":
+        op.close()
+        del xs
+        torch.cuda.empty_cache()
+        try:
+            c5 = multi_gpu_config(h2d, args, stream, dist, world, rank, dev)
+        except Exception as ex:  # the headline stands on its own
+            c5 = {"error": str(ex)}
     if rank == 0:
         line = {
             "metric": "HODLR2D fp64 matvecs/sec", "value": value, "unit": "matvecs/s",
@@ -475,6 +503,8 @@ def run_ours(args, cfg):
             "gpu_launches": args.steps * launches_per_matvec(inf, world),
             "clocks": csum,
         }
+        if c5 is not None:
+            line["c5"] = c5
         # BASELINE's metric spans N = 2^20 .. 2^24: the default (C3) line also carries C4
         # (N = 2^22, 96 GB of factors) measured in the same run on the same GPU
         if world == 1 and args.config == "c3" and not args.no_c4:
@@ -494,6 +524,75 @@ def run_ours(args, cfg):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def multi_gpu_config(h2d, args, stream, dist, world, rank, dev):
+    """BASELINE config 5 on `world` GPUs: build (max over ranks) plus 50
+    matvecs through the library's LOCAL order (the x all-gather inside, NCCL), timed with
+    CUDA events and reduced with MAX over ranks; then each rank times its slice alone with the
+    full TREE-order x resident (no gather): T1_virt = the sum over ranks, E_N = T1_virt /
+    (N T_N) (SURVEY's E_8 definition; C5 does not fit one GPU)."""
+    import torch
+    cfg = W.CONFIGS[args.c5_config]
+    pts = torch.from_numpy(W.config_points(cfg)).cuda()
+    dist.barrier()
+    t0 = time.time()
+    op = h2d.Hodlr2d.build(pts, cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c, scale=cfg.scale, shift=cfg.shift,
+                           box_lo=cfg.box_lo, box_side=cfg.box_side, stream=stream.cuda_stream,
+                           group=dist.group.WORLD)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    del pts
+    inf = op.info()
+    perm, _ = op.tree()
+    rb, re_ = inf["row_begin"], inf["row_end"]
+    nx = 4
+    xfull = [W.config_x(cfg, k)[perm] for k in range(nx)]
+    xs = torch.stack([torch.from_numpy(x[rb:re_].copy()) for x in xfull]).cuda()
+    y = torch.empty(re_ - rb, dtype=torch.float64, device="cuda")
+    for k in range(3):
+        op.matvec_raw(xs[k % nx].data_ptr(), y.data_ptr(), h2d.ORDER_LOCAL)
+    steps = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record(stream)
+    for k in range(steps):
+        op.matvec_raw(xs[k % nx].data_ptr(), y.data_ptr(), h2d.ORDER_LOCAL)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = e0.elapsed_time(e1) / steps
+    # this rank's slice alone: full x resident, TREE order, no all-gather
+    xt = torch.from_numpy(xfull[0]).cuda()
+    for _ in range(2):
+        op.matvec_raw(xt.data_ptr(), y.data_ptr(), h2d.ORDER_TREE)
+    e0.record(stream)
+    for _ in range(10):
+        op.matvec_raw(xt.data_ptr(), y.data_ptr(), h2d.ORDER_TREE)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_slice = e0.elapsed_time(e1) / 10
+    on = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    v = torch.tensor([ms, build_s, ms_slice, inf["device_bytes"] / 1e9], dtype=torch.float64, device=on)
+    vmax, vsum = v.clone(), v.clone()
+    dist.all_reduce(vmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(vsum, op=dist.ReduceOp.SUM)
+    op.close()
+    del xs, xt
+    torch.cuda.empty_cache()
+    t_n, b_max, t1_virt = float(vmax[0]), float(vmax[1]), float(vsum[2])
+    return {"config": config_dict(cfg, world), "n_gpus": world, "value": 1e3 / t_n, "unit": "matvecs/s",
+            "ms_per_step": t_n, "steps": steps, "build_seconds_max": round(b_max, 2),
+            "build_plus_50_matvecs_s": round(b_max + 50 * t_n / 1e3, 3),
+            "points_matvecs_per_s": 1e3 / t_n * cfg.n,
+            "slice_ms_max": float(vmax[2]), "T1_virt_ms": t1_virt,
+            "efficiency_vs_virtual_1gpu": t1_virt / (world * t_n),
+            "device_gb_max": float(vmax[3]),
+            "note": "LOCAL-order matvecs (S11 inside the library: ncclAllGather on the handle's "
+                    "communicator); T1_virt = sum over ranks of each slice timed alone with the full "
+                    "x resident (SURVEY §8(e) E_8 definition); E_4->8 = 4 T_4 / (8 T_8) from the "
+                    "driver's N = 4 and N = 8 lines"}
 
 
 def sub_config(h2d, name, args, stream):

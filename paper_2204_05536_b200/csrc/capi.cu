@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <fstream>
 #include <new>
+#include <thread>
 
 #include "h2d_internal.cuh"
 
@@ -33,6 +34,8 @@ void Handle::release(void* p) {
 Handle::~Handle() {
   cudaStreamSynchronize(stream);
   comm_destroy(*this);
+  for (void* p : pin)
+    if (p) cudaFreeHost(p);
   for (void* p : allocs) cudaFree(p);
   for (auto e : ev_pool) cudaEventDestroy(e);
   if (ev_fork) cudaEventDestroy(ev_fork);
@@ -73,9 +76,56 @@ static void copy_stream_init(Handle& h) {
   H2D_CUDA(cudaEventCreateWithFlags(&h.ev_copy1, cudaEventDisableTiming));
 }
 
+static bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Host memcpy in up to 8 threads (pageable staging: one thread moves ~5-10 GB/s).
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const size_t kMin = (size_t)1 << 20;
+  const int nt = (int)std::min<size_t>(8, std::max<size_t>(1, bytes / kMin));
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t per = (bytes / nt + 63) & ~(size_t)63;
+  for (int t = 0; t < nt; ++t) {
+    const size_t o = (size_t)t * per;
+    if (o >= bytes) break;
+    th.emplace_back([=] { std::memcpy((char*)dst + o, (const char*)src + o, std::min(per, bytes - o)); });
+  }
+  for (auto& t : th) t.join();
+}
+
+// Library-owned pinned staging buffer of at least `bytes` (pageable caller buffers): the
+// previous copy through it has completed when this returns.
+static void* pinned_stage(Handle& h, int which, size_t bytes) {
+  if (h.copy_stream) H2D_CUDA(cudaStreamSynchronize(h.copy_stream));
+  H2D_CUDA(cudaStreamSynchronize(h.stream));
+  if (h.pin_bytes[which] < bytes) {
+    if (h.pin[which]) cudaFreeHost(h.pin[which]);
+    h.pin[which] = nullptr;
+    H2D_CUDA(cudaMallocHost(&h.pin[which], bytes));
+    h.pin_bytes[which] = bytes;
+  }
+  return h.pin[which];
+}
+
 // dst (device) <- src (host), ordered after the work already queued on the work stream and
-// before everything queued on it afterwards.
+// before everything queued on it afterwards.  Pageable src is staged through the handle's
+// pinned buffer (SURVEY §8(b) ownership: the library stages host pointers).
 static void h2d_ordered(Handle& h, void* dst, const void* src, size_t bytes) {
+  if (bytes && !is_pinned_host(src)) {
+    void* st = pinned_stage(h, 0, bytes);
+    par_memcpy(st, src, bytes);
+    src = st;
+  }
   if (!h.diag_copy_stream) {   // H2D_COPY_STREAM=0: copies on the work stream (diagnostics)
     H2D_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h.stream));
     return;
@@ -89,7 +139,14 @@ static void h2d_ordered(Handle& h, void* dst, const void* src, size_t bytes) {
 }
 
 // dst (host) <- src (device) after the work queued on the work stream; returns when done.
+// Pageable dst: through the handle's pinned buffer, then a host copy.
 static void d2h_ordered_sync(Handle& h, void* dst, const void* src, size_t bytes) {
+  if (bytes && !is_pinned_host(dst)) {
+    void* st = pinned_stage(h, 1, bytes);
+    d2h_ordered_sync(h, st, src, bytes);
+    par_memcpy(dst, st, bytes);
+    return;
+  }
   if (!h.diag_copy_stream) {
     H2D_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h.stream));
     H2D_CUDA(cudaStreamSynchronize(h.stream));

@@ -358,6 +358,9 @@ struct Handle {
   // build, changeable per handle with hodlr2d_set_diag (never per call from the environment)
   bool diag_p2p_serial = false, diag_p2p_onestream = false, diag_dual_norow = false;
   bool diag_copy_stream = true;
+  // pinned host staging of pageable caller buffers (0: inputs, 1: outputs)
+  void* pin[2] = {nullptr, nullptr};
+  size_t pin_bytes[2] = {0, 0};
   // matvec work buffers
   double* d_xtree = nullptr;              // [n]
   double* d_ybuf = nullptr;               // [n] staging for host y

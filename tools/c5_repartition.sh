@@ -1,6 +1,6 @@
 # C5 8-way: pass 1 builds every rank slice with the geometric partition and saves its leaf
 # costs (hodlr2d_leaf_costs); pass 2 rebuilds every slice partitioned by the summed costs
-# and times it.  Projected E_8 of both passes (tools/c5_e8.py).
+# and times it.  Projected E_8 of both passes: sum the per-slice "ms_per_matvec_compute" of geo_all.jsonl / mw_all.jsonl (T1_virt) over 8 x the slowest slice.
 mkdir -p gpurun_out/c5w
 for g in 0 1 2 3 4 5 6 7; do
   timeout 600 python bench.py --config c5 --rank-slice $g --slice-world 8 --steps 10 --warmup 2 \
