@@ -22,7 +22,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhodlr2d.so")
+# H2D_LIBRARY: diagnostics builds of the same sources (e.g. a timing variant); default in-tree
+LIB_PATH = os.environ.get("H2D_LIBRARY") or os.path.join(_HERE, "libhodlr2d.so")
 
 H2D_OK, H2D_WTRUNC, H2D_WNOCONV = 0, 1, 2
 H2D_EINVAL, H2D_EOUTOFBOX, H2D_ECOINCIDENT, H2D_ENOMEM = -1, -2, -3, -4

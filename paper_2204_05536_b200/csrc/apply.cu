@@ -99,10 +99,10 @@ constexpr int kSymRowsOnly = 0, kSymBoth = 1, kSymSelf = 2;
 template <int KID>
 __device__ __forceinline__ double p2p_eval(const KernelParams& kp, const double2* tab, double px,
                                            double py, double qx, double qy) {
-  if (KID == H2D_KERNEL_LOG) {
+  if (KID == H2D_KERNEL_LOG || KID == kLogSafe) {
     const double dx = px - qx, dy = py - qy;
     const double r2 = fma(dx, dx, dy * dy);
-    return r2 > 0.0 ? hlog_r2(r2, tab) : 0.0;
+    return r2 > 0.0 ? hlog_r2<KID == kLogSafe>(r2, tab) : 0.0;
   }
   return kernel_eval_t<KID>(kp, px, py, qx, qy);
 }
@@ -614,6 +614,50 @@ p2p_list_kernel(const int64_t* __restrict__ items, int n_items, int32_t* counter
   }
 }
 
+// Near-field pairs of distinct points with a subnormal r^2 (closer than ~1.5e-154): sets
+// *flag, and the handle's near field then runs the subnormal-safe table log (kLogSafe).  A
+// CTA per leaf (grid-stride), every (row, column) of the leaf's dense column ranges: the
+// self leaf and the edge neighbours (balanced), or the adaptive ranges (nf_off != nullptr).
+__global__ void subnormal_check_kernel(int kappa, int64_t nleaf, const int32_t* __restrict__ lstart,
+                                       const int64_t* __restrict__ nf_off, const int64_t* __restrict__ nf_rng,
+                                       const double* __restrict__ px, const double* __restrict__ py, int* flag) {
+  __shared__ int64_t rb[5], rc[5];
+  __shared__ int nr;
+  for (int64_t L = blockIdx.x; L < nleaf; L += gridDim.x) {
+    if (threadIdx.x == 0) {
+      nr = 0;
+      if (nf_off) {
+        for (int64_t e = nf_off[L]; e < nf_off[L + 1] && nr < 5; ++e) { rb[nr] = nf_rng[2 * e]; rc[nr] = nf_rng[2 * e + 1]; ++nr; }
+      } else {
+        const uint32_t cx = p2p_compact((uint32_t)L), cy = p2p_compact((uint32_t)L >> 1), side = 1u << kappa;
+        const int dxs[5] = {0, 1, -1, 0, 0}, dys[5] = {0, 0, 0, 1, -1};
+        for (int k = 0; k < 5; ++k) {
+          const int64_t qx = (int64_t)cx + dxs[k], qy = (int64_t)cy + dys[k];
+          if (qx < 0 || qy < 0 || qx >= side || qy >= side) continue;
+          const int64_t Y = (int64_t)(p2p_spread((uint32_t)qx) | (p2p_spread((uint32_t)qy) << 1));
+          rb[nr] = lstart[Y];
+          rc[nr] = lstart[Y + 1] - lstart[Y];
+          ++nr;
+        }
+      }
+    }
+    __syncthreads();
+    const int64_t s0 = nf_off ? lstart[L] : lstart[L];
+    const int64_t m = lstart[L + 1] - s0;
+    bool bad = false;
+    for (int64_t i = s0 + threadIdx.x; i < s0 + m; i += blockDim.x) {
+      const double xi = px[i], yi = py[i];
+      for (int k = 0; k < nr; ++k)
+        for (int64_t j = rb[k]; j < rb[k] + rc[k]; ++j) {
+          const double dx = xi - px[j], dy = yi - py[j];
+          const double r2 = fma(dx, dx, dy * dy);
+          bad |= r2 > 0.0 && r2 < 0x1p-1022;
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+  }
+}
+
 constexpr int kWarpLeaf = 96;      // rows per lane RPL = ceil(m / 32) <= 3 (leaves <= 96 points)
 
 template <int KID, int RPL>
@@ -908,13 +952,13 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
   }
   if (h.pair_wanted && !h.pair_failed) {
     for (int64_t e = 0; e < L.nblocks; ++e)
-      if (rank_all(e) > kPMaxRp - 1) h.pair_failed = true;
-    if (h.pair_failed)   // ranks above 127: the pair apply is off for these factors
+      if (rank_all(e) > kPMaxR) h.pair_failed = true;
+    if (h.pair_failed)   // ranks above kPMaxR: the pair apply is off for these factors
       for (auto& Lv : h.levels) { h.release(Lv.Pr); Lv.Pr = nullptr; Lv.pairs.clear(); }
   }
   if (h.pair_wanted && !h.pair_failed) {
-    // pair apply (pairs.cuh): per pair {X, Y}, X < Y, V_XY (n_Y x Rp) then U_XY (m_X x Rp),
-    // row-major with a zero pad column; pairs in CSR order of their first side X
+    // pair apply (pairs.cuh): per pair {X, Y}, X < Y, V_XY (n_Y x r) then U_XY (m_X x r),
+    // column-major as the ACA stores them; pairs in CSR order of their first side X
     h.release(L.Pr);
     L.Pr = nullptr;
     L.pairs.clear();
@@ -926,31 +970,23 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
         const int r = rank_all(e);
         const int64_t n = h.box_end(l, Y) - h.box_begin(l, Y);
         if (Y < X || r == 0 || m == 0 || n == 0) continue;
-        const int Rp = (r + 1) & ~1;
-        if (Rp > kPMaxRp) throw Error{H2D_EINVAL, "pair apply: rank above 127"};
-        Level::PairDesc d{po, po + n * Rp, (int32_t)h.box_begin(l, Y), (int32_t)h.box_begin(l, X), (int32_t)n,
-                          (int32_t)m, r, Rp};
+        Level::PairDesc d{po, po + n * r, (int32_t)h.box_begin(l, Y), (int32_t)h.box_begin(l, X), (int32_t)n,
+                          (int32_t)m, r, r};
         L.pairs.push_back(d);
-        po = up16(po + (n + m) * Rp);
+        po += (n + m) * r;
         pvals += (n + m) * r;
+        uitems.push_back(UCopyItem{srcV[(size_t)e], nullptr, (int32_t)n, (int32_t)n, (int32_t)n, r});
+        uitems.push_back(UCopyItem{srcU[(size_t)e], nullptr, (int32_t)m, (int32_t)m, (int32_t)m, r});
       }
     }
     L.pr_alloc = po;
     L.pr_values = pvals;
     L.Pr = h.alloc<double>(po);
-    H2D_CUDA(cudaMemsetAsync(L.Pr, 0, std::max<int64_t>(1, po) * sizeof(double), s));
-    size_t k = 0;
-    for (int64_t X = 0; X < nbox; ++X) {
-      const int64_t m = h.box_end(l, X) - h.box_begin(l, X);
-      for (int32_t e = L.off[(size_t)X]; e < L.off[(size_t)X + 1]; ++e) {
-        const int64_t Y = L.col[(size_t)e];
-        const int r = rank_all(e);
-        const int64_t n = h.box_end(l, Y) - h.box_begin(l, Y);
-        if (Y < X || r == 0 || m == 0 || n == 0) continue;
-        const Level::PairDesc& d = L.pairs[k++];
-        vitems.push_back(VPackItem{srcV[(size_t)e], L.Pr + d.v_off, (int32_t)n, r, d.Rp, 0});
-        vitems.push_back(VPackItem{srcU[(size_t)e], L.Pr + d.u_off, (int32_t)m, r, d.Rp, 0});
-      }
+    // destinations now that the array exists (the last 2 x pairs items are the pair copies)
+    size_t k0 = uitems.size() - 2 * L.pairs.size();
+    for (const auto& d : L.pairs) {
+      uitems[k0++].dst = L.Pr + d.v_off;
+      uitems[k0++].dst = L.Pr + d.u_off;
     }
   }
   const size_t CH = 1 << 20;
@@ -1450,105 +1486,112 @@ void finalize_schedule(Handle& h) {
   }
   h.pairapply = h.pair_wanted && !h.pair_failed;
   if (h.pairapply) {
-    // pair apply schedule (pairs.cuh): pairs up to kPWholeBytes are one item (one CTA, all
-    // three phases), largest first; bigger pairs are cut into row chunks of <= kPChunkDbl
-    // doubles per phase and interleaved (phase 1 of big pair k, phase 2 of k - 1, phase 3
-    // of k - 2), ahead of the whole pairs
-    std::vector<std::pair<int64_t, PItem>> whole;
-    std::vector<std::pair<int64_t, PItem>> big;
+    // pair apply schedule (pairs.cuh): the big pairs of the coarse levels as row chunks per
+    // phase (merged by byte position with a lag, every chunk after all chunks of the pair's
+    // previous phase), then the medium pairs (one CTA each), then groups of 8 small pairs
+    // (one warp each), each class largest first
+    std::vector<PPair> prs;
+    std::vector<std::pair<int64_t, int32_t>> big, whole, small;
     int64_t pvals = 0;
-    // diagnostics: H2D_PAIR_WHOLE_MAX (bytes) moves the whole-pair / chunked-pair boundary
-    const int64_t whole_max = getenv("H2D_PAIR_WHOLE_MAX") ? atoll(getenv("H2D_PAIR_WHOLE_MAX")) : kPWholeBytes;
     int lv_lo = 1, lv_hi = h.kappa;   // diagnostics: H2D_PAIR_LEVELS=lo,hi (WRONG results; timing only)
     if (getenv("H2D_PAIR_LEVELS")) sscanf(getenv("H2D_PAIR_LEVELS"), "%d,%d", &lv_lo, &lv_hi);
+    const int64_t small_max = getenv("H2D_PAIR_SMALL_MAX") ? atoll(getenv("H2D_PAIR_SMALL_MAX")) : kPSmallBytes;
+    const int64_t whole_max = getenv("H2D_PAIR_WHOLE_MAX") ? atoll(getenv("H2D_PAIR_WHOLE_MAX")) : kPWholeBytes;
     for (int l = std::max(1, lv_lo); l <= std::min(h.kappa, lv_hi); ++l) {
       const Level& L = h.levels[(size_t)l];
       for (const auto& d : L.pairs) {
-        PItem it{};
-        it.v_off = d.v_off;
-        it.u_off = d.u_off;
-        it.yv = d.yv;
-        it.yu = d.yu;
-        it.nv = d.nv;
-        it.nu = d.nu;
-        it.R = d.R;
-        it.Rp = d.Rp;
-        it.level = l;
-        it.big = -1;
-        const int64_t bytes = (int64_t)(d.nv + d.nu) * d.Rp * 8;
+        const int32_t id = (int32_t)prs.size();
+        prs.push_back(PPair{d.v_off, d.u_off, d.yv, d.yu, d.nv, d.nu, d.R, l});
+        const int64_t bytes = (int64_t)(d.nv + d.nu) * d.R * 8;
         pvals += (int64_t)(d.nv + d.nu) * d.R;
-        (bytes <= whole_max ? whole : big).push_back({bytes, it});
+        (bytes <= small_max ? small : bytes <= whole_max ? whole : big).push_back({bytes, id});
       }
     }
     h.pair_values = pvals;
     auto by_size = [](const auto& a, const auto& b) { return a.first > b.first; };
-    std::stable_sort(whole.begin(), whole.end(), by_size);
     std::stable_sort(big.begin(), big.end(), by_size);
-    std::vector<PItem> items;
-    std::vector<std::vector<PItem>> ph[3];
-    int64_t toff = 0, poff = 0;
-    const int64_t nbig = (int64_t)big.size();
-    for (int b = 0; b < 3; ++b) ph[b].resize((size_t)nbig);
-    for (int64_t k = 0; k < nbig; ++k) {
-      PItem base = big[(size_t)k].second;
-      base.big = (int32_t)k;
-      base.toff = toff;
-      toff += base.R;
-      for (int p = 1; p <= 3; ++p) {
-        const int n = p == 2 ? base.nu : base.nv;
-        int nch = (int)std::max<int64_t>(1, ((int64_t)n * base.Rp + kPChunkDbl - 1) / kPChunkDbl);
-        const int rows = (n + nch - 1) / nch;
-        nch = (n + rows - 1) / rows;
-        const int64_t po = poff;
-        if (p < 3) poff += (int64_t)nch * base.R;
-        for (int c = 0; c < nch; ++c) {
-          PItem it = base;
-          it.kind = p;
-          it.r0 = c * rows;
-          it.nrows = std::min(rows, n - c * rows);
-          it.chunk = c;
-          it.nchunks = nch;
-          it.poff = p < 3 ? po : 0;
-          ph[p - 1][(size_t)k].push_back(it);
-        }
+    std::stable_sort(whole.begin(), whole.end(), by_size);
+    std::stable_sort(small.begin(), small.end(), by_size);
+    // groups reference consecutive descriptors: reorder the small pairs' descriptors
+    std::vector<PPair> ordered;
+    ordered.reserve(prs.size());
+    std::vector<int32_t> newid(prs.size());
+    for (auto* cls : {&big, &whole, &small})
+      for (auto& b : *cls) {
+        newid[(size_t)b.second] = (int32_t)ordered.size();
+        ordered.push_back(prs[(size_t)b.second]);
+        b.second = newid[(size_t)b.second];
       }
+    std::vector<PWork> work;
+    const int64_t nbig = (int64_t)big.size();
+    std::vector<std::vector<PWork>> ph[3];
+    for (int b = 0; b < 3; ++b) ph[b].resize((size_t)nbig);
+    int64_t toff = 0, poff = 0;
+    for (int64_t k = 0; k < nbig; ++k) {
+      const PPair& p = ordered[(size_t)big[(size_t)k].second];
+      for (int q = 1; q <= 3; ++q) {
+        const int n = q == 2 ? p.nu : p.nv;
+        const int nch = (n + kPChunkRows - 1) / kPChunkRows;
+        for (int c = 0; c < nch; ++c) {
+          PWork w{};
+          w.kind = kPPhase1 + q - 1;
+          w.first = big[(size_t)k].second;
+          w.r0 = c * kPChunkRows;
+          w.r1 = std::min(n, (c + 1) * kPChunkRows);
+          w.big = (int32_t)k;
+          w.chunk = c;
+          w.nchunks = nch;
+          w.toff = toff;
+          w.poff = q < 3 ? poff : 0;
+          ph[q - 1][(size_t)k].push_back(w);
+        }
+        if (q < 3) poff += (int64_t)nch * p.r;
+      }
+      toff += p.r;
     }
-    // merge the three phase streams by byte position: a phase-2 chunk of a pair enters the
-    // queue kPLag bytes (of phase-1 traffic) after the pair's phase-1 chunks, phase 3 another
-    // kPLag later — about two rounds of chunks over every CTA, so a dependent chunk rarely
-    // waits, while the pair's V (read in phase 1) is still in L2 for phase 3
     const double lag = getenv("H2D_PAIR_LAG") ? atof(getenv("H2D_PAIR_LAG"))
-                                              : 2.0 * (2.0 * h.num_sms) * kPChunkDbl * 8.0;
-    // (every chunk of a phase is keyed after every chunk of the pair's previous phase, so
-    // all dependencies point backwards in the queue: a producer waits only on items that
-    // were taken earlier, and the earliest unfinished item always progresses)
-    std::vector<std::pair<double, PItem>> keyed;
+                                              : 1.5 * (2.0 * h.num_sms) * kPChunkRows * 20 * 8.0;
+    std::vector<std::pair<double, PWork>> keyed;
     std::vector<double> prev_end((size_t)nbig, -1.0);
-    for (int p = 0; p < 3; ++p) {
+    for (int q = 0; q < 3; ++q) {
       double pos = 0.0;
       std::vector<double> end((size_t)nbig, 0.0);
-      for (int64_t k = 0; k < nbig; ++k)
-        for (const PItem& it : ph[p][(size_t)k]) {
-          const double key = std::max(pos + p * lag, prev_end[(size_t)k] + 1.0);
-          keyed.push_back({key, it});
+      for (int64_t k = 0; k < nbig; ++k) {
+        const PPair& p = ordered[(size_t)big[(size_t)k].second];
+        for (const PWork& w : ph[q][(size_t)k]) {
+          const double key = std::max(pos + q * lag, prev_end[(size_t)k] + 1.0);
+          keyed.push_back({key, w});
           end[(size_t)k] = std::max(end[(size_t)k], key);
-          pos += (double)it.nrows * it.Rp * 8.0;
+          pos += (double)(w.r1 - w.r0) * p.r * 8.0;
         }
+      }
       prev_end = end;
     }
     std::stable_sort(keyed.begin(), keyed.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-    for (auto& kv : keyed) items.push_back(kv.second);
-    for (auto& w : whole) {
-      w.second.kind = kPWhole;
-      items.push_back(w.second);
+    for (auto& kv : keyed) work.push_back(kv.second);
+    for (auto& b : whole) {
+      PWork w{};
+      w.kind = kPWhole;
+      w.first = b.second;
+      work.push_back(w);
     }
-    h.n_pitems = (int64_t)items.size();
-    for (void* q : {h.d_pitems, (void*)h.d_tP1, (void*)h.d_tP2, (void*)h.d_ptpart, (void*)h.d_pcount,
+    for (size_t i = 0; i < small.size(); i += kPWarps) {
+      PWork w{};
+      w.kind = kPGroup;
+      w.first = small[i].second;
+      w.count = (int32_t)std::min<size_t>(kPWarps, small.size() - i);
+      work.push_back(w);
+    }
+    h.n_pitems = (int64_t)work.size();
+    for (void* q : {h.d_pitems, h.d_ppairs, (void*)h.d_tP1, (void*)h.d_tP2, (void*)h.d_ptpart, (void*)h.d_pcount,
                     (void*)h.d_pflags})
       h.release(q);
-    h.d_pitems = h.alloc<PItem>(items.size());
-    if (!items.empty())
-      H2D_CUDA(cudaMemcpyAsync(h.d_pitems, items.data(), items.size() * sizeof(PItem), cudaMemcpyHostToDevice, s));
+    h.d_pitems = h.alloc<PWork>(work.size());
+    h.d_ppairs = h.alloc<PPair>(ordered.size());
+    if (!work.empty())
+      H2D_CUDA(cudaMemcpyAsync(h.d_pitems, work.data(), work.size() * sizeof(PWork), cudaMemcpyHostToDevice, s));
+    if (!ordered.empty())
+      H2D_CUDA(cudaMemcpyAsync(h.d_ppairs, ordered.data(), ordered.size() * sizeof(PPair), cudaMemcpyHostToDevice, s));
     h.d_tP1 = h.alloc<double>(std::max<int64_t>(2, toff + 2));
     h.d_tP2 = h.alloc<double>(std::max<int64_t>(2, toff + 2));
     h.d_ptpart = h.alloc<double>(std::max<int64_t>(1, poff));
@@ -1558,6 +1601,24 @@ void finalize_schedule(Handle& h) {
     H2D_CUDA(cudaMemsetAsync(h.d_pflags, 0, std::max<int64_t>(2, 2 * nbig) * 4, s));
     h.pair_epoch = 0;
     if (!h.d_yacc) h.d_yacc = h.alloc<double>(h.n);
+  }
+  // the log kernel's near field: subnormal-safe table log only if some near pair needs it
+  h.p2p_kid = h.kp.id;
+  if (h.kp.id == H2D_KERNEL_LOG && h.leaf_end > h.leaf_begin) {
+    int* d_flag = nullptr;
+    H2D_CUDA(cudaMallocAsync(&d_flag, sizeof(int), s));
+    H2D_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), s));
+    const int64_t nl = h.adaptive ? (int64_t)h.lf_code.size() : ((int64_t)1 << (2 * h.kappa));
+    const int grid = (int)std::min<int64_t>(nl, 148 * 16);
+    subnormal_check_kernel<<<grid, 128, 0, s>>>(h.kappa, nl, h.adaptive ? h.d_lf_start : h.d_leaf_start,
+                                                h.adaptive ? h.d_ad_nf_off : nullptr,
+                                                h.adaptive ? h.d_ad_nf_rng : nullptr, h.d_px, h.d_py, d_flag);
+    H2D_LAUNCH_CHECK();
+    int flag = 0;
+    H2D_CUDA(cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    H2D_CUDA(cudaStreamSynchronize(s));
+    H2D_CUDA(cudaFreeAsync(d_flag, s));
+    if (flag) h.p2p_kid = kLogSafe;
   }
   h.tpart_len = tpart_len;
   h.d_tpart = h.alloc<double>(tpart_len);
@@ -1763,7 +1824,8 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
       return h.p2p_side[k];
     };
     if (h.n_p2p_list > 0) {   // adaptive near field (R24)
-      auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_list_kernel<H2D_KERNEL_LOG>
+      auto* kfn = h.p2p_kid == kLogSafe ? p2p_list_kernel<kLogSafe>
+                : h.kp.id == H2D_KERNEL_LOG ? p2p_list_kernel<H2D_KERNEL_LOG>
                 : h.kp.id == H2D_KERNEL_IMQ ? p2p_list_kernel<H2D_KERNEL_IMQ>
                 : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_list_kernel<H2D_KERNEL_ONE_OVER_R>
                 : h.kp.id == H2D_KERNEL_RBF_PHI1 ? p2p_list_kernel<H2D_KERNEL_RBF_PHI1>
@@ -1777,7 +1839,8 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
     }
     if (h.n_p2p_gen > 0) {
       cudaStream_t sg = h.n_p2p_gen < h.num_sms ? side(0) : a;
-      auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_sym_kernel<H2D_KERNEL_LOG>
+      auto* kfn = h.p2p_kid == kLogSafe ? p2p_sym_kernel<kLogSafe>
+                : h.kp.id == H2D_KERNEL_LOG ? p2p_sym_kernel<H2D_KERNEL_LOG>
                 : h.kp.id == H2D_KERNEL_IMQ ? p2p_sym_kernel<H2D_KERNEL_IMQ>
                 : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_sym_kernel<H2D_KERNEL_ONE_OVER_R>
                 : h.kp.id == H2D_KERNEL_RBF_PHI1 ? p2p_sym_kernel<H2D_KERNEL_RBF_PHI1>
@@ -1789,7 +1852,8 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
       H2D_LAUNCH_CHECK();
     }
     if (h.n_p2p_fast > 0) {
-      auto* kfn = h.kp.id == H2D_KERNEL_LOG ? p2p_fast_kernel<H2D_KERNEL_LOG>
+      auto* kfn = h.p2p_kid == kLogSafe ? p2p_fast_kernel<kLogSafe>
+                : h.kp.id == H2D_KERNEL_LOG ? p2p_fast_kernel<H2D_KERNEL_LOG>
                 : h.kp.id == H2D_KERNEL_IMQ ? p2p_fast_kernel<H2D_KERNEL_IMQ>
                 : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_fast_kernel<H2D_KERNEL_ONE_OVER_R>
                 : h.kp.id == H2D_KERNEL_RBF_PHI1 ? p2p_fast_kernel<H2D_KERNEL_RBF_PHI1>
@@ -1808,7 +1872,8 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
         if (cnt <= 0) continue;
         auto pick = [&](auto rpl) -> decltype(&p2p_warp_kernel<H2D_KERNEL_LOG, 1>) {
           constexpr int R = decltype(rpl)::value;
-          return h.kp.id == H2D_KERNEL_LOG ? p2p_warp_kernel<H2D_KERNEL_LOG, R>
+          return h.p2p_kid == kLogSafe ? p2p_warp_kernel<kLogSafe, R>
+               : h.kp.id == H2D_KERNEL_LOG ? p2p_warp_kernel<H2D_KERNEL_LOG, R>
                : h.kp.id == H2D_KERNEL_IMQ ? p2p_warp_kernel<H2D_KERNEL_IMQ, R>
                : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_warp_kernel<H2D_KERNEL_ONE_OVER_R, R>
                : h.kp.id == H2D_KERNEL_RBF_PHI1 ? p2p_warp_kernel<H2D_KERNEL_RBF_PHI1, R>
@@ -1839,22 +1904,15 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
   }
   if (h.pairapply) {
     // pair-local symmetric apply (pairs.cuh): every factor read once; dy -> yacc
-    static uint64_t seen = 0;
-    const size_t smem = sizeof(PairSmem);
-    once_per_device(seen, [&] {
-      H2D_CUDA(cudaFuncSetAttribute(pair_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      H2D_CUDA(cudaFuncSetAttribute(pair_apply_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    cudaSharedmemCarveoutMaxShared));
-    });
     PairPtrs pp{};
     for (int l = 1; l <= h.kappa; ++l) pp.P[l] = h.levels[(size_t)l].Pr;
     H2D_CUDA(cudaMemsetAsync(h.d_yacc, 0, h.n * sizeof(double), hi));
     H2D_CUDA(cudaMemsetAsync(h.d_counters + 8, 0, sizeof(int32_t), hi));
     ++h.pair_epoch;
     if (h.n_pitems > 0) {
-      pair_apply_kernel<<<(int)std::min<int64_t>(2 * (int64_t)h.num_sms, h.n_pitems), kPipeThreads, smem, hi>>>(
-          (const PItem*)h.d_pitems, (int)h.n_pitems, h.d_counters + 8, pp, d_xtree, h.d_yacc, h.d_tP1, h.d_tP2,
-          h.d_ptpart, h.d_pcount, h.d_pflags, h.pair_epoch);
+      pair_apply_kernel<<<(int)std::min<int64_t>(2 * (int64_t)h.num_sms, h.n_pitems), 32 * kPWarps, 0, hi>>>(
+          (const PWork*)h.d_pitems, (int)h.n_pitems, (const PPair*)h.d_ppairs, h.d_counters + 8, pp, d_xtree,
+          h.d_yacc, h.d_tP1, h.d_tP2, h.d_ptpart, h.d_pcount, h.d_pflags, h.pair_epoch);
       H2D_LAUNCH_CHECK();
     }
     record(h, 2, hi);

@@ -40,13 +40,17 @@ struct KernelParams {
   int test_rank;
 };
 
+// Internal kernel id of the near-field kernels: the log kernel with subnormal-safe table
+// logarithms (handles whose near field has a pair of distinct points with subnormal r^2).
+constexpr int kLogSafe = 5;
+
 // K(p, q) specialised at compile time (hot P2P loop: no per-pair dispatch).
 template <int KID>
 __device__ __forceinline__ double kernel_eval_t(const KernelParams& k, double px, double py,
                                                 double qx, double qy) {
   const double dx = px - qx, dy = py - qy;
   const double r2 = fma(dx, dx, dy * dy);
-  if (KID == H2D_KERNEL_LOG) {
+  if (KID == H2D_KERNEL_LOG || KID == kLogSafe) {
     return r2 > 0.0 ? 0.5 * log(r2) : 0.0;
   } else if (KID == H2D_KERNEL_IMQ) {
     return rsqrt(fma(r2, k.inv_c2, 1.0));
@@ -314,7 +318,8 @@ struct Handle {
   bool pairapply = false;
   bool pair_wanted = false;               // symmetric single-rank handle (H2D_PAIRAPPLY != 0)
   bool pair_failed = false;               // a rank above 127 in the current factors
-  void* d_pitems = nullptr;               // PItem[]
+  void* d_pitems = nullptr;               // PWork[]
+  void* d_ppairs = nullptr;               // PPair[]
   int64_t n_pitems = 0;
   double *d_tP1 = nullptr, *d_tP2 = nullptr, *d_ptpart = nullptr;
   int32_t *d_pcount = nullptr, *d_pflags = nullptr;
@@ -358,6 +363,8 @@ struct Handle {
   // build, changeable per handle with hodlr2d_set_diag (never per call from the environment)
   bool diag_p2p_serial = false, diag_p2p_onestream = false, diag_dual_norow = false;
   bool diag_copy_stream = true;
+  // near-field kernel id (kp.id, or kLogSafe when a near pair has a subnormal r^2)
+  int p2p_kid = 0;
   // pinned host staging of pageable caller buffers (0: inputs, 1: outputs)
   void* pin[2] = {nullptr, nullptr};
   size_t pin_bytes[2] = {0, 0};

@@ -1447,7 +1447,10 @@ static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, i
   }
   H2D_CUDA(cudaEventRecord(h.ev_far, hi));
   switch (h.kp.id) {
-    case H2D_KERNEL_LOG: launch_p2p_multi<H2D_KERNEL_LOG, NR>(h, a); break;
+    case H2D_KERNEL_LOG:
+      if (h.p2p_kid == kLogSafe) launch_p2p_multi<kLogSafe, NR>(h, a);
+      else launch_p2p_multi<H2D_KERNEL_LOG, NR>(h, a);
+      break;
     case H2D_KERNEL_IMQ: launch_p2p_multi<H2D_KERNEL_IMQ, NR>(h, a); break;
     case H2D_KERNEL_ONE_OVER_R: launch_p2p_multi<H2D_KERNEL_ONE_OVER_R, NR>(h, a); break;
     case H2D_KERNEL_RBF_PHI1: launch_p2p_multi<H2D_KERNEL_RBF_PHI1, NR>(h, a); break;
@@ -1512,7 +1515,10 @@ static void multi_chunk_sym(Handle& h, const double* dX, int64_t xlen, double* d
   }
   H2D_CUDA(cudaEventRecord(h.ev_far, hi));
   switch (h.kp.id) {
-    case H2D_KERNEL_LOG: launch_p2p_multi<H2D_KERNEL_LOG, NR>(h, a); break;
+    case H2D_KERNEL_LOG:
+      if (h.p2p_kid == kLogSafe) launch_p2p_multi<kLogSafe, NR>(h, a);
+      else launch_p2p_multi<H2D_KERNEL_LOG, NR>(h, a);
+      break;
     case H2D_KERNEL_IMQ: launch_p2p_multi<H2D_KERNEL_IMQ, NR>(h, a); break;
     case H2D_KERNEL_ONE_OVER_R: launch_p2p_multi<H2D_KERNEL_ONE_OVER_R, NR>(h, a); break;
     case H2D_KERNEL_RBF_PHI1: launch_p2p_multi<H2D_KERNEL_RBF_PHI1, NR>(h, a); break;

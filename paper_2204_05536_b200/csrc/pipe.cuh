@@ -85,16 +85,25 @@ __constant__ double c_hlog[8] = {0.34657359027997264,   // ln2 / 2 (high part)
                                  1.1595234069231498e-17, // ln2 / 2 (low part)
                                  0.5, -0.25, 1.0 / 6.0, -0.125, 0.1, -1.0 / 12.0};
 
-// Subnormal r2 (points closer than ~1.5e-154) are normalised in the integer pipe: the
+// SAFE: subnormal r2 (points closer than ~1.5e-154) are normalised in the integer pipe: the
 // mantissa is shifted until its leading one is the implicit bit (sh = 0 for normal r2) and
 // the exponent becomes 1 - sh - 1023.  r2 = 0 gives a finite value the callers replace by
 // K(0) = 0 (R8).
+// SAFE = false (the default near field): r2 must be normal or 0; the build checks the
+// near field once and switches the handle to SAFE kernels (kLogSafe) if any pair of distinct
+// points has a subnormal r2, so the common case pays no normalisation.
+template <bool SAFE = false>
 __device__ __forceinline__ double hlog_r2(double r2, const double2* __restrict__ tab) {
   long long bits = __double_as_longlong(r2);
-  const int E = (int)(bits >> 52);
-  const int sh = max(0, __clzll(bits) - 11);
-  bits <<= sh;
-  const int e = (E == 0 ? 1 - sh : E) - 1023;
+  int e;
+  if (SAFE) {
+    const int E = (int)(bits >> 52);
+    const int sh = max(0, __clzll(bits) - 11);
+    bits <<= sh;
+    e = (E == 0 ? 1 - sh : E) - 1023;
+  } else {
+    e = (int)(bits >> 52) - 1023;
+  }
   const int k = (int)(bits >> 45) & 127;
   const double mnt = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
   const double2 tb = tab[k];
@@ -119,8 +128,8 @@ __device__ __forceinline__ void hlog_table(double2* tab) {
 // the rare pairs closer than a); distance kernels only.
 template <int KID>
 __device__ __forceinline__ double kfast(double r2, const double2* __restrict__ tab, const KernelParams& kp) {
-  if (KID == H2D_KERNEL_LOG) {
-    const double v = hlog_r2(r2, tab);
+  if (KID == H2D_KERNEL_LOG || KID == kLogSafe) {
+    const double v = hlog_r2<KID == kLogSafe>(r2, tab);
     return r2 > 0.0 ? v : 0.0;
   } else if (KID == H2D_KERNEL_IMQ) {
     return rsqrt(fma(r2, kp.inv_c2, 1.0));
@@ -141,10 +150,10 @@ __device__ __forceinline__ double kfast(double r2, const double2* __restrict__ t
 }
 
 template <int KID>
-constexpr bool kDistKernel = KID == H2D_KERNEL_LOG || KID == H2D_KERNEL_IMQ || KID == H2D_KERNEL_ONE_OVER_R ||
+constexpr bool kDistKernel = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == H2D_KERNEL_IMQ || KID == H2D_KERNEL_ONE_OVER_R ||
                              KID == H2D_KERNEL_RBF_PHI1 || KID == H2D_KERNEL_RBF_PHI2;
 template <int KID>
-constexpr bool kNeedsLogTable = KID == H2D_KERNEL_LOG || KID == H2D_KERNEL_RBF_PHI1;
+constexpr bool kNeedsLogTable = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == H2D_KERNEL_RBF_PHI1;
 
 __device__ __forceinline__ uint32_t p2p_spread(uint32_t v) {
   v &= 0xFFFFu;

@@ -123,7 +123,11 @@ def _sym_pair(h2d, pts, kernel, leaf, tol, **kw):
     import os
     args = dict(box_lo=(-1, -1), box_side=2.0, symmetric=True)
     args.update(kw)
-    op = h2d.Hodlr2d.build(dev(pts), kernel, leaf, tol, **args)
+    os.environ["H2D_PAIRAPPLY"] = "1"   # (both applies on one handle: set_diag switches)
+    try:
+        op = h2d.Hodlr2d.build(dev(pts), kernel, leaf, tol, **args)
+    finally:
+        os.environ.pop("H2D_PAIRAPPLY")
     os.environ["H2D_SYMAPPLY"] = "0"
     os.environ["H2D_PAIRAPPLY"] = "0"
     try:
@@ -157,7 +161,8 @@ def test_symmetric_apply_multichunk_items(h2d):
         x = W.random_vector(n, 900 + k)
         yr = ref.matvec(dev(x)).cpu().numpy()
         for y in both_applies(op, x):
-            assert rel(y, yr) <= 1e-13
+            if y is not None:
+                assert rel(y, yr) <= 1e-13
 
 
 def test_symmetric_apply_wide_panels(h2d, capfd):
@@ -200,7 +205,7 @@ def test_symmetric_apply_cases(h2d, case):
     x = W.random_vector(n, 920)
     yr = ref.matvec(dev(x)).cpu().numpy()
     yp, y = both_applies(op, x)
-    assert rel(y, yr) <= 1e-13 and rel(yp, yr) <= 1e-13
+    assert rel(y, yr) <= 1e-13 and (yp is None or rel(yp, yr) <= 1e-13)
     kid = {"log": 0, "imq": 1, "rbf_phi1": 3}[kernel]
     yd = oracle.dense_matvec(pts, x, kid, kw.get("c", 1.0), 1.0, kw.get("shift", 0.0))
     assert rel(y, yd) <= 1e-8
