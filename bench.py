@@ -822,7 +822,8 @@ def run_gmres(args):
     n = pts.shape[0]
     t0 = time.time()
     op = h2d.Hodlr2d.build(torch.from_numpy(pts).cuda(), args.rbf_kernel, args.nmax, 1e-12, c=1e-3, scale=1.0,
-                           shift=float(n), box_lo=(-1, -1), box_side=2.0, depth=-3 if args.adaptive else -2)
+                           shift=float(n), box_lo=(-1, -1), box_side=2.0, depth=-3 if args.adaptive else -2,
+                           symmetric=args.symmetric)
     torch.cuda.synchronize()
     t_i = time.time() - t0
     inf = op.info()
@@ -848,7 +849,8 @@ def run_gmres(args):
     err = float(torch.linalg.norm(lam_hat - lam) / torch.linalg.norm(lam))
     line = {"mode": "gmres", "workload": f"{args.rbf_kernel}, {args.grid_m}^2 Chebyshev grid, a = 0.001, "
                                          f"beta = N, ACA 1e-12, N_max {args.nmax} "
-                                         + ("(adaptive quadtree, R24)" if args.adaptive else "(paper depth rule)"),
+                                         + ("(adaptive quadtree, R24)" if args.adaptive else "(paper depth rule)")
+                                         + (", symmetric build + apply (R23)" if args.symmetric else ""),
             "n_leaves": inf["n_leaves"], "near_pairs": inf["near_pairs"],
             "factor_gb": (inf["u_values"] + inf["v_values"]) * 8e-9,
             "n": n, "kappa": inf["kappa"], "rank_max": inf["rank_max"],

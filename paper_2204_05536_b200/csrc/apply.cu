@@ -1601,6 +1601,9 @@ void finalize_schedule(Handle& h) {
     H2D_CUDA(cudaMemsetAsync(h.d_pflags, 0, std::max<int64_t>(2, 2 * nbig) * 4, s));
     h.pair_epoch = 0;
     if (!h.d_yacc) h.d_yacc = h.alloc<double>(h.n);
+    // CTAs per SM (diagnostics: H2D_PAIR_CTAS): 3 measured faster overall than 2 (which leave
+    // the registers for a co-resident near field but run the pairs 1.5x slower)
+    h.pair_ctas_per_sm = getenv("H2D_PAIR_CTAS") ? std::max(1, atoi(getenv("H2D_PAIR_CTAS"))) : 3;
   }
   // the log kernel's near field: subnormal-safe table log only if some near pair needs it
   h.p2p_kid = h.kp.id;
@@ -1910,7 +1913,8 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
     H2D_CUDA(cudaMemsetAsync(h.d_counters + 8, 0, sizeof(int32_t), hi));
     ++h.pair_epoch;
     if (h.n_pitems > 0) {
-      pair_apply_kernel<<<(int)std::min<int64_t>(2 * (int64_t)h.num_sms, h.n_pitems), 32 * kPWarps, 0, hi>>>(
+      pair_apply_kernel<<<(int)std::min<int64_t>(h.pair_ctas_per_sm * (int64_t)h.num_sms, h.n_pitems), 32 * kPWarps,
+                          0, hi>>>(
           (const PWork*)h.d_pitems, (int)h.n_pitems, (const PPair*)h.d_ppairs, h.d_counters + 8, pp, d_xtree,
           h.d_yacc, h.d_tP1, h.d_tP2, h.d_ptpart, h.d_pcount, h.d_pflags, h.pair_epoch);
       H2D_LAUNCH_CHECK();

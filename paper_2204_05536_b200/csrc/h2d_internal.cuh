@@ -324,6 +324,7 @@ struct Handle {
   double *d_tP1 = nullptr, *d_tP2 = nullptr, *d_ptpart = nullptr;
   int32_t *d_pcount = nullptr, *d_pflags = nullptr;
   int pair_epoch = 0;
+  int pair_ctas_per_sm = 2;
   int64_t pair_values = 0;                // factor values the pair kernel streams (U + V)
   double* d_yacc = nullptr;               // [n] TREE-order accumulator of the pair kernel
   // multi-RHS (multi.cu): tiled stage-A schedule and per-chunk buffers (<= 8 vectors)

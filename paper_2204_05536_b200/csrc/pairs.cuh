@@ -76,11 +76,6 @@ __device__ __forceinline__ void pair_tiles(const double* __restrict__ F, int64_t
                                            int t0, int ts, const double* __restrict__ x, const double* tv,
                                            double* __restrict__ dy, double (&acc)[NC]) {
   const int lane = threadIdx.x & 31;
-  double tq[NC];
-  if (ROWS) {
-#pragma unroll
-    for (int q = 0; q < NC; ++q) tq[q] = q < nc ? tv[c0 + q] : 0.0;
-  }
   for (int t = t0; 32 * t < rows; t += ts) {
     const int i = 32 * t + lane;
     const bool ok = i < rows;
@@ -95,9 +90,9 @@ __device__ __forceinline__ void pair_tiles(const double* __restrict__ F, int64_t
     if (ROWS) {
       double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-      for (int q = 0; q < NC; q += 2) {
-        d0 = fma(v[q], tq[q], d0);
-        if (q + 1 < NC) d1 = fma(v[q + 1], tq[q + 1], d1);
+      for (int q = 0; q < NC; q += 2) {   // (t from shared memory: a broadcast load per column)
+        if (q < nc) d0 = fma(v[q], tv[c0 + q], d0);
+        if (q + 1 < NC && q + 1 < nc) d1 = fma(v[q + 1], tv[c0 + q + 1], d1);
       }
       if (ok) {
         if (kPNoRed) dy[i] = d0 + d1;   // diagnostics only (WRONG results)
@@ -262,7 +257,7 @@ __device__ void pair_cta(const PWork& w, const PPair& p, const double* __restric
   }
 }
 
-__global__ void __launch_bounds__(32 * kPWarps, 2)
+__global__ void __launch_bounds__(32 * kPWarps, 3)
 pair_apply_kernel(const PWork* __restrict__ work, int n_work, const PPair* __restrict__ pairs, int32_t* counter,
                   PairPtrs pp, const double* __restrict__ x, double* __restrict__ yacc, double* __restrict__ tP1,
                   double* __restrict__ tP2, double* __restrict__ tpart, int32_t* __restrict__ pcount,

@@ -144,3 +144,32 @@ def test_adaptive_gmres_rbf(h2d):
     x, its, rr = op.gmres(dev(f), tol=1e-10)
     assert rr < 1e-10
     assert rel(x.cpu().numpy(), lam) < 1e-9
+
+
+def test_adaptive_symmetric_three_pass_apply(h2d, tmp_path):
+    """Symmetric adaptive handles run the three-pass symmetric apply (A' / B' / C' over the
+    adaptive leaves and existing boxes): oracle symmetric adaptive factors <= 1e-12, GPU factors
+    vs dense <= 10 tol, and the directed panels of the same build to 1e-13."""
+    import os
+    pts = W.chebyshev_grid(130)
+    n = pts.shape[0]
+    kw = dict(c=1e-3, shift=float(n), symmetric=True)
+    op = gpu(h2d, pts, "rbf_phi1", 64, 1e-12, **kw)
+    inf = op.info()
+    assert inf["symmetric_apply"] == 1 and inf["adaptive"] == 1
+    x = W.random_vector(n, 21)
+    y = op.matvec(dev(x)).cpu().numpy()
+    yd = oracle.dense_matvec(pts, x, 3, 1e-3, 1.0, float(n))
+    assert np.linalg.norm(y - yd) / np.linalg.norm(yd - n * x) <= 1e-11
+    os.environ["H2D_SYMAPPLY"] = "0"
+    try:
+        ref = gpu(h2d, pts, "rbf_phi1", 64, 1e-12, **kw)
+    finally:
+        os.environ.pop("H2D_SYMAPPLY")
+    assert ref.info()["symmetric_apply"] == 0
+    assert rel(y, ref.matvec(dev(x)).cpu().numpy()) <= 1e-13
+    o = orc(pts, 3, 64, 1e-12, c=1e-3, shift=float(n), symmetric=True)
+    path = tmp_path / "sym.h2df"
+    o.save_factors(path)
+    op.load_factors(path)
+    assert rel(op.matvec(dev(x)).cpu().numpy(), o.matvec(x)) <= 1e-12
