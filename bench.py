@@ -453,8 +453,9 @@ def run_ours(args, cfg):
         _, ls = op.tree()
         msz = np.diff(ls[inf["leaf_begin"]: inf["leaf_end"] + 1]).astype(np.float64)
         self_pairs = float((msz * msz).sum())
-        warp_only = inf["p2p_leaves"][1] == 0 and inf["p2p_leaves"][2] == 0
-        evals = self_pairs + (inf["p2p_pairs"] - self_pairs) / 2.0 if warp_only else (inf["p2p_pairs"] + served) / 2.0
+        warp = msz <= 96   # warp-per-leaf path: full self blocks; CTA paths: i <= j only
+        evals = float((msz[warp] ** 2).sum() + (msz[~warp] * (msz[~warp] + 1) / 2).sum()) \
+            + (inf["p2p_pairs"] - self_pairs) / 2.0
     alone_ms = p2p_standalone_ms(op, step, args) if world == 1 else None
     peak_ops, peak_ops_kind = 148 * 64 * sm_hz, "nominal: 148 SMs x 64 FP64 lanes x SM clock"
     try:
