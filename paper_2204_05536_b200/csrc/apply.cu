@@ -70,24 +70,6 @@ __global__ void vpack_kernel(const VPackItem* __restrict__ items) {
   }
 }
 
-// Column-major n x r -> tile-major (pairs.cuh): 32-row tiles, the last one padded to an even
-// row count with zero rows, each tile column-major (leading dimension = its padded rows).
-struct TilePackItem {
-  const double* src;
-  double* dst;
-  int32_t n, r;
-};
-__global__ void tilepack_kernel(const TilePackItem* __restrict__ items) {
-  const TilePackItem it = items[blockIdx.x];
-  const int64_t tot = (int64_t)it.n * it.r;
-  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
-    const int64_t q = e / it.n, i = e - q * it.n;
-    const int64_t t = i >> 5, j = i & 31;
-    const int64_t rows = min((int64_t)32, (int64_t)it.n - 32 * t), prow = (rows + 1) & ~1;
-    it.dst[32 * t * it.r + q * prow + j] = it.src[e];
-  }
-}
-
 template <class T>
 T* upload_tmp(const std::vector<T>& v, cudaStream_t s) {
   T* p = nullptr;
@@ -974,15 +956,12 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
     if (h.pair_failed)   // ranks above kPMaxR: the pair apply is off for these factors
       for (auto& Lv : h.levels) { h.release(Lv.Pr); Lv.Pr = nullptr; Lv.pairs.clear(); }
   }
-  std::vector<TilePackItem> titems;
   if (h.pair_wanted && !h.pair_failed) {
     // pair apply (pairs.cuh): per pair {X, Y}, X < Y, V_XY (n_Y x r) then U_XY (m_X x r),
-    // tile-major (32-row tiles, the last padded to an even row count); pairs in CSR order of
-    // their first side X
+    // column-major as the ACA stores them; pairs in CSR order of their first side X
     h.release(L.Pr);
     L.Pr = nullptr;
     L.pairs.clear();
-    auto tiled = [](int64_t n) { return n <= 0 ? 0 : 32 * ((n - 1) / 32) + ((n - 32 * ((n - 1) / 32) + 1) & ~1); };
     int64_t po = 0, pvals = 0;
     for (int64_t X = 0; X < nbox; ++X) {
       const int64_t m = h.box_end(l, X) - h.box_begin(l, X);
@@ -991,23 +970,23 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
         const int r = rank_all(e);
         const int64_t n = h.box_end(l, Y) - h.box_begin(l, Y);
         if (Y < X || r == 0 || m == 0 || n == 0) continue;
-        Level::PairDesc d{po, po + tiled(n) * r, (int32_t)h.box_begin(l, Y), (int32_t)h.box_begin(l, X), (int32_t)n,
+        Level::PairDesc d{po, po + n * r, (int32_t)h.box_begin(l, Y), (int32_t)h.box_begin(l, X), (int32_t)n,
                           (int32_t)m, r, r};
         L.pairs.push_back(d);
-        po = (po + (tiled(n) + tiled(m)) * r + 1) & ~(int64_t)1;   // 16-byte aligned pairs
+        po += (n + m) * r;
         pvals += (n + m) * r;
-        titems.push_back(TilePackItem{srcV[(size_t)e], nullptr, (int32_t)n, r});
-        titems.push_back(TilePackItem{srcU[(size_t)e], nullptr, (int32_t)m, r});
+        uitems.push_back(UCopyItem{srcV[(size_t)e], nullptr, (int32_t)n, (int32_t)n, (int32_t)n, r});
+        uitems.push_back(UCopyItem{srcU[(size_t)e], nullptr, (int32_t)m, (int32_t)m, (int32_t)m, r});
       }
     }
     L.pr_alloc = po;
     L.pr_values = pvals;
     L.Pr = h.alloc<double>(po);
-    H2D_CUDA(cudaMemsetAsync(L.Pr, 0, std::max<int64_t>(1, po) * sizeof(double), s));   // pad rows
-    size_t k0 = 0;
+    // destinations now that the array exists (the last 2 x pairs items are the pair copies)
+    size_t k0 = uitems.size() - 2 * L.pairs.size();
     for (const auto& d : L.pairs) {
-      titems[k0++].dst = L.Pr + d.v_off;
-      titems[k0++].dst = L.Pr + d.u_off;
+      uitems[k0++].dst = L.Pr + d.v_off;
+      uitems[k0++].dst = L.Pr + d.u_off;
     }
   }
   const size_t CH = 1 << 20;
@@ -1022,13 +1001,6 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
     std::vector<VPackItem> part(vitems.begin() + c0, vitems.begin() + std::min(vitems.size(), c0 + CH));
     VPackItem* d = upload_tmp(part, s);
     vpack_kernel<<<(int)part.size(), 256, 0, s>>>(d);
-    H2D_LAUNCH_CHECK();
-    H2D_CUDA(cudaFreeAsync(d, s));
-  }
-  for (size_t c0 = 0; c0 < titems.size(); c0 += CH) {
-    std::vector<TilePackItem> part(titems.begin() + c0, titems.begin() + std::min(titems.size(), c0 + CH));
-    TilePackItem* d = upload_tmp(part, s);
-    tilepack_kernel<<<(int)part.size(), 256, 0, s>>>(d);
     H2D_LAUNCH_CHECK();
     H2D_CUDA(cudaFreeAsync(d, s));
   }
@@ -1514,14 +1486,16 @@ void finalize_schedule(Handle& h) {
   }
   h.pairapply = h.pair_wanted && !h.pair_failed;
   if (h.pairapply) {
-    // pair apply schedule (pairs.cuh): the big pairs of the coarse levels as chunks of
-    // kPChunkTiles tiles per phase (merged by byte position with a lag, every chunk after all
-    // chunks of its pair's previous phase), then the whole pairs, largest first
+    // pair apply schedule (pairs.cuh): the big pairs of the coarse levels as row chunks per
+    // phase (merged by byte position with a lag, every chunk after all chunks of the pair's
+    // previous phase), then the medium pairs (one CTA each), then groups of 8 small pairs
+    // (one warp each), each class largest first
     std::vector<PPair> prs;
-    std::vector<std::pair<int64_t, int32_t>> big, whole;
+    std::vector<std::pair<int64_t, int32_t>> big, whole, small;
     int64_t pvals = 0;
     int lv_lo = 1, lv_hi = h.kappa;   // diagnostics: H2D_PAIR_LEVELS=lo,hi (WRONG results; timing only)
     if (getenv("H2D_PAIR_LEVELS")) sscanf(getenv("H2D_PAIR_LEVELS"), "%d,%d", &lv_lo, &lv_hi);
+    const int64_t small_max = getenv("H2D_PAIR_SMALL_MAX") ? atoll(getenv("H2D_PAIR_SMALL_MAX")) : kPSmallBytes;
     const int64_t whole_max = getenv("H2D_PAIR_WHOLE_MAX") ? atoll(getenv("H2D_PAIR_WHOLE_MAX")) : kPWholeBytes;
     for (int l = std::max(1, lv_lo); l <= std::min(h.kappa, lv_hi); ++l) {
       const Level& L = h.levels[(size_t)l];
@@ -1530,30 +1504,40 @@ void finalize_schedule(Handle& h) {
         prs.push_back(PPair{d.v_off, d.u_off, d.yv, d.yu, d.nv, d.nu, d.R, l});
         const int64_t bytes = (int64_t)(d.nv + d.nu) * d.R * 8;
         pvals += (int64_t)(d.nv + d.nu) * d.R;
-        (bytes <= whole_max ? whole : big).push_back({bytes, id});
+        (bytes <= small_max ? small : bytes <= whole_max ? whole : big).push_back({bytes, id});
       }
     }
     h.pair_values = pvals;
     auto by_size = [](const auto& a, const auto& b) { return a.first > b.first; };
     std::stable_sort(big.begin(), big.end(), by_size);
     std::stable_sort(whole.begin(), whole.end(), by_size);
+    std::stable_sort(small.begin(), small.end(), by_size);
+    // groups reference consecutive descriptors: reorder the small pairs' descriptors
+    std::vector<PPair> ordered;
+    ordered.reserve(prs.size());
+    std::vector<int32_t> newid(prs.size());
+    for (auto* cls : {&big, &whole, &small})
+      for (auto& b : *cls) {
+        newid[(size_t)b.second] = (int32_t)ordered.size();
+        ordered.push_back(prs[(size_t)b.second]);
+        b.second = newid[(size_t)b.second];
+      }
     std::vector<PWork> work;
     const int64_t nbig = (int64_t)big.size();
     std::vector<std::vector<PWork>> ph[3];
     for (int b = 0; b < 3; ++b) ph[b].resize((size_t)nbig);
     int64_t toff = 0, poff = 0;
     for (int64_t k = 0; k < nbig; ++k) {
-      const PPair& p = prs[(size_t)big[(size_t)k].second];
+      const PPair& p = ordered[(size_t)big[(size_t)k].second];
       for (int q = 1; q <= 3; ++q) {
         const int n = q == 2 ? p.nu : p.nv;
-        const int ntile = (n + 31) / 32;
-        const int nch = (ntile + kPChunkTiles - 1) / kPChunkTiles;
+        const int nch = (n + kPChunkRows - 1) / kPChunkRows;
         for (int c = 0; c < nch; ++c) {
           PWork w{};
-          w.kind = q;
-          w.pair = big[(size_t)k].second;
-          w.t0 = c * kPChunkTiles;
-          w.t1 = std::min(ntile, (c + 1) * kPChunkTiles);
+          w.kind = kPPhase1 + q - 1;
+          w.first = big[(size_t)k].second;
+          w.r0 = c * kPChunkRows;
+          w.r1 = std::min(n, (c + 1) * kPChunkRows);
           w.big = (int32_t)k;
           w.chunk = c;
           w.nchunks = nch;
@@ -1565,21 +1549,20 @@ void finalize_schedule(Handle& h) {
       }
       toff += p.r;
     }
-    // lag ~ two rounds of chunks over every warp of the grid
     const double lag = getenv("H2D_PAIR_LAG") ? atof(getenv("H2D_PAIR_LAG"))
-                                              : 2.0 * (kPWarps * (double)h.num_sms) * kPChunkTiles * 32 * 16 * 8.0;
+                                              : 1.5 * (2.0 * h.num_sms) * kPChunkRows * 20 * 8.0;
     std::vector<std::pair<double, PWork>> keyed;
     std::vector<double> prev_end((size_t)nbig, -1.0);
     for (int q = 0; q < 3; ++q) {
       double pos = 0.0;
       std::vector<double> end((size_t)nbig, 0.0);
       for (int64_t k = 0; k < nbig; ++k) {
-        const PPair& p = prs[(size_t)big[(size_t)k].second];
+        const PPair& p = ordered[(size_t)big[(size_t)k].second];
         for (const PWork& w : ph[q][(size_t)k]) {
           const double key = std::max(pos + q * lag, prev_end[(size_t)k] + 1.0);
           keyed.push_back({key, w});
           end[(size_t)k] = std::max(end[(size_t)k], key);
-          pos += (double)(w.t1 - w.t0) * 32 * p.r * 8.0;
+          pos += (double)(w.r1 - w.r0) * p.r * 8.0;
         }
       }
       prev_end = end;
@@ -1589,7 +1572,14 @@ void finalize_schedule(Handle& h) {
     for (auto& b : whole) {
       PWork w{};
       w.kind = kPWhole;
-      w.pair = b.second;
+      w.first = b.second;
+      work.push_back(w);
+    }
+    for (size_t i = 0; i < small.size(); i += kPWarps) {
+      PWork w{};
+      w.kind = kPGroup;
+      w.first = small[i].second;
+      w.count = (int32_t)std::min<size_t>(kPWarps, small.size() - i);
       work.push_back(w);
     }
     h.n_pitems = (int64_t)work.size();
@@ -1597,11 +1587,11 @@ void finalize_schedule(Handle& h) {
                     (void*)h.d_pflags})
       h.release(q);
     h.d_pitems = h.alloc<PWork>(work.size());
-    h.d_ppairs = h.alloc<PPair>(prs.size());
+    h.d_ppairs = h.alloc<PPair>(ordered.size());
     if (!work.empty())
       H2D_CUDA(cudaMemcpyAsync(h.d_pitems, work.data(), work.size() * sizeof(PWork), cudaMemcpyHostToDevice, s));
-    if (!prs.empty())
-      H2D_CUDA(cudaMemcpyAsync(h.d_ppairs, prs.data(), prs.size() * sizeof(PPair), cudaMemcpyHostToDevice, s));
+    if (!ordered.empty())
+      H2D_CUDA(cudaMemcpyAsync(h.d_ppairs, ordered.data(), ordered.size() * sizeof(PPair), cudaMemcpyHostToDevice, s));
     h.d_tP1 = h.alloc<double>(std::max<int64_t>(2, toff + 2));
     h.d_tP2 = h.alloc<double>(std::max<int64_t>(2, toff + 2));
     h.d_ptpart = h.alloc<double>(std::max<int64_t>(1, poff));
@@ -1611,6 +1601,9 @@ void finalize_schedule(Handle& h) {
     H2D_CUDA(cudaMemsetAsync(h.d_pflags, 0, std::max<int64_t>(2, 2 * nbig) * 4, s));
     h.pair_epoch = 0;
     if (!h.d_yacc) h.d_yacc = h.alloc<double>(h.n);
+    // CTAs per SM (diagnostics: H2D_PAIR_CTAS): 3 measured faster overall than 2 (which leave
+    // the registers for a co-resident near field but run the pairs 1.5x slower)
+    h.pair_ctas_per_sm = getenv("H2D_PAIR_CTAS") ? std::max(1, atoi(getenv("H2D_PAIR_CTAS"))) : 3;
   }
   // the log kernel's near field: subnormal-safe table log only if some near pair needs it
   h.p2p_kid = h.kp.id;
@@ -1920,14 +1913,10 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
     H2D_CUDA(cudaMemsetAsync(h.d_counters + 8, 0, sizeof(int32_t), hi));
     ++h.pair_epoch;
     if (h.n_pitems > 0) {
-      static uint64_t seen = 0;
-      const size_t smem = kPWarps * sizeof(PairWarpSmem);
-      once_per_device(seen, [&] {
-        H2D_CUDA(cudaFuncSetAttribute(pair_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      });
-      pair_apply_kernel<<<(int)std::min<int64_t>(h.num_sms, (h.n_pitems + kPWarps - 1) / kPWarps), 32 * kPWarps, smem,
-                          hi>>>((const PWork*)h.d_pitems, (int)h.n_pitems, (const PPair*)h.d_ppairs, h.d_counters + 8, pp,
-                                d_xtree, h.d_yacc, h.d_tP1, h.d_tP2, h.d_ptpart, h.d_pcount, h.d_pflags, h.pair_epoch);
+      pair_apply_kernel<<<(int)std::min<int64_t>(h.pair_ctas_per_sm * (int64_t)h.num_sms, h.n_pitems), 32 * kPWarps,
+                          0, hi>>>(
+          (const PWork*)h.d_pitems, (int)h.n_pitems, (const PPair*)h.d_ppairs, h.d_counters + 8, pp, d_xtree,
+          h.d_yacc, h.d_tP1, h.d_tP2, h.d_ptpart, h.d_pcount, h.d_pflags, h.pair_epoch);
       H2D_LAUNCH_CHECK();
     }
     record(h, 2, hi);

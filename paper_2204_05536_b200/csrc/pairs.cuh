@@ -1,4 +1,4 @@
-// Pair-local symmetric apply (NEXT N1 payoff, R23 / §10 "pair apply").
+// Pair-local symmetric apply (NEXT N1 payoff, R23 / §6 "pair apply").
 //
 // A symmetric build stores one factor pair per unordered box pair {X, Y}, X < Y (Morton):
 // K(X, Y) ~ U V^T and K(Y, X) ~ V U^T (the paper's symmetric setting).  Alg. 2 l.15
@@ -9,70 +9,47 @@
 //   phase 1  V rows          -> column sums t1 = V^T x_Y
 //   phase 2  U rows          -> column sums t2 = U^T x_X and row dots dy_X = U t1
 //   phase 3  V rows again    -> row dots dy_Y = V t2 (an L2 hit: V was just read)
-// Layout: each factor (n rows x r columns) is stored tile-major — 32-row tiles (the last one
-// padded to an even row count), each tile column-major — so any (tile, block of <= 16
-// columns) is one contiguous range: a "sub-tile".  Every warp runs its own pipeline: it
-// reserves work items from a queue, issues the sub-tiles of its items into a ring of kPSlots
-// shared-memory slots by bulk copies (TMA engine; the x values of the rows by 8-byte
-// cp.async on the same mbarrier) up to kPSlots ahead, across item boundaries, and consumes
-// them in order with lane = row: column sums by warp shuffles at the end of each column block,
-// row dots added to the TREE-order accumulator yacc by fp64 REDs.  Items: a whole small /
-// medium pair (all three phases in one warp), or a chunk of tiles of one phase of a big pair
-// (any warp; the last chunk of a phase reduces the partials in chunk order and publishes t1 /
-// t2 behind a flag = matvec epoch; a later phase's chunk waits for it when it starts consuming).
-// The queue puts every chunk after all chunks of its pair's previous phase, and a warp only
-// waits on items earlier in the queue than the one it consumes, so the earliest unfinished
-// item always progresses.  Not bitwise reproducible (the order of the y accumulations varies).
+// The factors stay in the ACA's column-major layout, V then U per pair.  Lane = row: a warp
+// reads a 32-row tile of a column as one coalesced 256-byte load, so the narrow per-pair
+// panels (rank ~10-40) use every lane; column sums are reduced by warp shuffles, row dots
+// need none.  dy rows go to the TREE-order accumulator yacc (L2-resident) by fp64 REDs on
+// 32 consecutive rows.  Work items: groups of up to 8 small pairs (one warp each), medium
+// pairs (the 8 warps of a CTA split the tiles), and row chunks of the big pairs of the coarse
+// levels (any CTA; the last chunk of a phase reduces the partials in chunk order and
+// publishes t1 / t2 with a flag = matvec epoch; a later phase's chunk waits for it).
+// Not bitwise reproducible: the order of the y accumulations varies between runs.
 #pragma once
 #include "pipe.cuh"
 
 namespace h2d {
 namespace {
 
-constexpr int kPWarps = 8;                  // warps per CTA (each its own pipeline)
-constexpr int kPSlots = 5;                  // ring slots per warp
-constexpr int kPCB = 16;                    // columns per sub-tile
-constexpr int kPMaxR = 128;                 // widest pair (rank)
-constexpr int kPWholeBytes = 96 * 1024;     // pairs up to this: one warp, all phases
-constexpr int kPChunkTiles = 16;            // big pairs: chunks of 16 tiles (512 rows) per phase
+constexpr int kPWarps = 8;                  // warps per CTA
+constexpr int kPMaxR = 128;                 // widest pair (rank), column blocks of <= 16
+constexpr int kPSmallBytes = 48 * 1024;     // pairs up to this: one warp
+constexpr int kPWholeBytes = 640 * 1024;    // pairs up to this: one CTA, all phases
+constexpr int kPChunkRows = 2048;           // big pairs: row chunks (per phase)
 
-enum { kPWhole = 0, kPPhase1 = 1, kPPhase2 = 2, kPPhase3 = 3 };
+enum { kPGroup = 0, kPWhole = 1, kPPhase1 = 2, kPPhase2 = 3, kPPhase3 = 4 };
+#ifndef H2D_PAIR_NORED
+#define H2D_PAIR_NORED 0
+#endif
+constexpr bool kPNoRed = H2D_PAIR_NORED;   // build-time diagnostics switch (timing of the REDs)
 
 struct PPair {              // one stored pair
-  int64_t v_off, u_off;     // V (nv x r) and U (nu x r), tile-major, in the level's pair array
+  int64_t v_off, u_off;     // V (nv x r) and U (nu x r), column-major, in the level's pair array
   int32_t yv, yu;           // TREE rows of Y (V rows) and X (U rows)
   int32_t nv, nu, r, level;
 };
-struct PWork {              // one work item (a warp takes it)
-  int32_t kind;             // kPWhole, or the phase of a chunk
-  int32_t pair;
-  int32_t t0, t1;           // chunk: tiles [t0, t1) of the phase's factor
-  int32_t big, chunk, nchunks, pad;
+struct PWork {              // one work item (a CTA takes it)
+  int32_t kind;
+  int32_t first, count;     // kPGroup: pairs [first, first + count); else the pair `first`
+  int32_t r0, r1;           // chunk: rows [r0, r1) of the phase's factor
+  int32_t big, chunk, nchunks;
   int64_t toff, poff;       // big pair: t1 / t2 offset; partial slots of the phase
 };
 struct PairPtrs {
   const double* P[H2D_MAX_LEVELS + 1];
-};
-
-// one issued sub-tile (shared, per slot)
-struct PSub {
-  int32_t item;             // work item index; -1 = none (end of the queue)
-  int32_t ph;               // phase 1..3
-  int32_t c0, nc;           // column block
-  int32_t rows;             // rows of the tile (unpadded)
-  int32_t y0;               // TREE row of the tile's first row
-  int32_t flags;            // kSubFirstBlk / kSubLastBlk / kSubLastPh / kSubFirstItem
-  int32_t prow;             // padded rows (leading dimension in the slot)
-  int32_t t;                // tile index in the factor
-};
-constexpr int kSubFirstBlk = 1, kSubLastBlk = 2, kSubLastPh = 4, kSubFirstItem = 8;
-
-struct PairWarpSmem {
-  double data[kPSlots][32 * kPCB];
-  double xs[kPSlots][32];
-  PSub sub[kPSlots];
-  uint64_t full[kPSlots];
-  double t[2][kPMaxR];      // whole pairs: t1, t2; chunks: t of the phase in t[0]
 };
 
 __device__ __forceinline__ int ld_acquire(const int32_t* p) {
@@ -83,204 +60,234 @@ __device__ __forceinline__ int ld_acquire(const int32_t* p) {
 __device__ __forceinline__ void st_release(int32_t* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
-// The issue side of a warp's pipeline: walks the sub-tiles of its reserved items in order.
-struct PIssue {
-  int item = -1;            // current item (-1: reserve the next one)
-  PWork w;
-  PPair p;
-  int ph = 1, cb = 0, t = 0, tend = 0;
-  bool done = false;
-  bool first = true;
-};
-
-__device__ void pair_issue_next(PIssue& is, const PWork* __restrict__ work, int n_work, const PPair* __restrict__ pairs,
-                                int32_t* counter, PSub& s) {
+// One warp over the rows {tile * 32 + lane : tile = t0, t0 + ts, ...} < rows of columns
+// [c0, c0 + nc) (nc <= NC) of a column-major factor F (leading dimension ld):
+//   COLS  acc[q] += F[i, c0 + q] x[i]           (column sums, per lane)
+//   ROWS  dy[i]  += sum_q F[i, c0 + q] t[c0 + q] (row dots, one fp64 RED per row)
+template <int NC, bool COLS, bool ROWS>
+__device__ __forceinline__ void pair_tiles(const double* __restrict__ F, int64_t ld, int rows, int c0, int nc,
+                                           int t0, int ts, const double* __restrict__ x, const double* tv,
+                                           double* __restrict__ dy, double (&acc)[NC]) {
   const int lane = threadIdx.x & 31;
-  if (is.done) { s.item = -1; return; }
-  if (is.item < 0) {
-    int idx = 0;
-    if (lane == 0) idx = atomicAdd(counter, 1);
-    idx = __shfl_sync(0xffffffffu, idx, 0);
-    if (idx >= n_work) { is.done = true; s.item = -1; return; }
-    is.item = idx;
-    is.w = work[idx];
-    is.p = pairs[is.w.pair];
-    is.ph = is.w.kind == kPWhole ? 1 : is.w.kind;
-    is.cb = 0;
-    const int n = is.ph == 2 ? is.p.nu : is.p.nv;
-    is.t = is.w.kind == kPWhole ? 0 : is.w.t0;
-    is.tend = is.w.kind == kPWhole ? (n + 31) / 32 : is.w.t1;
-    is.first = true;
-  }
-  const PPair& p = is.p;
-  const int n = is.ph == 2 ? p.nu : p.nv;
-  const int nblk = (p.r + kPCB - 1) / kPCB;
-  s.item = is.item;
-  s.ph = is.ph;
-  s.c0 = is.cb * kPCB;
-  s.nc = min(kPCB, p.r - s.c0);
-  s.rows = min(32, n - 32 * is.t);
-  s.prow = (s.rows + 1) & ~1;
-  s.y0 = (is.ph == 2 ? p.yu : p.yv) + 32 * is.t;
-  s.t = is.t;
-  const int t0 = is.w.kind == kPWhole ? 0 : is.w.t0;
-  s.flags = (is.t == t0 ? kSubFirstBlk : 0) | (is.t + 1 == is.tend ? kSubLastBlk : 0) |
-            (is.first ? kSubFirstItem : 0);
-  const bool last_blk_of_phase = is.t + 1 == is.tend && is.cb + 1 == nblk;
-  if (last_blk_of_phase) s.flags |= kSubLastPh;
-  is.first = false;
-  // advance: tiles inner, column blocks outer, phases (whole pairs) outermost
-  if (++is.t == is.tend) {
-    is.t = t0;
-    if (++is.cb == nblk) {
-      is.cb = 0;
-      if (is.w.kind == kPWhole && is.ph < 3) {
-        ++is.ph;
-        const int n2 = is.ph == 2 ? p.nu : p.nv;
-        is.t = 0;
-        is.tend = (n2 + 31) / 32;
-      } else {
-        is.item = -1;
+  for (int t = t0; 32 * t < rows; t += ts) {
+    const int i = 32 * t + lane;
+    const bool ok = i < rows;
+    double v[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) v[q] = (ok && q < nc) ? __ldcs(F + (int64_t)(c0 + q) * ld + i) : 0.0;
+    if (COLS) {
+      const double xi = ok ? __ldg(x + i) : 0.0;
+#pragma unroll
+      for (int q = 0; q < NC; ++q) acc[q] = fma(v[q], xi, acc[q]);
+    }
+    if (ROWS) {
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < NC; q += 2) {   // (t from shared memory: a broadcast load per column)
+        if (q < nc) d0 = fma(v[q], tv[c0 + q], d0);
+        if (q + 1 < NC && q + 1 < nc) d1 = fma(v[q + 1], tv[c0 + q + 1], d1);
+      }
+      if (ok) {
+        if (kPNoRed) dy[i] = d0 + d1;   // diagnostics only (WRONG results)
+        else atomicAdd(dy + i, d0 + d1);
       }
     }
   }
 }
 
-__global__ void __launch_bounds__(32 * kPWarps, 1)
+template <int NC>
+__device__ __forceinline__ void zero_acc(double (&acc)[NC]) {
+#pragma unroll
+  for (int q = 0; q < NC; ++q) acc[q] = 0.0;
+}
+
+// Warp-level column sums of columns [c0, c0 + nc) into ts[c0 + q] (shared, per warp).
+template <int NC>
+__device__ __forceinline__ void warp_colsum_store(double (&acc)[NC], int c0, int nc, double* ts) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    const double s = warp_sum(acc[q]);
+    if (lane == 0 && q < nc) ts[c0 + q] = s;
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------- one warp, one pair
+template <int NC>
+__device__ void pair_warp(const PPair& p, const double* __restrict__ base, const double* __restrict__ x,
+                          double* __restrict__ yacc, double* ts1, double* ts2) {
+  const double* V = base + p.v_off;
+  const double* U = base + p.u_off;
+  double acc[NC];
+  for (int c0 = 0; c0 < p.r; c0 += NC) {   // phase 1: t1 = V^T x_Y
+    const int nc = min(NC, p.r - c0);
+    zero_acc(acc);
+    pair_tiles<NC, true, false>(V, p.nv, p.nv, c0, nc, 0, 1, x + p.yv, nullptr, nullptr, acc);
+    warp_colsum_store(acc, c0, nc, ts1);
+  }
+  for (int c0 = 0; c0 < p.r; c0 += NC) {   // phase 2: t2 = U^T x_X, y_X += U t1
+    const int nc = min(NC, p.r - c0);
+    zero_acc(acc);
+    pair_tiles<NC, true, true>(U, p.nu, p.nu, c0, nc, 0, 1, x + p.yu, ts1, yacc + p.yu, acc);
+    warp_colsum_store(acc, c0, nc, ts2);
+  }
+  for (int c0 = 0; c0 < p.r; c0 += NC) {   // phase 3: y_Y += V t2
+    const int nc = min(NC, p.r - c0);
+    pair_tiles<NC, false, true>(V, p.nv, p.nv, c0, nc, 0, 1, nullptr, ts2, yacc + p.yv, acc);
+  }
+}
+
+// ---------------------------------------------------------------- the CTA, one pair / chunk
+// CTA column sums: warp partials -> red[w][q] -> sum over the warps -> out[q] (shared or
+// global), then a barrier.
+template <int NC>
+__device__ __forceinline__ void cta_colsum(double (&acc)[NC], int c0, int nc, double* red, double* out) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    const double s = warp_sum(acc[q]);
+    if (lane == 0) red[w * kPMaxR + c0 + q] = s;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < kPWarps; ++ww) s += red[ww * kPMaxR + c0 + q];
+    out[c0 + q] = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void wait_flag(const int32_t* f, int epoch) {
+  if (threadIdx.x == 0)
+    while (ld_acquire(f) < epoch) __nanosleep(100);
+  __syncthreads();
+  __threadfence();   // (invalidates this SM's L1 before the t loads)
+}
+
+template <int NC>
+__device__ void pair_cta(const PWork& w, const PPair& p, const double* __restrict__ base,
+                         const double* __restrict__ x, double* __restrict__ yacc, double* __restrict__ tP1,
+                         double* __restrict__ tP2, double* __restrict__ tpart, int32_t* __restrict__ pcount,
+                         int32_t* __restrict__ flags, int epoch, double* st1, double* st2, double* red,
+                         int* sflag) {
+  const int wid = threadIdx.x >> 5;
+  const double* V = base + p.v_off;
+  const double* U = base + p.u_off;
+  double acc[NC];
+  if (w.kind == kPWhole) {
+    for (int c0 = 0; c0 < p.r; c0 += NC) {
+      const int nc = min(NC, p.r - c0);
+      zero_acc(acc);
+      pair_tiles<NC, true, false>(V, p.nv, p.nv, c0, nc, wid, kPWarps, x + p.yv, nullptr, nullptr, acc);
+      cta_colsum(acc, c0, nc, red, st1);
+    }
+    for (int c0 = 0; c0 < p.r; c0 += NC) {
+      const int nc = min(NC, p.r - c0);
+      zero_acc(acc);
+      pair_tiles<NC, true, true>(U, p.nu, p.nu, c0, nc, wid, kPWarps, x + p.yu, st1, yacc + p.yu, acc);
+      cta_colsum(acc, c0, nc, red, st2);
+    }
+    for (int c0 = 0; c0 < p.r; c0 += NC) {
+      const int nc = min(NC, p.r - c0);
+      pair_tiles<NC, false, true>(V, p.nv, p.nv, c0, nc, wid, kPWarps, nullptr, st2, yacc + p.yv, acc);
+    }
+    return;
+  }
+  // a row chunk [r0, r1) of one phase of a big pair
+  const int ph = w.kind - kPPhase1 + 1;
+  const double* F = ph == 2 ? U : V;
+  const int64_t ld = ph == 2 ? p.nu : p.nv;
+  const int y0 = ph == 2 ? p.yu : p.yv;
+  const int rows = w.r1 - w.r0;
+  const double* Fc = F + w.r0;            // column q of the chunk: Fc + q ld
+  if (ph >= 2) {                          // the other factor's reduction must be published
+    wait_flag(flags + 2 * w.big + (ph - 2), epoch);
+    const double* tg = (ph == 2 ? tP1 : tP2) + w.toff;
+    for (int q = threadIdx.x; q < p.r; q += blockDim.x) st1[q] = tg[q];
+    __syncthreads();
+  }
+  for (int c0 = 0; c0 < p.r; c0 += NC) {
+    const int nc = min(NC, p.r - c0);
+    zero_acc(acc);
+    if (ph == 1)
+      pair_tiles<NC, true, false>(Fc, ld, rows, c0, nc, wid, kPWarps, x + y0 + w.r0, nullptr, nullptr, acc);
+    else if (ph == 2)
+      pair_tiles<NC, true, true>(Fc, ld, rows, c0, nc, wid, kPWarps, x + y0 + w.r0, st1, yacc + y0 + w.r0, acc);
+    else
+      pair_tiles<NC, false, true>(Fc, ld, rows, c0, nc, wid, kPWarps, nullptr, st1, yacc + y0 + w.r0, acc);
+    if (ph < 3) cta_colsum(acc, c0, nc, red, tpart + w.poff + (int64_t)w.chunk * p.r);
+  }
+  if (ph == 3) return;
+  // the last chunk of the phase sums the partials in chunk order and publishes t1 / t2
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int last = atomicAdd(pcount + 2 * w.big + (ph - 1), 1) == w.nchunks - 1;
+    if (last) __threadfence();
+    *sflag = last;
+  }
+  __syncthreads();
+  if (*sflag) {
+    double* tout = (ph == 1 ? tP1 : tP2) + w.toff;
+    for (int q = threadIdx.x; q < p.r; q += blockDim.x) {
+      const double* __restrict__ pq = tpart + w.poff + q;
+      double a0 = 0.0, a1 = 0.0;
+      int c = 0;
+      for (; c + 1 < w.nchunks; c += 2) {
+        a0 += __ldcg(pq + (int64_t)c * p.r);
+        a1 += __ldcg(pq + (int64_t)(c + 1) * p.r);
+      }
+      if (c < w.nchunks) a0 += __ldcg(pq + (int64_t)c * p.r);
+      tout[q] = a0 + a1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      pcount[2 * w.big + (ph - 1)] = 0;
+      __threadfence();
+      st_release(flags + 2 * w.big + (ph - 1), epoch);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32 * kPWarps, 3)
 pair_apply_kernel(const PWork* __restrict__ work, int n_work, const PPair* __restrict__ pairs, int32_t* counter,
                   PairPtrs pp, const double* __restrict__ x, double* __restrict__ yacc, double* __restrict__ tP1,
                   double* __restrict__ tP2, double* __restrict__ tpart, int32_t* __restrict__ pcount,
                   int32_t* __restrict__ flags, int epoch) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  PairWarpSmem& S = reinterpret_cast<PairWarpSmem*>(smem_raw)[wid];
-  if (lane == 0) {
-    for (int k = 0; k < kPSlots; ++k) mbar_init(&S.full[k], 1 + 32);
-    mbar_fence_init();
-  }
-  __syncwarp();
-  const uint64_t pol_first = l2_evict_first_policy();
-  PIssue is;
-  uint32_t phase_bits = 0;   // parity of each slot's next completion
-  int issue_k = 0, cons_k = 0, inflight = 0;
-  // issue one sub-tile into slot issue_k (returns false at the end of the queue)
-  auto issue = [&]() -> bool {
-    PSub s;
-    pair_issue_next(is, work, n_work, pairs, counter, s);
-    if (s.item < 0) return false;
-    const int k = issue_k;
-    __syncwarp();
-    if (lane == 0) S.sub[k] = s;
-    const PPair& p = is.p;   // (the pair of s: replaced only when the next item is reserved)
-    const double* base = pp.P[p.level] + (s.ph == 2 ? p.u_off : p.v_off);
-    // tile t starts after t full tiles (32 x r each); column block c0 inside it
-    const double* src = base + (int64_t)32 * s.t * p.r + (int64_t)s.c0 * s.prow;
-    if (lane == 0) {
-      const uint32_t bytes = (uint32_t)s.prow * (uint32_t)s.nc * 8u;
-      mbar_arrive_expect_tx(&S.full[k], bytes);
-      if (s.ph == 1) bulk_g2s_keep(S.data[k], src, bytes, &S.full[k]);
-      else bulk_g2s(S.data[k], src, bytes, &S.full[k], pol_first);
-    }
-    if (s.ph != 3 && lane < s.rows) cp_async8(&S.xs[k][lane], x + s.y0 + lane);
-    cp_async_arrive_noinc(&S.full[k]);
-    issue_k = issue_k + 1 == kPSlots ? 0 : issue_k + 1;
-    ++inflight;
-    return true;
-  };
-  bool more = true;
-  while (more && inflight < kPSlots - 1) more = issue();
-  double acc[kPCB];
-  while (inflight > 0) {
-    const int k = cons_k;
-    mbar_wait(&S.full[k], (phase_bits >> k) & 1u);
-    phase_bits ^= 1u << k;
-    const PSub s = S.sub[k];
-    const PWork w = work[s.item];
-    const PPair p = pairs[w.pair];
-    const bool whole = w.kind == kPWhole;
-    double* tv = S.t[0];      // t of the phase's row dots (whole: t1 in t[0], t2 in t[1])
-    if (whole && s.ph == 3) tv = S.t[1];
-    if (!whole && s.ph >= 2 && (s.flags & kSubFirstItem)) {
-      // a phase 2 / 3 chunk: wait for the other factor's published reduction
-      const int32_t* f = flags + 2 * w.big + (s.ph - 2);
-      if (lane == 0)
-        while (ld_acquire(f) < epoch) __nanosleep(100);
-      __syncwarp();
-      __threadfence();
-      const double* tg = (s.ph == 2 ? tP1 : tP2) + w.toff;
-      for (int q = lane; q < p.r; q += 32) S.t[0][q] = __ldcg(tg + q);
-      __syncwarp();
-    }
-    if (s.flags & kSubFirstBlk) {
-#pragma unroll
-      for (int q = 0; q < kPCB; ++q) acc[q] = 0.0;
-    }
-    const double* d = S.data[k];
-    const bool ok = lane < s.rows;
-    const double xv = (s.ph != 3 && ok) ? S.xs[k][lane] : 0.0;
-    double dot0 = 0.0, dot1 = 0.0;
-#pragma unroll
-    for (int q = 0; q < kPCB; ++q) {
-      if (q < s.nc) {
-        const double v = ok ? d[q * s.prow + lane] : 0.0;
-        if (s.ph != 3) acc[q] = fma(v, xv, acc[q]);
-        if (s.ph != 1) {
-          if (q & 1) dot1 = fma(v, tv[s.c0 + q], dot1);
-          else dot0 = fma(v, tv[s.c0 + q], dot0);
-        }
+  __shared__ double st[kPWarps][2][kPMaxR];     // per-warp t1 / t2 (groups); st[0] for CTA items
+  __shared__ double red[kPWarps * kPMaxR];
+  __shared__ int sidx, sflag;
+  const int wid = threadIdx.x >> 5;
+  for (;;) {
+    if (threadIdx.x == 0) sidx = atomicAdd(counter, 1);
+    __syncthreads();
+    const int idx = sidx;
+    __syncthreads();
+    if (idx >= n_work) break;
+    const PWork w = work[idx];
+    if (w.kind == kPGroup) {
+      if (wid < w.count) {
+        const PPair p = pairs[w.first + wid];
+        const double* base = pp.P[p.level];
+        if (p.r <= 8) pair_warp<8>(p, base, x, yacc, st[wid][0], st[wid][1]);
+        else pair_warp<16>(p, base, x, yacc, st[wid][0], st[wid][1]);
       }
+      continue;   // (the next item's barrier waits for every warp)
     }
-    __syncwarp();   // the slot's data and header are read: it may be refilled
-    cons_k = cons_k + 1 == kPSlots ? 0 : cons_k + 1;
-    --inflight;
-    if (more) more = issue();
-    if (s.ph != 1 && ok) atomicAdd(yacc + s.y0 + lane, dot0 + dot1);
-    if (s.ph != 3 && (s.flags & kSubLastBlk)) {
-      // end of a column block: column sums of this warp
-      double* out = whole ? S.t[s.ph - 1] : tpart + w.poff + (int64_t)w.chunk * p.r;
-#pragma unroll
-      for (int q = 0; q < kPCB; ++q) {
-        const double v = warp_sum(acc[q]);
-        if (lane == 0 && q < s.nc) out[s.c0 + q] = v;
-      }
-      __syncwarp();
-      if (!whole && (s.flags & kSubLastPh)) {
-        // the last chunk of the phase reduces the partials in chunk order and publishes t
-        int last = 0;
-        if (lane == 0) {
-          __threadfence();
-          last = atomicAdd(pcount + 2 * w.big + (s.ph - 1), 1) == w.nchunks - 1;
-          if (last) __threadfence();
-        }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {
-          double* tout = (s.ph == 1 ? tP1 : tP2) + w.toff;
-          for (int q = lane; q < p.r; q += 32) {
-            const double* __restrict__ pq = tpart + w.poff + q;
-            double a0 = 0.0, a1 = 0.0;
-            int c = 0;
-            for (; c + 1 < w.nchunks; c += 2) {
-              a0 += __ldcg(pq + (int64_t)c * p.r);
-              a1 += __ldcg(pq + (int64_t)(c + 1) * p.r);
-            }
-            if (c < w.nchunks) a0 += __ldcg(pq + (int64_t)c * p.r);
-            tout[q] = a0 + a1;
-          }
-          __syncwarp();
-          if (lane == 0) {
-            pcount[2 * w.big + (s.ph - 1)] = 0;
-            __threadfence();
-            st_release(flags + 2 * w.big + (s.ph - 1), epoch);
-          }
-        }
-      }
-    }
+    const PPair p = pairs[w.first];
+    const double* base = pp.P[p.level];
+    if (p.r <= 8)
+      pair_cta<8>(w, p, base, x, yacc, tP1, tP2, tpart, pcount, flags, epoch, st[0][0], st[0][1], red, &sflag);
+    else
+      pair_cta<16>(w, p, base, x, yacc, tP1, tP2, tpart, pcount, flags, epoch, st[0][0], st[0][1], red, &sflag);
   }
 }
 

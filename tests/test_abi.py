@@ -94,6 +94,27 @@ def test_argument_validation_codes(h2d):
     assert h.value is None
     assert L.hodlr2d_destroy(None) == 0
     assert L.hodlr2d_num_blocks(None, 1) == -1
+    assert L.hodlr2d_copy_leaves(None, None, None) == -1
+    # the adaptive tree is single-rank only; depth below -3 is invalid
+    o = h2d.default_options()
+    o.depth, o.world, o.rank = -3, 2, 0
+    assert L.hodlr2d_build_ex(pts.ctypes.data, 4, 0, 64, 1e-8, C.byref(o), C.byref(h)) == h2d.H2D_EINVAL
+    o = h2d.default_options()
+    o.depth = -4
+    assert L.hodlr2d_build_ex(pts.ctypes.data, 4, 0, 64, 1e-8, C.byref(o), C.byref(h)) == h2d.H2D_EINVAL
+    # hodlr2d_partition (host only): bad arguments are reported, not thrown across the ABI
+    ls = np.zeros(17, np.int32)
+    lb, le = C.c_int64(), C.c_int64()
+    assert L.hodlr2d_partition(ls.ctypes.data, 2, 0, 0, C.byref(lb), C.byref(le)) == h2d.H2D_EINVAL
+    assert L.hodlr2d_partition(ls.ctypes.data, 16, 1, 0, C.byref(lb), C.byref(le)) == h2d.H2D_EINVAL
+    assert L.hodlr2d_partition(None, 2, 1, 0, C.byref(lb), C.byref(le)) == h2d.H2D_EINVAL
+    ls = np.arange(17, dtype=np.int32) * 3
+    assert L.hodlr2d_partition(ls.ctypes.data, 2, 2, 1, C.byref(lb), C.byref(le)) == 0 and le.value == 16
+    # the NCCL unique id: H2D_OK where NCCL loads, else H2D_ENCCL (never a crash)
+    idb = (C.c_ubyte * h2d.COMM_ID_BYTES)()
+    assert L.hodlr2d_comm_unique_id(C.cast(idb, C.c_void_p)) in (0, h2d.H2D_ENCCL)
+    assert L.hodlr2d_comm_unique_id(None) == h2d.H2D_EINVAL
+    assert L.hodlr2d_set_diag(None, b"p2p_serial", 1) == h2d.H2D_EINVAL
 
 
 def test_product_package_does_not_touch_the_oracle():
