@@ -715,12 +715,13 @@ def launches_per_matvec(inf, world):
     return 2 + inf.get("apply_launches", 2) + inf.get("p2p_launches", 1)
 
 
-# FP64-pipe instructions per kernel evaluation in p2p_warp_kernel's self-block loop,
-# counted from `cuobjdump -sass` of libhodlr2d.so; keyed by kernel id.
-# log (p2p_warp_kernel<0, 2>): 44 DFMA + 8 DADD + 4 DMUL + 4 DSETP + 4 I2F.F64 per 4
-# evaluations = 16; IMQ / 1/r: distance + rsqrt (MUFU.RSQ64H seed + Newton) + the
-# accumulation, ~12 (estimate).
-P2P_FP64_OPS_PER_EVAL = {0: 16, 1: 12, 2: 12}
+# FP64-pipe instructions per kernel evaluation in p2p_warp_kernel's self-block loop
+# (DESIGN.md §6); keyed by kernel id.  log (p2p_warp_kernel<kLogNoSel, 2>, round 2): distance
+# 2 DADD + DMUL + DFMA, table log 7 DFMA + 1 DADD (exponent), accumulation 1 DFMA = 13 (the
+# round-1 form counted from `cuobjdump -sass`: 44 DFMA + 8 DADD + 4 DMUL + 4 DSETP + 4
+# I2F.F64 per 4 evaluations = 16); IMQ / 1/r: distance + rsqrt (MUFU.RSQ64H seed + Newton) +
+# the accumulation, ~12 (estimate).
+P2P_FP64_OPS_PER_EVAL = {0: 13, 1: 12, 2: 12}
 
 
 def p2p_standalone_ms(op, step, args, n=10):
@@ -847,6 +848,13 @@ def run_gmres(args):
     e1.record()
     torch.cuda.synchronize()
     mv_ms = e0.elapsed_time(e1) / 20
+    op.set_timing(True)
+    op.stage_times(reset=True)
+    for _ in range(5):
+        op.matvec_raw(lam.data_ptr(), y.data_ptr(), h2d.ORDER_ORIGINAL)
+    st, cnt = op.stage_times(reset=True)
+    op.set_timing(False)
+    stage_ms = {k: round(v / max(cnt, 1), 4) for k, v in st.items()}
     err = float(torch.linalg.norm(lam_hat - lam) / torch.linalg.norm(lam))
     line = {"mode": "gmres", "workload": f"{args.rbf_kernel}, {args.grid_m}^2 Chebyshev grid, a = 0.001, "
                                          f"beta = N, ACA 1e-12, N_max {args.nmax} "
@@ -856,7 +864,8 @@ def run_gmres(args):
             "factor_gb": (inf["u_values"] + inf["v_values"]) * 8e-9,
             "n": n, "kappa": inf["kappa"], "rank_max": inf["rank_max"],
             "compression_ratio": inf["compression_ratio"], "T_I_s": round(t_i, 3), "T_G_s": round(t_g, 4),
-            "T_G_runs_s": [round(v, 4) for v in tgs], "matvec_ms": round(mv_ms, 3),
+            "T_G_runs_s": [round(v, 4) for v in tgs], "matvec_ms": round(mv_ms, 3), "stage_ms_per_matvec": stage_ms,
+            "matvec_gbytes": inf["matvec_bytes"] / 1e9,
             "p2p_leaves_warp_fast_generic": inf["p2p_leaves"], "small_items_A_B": inf["small_items"],
             "iterations": its, "rel_residual": rr, "solution_rel_error": err,
             "paper_context": PAPER_RBF_250000.get(args.rbf_kernel) if n == 250000 else None,

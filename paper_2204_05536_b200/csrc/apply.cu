@@ -99,7 +99,7 @@ constexpr int kSymRowsOnly = 0, kSymBoth = 1, kSymSelf = 2;
 template <int KID>
 __device__ __forceinline__ double p2p_eval(const KernelParams& kp, const double2* tab, double px,
                                            double py, double qx, double qy) {
-  if (KID == H2D_KERNEL_LOG || KID == kLogSafe) {
+  if (KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel) {
     const double dx = px - qx, dy = py - qy;
     const double r2 = fma(dx, dx, dy * dy);
     return r2 > 0.0 ? hlog_r2<KID == kLogSafe>(r2, tab) : 0.0;
@@ -267,7 +267,7 @@ p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end, const int32_t* _
                double* __restrict__ s0, double* __restrict__ sL, double* __restrict__ sD) {
   __shared__ double s_a[3 * kSymTile], s_b[3 * kSymTile], s_c[3 * kSymTile], srow[kSymTile];
   __shared__ double scol[16][kSymTile + 1];
-  __shared__ double2 s_logtab[128];
+  __shared__ double2 s_logtab[kHlogBins];
   const int64_t X = leaves[blockIdx.x];
   const int tid = threadIdx.x;
   if (kNeedsLogTable<KID>) hlog_table(s_logtab);
@@ -478,7 +478,7 @@ p2p_fast_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int
   __shared__ double tiles[2][3][3 * kSymTile];   // [buffer][X, +x, +y][px | py | x]
   __shared__ double acc[kSymTile], srow[kSymTile];
   __shared__ double scol8[8][kSymTile + 1];
-  __shared__ double2 tab[128];
+  __shared__ double2 tab[kHlogBins];
   __shared__ int s_next;
   const int tid = threadIdx.x;
   const double k0 = KID == H2D_KERNEL_IMQ ? 1.0 : 0.0;
@@ -561,7 +561,7 @@ p2p_list_kernel(const int64_t* __restrict__ items, int n_items, int32_t* counter
                 double* __restrict__ s0) {
   __shared__ double2 sq[8][32];
   __shared__ double sxv[8][32];
-  __shared__ double2 tab[128];
+  __shared__ double2 tab[kHlogBins];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (kNeedsLogTable<KID>) hlog_table(tab);
   __syncthreads();
@@ -644,7 +644,7 @@ __global__ void subnormal_check_kernel(int kappa, int64_t nleaf, const int32_t* 
     __syncthreads();
     const int64_t s0 = nf_off ? lstart[L] : lstart[L];
     const int64_t m = lstart[L + 1] - s0;
-    bool bad = false;
+    bool bad = false, same = false;
     for (int64_t i = s0 + threadIdx.x; i < s0 + m; i += blockDim.x) {
       const double xi = px[i], yi = py[i];
       for (int k = 0; k < nr; ++k)
@@ -652,9 +652,11 @@ __global__ void subnormal_check_kernel(int kappa, int64_t nleaf, const int32_t* 
           const double dx = xi - px[j], dy = yi - py[j];
           const double r2 = fma(dx, dx, dy * dy);
           bad |= r2 > 0.0 && r2 < 0x1p-1022;
+          same |= r2 == 0.0 && j != i;
         }
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+    if (__syncthreads_or(same) && threadIdx.x == 0) atomicOr(flag, 2);
   }
 }
 
@@ -708,7 +710,7 @@ p2p_warp_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int
                 double* __restrict__ s0, double* __restrict__ sL, double* __restrict__ sD) {
   __shared__ double2 sself[8][32 * RPL], snb[8][32];
   __shared__ double xself[8][32 * RPL], xnb[8][32];
-  __shared__ double2 tab[128];
+  __shared__ double2 tab[kHlogBins];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (kNeedsLogTable<KID>) hlog_table(tab);
   __syncthreads();
@@ -740,6 +742,11 @@ p2p_warp_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int
         const double dx = pi[r] - q.x, dy = qi[r] - q.y;
         acc[r] = fma(kfast<KID>(fma(dx, dx, dy * dy), tab, kp), xj, acc[r]);
       }
+    }
+    if (KID == kLogNoSel) {   // the diagonal (r2 = 0) was evaluated as hlog_r2(0): take it out
+      const double g = hlog_r2<false>(0.0, tab);
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) acc[r] = fma(-g, xi[r], acc[r]);
     }
     if (M.has_r)
       warp_nbr<KID, RPL>(lane, pi, qi, xi, M.rn, M.rs, px, py, x, snb[w], xnb[w], tab, kp, acc, sL + M.rs);
@@ -1621,7 +1628,8 @@ void finalize_schedule(Handle& h) {
     H2D_CUDA(cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
     H2D_CUDA(cudaStreamSynchronize(s));
     H2D_CUDA(cudaFreeAsync(d_flag, s));
-    if (flag) h.p2p_kid = kLogSafe;
+    if (flag & 1) h.p2p_kid = kLogSafe;
+    else if (!(flag & 2) && !getenv("H2D_P2P_SELECT")) h.p2p_kid = kLogNoSel;   // (diagnostics: keep the select)
   }
   h.tpart_len = tpart_len;
   h.d_tpart = h.alloc<double>(tpart_len);
@@ -1876,6 +1884,7 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
         auto pick = [&](auto rpl) -> decltype(&p2p_warp_kernel<H2D_KERNEL_LOG, 1>) {
           constexpr int R = decltype(rpl)::value;
           return h.p2p_kid == kLogSafe ? p2p_warp_kernel<kLogSafe, R>
+               : h.p2p_kid == kLogNoSel ? p2p_warp_kernel<kLogNoSel, R>
                : h.kp.id == H2D_KERNEL_LOG ? p2p_warp_kernel<H2D_KERNEL_LOG, R>
                : h.kp.id == H2D_KERNEL_IMQ ? p2p_warp_kernel<H2D_KERNEL_IMQ, R>
                : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_warp_kernel<H2D_KERNEL_ONE_OVER_R, R>
@@ -1884,7 +1893,9 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
         };
         auto* kfn = r == 0 ? pick(std::integral_constant<int, 1>{})
                   : r == 1 ? pick(std::integral_constant<int, 2>{}) : pick(std::integral_constant<int, 3>{});
-        const int grid = (int)std::min<int64_t>(h.num_sms, (cnt + 7) / 8);
+        // beside the streams one CTA per SM fits (registers); run alone (p2p_serial) the near
+        // field has the GPU and 4 CTAs per SM hide its dependent DFMA chains
+        const int grid = (int)std::min<int64_t>((p2p_serial ? 4 : 1) * (int64_t)h.num_sms, (cnt + 7) / 8);
         cudaStream_t sw = r > 0 && grid < h.num_sms ? side(3 - r) : a;
         H2D_CUDA(cudaMemsetAsync(h.d_counters + 4 + r, 0, sizeof(int32_t), sw));
         kfn<<<grid, 256, 0, sw>>>(h.kappa, h.d_p2p_warp + off, (int)cnt, h.d_counters + 4 + r, h.d_leaf_start,

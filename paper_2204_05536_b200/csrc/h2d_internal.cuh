@@ -43,6 +43,10 @@ struct KernelParams {
 // Internal kernel id of the near-field kernels: the log kernel with subnormal-safe table
 // logarithms (handles whose near field has a pair of distinct points with subnormal r^2).
 constexpr int kLogSafe = 5;
+// ... and the log kernel without the K(r = 0) select in the warp-per-leaf near field (handles
+// whose near field has no two distinct points at distance 0 and no subnormal r^2): the self
+// block's diagonal term is taken out once per row instead of a select per evaluation.
+constexpr int kLogNoSel = 6;
 
 // K(p, q) specialised at compile time (hot P2P loop: no per-pair dispatch).
 template <int KID>
@@ -50,7 +54,7 @@ __device__ __forceinline__ double kernel_eval_t(const KernelParams& k, double px
                                                 double qx, double qy) {
   const double dx = px - qx, dy = py - qy;
   const double r2 = fma(dx, dx, dy * dy);
-  if (KID == H2D_KERNEL_LOG || KID == kLogSafe) {
+  if (KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel) {
     return r2 > 0.0 ? 0.5 * log(r2) : 0.0;
   } else if (KID == H2D_KERNEL_IMQ) {
     return rsqrt(fma(r2, k.inv_c2, 1.0));

@@ -1115,7 +1115,7 @@ p2p_multi_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf
                  const double* __restrict__ xm, int64_t n, KernelParams kp, double* __restrict__ ynearm) {
   __shared__ double tpx[kMTile], tpy[kMTile], tx[NR][kMTile];
   __shared__ double red[256];
-  __shared__ double2 tab[128];
+  __shared__ double2 tab[kHlogBins];
   const int tid = threadIdx.x;
   if (kNeedsLogTable<KID>) hlog_table(tab);
   const int64_t X = leaf_begin + blockIdx.x;

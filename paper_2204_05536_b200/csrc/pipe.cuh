@@ -76,11 +76,13 @@ __device__ __forceinline__ double warp_transpose_sum8(const double (&c)[8], int 
 
 constexpr int kSymTile = 96, kSymMaxB = kSymTile / 16;
 
-// 0.5 log(r2) for r2 > 0: r2 = 2^e m, m in [1, 2); c_k = 1 + (k + 1/2)/128 is the
-// centre of m's 1/128 bin (k = top 7 mantissa bits), tab[k] = (1/c_k, 0.5 log c_k);
-// 0.5 log r2 = e ln2/2 + 0.5 log c_k + 0.5 log1p(f), f = m/c_k - 1, |f| <= 2^-8, with
-// 0.5 log1p(f) = f p(f), p the degree-5 Taylor polynomial (truncation f^7/7 <= 2e-18).
-// 9 DFMA; the coefficients are constant-bank operands (no register materialisation).
+// 0.5 log(r2) for r2 > 0: r2 = 2^e m, m in [1, 2); c_k = 1 + (k + 1/2)/512 is the
+// centre of m's 1/512 bin (k = top 9 mantissa bits), tab[k] = (1/c_k, 0.5 log c_k);
+// 0.5 log r2 = e ln2/2 + 0.5 log c_k + 0.5 log1p(f), f = m/c_k - 1, |f| <= 2^-10, with
+// 0.5 log1p(f) = f p(f), p the degree-3 Taylor polynomial (truncation f^5/10 <= 9e-17).
+// 7 DFMA in a chain of 6 (the 128-bin, degree-5 version: 9 / 8): the near field is bound by
+// these dependent chains.  The coefficients are constant-bank operands.
+constexpr int kHlogBins = 512;
 __constant__ double c_hlog[8] = {0.34657359027997264,   // ln2 / 2 (high part)
                                  1.1595234069231498e-17, // ln2 / 2 (low part)
                                  0.5, -0.25, 1.0 / 6.0, -0.125, 0.1, -1.0 / 12.0};
@@ -104,23 +106,25 @@ __device__ __forceinline__ double hlog_r2(double r2, const double2* __restrict__
   } else {
     e = (int)(bits >> 52) - 1023;
   }
-  const int k = (int)(bits >> 45) & 127;
+  const int k = (int)(bits >> 43) & (kHlogBins - 1);
   const double mnt = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
   const double2 tb = tab[k];
   const double f = fma(mnt, tb.x, -1.0);
-  double p = fma(f, c_hlog[7], c_hlog[6]);
-  p = fma(f, p, c_hlog[5]);
-  p = fma(f, p, c_hlog[4]);
+  double p = fma(f, c_hlog[5], c_hlog[4]);
   p = fma(f, p, c_hlog[3]);
   p = fma(f, p, c_hlog[2]);
-  const double ed = (double)e;
+  // the exponent as a double: SAFE by conversion; else by the 2^52 trick (one DADD instead of
+  // an I2F.F64: the biased exponent field E placed in a mantissa, 2^52 + E - (2^52 + 1023))
+  double ed;
+  if (SAFE) ed = (double)e;
+  else ed = __longlong_as_double(0x4330000000000000LL | (long long)(e + 1023)) - 4503599627371519.0;
   return fma(ed, c_hlog[0], fma(p, f, fma(ed, c_hlog[1], tb.y)));
 }
 
 __device__ __forceinline__ void hlog_table(double2* tab) {
-  if (threadIdx.x < 128) {
-    const double c = 1.0 + (threadIdx.x + 0.5) / 128.0;
-    tab[threadIdx.x] = make_double2(1.0 / c, 0.5 * log(c));
+  for (int k = threadIdx.x; k < kHlogBins; k += blockDim.x) {
+    const double c = 1.0 + (k + 0.5) / kHlogBins;
+    tab[k] = make_double2(1.0 / c, 0.5 * log(c));
   }
 }
 
@@ -128,7 +132,9 @@ __device__ __forceinline__ void hlog_table(double2* tab) {
 // the rare pairs closer than a); distance kernels only.
 template <int KID>
 __device__ __forceinline__ double kfast(double r2, const double2* __restrict__ tab, const KernelParams& kp) {
-  if (KID == H2D_KERNEL_LOG || KID == kLogSafe) {
+  if (KID == kLogNoSel) {   // no r2 = 0 select: the caller corrects the diagonal (warp kernel)
+    return hlog_r2<false>(r2, tab);
+  } else if (KID == H2D_KERNEL_LOG || KID == kLogSafe) {
     const double v = hlog_r2<KID == kLogSafe>(r2, tab);
     return r2 > 0.0 ? v : 0.0;
   } else if (KID == H2D_KERNEL_IMQ) {
@@ -150,10 +156,10 @@ __device__ __forceinline__ double kfast(double r2, const double2* __restrict__ t
 }
 
 template <int KID>
-constexpr bool kDistKernel = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == H2D_KERNEL_IMQ || KID == H2D_KERNEL_ONE_OVER_R ||
+constexpr bool kDistKernel = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == H2D_KERNEL_IMQ || KID == H2D_KERNEL_ONE_OVER_R ||
                              KID == H2D_KERNEL_RBF_PHI1 || KID == H2D_KERNEL_RBF_PHI2;
 template <int KID>
-constexpr bool kNeedsLogTable = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == H2D_KERNEL_RBF_PHI1;
+constexpr bool kNeedsLogTable = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == H2D_KERNEL_RBF_PHI1;
 
 __device__ __forceinline__ uint32_t p2p_spread(uint32_t v) {
   v &= 0xFFFFu;
