@@ -765,7 +765,7 @@ def run_rank_slice(args, cfg):
     lw = np.load(args.leaf_weights) if args.leaf_weights else None
     op = h2d.Hodlr2d.build(torch.from_numpy(pts).cuda(), cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c,
                            scale=cfg.scale, shift=cfg.shift, box_lo=cfg.box_lo, box_side=cfg.box_side,
-                           world=P, rank=g, stream=stream.cuda_stream, leaf_weights=lw)
+                           world=P, rank=g, stream=stream.cuda_stream, leaf_weights=lw, symmetric=args.symmetric)
     torch.cuda.synchronize()
     build_s = time.time() - t0
     inf = op.info()
@@ -793,6 +793,7 @@ def run_rank_slice(args, cfg):
     peak, peak_kind = peaks()
     gather_ms = 8.0 * cfg.n * (P - 1) / P / 770e9 * 1e3
     line = {"mode": "rank_slice", "config": config_dict(cfg, P), "slice_world": P, "rank": g,
+            "symmetric": bool(args.symmetric), "symmetric_apply": bool(inf["symmetric_apply"]),
             "partition": "measured leaf costs (--leaf-weights)" if lw is not None else "geometric weight",
             "rows": [inf["row_begin"], inf["row_end"]], "build_seconds": round(build_s, 2),
             "ms_per_matvec_compute": ms, "steps": args.steps, "warmup": args.warmup,

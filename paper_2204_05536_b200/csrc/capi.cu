@@ -637,7 +637,9 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
     const bool want = e ? atoi(e) != 0 : false;
     h.pair_wanted = want && opts->symmetric && h.row_begin == 0 && h.row_end == h.n && h.kappa >= 1;
   }
-  h.symapply = opts->symmetric && h.row_begin == 0 && h.row_end == h.n && h.kappa >= 1 &&
+  // (multi-rank handles too: A' / B' run over the whole boxes of every pair that touches the
+  // served rows, C' over the served leaves, the combine keeps the served rows)
+  h.symapply = opts->symmetric && h.kappa >= 1 &&
                !(getenv("H2D_SYMAPPLY") && atoi(getenv("H2D_SYMAPPLY")) == 0);
   h.tree_seconds = now_s() - t0;
   if (opts->skip_aca) skip_factors(h); else run_aca(h);

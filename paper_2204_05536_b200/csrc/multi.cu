@@ -1359,7 +1359,7 @@ static void build_multi_schedule(Handle& h) {
         upos += R;
       }
     }
-    h.m_sym_ok = ok;
+    h.m_sym_ok = ok && h.row_begin == 0 && h.row_end == h.n;   // (multi-rank: one vector at a time)
     if (ok) {
       std::stable_sort(bitems.begin(), bitems.end(), [](const AItem& a, const AItem& b) {
         return (int64_t)a.nrows * a.R > (int64_t)b.nrows * b.R;

@@ -80,18 +80,31 @@ def test_symmetric_blocks_mirrored_and_operator_symmetric(h2d):
     assert asym < 1e-14
 
 
-def test_symmetric_partition_union(h2d):
-    cfg = W.CONFIGS["c1"]
+@pytest.mark.parametrize("name,world", [("c1", 2), ("c1", 3), ("c2", 2), ("c2", 4)])
+def test_symmetric_partition_union(h2d, name, world):
+    """Multi-rank symmetric handles run the three-pass symmetric apply (A' / B' over the whole
+    boxes of every pair that touches the rank's rows, C' over its leaves) and store each pair
+    ~once instead of both directed blocks: the ranks reassemble the single-rank operator."""
+    cfg = W.CONFIGS[name]
     pts = W.config_points(cfg)
     full = build(h2d, cfg, pts)
     perm, _ = full.tree()
     x = W.config_x(cfg, 3)[perm]
     yfull = full.matvec(dev(x), order="tree").cpu().numpy()
-    parts = []
-    for rank in range(2):
-        p = build(h2d, cfg, pts, world=2, rank=rank)
+    parts, dev_bytes = [], 0
+    import os
+    os.environ["H2D_SYMAPPLY"] = "0"
+    try:
+        directed = [build(h2d, cfg, pts, world=world, rank=r).info()["device_bytes"] for r in range(world)]
+    finally:
+        os.environ.pop("H2D_SYMAPPLY")
+    for rank in range(world):
+        p = build(h2d, cfg, pts, world=world, rank=rank)
+        assert p.info()["symmetric_apply"] == 1
+        dev_bytes += p.info()["device_bytes"]
         parts.append(p.matvec(dev(x), order="tree").cpu().numpy())
     assert rel(np.concatenate(parts), yfull) <= 1e-13
+    assert dev_bytes < 0.97 * sum(directed)
 
 
 @pytest.mark.parametrize("name", ["c1", "c2"])
@@ -276,8 +289,8 @@ def test_symmetric_gmres(h2d):
 
 
 def test_symmetric_partitioned_multi_rhs(h2d):
-    """A symmetric build on a world-2 partition keeps the directed panels (no symmetric
-    apply across ranks); its multi-RHS path (16 + 4 + 1 vectors, TREE order) equals its
+    """A symmetric build on a world-2 partition runs the symmetric apply; its multi-RHS path
+    (one vector at a time on multi-rank symmetric handles, TREE order) equals its
     single-vector matvecs, and the two ranks reassemble the single-rank symmetric operator."""
     cfg = W.CONFIGS["c1"]
     pts = W.config_points(cfg)
@@ -288,7 +301,7 @@ def test_symmetric_partitioned_multi_rhs(h2d):
     parts = []
     for rank in range(2):
         p = build(h2d, cfg, pts, world=2, rank=rank)
-        assert p.info()["symmetric_apply"] == 0
+        assert p.info()["symmetric_apply"] == 1
         Y = p.matvec_multi(dev(X), order="tree").cpu().numpy()
         for k in (0, 15, 16, 20):
             assert rel(Y[k], p.matvec(dev(X[k]), order="tree").cpu().numpy()) <= 1e-13, k
@@ -298,15 +311,18 @@ def test_symmetric_partitioned_multi_rhs(h2d):
 
 # ------------------------------------------------------------------ pair-local apply
 
-@pytest.mark.parametrize("name", ["c1", "c2"])
-def test_pair_apply_matches_three_pass_and_oracle(h2d, name, tmp_path, monkeypatch):
-    """The pair-local apply (default for symmetric single-rank handles: each factor read once,
-    big pairs in row chunks shared by CTAs with flag-published t1 / t2) computes the same
-    operator as the three-pass apply and, with the oracle's symmetric factors, the oracle
-    matvec to <= 1e-12."""
+@pytest.mark.parametrize("name,lag", [("c1", None), ("c2", None), ("c2", "0")])
+def test_pair_apply_matches_three_pass_and_oracle(h2d, name, lag, tmp_path, monkeypatch):
+    """The pair-local apply (opt-in on symmetric single-rank handles: each factor read once;
+    pairs that fit a ring slot in one warp, larger pairs in row chunks per phase with
+    flag-published t1 / t2) computes the same operator as the three-pass apply and, with the
+    oracle's symmetric factors, the oracle matvec to <= 1e-12.  lag 0 puts every phase-2 / 3
+    chunk right behind its inputs in the queue (the flag waits actually happen)."""
     cfg = W.CONFIGS[name]
     pts = W.config_points(cfg)
     monkeypatch.setenv("H2D_PAIRAPPLY", "1")
+    if lag is not None:
+        monkeypatch.setenv("H2D_PAIR_LAG", lag)
     op = build(h2d, cfg, pts)
     assert op.info()["pair_apply"] == 1
     for k in range(3):
