@@ -972,16 +972,11 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
       for (auto& Lv : h.levels) { h.release(Lv.Pr); Lv.Pr = nullptr; Lv.pairs.clear(); }
   }
   if (h.pair_wanted && !h.pair_failed) {
-    // pair apply (pairs.cuh): per pair {X, Y}, X < Y, V (n_Y x r) then U (m_X x r), column-
-    // major with the row count rounded up to even (16-byte bulk copies).  A pair whose V and
-    // U (and the x of their rows) fit one ring slot is stored whole; a larger one as row
-    // chunks of ch rows per factor, each chunk column-major on its own rows
+    // pair apply (pairs.cuh): per pair {X, Y}, X < Y, V_XY (n_Y x r) then U_XY (m_X x r),
+    // column-major as the ACA stores them; pairs in CSR order of their first side X
     h.release(L.Pr);
     L.Pr = nullptr;
     L.pairs.clear();
-    auto ev = [](int64_t v) { return (v + 1) & ~(int64_t)1; };
-    struct PCopy { const double* src; int64_t dst; int32_t lds, ldd, rows, cols; };
-    std::vector<PCopy> pc;
     int64_t po = 0, pvals = 0;
     for (int64_t X = 0; X < nbox; ++X) {
       const int64_t m = h.box_end(l, X) - h.box_begin(l, X);
@@ -990,33 +985,24 @@ void pack_level(Handle& h, Level& L, const std::vector<const double*>& srcU,
         const int r = rank_all(e);
         const int64_t n = h.box_end(l, Y) - h.box_begin(l, Y);
         if (Y < X || r == 0 || m == 0 || n == 0) continue;
-        Level::PairDesc d{po, (int32_t)h.box_begin(l, Y), (int32_t)h.box_begin(l, X), (int32_t)n, (int32_t)m, r, 0};
-        if ((ev(n) + ev(m)) * r + (n + 2) + (m + 2) <= kPSlotDbl) {   // (+ the x segments)
-          pc.push_back(PCopy{srcV[(size_t)e], po, (int32_t)n, (int32_t)ev(n), (int32_t)n, r});
-          pc.push_back(PCopy{srcU[(size_t)e], po + ev(n) * r, (int32_t)m, (int32_t)ev(m), (int32_t)m, r});
-          po += (ev(n) + ev(m)) * r;
-        } else {
-          d.ch = ((kPSlotDbl - 2) / (r + 1)) & ~1;   // ch x r factor values + ch + 2 of x
-          if (d.ch >= 64) d.ch &= ~31;
-          for (int f = 0; f < 2; ++f) {
-            const double* src = f == 0 ? srcV[(size_t)e] : srcU[(size_t)e];
-            const int64_t rows = f == 0 ? n : m;
-            for (int64_t c0 = 0; c0 < rows; c0 += d.ch) {
-              const int64_t rc = std::min<int64_t>(d.ch, rows - c0);
-              pc.push_back(PCopy{src + c0, po, (int32_t)rows, (int32_t)ev(rc), (int32_t)rc, r});
-              po += ev(rc) * r;
-            }
-          }
-        }
-        pvals += (n + m) * r;
+        Level::PairDesc d{po, po + n * r, (int32_t)h.box_begin(l, Y), (int32_t)h.box_begin(l, X), (int32_t)n,
+                          (int32_t)m, r, r};
         L.pairs.push_back(d);
+        po += (n + m) * r;
+        pvals += (n + m) * r;
+        uitems.push_back(UCopyItem{srcV[(size_t)e], nullptr, (int32_t)n, (int32_t)n, (int32_t)n, r});
+        uitems.push_back(UCopyItem{srcU[(size_t)e], nullptr, (int32_t)m, (int32_t)m, (int32_t)m, r});
       }
     }
     L.pr_alloc = po;
     L.pr_values = pvals;
     L.Pr = h.alloc<double>(po);
-    H2D_CUDA(cudaMemsetAsync(L.Pr, 0, std::max<int64_t>(1, po) * sizeof(double), s));
-    for (const PCopy& c : pc) uitems.push_back(UCopyItem{c.src, L.Pr + c.dst, c.lds, c.ldd, c.rows, c.cols});
+    // destinations now that the array exists (the last 2 x pairs items are the pair copies)
+    size_t k0 = uitems.size() - 2 * L.pairs.size();
+    for (const auto& d : L.pairs) {
+      uitems[k0++].dst = L.Pr + d.v_off;
+      uitems[k0++].dst = L.Pr + d.u_off;
+    }
   }
   const size_t CH = 1 << 20;
   for (size_t c0 = 0; c0 < uitems.size(); c0 += CH) {
@@ -1527,116 +1513,124 @@ void finalize_schedule(Handle& h) {
   }
   h.pairapply = h.pair_wanted && !h.pair_failed;
   if (h.pairapply) {
-    // pair apply queue (pairs.cuh): the chunked pairs' phase chunks, merged by byte position
-    // with a lag per phase and every chunk after all chunks of its pair's previous phase,
-    // then the whole pairs; each class largest first
-    auto ev = [](int64_t v) { return (v + 1) & ~(int64_t)1; };
-    std::vector<std::pair<int64_t, PUnit>> whole;
-    struct BigPair { int64_t bytes; int level; Level::PairDesc d; };
-    std::vector<BigPair> big;
+    // pair apply schedule (pairs.cuh): the big pairs of the coarse levels as row chunks per
+    // phase (merged by byte position with a lag, every chunk after all chunks of the pair's
+    // previous phase), then the medium pairs (one CTA each), then groups of 8 small pairs
+    // (one warp each), each class largest first
+    std::vector<PPair> prs;
+    std::vector<std::pair<int64_t, int32_t>> big, whole, small;
     int64_t pvals = 0;
     int lv_lo = 1, lv_hi = h.kappa;   // diagnostics: H2D_PAIR_LEVELS=lo,hi (WRONG results; timing only)
     if (getenv("H2D_PAIR_LEVELS")) sscanf(getenv("H2D_PAIR_LEVELS"), "%d,%d", &lv_lo, &lv_hi);
+    const int64_t small_max = getenv("H2D_PAIR_SMALL_MAX") ? atoll(getenv("H2D_PAIR_SMALL_MAX")) : kPSmallBytes;
+    const int64_t whole_max = getenv("H2D_PAIR_WHOLE_MAX") ? atoll(getenv("H2D_PAIR_WHOLE_MAX")) : kPWholeBytes;
     for (int l = std::max(1, lv_lo); l <= std::min(h.kappa, lv_hi); ++l) {
       const Level& L = h.levels[(size_t)l];
       for (const auto& d : L.pairs) {
-        pvals += (int64_t)(d.nv + d.nu) * d.r;
-        const int64_t bytes = (int64_t)(d.nv + d.nu) * d.r * 8;
-        if (d.ch == 0) {
-          PUnit u{};
-          u.off = d.off;
-          u.bytes = (int32_t)((ev(d.nv) + ev(d.nu)) * d.r * 8);
-          u.kind = kPWhole;
-          u.level = l;
-          u.r = d.r;
-          u.ya = d.yv;
-          u.rows_a = d.nv;
-          u.lda = (int32_t)ev(d.nv);
-          u.yb = d.yu;
-          u.rows_b = d.nu;
-          u.ldb = (int32_t)ev(d.nu);
-          whole.push_back({bytes, u});
-        } else {
-          big.push_back(BigPair{bytes, l, d});
-        }
+        const int32_t id = (int32_t)prs.size();
+        prs.push_back(PPair{d.v_off, d.u_off, d.yv, d.yu, d.nv, d.nu, d.R, l});
+        const int64_t bytes = (int64_t)(d.nv + d.nu) * d.R * 8;
+        pvals += (int64_t)(d.nv + d.nu) * d.R;
+        (bytes <= small_max ? small : bytes <= whole_max ? whole : big).push_back({bytes, id});
       }
     }
     h.pair_values = pvals;
-    std::stable_sort(big.begin(), big.end(), [](const BigPair& a, const BigPair& b) { return a.bytes > b.bytes; });
-    std::stable_sort(whole.begin(), whole.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
-    const int64_t nbig = (int64_t)big.size();
-    std::vector<std::vector<PUnit>> ph[3];
-    for (int q = 0; q < 3; ++q) ph[q].resize((size_t)nbig);
-    int64_t toff = 0;
-    for (int64_t k = 0; k < nbig; ++k) {
-      const Level::PairDesc& d = big[(size_t)k].d;
-      int64_t vsize = 0;
-      for (int64_t c0 = 0; c0 < d.nv; c0 += d.ch) vsize += ev(std::min<int64_t>(d.ch, d.nv - c0)) * d.r;
-      for (int q = 1; q <= 3; ++q) {
-        const int64_t rows = q == 2 ? d.nu : d.nv;
-        const int nch = (int)((rows + d.ch - 1) / d.ch);
-        for (int c = 0; c < nch; ++c) {
-          const int64_t rc = std::min<int64_t>(d.ch, rows - (int64_t)c * d.ch);
-          PUnit u{};
-          u.off = d.off + (q == 2 ? vsize : 0) + (int64_t)c * d.ch * d.r;
-          u.bytes = (int32_t)(ev(rc) * d.r * 8);
-          u.kind = q;   // kPPhase1 .. kPPhase3
-          u.level = big[(size_t)k].level;
-          u.r = d.r;
-          u.ya = (q == 2 ? d.yu : d.yv) + c * d.ch;
-          u.rows_a = (int32_t)rc;
-          u.lda = (int32_t)ev(rc);
-          u.big = (int32_t)k;
-          u.nchunks = nch;
-          u.toff = (int32_t)toff;
-          ph[q - 1][(size_t)k].push_back(u);
-        }
+    auto by_size = [](const auto& a, const auto& b) { return a.first > b.first; };
+    std::stable_sort(big.begin(), big.end(), by_size);
+    std::stable_sort(whole.begin(), whole.end(), by_size);
+    std::stable_sort(small.begin(), small.end(), by_size);
+    // groups reference consecutive descriptors: reorder the small pairs' descriptors
+    std::vector<PPair> ordered;
+    ordered.reserve(prs.size());
+    std::vector<int32_t> newid(prs.size());
+    for (auto* cls : {&big, &whole, &small})
+      for (auto& b : *cls) {
+        newid[(size_t)b.second] = (int32_t)ordered.size();
+        ordered.push_back(prs[(size_t)b.second]);
+        b.second = newid[(size_t)b.second];
       }
-      toff += d.r;
+    std::vector<PWork> work;
+    const int64_t nbig = (int64_t)big.size();
+    std::vector<std::vector<PWork>> ph[3];
+    for (int b = 0; b < 3; ++b) ph[b].resize((size_t)nbig);
+    int64_t toff = 0, poff = 0;
+    for (int64_t k = 0; k < nbig; ++k) {
+      const PPair& p = ordered[(size_t)big[(size_t)k].second];
+      for (int q = 1; q <= 3; ++q) {
+        const int n = q == 2 ? p.nu : p.nv;
+        const int nch = (n + kPChunkRows - 1) / kPChunkRows;
+        for (int c = 0; c < nch; ++c) {
+          PWork w{};
+          w.kind = kPPhase1 + q - 1;
+          w.first = big[(size_t)k].second;
+          w.r0 = c * kPChunkRows;
+          w.r1 = std::min(n, (c + 1) * kPChunkRows);
+          w.big = (int32_t)k;
+          w.chunk = c;
+          w.nchunks = nch;
+          w.toff = toff;
+          w.poff = q < 3 ? poff : 0;
+          ph[q - 1][(size_t)k].push_back(w);
+        }
+        if (q < 3) poff += (int64_t)nch * p.r;
+      }
+      toff += p.r;
     }
-    if (toff > INT32_MAX) throw Error{H2D_EINVAL, "pair apply: t too long"};
-    // lag: 1.5 x the bytes all rings hold, so a chunk's inputs are normally published before
-    // it is taken (the phase-3 V re-read then lands ~2 lags behind phase 1)
     const double lag = getenv("H2D_PAIR_LAG") ? atof(getenv("H2D_PAIR_LAG"))
-                                              : 1.5 * h.num_sms * kPSlots * kPSlotDbl * 8.0;
-    std::vector<std::pair<double, PUnit>> keyed;
+                                              : 1.5 * (2.0 * h.num_sms) * kPChunkRows * 20 * 8.0;
+    std::vector<std::pair<double, PWork>> keyed;
     std::vector<double> prev_end((size_t)nbig, -1.0);
     for (int q = 0; q < 3; ++q) {
       double pos = 0.0;
       std::vector<double> end((size_t)nbig, 0.0);
-      for (int64_t k = 0; k < nbig; ++k)
-        for (const PUnit& u : ph[q][(size_t)k]) {
+      for (int64_t k = 0; k < nbig; ++k) {
+        const PPair& p = ordered[(size_t)big[(size_t)k].second];
+        for (const PWork& w : ph[q][(size_t)k]) {
           const double key = std::max(pos + q * lag, prev_end[(size_t)k] + 1.0);
-          keyed.push_back({key, u});
+          keyed.push_back({key, w});
           end[(size_t)k] = std::max(end[(size_t)k], key);
-          pos += (double)u.bytes;
+          pos += (double)(w.r1 - w.r0) * p.r * 8.0;
         }
+      }
       prev_end = end;
     }
     std::stable_sort(keyed.begin(), keyed.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-    std::vector<PUnit> work;
-    work.reserve(keyed.size() + whole.size());
     for (auto& kv : keyed) work.push_back(kv.second);
-    for (auto& w : whole) work.push_back(w.second);
-    if ((int64_t)work.size() > INT32_MAX) throw Error{H2D_EINVAL, "pair apply: too many units"};
+    for (auto& b : whole) {
+      PWork w{};
+      w.kind = kPWhole;
+      w.first = b.second;
+      work.push_back(w);
+    }
+    for (size_t i = 0; i < small.size(); i += kPWarps) {
+      PWork w{};
+      w.kind = kPGroup;
+      w.first = small[i].second;
+      w.count = (int32_t)std::min<size_t>(kPWarps, small.size() - i);
+      work.push_back(w);
+    }
     h.n_pitems = (int64_t)work.size();
-    for (void* q : {h.d_pitems, (void*)h.d_tP1, (void*)h.d_pcount, (void*)h.d_pflags}) h.release(q);
-    h.d_pitems = h.alloc<PUnit>(work.size());
+    for (void* q : {h.d_pitems, h.d_ppairs, (void*)h.d_tP1, (void*)h.d_tP2, (void*)h.d_ptpart, (void*)h.d_pcount,
+                    (void*)h.d_pflags})
+      h.release(q);
+    h.d_pitems = h.alloc<PWork>(work.size());
+    h.d_ppairs = h.alloc<PPair>(ordered.size());
     if (!work.empty())
-      H2D_CUDA(cudaMemcpyAsync(h.d_pitems, work.data(), work.size() * sizeof(PUnit), cudaMemcpyHostToDevice, s));
-    h.pair_t_len = toff;
-    h.d_tP1 = h.alloc<double>(std::max<int64_t>(2, 2 * toff));   // t1 then t2: one memset per matvec
-    h.d_tP2 = h.d_tP1 + toff;
+      H2D_CUDA(cudaMemcpyAsync(h.d_pitems, work.data(), work.size() * sizeof(PWork), cudaMemcpyHostToDevice, s));
+    if (!ordered.empty())
+      H2D_CUDA(cudaMemcpyAsync(h.d_ppairs, ordered.data(), ordered.size() * sizeof(PPair), cudaMemcpyHostToDevice, s));
+    h.d_tP1 = h.alloc<double>(std::max<int64_t>(2, toff + 2));
+    h.d_tP2 = h.alloc<double>(std::max<int64_t>(2, toff + 2));
+    h.d_ptpart = h.alloc<double>(std::max<int64_t>(1, poff));
     h.d_pcount = h.alloc<int32_t>(std::max<int64_t>(2, 2 * nbig));
     h.d_pflags = h.alloc<int32_t>(std::max<int64_t>(2, 2 * nbig));
     H2D_CUDA(cudaMemsetAsync(h.d_pcount, 0, std::max<int64_t>(2, 2 * nbig) * 4, s));
     H2D_CUDA(cudaMemsetAsync(h.d_pflags, 0, std::max<int64_t>(2, 2 * nbig) * 4, s));
     h.pair_epoch = 0;
     if (!h.d_yacc) h.d_yacc = h.alloc<double>(h.n);
-    H2D_CUDA(cudaFuncSetAttribute(pair_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sizeof(PairSmem)));
-    H2D_CUDA(cudaFuncSetAttribute(pair_apply_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                  cudaSharedmemCarveoutMaxShared));   // (same split as the near field)
+    // CTAs per SM (diagnostics: H2D_PAIR_CTAS): 3 measured faster overall than 2 (which leave
+    // the registers for a co-resident near field but run the pairs 1.5x slower)
+    h.pair_ctas_per_sm = getenv("H2D_PAIR_CTAS") ? std::max(1, atoi(getenv("H2D_PAIR_CTAS"))) : 3;
   }
   // the log kernel's near field: subnormal-safe table log only if some near pair needs it
   h.p2p_kid = h.kp.id;
@@ -1949,11 +1943,11 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
     H2D_CUDA(cudaMemsetAsync(h.d_yacc, 0, h.n * sizeof(double), hi));
     H2D_CUDA(cudaMemsetAsync(h.d_counters + 8, 0, sizeof(int32_t), hi));
     ++h.pair_epoch;
-    if (h.pair_t_len > 0) H2D_CUDA(cudaMemsetAsync(h.d_tP1, 0, 2 * h.pair_t_len * sizeof(double), hi));
     if (h.n_pitems > 0) {
-      pair_apply_kernel<<<(int)std::min<int64_t>(h.num_sms, h.n_pitems), kPThreads, sizeof(PairSmem), hi>>>(
-          (const PUnit*)h.d_pitems, (int)h.n_pitems, h.d_counters + 8, pp, d_xtree, h.d_yacc, h.d_tP1, h.d_tP2,
-          h.d_pcount, h.d_pflags, h.pair_epoch);
+      pair_apply_kernel<<<(int)std::min<int64_t>(h.pair_ctas_per_sm * (int64_t)h.num_sms, h.n_pitems), 32 * kPWarps,
+                          0, hi>>>(
+          (const PWork*)h.d_pitems, (int)h.n_pitems, (const PPair*)h.d_ppairs, h.d_counters + 8, pp, d_xtree,
+          h.d_yacc, h.d_tP1, h.d_tP2, h.d_ptpart, h.d_pcount, h.d_pflags, h.pair_epoch);
       H2D_LAUNCH_CHECK();
     }
     record(h, 2, hi);

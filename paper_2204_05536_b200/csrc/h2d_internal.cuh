@@ -148,12 +148,11 @@ struct Level {
   std::vector<int32_t> ubcol;               // per block (first side): column in the Ub panel of X
   std::vector<int32_t> t1base;              // per box + 1: prefix of R^F (t1 layout)
   int64_t t1_base = 0;                      // first t1 entry of the level
-  // pair apply (Handle::pairapply, pairs.cuh): per pair {X, Y}, X < Y, rank r > 0, from
-  // Pr + off: V (n_Y rows) then U (m_X rows), column-major, whole (ch = 0) or as row chunks
-  // of ch rows per factor, each block's row count rounded up to even
+  // pair apply (Handle::pairapply): per pair {X, Y}, X < Y, rank r > 0, V (n_Y x Rp) then
+  // U (m_X x Rp), row-major, Rp = r rounded up to even (zero pad column), in Pr
   struct PairDesc {
-    int64_t off;
-    int32_t yv, yu, nv, nu, r, ch;
+    int64_t v_off, u_off;
+    int32_t yv, yu, nv, nu, R, Rp;
   };
   double* Pr = nullptr;
   int64_t pr_values = 0, pr_alloc = 0;
@@ -323,12 +322,13 @@ struct Handle {
   bool pairapply = false;
   bool pair_wanted = false;               // symmetric single-rank handle (H2D_PAIRAPPLY != 0)
   bool pair_failed = false;               // a rank above 127 in the current factors
-  void* d_pitems = nullptr;               // PUnit[] (the ring's work queue)
+  void* d_pitems = nullptr;               // PWork[]
+  void* d_ppairs = nullptr;               // PPair[]
   int64_t n_pitems = 0;
-  double *d_tP1 = nullptr, *d_tP2 = nullptr;   // chunked pairs: t1 / t2 (zeroed per matvec)
-  int64_t pair_t_len = 0;
+  double *d_tP1 = nullptr, *d_tP2 = nullptr, *d_ptpart = nullptr;
   int32_t *d_pcount = nullptr, *d_pflags = nullptr;
   int pair_epoch = 0;
+  int pair_ctas_per_sm = 2;
   int64_t pair_values = 0;                // factor values the pair kernel streams (U + V)
   double* d_yacc = nullptr;               // [n] TREE-order accumulator of the pair kernel
   // multi-RHS (multi.cu): tiled stage-A schedule and per-chunk buffers (<= 8 vectors)

@@ -1,83 +1,56 @@
-// Pair-local symmetric apply (NEXT N1 payoff, R23 / §10 "pair apply").
+// Pair-local symmetric apply (NEXT N1 payoff, R23 / §6 "pair apply").
 //
 // A symmetric build stores one factor pair per unordered box pair {X, Y}, X < Y (Morton):
 // K(X, Y) ~ U V^T and K(Y, X) ~ V U^T (the paper's symmetric setting).  Alg. 2 l.15
 // then needs, per pair, t1 = V^T x_Y, t2 = U^T x_X, y_X += U t1 and y_Y += V t2:
 // each factor is used twice, and each product of one factor needs the other factor's
 // reduction first.  The three-pass apply (A' / B' / C') reads 3 of the 4 factor streams;
-// this kernel reads each factor once from HBM:
+// this kernel reads each factor once from HBM by keeping the pair local:
 //   phase 1  V rows          -> column sums t1 = V^T x_Y
 //   phase 2  U rows          -> column sums t2 = U^T x_X and row dots dy_X = U t1
-//   phase 3  V rows again    -> row dots dy_Y = V t2
-// Persistent kernel, one CTA per SM: a producer warp streams work units into a ring of
-// 32 KB shared-memory slots (cp.async.bulk: the unit's factor block plus the x segments of
-// its rows, completion on the slot's mbarrier); consumer warps take the slots in order and
-// compute from shared memory only (lane = row of a column-major block: conflict-free), so
-// a unit costs no global round trip (the y / t updates are fire-and-forget REDs).  The
-// producer takes units from the global queue in batches (one atomic and one coalesced
-// descriptor load per batch, the next batch's atomic in flight meanwhile).
-// Units:
-//   whole  a pair whose V and U fit one slot together: all three phases in one warp, phase 3
-//          re-reads V from shared memory (no second HBM or L2 read);
-//   chunk  one row chunk of one phase of a larger pair (the coarse levels): phases 1 / 2
-//          add their column sums to t1 / t2 in global memory (fp64 REDs); the last chunk of
-//          a phase publishes a flag (= matvec epoch); a phase-2 / 3 chunk waits for it.
-//          The phase-3 V chunk is re-read (the schedule places it close behind phase 1, so
-//          it mostly hits L2; phase-1 copies carry no evict-first hint for that reason).
-// Deadlock freedom: the global queue puts every chunk after all chunks of its pair's
-// previous phase, the producer takes a unit only once a slot is free (it never waits on
-// anything else), and consumers take units in queue order; the earliest unfinished unit
-// therefore has its inputs complete and is being processed.
-// dy rows go to the TREE-order accumulator yacc (L2-resident) by fp64 REDs; not bitwise
-// reproducible (the order of the y accumulations varies between runs).
+//   phase 3  V rows again    -> row dots dy_Y = V t2 (an L2 hit: V was just read)
+// The factors stay in the ACA's column-major layout, V then U per pair.  Lane = row: a warp
+// reads a 32-row tile of a column as one coalesced 256-byte load, so the narrow per-pair
+// panels (rank ~10-40) use every lane; column sums are reduced by warp shuffles, row dots
+// need none.  dy rows go to the TREE-order accumulator yacc (L2-resident) by fp64 REDs on
+// 32 consecutive rows.  Work items: groups of up to 8 small pairs (one warp each), medium
+// pairs (the 8 warps of a CTA split the tiles), and row chunks of the big pairs of the coarse
+// levels (any CTA; the last chunk of a phase reduces the partials in chunk order and
+// publishes t1 / t2 with a flag = matvec epoch; a later phase's chunk waits for it).
+// Not bitwise reproducible: the order of the y accumulations varies between runs.
 #pragma once
 #include "pipe.cuh"
 
 namespace h2d {
 namespace {
 
-constexpr int kPSlotDbl = 4096;             // ring slot: 32 KB (factor block + x segments)
-constexpr int kPSlots = 5;                  // slots per CTA (160 KB: a near-field CTA co-resides)
-constexpr int kPCons = 5;                   // consumer warps (<= kPSlots: the end markers)
-constexpr int kPBatch = 16;                 // units per queue grab
-constexpr int kPThreads = 32 * (kPCons + 1);
-constexpr int kPMaxR = 128;                 // widest pair (rank)
+constexpr int kPWarps = 8;                  // warps per CTA
+constexpr int kPMaxR = 128;                 // widest pair (rank), column blocks of <= 16
+constexpr int kPSmallBytes = 48 * 1024;     // pairs up to this: one warp
+constexpr int kPWholeBytes = 640 * 1024;    // pairs up to this: one CTA, all phases
+constexpr int kPChunkRows = 2048;           // big pairs: row chunks (per phase)
 
-enum { kPWhole = 0, kPPhase1 = 1, kPPhase2 = 2, kPPhase3 = 3, kPEnd = 4 };
+enum { kPGroup = 0, kPWhole = 1, kPPhase1 = 2, kPPhase2 = 3, kPPhase3 = 4 };
 #ifndef H2D_PAIR_NORED
 #define H2D_PAIR_NORED 0
 #endif
 constexpr bool kPNoRed = H2D_PAIR_NORED;   // build-time diagnostics switch (timing of the REDs)
 
-// One ring unit: `bytes` of factors from the level's pair array at `off`, then the x
-// segments of its rows (whole: V rows, U rows; phase 1 / 2 chunk: its rows; phase 3: none),
-// each copied from the even row at or below its first row (16-byte aligned).
-struct PUnit {
-  int64_t off;
-  int32_t bytes, kind, level, r;
-  int32_t ya, rows_a, lda;  // first block (whole: V; chunk: the chunk): TREE row, rows, ld
-  int32_t yb, rows_b, ldb;  // whole: U
-  int32_t big, nchunks;     // chunk: counter / flag index of the pair, chunks of the phase
-  int32_t toff, pad;        // chunk: t1 / t2 offset of the pair
+struct PPair {              // one stored pair
+  int64_t v_off, u_off;     // V (nv x r) and U (nu x r), column-major, in the level's pair array
+  int32_t yv, yu;           // TREE rows of Y (V rows) and X (U rows)
+  int32_t nv, nu, r, level;
 };
-static_assert(sizeof(PUnit) == 64, "PUnit layout");
-
+struct PWork {              // one work item (a CTA takes it)
+  int32_t kind;
+  int32_t first, count;     // kPGroup: pairs [first, first + count); else the pair `first`
+  int32_t r0, r1;           // chunk: rows [r0, r1) of the phase's factor
+  int32_t big, chunk, nchunks;
+  int64_t toff, poff;       // big pair: t1 / t2 offset; partial slots of the phase
+};
 struct PairPtrs {
   const double* P[H2D_MAX_LEVELS + 1];
 };
-
-struct PairSmem {
-  double slot[kPSlots][kPSlotDbl];
-  double ts[kPCons][2][kPMaxR];      // per consumer warp: t1 / t2 of its unit
-  PUnit meta[kPSlots];
-  PUnit batch[kPBatch];
-  uint64_t full[kPSlots], empty[kPSlots];
-  int next;
-};
-
-__host__ __device__ __forceinline__ int pair_xseg(int y, int rows) {   // doubles copied
-  return ((y & 1) + rows + 1) & ~1;
-}
 
 __device__ __forceinline__ int ld_acquire(const int32_t* p) {
   int v;
@@ -88,228 +61,233 @@ __device__ __forceinline__ void st_release(int32_t* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ void pair_red(double* p, double v) {
-  if (kPNoRed) *p = v;   // diagnostics only (WRONG results)
-  else atomicAdd(p, v);
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
-// Column sums of a column-major block F (ld, rows, columns [0, r)) against x[0, rows), in
-// blocks of 8 columns (transposed butterfly, pipe.cuh).  The sum of column c ends up in
-// lane 4 (c & 7) for its block; emit(c, value) is called by that lane.
-template <class Emit>
-__device__ __forceinline__ void pair_colsums(const double* F, int ld, int rows, int r, const double* x, Emit emit) {
+// One warp over the rows {tile * 32 + lane : tile = t0, t0 + ts, ...} < rows of columns
+// [c0, c0 + nc) (nc <= NC) of a column-major factor F (leading dimension ld):
+//   COLS  acc[q] += F[i, c0 + q] x[i]           (column sums, per lane)
+//   ROWS  dy[i]  += sum_q F[i, c0 + q] t[c0 + q] (row dots, one fp64 RED per row)
+template <int NC, bool COLS, bool ROWS>
+__device__ __forceinline__ void pair_tiles(const double* __restrict__ F, int64_t ld, int rows, int c0, int nc,
+                                           int t0, int ts, const double* __restrict__ x, const double* tv,
+                                           double* __restrict__ dy, double (&acc)[NC]) {
   const int lane = threadIdx.x & 31;
-  for (int c0 = 0; c0 < r; c0 += 8) {
-    double acc[8];
+  for (int t = t0; 32 * t < rows; t += ts) {
+    const int i = 32 * t + lane;
+    const bool ok = i < rows;
+    double v[NC];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-    const double* Fc = F + (int64_t)c0 * ld;
-    const int nc = min(8, r - c0);
-#pragma unroll 2
-    for (int i = lane; i < rows; i += 32) {
-      const double xi = x[i];
+    for (int q = 0; q < NC; ++q) v[q] = (ok && q < nc) ? __ldcs(F + (int64_t)(c0 + q) * ld + i) : 0.0;
+    if (COLS) {
+      const double xi = ok ? __ldg(x + i) : 0.0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q < nc) acc[q] = fma(Fc[q * ld + i], xi, acc[q]);
+      for (int q = 0; q < NC; ++q) acc[q] = fma(v[q], xi, acc[q]);
     }
-    const double s = warp_transpose_sum8(acc, lane);
-    const int c = c0 + (lane >> 2);
-    if ((lane & 3) == 0 && c < r) emit(c, s);
-  }
-}
-
-// Row dots dy[i] = sum_q F[i, q] t[q] (t in shared memory), one RED per row.
-__device__ __forceinline__ void pair_rowdots(const double* F, int ld, int rows, int r, const double* t,
-                                             double* __restrict__ y) {
-  const int lane = threadIdx.x & 31;
-  for (int i = lane; i < rows; i += 32) {
-    double d0 = 0.0, d1 = 0.0;
-    int q = 0;
-    for (; q + 1 < r; q += 2) {
-      d0 = fma(F[q * ld + i], t[q], d0);
-      d1 = fma(F[(q + 1) * ld + i], t[q + 1], d1);
-    }
-    if (q < r) d0 = fma(F[q * ld + i], t[q], d0);
-    pair_red(y + i, d0 + d1);
-  }
-}
-
-// Phase 2 of a narrow pair (r <= 8) in one pass: column sums against x and row dots with t.
-template <class Emit>
-__device__ __forceinline__ void pair_colsum_rowdot8(const double* F, int ld, int rows, int r,
-                                                    const double* x, const double* t,
-                                                    double* __restrict__ y, Emit emit) {
-  const int lane = threadIdx.x & 31;
-  double acc[8], tq[8];
+    if (ROWS) {
+      double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    acc[q] = 0.0;
-    tq[q] = q < r ? t[q] : 0.0;
-  }
-#pragma unroll 2
-  for (int i = lane; i < rows; i += 32) {
-    const double xi = x[i];
-    double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-    for (int q = 0; q < 8; q += 2) {
-      if (q < r) {
-        const double f = F[q * ld + i];
-        acc[q] = fma(f, xi, acc[q]);
-        d0 = fma(f, tq[q], d0);
+      for (int q = 0; q < NC; q += 2) {   // (t from shared memory: a broadcast load per column)
+        if (q < nc) d0 = fma(v[q], tv[c0 + q], d0);
+        if (q + 1 < NC && q + 1 < nc) d1 = fma(v[q + 1], tv[c0 + q + 1], d1);
       }
-      if (q + 1 < r) {
-        const double f = F[(q + 1) * ld + i];
-        acc[q + 1] = fma(f, xi, acc[q + 1]);
-        d1 = fma(f, tq[q + 1], d1);
+      if (ok) {
+        if (kPNoRed) dy[i] = d0 + d1;   // diagnostics only (WRONG results)
+        else atomicAdd(dy + i, d0 + d1);
       }
     }
-    pair_red(y + i, d0 + d1);
-  }
-  const double s = warp_transpose_sum8(acc, lane);
-  const int c = lane >> 2;
-  if ((lane & 3) == 0 && c < r) emit(c, s);
-}
-
-__device__ __forceinline__ void pair_wait_flag(const int32_t* f, int epoch) {
-  if ((threadIdx.x & 31) == 0)
-    while (ld_acquire(f) < epoch) __nanosleep(64);
-  __syncwarp();
-  __threadfence();
-}
-
-// A chunk of phase 1 / 2 has added its column sums: count it; the last chunk publishes.
-__device__ __forceinline__ void pair_chunk_done(int32_t* cnt, int32_t* flag, int nchunks, int epoch) {
-  __threadfence();
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0 && atomicAdd(cnt, 1) == nchunks - 1) {
-    *cnt = 0;   // (the next matvec's chunks start after this kernel)
-    __threadfence();
-    st_release(flag, epoch);
   }
 }
 
-__global__ void __launch_bounds__(kPThreads, 1)
-pair_apply_kernel(const PUnit* __restrict__ units, int n_units, int32_t* counter, PairPtrs pp,
-                  const double* __restrict__ x, double* __restrict__ yacc, double* __restrict__ tP1,
-                  double* __restrict__ tP2, int32_t* __restrict__ pcount, int32_t* __restrict__ flags, int epoch) {
-  extern __shared__ __align__(128) unsigned char pair_smem_raw[];
-  PairSmem& S = *reinterpret_cast<PairSmem*>(pair_smem_raw);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kPSlots; ++s) {
-      mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], 1);
-    }
-    S.next = 0;
-    mbar_fence_init();
+template <int NC>
+__device__ __forceinline__ void zero_acc(double (&acc)[NC]) {
+#pragma unroll
+  for (int q = 0; q < NC; ++q) acc[q] = 0.0;
+}
+
+// Warp-level column sums of columns [c0, c0 + nc) into ts[c0 + q] (shared, per warp).
+template <int NC>
+__device__ __forceinline__ void warp_colsum_store(double (&acc)[NC], int c0, int nc, double* ts) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    const double s = warp_sum(acc[q]);
+    if (lane == 0 && q < nc) ts[c0 + q] = s;
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------- one warp, one pair
+template <int NC>
+__device__ void pair_warp(const PPair& p, const double* __restrict__ base, const double* __restrict__ x,
+                          double* __restrict__ yacc, double* ts1, double* ts2) {
+  const double* V = base + p.v_off;
+  const double* U = base + p.u_off;
+  double acc[NC];
+  for (int c0 = 0; c0 < p.r; c0 += NC) {   // phase 1: t1 = V^T x_Y
+    const int nc = min(NC, p.r - c0);
+    zero_acc(acc);
+    pair_tiles<NC, true, false>(V, p.nv, p.nv, c0, nc, 0, 1, x + p.yv, nullptr, nullptr, acc);
+    warp_colsum_store(acc, c0, nc, ts1);
+  }
+  for (int c0 = 0; c0 < p.r; c0 += NC) {   // phase 2: t2 = U^T x_X, y_X += U t1
+    const int nc = min(NC, p.r - c0);
+    zero_acc(acc);
+    pair_tiles<NC, true, true>(U, p.nu, p.nu, c0, nc, 0, 1, x + p.yu, ts1, yacc + p.yu, acc);
+    warp_colsum_store(acc, c0, nc, ts2);
+  }
+  for (int c0 = 0; c0 < p.r; c0 += NC) {   // phase 3: y_Y += V t2
+    const int nc = min(NC, p.r - c0);
+    pair_tiles<NC, false, true>(V, p.nv, p.nv, c0, nc, 0, 1, nullptr, ts2, yacc + p.yv, acc);
+  }
+}
+
+// ---------------------------------------------------------------- the CTA, one pair / chunk
+// CTA column sums: warp partials -> red[w][q] -> sum over the warps -> out[q] (shared or
+// global), then a barrier.
+template <int NC>
+__device__ __forceinline__ void cta_colsum(double (&acc)[NC], int c0, int nc, double* red, double* out) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    const double s = warp_sum(acc[q]);
+    if (lane == 0) red[w * kPMaxR + c0 + q] = s;
   }
   __syncthreads();
-  if (warp == 0) {   // producer
-    const uint64_t pol = l2_evict_first_policy();
-    int k = 0, ends = 0;
-    int base = 0;
-    if (lane == 0) base = atomicAdd(counter, kPBatch);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    PUnit cur;
-    if (base + lane < n_units && lane < kPBatch) cur = units[base + lane];
-    for (;;) {
-      const int cnt = max(0, min(kPBatch, n_units - base));
-      if (lane < cnt) S.batch[lane] = cur;
-      int nbase = 0;
-      if (lane == 0 && cnt > 0) nbase = atomicAdd(counter, kPBatch);   // (used after this batch)
-      __syncwarp();
-      if (lane == 0) {
-        for (int j = 0; j < cnt; ++j, ++k) {
-          const int s = k % kPSlots;
-          if (k >= kPSlots) mbar_wait(&S.empty[s], ((k / kPSlots) - 1) & 1);
-          const PUnit u = S.batch[j];
-          S.meta[s] = u;
-          const int xa = u.kind == kPPhase3 ? 0 : pair_xseg(u.ya, u.rows_a);
-          const int xb = u.kind == kPWhole ? pair_xseg(u.yb, u.rows_b) : 0;
-          mbar_arrive_expect_tx(&S.full[s], (uint32_t)(u.bytes + 8 * (xa + xb)));
-          double* dst = S.slot[s];
-          if (u.kind == kPPhase1) bulk_g2s_keep(dst, pp.P[u.level] + u.off, (uint32_t)u.bytes, &S.full[s]);
-          else bulk_g2s(dst, pp.P[u.level] + u.off, (uint32_t)u.bytes, &S.full[s], pol);
-          dst += u.bytes / 8;
-          if (xa) bulk_g2s_keep(dst, x + (u.ya & ~1), 8u * xa, &S.full[s]);
-          if (xb) bulk_g2s_keep(dst + xa, x + (u.yb & ~1), 8u * xb, &S.full[s]);
-        }
-        if (cnt == 0) {   // queue exhausted: one end marker per consumer warp
-          for (; ends < kPCons; ++ends, ++k) {
-            const int s = k % kPSlots;
-            if (k >= kPSlots) mbar_wait(&S.empty[s], ((k / kPSlots) - 1) & 1);
-            S.meta[s].kind = kPEnd;
-            mbar_arrive(&S.full[s]);
-          }
-        }
-      }
-      if (cnt == 0) break;
-      __syncwarp();
-      base = __shfl_sync(0xffffffffu, nbase, 0);
-      if (base + lane < n_units && lane < kPBatch) cur = units[base + lane];
+  for (int q = threadIdx.x; q < nc; q += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < kPWarps; ++ww) s += red[ww * kPMaxR + c0 + q];
+    out[c0 + q] = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void wait_flag(const int32_t* f, int epoch) {
+  if (threadIdx.x == 0)
+    while (ld_acquire(f) < epoch) __nanosleep(100);
+  __syncthreads();
+  __threadfence();   // (invalidates this SM's L1 before the t loads)
+}
+
+template <int NC>
+__device__ void pair_cta(const PWork& w, const PPair& p, const double* __restrict__ base,
+                         const double* __restrict__ x, double* __restrict__ yacc, double* __restrict__ tP1,
+                         double* __restrict__ tP2, double* __restrict__ tpart, int32_t* __restrict__ pcount,
+                         int32_t* __restrict__ flags, int epoch, double* st1, double* st2, double* red,
+                         int* sflag) {
+  const int wid = threadIdx.x >> 5;
+  const double* V = base + p.v_off;
+  const double* U = base + p.u_off;
+  double acc[NC];
+  if (w.kind == kPWhole) {
+    for (int c0 = 0; c0 < p.r; c0 += NC) {
+      const int nc = min(NC, p.r - c0);
+      zero_acc(acc);
+      pair_tiles<NC, true, false>(V, p.nv, p.nv, c0, nc, wid, kPWarps, x + p.yv, nullptr, nullptr, acc);
+      cta_colsum(acc, c0, nc, red, st1);
+    }
+    for (int c0 = 0; c0 < p.r; c0 += NC) {
+      const int nc = min(NC, p.r - c0);
+      zero_acc(acc);
+      pair_tiles<NC, true, true>(U, p.nu, p.nu, c0, nc, wid, kPWarps, x + p.yu, st1, yacc + p.yu, acc);
+      cta_colsum(acc, c0, nc, red, st2);
+    }
+    for (int c0 = 0; c0 < p.r; c0 += NC) {
+      const int nc = min(NC, p.r - c0);
+      pair_tiles<NC, false, true>(V, p.nv, p.nv, c0, nc, wid, kPWarps, nullptr, st2, yacc + p.yv, acc);
     }
     return;
   }
-  const int cw = warp - 1;
-  double* ts1 = S.ts[cw][0];
-  double* ts2 = S.ts[cw][1];
+  // a row chunk [r0, r1) of one phase of a big pair
+  const int ph = w.kind - kPPhase1 + 1;
+  const double* F = ph == 2 ? U : V;
+  const int64_t ld = ph == 2 ? p.nu : p.nv;
+  const int y0 = ph == 2 ? p.yu : p.yv;
+  const int rows = w.r1 - w.r0;
+  const double* Fc = F + w.r0;            // column q of the chunk: Fc + q ld
+  if (ph >= 2) {                          // the other factor's reduction must be published
+    wait_flag(flags + 2 * w.big + (ph - 2), epoch);
+    const double* tg = (ph == 2 ? tP1 : tP2) + w.toff;
+    for (int q = threadIdx.x; q < p.r; q += blockDim.x) st1[q] = tg[q];
+    __syncthreads();
+  }
+  for (int c0 = 0; c0 < p.r; c0 += NC) {
+    const int nc = min(NC, p.r - c0);
+    zero_acc(acc);
+    if (ph == 1)
+      pair_tiles<NC, true, false>(Fc, ld, rows, c0, nc, wid, kPWarps, x + y0 + w.r0, nullptr, nullptr, acc);
+    else if (ph == 2)
+      pair_tiles<NC, true, true>(Fc, ld, rows, c0, nc, wid, kPWarps, x + y0 + w.r0, st1, yacc + y0 + w.r0, acc);
+    else
+      pair_tiles<NC, false, true>(Fc, ld, rows, c0, nc, wid, kPWarps, nullptr, st1, yacc + y0 + w.r0, acc);
+    if (ph < 3) cta_colsum(acc, c0, nc, red, tpart + w.poff + (int64_t)w.chunk * p.r);
+  }
+  if (ph == 3) return;
+  // the last chunk of the phase sums the partials in chunk order and publishes t1 / t2
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int last = atomicAdd(pcount + 2 * w.big + (ph - 1), 1) == w.nchunks - 1;
+    if (last) __threadfence();
+    *sflag = last;
+  }
+  __syncthreads();
+  if (*sflag) {
+    double* tout = (ph == 1 ? tP1 : tP2) + w.toff;
+    for (int q = threadIdx.x; q < p.r; q += blockDim.x) {
+      const double* __restrict__ pq = tpart + w.poff + q;
+      double a0 = 0.0, a1 = 0.0;
+      int c = 0;
+      for (; c + 1 < w.nchunks; c += 2) {
+        a0 += __ldcg(pq + (int64_t)c * p.r);
+        a1 += __ldcg(pq + (int64_t)(c + 1) * p.r);
+      }
+      if (c < w.nchunks) a0 += __ldcg(pq + (int64_t)c * p.r);
+      tout[q] = a0 + a1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      pcount[2 * w.big + (ph - 1)] = 0;
+      __threadfence();
+      st_release(flags + 2 * w.big + (ph - 1), epoch);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32 * kPWarps, 3)
+pair_apply_kernel(const PWork* __restrict__ work, int n_work, const PPair* __restrict__ pairs, int32_t* counter,
+                  PairPtrs pp, const double* __restrict__ x, double* __restrict__ yacc, double* __restrict__ tP1,
+                  double* __restrict__ tP2, double* __restrict__ tpart, int32_t* __restrict__ pcount,
+                  int32_t* __restrict__ flags, int epoch) {
+  __shared__ double st[kPWarps][2][kPMaxR];     // per-warp t1 / t2 (groups); st[0] for CTA items
+  __shared__ double red[kPWarps * kPMaxR];
+  __shared__ int sidx, sflag;
+  const int wid = threadIdx.x >> 5;
   for (;;) {
-    int k = 0;
-    if (lane == 0) k = atomicAdd(&S.next, 1);
-    k = __shfl_sync(0xffffffffu, k, 0);
-    const int s = k % kPSlots;
-    mbar_wait(&S.full[s], (k / kPSlots) & 1);
-    const PUnit u = S.meta[s];
-    if (u.kind == kPEnd) break;
-    const double* F = S.slot[s];
-    const int r = u.r;
-    const double* xa = F + u.bytes / 8 + (u.ya & 1);                      // x of the first block's rows
-    const double* xb = F + u.bytes / 8 + pair_xseg(u.ya, u.rows_a) + (u.yb & 1);   // whole: x of U's rows
-    auto release = [&]() {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[s]);
-    };
-    if (u.kind == kPWhole) {
-      const double* V = F;
-      const double* U = F + (int64_t)u.lda * r;
-      pair_colsums(V, u.lda, u.rows_a, r, xa, [&](int c, double v) { ts1[c] = v; });
-      __syncwarp();
-      if (r <= 8) {
-        pair_colsum_rowdot8(U, u.ldb, u.rows_b, r, xb, ts1, yacc + u.yb, [&](int c, double v) { ts2[c] = v; });
-      } else {
-        pair_colsums(U, u.ldb, u.rows_b, r, xb, [&](int c, double v) { ts2[c] = v; });
-        pair_rowdots(U, u.ldb, u.rows_b, r, ts1, yacc + u.yb);
+    if (threadIdx.x == 0) sidx = atomicAdd(counter, 1);
+    __syncthreads();
+    const int idx = sidx;
+    __syncthreads();
+    if (idx >= n_work) break;
+    const PWork w = work[idx];
+    if (w.kind == kPGroup) {
+      if (wid < w.count) {
+        const PPair p = pairs[w.first + wid];
+        const double* base = pp.P[p.level];
+        if (p.r <= 8) pair_warp<8>(p, base, x, yacc, st[wid][0], st[wid][1]);
+        else pair_warp<16>(p, base, x, yacc, st[wid][0], st[wid][1]);
       }
-      __syncwarp();
-      pair_rowdots(V, u.lda, u.rows_a, r, ts2, yacc + u.ya);
-      release();
-      continue;
+      continue;   // (the next item's barrier waits for every warp)
     }
-    if (u.kind == kPPhase1) {
-      pair_colsums(F, u.lda, u.rows_a, r, xa, [&](int c, double v) { pair_red(tP1 + u.toff + c, v); });
-      release();
-      pair_chunk_done(pcount + 2 * u.big, flags + 2 * u.big, u.nchunks, epoch);
-      continue;
-    }
-    // phases 2 / 3 need the other factor's column sums
-    pair_wait_flag(flags + 2 * u.big + (u.kind - 2), epoch);
-    const double* tg = (u.kind == kPPhase2 ? tP1 : tP2) + u.toff;
-    for (int q = lane; q < r; q += 32) ts1[q] = __ldcg(tg + q);
-    __syncwarp();
-    if (u.kind == kPPhase2) {
-      auto emit = [&](int c, double v) { pair_red(tP2 + u.toff + c, v); };
-      if (r <= 8) {
-        pair_colsum_rowdot8(F, u.lda, u.rows_a, r, xa, ts1, yacc + u.ya, emit);
-      } else {
-        pair_colsums(F, u.lda, u.rows_a, r, xa, emit);
-        pair_rowdots(F, u.lda, u.rows_a, r, ts1, yacc + u.ya);
-      }
-      release();
-      pair_chunk_done(pcount + 2 * u.big + 1, flags + 2 * u.big + 1, u.nchunks, epoch);
-    } else {
-      pair_rowdots(F, u.lda, u.rows_a, r, ts1, yacc + u.ya);
-      release();
-    }
+    const PPair p = pairs[w.first];
+    const double* base = pp.P[p.level];
+    if (p.r <= 8)
+      pair_cta<8>(w, p, base, x, yacc, tP1, tP2, tpart, pcount, flags, epoch, st[0][0], st[0][1], red, &sflag);
+    else
+      pair_cta<16>(w, p, base, x, yacc, tP1, tP2, tpart, pcount, flags, epoch, st[0][0], st[0][1], red, &sflag);
   }
 }
 

@@ -314,7 +314,7 @@ def test_symmetric_partitioned_multi_rhs(h2d):
 @pytest.mark.parametrize("name,lag", [("c1", None), ("c2", None), ("c2", "0")])
 def test_pair_apply_matches_three_pass_and_oracle(h2d, name, lag, tmp_path, monkeypatch):
     """The pair-local apply (opt-in on symmetric single-rank handles: each factor read once;
-    pairs that fit a ring slot in one warp, larger pairs in row chunks per phase with
+    small pairs one warp each, medium pairs one CTA, big pairs in row chunks per phase with
     flag-published t1 / t2) computes the same operator as the three-pass apply and, with the
     oracle's symmetric factors, the oracle matvec to <= 1e-12.  lag 0 puts every phase-2 / 3
     chunk right behind its inputs in the queue (the flag waits actually happen)."""
