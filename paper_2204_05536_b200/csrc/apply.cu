@@ -702,8 +702,11 @@ __device__ __forceinline__ void warp_nbr(int lane, const double (&pi)[RPL], cons
   }
 }
 
+#ifndef H2D_P2P_WARP_MINB
+#define H2D_P2P_WARP_MINB 3
+#endif
 template <int KID, int RPL>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, H2D_P2P_WARP_MINB)
 p2p_warp_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int32_t* counter,
                 const int32_t* __restrict__ leaf_start, const double* __restrict__ px,
                 const double* __restrict__ py, const double* __restrict__ x, KernelParams kp,
