@@ -161,9 +161,10 @@ typedef struct {
   int64_t device_bytes;      /* device memory held by the handle                      */
   int64_t gather_stride;     /* max rows over ranks (slot size of H2D_ORDER_GATHERED) */
   int64_t p2p_bytes;         /* algorithmic bytes of the near-field P2P kernel        */
-  int symmetric_apply;       /* 1 -> matvecs run the symmetric three-pass apply (R23):
-                                stage slot 1 = A' + B', slot 2 = C'; stageA_bytes /
-                                stageB_bytes then count those passes                  */
+  int symmetric_apply;       /* 1 -> matvecs run the symmetric three-pass apply (R23;
+                                every symmetric build unless H2D_SYMAPPLY=0, a rank of a
+                                partition too): stage slot 1 = A' + B', slot 2 = C';
+                                stageA_bytes / stageB_bytes then count those passes    */
   int p2p_launches;          /* near-field kernels per matvec: warp-per-leaf (one per rows-
                                 per-lane class 1..3, leaves <= 96 points), CTA fast path,
                                 generic (1..5)                                         */
@@ -213,7 +214,8 @@ int hodlr2d_matvec_ex(hodlr2d_t h, const double* x, double* y, int order);
  * H2D_ORDER_GATHERED (x = one padded all-gather buffer per vector, len_x = world *
  * info.gather_stride; y as for TREE).  The factor panels are streamed once per chunk of up
  * to 16 vectors (chunks of 16, 8, 4, 2; a last single vector takes the hodlr2d_matvec
- * path; symmetric-apply handles: chunks of 8), so throughput in matvecs/s grows with nrhs
+ * path; symmetric-apply handles: chunks of 8, one vector at a time on a rank of a
+ * partition), so throughput in matvecs/s grows with nrhs
  * until the FP64 pipes, not HBM, bound it.  Host or device pointers; Y is overwritten.
  * Results equal nrhs separate hodlr2d_matvec_ex calls up to rounding (different
  * summation order). */
