@@ -447,6 +447,7 @@ def run_ours(args, cfg):
     ops_eval = P2P_FP64_OPS_PER_EVAL.get(cfg.kernel)
     sm_hz = (csum["sm_mhz"] or 1965.0) * 1e6
     served = inf["row_end"] - inf["row_begin"]
+    self_evals = 0.0
     if inf.get("adaptive"):   # p2p_list_kernel: every directed pair of the dense blocks
         evals = float(inf["p2p_pairs"])
     else:
@@ -454,8 +455,11 @@ def run_ours(args, cfg):
         msz = np.diff(ls[inf["leaf_begin"]: inf["leaf_end"] + 1]).astype(np.float64)
         self_pairs = float((msz * msz).sum())
         warp = msz <= 96   # warp-per-leaf path: full self blocks; CTA paths: i <= j only
-        evals = float((msz[warp] ** 2).sum() + (msz[~warp] * (msz[~warp] + 1) / 2).sum()) \
-            + (inf["p2p_pairs"] - self_pairs) / 2.0
+        self_evals = float((msz[warp] ** 2).sum() + (msz[~warp] * (msz[~warp] + 1) / 2).sum())
+        evals = self_evals + (inf["p2p_pairs"] - self_pairs) / 2.0
+    if ops_eval is not None and cfg.kernel == 0 and self_evals > 0:
+        # log: a neighbour-block evaluation adds its column-sum DFMA to the self-block count
+        ops_eval = (self_evals * ops_eval + (evals - self_evals) * (ops_eval + 1)) / evals
     alone_ms = p2p_standalone_ms(op, step, args) if world == 1 else None
     peak_ops, peak_ops_kind = 148 * 64 * sm_hz, "nominal: 148 SMs x 64 FP64 lanes x SM clock"
     try:
@@ -716,12 +720,13 @@ def launches_per_matvec(inf, world):
 
 
 # FP64-pipe instructions per kernel evaluation in p2p_warp_kernel's self-block loop
-# (DESIGN.md §6); keyed by kernel id.  log (p2p_warp_kernel<kLogNoSel, 2>, round 2): distance
-# 2 DADD + DMUL + DFMA, table log 7 DFMA + 1 DADD (exponent), accumulation 1 DFMA = 13 (the
-# round-1 form counted from `cuobjdump -sass`: 44 DFMA + 8 DADD + 4 DMUL + 4 DSETP + 4
-# I2F.F64 per 4 evaluations = 16); IMQ / 1/r: distance + rsqrt (MUFU.RSQ64H seed + Newton) +
-# the accumulation, ~12 (estimate).
-P2P_FP64_OPS_PER_EVAL = {0: 13, 1: 12, 2: 12}
+# (DESIGN.md §6); keyed by kernel id.  log (p2p_warp_kernel<kLogNoSel, 2>, round 2, counted in
+# `cuobjdump -sass` of the unrolled self loop: 48 FP64 per 4 evaluations): distance 2 DADD +
+# DMUL + DFMA, table log 6 DFMA + 1 DADD (exponent; ln2 / 2 without its lo part),
+# accumulation 1 DFMA = 12; a neighbour-block evaluation adds its column-sum DFMA (13).
+# (Round 1: 16 with the select and I2F.F64; round 2 before the high-word log: 13.)  IMQ / 1/r:
+# distance + rsqrt (MUFU.RSQ64H seed + Newton) + the accumulation, ~12 (estimate).
+P2P_FP64_OPS_PER_EVAL = {0: 12, 1: 12, 2: 12}
 
 
 def p2p_standalone_ms(op, step, args, n=10):

@@ -39,7 +39,7 @@ constexpr int kT1Max = kT1Smem;      // symmetric stage B': widest first-side pa
 // stage B' ring: 2 x 44 KB slots.  The fused column-sum + row-dot pass is issue-bound, not
 // latency-bound (the second CTA on the SM hides the copy latency), so fewer, larger stages
 // win by amortising the per-stage overhead: A'+B' 2.20 ms (5 x 16 KB) -> 1.76 ms (C3).
-constexpr int kNSDual = 2, kSDDual = 5632;
+constexpr int kNSDual = 2, kSDDual = 5632;   // (4 x 2816 measured slower: C3 symmetric 406 -> 390 / s)
 
 struct UCopyItem {
   const double* src;   // column-major, leading dimension ld_src
@@ -574,6 +574,41 @@ p2p_list_kernel(const int64_t* __restrict__ items, int n_items, int32_t* counter
     const int64_t lf = it >> 8;
     const int64_t xs = (int64_t)lf_start[lf] + 64 * (it & 255);
     const int m = (int)min((int64_t)64, (int64_t)lf_start[lf + 1] - xs);
+    if (m <= 32) {
+      // small pass (the adaptive tree's typical leaf): G = 32 / S column groups of S >= m
+      // lanes, lane = (group g, row i); the groups take every G-th column of a tile and
+      // their row sums meet by xor shuffles (the two-row mapping evaluated 64 rows per pass)
+      const int S = m <= 8 ? 8 : m <= 16 ? 16 : 32;
+      const int G = 32 / S, g = lane / S, i = lane - g * S;
+      const double pr = i < m ? px[xs + i] : 0.0, qr = i < m ? py[xs + i] : 0.0;
+      double a = 0.0;
+      for (int64_t e = nf_off[lf]; e < nf_off[lf + 1]; ++e) {
+        const int64_t c0 = nf_rng[2 * e], cnt = nf_rng[2 * e + 1];
+        for (int64_t t = 0; t < cnt; t += 32) {
+          const int64_t j = t + lane;
+          __syncwarp();
+          sq[w][lane] = j < cnt ? make_double2(px[c0 + j], py[c0 + j]) : make_double2(0.0, 0.0);
+          sxv[w][lane] = j < cnt ? x[c0 + j] : 0.0;
+          __syncwarp();
+          const int nt = (int)min((int64_t)32, cnt - t);
+          for (int jj = g; jj < nt; jj += G) {
+            const double2 q = sq[w][jj];
+            double k;
+            if constexpr (kDistKernel<KID>) {
+              const double dx = pr - q.x, dy = qr - q.y;
+              k = kfast<KID>(fma(dx, dx, dy * dy), tab, kp);
+            } else {
+              k = kernel_eval_t<KID>(kp, pr, qr, q.x, q.y);
+            }
+            a = fma(k, sxv[w][jj], a);
+          }
+        }
+      }
+      if (G >= 4) a += __shfl_xor_sync(0xffffffffu, a, 8);
+      if (G >= 2) a += __shfl_xor_sync(0xffffffffu, a, 16);
+      if (g == 0 && i < m) s0[xs + i] = a;
+      continue;
+    }
     double pi[2], qi[2], acc[2];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
@@ -672,10 +707,11 @@ __device__ __forceinline__ void warp_nbr(int lane, const double (&pi)[RPL], cons
   for (int cb = 0; cb < n; cb += 32) {
     const int nc = min(32, n - cb);
     __syncwarp();
-    if (lane < nc) {
-      spq[lane] = make_double2(px[nb0 + cb + lane], py[nb0 + cb + lane]);
-      sx[lane] = x[nb0 + cb + lane];
-    }
+    // slots past the chunk hold a far dummy point with zero weight, so every group of 8
+    // columns runs branch-free (its row sums gain K * 0; its column sums are never written)
+    const bool vj = lane < nc;
+    spq[lane] = vj ? make_double2(px[nb0 + cb + lane], py[nb0 + cb + lane]) : make_double2(1e30, 1e30);
+    sx[lane] = vj ? x[nb0 + cb + lane] : 0.0;
     __syncwarp();
     for (int g = 0; g < nc; g += 8) {
       double c[8];
@@ -683,16 +719,14 @@ __device__ __forceinline__ void warp_nbr(int lane, const double (&pi)[RPL], cons
       for (int t = 0; t < 8; ++t) {
         const int j = g + t;
         c[t] = 0.0;
-        if (j < nc) {   // warp-uniform
-          const double2 q = spq[j];
-          const double xj = sx[j];
+        const double2 q = spq[j];
+        const double xj = sx[j];
 #pragma unroll
-          for (int r = 0; r < RPL; ++r) {
-            const double dx = pi[r] - q.x, dy = qi[r] - q.y;
-            const double v = kfast<KID>(fma(dx, dx, dy * dy), tab, kp);
-            acc[r] = fma(v, xj, acc[r]);
-            c[t] = fma(v, xi[r], c[t]);   // xi = 0 on rows past the leaf
-          }
+        for (int r = 0; r < RPL; ++r) {
+          const double dx = pi[r] - q.x, dy = qi[r] - q.y;
+          const double v = kfast<KID>(fma(dx, dx, dy * dy), tab, kp);
+          acc[r] = fma(v, xj, acc[r]);
+          c[t] = fma(v, xi[r], c[t]);   // xi = 0 on rows past the leaf
         }
       }
       const double v = warp_transpose_sum8(c, lane);
@@ -1219,7 +1253,14 @@ void finalize_schedule(Handle& h) {
   // H2D_SMALL_MIN (tests): the minimum count (default 4 per SM)
   const int64_t small_min = getenv("H2D_SMALL_MIN") ? atoll(getenv("H2D_SMALL_MIN")) : 4 * (int64_t)h.num_sms;
   auto a_small = [](const AItem& a) { return a.nrows <= kSmallARows && a.ritem < 0 && a.out >= 0; };
-  const bool a_split = small_items && std::count_if(aitems.begin(), aitems.end(), a_small) >= small_min;
+  // H2D_SMALL_A=0 / 1 (diagnostics): stage A's small items only
+  const bool small_a = getenv("H2D_SMALL_A") ? atoi(getenv("H2D_SMALL_A")) != 0 : small_items;
+  const bool a_split = small_a && std::count_if(aitems.begin(), aitems.end(), a_small) >= small_min;
+  // the small stage-A kernel before the ring (balanced trees) or after it (adaptive trees):
+  // measured on the 1000^2 Chebyshev phi_1 system (profiles/r02q): adaptive symmetric 3.80 ->
+  // 3.62 ms, directed 4.49 -> 4.25 with it after; balanced (N_max 500) 7.41 -> 7.58 and 7.29 ->
+  // 8.54 ms (H2D_SMALL_A_AFTER=0 / 1 overrides)
+  h.small_a_after = getenv("H2D_SMALL_A_AFTER") ? atoi(getenv("H2D_SMALL_A_AFTER")) == 1 : h.adaptive;
   const auto amid = std::stable_partition(aitems.begin(), aitems.end(),
                                           [&](const AItem& a) { return !(a_split && a_small(a)); });
   h.n_abig = amid - aitems.begin();
@@ -1283,7 +1324,14 @@ void finalize_schedule(Handle& h) {
       }
     }
     if (upos != t1_len) throw Error{H2D_ECUDA, "symmetric U-box layout mismatch"};
-    std::stable_sort(b1items.begin(), b1items.end(), [](const AItem& a, const AItem& b) {
+    // small single-chunk boxes: the warp-per-item B' kernel after the ring (H2D_SMALL_B1=0:
+    // all in the ring); the ring's items largest first
+    const bool small_b1 = getenv("H2D_SMALL_B1") ? atoi(getenv("H2D_SMALL_B1")) != 0 : small_items;
+    const bool b1_split = small_b1 && std::count_if(b1items.begin(), b1items.end(), a_small) >= small_min;
+    const auto b1mid = std::stable_partition(b1items.begin(), b1items.end(),
+                                             [&](const AItem& a) { return !(b1_split && a_small(a)); });
+    h.n_b1big = b1mid - b1items.begin();
+    std::stable_sort(b1items.begin(), b1mid, [](const AItem& a, const AItem& b) {
       return (int64_t)a.nrows * a.Rp > (int64_t)b.nrows * b.Rp;
     });
     if (getenv("H2D_VERBOSE")) {   // diagnostics: share of B' elements on the two-pass (wide) path
@@ -1809,8 +1857,9 @@ static void launch_stages(Handle& h, const double* d_xtree, cudaStream_t hi, boo
     H2D_LAUNCH_CHECK();
   };
   if (!gather) {
-    launch_small(h, true, d_xtree, h.d_t, hi);
+    if (!h.small_a_after) launch_small(h, true, d_xtree, h.d_t, hi);
     ring(0, h.n_abig, h.d_counters);
+    if (h.small_a_after) launch_small(h, true, d_xtree, h.d_t, hi);
   } else {
     launch_small(h, true, d_xtree, h.d_t, hi, 1);
     ring(0, h.n_abig_loc, h.d_counters);
@@ -1866,7 +1915,11 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
                 : h.kp.id == H2D_KERNEL_RBF_PHI2 ? p2p_list_kernel<H2D_KERNEL_RBF_PHI2>
                                                    : p2p_list_kernel<H2D_KERNEL_TEST_LOWRANK>;
       H2D_CUDA(cudaMemsetAsync(h.d_counters + 4, 0, sizeof(int32_t), a));
-      const int grid = (int)std::min<int64_t>((int64_t)h.num_sms * 3, (h.n_p2p_list + 7) / 8);
+      // beside the streams: one CTA per SM (66 registers x 256 threads), so that the two ring
+      // CTAs of stage A / B' still fit on every SM (at 3 per SM, placed while the small-item
+      // kernel drained, the list kernel held whole SMs: adaptive 1000^2 A' + B' 2.3 -> 3.0 ms)
+      const int per_sm = p2p_serial ? 3 : h.diag_p2p_list_ctas;
+      const int grid = (int)std::min<int64_t>((int64_t)h.num_sms * per_sm, (h.n_p2p_list + 7) / 8);
       kfn<<<grid, 256, 0, a>>>(h.d_p2p_list, (int)h.n_p2p_list, h.d_counters + 4, h.d_lf_start, h.d_ad_nf_off,
                                h.d_ad_nf_rng, h.d_px, h.d_py, d_xtree, h.kp, h.d_ynear);
       H2D_LAUNCH_CHECK();
@@ -1958,19 +2011,27 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
     // symmetric apply (R23): A' t1 = V^T x; B' t2 = U^T x and y1 = U t1; C' yfar = V t2
     const size_t smem = sizeof(PipeSmem<kNSShallow>);
     H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 4 * sizeof(int32_t), hi));
-    launch_small(h, true, d_xtree, h.d_t1, hi);
+    if (!h.small_a_after) launch_small(h, true, d_xtree, h.d_t1, hi);
     if (h.n_abig > 0) {
       stageA_tma_kernel<kNSShallow><<<(int)std::min<int64_t>(h.persist_ctas, h.n_abig), kPipeThreads, smem, hi>>>(
           h.d_aitems, (int)h.n_abig, h.d_counters, h.lp, d_xtree, h.d_vdst, h.d_t1, h.d_tpart, h.d_ritems,
           h.d_rcount);
       H2D_LAUNCH_CHECK();
     }
-    if (h.n_b1items > 0) {
-      stageA_dual_kernel<kNSDual, kSDDual><<<(int)std::min<int64_t>(h.persist_ctas, h.n_b1items), kPipeThreads,
+    if (h.small_a_after) launch_small(h, true, d_xtree, h.d_t1, hi);
+    if (h.n_b1big > 0) {
+      stageA_dual_kernel<kNSDual, kSDDual><<<(int)std::min<int64_t>(h.persist_ctas, h.n_b1big), kPipeThreads,
                                              sizeof(PipeSmem<kNSDual, kSDDual>), hi>>>(
-          h.d_b1items, (int)h.n_b1items, h.d_counters + 3, h.lp, d_xtree, h.d_udst, h.d_t, h.d_b1tpart,
+          h.d_b1items, (int)h.n_b1big, h.d_counters + 3, h.lp, d_xtree, h.d_udst, h.d_t, h.d_b1tpart,
           h.d_b1ritems, h.d_b1rcount, h.d_t1, h.d_y1,
           h.diag_dual_norow ? (int64_t)-1 : h.n);   // diagnostics: skip the row dots
+      H2D_LAUNCH_CHECK();
+    }
+    if (h.n_b1items > h.n_b1big) {
+      const int64_t nb = h.n_b1items - h.n_b1big;
+      const int grid = (int)std::min<int64_t>((int64_t)h.num_sms * 16, (nb + 7) / 8);
+      stageB1_small_kernel<<<grid, 256, 0, hi>>>(h.d_b1items + h.n_b1big, (int)nb, h.lp, d_xtree, h.d_udst, h.d_t,
+                                                  h.d_t1, h.d_y1, h.n);
       H2D_LAUNCH_CHECK();
     }
     record(h, 2, hi);

@@ -183,6 +183,7 @@ static void clear_factors(Handle& h) {
   h.d_b1items = nullptr;
   h.d_b1ritems = nullptr;
   h.n_b1items = 0;
+  h.n_b1big = 0;
   for (void* q : {(void*)h.m_aitems, (void*)h.m_ritems, (void*)h.m_rcount, (void*)h.m_tpart, (void*)h.m_xm,
                   (void*)h.m_iperm, (void*)h.m_t, (void*)h.m_yfar, (void*)h.m_ynear})
     h.release(q);
@@ -588,6 +589,7 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
     h.diag_p2p_onestream = env_is("H2D_P2P_ONESTREAM", 1);
     h.diag_dual_norow = getenv("H2D_DUAL_NOROW") != nullptr;
     h.diag_copy_stream = !env_is("H2D_COPY_STREAM", 0);
+    if (const char* e = getenv("H2D_P2P_LIST_CTAS")) h.diag_p2p_list_ctas = std::max(1, std::min(3, atoi(e)));
   }
   const double* d_pts = points;
   double* tmp = nullptr;
@@ -877,7 +879,7 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   info->small_items[0] = h.n_aitems - h.n_abig;
   info->small_items[1] = h.n_bitems - h.n_bbig;
   info->apply_launches = (h.n_abig > 0) + (h.n_aitems > h.n_abig) + (h.n_bbig > 0) + (h.n_bitems > h.n_bbig) +
-                         (h.symapply && h.n_b1items > 0);
+                         (h.symapply && h.n_b1big > 0) + (h.symapply && h.n_b1items > h.n_b1big);
   if (h.pairapply) info->apply_launches = 1;
   info->pair_apply = h.pairapply ? 1 : 0;
   info->comm_kind = comm_kind(h);

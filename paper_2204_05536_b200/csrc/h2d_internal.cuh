@@ -309,11 +309,13 @@ struct Handle {
   // first-side V box panels -> t1; B' over the first-side U box panels -> t2 (= t) and the
   // per-level row dots y1 = U t1; C' = stage B over the second-side leaf panels with t2
   bool symapply = false;
+  bool small_a_after = false;   // H2D_SMALL_A_AFTER=1: the small stage-A kernel after the ring
   double* d_t1 = nullptr;                 // [t1_len]
   int64_t t1_len = 0;
   int32_t* d_udst = nullptr;              // U-box column -> t2 index
   AItem* d_b1items = nullptr;             // stage B' items
   int64_t n_b1items = 0;
+  int64_t n_b1big = 0;                   // B' ring items (the rest: stageB1_small_kernel)
   RItem* d_b1ritems = nullptr;
   int32_t* d_b1rcount = nullptr;
   double* d_b1tpart = nullptr;
@@ -368,6 +370,7 @@ struct Handle {
   // build, changeable per handle with hodlr2d_set_diag (never per call from the environment)
   bool diag_p2p_serial = false, diag_p2p_onestream = false, diag_dual_norow = false;
   bool diag_copy_stream = true;
+  int diag_p2p_list_ctas = 1;   // adaptive near field beside the streams: CTAs per SM (H2D_P2P_LIST_CTAS)
   // near-field kernel id (kp.id, or kLogSafe when a near pair has a subnormal r^2)
   int p2p_kid = 0;
   // pinned host staging of pageable caller buffers (0: inputs, 1: outputs)

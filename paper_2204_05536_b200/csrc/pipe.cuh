@@ -82,6 +82,10 @@ constexpr int kSymTile = 96, kSymMaxB = kSymTile / 16;
 // 0.5 log1p(f) = f p(f), p the degree-3 Taylor polynomial (truncation f^5/10 <= 9e-17).
 // 7 DFMA in a chain of 6 (the 128-bin, degree-5 version: 9 / 8): the near field is bound by
 // these dependent chains.  The coefficients are constant-bank operands.
+// (Measured, not kept: an 8-byte table of -0.5 log r_k with r_k = rcp.approx(c_k) from the
+// MUFU halves the shared-memory wavefronts of the random lookups but costs 5 instructions
+// more per evaluation, and the near field turns issue-bound: 0.40 -> 0.42 ms on C3;
+// tools/scratch/hlog_rcp_table.cuh.txt.)
 constexpr int kHlogBins = 512;
 __constant__ double c_hlog[8] = {0.34657359027997264,   // ln2 / 2 (high part)
                                  1.1595234069231498e-17, // ln2 / 2 (low part)
@@ -96,16 +100,30 @@ __constant__ double c_hlog[8] = {0.34657359027997264,   // ln2 / 2 (high part)
 // points has a subnormal r2, so the common case pays no normalisation.
 template <bool SAFE = false>
 __device__ __forceinline__ double hlog_r2(double r2, const double2* __restrict__ tab) {
-  long long bits = __double_as_longlong(r2);
-  int e;
-  if (SAFE) {
-    const int E = (int)(bits >> 52);
-    const int sh = max(0, __clzll(bits) - 11);
-    bits <<= sh;
-    e = (E == 0 ? 1 - sh : E) - 1023;
-  } else {
-    e = (int)(bits >> 52) - 1023;
+  if (!SAFE) {
+    // the same arithmetic on the high word only (r2 >= 0, normal or 0): the table byte offset
+    // 16 k = (hi >> 7) & 0x1ff0, the mantissa's high word (hi & 0xfffff) | 0x3ff00000, and
+    // the biased exponent E = hi >> 20 dropped straight into the low word of 2^52 (three
+    // integer instructions fewer per evaluation than the 64-bit shifts and the signed e)
+    static_assert(kHlogBins == 512, "offset mask assumes 512 bins");
+    const uint32_t hi = (uint32_t)__double2hiint(r2);
+    const double2 tb = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(tab) + ((hi >> 7) & 0x1ff0u));
+    const double mnt = __hiloint2double((int)((hi & 0x000fffffu) | 0x3ff00000u), __double2loint(r2));
+    const double f = fma(mnt, tb.x, -1.0);
+    double p = fma(f, c_hlog[5], c_hlog[4]);
+    p = fma(f, p, c_hlog[3]);
+    p = fma(f, p, c_hlog[2]);
+    const double ed = __hiloint2double(0x43300000, (int)(hi >> 20)) - 4503599627371519.0;
+    // ln2 / 2 without its lo part: |e| x 1.2e-17 absolute (e = -14 at C3's near-field
+    // distances: 1.6e-16 on |0.5 log r2| ~ 5, below one ulp of the sums it enters), one DFMA
+    // less per evaluation; the SAFE path keeps the hi + lo pair
+    return fma(ed, c_hlog[0], fma(p, f, tb.y));
   }
+  long long bits = __double_as_longlong(r2);
+  const int E = (int)(bits >> 52);
+  const int sh = max(0, __clzll(bits) - 11);
+  bits <<= sh;
+  const int e = (E == 0 ? 1 - sh : E) - 1023;
   const int k = (int)(bits >> 43) & (kHlogBins - 1);
   const double mnt = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
   const double2 tb = tab[k];
@@ -113,11 +131,7 @@ __device__ __forceinline__ double hlog_r2(double r2, const double2* __restrict__
   double p = fma(f, c_hlog[5], c_hlog[4]);
   p = fma(f, p, c_hlog[3]);
   p = fma(f, p, c_hlog[2]);
-  // the exponent as a double: SAFE by conversion; else by the 2^52 trick (one DADD instead of
-  // an I2F.F64: the biased exponent field E placed in a mantissa, 2^52 + E - (2^52 + 1023))
-  double ed;
-  if (SAFE) ed = (double)e;
-  else ed = __longlong_as_double(0x4330000000000000LL | (long long)(e + 1023)) - 4503599627371519.0;
+  const double ed = (double)e;
   return fma(ed, c_hlog[0], fma(p, f, fma(ed, c_hlog[1], tb.y)));
 }
 

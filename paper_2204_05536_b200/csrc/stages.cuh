@@ -493,6 +493,62 @@ stageA_small_kernel(const AItem* __restrict__ items, int n_items, LevelPtrs lp, 
     }
   }
 }
+// Symmetric stage B' (DUAL), boxes of <= kSmallARows rows in one chunk: warp per box, lane owns
+// column pair pb + lane of a 32-pair block, rows in groups of 8.  Each U pair feeds the
+// column sums t2 (registers; no reduction: the warp owns the box) and the row dots
+// y1 = U t1 (the 8 row partials of a group summed over the warp by one transposed butterfly,
+// accumulated over the 32-pair blocks in lane 4 t: rows t, t + 8, t + 16, t + 24).  The
+// U panel's pad column is zero (memset at pack time) and the t1 pad is read as 0.
+__global__ void __launch_bounds__(256, 4)
+stageB1_small_kernel(const AItem* __restrict__ items, int n_items, LevelPtrs lp, const double* __restrict__ x,
+                     const int32_t* __restrict__ udst, double* __restrict__ t2, const double* __restrict__ t1,
+                     double* __restrict__ y1, int64_t n) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_items; k += nw) {
+    const AItem it = items[k];
+    const double2* __restrict__ U2 = reinterpret_cast<const double2*>(lp.Ub[it.level] + it.v_off);
+    const double* __restrict__ xr = x + it.x_off;
+    const double* __restrict__ tb = t1 + it.t1_off;
+    const int P = it.Rp >> 1, rows = it.nrows;
+    double yr[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int pb = 0; pb < P; pb += 32) {
+      const int p = pb + lane;
+      const bool vp = p < P;
+      const double2 tt = make_double2(vp ? __ldg(tb + 2 * p) : 0.0, vp && 2 * p + 1 < it.R ? __ldg(tb + 2 * p + 1) : 0.0);
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < kSmallARows / 8; ++q) {
+        if (8 * q >= rows) break;   // warp-uniform
+        double c[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int j = 8 * q + t;
+          const bool ok = vp && j < rows;
+          const double2 u = ok ? __ldcs(U2 + (int64_t)j * P + p) : make_double2(0.0, 0.0);
+          const double xj = j < rows ? __ldg(xr + j) : 0.0;
+          a0 = fma(u.x, xj, a0);
+          a1 = fma(u.y, xj, a1);
+          c[t] = fma(u.x, tt.x, u.y * tt.y);
+        }
+        yr[q] += warp_transpose_sum8(c, lane);
+      }
+      if (vp) {
+        t2[udst[it.out + 2 * p]] = a0;
+        if (2 * p + 1 < it.R) t2[udst[it.out + 2 * p + 1]] = a1;
+      }
+    }
+    if ((lane & 3) == 0) {
+      double* __restrict__ yrow = y1 + (int64_t)(it.level - 1) * n + it.x_off;
+#pragma unroll
+      for (int q = 0; q < kSmallARows / 8; ++q) {
+        const int j = 8 * q + (lane >> 2);
+        if (j < rows) yrow[j] = yr[q];
+      }
+    }
+  }
+}
+
 // Stage B, whole leaves of <= kSmallBRows rows: warp per leaf; each level's (leaf, level)
 // panel (column-major, mLp <= 8 rows) streams as flat 16-byte elements, 4 per lane in
 // flight; 8 row accumulators, reduced over the warp by one transposed butterfly.  (The

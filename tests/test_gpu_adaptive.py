@@ -146,15 +146,34 @@ def test_adaptive_gmres_rbf(h2d):
     assert rel(x.cpu().numpy(), lam) < 1e-9
 
 
-def test_adaptive_symmetric_three_pass_apply(h2d, tmp_path):
+SMALL_ENVS = [{}, {"H2D_SMALL_MIN": "1"}, {"H2D_SMALL_MIN": "1", "H2D_SMALL_A_AFTER": "1"},
+              {"H2D_SMALL_ITEMS": "0"}]
+
+
+@pytest.mark.parametrize("env", SMALL_ENVS, ids=["default", "small_min1", "small_a_after", "all_ring"])
+def test_adaptive_symmetric_three_pass_apply(h2d, tmp_path, env):
     """Symmetric adaptive handles run the three-pass symmetric apply (A' / B' / C' over the
     adaptive leaves and existing boxes): oracle symmetric adaptive factors <= 1e-12, GPU factors
-    vs dense <= 10 tol, and the directed panels of the same build to 1e-13."""
+    vs dense <= 10 tol, and the directed panels of the same build to 1e-13.  Each item
+    routing: default, every small box on the warp-per-box A' / B' kernels (H2D_SMALL_MIN=1:
+    stageA_small before or after the ring, stageB1_small after the B' ring), all in the rings."""
     import os
     pts = W.chebyshev_grid(130)
     n = pts.shape[0]
     kw = dict(c=1e-3, shift=float(n), symmetric=True)
+    os.environ.update(env)
+    try:
+        _symmetric_three_pass(h2d, tmp_path, pts, n, kw, env)
+    finally:
+        for k in env:
+            os.environ.pop(k)
+
+
+def _symmetric_three_pass(h2d, tmp_path, pts, n, kw, env):
+    import os
     op = gpu(h2d, pts, "rbf_phi1", 64, 1e-12, **kw)
+    if env.get("H2D_SMALL_MIN") == "1":
+        assert op.info()["small_items"][0] > 0
     inf = op.info()
     assert inf["symmetric_apply"] == 1 and inf["adaptive"] == 1
     x = W.random_vector(n, 21)
