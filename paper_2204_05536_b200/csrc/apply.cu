@@ -39,7 +39,11 @@ constexpr int kT1Max = kT1Smem;      // symmetric stage B': widest first-side pa
 // stage B' ring: 2 x 44 KB slots.  The fused column-sum + row-dot pass is issue-bound, not
 // latency-bound (the second CTA on the SM hides the copy latency), so fewer, larger stages
 // win by amortising the per-stage overhead: A'+B' 2.20 ms (5 x 16 KB) -> 1.76 ms (C3).
-constexpr int kNSDual = 2, kSDDual = 5632;   // (4 x 2816 measured slower: C3 symmetric 406 -> 390 / s)
+#ifndef H2D_NS_DUAL
+#define H2D_NS_DUAL 2
+#define H2D_SD_DUAL 5632
+#endif
+constexpr int kNSDual = H2D_NS_DUAL, kSDDual = H2D_SD_DUAL;   // (4 x 2816 measured slower: C3 symmetric 406 -> 390 / s)
 
 struct UCopyItem {
   const double* src;   // column-major, leading dimension ld_src
