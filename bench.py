@@ -390,9 +390,29 @@ def run_ours(args, cfg):
             op.matvec_raw(xh.data_ptr(), yh.data_ptr(), h2d.ORDER_ORIGINAL)
         e1.record(stream)
         torch.cuda.synchronize()
-        e2e = {"value": 1e3 * ke / e0.elapsed_time(e1), "unit": "matvecs/s",
+        sync_value = 1e3 * ke / e0.elapsed_time(e1)
+        # the headline e2e: hodlr2d_matvec_async, fresh pinned x per step (the device run's
+        # vectors), y into two alternating pinned buffers; upload of step k + 1 and download of
+        # step k - 1 overlap step k's kernels (two copy-engine streams, library staging slots).
+        # Host wall clock from a synchronised start to hodlr2d_wait: every copy is inside.
+        xhs = [xs[k % len(xs)].cpu().pin_memory() for k in range(min(len(xs), 4))]
+        yhs = [torch.empty(cfg.n, dtype=torch.float64).pin_memory() for _ in range(2)]
+        for k in range(4):
+            op.matvec_async_raw(xhs[k % len(xhs)].data_ptr(), yhs[k % 2].data_ptr(), h2d.ORDER_ORIGINAL)
+        op.wait()
+        torch.cuda.synchronize()
+        ka = max(20, args.steps)
+        t0 = time.perf_counter()
+        for k in range(ka):
+            op.matvec_async_raw(xhs[k % len(xhs)].data_ptr(), yhs[k % 2].data_ptr(), h2d.ORDER_ORIGINAL)
+        op.wait()
+        ta = time.perf_counter() - t0
+        e2e = {"value": ka / ta, "unit": "matvecs/s",
                "h2d_bytes_per_step": 8 * cfg.n, "d2h_bytes_per_step": 8 * cfg.n,
-               "buffers": "pinned host (torch pin_memory)"}
+               "buffers": "pinned host (torch pin_memory), hodlr2d_matvec_async pipeline",
+               "timing": f"host wall clock over {ka} steps, synchronised start, ends at hodlr2d_wait",
+               "sync_calls": {"value": sync_value, "unit": "matvecs/s",
+                              "timing": "hodlr2d_matvec_ex per step (returns after y is on the host), CUDA events"}}
         # the same with pageable host buffers (numpy): the library stages them through its
         # own pinned buffers (multi-threaded host copies)
         xp = xh.numpy().copy()
@@ -654,8 +674,21 @@ def sub_config(h2d, name, args, stream):
         op.matvec_raw(xh.data_ptr(), yh.data_ptr(), h2d.ORDER_ORIGINAL)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e = {"value": 1e3 * ke / e0.elapsed_time(e1), "unit": "matvecs/s",
-           "h2d_bytes_per_step": 8 * cfg.n, "d2h_bytes_per_step": 8 * cfg.n}
+    sync_value = 1e3 * ke / e0.elapsed_time(e1)
+    xhs = [xs[k % nx].cpu().pin_memory() for k in range(min(nx, 2))]
+    yhs = [torch.empty(cfg.n, dtype=torch.float64).pin_memory() for _ in range(2)]
+    for k in range(2):
+        op.matvec_async_raw(xhs[k % len(xhs)].data_ptr(), yhs[k % 2].data_ptr(), h2d.ORDER_ORIGINAL)
+    op.wait()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(ke):
+        op.matvec_async_raw(xhs[k % len(xhs)].data_ptr(), yhs[k % 2].data_ptr(), h2d.ORDER_ORIGINAL)
+    op.wait()
+    e2e = {"value": ke / (time.perf_counter() - t0), "unit": "matvecs/s",
+           "h2d_bytes_per_step": 8 * cfg.n, "d2h_bytes_per_step": 8 * cfg.n,
+           "buffers": "pinned host, hodlr2d_matvec_async pipeline (host wall clock)",
+           "sync_calls": {"value": sync_value, "unit": "matvecs/s"}}
     out = {"value": 1e3 / ms, "unit": "matvecs/s", "ms_per_step": ms, "steps": steps,
            "config": config_dict(cfg, 1), "points_matvecs_per_s": 1e3 / ms * cfg.n,
            "build_seconds": round(build_s, 3),

@@ -207,6 +207,23 @@ int hodlr2d_matvec(hodlr2d_t h, const double* x, double* y);
  * hodlr2d_matvec (single-rank handles only). */
 int hodlr2d_matvec_ex(hodlr2d_t h, const double* x, double* y, int order);
 
+/* Stream-ordered y = A x for a sequence of matvecs on host buffers (the same operation as
+ * hodlr2d_matvec_ex, Alg. 2 of the paper): enqueues the host -> device copy of x,
+ * the matvec and the device -> host copy of y, and RETURNS BEFORE THEY RUN.  x and y must be
+ * pinned host memory (cudaMallocHost / cudaHostRegister / torch pin_memory) or device
+ * memory; order = H2D_ORDER_ORIGINAL, TREE or GATHERED with the lengths of hodlr2d_matvec_ex.
+ * The copies run on two library-owned streams (one per copy engine) and the library keeps two
+ * device staging slots, so call k + 1's upload and call k - 1's download overlap call k's
+ * kernels.  Ownership: the caller must not modify x or read y until hodlr2d_wait(h) returns
+ * (which waits for every call enqueued so far); the library owns the staging buffers.
+ * Results are bitwise those of hodlr2d_matvec_ex.  Errors: H2D_EINVAL for pageable host
+ * buffers, a null pointer, LOCAL order or a bad order/handle combination (nothing is
+ * enqueued); asynchronous CUDA errors surface from hodlr2d_wait as H2D_ECUDA. */
+int hodlr2d_matvec_async(hodlr2d_t h, const double* x, double* y, int order);
+
+/* Block until every hodlr2d_matvec_async call on h has completed (its y written). */
+int hodlr2d_wait(hodlr2d_t h);
+
 /* Y = A X for nrhs vectors at once (NEXT N2; the paper applies its matvec to ten input
  * vectors).  Vector k is X + k * len_x and Y + k * len_y; order =
  * H2D_ORDER_ORIGINAL (single-rank handles, len_x = len_y = N), H2D_ORDER_TREE (x in TREE

@@ -44,7 +44,8 @@ ABI_FUNCTIONS = (
     "hodlr2d_num_blocks", "hodlr2d_copy_ranks", "hodlr2d_copy_block", "hodlr2d_load_factors",
     "hodlr2d_save_factors", "hodlr2d_stage_times", "hodlr2d_set_timing", "hodlr2d_destroy",
     "hodlr2d_last_error", "hodlr2d_partition", "hodlr2d_gmres", "hodlr2d_matvec_multi", "hodlr2d_leaf_costs",
-    "hodlr2d_comm_unique_id", "hodlr2d_set_diag", "hodlr2d_copy_leaves",
+    "hodlr2d_comm_unique_id", "hodlr2d_set_diag", "hodlr2d_copy_leaves", "hodlr2d_matvec_async",
+    "hodlr2d_wait",
 )
 
 
@@ -117,6 +118,8 @@ def lib() -> C.CDLL:
             L.hodlr2d_build_ex.argtypes = [vp, i64, i, i, d, C.POINTER(Options), C.POINTER(vp)]
             L.hodlr2d_matvec.argtypes = [vp, vp, vp]
             L.hodlr2d_matvec_ex.argtypes = [vp, vp, vp, i]
+            L.hodlr2d_matvec_async.argtypes = [vp, vp, vp, i]
+            L.hodlr2d_wait.argtypes = [vp]
             L.hodlr2d_get_info.argtypes = [vp, C.POINTER(Info)]
             L.hodlr2d_copy_tree.argtypes = [vp, vp, vp]
             L.hodlr2d_copy_lists.argtypes = [vp, i, vp, vp]
@@ -413,6 +416,25 @@ class Hodlr2d:
 
     def matvec_raw(self, x_ptr: int, y_ptr: int, order: int = ORDER_ORIGINAL):
         _check(lib().hodlr2d_matvec_ex(self._h, x_ptr, y_ptr, order))
+
+    def matvec_async(self, x, y, order="original"):
+        """hodlr2d_matvec_async: enqueue y = A x on pinned host (or device) tensors and return;
+        x must stay unmodified and y unread until wait()."""
+        o = ORDERS[order] if isinstance(order, str) else order
+        lx, ly = self._lens(o)
+        self._check_vec(x, lx, "x")
+        self._check_vec(y, ly, "y")
+        for t, nm in ((x, "x"), (y, "y")):
+            if t.device.type == "cpu" and not t.is_pinned():
+                raise ValueError(f"matvec_async: {nm} must be pinned host or device memory")
+        _check(lib().hodlr2d_matvec_async(self._h, _ptr(x), _ptr(y), o))
+
+    def matvec_async_raw(self, x_ptr: int, y_ptr: int, order: int = ORDER_ORIGINAL):
+        _check(lib().hodlr2d_matvec_async(self._h, x_ptr, y_ptr, order))
+
+    def wait(self):
+        """hodlr2d_wait: every matvec_async call so far has completed."""
+        _check(lib().hodlr2d_wait(self._h))
 
     # -------------------------------------------------------------- inspection
     def leaf_costs(self):

@@ -43,7 +43,7 @@ constexpr int kT1Max = kT1Smem;      // symmetric stage B': widest first-side pa
 #define H2D_NS_DUAL 2
 #define H2D_SD_DUAL 5632
 #endif
-constexpr int kNSDual = H2D_NS_DUAL, kSDDual = H2D_SD_DUAL;   // (4 x 2816 measured slower: C3 symmetric 406 -> 390 / s)
+constexpr int kNSDual = H2D_NS_DUAL, kSDDual = H2D_SD_DUAL;   // (4 x 2816 / 3 x 4096 / 3 x 3584 measured slower: C3 symmetric 406 -> 390 / 402 / 400 per s)
 
 struct UCopyItem {
   const double* src;   // column-major, leading dimension ld_src

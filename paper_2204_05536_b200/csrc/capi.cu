@@ -51,6 +51,14 @@ Handle::~Handle() {
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (ev_copy0) cudaEventDestroy(ev_copy0);
   if (ev_copy1) cudaEventDestroy(ev_copy1);
+  if (as_h2d) cudaStreamSynchronize(as_h2d);
+  if (as_d2h) cudaStreamSynchronize(as_d2h);
+  if (as_h2d) cudaStreamDestroy(as_h2d);
+  if (as_d2h) cudaStreamDestroy(as_d2h);
+  for (int k = 0; k < 2; ++k) {
+    for (cudaEvent_t e : {as_xin[k], as_xfree[k], as_ydone[k], as_yfree[k]})
+      if (e) cudaEventDestroy(e);
+  }
 }
 
 static double now_s() {
@@ -384,6 +392,78 @@ static void do_matvec(Handle& h, const double* x, double* y, int order) {
   (void)s;
 }
 
+// Stream-ordered matvec on pinned host (or device) buffers: H2D of x on as_h2d, the matvec on
+// the work stream, D2H of y on as_d2h, each ordered by events; returns once enqueued.  Device
+// staging slot k & 1: call k's H2D waits until call k - 2's kernels no longer read its x
+// slot, its kernels wait until call k - 2's D2H has drained its y slot.
+static void matvec_async(Handle& h, const double* x, double* y, int order) {
+  if (order != H2D_ORDER_ORIGINAL && order != H2D_ORDER_TREE && order != H2D_ORDER_GATHERED)
+    throw Error{H2D_EINVAL, "async matvec: order must be ORIGINAL, TREE or GATHERED"};
+  if (!x || !y) throw Error{H2D_EINVAL, "null x or y"};
+  if (order == H2D_ORDER_ORIGINAL && (h.row_begin != 0 || h.row_end != h.n))
+    throw Error{H2D_EINVAL, "ORIGINAL order needs a single-rank (full-range) handle"};
+  if (order == H2D_ORDER_GATHERED && h.rank_rows.empty())
+    throw Error{H2D_EINVAL, "GATHERED order needs a world/rank partition"};
+  const bool xdev = is_device_ptr(x), ydev = is_device_ptr(y);
+  if ((!xdev && !is_pinned_host(x)) || (!ydev && !is_pinned_host(y)))
+    throw Error{H2D_EINVAL, "async matvec: x and y must be pinned host or device memory"};
+  const int64_t xlen = order == H2D_ORDER_GATHERED ? h.gather_stride * h.opts.world : h.n;
+  const int64_t ylen = order == H2D_ORDER_ORIGINAL ? h.n : (h.row_end - h.row_begin);
+  if (!h.as_h2d) {
+    H2D_CUDA(cudaStreamCreateWithFlags(&h.as_h2d, cudaStreamNonBlocking));
+    H2D_CUDA(cudaStreamCreateWithFlags(&h.as_d2h, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k)
+      for (cudaEvent_t* e : {&h.as_xin[k], &h.as_xfree[k], &h.as_ydone[k], &h.as_yfree[k]})
+        H2D_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    // the first calls must not overtake work already queued on the caller's stream
+    H2D_CUDA(cudaEventRecord(h.as_xfree[0], h.stream));
+    H2D_CUDA(cudaEventRecord(h.as_xfree[1], h.stream));
+  }
+  const int sl = (int)(h.as_calls & 1);
+  cudaStream_t s = h.stream;
+  const double* xin = x;
+  if (!xdev) {
+    if (!h.as_x[sl]) h.as_x[sl] = h.alloc<double>(std::max<int64_t>(h.n, h.gather_stride * h.opts.world));
+    H2D_CUDA(cudaStreamWaitEvent(h.as_h2d, h.as_xfree[sl], 0));
+    H2D_CUDA(cudaMemcpyAsync(h.as_x[sl], x, xlen * sizeof(double), cudaMemcpyHostToDevice, h.as_h2d));
+    H2D_CUDA(cudaEventRecord(h.as_xin[sl], h.as_h2d));
+    H2D_CUDA(cudaStreamWaitEvent(s, h.as_xin[sl], 0));
+    xin = h.as_x[sl];
+  }
+  double* yout = y;
+  if (!ydev) {
+    if (!h.as_y[sl]) h.as_y[sl] = h.alloc<double>(h.n);
+    H2D_CUDA(cudaStreamWaitEvent(s, h.as_yfree[sl], 0));
+    yout = h.as_y[sl];
+  }
+  begin_matvec_timing(h);
+  const double* xt = xin;
+  if (order == H2D_ORDER_ORIGINAL) {
+    permute_in(h, xin, h.d_xtree);
+    xt = h.d_xtree;
+  } else if (order == H2D_ORDER_GATHERED) {
+    unpad_gathered(h, xin, h.d_xtree);
+    xt = h.d_xtree;
+  }
+  mark_after_input(h);
+  matvec_tree(h, xt, yout, order == H2D_ORDER_ORIGINAL ? H2D_ORDER_ORIGINAL : H2D_ORDER_TREE, h.row_begin, false);
+  if (h.timing) h.timed_count++;
+  if (!xdev) H2D_CUDA(cudaEventRecord(h.as_xfree[sl], s));   // (TREE order reads x throughout)
+  if (!ydev) {
+    H2D_CUDA(cudaEventRecord(h.as_ydone[sl], s));
+    H2D_CUDA(cudaStreamWaitEvent(h.as_d2h, h.as_ydone[sl], 0));
+    H2D_CUDA(cudaMemcpyAsync(y, yout, ylen * sizeof(double), cudaMemcpyDeviceToHost, h.as_d2h));
+    H2D_CUDA(cudaEventRecord(h.as_yfree[sl], h.as_d2h));
+  }
+  ++h.as_calls;
+}
+
+static void async_wait(Handle& h) {
+  if (h.as_h2d) H2D_CUDA(cudaStreamSynchronize(h.as_h2d));
+  H2D_CUDA(cudaStreamSynchronize(h.stream));
+  if (h.as_d2h) H2D_CUDA(cudaStreamSynchronize(h.as_d2h));
+}
+
 // ---------------------------------------------------------------- factor interchange (R11)
 struct FileHeader {
   int64_t N;
@@ -676,6 +756,22 @@ int hodlr2d_matvec_ex(hodlr2d_t H, const double* x, double* y, int order) {
   H2D_TRY
   if (!H) throw Error{H2D_EINVAL, "null handle"};
   do_matvec(H->h, x, y, order);
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_matvec_async(hodlr2d_t H, const double* x, double* y, int order) {
+  H2D_TRY
+  if (!H) throw Error{H2D_EINVAL, "null handle"};
+  matvec_async(H->h, x, y, order);
+  return H2D_OK;
+  H2D_CATCH
+}
+
+int hodlr2d_wait(hodlr2d_t H) {
+  H2D_TRY
+  if (!H) throw Error{H2D_EINVAL, "null handle"};
+  async_wait(H->h);
   return H2D_OK;
   H2D_CATCH
 }

@@ -361,6 +361,15 @@ struct Handle {
   cudaStream_t aux_stream = nullptr;      // P2P (low priority), concurrent with A and B
   cudaStream_t copy_stream = nullptr;     // host <-> device copies of host-pointer calls
   cudaEvent_t ev_copy0 = nullptr, ev_copy1 = nullptr;
+  // stream-ordered host-buffer matvecs (hodlr2d_matvec_async): H2D and D2H on their own
+  // streams (the two copy engines), double-buffered device x / y so call k + 1's H2D and
+  // call k - 1's D2H run under call k's kernels
+  cudaStream_t as_h2d = nullptr, as_d2h = nullptr;
+  double* as_x[2] = {nullptr, nullptr};
+  double* as_y[2] = {nullptr, nullptr};
+  cudaEvent_t as_xin[2] = {nullptr, nullptr}, as_xfree[2] = {nullptr, nullptr};
+  cudaEvent_t as_ydone[2] = {nullptr, nullptr}, as_yfree[2] = {nullptr, nullptr};
+  int64_t as_calls = 0;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_far = nullptr;
   // P2P classes (generic CTA leaves, warp leaves of 3 / 2 rows per lane) fork from aux_stream
   // onto their own low-priority streams so their under-filled grids overlap
