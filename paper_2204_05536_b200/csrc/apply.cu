@@ -1265,6 +1265,7 @@ void finalize_schedule(Handle& h) {
   // 3.62 ms, directed 4.49 -> 4.25 with it after; balanced (N_max 500) 7.41 -> 7.58 and 7.29 ->
   // 8.54 ms (H2D_SMALL_A_AFTER=0 / 1 overrides)
   h.small_a_after = getenv("H2D_SMALL_A_AFTER") ? atoi(getenv("H2D_SMALL_A_AFTER")) == 1 : h.adaptive;
+  h.p2p_after_b1 = getenv("H2D_P2P_AFTER_B1") && atoi(getenv("H2D_P2P_AFTER_B1")) == 1;
   const auto amid = std::stable_partition(aitems.begin(), aitems.end(),
                                           [&](const AItem& a) { return !(a_split && a_small(a)); });
   h.n_abig = amid - aitems.begin();
@@ -2038,6 +2039,10 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
                                                   h.d_t1, h.d_y1, h.n);
       H2D_LAUNCH_CHECK();
     }
+    if (h.p2p_after_b1) {   // diagnostics: the near field only beside C'
+      if (!h.ev_b1) H2D_CUDA(cudaEventCreateWithFlags(&h.ev_b1, cudaEventDisableTiming));
+      H2D_CUDA(cudaEventRecord(h.ev_b1, hi));
+    }
     record(h, 2, hi);
     launch_stageB(h, hi);
   } else {
@@ -2049,6 +2054,7 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
   record(h, 3, hi);
   H2D_CUDA(cudaEventRecord(h.ev_far, hi));
   if (xready) H2D_CUDA(cudaStreamWaitEvent(a, xready, 0));   // the near field reads remote x
+  if (h.symapply && h.p2p_after_b1 && !p2p_serial) H2D_CUDA(cudaStreamWaitEvent(a, h.ev_b1, 0));
   if (!p2p_serial) p2p();   // after stage A's launch: its CTAs are placed first
   H2D_CUDA(cudaStreamWaitEvent(s, h.ev_far, 0));
   H2D_CUDA(cudaStreamWaitEvent(s, h.ev_join, 0));

@@ -49,6 +49,7 @@ Handle::~Handle() {
   if (ev_p2p_fork) cudaEventDestroy(ev_p2p_fork);
   if (hi_stream) cudaStreamDestroy(hi_stream);
   if (copy_stream) cudaStreamDestroy(copy_stream);
+  if (ev_b1) cudaEventDestroy(ev_b1);
   if (ev_copy0) cudaEventDestroy(ev_copy0);
   if (ev_copy1) cudaEventDestroy(ev_copy1);
   if (as_h2d) cudaStreamSynchronize(as_h2d);

@@ -309,7 +309,9 @@ struct Handle {
   // first-side V box panels -> t1; B' over the first-side U box panels -> t2 (= t) and the
   // per-level row dots y1 = U t1; C' = stage B over the second-side leaf panels with t2
   bool symapply = false;
-  bool small_a_after = false;   // H2D_SMALL_A_AFTER=1: the small stage-A kernel after the ring
+  bool small_a_after = false;
+  bool p2p_after_b1 = false;    // H2D_P2P_AFTER_B1=1: symmetric near field waits for B' (beside C' only)
+  cudaEvent_t ev_b1 = nullptr;   // H2D_SMALL_A_AFTER=1: the small stage-A kernel after the ring
   double* d_t1 = nullptr;                 // [t1_len]
   int64_t t1_len = 0;
   int32_t* d_udst = nullptr;              // U-box column -> t2 index

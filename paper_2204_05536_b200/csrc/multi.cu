@@ -30,6 +30,18 @@ constexpr int kBRowsMax = 224;       // stage-B item rows (apply.cu kBRows)
 constexpr int kNSMulti = 2, kSDMulti = 5632, kSVMulti = 704;   // ring: stages, doubles, vector values
 constexpr int kSDMulti16 = 4096, kSVMulti16 = 1024;              // 16 vectors: 64 rows x 64 columns
 
+// 16-vector records (x_m, t_m: 128 bytes each) are stored swizzled: vector v of the record
+// at address A sits in slot v ^ 8 * ((A >> 7) & 1), i.e. the two 8-vector halves swap in
+// every other record.  The DMMA B fragments read vector gq (and 8 + gq) of 4 consecutive
+// records (lanes tq): unswizzled all 32 lanes hit 8 bank pairs (4-way conflicts, ncu r02x:
+// 68 % of stage B's shared wavefronts were replays); swizzled each bank pair serves 2 lanes.
+// Every writer and reader derives the swap from the record's own address (global) or from
+// the parity of the stage's first record passed in the stage header (shared memory copies).
+template <int NR>
+__device__ __forceinline__ int rec_swz(const double* rec) {
+  return NR == 16 ? (int)((reinterpret_cast<uintptr_t>(rec) >> 7) & 1) << 3 : 0;
+}
+
 // ---------------------------------------------------------------- stage A (multi)
 // Stage header: a = W (tile width), b = Wp (row stride of the stage, W rounded up to even),
 // c = out, d = ritem.
@@ -70,6 +82,7 @@ __device__ void mA_producer(PipeSmem<NS, SD, SV>& S, const AItem* __restrict__ i
         h.b = Wp;
         h.c = it.out;
         h.d = it.ritem;
+        h.f = done ? 0 : rec_swz<NR>(xm + (it.x_off + r0) * NR);
         const uint32_t bytes = (uint32_t)rows * (uint32_t)Wp * 8u, xbytes = (uint32_t)rows * NR * 8u;
         mbar_arrive_expect_tx(&S.full[stage], bytes + xbytes);
         if (bytes && contiguous) bulk_g2s(S.ring[stage], V + (int64_t)r0 * it.Rp, bytes, &S.full[stage], pol);
@@ -184,7 +197,8 @@ __device__ void mA_consumers(PipeSmem<NS, SD, SV>& S, const int32_t* __restrict_
             a1 += __ldcg(pp + (c + 1) * cs);
           }
           if (c < ri.nchunks) a0 += __ldcg(pp + c * cs);
-          tm[(int64_t)vdst[ri.vpos + q] * NR + k] = a0 + a1;
+          double* rec = tm + (int64_t)vdst[ri.vpos + q] * NR;
+          rec[k ^ rec_swz<NR>(rec)] = a0 + a1;
         }
         if (tid == 0) rcount[h.d] = 0;
       }
@@ -338,7 +352,8 @@ __device__ void mA_consumers_dmma(PipeSmem<NS, SD, SV>& S, const int32_t* __rest
             a1 += __ldcg(pp + (c + 1) * cs);
           }
           if (c < ri.nchunks) a0 += __ldcg(pp + c * cs);
-          tm[(int64_t)vdst[ri.vpos + q] * NR + k] = a0 + a1;
+          double* rec = tm + (int64_t)vdst[ri.vpos + q] * NR;
+          rec[k ^ rec_swz<NR>(rec)] = a0 + a1;
         }
         if (tid == 0) rcount[h.d] = 0;
       }
@@ -473,14 +488,16 @@ constexpr int kMaxMTK16 = 6;   // (8: 80-register cap spills, 4.39 vs 3.32 ms)
 template <int CNT>
 __device__ __forceinline__ void colsum16_mtiles(double (&d)[kMaxMTA16][2][2], const double* __restrict__ sv,
                                                 const double* __restrict__ sx, int rows, int Wp, int w, int gq,
-                                                int tq) {
+                                                int tq, int swz0) {
   int cidx[CNT];
 #pragma unroll
   for (int i = 0; i < CNT; ++i) cidx[i] = (w + kConsWarps * i) * 8 + gq;
+  // record r's swap is swz0 ^ 8 (r & 1); r = k0 + tq with k0 a multiple of 4
+  const int o0 = gq ^ swz0 ^ ((tq & 1) << 3);
   int k0 = 0;
   for (; k0 + 4 <= rows; k0 += 4) {
     const int r = k0 + tq;
-    const double b0 = sx[r * 16 + gq], b1 = sx[r * 16 + 8 + gq];
+    const double b0 = sx[r * 16 + o0], b1 = sx[r * 16 + (o0 ^ 8)];
 #pragma unroll
     for (int i = 0; i < CNT; ++i) {
       const double a = cidx[i] < Wp ? sv[r * Wp + cidx[i]] : 0.0;
@@ -491,7 +508,7 @@ __device__ __forceinline__ void colsum16_mtiles(double (&d)[kMaxMTA16][2][2], co
   if (k0 < rows) {
     const int r = k0 + tq;
     const bool rv = r < rows;
-    const double b0 = rv ? sx[r * 16 + gq] : 0.0, b1 = rv ? sx[r * 16 + 8 + gq] : 0.0;
+    const double b0 = rv ? sx[r * 16 + o0] : 0.0, b1 = rv ? sx[r * 16 + (o0 ^ 8)] : 0.0;
 #pragma unroll
     for (int i = 0; i < CNT; ++i) {
       const double a = (rv && cidx[i] < Wp) ? sv[r * Wp + cidx[i]] : 0.0;
@@ -530,10 +547,10 @@ __device__ void mA16_consumers(PipeSmem<NS, SD, SV>& S, const int32_t* __restric
     const int cnt = MT > w ? (MT - w + kConsWarps - 1) / kConsWarps : 0;
     switch (cnt) {
       case 0: break;
-      case 1: colsum16_mtiles<1>(d, sv, sx, h.cnt, Wp, w, gq, tq); break;
-      case 2: colsum16_mtiles<2>(d, sv, sx, h.cnt, Wp, w, gq, tq); break;
-      case 3: colsum16_mtiles<3>(d, sv, sx, h.cnt, Wp, w, gq, tq); break;
-      default: colsum16_mtiles<kMaxMTA16>(d, sv, sx, h.cnt, Wp, w, gq, tq); break;
+      case 1: colsum16_mtiles<1>(d, sv, sx, h.cnt, Wp, w, gq, tq, h.f); break;
+      case 2: colsum16_mtiles<2>(d, sv, sx, h.cnt, Wp, w, gq, tq, h.f); break;
+      case 3: colsum16_mtiles<3>(d, sv, sx, h.cnt, Wp, w, gq, tq, h.f); break;
+      default: colsum16_mtiles<kMaxMTA16>(d, sv, sx, h.cnt, Wp, w, gq, tq, h.f); break;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.empty[stage]);
@@ -549,8 +566,12 @@ __device__ void mA16_consumers(PipeSmem<NS, SD, SV>& S, const int32_t* __restric
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int k = 8 * g + 2 * tq + e;
-            if (h.c >= 0) tm[(int64_t)vdst[h.c + q] * NR + k] = d[i][g][e];
-            else tpartm[((int64_t)(-h.c - 1) + q) * NR + k] = d[i][g][e];
+            if (h.c >= 0) {
+              double* rec = tm + (int64_t)vdst[h.c + q] * NR;
+              rec[k ^ rec_swz<NR>(rec)] = d[i][g][e];
+            } else {
+              tpartm[((int64_t)(-h.c - 1) + q) * NR + k] = d[i][g][e];
+            }
           }
       }
     }
@@ -576,7 +597,8 @@ __device__ void mA16_consumers(PipeSmem<NS, SD, SV>& S, const int32_t* __restric
             a1 += __ldcg(pp + (c + 1) * cs);
           }
           if (c < ri.nchunks) a0 += __ldcg(pp + c * cs);
-          tm[(int64_t)vdst[ri.vpos + q] * NR + k] = a0 + a1;
+          double* rec = tm + (int64_t)vdst[ri.vpos + q] * NR;
+          rec[k ^ rec_swz<NR>(rec)] = a0 + a1;
         }
         if (tid == 0) rcount[h.d] = 0;
       }
@@ -588,12 +610,13 @@ constexpr int kAcc16 = 4 * 6;   // flat accumulators of the 16-vector stage B (b
 template <int CNT>
 __device__ __forceinline__ void bsplit16_mtiles(double (&d)[kAcc16], const double* __restrict__ su,
                                                 const double* __restrict__ tv, int cols, int rowsp, int w, int gq,
-                                                int tq) {
+                                                int tq, int swz0) {
   const bool last_ok = (CNT - 1) * 8 + gq < rowsp;
+  const int o0 = gq ^ swz0 ^ ((tq & 1) << 3);   // record c = k0 + tq, k0 a multiple of 4
   for (int k0 = 4 * w; k0 < cols; k0 += 4 * kConsWarps) {
     const int c = k0 + tq;
     const bool cv = c < cols;
-    const double b0 = cv ? tv[c * 16 + gq] : 0.0, b1 = cv ? tv[c * 16 + 8 + gq] : 0.0;
+    const double b0 = cv ? tv[c * 16 + o0] : 0.0, b1 = cv ? tv[c * 16 + (o0 ^ 8)] : 0.0;
     const double* __restrict__ col = su + c * rowsp + gq;
 #pragma unroll
     for (int i = 0; i < CNT; ++i) {
@@ -608,7 +631,9 @@ __device__ __forceinline__ void bsplit16_mtiles(double (&d)[kAcc16], const doubl
 // load for two DMMAs), each warp over all k-steps of the stage, exact per-warp count.
 template <int CNT>
 __device__ __forceinline__ void bmt16(double (&d)[kAcc16], const double* __restrict__ su,
-                                      const double* __restrict__ tv, int cols, int rowsp, int w, int gq, int tq) {
+                                      const double* __restrict__ tv, int cols, int rowsp, int w, int gq, int tq,
+                                      int swz0) {
+  const int o0 = gq ^ swz0 ^ ((tq & 1) << 3);
   int roff[CNT];
   bool rok[CNT];
 #pragma unroll
@@ -619,7 +644,7 @@ __device__ __forceinline__ void bmt16(double (&d)[kAcc16], const double* __restr
   for (int k0 = 0; k0 < cols; k0 += 4) {
     const int c = k0 + tq;
     const bool cv = c < cols;
-    const double b0 = cv ? tv[c * 16 + gq] : 0.0, b1 = cv ? tv[c * 16 + 8 + gq] : 0.0;
+    const double b0 = cv ? tv[c * 16 + o0] : 0.0, b1 = cv ? tv[c * 16 + (o0 ^ 8)] : 0.0;
     const double* __restrict__ col = su + c * rowsp;
 #pragma unroll
     for (int j = 0; j < CNT; ++j) {
@@ -660,21 +685,21 @@ __device__ void mB16_consumers(PipeSmem<NS, SD, SV>& S, double* __restrict__ yfa
     const int cols = h.cnt;
     if (ksplit) {
       switch (MT) {
-        case 1: bsplit16_mtiles<1>(d, su, tv, cols, rowsp, w, gq, tq); break;
-        case 2: bsplit16_mtiles<2>(d, su, tv, cols, rowsp, w, gq, tq); break;
-        case 3: bsplit16_mtiles<3>(d, su, tv, cols, rowsp, w, gq, tq); break;
-        case 4: bsplit16_mtiles<4>(d, su, tv, cols, rowsp, w, gq, tq); break;
-        case 5: bsplit16_mtiles<5>(d, su, tv, cols, rowsp, w, gq, tq); break;
-        default: bsplit16_mtiles<kMaxMTK16>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 1: bsplit16_mtiles<1>(d, su, tv, cols, rowsp, w, gq, tq, h.f); break;
+        case 2: bsplit16_mtiles<2>(d, su, tv, cols, rowsp, w, gq, tq, h.f); break;
+        case 3: bsplit16_mtiles<3>(d, su, tv, cols, rowsp, w, gq, tq, h.f); break;
+        case 4: bsplit16_mtiles<4>(d, su, tv, cols, rowsp, w, gq, tq, h.f); break;
+        case 5: bsplit16_mtiles<5>(d, su, tv, cols, rowsp, w, gq, tq, h.f); break;
+        default: bsplit16_mtiles<kMaxMTK16>(d, su, tv, cols, rowsp, w, gq, tq, h.f); break;
       }
     } else {
       const int cnt = MT > w ? (MT - w + kConsWarps - 1) / kConsWarps : 0;
       switch (cnt) {
         case 0: break;
-        case 1: bmt16<1>(d, su, tv, cols, rowsp, w, gq, tq); break;
-        case 2: bmt16<2>(d, su, tv, cols, rowsp, w, gq, tq); break;
-        case 3: bmt16<3>(d, su, tv, cols, rowsp, w, gq, tq); break;
-        default: bmt16<kMaxMTB>(d, su, tv, cols, rowsp, w, gq, tq); break;
+        case 1: bmt16<1>(d, su, tv, cols, rowsp, w, gq, tq, h.f); break;
+        case 2: bmt16<2>(d, su, tv, cols, rowsp, w, gq, tq, h.f); break;
+        case 3: bmt16<3>(d, su, tv, cols, rowsp, w, gq, tq, h.f); break;
+        default: bmt16<kMaxMTB>(d, su, tv, cols, rowsp, w, gq, tq, h.f); break;
       }
     }
     __syncwarp();
@@ -994,6 +1019,7 @@ __device__ void mB_producer(PipeSmem<NS, SD, SV>& S, const BItem* __restrict__ i
           h.a = it.rows;
           h.b = rowsp;
           h.c = it.yrow;
+          h.f = rec_swz<NR>(tb + (int64_t)c0 * NR);
           const uint32_t tbytes = (uint32_t)cols * NR * 8u;
           mbar_arrive_expect_tx(&S.full[stage], (uint32_t)cols * (uint32_t)rowsp * 8u + tbytes);
           if (whole)
@@ -1150,7 +1176,7 @@ p2p_multi_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf
         }
         for (int q = tid; q < nt * NR; q += 256) {   // x records of the tile, coalesced
           const int e = q / NR;
-          tx[q - e * NR][e] = xm[(ys + cb) * NR + q];
+          tx[(q - e * NR) ^ rec_swz<NR>(xm + (ys + cb + e) * NR)][e] = xm[(ys + cb) * NR + q];
         }
         __syncthreads();
         if (act) {
@@ -1196,8 +1222,9 @@ __global__ void permute_multi_kernel(int NR, const double* __restrict__ X, int64
   for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = iperm ? iperm[o] : o;
     double2* __restrict__ rec = reinterpret_cast<double2*>(xm + s * NR);
+    const int sw = NR == 16 ? rec_swz<16>(xm + s * NR) : 0;   // (swizzled 16-vector records)
     for (int k = 0; k < NR; k += 2)
-      rec[k >> 1] = make_double2(X[(int64_t)k * xlen + o], X[(int64_t)(k + 1) * xlen + o]);
+      rec[(k ^ sw) >> 1] = make_double2(X[(int64_t)k * xlen + o], X[(int64_t)(k + 1) * xlen + o]);
   }
 }
 
@@ -1214,8 +1241,9 @@ __global__ void combine_multi_kernel(int NR, int64_t row_begin, int64_t rows, co
     const double2* __restrict__ yf = reinterpret_cast<const double2*>(yfarm + (r - row_begin) * NR);
     const double2* __restrict__ yn = reinterpret_cast<const double2*>(ynearm + r * NR);
     const double2* __restrict__ xr = reinterpret_cast<const double2*>(xm + r * NR);
+    const int sw = NR == 16 ? rec_swz<16>(xm + r * NR) : 0;
     for (int k = 0; k < NR; k += 2) {
-      const double2 f = yf[k >> 1], e = yn[k >> 1], xv = xr[k >> 1];
+      const double2 f = yf[k >> 1], e = yn[k >> 1], xv = xr[(k ^ sw) >> 1];
       Y[(int64_t)k * ylen + o] = f.x + fma(scale, e.x, shift * xv.x);
       Y[(int64_t)(k + 1) * ylen + o] = f.y + fma(scale, e.y, shift * xv.y);
     }
