@@ -34,6 +34,7 @@ struct NcclApi {
   ncclResult_t (*MemFree)(void*) = nullptr;
   ncclResult_t (*CommRegister)(const ncclComm_t, void*, size_t, void**) = nullptr;
   ncclResult_t (*CommDeregister)(const ncclComm_t, void*) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -56,6 +57,7 @@ NcclApi load_nccl() {
   a.MemFree = (decltype(a.MemFree))sym("ncclMemFree");
   a.CommRegister = (decltype(a.CommRegister))sym("ncclCommRegister");
   a.CommDeregister = (decltype(a.CommDeregister))sym("ncclCommDeregister");
+  a.CommGetAsyncError = (decltype(a.CommGetAsyncError))sym("ncclCommGetAsyncError");
   a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.GetErrorString;
   if (!a.ok) a.why = "libnccl.so.2 lacks ncclGetUniqueId / ncclCommInitRank / ncclAllGather";
   return a;
@@ -172,6 +174,13 @@ void comm_init(Handle& h) {
 // the in-place all-gather on the comm stream, ordered after the caller's stream.
 void comm_gather_start(Handle& h, const double* d_xl, double* d_xtree) {
   Comm* c = h.comm;
+  // failure detection: an error NCCL raised asynchronously on this communicator (a peer
+  // that died, a network fault) surfaces here as H2D_ENCCL instead of a hang in the gather
+  if (c->nc && nccl().CommGetAsyncError) {
+    ncclResult_t ae = ncclSuccess;
+    nccl_check(nccl().CommGetAsyncError(c->nc, &ae), "ncclCommGetAsyncError");
+    if (ae != ncclSuccess && ae != ncclInProgress) nccl_check(ae, "NCCL asynchronous error on the communicator");
+  }
   const int64_t rows = h.row_end - h.row_begin;
   double* slot = c->gbuf + (int64_t)c->rank * h.gather_stride;
   if (rows > 0) {
