@@ -1121,7 +1121,11 @@ stageB_multi_kernel(const BItem* __restrict__ items, const BLevel* __restrict__ 
 // One CTA per served leaf X; rows of X in blocks of <= 128, thread (g, i) = (tid / RB,
 // tid % RB) owns row i and the tile columns g, g + G, ...; every column tile (<= 96
 // points of {X} u E_X) is staged in smem with its NR x values; K(r) is evaluated once
-// per (row, column) and applied to the NR vectors.  ynear_m[k * n + row] = sum_Y K x_Y.
+// per (row, column) and applied to the NR vectors, whose values sit in the tile as one
+// record per column (NR / 2 16-byte loads per evaluation; vector-major, NR 8-byte loads:
+// 16 vectors at C3 1.71 -> 1.50 ms standalone).  ynear_m[row * NR + k] = sum_Y K x_Y.
+// (A DMMA version, every A-fragment entry evaluated by its lane, measured slower:
+// tools/scratch/p2p_multi_dmma.cuh.txt.)
 constexpr int kMTile = 96, kMRows = 128;
 
 template <int KID>
@@ -1139,7 +1143,8 @@ __global__ void __launch_bounds__(256, 3)
 p2p_multi_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_start,
                  const double* __restrict__ px, const double* __restrict__ py,
                  const double* __restrict__ xm, int64_t n, KernelParams kp, double* __restrict__ ynearm) {
-  __shared__ double tpx[kMTile], tpy[kMTile], tx[NR][kMTile];
+  __shared__ double tpx[kMTile], tpy[kMTile];
+  __shared__ __align__(16) double tx[kMTile][NR];   // the tile's x records, unswizzled
   __shared__ double red[256];
   __shared__ double2 tab[kHlogBins];
   const int tid = threadIdx.x;
@@ -1176,21 +1181,38 @@ p2p_multi_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf
         }
         for (int q = tid; q < nt * NR; q += 256) {   // x records of the tile, coalesced
           const int e = q / NR;
-          tx[(q - e * NR) ^ rec_swz<NR>(xm + (ys + cb + e) * NR)][e] = xm[(ys + cb) * NR + q];
+          tx[e][(q - e * NR) ^ rec_swz<NR>(xm + (ys + cb + e) * NR)] = xm[(ys + cb) * NR + q];
         }
         __syncthreads();
         if (act) {
           int j = g;
-          for (; j + G < nt; j += 2 * G) {
-            const double k0v = keval_m<KID>(kp, tab, rpx, rpy, tpx[j], tpy[j]);
-            const double k1v = keval_m<KID>(kp, tab, rpx, rpy, tpx[j + G], tpy[j + G]);
+          // a column's NR x values are one record: NR / 2 16-byte loads; two columns per step
+          // below 16 vectors, one at 16 (two would spill at the 80-register cap)
+          constexpr int CPS = NR >= 16 ? 1 : 2;
+          for (; j + (CPS - 1) * G < nt; j += CPS * G) {
+            double kv[CPS];
 #pragma unroll
-            for (int k = 0; k < NR; ++k) racc[k] = fma(k1v, tx[k][j + G], fma(k0v, tx[k][j], racc[k]));
+            for (int c = 0; c < CPS; ++c) kv[c] = keval_m<KID>(kp, tab, rpx, rpy, tpx[j + c * G], tpy[j + c * G]);
+#pragma unroll
+            for (int c = 0; c < CPS; ++c) {
+              const double2* rc = reinterpret_cast<const double2*>(tx[j + c * G]);
+#pragma unroll
+              for (int k = 0; k < NR; k += 2) {
+                const double2 v = rc[k >> 1];
+                racc[k] = fma(kv[c], v.x, racc[k]);
+                racc[k + 1] = fma(kv[c], v.y, racc[k + 1]);
+              }
+            }
           }
-          if (j < nt) {
+          if (CPS == 2 && j < nt) {
             const double k0v = keval_m<KID>(kp, tab, rpx, rpy, tpx[j], tpy[j]);
+            const double2* r0 = reinterpret_cast<const double2*>(tx[j]);
 #pragma unroll
-            for (int k = 0; k < NR; ++k) racc[k] = fma(k0v, tx[k][j], racc[k]);
+            for (int k = 0; k < NR; k += 2) {
+              const double2 v = r0[k >> 1];
+              racc[k] = fma(k0v, v.x, racc[k]);
+              racc[k + 1] = fma(k0v, v.y, racc[k + 1]);
+            }
           }
         }
       }
@@ -1209,43 +1231,71 @@ p2p_multi_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf
   }
 }
 
-// x_m[s * NR + k] (one record of the NR values per TREE row s) from NR vectors of length
-// xlen, in the caller's order: ORIGINAL -> thread per original index o, s = iperm[o] (the
-// reads of X coalesce, each thread writes one record); TREE -> s = o.
 __global__ void invert_perm_kernel(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ iperm) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
     iperm[perm[s]] = (int32_t)s;
 }
 
-__global__ void permute_multi_kernel(int NR, const double* __restrict__ X, int64_t xlen,
-                                     const int32_t* __restrict__ iperm, int64_t n, double* __restrict__ xm) {
-  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = iperm ? iperm[o] : o;
-    double2* __restrict__ rec = reinterpret_cast<double2*>(xm + s * NR);
-    const int sw = NR == 16 ? rec_swz<16>(xm + s * NR) : 0;   // (swizzled 16-vector records)
-    for (int k = 0; k < NR; k += 2)
-      rec[(k ^ sw) >> 1] = make_double2(X[(int64_t)k * xlen + o], X[(int64_t)(k + 1) * xlen + o]);
+// x_m[s * NR + k] (one record of the NR values per TREE row s) from NR vectors of length
+// xlen in the caller's order (ORIGINAL: s = iperm[o]; TREE: s = o), and back in combine.
+// Both go through a shared-memory tile of 256 rows x NR values (row stride NR + 1): the
+// vector-major side moves in coalesced 256-element runs, the record side in whole records
+// (consecutive lanes on consecutive values of a record), so a warp access touches no more
+// lines than it fills (thread-per-record versions: 32 partial lines per instruction,
+// 0.155 / 0.227 ms for 16 vectors at C3).
+constexpr int kPermTile = 256;
+
+template <int NR>
+__global__ void __launch_bounds__(256) permute_multi_kernel(const double* __restrict__ X, int64_t xlen,
+                                                            const int32_t* __restrict__ iperm, int64_t n,
+                                                            double* __restrict__ xm) {
+  __shared__ double sm[kPermTile][NR + 1];
+  const int tid = threadIdx.x;
+  for (int64_t o0 = (int64_t)blockIdx.x * kPermTile; o0 < n; o0 += (int64_t)gridDim.x * kPermTile) {
+    const int cnt = (int)min((int64_t)kPermTile, n - o0);
+    __syncthreads();
+    if (tid < cnt) {
+#pragma unroll
+      for (int k = 0; k < NR; ++k) sm[tid][k] = X[(int64_t)k * xlen + o0 + tid];
+    }
+    __syncthreads();
+    for (int q = tid; q < cnt * NR; q += 256) {
+      const int e = q / NR, k = q - e * NR;
+      const int64_t sr = iperm ? (int64_t)iperm[o0 + e] : o0 + e;
+      double* rec = xm + sr * NR;
+      rec[k ^ rec_swz<NR>(rec)] = sm[e][k];
+    }
   }
 }
 
 // Y[k * ylen + o] = yfar_m[r] + scale ynear_m[r] + shift x_m[r] (records of NR values per
-// TREE row r).  ORIGINAL: thread per output index o, r = iperm[o] (coalesced Y writes,
-// record reads); TREE: r = row_begin + o' with o = r - y_row0.
-__global__ void combine_multi_kernel(int NR, int64_t row_begin, int64_t rows, const double* __restrict__ yfarm,
-                                     const double* __restrict__ ynearm, int64_t n, const double* __restrict__ xm,
-                                     double scale, double shift, double* __restrict__ Y, int64_t ylen,
-                                     const int32_t* __restrict__ iperm, int order_out, int64_t y_row0) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < rows; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = order_out == H2D_ORDER_ORIGINAL ? (int64_t)iperm[q] : row_begin + q;
-    const int64_t o = order_out == H2D_ORDER_ORIGINAL ? q : r - y_row0;
-    const double2* __restrict__ yf = reinterpret_cast<const double2*>(yfarm + (r - row_begin) * NR);
-    const double2* __restrict__ yn = reinterpret_cast<const double2*>(ynearm + r * NR);
-    const double2* __restrict__ xr = reinterpret_cast<const double2*>(xm + r * NR);
-    const int sw = NR == 16 ? rec_swz<16>(xm + r * NR) : 0;
-    for (int k = 0; k < NR; k += 2) {
-      const double2 f = yf[k >> 1], e = yn[k >> 1], xv = xr[(k ^ sw) >> 1];
-      Y[(int64_t)k * ylen + o] = f.x + fma(scale, e.x, shift * xv.x);
-      Y[(int64_t)(k + 1) * ylen + o] = f.y + fma(scale, e.y, shift * xv.y);
+// TREE row r).  ORIGINAL: output index o = q, r = iperm[q]; TREE: r = row_begin + q,
+// o = r - y_row0.
+template <int NR>
+__global__ void __launch_bounds__(256) combine_multi_kernel(int64_t row_begin, int64_t rows,
+                                                            const double* __restrict__ yfarm,
+                                                            const double* __restrict__ ynearm, int64_t n,
+                                                            const double* __restrict__ xm, double scale, double shift,
+                                                            double* __restrict__ Y, int64_t ylen,
+                                                            const int32_t* __restrict__ iperm, int order_out,
+                                                            int64_t y_row0) {
+  __shared__ double sm[kPermTile][NR + 1];
+  const int tid = threadIdx.x;
+  const bool orig = order_out == H2D_ORDER_ORIGINAL;
+  for (int64_t q0 = (int64_t)blockIdx.x * kPermTile; q0 < rows; q0 += (int64_t)gridDim.x * kPermTile) {
+    const int cnt = (int)min((int64_t)kPermTile, rows - q0);
+    __syncthreads();
+    for (int q = tid; q < cnt * NR; q += 256) {
+      const int e = q / NR, k = q - e * NR;
+      const int64_t r = orig ? (int64_t)iperm[q0 + e] : row_begin + q0 + e;
+      const double* xr = xm + r * NR;
+      sm[e][k] = yfarm[(r - row_begin) * NR + k] + fma(scale, ynearm[r * NR + k], shift * xr[k ^ rec_swz<NR>(xr)]);
+    }
+    __syncthreads();
+    if (tid < cnt) {
+      const int64_t o = orig ? q0 + tid : row_begin + q0 + tid - y_row0;
+#pragma unroll
+      for (int k = 0; k < NR; ++k) Y[(int64_t)k * ylen + o] = sm[tid][k];
     }
   }
 }
@@ -1450,7 +1500,7 @@ static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, i
   set_multi_attrs<NR, NS, SD, SV>();
   cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
   const int grid = (int)std::min<int64_t>((h.n + 255) / 256, 148 * 16);
-  permute_multi_kernel<<<grid, 256, 0, s>>>(NR, dX, xlen, order == H2D_ORDER_ORIGINAL ? h.m_iperm : nullptr, h.n,
+  permute_multi_kernel<NR><<<grid, 256, 0, s>>>(dX, xlen, order == H2D_ORDER_ORIGINAL ? h.m_iperm : nullptr, h.n,
                                             h.m_xm);
   H2D_LAUNCH_CHECK();
   H2D_CUDA(cudaEventRecord(h.ev_fork, s));
@@ -1491,7 +1541,7 @@ static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, i
   const int64_t rows = h.row_end - h.row_begin;
   if (rows > 0) {
     const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 148 * 8);
-    combine_multi_kernel<<<blocks, 256, 0, s>>>(NR, h.row_begin, rows, h.m_yfar, h.m_ynear, h.n, h.m_xm,
+    combine_multi_kernel<NR><<<blocks, 256, 0, s>>>(h.row_begin, rows, h.m_yfar, h.m_ynear, h.n, h.m_xm,
                                                 h.kp.scale, h.kp.shift, dY, ylen, h.m_iperm,
                                                 order == H2D_ORDER_ORIGINAL ? H2D_ORDER_ORIGINAL : H2D_ORDER_TREE,
                                                 h.row_begin);
@@ -1515,7 +1565,7 @@ static void multi_chunk_sym(Handle& h, const double* dX, int64_t xlen, double* d
   });
   cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
   const int grid = (int)std::min<int64_t>((h.n + 255) / 256, 148 * 16);
-  permute_multi_kernel<<<grid, 256, 0, s>>>(NR, dX, xlen, order == H2D_ORDER_ORIGINAL ? h.m_iperm : nullptr, h.n,
+  permute_multi_kernel<NR><<<grid, 256, 0, s>>>(dX, xlen, order == H2D_ORDER_ORIGINAL ? h.m_iperm : nullptr, h.n,
                                             h.m_xm);
   H2D_LAUNCH_CHECK();
   H2D_CUDA(cudaEventRecord(h.ev_fork, s));
