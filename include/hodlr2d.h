@@ -321,8 +321,10 @@ int hodlr2d_partition(const int32_t* leaf_start, int kappa, int world, int rank,
  * results, for timing only): "p2p_serial" (the near field alone, before stage A),
  * "p2p_onestream" (every near-field class on one stream), "dual_norow", "copy_stream" (0:
  * host copies on the work stream), "pair_apply" (symmetric handles: 1 the pair-local apply,
- * 0 the three-pass apply).  Defaults come from the H2D_* environment variables at
- * build time.  H2D_EINVAL for an unknown name. */
+ * 0 the three-pass apply), "multi_stored_near" (16-vector multi-RHS chunks: 1 (default) the
+ * stored dense near-field blocks of Alg. 1 l.5, built on the first such call when they
+ * fit in half the free device memory; 0 the on-the-fly near field).  Defaults come from the
+ * H2D_* environment variables at build time.  H2D_EINVAL for an unknown name. */
 int hodlr2d_set_diag(hodlr2d_t h, const char* name, int value);
 
 /* Write a fresh NCCL unique id (H2D_COMM_ID_BYTES bytes) to id[] for options.nccl_id

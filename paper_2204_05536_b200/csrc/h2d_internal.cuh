@@ -358,6 +358,13 @@ struct Handle {
   int32_t* m_b1rcount = nullptr;
   double *m_b1tpart = nullptr, *m_t1 = nullptr, *m_y1 = nullptr;
   double* d_ynear = nullptr;              // [3n] near-field P2P slots (p2p_sym_kernel)
+  // stored near field for 16-vector chunks (Alg. 1 l.5: the dense self / edge-sharer blocks
+  // of every served leaf, column-major mp x ncolp per leaf at nf_off[leaf - leaf_begin])
+  int nf_state = 0;                       // 0 not built, 1 built, -1 skipped (memory)
+  bool nf_enabled = true;                 // set_diag "multi_stored_near"
+  double* d_snf = nullptr;
+  int64_t* d_snf_off = nullptr;
+  int64_t nf_values = 0;
   double* d_yfar = nullptr;               // [served] low-rank part (stage B output)
   cudaStream_t hi_stream = nullptr;       // stages A, B (high priority)
   cudaStream_t aux_stream = nullptr;      // P2P (low priority), concurrent with A and B

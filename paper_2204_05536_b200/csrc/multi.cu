@@ -1231,6 +1231,138 @@ p2p_multi_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf
   }
 }
 
+// ---------------------------------------------------------------- stored near field (16 vectors)
+// Alg. 1 l.5 computes the dense self and edge-sharer blocks of every leaf once, at
+// build time; the single-vector path instead evaluates them on the fly (the evaluations hide
+// under the factor streams, and storing them would add 2.7 GB of HBM reads per matvec at C3).
+// With 16 vectors per call the evaluations no longer hide (~0.95 ms exposed beside the DMMA
+// stage kernels, profiles/r02ae_multi16.md) while reading the stored blocks costs ~0.4 ms of
+// HBM, so 16-vector chunks use the paper's stored blocks, built on the first such call when
+// they fit in half the free device memory (C3: 2.9 GB; C3 16 vectors 5.40 -> 5.11 ms per call,
+// the kernel alone 1.06 ms at 42 % DRAM: latency-bound, four k-steps of loads in flight per
+// warp at 80 registers beat more warps at 64 / 48, profiles/r02ae_multi16.md).  Per served leaf X: the columns of
+// {X} u E_X (order X, +x, +y, -x, -y, each segment padded to a multiple of 4 with zero
+// columns), rows padded to mp = 8 ceil(m / 8) with zeros, column-major mp x ncolp.  The
+// product Y_X = D_X X_near runs on DMMA: lane t loads its A-fragment entry D[8 i + t/4][4 k +
+// t%4] straight from HBM (four 64-byte runs per warp load) and the B fragments from the x
+// records (L1 / L2: a leaf's columns are shared by its m-tiles and neighbours).
+__device__ __forceinline__ int nf_segments(int kappa, int64_t X, const int32_t* __restrict__ leaf_start,
+                                           int64_t (&ys)[5], int (&ny)[5]) {
+  const uint32_t cx = p2p_compact((uint32_t)X), cy = p2p_compact((uint32_t)X >> 1);
+  const uint32_t side = 1u << kappa;
+  int64_t nb[5];
+  int nn = 0;
+  nb[nn++] = X;
+  if (cx + 1 < side) nb[nn++] = (int64_t)(p2p_spread(cx + 1) | (p2p_spread(cy) << 1));
+  if (cy + 1 < side) nb[nn++] = (int64_t)(p2p_spread(cx) | (p2p_spread(cy + 1) << 1));
+  if (cx > 0) nb[nn++] = (int64_t)(p2p_spread(cx - 1) | (p2p_spread(cy) << 1));
+  if (cy > 0) nb[nn++] = (int64_t)(p2p_spread(cx) | (p2p_spread(cy - 1) << 1));
+#pragma unroll
+  for (int a = 0; a < 5; ++a) {
+    ys[a] = a < nn ? leaf_start[nb[a]] : 0;
+    ny[a] = a < nn ? leaf_start[nb[a] + 1] - (int)ys[a] : 0;
+  }
+  return nn;
+}
+
+template <int KID>
+__global__ void __launch_bounds__(256) nf_fill_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_start,
+                                                      const double* __restrict__ px, const double* __restrict__ py,
+                                                      KernelParams kp, const int64_t* __restrict__ nf_off,
+                                                      double* __restrict__ nf) {
+  __shared__ double2 tab[kHlogBins];
+  if (kNeedsLogTable<KID>) hlog_table(tab);
+  __syncthreads();
+  const int64_t X = leaf_begin + blockIdx.x;
+  int64_t ys[5];
+  int ny[5];
+  nf_segments(kappa, X, leaf_start, ys, ny);
+  const int64_t xs = ys[0];
+  const int m = ny[0], mp = (m + 7) & ~7;
+  double* __restrict__ D = nf + nf_off[blockIdx.x];
+  int64_t cb = 0;
+#pragma unroll 1
+  for (int a = 0; a < 5; ++a) {
+    const int nyp = (ny[a] + 3) & ~3;
+    for (int64_t q = threadIdx.x; q < (int64_t)nyp * mp; q += blockDim.x) {
+      const int c = (int)(q / mp), r = (int)(q - (int64_t)c * mp);
+      double v = 0.0;
+      if (c < ny[a] && r < m) v = keval_m<KID>(kp, tab, px[xs + r], py[xs + r], px[ys[a] + c], py[ys[a] + c]);
+      D[(cb + c) * mp + r] = v;
+    }
+    cb += nyp;
+  }
+}
+
+constexpr int kNfWarps = 4;
+
+#ifndef H2D_NF_MINB
+#define H2D_NF_MINB 6
+#endif
+__global__ void __launch_bounds__(32 * kNfWarps, H2D_NF_MINB)
+p2p_stored_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf_start,
+                  const double* __restrict__ xm, const int64_t* __restrict__ nf_off,
+                  const double* __restrict__ nf, double* __restrict__ ynearm) {
+  constexpr int NR = 16;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, tr = lane >> 2, tc = lane & 3;
+  const int64_t X = leaf_begin + blockIdx.x;
+  int64_t ys[5];
+  int ny[5];
+  nf_segments(kappa, X, leaf_start, ys, ny);
+  const int64_t xs = ys[0];
+  const int m = ny[0], mp = (m + 7) & ~7, MT = mp >> 3;
+  const double* __restrict__ D = nf + nf_off[blockIdx.x];
+  for (int mt = w; mt < MT; mt += kNfWarps) {
+    double d[2][2][2] = {};   // [chain][vector group][pair]: two DMMA chains per group
+    const double* __restrict__ Dm = D + 8 * mt + tr;
+    int64_t cb = 0;
+#pragma unroll 1
+    for (int a = 0; a < 5; ++a) {
+      const int n = ny[a], nk = (n + 3) >> 2;
+      const double* __restrict__ xa = xm + ys[a] * NR;
+      int k = 0;
+      // four k-steps per iteration, every load issued before the first DMMA (HBM latency:
+      // four 256-byte A loads and eight x loads in flight per warp), two DMMA chains
+      for (; k + 3 < nk; k += 4) {
+        double av[4], b0[4], b1[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) av[u] = __ldcs(Dm + (cb + 4 * (k + u) + tc) * mp);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int col = 4 * (k + u) + tc;
+          const double* rec = xa + (int64_t)min(col, n - 1) * NR;
+          const int sw = rec_swz<NR>(rec);
+          b0[u] = col < n ? rec[tr ^ sw] : 0.0;
+          b1[u] = col < n ? rec[(8 + tr) ^ sw] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          dmma884(d[u & 1][0][0], d[u & 1][0][1], av[u], b0[u]);
+          dmma884(d[u & 1][1][0], d[u & 1][1][1], av[u], b1[u]);
+        }
+      }
+      for (; k < nk; ++k) {
+        const int col = 4 * k + tc;
+        const double av = __ldcs(Dm + (cb + col) * mp);
+        const double* rec = xa + (int64_t)min(col, n - 1) * NR;
+        const int sw = rec_swz<NR>(rec);
+        const double b0 = col < n ? rec[tr ^ sw] : 0.0, b1 = col < n ? rec[(8 + tr) ^ sw] : 0.0;
+        dmma884(d[0][0][0], d[0][0][1], av, b0);
+        dmma884(d[0][1][0], d[0][1][1], av, b1);
+      }
+      cb += 4 * nk;
+    }
+    // D fragment: lane t holds rows 8 mt + t/4, vectors 8 g + 2 (t%4) + {0, 1}
+    const int r = 8 * mt + tr;
+    if (r < m) {
+#pragma unroll
+      for (int g = 0; g < 2; ++g)
+        *reinterpret_cast<double2*>(ynearm + (xs + r) * NR + 8 * g + 2 * tc) =
+            make_double2(d[0][g][0] + d[1][g][0], d[0][g][1] + d[1][g][1]);
+    }
+  }
+}
+
 __global__ void invert_perm_kernel(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ iperm) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
     iperm[perm[s]] = (int32_t)s;
@@ -1495,9 +1627,73 @@ static void launch_p2p_multi(Handle& h, cudaStream_t a) {
   H2D_LAUNCH_CHECK();
 }
 
+// The stored near field of the served leaves (16-vector chunks): sizes from the host copy
+// of leaf_start, one fill launch; skipped (on-the-fly kernel) when it would take more than
+// half the free device memory.
+static void build_stored_near(Handle& h) {
+  const int64_t nl = h.leaf_end - h.leaf_begin;
+  std::vector<int64_t> off((size_t)nl + 1, 0);
+  const uint32_t side = 1u << h.kappa;
+  auto spread = [](uint32_t v) {
+    uint64_t x = v & 0xffffu;
+    x = (x | (x << 8)) & 0x00ff00ffu;
+    x = (x | (x << 4)) & 0x0f0f0f0fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+  };
+  auto cnt = [&](uint64_t Y) { return (int64_t)h.leaf_start[(size_t)Y + 1] - h.leaf_start[(size_t)Y]; };
+  for (int64_t i = 0; i < nl; ++i) {
+    const uint64_t X = (uint64_t)(h.leaf_begin + i);
+    uint32_t cx = 0, cy = 0;
+    for (int b = 0; b < h.kappa; ++b) {
+      cx |= (uint32_t)((X >> (2 * b)) & 1) << b;
+      cy |= (uint32_t)((X >> (2 * b + 1)) & 1) << b;
+    }
+    int64_t ncolp = (cnt(X) + 3) & ~3LL;
+    if (cx + 1 < side) ncolp += (cnt(spread(cx + 1) | (spread(cy) << 1)) + 3) & ~3LL;
+    if (cy + 1 < side) ncolp += (cnt(spread(cx) | (spread(cy + 1) << 1)) + 3) & ~3LL;
+    if (cx > 0) ncolp += (cnt(spread(cx - 1) | (spread(cy) << 1)) + 3) & ~3LL;
+    if (cy > 0) ncolp += (cnt(spread(cx) | (spread(cy - 1) << 1)) + 3) & ~3LL;
+    off[(size_t)i + 1] = off[(size_t)i] + ((cnt(X) + 7) & ~7LL) * ncolp;
+  }
+  size_t fr = 0, tot = 0;
+  H2D_CUDA(cudaMemGetInfo(&fr, &tot));
+  const int64_t values = off[(size_t)nl];
+  if (nl <= 0 || (size_t)values * 8 > fr / 2) {
+    h.nf_state = -1;
+    return;
+  }
+  h.d_snf = h.alloc<double>((size_t)values);
+  h.d_snf_off = h.alloc<int64_t>((size_t)nl + 1);
+  h.nf_values = values;
+  cudaStream_t s = h.stream;
+  H2D_CUDA(cudaMemcpyAsync(h.d_snf_off, off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  auto fill = [&](auto kid) {
+    constexpr int KID = decltype(kid)::value;
+    nf_fill_kernel<KID><<<(int)nl, 256, 0, s>>>(h.kappa, h.leaf_begin, h.d_leaf_start, h.d_px, h.d_py, h.kp,
+                                                h.d_snf_off, h.d_snf);
+  };
+  switch (h.kp.id) {
+    case H2D_KERNEL_LOG:
+      if (h.p2p_kid == kLogSafe) fill(std::integral_constant<int, kLogSafe>{});
+      else fill(std::integral_constant<int, H2D_KERNEL_LOG>{});
+      break;
+    case H2D_KERNEL_IMQ: fill(std::integral_constant<int, H2D_KERNEL_IMQ>{}); break;
+    case H2D_KERNEL_ONE_OVER_R: fill(std::integral_constant<int, H2D_KERNEL_ONE_OVER_R>{}); break;
+    case H2D_KERNEL_RBF_PHI1: fill(std::integral_constant<int, H2D_KERNEL_RBF_PHI1>{}); break;
+    case H2D_KERNEL_RBF_PHI2: fill(std::integral_constant<int, H2D_KERNEL_RBF_PHI2>{}); break;
+    default: fill(std::integral_constant<int, H2D_KERNEL_TEST_LOWRANK>{}); break;
+  }
+  H2D_LAUNCH_CHECK();
+  H2D_CUDA(cudaStreamSynchronize(s));
+  h.nf_state = 1;
+}
+
 template <int NR, int NS, int SD, int SV>
 static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, int64_t ylen, int order) {
   set_multi_attrs<NR, NS, SD, SV>();
+  if (NR == 16 && h.nf_enabled && h.nf_state == 0) build_stored_near(h);
   cudaStream_t s = h.stream, hi = h.hi_stream, a = h.aux_stream;
   const int grid = (int)std::min<int64_t>((h.n + 255) / 256, 148 * 16);
   permute_multi_kernel<NR><<<grid, 256, 0, s>>>(dX, xlen, order == H2D_ORDER_ORIGINAL ? h.m_iperm : nullptr, h.n,
@@ -1524,16 +1720,22 @@ static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, i
     H2D_LAUNCH_CHECK();
   }
   H2D_CUDA(cudaEventRecord(h.ev_far, hi));
-  switch (h.kp.id) {
-    case H2D_KERNEL_LOG:
-      if (h.p2p_kid == kLogSafe) launch_p2p_multi<kLogSafe, NR>(h, a);
-      else launch_p2p_multi<H2D_KERNEL_LOG, NR>(h, a);
-      break;
-    case H2D_KERNEL_IMQ: launch_p2p_multi<H2D_KERNEL_IMQ, NR>(h, a); break;
-    case H2D_KERNEL_ONE_OVER_R: launch_p2p_multi<H2D_KERNEL_ONE_OVER_R, NR>(h, a); break;
-    case H2D_KERNEL_RBF_PHI1: launch_p2p_multi<H2D_KERNEL_RBF_PHI1, NR>(h, a); break;
-    case H2D_KERNEL_RBF_PHI2: launch_p2p_multi<H2D_KERNEL_RBF_PHI2, NR>(h, a); break;
-    default: launch_p2p_multi<H2D_KERNEL_TEST_LOWRANK, NR>(h, a); break;
+  if (NR == 16 && h.nf_state == 1 && h.nf_enabled) {
+    p2p_stored_kernel<<<(int)(h.leaf_end - h.leaf_begin), 32 * kNfWarps, 0, a>>>(
+        h.kappa, h.leaf_begin, h.d_leaf_start, h.m_xm, h.d_snf_off, h.d_snf, h.m_ynear);
+    H2D_LAUNCH_CHECK();
+  } else {
+    switch (h.kp.id) {
+      case H2D_KERNEL_LOG:
+        if (h.p2p_kid == kLogSafe) launch_p2p_multi<kLogSafe, NR>(h, a);
+        else launch_p2p_multi<H2D_KERNEL_LOG, NR>(h, a);
+        break;
+      case H2D_KERNEL_IMQ: launch_p2p_multi<H2D_KERNEL_IMQ, NR>(h, a); break;
+      case H2D_KERNEL_ONE_OVER_R: launch_p2p_multi<H2D_KERNEL_ONE_OVER_R, NR>(h, a); break;
+      case H2D_KERNEL_RBF_PHI1: launch_p2p_multi<H2D_KERNEL_RBF_PHI1, NR>(h, a); break;
+      case H2D_KERNEL_RBF_PHI2: launch_p2p_multi<H2D_KERNEL_RBF_PHI2, NR>(h, a); break;
+      default: launch_p2p_multi<H2D_KERNEL_TEST_LOWRANK, NR>(h, a); break;
+    }
   }
   H2D_CUDA(cudaEventRecord(h.ev_join, a));
   H2D_CUDA(cudaStreamWaitEvent(s, h.ev_far, 0));

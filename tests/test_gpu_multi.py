@@ -148,3 +148,22 @@ def test_multi_gathered_order(h2d):
         Yg = op.matvec_multi(dev(Xg), order="gathered").cpu().numpy()
         Yt = op.matvec_multi(dev(Xt), order="tree").cpu().numpy()
         assert np.array_equal(Yg, Yt)
+
+
+@pytest.mark.parametrize("name", ["c2", "c1"])
+def test_multi_stored_near_field(h2d, name):
+    """16-vector chunks read the stored dense near-field blocks (Alg. 1 l.5) through
+    DMMA; the on-the-fly near field (multi_stored_near = 0) gives the same columns to 1e-13,
+    and both match the single-vector matvec."""
+    cfg = W.CONFIGS[name]
+    pts, op = cfg_build(h2d, cfg)
+    X = np.stack([W.config_x(cfg, k) for k in range(16)])
+    Ys = op.matvec_multi(dev(X)).cpu().numpy()
+    op.set_diag("multi_stored_near", 0)
+    Yf = op.matvec_multi(dev(X)).cpu().numpy()
+    op.set_diag("multi_stored_near", 1)
+    assert np.array_equal(op.matvec_multi(dev(X)).cpu().numpy(), Ys)   # deterministic
+    for k in range(16):
+        y1 = op.matvec(dev(X[k])).cpu().numpy()
+        assert rel(Ys[k], Yf[k]) <= 1e-13, k
+        assert rel(Ys[k], y1) <= 1e-13, k

@@ -17,6 +17,8 @@ pts = torch.from_numpy(W.config_points(cfg)).cuda()
 op = h2d.Hodlr2d.build(pts, cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c, scale=cfg.scale, shift=cfg.shift,
                        box_lo=cfg.box_lo, box_side=cfg.box_side,
                        symmetric=os.environ.get("SYM", "0") == "1")
+if "NF" in os.environ:
+    op.set_diag("multi_stored_near", int(os.environ["NF"]))
 X = torch.rand(K, cfg.n, dtype=torch.float64, device="cuda") * 2 - 1
 Y = torch.empty_like(X)
 s = torch.cuda.current_stream()
