@@ -1312,21 +1312,29 @@ p2p_stored_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ lea
   const int64_t xs = ys[0];
   const int m = ny[0], mp = (m + 7) & ~7, MT = mp >> 3;
   const double* __restrict__ D = nf + nf_off[blockIdx.x];
-  for (int mt = w; mt < MT; mt += kNfWarps) {
-    double d[2][2][2] = {};   // [chain][vector group][pair]: two DMMA chains per group
-    const double* __restrict__ Dm = D + 8 * mt + tr;
+  // a warp takes m-tile pairs (2 p, 2 p + 1), p = w, w + 4, ...: the pair shares every B
+  // fragment and doubles the A loads in flight (four k-steps of both tiles' loads issued
+  // before the first DMMA)
+  for (int p = w; 2 * p < MT; p += kNfWarps) {
+    const int mt0 = 2 * p;
+    const bool two = mt0 + 1 < MT;
+    double d[2][2][2] = {};   // [tile][vector group][pair]
+    const double* __restrict__ D0 = D + 8 * mt0 + tr;
+    const double* __restrict__ D1 = D0 + (two ? 8 : 0);
     int64_t cb = 0;
 #pragma unroll 1
     for (int a = 0; a < 5; ++a) {
       const int n = ny[a], nk = (n + 3) >> 2;
       const double* __restrict__ xa = xm + ys[a] * NR;
       int k = 0;
-      // four k-steps per iteration, every load issued before the first DMMA (HBM latency:
-      // four 256-byte A loads and eight x loads in flight per warp), two DMMA chains
       for (; k + 3 < nk; k += 4) {
-        double av[4], b0[4], b1[4];
+        double a0[4], a1[4], b0[4], b1[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) av[u] = __ldcs(Dm + (cb + 4 * (k + u) + tc) * mp);
+        for (int u = 0; u < 4; ++u) {
+          const int64_t o = (cb + 4 * (k + u) + tc) * mp;
+          a0[u] = __ldcs(D0 + o);
+          a1[u] = __ldcs(D1 + o);   // (the first tile again when there is no second)
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int col = 4 * (k + u) + tc;
@@ -1337,28 +1345,35 @@ p2p_stored_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ lea
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          dmma884(d[u & 1][0][0], d[u & 1][0][1], av[u], b0[u]);
-          dmma884(d[u & 1][1][0], d[u & 1][1][1], av[u], b1[u]);
+          dmma884(d[0][0][0], d[0][0][1], a0[u], b0[u]);
+          dmma884(d[0][1][0], d[0][1][1], a0[u], b1[u]);
+          dmma884(d[1][0][0], d[1][0][1], a1[u], b0[u]);
+          dmma884(d[1][1][0], d[1][1][1], a1[u], b1[u]);
         }
       }
       for (; k < nk; ++k) {
         const int col = 4 * k + tc;
-        const double av = __ldcs(Dm + (cb + col) * mp);
+        const int64_t o = (cb + col) * mp;
+        const double av0 = __ldcs(D0 + o), av1 = __ldcs(D1 + o);
         const double* rec = xa + (int64_t)min(col, n - 1) * NR;
         const int sw = rec_swz<NR>(rec);
         const double b0 = col < n ? rec[tr ^ sw] : 0.0, b1 = col < n ? rec[(8 + tr) ^ sw] : 0.0;
-        dmma884(d[0][0][0], d[0][0][1], av, b0);
-        dmma884(d[0][1][0], d[0][1][1], av, b1);
+        dmma884(d[0][0][0], d[0][0][1], av0, b0);
+        dmma884(d[0][1][0], d[0][1][1], av0, b1);
+        dmma884(d[1][0][0], d[1][0][1], av1, b0);
+        dmma884(d[1][1][0], d[1][1][1], av1, b1);
       }
       cb += 4 * nk;
     }
     // D fragment: lane t holds rows 8 mt + t/4, vectors 8 g + 2 (t%4) + {0, 1}
-    const int r = 8 * mt + tr;
-    if (r < m) {
 #pragma unroll
-      for (int g = 0; g < 2; ++g)
-        *reinterpret_cast<double2*>(ynearm + (xs + r) * NR + 8 * g + 2 * tc) =
-            make_double2(d[0][g][0] + d[1][g][0], d[0][g][1] + d[1][g][1]);
+    for (int q = 0; q < 2; ++q) {
+      const int r = 8 * (mt0 + q) + tr;
+      if ((q == 0 || two) && r < m) {
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+          *reinterpret_cast<double2*>(ynearm + (xs + r) * NR + 8 * g + 2 * tc) = make_double2(d[q][g][0], d[q][g][1]);
+      }
     }
   }
 }
