@@ -1312,58 +1312,63 @@ p2p_stored_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ lea
   const int64_t xs = ys[0];
   const int m = ny[0], mp = (m + 7) & ~7, MT = mp >> 3;
   const double* __restrict__ D = nf + nf_off[blockIdx.x];
+  // padded column starts of the segments: every k-step (4 columns) lies in one segment
+  int cp1 = (ny[0] + 3) & ~3;
+  const int cp2 = cp1 + ((ny[1] + 3) & ~3), cp3 = cp2 + ((ny[2] + 3) & ~3), cp4 = cp3 + ((ny[3] + 3) & ~3);
+  const int nkt = (cp4 + ((ny[4] + 3) & ~3)) >> 2;
   // a warp takes m-tile pairs (2 p, 2 p + 1), p = w, w + 4, ...: the pair shares every B
-  // fragment and doubles the A loads in flight (four k-steps of both tiles' loads issued
-  // before the first DMMA)
+  // fragment; the k-steps of all segments run as one loop, four per iteration, with the
+  // next iteration's A loads (HBM) issued before this iteration's DMMAs
   for (int p = w; 2 * p < MT; p += kNfWarps) {
     const int mt0 = 2 * p;
     const bool two = mt0 + 1 < MT;
     double d[2][2][2] = {};   // [tile][vector group][pair]
     const double* __restrict__ D0 = D + 8 * mt0 + tr;
-    const double* __restrict__ D1 = D0 + (two ? 8 : 0);
-    int64_t cb = 0;
-#pragma unroll 1
-    for (int a = 0; a < 5; ++a) {
-      const int n = ny[a], nk = (n + 3) >> 2;
-      const double* __restrict__ xa = xm + ys[a] * NR;
-      int k = 0;
-      for (; k + 3 < nk; k += 4) {
-        double a0[4], a1[4], b0[4], b1[4];
+    const double* __restrict__ D1 = D0 + (two ? 8 : 0);   // (the first tile again when there is no second)
+    auto bfrag = [&](int kk, double& b0, double& b1) {
+      const int c = 4 * kk + tc;
+      const int sa = (c >= cp1) + (c >= cp2) + (c >= cp3) + (c >= cp4);
+      // selects, not ys[sa] / ny[sa]: a dynamic index would put the arrays in local memory
+      const int base = sa == 0 ? 0 : sa == 1 ? cp1 : sa == 2 ? cp2 : sa == 3 ? cp3 : cp4;
+      const int n = sa == 0 ? ny[0] : sa == 1 ? ny[1] : sa == 2 ? ny[2] : sa == 3 ? ny[3] : ny[4];
+      const int64_t y0 = sa == 0 ? ys[0] : sa == 1 ? ys[1] : sa == 2 ? ys[2] : sa == 3 ? ys[3] : ys[4];
+      const int loc = c - base;
+      const double* rec = xm + (y0 + min(loc, n - 1)) * NR;
+      const int sw = rec_swz<NR>(rec);
+      b0 = loc < n ? rec[tr ^ sw] : 0.0;
+      b1 = loc < n ? rec[(8 + tr) ^ sw] : 0.0;
+    };
+    double a0[4], a1[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t o = (cb + 4 * (k + u) + tc) * mp;
-          a0[u] = __ldcs(D0 + o);
-          a1[u] = __ldcs(D1 + o);   // (the first tile again when there is no second)
-        }
+    for (int u = 0; u < 4; ++u) {
+      const int64_t o = (int64_t)(4 * min(u, nkt - 1) + tc) * mp;
+      a0[u] = __ldcs(D0 + o);
+      a1[u] = __ldcs(D1 + o);
+    }
+    for (int k = 0; k < nkt; k += 4) {
+      double b0[4], b1[4], n0[4], n1[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int col = 4 * (k + u) + tc;
-          const double* rec = xa + (int64_t)min(col, n - 1) * NR;
-          const int sw = rec_swz<NR>(rec);
-          b0[u] = col < n ? rec[tr ^ sw] : 0.0;
-          b1[u] = col < n ? rec[(8 + tr) ^ sw] : 0.0;
-        }
+      for (int u = 0; u < 4; ++u) bfrag(min(k + u, nkt - 1), b0[u], b1[u]);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 4; ++u) {   // next iteration's A (clamped to the leaf's last k-step)
+        const int64_t o = (int64_t)(4 * min(k + 4 + u, nkt - 1) + tc) * mp;
+        n0[u] = __ldcs(D0 + o);
+        n1[u] = __ldcs(D1 + o);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (k + u < nkt) {
           dmma884(d[0][0][0], d[0][0][1], a0[u], b0[u]);
           dmma884(d[0][1][0], d[0][1][1], a0[u], b1[u]);
           dmma884(d[1][0][0], d[1][0][1], a1[u], b0[u]);
           dmma884(d[1][1][0], d[1][1][1], a1[u], b1[u]);
         }
       }
-      for (; k < nk; ++k) {
-        const int col = 4 * k + tc;
-        const int64_t o = (cb + col) * mp;
-        const double av0 = __ldcs(D0 + o), av1 = __ldcs(D1 + o);
-        const double* rec = xa + (int64_t)min(col, n - 1) * NR;
-        const int sw = rec_swz<NR>(rec);
-        const double b0 = col < n ? rec[tr ^ sw] : 0.0, b1 = col < n ? rec[(8 + tr) ^ sw] : 0.0;
-        dmma884(d[0][0][0], d[0][0][1], av0, b0);
-        dmma884(d[0][1][0], d[0][1][1], av0, b1);
-        dmma884(d[1][0][0], d[1][0][1], av1, b0);
-        dmma884(d[1][1][0], d[1][1][1], av1, b1);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a0[u] = n0[u];
+        a1[u] = n1[u];
       }
-      cb += 4 * nk;
     }
     // D fragment: lane t holds rows 8 mt + t/4, vectors 8 g + 2 (t%4) + {0, 1}
 #pragma unroll
