@@ -1238,9 +1238,10 @@ p2p_multi_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf
 // With 16 vectors per call the evaluations no longer hide (~0.95 ms exposed beside the DMMA
 // stage kernels, profiles/r02ae_multi16.md) while reading the stored blocks costs ~0.4 ms of
 // HBM, so 16-vector chunks use the paper's stored blocks, built on the first such call when
-// they fit in half the free device memory (C3: 2.9 GB; C3 16 vectors 5.40 -> 5.11 ms per call,
-// the kernel alone 1.06 ms at 42 % DRAM: latency-bound, four k-steps of loads in flight per
-// warp at 80 registers beat more warps at 64 / 48, profiles/r02ae_multi16.md).  Per served leaf X: the columns of
+// they fit in half the free device memory (C3: 2.9 GB; C3 16 vectors 5.40 -> 4.97 ms per call,
+// the kernel alone 0.86 ms: latency-bound; 80 registers with four k-steps of both tiles' A
+// loads in flight beat more warps at 64 / 48 registers and B prefetch at 122,
+// profiles/r02ae_multi16.md).  Per served leaf X: the columns of
 // {X} u E_X (order X, +x, +y, -x, -y, each segment padded to a multiple of 4 with zero
 // columns), rows padded to mp = 8 ceil(m / 8) with zeros, column-major mp x ncolp.  The
 // product Y_X = D_X X_near runs on DMMA: lane t loads its A-fragment entry D[8 i + t/4][4 k +
