@@ -443,10 +443,22 @@ def run_ours(args, cfg):
         m1.record(stream)
         torch.cuda.synchronize()
         ms_b = m0.elapsed_time(m1) / nb
+        # bytes per call: the factor panels once per chunk (16 / 8 / 4 / 2 vectors), plus the
+        # stored near-field blocks (Alg. 1 l.5) that 16-vector chunks read
+        chunks, left, n16 = 0, K, 0
+        for c in (16, 8, 4, 2, 1):
+            chunks += left // c
+            n16 += left // c if c == 16 else 0
+            left %= c
+        nf_bytes = 8 * op.info()["stored_near_values"] * n16
+        fbytes = inf["stageA_bytes"] + inf["stageB_bytes"]
+        mbytes = fbytes * chunks + nf_bytes
         multi = {"nrhs": K, "matvecs_per_s": 1e3 * K / ms_b, "ms_per_call": ms_b, "calls": nb,
-                 "factor_bytes_per_call": inf["stageA_bytes"] + inf["stageB_bytes"],
-                 "note": "hodlr2d_matvec_multi: factor panels streamed once per call of nrhs "
-                         "vectors; a batched-throughput figure, not the per-vector headline"}
+                 "factor_bytes_per_call": fbytes * chunks, "stored_near_bytes_per_call": nf_bytes,
+                 "hbm_frac": round(mbytes / (ms_b * 1e-3) / 1e9 / peaks()[0], 4),
+                 "note": "hodlr2d_matvec_multi: factor panels streamed once per chunk of <= 16 "
+                         "vectors (16-vector chunks also read the stored near-field blocks); a "
+                         "batched-throughput figure, not the per-vector headline"}
 
     # symmetric block storage (NEXT N1, R23): the same workload built with one ACA
     # per unordered pair and applied by the three-pass symmetric apply; reported beside the

@@ -180,6 +180,9 @@ typedef struct {
   int64_t n_leaves;          /* leaves (adaptive: hodlr2d_copy_leaves; else 4^kappa)      */
   int64_t local_items[2];    /* H2D_ORDER_LOCAL: stage-A items (ring, small) whose column box
                                 is local, run while the x all-gather is in flight        */
+  int64_t stored_near_values;/* fp64 values of the stored near-field blocks that 16-vector
+                                multi-RHS chunks read (Alg. 1 l.5; built on the
+                                first such call, 0 before it or when it did not fit)     */
 } hodlr2d_info;
 
 /* Fill *opts with the defaults listed above. */

@@ -82,7 +82,7 @@ class Info(C.Structure):
         ("symmetric_apply", C.c_int), ("p2p_launches", C.c_int), ("p2p_leaves", C.c_int64 * 3),
         ("apply_launches", C.c_int), ("small_items", C.c_int64 * 2),
         ("comm_kind", C.c_int), ("adaptive", C.c_int), ("pair_apply", C.c_int), ("n_leaves", C.c_int64),
-        ("local_items", C.c_int64 * 2),
+        ("local_items", C.c_int64 * 2), ("stored_near_values", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -982,6 +982,7 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   info->comm_kind = comm_kind(h);
   info->local_items[0] = h.n_abig_loc;
   info->local_items[1] = h.n_asmall_loc;
+  info->stored_near_values = h.nf_state == 1 ? h.nf_values : 0;
   (void)rsum;
   return H2D_OK;
   H2D_CATCH
