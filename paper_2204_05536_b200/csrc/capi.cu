@@ -50,6 +50,9 @@ Handle::~Handle() {
   if (hi_stream) cudaStreamDestroy(hi_stream);
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (ev_b1) cudaEventDestroy(ev_b1);
+  for (auto& pe : place_ev)
+    for (cudaEvent_t e : pe)
+      if (e) cudaEventDestroy(e);
   if (ev_copy0) cudaEventDestroy(ev_copy0);
   if (ev_copy1) cudaEventDestroy(ev_copy1);
   if (as_h2d) cudaStreamSynchronize(as_h2d);
@@ -667,6 +670,7 @@ int hodlr2d_build_ex(const double* points, int64_t n, int kernel_id, int leaf_si
   {   // diagnostics switches, read once here
     auto env_is = [](const char* name, int v) { const char* e = getenv(name); return e && atoi(e) == v; };
     h.diag_p2p_serial = env_is("H2D_P2P_SERIAL", 1);
+    if (getenv("H2D_P2P_PLACE")) h.p2p_place = std::max(-1, std::min(1, atoi(getenv("H2D_P2P_PLACE"))));
     h.diag_p2p_onestream = env_is("H2D_P2P_ONESTREAM", 1);
     h.diag_dual_norow = getenv("H2D_DUAL_NOROW") != nullptr;
     h.diag_copy_stream = !env_is("H2D_COPY_STREAM", 0);
@@ -1154,6 +1158,11 @@ int hodlr2d_set_diag(hodlr2d_t H, const char* name, int value) {
   const std::string nm(name);
   if (nm == "p2p_serial") h.diag_p2p_serial = value != 0;
   else if (nm == "p2p_onestream") h.diag_p2p_onestream = value != 0;
+  else if (nm == "p2p_place") {   // near field beside stage A (0) / stage B (1) / timed (-1)
+    if (value < -1 || value > 1) throw Error{H2D_EINVAL, "p2p_place: -1, 0 or 1"};
+    h.p2p_place = value;
+    h.place_calls = 0;
+  }
   else if (nm == "dual_norow") h.diag_dual_norow = value != 0;
   else if (nm == "copy_stream") h.diag_copy_stream = value != 0;
   else if (nm == "multi_stored_near") h.nf_enabled = value != 0;

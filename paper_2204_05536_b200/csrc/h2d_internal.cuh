@@ -380,6 +380,10 @@ struct Handle {
   cudaEvent_t as_ydone[2] = {nullptr, nullptr}, as_yfree[2] = {nullptr, nullptr};
   int64_t as_calls = 0;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_far = nullptr;
+  // near-field placement on directed single-pass matvecs (apply.cu place_pick): beside stage A
+  // (0, default) or beside stage B (1); -1: chosen by timing matvec calls 1-2 (A) against 3-4 (B)
+  int p2p_place = 0, place_calls = 0;
+  cudaEvent_t place_ev[4][2] = {};
   // P2P classes (generic CTA leaves, warp leaves of 3 / 2 rows per lane) fork from aux_stream
   // onto their own low-priority streams so their under-filled grids overlap
   cudaStream_t p2p_side[3] = {nullptr, nullptr, nullptr};

@@ -68,8 +68,18 @@ def test_gmres_restart_bound_and_diag_names(h2d, op):
     x = W.random_vector(3000, 5)
     y1 = o.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
     o.set_diag("p2p_serial", 0)
+    o.set_diag("p2p_place", 1)   # near field beside stage B
+    y2 = o.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    o.set_diag("p2p_place", 0)   # beside stage A
     y0 = o.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
     assert np.array_equal(y0, y1)
+    assert np.array_equal(y0, y2)
+    with pytest.raises(h2d.Hodlr2dError):
+        o.set_diag("p2p_place", 2)
+    o.set_diag("p2p_place", -1)  # timed placement: calls 1-2 beside A, 3-4 beside B, then the faster
+    for _ in range(8):
+        assert np.array_equal(o.matvec(torch.from_numpy(x).cuda()).cpu().numpy(), y0)
+    o.set_diag("p2p_place", 0)
 
 
 def test_pageable_host_buffers(h2d, op):
