@@ -103,10 +103,10 @@ constexpr int kSymRowsOnly = 0, kSymBoth = 1, kSymSelf = 2;
 template <int KID>
 __device__ __forceinline__ double p2p_eval(const KernelParams& kp, const double2* tab, double px,
                                            double py, double qx, double qy) {
-  if (KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel) {
+  if (KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == kLogNoSelRepl) {
     const double dx = px - qx, dy = py - qy;
     const double r2 = fma(dx, dx, dy * dy);
-    return r2 > 0.0 ? hlog_r2<KID == kLogSafe>(r2, tab) : 0.0;
+    return r2 > 0.0 ? hlog_r2<KID == kLogSafe, KID == kLogNoSelRepl>(r2, tab) : 0.0;
   }
   return kernel_eval_t<KID>(kp, px, py, qx, qy);
 }
@@ -274,7 +274,7 @@ p2p_sym_kernel(int kappa, int64_t leaf_begin, int64_t leaf_end, const int32_t* _
   __shared__ double2 s_logtab[kHlogBins];
   const int64_t X = leaves[blockIdx.x];
   const int tid = threadIdx.x;
-  if (kNeedsLogTable<KID>) hlog_table(s_logtab);
+  if (kNeedsLogTable<KID>) hlog_table<KID>(s_logtab);
   const uint32_t cx = p2p_compact((uint32_t)X), cy = p2p_compact((uint32_t)X >> 1);
   const uint32_t side = 1u << kappa;
   const int64_t xs = leaf_start[X];
@@ -486,7 +486,7 @@ p2p_fast_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int
   __shared__ int s_next;
   const int tid = threadIdx.x;
   const double k0 = KID == H2D_KERNEL_IMQ ? 1.0 : 0.0;
-  if (kNeedsLogTable<KID>) hlog_table(tab);
+  if (kNeedsLogTable<KID>) hlog_table<KID>(tab);
   if (tid == 0) s_next = atomicAdd(counter, 1);
   __syncthreads();
   int cur = s_next;
@@ -567,7 +567,7 @@ p2p_list_kernel(const int64_t* __restrict__ items, int n_items, int32_t* counter
   __shared__ double sxv[8][32];
   __shared__ double2 tab[kHlogBins];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (kNeedsLogTable<KID>) hlog_table(tab);
+  if (kNeedsLogTable<KID>) hlog_table<KID>(tab);
   __syncthreads();
   for (;;) {
     int idx = 0;
@@ -753,7 +753,7 @@ p2p_warp_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int
   __shared__ double xself[8][32 * RPL], xnb[8][32];
   __shared__ double2 tab[kHlogBins];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (kNeedsLogTable<KID>) hlog_table(tab);
+  if (kNeedsLogTable<KID>) hlog_table<KID>(tab);
   __syncthreads();
   for (;;) {
     int idx = 0;
@@ -784,8 +784,8 @@ p2p_warp_kernel(int kappa, const int32_t* __restrict__ leaves, int n_leaves, int
         acc[r] = fma(kfast<KID>(fma(dx, dx, dy * dy), tab, kp), xj, acc[r]);
       }
     }
-    if (KID == kLogNoSel) {   // the diagonal (r2 = 0) was evaluated as hlog_r2(0): take it out
-      const double g = hlog_r2<false>(0.0, tab);
+    if (KID == kLogNoSel || KID == kLogNoSelRepl) {   // the diagonal (r2 = 0) was evaluated as hlog_r2(0): take it out
+      const double g = hlog_r2<false, KID == kLogNoSelRepl>(0.0, tab);
 #pragma unroll
       for (int r = 0; r < RPL; ++r) acc[r] = fma(-g, xi[r], acc[r]);
     }
@@ -1139,6 +1139,66 @@ static void set_pipe_attrs() {
 
 // Build the stage-A / reduce schedule, the t layout (U-column order), the stage-B items
 // and the per-level device tables.
+// The warp-per-leaf near-field classes with kernel KID, run alone (4 CTAs per SM) on st.
+template <int KID>
+static void warp_classes_alone(Handle& h, const double* x, cudaStream_t st) {
+  int64_t off = 0;
+  for (int r = 0; r < 3; ++r) {
+    const int64_t cnt = h.n_p2p_warp_rpl[r];
+    if (cnt <= 0) continue;
+    auto* kfn = r == 0 ? p2p_warp_kernel<KID, 1> : r == 1 ? p2p_warp_kernel<KID, 2> : p2p_warp_kernel<KID, 3>;
+    const int grid = (int)std::min<int64_t>(4 * (int64_t)h.num_sms, (cnt + 7) / 8);
+    H2D_CUDA(cudaMemsetAsync(h.d_counters + 4 + r, 0, sizeof(int32_t), st));
+    kfn<<<grid, 256, 0, st>>>(h.kappa, h.d_p2p_warp + off, (int)cnt, h.d_counters + 4 + r, h.d_leaf_start, h.d_px,
+                              h.d_py, x, h.kp, h.d_ynear, h.d_ynear + h.n, h.d_ynear + 2 * h.n);
+    H2D_LAUNCH_CHECK();
+    off += cnt;
+  }
+}
+
+// Log table of the warp-per-leaf near field (kLogNoSel handles): the 512-bin table or the
+// replicated 64-bin one (kLogNoSelRepl, pipe.cuh).  Which is faster depends on how the
+// near field's r^2 mantissas spread over the shared-memory banks (a regular grid: few
+// distinct values, many conflicts), so the build times both on this handle's leaves (a
+// warm-up and the best of three each, x = 0: the time does not depend on x) and keeps the
+// replicated table only when it is at least 10 % faster (so that handles of the same points
+// do not flip between the two on timing noise).  The two differ by rounding only (<= 1e-16
+// absolute per evaluation).
+// H2D_P2P_TABLE=0 / 1 forces the 512-bin / replicated table.
+static void pick_log_table(Handle& h, cudaStream_t s) {
+  const char* env = getenv("H2D_P2P_TABLE");
+  if (env) {
+    if (atoi(env) == 1) h.p2p_kid = kLogNoSelRepl;
+    return;
+  }
+  double* x0 = nullptr;
+  H2D_CUDA(cudaMallocAsync(&x0, h.n * sizeof(double), s));
+  H2D_CUDA(cudaMemsetAsync(x0, 0, h.n * sizeof(double), s));
+  cudaEvent_t e0, e1;
+  H2D_CUDA(cudaEventCreate(&e0));
+  H2D_CUDA(cudaEventCreate(&e1));
+  float best[2] = {1e30f, 1e30f};
+  for (int rep = 0; rep < 4; ++rep)
+    for (int v = 0; v < 2; ++v) {
+      H2D_CUDA(cudaEventRecord(e0, s));
+      if (v == 0) warp_classes_alone<kLogNoSel>(h, x0, s);
+      else warp_classes_alone<kLogNoSelRepl>(h, x0, s);
+      H2D_CUDA(cudaEventRecord(e1, s));
+      H2D_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      H2D_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      if (rep > 0) best[v] = std::min(best[v], ms);
+    }
+  H2D_CUDA(cudaEventDestroy(e0));
+  H2D_CUDA(cudaEventDestroy(e1));
+  H2D_CUDA(cudaFreeAsync(x0, s));
+  const bool repl = best[1] < 0.9f * best[0];
+  if (repl) h.p2p_kid = kLogNoSelRepl;
+  if (getenv("H2D_VERBOSE"))
+    fprintf(stderr, "[h2d] near-field log table: %s (512 bins %.4f ms, replicated 64 bins %.4f ms alone)\n",
+            repl ? "replicated" : "512 bins", best[0], best[1]);
+}
+
 void finalize_schedule(Handle& h) {
   cudaStream_t s = h.stream;
   int64_t t_len = 0, tpart_len = 0;
@@ -1775,6 +1835,7 @@ void finalize_schedule(Handle& h) {
                                     cudaSharedmemCarveoutMaxShared));
     h.num_sms = sm;
   }
+  if (h.p2p_kid == kLogNoSel && h.n_p2p_warp > 0) pick_log_table(h, s);
   H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 4 * sizeof(int32_t), s));
   H2D_CUDA(cudaStreamSynchronize(s));
 }
@@ -2011,6 +2072,7 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
           constexpr int R = decltype(rpl)::value;
           return h.p2p_kid == kLogSafe ? p2p_warp_kernel<kLogSafe, R>
                : h.p2p_kid == kLogNoSel ? p2p_warp_kernel<kLogNoSel, R>
+               : h.p2p_kid == kLogNoSelRepl ? p2p_warp_kernel<kLogNoSelRepl, R>
                : h.kp.id == H2D_KERNEL_LOG ? p2p_warp_kernel<H2D_KERNEL_LOG, R>
                : h.kp.id == H2D_KERNEL_IMQ ? p2p_warp_kernel<H2D_KERNEL_IMQ, R>
                : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_warp_kernel<H2D_KERNEL_ONE_OVER_R, R>

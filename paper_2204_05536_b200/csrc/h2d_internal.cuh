@@ -47,6 +47,10 @@ constexpr int kLogSafe = 5;
 // whose near field has no two distinct points at distance 0 and no subnormal r^2): the self
 // block's diagonal term is taken out once per row instead of a select per evaluation.
 constexpr int kLogNoSel = 6;
+// ... and the same with the replicated 64-bin log table (pipe.cuh hlog_r2<false, true>): no
+// shared-memory bank conflicts on the table lookups, two more DFMAs per evaluation; the build
+// times both on the handle's own near field and keeps the faster (apply.cu pick_log_table).
+constexpr int kLogNoSelRepl = 7;
 
 // K(p, q) specialised at compile time (hot P2P loop: no per-pair dispatch).
 template <int KID>
@@ -54,7 +58,7 @@ __device__ __forceinline__ double kernel_eval_t(const KernelParams& k, double px
                                                 double qx, double qy) {
   const double dx = px - qx, dy = py - qy;
   const double r2 = fma(dx, dx, dy * dy);
-  if (KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel) {
+  if (KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == kLogNoSelRepl) {
     return r2 > 0.0 ? 0.5 * log(r2) : 0.0;
   } else if (KID == H2D_KERNEL_IMQ) {
     return rsqrt(fma(r2, k.inv_c2, 1.0));

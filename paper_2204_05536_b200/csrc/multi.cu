@@ -1148,7 +1148,7 @@ p2p_multi_kernel(int kappa, int64_t leaf_begin, const int32_t* __restrict__ leaf
   __shared__ double red[256];
   __shared__ double2 tab[kHlogBins];
   const int tid = threadIdx.x;
-  if (kNeedsLogTable<KID>) hlog_table(tab);
+  if (kNeedsLogTable<KID>) hlog_table<KID>(tab);
   const int64_t X = leaf_begin + blockIdx.x;
   const uint32_t cx = p2p_compact((uint32_t)X), cy = p2p_compact((uint32_t)X >> 1);
   const uint32_t side = 1u << kappa;
@@ -1272,7 +1272,7 @@ __global__ void __launch_bounds__(256) nf_fill_kernel(int kappa, int64_t leaf_be
                                                       KernelParams kp, const int64_t* __restrict__ nf_off,
                                                       double* __restrict__ nf) {
   __shared__ double2 tab[kHlogBins];
-  if (kNeedsLogTable<KID>) hlog_table(tab);
+  if (kNeedsLogTable<KID>) hlog_table<KID>(tab);
   __syncthreads();
   const int64_t X = leaf_begin + blockIdx.x;
   int64_t ys[5];

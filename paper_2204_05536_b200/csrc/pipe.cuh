@@ -86,7 +86,13 @@ constexpr int kSymTile = 96, kSymMaxB = kSymTile / 16;
 // MUFU halves the shared-memory wavefronts of the random lookups but costs 5 instructions
 // more per evaluation, and the near field turns issue-bound: 0.40 -> 0.42 ms on C3;
 // tools/scratch/hlog_rcp_table.cuh.txt.)
-constexpr int kHlogBins = 512;
+// REPL (kLogNoSelRepl handles): 64 bins, each stored 8 times side by side (the same 8 KB);
+// lane l reads copy l % 8, so the 8 lanes of a 128-bit shared-memory phase always hit 8
+// distinct bank quads (no replays) at two more DFMAs (degree 5: |f| <= 2^-7, truncation
+// f^7 / 14 <= 1.3e-16).  The 512-bin table's random lookups replay on bank conflicts, and
+// on a regular grid (few distinct r^2 mantissas) far more than on random points: C4's near
+// field 2.59 -> 1.34 ms alone, C3's 0.46 -> 0.49 (profiles/r02ai_logtable.md).
+constexpr int kHlogBins = 512;       // table entries (bins, or 64 bins x 8 copies)
 __constant__ double c_hlog[8] = {0.34657359027997264,   // ln2 / 2 (high part)
                                  1.1595234069231498e-17, // ln2 / 2 (low part)
                                  0.5, -0.25, 1.0 / 6.0, -0.125, 0.1, -1.0 / 12.0};
@@ -98,8 +104,9 @@ __constant__ double c_hlog[8] = {0.34657359027997264,   // ln2 / 2 (high part)
 // SAFE = false (the default near field): r2 must be normal or 0; the build checks the
 // near field once and switches the handle to SAFE kernels (kLogSafe) if any pair of distinct
 // points has a subnormal r2, so the common case pays no normalisation.
-template <bool SAFE = false>
+template <bool SAFE = false, bool REPL = false>
 __device__ __forceinline__ double hlog_r2(double r2, const double2* __restrict__ tab) {
+  static_assert(!(SAFE && REPL), "the subnormal-safe log uses the 512-bin table");
   if (!SAFE) {
     // the same arithmetic on the high word only (r2 >= 0, normal or 0): the table byte offset
     // 16 k = (hi >> 7) & 0x1ff0, the mantissa's high word (hi & 0xfffff) | 0x3ff00000, and
@@ -107,10 +114,21 @@ __device__ __forceinline__ double hlog_r2(double r2, const double2* __restrict__
     // integer instructions fewer per evaluation than the 64-bit shifts and the signed e)
     static_assert(kHlogBins == 512, "offset mask assumes 512 bins");
     const uint32_t hi = (uint32_t)__double2hiint(r2);
-    const double2 tb = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(tab) + ((hi >> 7) & 0x1ff0u));
+    // REPL: bin = top 6 mantissa bits, byte offset 128 bin + 16 (lane % 8) (the lane part is
+    // loop-invariant and hoisted)
+    const double2 tb = REPL ? *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(tab + (threadIdx.x & 7)) +
+                                                                ((hi >> 7) & 0x1f80u))
+                            : *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(tab) + ((hi >> 7) & 0x1ff0u));
     const double mnt = __hiloint2double((int)((hi & 0x000fffffu) | 0x3ff00000u), __double2loint(r2));
     const double f = fma(mnt, tb.x, -1.0);
-    double p = fma(f, c_hlog[5], c_hlog[4]);
+    double p;
+    if (REPL) {
+      p = fma(f, c_hlog[7], c_hlog[6]);
+      p = fma(f, p, c_hlog[5]);
+      p = fma(f, p, c_hlog[4]);
+    } else {
+      p = fma(f, c_hlog[5], c_hlog[4]);
+    }
     p = fma(f, p, c_hlog[3]);
     p = fma(f, p, c_hlog[2]);
     const double ed = __hiloint2double(0x43300000, (int)(hi >> 20)) - 4503599627371519.0;
@@ -124,8 +142,8 @@ __device__ __forceinline__ double hlog_r2(double r2, const double2* __restrict__
   const int sh = max(0, __clzll(bits) - 11);
   bits <<= sh;
   const int e = (E == 0 ? 1 - sh : E) - 1023;
-  const int k = (int)(bits >> 43) & (kHlogBins - 1);
   const double mnt = __longlong_as_double((bits & 0x000FFFFFFFFFFFFFLL) | 0x3FF0000000000000LL);
+  const int k = (int)(bits >> 43) & (kHlogBins - 1);
   const double2 tb = tab[k];
   const double f = fma(mnt, tb.x, -1.0);
   double p = fma(f, c_hlog[5], c_hlog[4]);
@@ -135,9 +153,12 @@ __device__ __forceinline__ double hlog_r2(double r2, const double2* __restrict__
   return fma(ed, c_hlog[0], fma(p, f, fma(ed, c_hlog[1], tb.y)));
 }
 
+template <int KID>
 __device__ __forceinline__ void hlog_table(double2* tab) {
+  constexpr bool repl = KID == kLogNoSelRepl;
   for (int k = threadIdx.x; k < kHlogBins; k += blockDim.x) {
-    const double c = 1.0 + (k + 0.5) / kHlogBins;
+    const int b = repl ? k >> 3 : k;   // (replicated: entry k is copy k % 8 of bin k / 8)
+    const double c = 1.0 + (b + 0.5) / (repl ? 64 : kHlogBins);
     tab[k] = make_double2(1.0 / c, 0.5 * log(c));
   }
 }
@@ -146,8 +167,8 @@ __device__ __forceinline__ void hlog_table(double2* tab) {
 // the rare pairs closer than a); distance kernels only.
 template <int KID>
 __device__ __forceinline__ double kfast(double r2, const double2* __restrict__ tab, const KernelParams& kp) {
-  if (KID == kLogNoSel) {   // no r2 = 0 select: the caller corrects the diagonal (warp kernel)
-    return hlog_r2<false>(r2, tab);
+  if (KID == kLogNoSel || KID == kLogNoSelRepl) {   // no r2 = 0 select: the caller corrects the diagonal (warp kernel)
+    return hlog_r2<false, KID == kLogNoSelRepl>(r2, tab);
   } else if (KID == H2D_KERNEL_LOG || KID == kLogSafe) {
     const double v = hlog_r2<KID == kLogSafe>(r2, tab);
     return r2 > 0.0 ? v : 0.0;
@@ -170,10 +191,10 @@ __device__ __forceinline__ double kfast(double r2, const double2* __restrict__ t
 }
 
 template <int KID>
-constexpr bool kDistKernel = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == H2D_KERNEL_IMQ || KID == H2D_KERNEL_ONE_OVER_R ||
+constexpr bool kDistKernel = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == kLogNoSelRepl || KID == H2D_KERNEL_IMQ || KID == H2D_KERNEL_ONE_OVER_R ||
                              KID == H2D_KERNEL_RBF_PHI1 || KID == H2D_KERNEL_RBF_PHI2;
 template <int KID>
-constexpr bool kNeedsLogTable = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == H2D_KERNEL_RBF_PHI1;
+constexpr bool kNeedsLogTable = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == kLogNoSelRepl || KID == H2D_KERNEL_RBF_PHI1;
 
 __device__ __forceinline__ uint32_t p2p_spread(uint32_t v) {
   v &= 0xFFFFu;

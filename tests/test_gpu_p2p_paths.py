@@ -190,3 +190,29 @@ def test_log_kernel_subnormal_distances(h2d, path):
     Y = op.matvec_multi(dev(X)).cpu().numpy()
     for k in (0, 7):
         assert rel(Y[k], oracle.dense_matvec(pts, X[k], 0)) <= 1e-9
+
+
+@pytest.mark.parametrize("gen", ["grid", "uniform"])
+def test_log_table_variants(h2d, gen):
+    """The warp near field's two log tables (H2D_P2P_TABLE=0: 512 bins; 1: 64 bins stored 8
+    times, degree-5 polynomial; unset: the build times both and keeps the faster) give the
+    same matvec to rounding, and each matches the dense product; on a regular grid (64-point
+    leaves, the C4 geometry at 128^2) and on uniform points (C3 geometry at 16384)."""
+    pts = W.grid_points(128) if gen == "grid" else W.uniform_points(16384, 5160)
+    n = pts.shape[0]
+    ops = []
+    for t in ("0", "1", None):
+        if t is not None:
+            os.environ["H2D_P2P_TABLE"] = t
+        try:
+            ops.append(h2d.Hodlr2d.build(dev(pts), "log", 64, 1e-10, box_lo=(-1, -1), box_side=2.0))
+        finally:
+            os.environ.pop("H2D_P2P_TABLE", None)
+    assert ops[0].info()["p2p_leaves"][0] > 0
+    x = W.random_vector(n, 5161)
+    ys = [o.matvec(dev(x)).cpu().numpy() for o in ops]
+    assert rel(ys[1], ys[0]) <= 1e-14
+    assert rel(ys[2], ys[0]) <= 1e-14
+    yd = oracle.dense_matvec(pts, x, 0)
+    for y in ys:
+        assert rel(y, yd) <= 1e-9
