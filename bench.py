@@ -475,44 +475,8 @@ def run_ours(args, cfg):
     # the spare SM resources, so its FP64 fraction is also probed standalone (set_diag
     # "p2p_serial": the near field alone, before stage A).
     csum = clk.summary()
-    p2p_ms = per["p2p_near"]
-    ops_eval = P2P_FP64_OPS_PER_EVAL.get(cfg.kernel)
-    sm_hz = (csum["sm_mhz"] or 1965.0) * 1e6
-    served = inf["row_end"] - inf["row_begin"]
-    self_evals = 0.0
-    if inf.get("adaptive"):   # p2p_list_kernel: every directed pair of the dense blocks
-        evals = float(inf["p2p_pairs"])
-    else:
-        _, ls = op.tree()
-        msz = np.diff(ls[inf["leaf_begin"]: inf["leaf_end"] + 1]).astype(np.float64)
-        self_pairs = float((msz * msz).sum())
-        warp = msz <= 96   # warp-per-leaf path: full self blocks; CTA paths: i <= j only
-        self_evals = float((msz[warp] ** 2).sum() + (msz[~warp] * (msz[~warp] + 1) / 2).sum())
-        evals = self_evals + (inf["p2p_pairs"] - self_pairs) / 2.0
-    if ops_eval is not None and cfg.kernel == 0 and self_evals > 0:
-        # log: a neighbour-block evaluation adds its column-sum DFMA to the self-block count
-        ops_eval = (self_evals * ops_eval + (evals - self_evals) * (ops_eval + 1)) / evals
     alone_ms = p2p_standalone_ms(op, step, args) if world == 1 else None
-    peak_ops, peak_ops_kind = 148 * 64 * sm_hz, "nominal: 148 SMs x 64 FP64 lanes x SM clock"
-    try:
-        with open(os.path.join(ROOT, "profiles", "fp64_peaks_measured.json")) as f:
-            peak_ops = json.load(f)["fp64_dfma_tflops"] * 1e12 / 2.0   # FP64-pipe instr/s
-        peak_ops_kind = "measured: tools/fp64_peak.cu sustained DFMA (profiles/fp64_peaks_measured.json)"
-    except Exception:
-        pass
-
-    def frac(ms):
-        return evals * ops_eval / (ms * 1e-3) / peak_ops if (ms and ops_eval) else None
-
-    p2p = {"directed_pairs": int(inf["p2p_pairs"]), "evaluations": int(evals),
-           "ms_per_launch_concurrent": round(p2p_ms, 4),
-           "ms_per_launch_standalone": round(alone_ms, 4) if alone_ms else None,
-           "fp64_ops_per_eval": ops_eval, "peak_fp64_lane_ops_per_s": peak_ops,
-           "peak_kind": peak_ops_kind,
-           "frac_fp64_pipe_standalone": frac(alone_ms),
-           "frac_fp64_pipe_concurrent": frac(p2p_ms),
-           "overlapped_with": "stageA_VTx + stageB_Ut (low-priority stream, co-resident CTAs)",
-           "exposed_ms": round(per["p2p_join_wait"], 4)}
+    p2p = p2p_roofline(op, inf, cfg, per, csum["sm_mhz"], alone_ms)
     roof["p2p"] = p2p
     # C5 (N = 2^24) is the config BASELINE quotes on 8 GPUs: at N >= --c5-min-world ranks the
     # line carries it too (every rank takes part: the all-gather is collective)
@@ -676,6 +640,9 @@ def sub_config(h2d, name, args, stream):
             "bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4),
             "stage_ms_per_matvec": {k: round(v, 4) for k, v in per.items()},
             "whole_matvec_frac": round(inf["matvec_bytes"] / (ms * 1e-3) / 1e9 / peak, 4)}
+    alone_ms = p2p_standalone_ms(
+        op, lambda k: op.matvec_raw(xs[k % nx].data_ptr(), y.data_ptr(), h2d.ORDER_ORIGINAL), args)
+    roof["p2p"] = p2p_roofline(op, inf, cfg, per, clk.summary()["sm_mhz"], alone_ms)
     xh = torch.empty(cfg.n, dtype=torch.float64).pin_memory()
     yh = torch.empty(cfg.n, dtype=torch.float64).pin_memory()
     xh.copy_(xs[0].cpu())
@@ -772,6 +739,56 @@ def launches_per_matvec(inf, world):
 # (Round 1: 16 with the select and I2F.F64; round 2 before the high-word log: 13.)  IMQ / 1/r:
 # distance + rsqrt (MUFU.RSQ64H seed + Newton) + the accumulation, ~12 (estimate).
 P2P_FP64_OPS_PER_EVAL = {0: 12, 1: 12, 2: 12}
+
+
+def p2p_roofline(op, inf, cfg, per, sm_mhz, alone_ms):
+    """Near-field P2P against the FP64 pipe.  The kernel that runs on the uniform / grid
+    configs is p2p_warp_kernel (every leaf <= 96 points): it evaluates each leaf's self block
+    in full (sum m^2) and each edge-neighbour leaf pair once, i.e. sum m^2 + (near_pairs -
+    sum m^2) / 2 kernel evaluations, each P2P_FP64_OPS_PER_EVAL FP64-pipe instructions
+    (counted in its SASS; + 2 DFMAs with the replicated log table,
+    info p2p_log_table = 1).  In the timed matvec it runs concurrently with stages A/B on the
+    spare SM resources, so its FP64 fraction is also probed standalone (set_diag
+    "p2p_serial": the near field alone, before stage A)."""
+    p2p_ms = per["p2p_near"]
+    ops_eval = P2P_FP64_OPS_PER_EVAL.get(cfg.kernel)
+    if ops_eval is not None and inf.get("p2p_log_table") == 1:
+        ops_eval += 2
+    sm_hz = (sm_mhz or 1965.0) * 1e6
+    self_evals = 0.0
+    if inf.get("adaptive"):   # p2p_list_kernel: every directed pair of the dense blocks
+        evals = float(inf["p2p_pairs"])
+    else:
+        _, ls = op.tree()
+        msz = np.diff(ls[inf["leaf_begin"]: inf["leaf_end"] + 1]).astype(np.float64)
+        self_pairs = float((msz * msz).sum())
+        warp = msz <= 96   # warp-per-leaf path: full self blocks; CTA paths: i <= j only
+        self_evals = float((msz[warp] ** 2).sum() + (msz[~warp] * (msz[~warp] + 1) / 2).sum())
+        evals = self_evals + (inf["p2p_pairs"] - self_pairs) / 2.0
+    if ops_eval is not None and cfg.kernel == 0 and self_evals > 0:
+        # log: a neighbour-block evaluation adds its column-sum DFMA to the self-block count
+        ops_eval = (self_evals * ops_eval + (evals - self_evals) * (ops_eval + 1)) / evals
+    peak_ops, peak_ops_kind = 148 * 64 * sm_hz, "nominal: 148 SMs x 64 FP64 lanes x SM clock"
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peaks_measured.json")) as f:
+            peak_ops = json.load(f)["fp64_dfma_tflops"] * 1e12 / 2.0   # FP64-pipe instr/s
+        peak_ops_kind = "measured: tools/fp64_peak.cu sustained DFMA (profiles/fp64_peaks_measured.json)"
+    except Exception:
+        pass
+
+    def frac(ms):
+        return evals * ops_eval / (ms * 1e-3) / peak_ops if (ms and ops_eval) else None
+
+    return {"directed_pairs": int(inf["p2p_pairs"]), "evaluations": int(evals),
+            "log_table": {1: "replicated 64 bins", 0: "512 bins"}.get(inf.get("p2p_log_table")),
+            "ms_per_launch_concurrent": round(p2p_ms, 4),
+            "ms_per_launch_standalone": round(alone_ms, 4) if alone_ms else None,
+            "fp64_ops_per_eval": ops_eval, "peak_fp64_lane_ops_per_s": peak_ops,
+            "peak_kind": peak_ops_kind,
+            "frac_fp64_pipe_standalone": frac(alone_ms),
+            "frac_fp64_pipe_concurrent": frac(p2p_ms),
+            "overlapped_with": "stageA_VTx + stageB_Ut (low-priority stream, co-resident CTAs)",
+            "exposed_ms": round(per["p2p_join_wait"], 4)}
 
 
 def p2p_standalone_ms(op, step, args, n=10):

@@ -83,6 +83,7 @@ class Info(C.Structure):
         ("apply_launches", C.c_int), ("small_items", C.c_int64 * 2),
         ("comm_kind", C.c_int), ("adaptive", C.c_int), ("pair_apply", C.c_int), ("n_leaves", C.c_int64),
         ("local_items", C.c_int64 * 2), ("stored_near_values", C.c_int64),
+        ("p2p_log_table", C.c_int),
     ]
 
     def as_dict(self) -> dict:

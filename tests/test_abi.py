@@ -57,9 +57,9 @@ int main(void) {{
          offsetof(hodlr2d_info, symmetric_apply), offsetof(hodlr2d_info, p2p_launches),
          offsetof(hodlr2d_info, p2p_leaves), offsetof(hodlr2d_info, apply_launches),
          offsetof(hodlr2d_info, small_items));
-  printf("%zu %zu %zu %zu %zu %zu\\n", offsetof(hodlr2d_options, nccl_id), offsetof(hodlr2d_options, allgather_ctx),
+  printf("%zu %zu %zu %zu %zu %zu %zu\\n", offsetof(hodlr2d_options, nccl_id), offsetof(hodlr2d_options, allgather_ctx),
          offsetof(hodlr2d_info, comm_kind), offsetof(hodlr2d_info, n_leaves), offsetof(hodlr2d_info, local_items),
-         offsetof(hodlr2d_info, stored_near_values));
+         offsetof(hodlr2d_info, stored_near_values), offsetof(hodlr2d_info, p2p_log_table));
   return 0;
 }}""")
     exe = tmp_path / "layout"
@@ -71,7 +71,7 @@ int main(void) {{
                     I.rank_hist.offset, I.matvec_bytes.offset, I.device_bytes.offset, I.symmetric_apply.offset,
                     I.p2p_launches.offset, I.p2p_leaves.offset, I.apply_launches.offset, I.small_items.offset,
                     O.nccl_id.offset, O.allgather_ctx.offset, I.comm_kind.offset, I.n_leaves.offset,
-                    I.local_items.offset, I.stored_near_values.offset]
+                    I.local_items.offset, I.stored_near_values.offset, I.p2p_log_table.offset]
 
 
 def test_default_options(h2d):

@@ -209,6 +209,8 @@ def test_log_table_variants(h2d, gen):
         finally:
             os.environ.pop("H2D_P2P_TABLE", None)
     assert ops[0].info()["p2p_leaves"][0] > 0
+    assert (ops[0].info()["p2p_log_table"], ops[1].info()["p2p_log_table"]) == (0, 1)
+    assert ops[2].info()["p2p_log_table"] in (0, 1)
     x = W.random_vector(n, 5161)
     ys = [o.matvec(dev(x)).cpu().numpy() for o in ops]
     assert rel(ys[1], ys[0]) <= 1e-14
