@@ -183,10 +183,11 @@ typedef struct {
   int64_t stored_near_values;/* fp64 values of the stored near-field blocks that 16-vector
                                 multi-RHS chunks read (Alg. 1 l.5; built on the
                                 first such call, 0 before it or when it did not fit)     */
-  int p2p_log_table;         /* log table of the warp-per-leaf near field: 0 the 512-bin
-                                table, 1 the replicated 64-bin table (picked at build by
-                                timing both), -1 none (other kernels, or the
-                                subnormal-safe log)                                      */
+  int p2p_log_table;         /* log table of the near field (the warp-per-leaf kernel; on
+                                adaptive handles the list kernel, log and phi_1): 0 the
+                                512-bin table, 1 the replicated 64-bin table (picked at
+                                build by timing both), -1 none (other
+                                kernels, or the subnormal-safe log)                      */
 } hodlr2d_info;
 
 /* Fill *opts with the defaults listed above. */

@@ -1199,6 +1199,57 @@ static void pick_log_table(Handle& h, cudaStream_t s) {
             repl ? "replicated" : "512 bins", best[0], best[1]);
 }
 
+// The adaptive list near field with kernel KID, run alone (3 CTAs per SM, as p2p_serial) on st.
+template <int KID>
+static void list_alone(Handle& h, const double* x, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((int64_t)h.num_sms * 3, (h.n_p2p_list + 7) / 8);
+  H2D_CUDA(cudaMemsetAsync(h.d_counters + 4, 0, sizeof(int32_t), st));
+  p2p_list_kernel<KID><<<grid, 256, 0, st>>>(h.d_p2p_list, (int)h.n_p2p_list, h.d_counters + 4, h.d_lf_start,
+                                             h.d_ad_nf_off, h.d_ad_nf_rng, h.d_px, h.d_py, x, h.kp, h.d_ynear);
+  H2D_LAUNCH_CHECK();
+}
+
+// pick_log_table for the adaptive list near field (log and RBF phi_1 kernels): the same
+// timing and 10 % margin; H2D_P2P_TABLE=0 / 1 forces either.
+static void pick_list_table(Handle& h, cudaStream_t s) {
+  const char* env = getenv("H2D_P2P_TABLE");
+  if (env) {
+    h.list_repl = atoi(env) == 1;
+    return;
+  }
+  const bool phi1 = h.kp.id == H2D_KERNEL_RBF_PHI1;
+  double* x0 = nullptr;
+  H2D_CUDA(cudaMallocAsync(&x0, h.n * sizeof(double), s));
+  H2D_CUDA(cudaMemsetAsync(x0, 0, h.n * sizeof(double), s));
+  cudaEvent_t e0, e1;
+  H2D_CUDA(cudaEventCreate(&e0));
+  H2D_CUDA(cudaEventCreate(&e1));
+  float best[2] = {1e30f, 1e30f};
+  for (int rep = 0; rep < 4; ++rep)
+    for (int v = 0; v < 2; ++v) {
+      H2D_CUDA(cudaEventRecord(e0, s));
+      if (phi1) {
+        if (v == 0) list_alone<H2D_KERNEL_RBF_PHI1>(h, x0, s);
+        else list_alone<kPhi1Repl>(h, x0, s);
+      } else {
+        if (v == 0) list_alone<H2D_KERNEL_LOG>(h, x0, s);
+        else list_alone<kLogRepl>(h, x0, s);
+      }
+      H2D_CUDA(cudaEventRecord(e1, s));
+      H2D_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      H2D_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      if (rep > 0) best[v] = std::min(best[v], ms);
+    }
+  H2D_CUDA(cudaEventDestroy(e0));
+  H2D_CUDA(cudaEventDestroy(e1));
+  H2D_CUDA(cudaFreeAsync(x0, s));
+  h.list_repl = best[1] < 0.9f * best[0];
+  if (getenv("H2D_VERBOSE"))
+    fprintf(stderr, "[h2d] adaptive near-field log table: %s (512 bins %.4f ms, replicated 64 bins %.4f ms alone)\n",
+            h.list_repl ? "replicated" : "512 bins", best[0], best[1]);
+}
+
 void finalize_schedule(Handle& h) {
   cudaStream_t s = h.stream;
   int64_t t_len = 0, tpart_len = 0;
@@ -1836,6 +1887,9 @@ void finalize_schedule(Handle& h) {
     h.num_sms = sm;
   }
   if (h.p2p_kid == kLogNoSel && h.n_p2p_warp > 0) pick_log_table(h, s);
+  h.list_repl = false;
+  if (h.n_p2p_list > 0 && h.p2p_kid != kLogSafe && (h.kp.id == H2D_KERNEL_LOG || h.kp.id == H2D_KERNEL_RBF_PHI1))
+    pick_list_table(h, s);
   H2D_CUDA(cudaMemsetAsync(h.d_counters, 0, 4 * sizeof(int32_t), s));
   H2D_CUDA(cudaStreamSynchronize(s));
 }
@@ -2019,10 +2073,11 @@ void matvec_tree(Handle& h, const double* d_xtree, double* d_y, int order_out, i
     };
     if (h.n_p2p_list > 0) {   // adaptive near field (R24)
       auto* kfn = h.p2p_kid == kLogSafe ? p2p_list_kernel<kLogSafe>
-                : h.kp.id == H2D_KERNEL_LOG ? p2p_list_kernel<H2D_KERNEL_LOG>
+                : h.kp.id == H2D_KERNEL_LOG ? (h.list_repl ? p2p_list_kernel<kLogRepl> : p2p_list_kernel<H2D_KERNEL_LOG>)
                 : h.kp.id == H2D_KERNEL_IMQ ? p2p_list_kernel<H2D_KERNEL_IMQ>
                 : h.kp.id == H2D_KERNEL_ONE_OVER_R ? p2p_list_kernel<H2D_KERNEL_ONE_OVER_R>
-                : h.kp.id == H2D_KERNEL_RBF_PHI1 ? p2p_list_kernel<H2D_KERNEL_RBF_PHI1>
+                : h.kp.id == H2D_KERNEL_RBF_PHI1 ? (h.list_repl ? p2p_list_kernel<kPhi1Repl>
+                                                                : p2p_list_kernel<H2D_KERNEL_RBF_PHI1>)
                 : h.kp.id == H2D_KERNEL_RBF_PHI2 ? p2p_list_kernel<H2D_KERNEL_RBF_PHI2>
                                                    : p2p_list_kernel<H2D_KERNEL_TEST_LOWRANK>;
       H2D_CUDA(cudaMemsetAsync(h.d_counters + 4, 0, sizeof(int32_t), a));

@@ -988,6 +988,8 @@ int hodlr2d_get_info(hodlr2d_t H, hodlr2d_info* info) {
   info->local_items[1] = h.n_asmall_loc;
   info->stored_near_values = h.nf_state == 1 ? h.nf_values : 0;
   info->p2p_log_table = h.p2p_kid == kLogNoSelRepl ? 1 : h.p2p_kid == kLogNoSel ? 0 : -1;
+  if (h.n_p2p_list > 0 && h.p2p_kid != kLogSafe && (h.kp.id == H2D_KERNEL_LOG || h.kp.id == H2D_KERNEL_RBF_PHI1))
+    info->p2p_log_table = h.list_repl ? 1 : 0;
   (void)rsum;
   return H2D_OK;
   H2D_CATCH

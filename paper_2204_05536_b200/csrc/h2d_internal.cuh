@@ -51,6 +51,9 @@ constexpr int kLogNoSel = 6;
 // shared-memory bank conflicts on the table lookups, two more DFMAs per evaluation; the build
 // times both on the handle's own near field and keeps the faster (apply.cu pick_log_table).
 constexpr int kLogNoSelRepl = 7;
+// ... and the replicated table in the adaptive list near field (p2p_list_kernel): the log
+// kernel (with the K(0) select) and the RBF phi_1 kernel (apply.cu pick_list_table).
+constexpr int kLogRepl = 8, kPhi1Repl = 9;
 
 // K(p, q) specialised at compile time (hot P2P loop: no per-pair dispatch).
 template <int KID>
@@ -58,13 +61,13 @@ __device__ __forceinline__ double kernel_eval_t(const KernelParams& k, double px
                                                 double qx, double qy) {
   const double dx = px - qx, dy = py - qy;
   const double r2 = fma(dx, dx, dy * dy);
-  if (KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == kLogNoSelRepl) {
+  if (KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == kLogNoSelRepl || KID == kLogRepl) {
     return r2 > 0.0 ? 0.5 * log(r2) : 0.0;
   } else if (KID == H2D_KERNEL_IMQ) {
     return rsqrt(fma(r2, k.inv_c2, 1.0));
   } else if (KID == H2D_KERNEL_ONE_OVER_R) {
     return r2 > 0.0 ? rsqrt(r2) : 0.0;
-  } else if (KID == H2D_KERNEL_RBF_PHI1) {
+  } else if (KID == H2D_KERNEL_RBF_PHI1 || KID == kPhi1Repl) {
     if (r2 == 0.0) return 0.0;
     if (r2 >= k.a2) return 0.5 * log(r2) * k.inv_log_a;
     const double r = sqrt(r2);
@@ -396,6 +399,7 @@ struct Handle {
   // build, changeable per handle with hodlr2d_set_diag (never per call from the environment)
   bool diag_p2p_serial = false, diag_p2p_onestream = false, diag_dual_norow = false;
   bool diag_copy_stream = true;
+  bool list_repl = false;       // adaptive near field on the replicated log table (pick_list_table)
   int diag_p2p_list_ctas = 1;   // adaptive near field beside the streams: CTAs per SM (H2D_P2P_LIST_CTAS)
   // near-field kernel id (kp.id, or kLogSafe when a near pair has a subnormal r^2)
   int p2p_kid = 0;

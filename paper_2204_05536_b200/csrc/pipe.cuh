@@ -155,7 +155,7 @@ __device__ __forceinline__ double hlog_r2(double r2, const double2* __restrict__
 
 template <int KID>
 __device__ __forceinline__ void hlog_table(double2* tab) {
-  constexpr bool repl = KID == kLogNoSelRepl;
+  constexpr bool repl = KID == kLogNoSelRepl || KID == kLogRepl || KID == kPhi1Repl;
   for (int k = threadIdx.x; k < kHlogBins; k += blockDim.x) {
     const int b = repl ? k >> 3 : k;   // (replicated: entry k is copy k % 8 of bin k / 8)
     const double c = 1.0 + (b + 0.5) / (repl ? 64 : kHlogBins);
@@ -169,16 +169,16 @@ template <int KID>
 __device__ __forceinline__ double kfast(double r2, const double2* __restrict__ tab, const KernelParams& kp) {
   if (KID == kLogNoSel || KID == kLogNoSelRepl) {   // no r2 = 0 select: the caller corrects the diagonal (warp kernel)
     return hlog_r2<false, KID == kLogNoSelRepl>(r2, tab);
-  } else if (KID == H2D_KERNEL_LOG || KID == kLogSafe) {
-    const double v = hlog_r2<KID == kLogSafe>(r2, tab);
+  } else if (KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogRepl) {
+    const double v = hlog_r2<KID == kLogSafe, KID == kLogRepl>(r2, tab);
     return r2 > 0.0 ? v : 0.0;
   } else if (KID == H2D_KERNEL_IMQ) {
     return rsqrt(fma(r2, kp.inv_c2, 1.0));
   } else if (KID == H2D_KERNEL_ONE_OVER_R) {
     const double v = rsqrt(r2);
     return r2 > 0.0 ? v : 0.0;
-  } else if (KID == H2D_KERNEL_RBF_PHI1) {
-    double v = hlog_r2(r2, tab) * kp.inv_log_a;          // log r / log a
+  } else if (KID == H2D_KERNEL_RBF_PHI1 || KID == kPhi1Repl) {
+    double v = hlog_r2<false, KID == kPhi1Repl>(r2, tab) * kp.inv_log_a;   // log r / log a
     if (r2 < kp.a2) {
       const double r = sqrt(r2);
       v = r2 > 0.0 ? fma(r, log(r), -1.0) * kp.inv_phi1_den : 0.0;
@@ -191,10 +191,10 @@ __device__ __forceinline__ double kfast(double r2, const double2* __restrict__ t
 }
 
 template <int KID>
-constexpr bool kDistKernel = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == kLogNoSelRepl || KID == H2D_KERNEL_IMQ || KID == H2D_KERNEL_ONE_OVER_R ||
+constexpr bool kDistKernel = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == kLogNoSelRepl || KID == kLogRepl || KID == kPhi1Repl || KID == H2D_KERNEL_IMQ || KID == H2D_KERNEL_ONE_OVER_R ||
                              KID == H2D_KERNEL_RBF_PHI1 || KID == H2D_KERNEL_RBF_PHI2;
 template <int KID>
-constexpr bool kNeedsLogTable = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == kLogNoSelRepl || KID == H2D_KERNEL_RBF_PHI1;
+constexpr bool kNeedsLogTable = KID == H2D_KERNEL_LOG || KID == kLogSafe || KID == kLogNoSel || KID == kLogNoSelRepl || KID == kLogRepl || KID == kPhi1Repl || KID == H2D_KERNEL_RBF_PHI1;
 
 __device__ __forceinline__ uint32_t p2p_spread(uint32_t v) {
   v &= 0xFFFFu;

@@ -192,3 +192,28 @@ def _symmetric_three_pass(h2d, tmp_path, pts, n, kw, env):
     o.save_factors(path)
     op.load_factors(path)
     assert rel(op.matvec(dev(x)).cpu().numpy(), o.matvec(x)) <= 1e-12
+
+
+@pytest.mark.parametrize("kernel,kid,c,shift", [("log", 0, 1.0, 0.0), ("rbf_phi1", 3, 1e-3, 14400.0)])
+def test_adaptive_log_table_variants(h2d, kernel, kid, c, shift):
+    """The adaptive list near field on the 512-bin and on the replicated 64-bin log table
+    (H2D_P2P_TABLE=0 / 1; unset: timed at build): the same matvec to rounding, each within
+    the dense product's bar; info p2p_log_table names the table."""
+    import os
+    pts = W.chebyshev_grid(120)
+    ops = []
+    for t in ("0", "1", None):
+        if t is not None:
+            os.environ["H2D_P2P_TABLE"] = t
+        try:
+            ops.append(gpu(h2d, pts, kernel, 64, 1e-12, c=c, shift=shift))
+        finally:
+            os.environ.pop("H2D_P2P_TABLE", None)
+    assert [o.info()["p2p_log_table"] for o in ops[:2]] == [0, 1]
+    assert ops[2].info()["p2p_log_table"] in (0, 1)
+    x = W.random_vector(pts.shape[0], 5170)
+    ys = [o.matvec(dev(x)).cpu().numpy() for o in ops]
+    assert rel(ys[1], ys[0]) <= 1e-14 and rel(ys[2], ys[0]) <= 1e-14
+    yd = oracle.dense_matvec(pts, x, kid, c, 1.0, shift)
+    for y in ys:
+        assert rel(y, yd) <= 1e-10
