@@ -1169,6 +1169,7 @@ int hodlr2d_set_diag(hodlr2d_t H, const char* name, int value) {
   else if (nm == "dual_norow") h.diag_dual_norow = value != 0;
   else if (nm == "copy_stream") h.diag_copy_stream = value != 0;
   else if (nm == "multi_stored_near") h.nf_enabled = value != 0;
+  else if (nm == "multi_log_table") h.multi_repl = value != 0;   // 1: replicated 64-bin table
   else if (nm == "pair_apply") {   // symmetric handles: pair apply (1) or the three-pass apply (0)
     if (value && (!h.pair_wanted || h.pair_failed)) throw Error{H2D_EINVAL, "pair apply not built for this handle"};
     if (!value && !h.symapply && h.pairapply) throw Error{H2D_EINVAL, "no three-pass apply on this handle"};

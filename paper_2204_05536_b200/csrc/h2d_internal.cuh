@@ -399,6 +399,7 @@ struct Handle {
   // build, changeable per handle with hodlr2d_set_diag (never per call from the environment)
   bool diag_p2p_serial = false, diag_p2p_onestream = false, diag_dual_norow = false;
   bool diag_copy_stream = true;
+  bool multi_repl = true;       // multi-RHS on-the-fly log near field on the replicated table (set_diag "multi_log_table")
   bool list_repl = false;       // adaptive near field on the replicated log table (pick_list_table)
   int diag_p2p_list_ctas = 1;   // adaptive near field beside the streams: CTAs per SM (H2D_P2P_LIST_CTAS)
   // near-field kernel id (kp.id, or kLogSafe when a near pair has a subnormal r^2)

@@ -1749,6 +1749,7 @@ static void multi_chunk(Handle& h, const double* dX, int64_t xlen, double* dY, i
     switch (h.kp.id) {
       case H2D_KERNEL_LOG:
         if (h.p2p_kid == kLogSafe) launch_p2p_multi<kLogSafe, NR>(h, a);
+        else if (h.multi_repl) launch_p2p_multi<kLogRepl, NR>(h, a);
         else launch_p2p_multi<H2D_KERNEL_LOG, NR>(h, a);
         break;
       case H2D_KERNEL_IMQ: launch_p2p_multi<H2D_KERNEL_IMQ, NR>(h, a); break;
@@ -1818,6 +1819,7 @@ static void multi_chunk_sym(Handle& h, const double* dX, int64_t xlen, double* d
   switch (h.kp.id) {
     case H2D_KERNEL_LOG:
       if (h.p2p_kid == kLogSafe) launch_p2p_multi<kLogSafe, NR>(h, a);
+      else if (h.multi_repl) launch_p2p_multi<kLogRepl, NR>(h, a);
       else launch_p2p_multi<H2D_KERNEL_LOG, NR>(h, a);
       break;
     case H2D_KERNEL_IMQ: launch_p2p_multi<H2D_KERNEL_IMQ, NR>(h, a); break;

@@ -167,3 +167,20 @@ def test_multi_stored_near_field(h2d, name):
         y1 = op.matvec(dev(X[k])).cpu().numpy()
         assert rel(Ys[k], Yf[k]) <= 1e-13, k
         assert rel(Ys[k], y1) <= 1e-13, k
+
+
+def test_multi_log_table_variants(h2d):
+    """The on-the-fly multi-RHS log near field on the replicated 64-bin table (default) and on
+    the 512-bin table (set_diag multi_log_table 0): the same columns to rounding, both equal to
+    the single-vector matvec to 1e-13; on a grid (C4 geometry) and on uniform points."""
+    for pts in (W.grid_points(128), W.uniform_points(16384, 5180)):
+        op = h2d.Hodlr2d.build(dev(pts), "log", 64, 1e-10, box_lo=(-1, -1), box_side=2.0)
+        X = np.stack([W.random_vector(pts.shape[0], 5181 + k) for k in range(8)])
+        Yr = op.matvec_multi(dev(X)).cpu().numpy()
+        op.set_diag("multi_log_table", 0)
+        Yt = op.matvec_multi(dev(X)).cpu().numpy()
+        op.set_diag("multi_log_table", 1)
+        for k in (0, 7):
+            y1 = op.matvec(dev(X[k])).cpu().numpy()
+            assert rel(Yr[k], Yt[k]) <= 1e-14, k
+            assert rel(Yr[k], y1) <= 1e-13, k

@@ -19,6 +19,8 @@ op = h2d.Hodlr2d.build(pts, cfg.kernel, cfg.leaf_size, cfg.tol, c=cfg.c, scale=c
                        symmetric=os.environ.get("SYM", "0") == "1")
 if "NF" in os.environ:
     op.set_diag("multi_stored_near", int(os.environ["NF"]))
+if "MT" in os.environ:
+    op.set_diag("multi_log_table", int(os.environ["MT"]))
 X = torch.rand(K, cfg.n, dtype=torch.float64, device="cuda") * 2 - 1
 Y = torch.empty_like(X)
 s = torch.cuda.current_stream()
