@@ -331,8 +331,12 @@ int hodlr2d_partition(const int32_t* leaf_start, int kappa, int world, int rank,
  * host copies on the work stream), "pair_apply" (symmetric handles: 1 the pair-local apply,
  * 0 the three-pass apply), "multi_stored_near" (16-vector multi-RHS chunks: 1 (default) the
  * stored dense near-field blocks of Alg. 1 l.5, built on the first such call when they
- * fit in half the free device memory; 0 the on-the-fly near field).  Defaults come from the
- * H2D_* environment variables at build time.  H2D_EINVAL for an unknown name. */
+ * fit in half the free device memory; 0 the on-the-fly near field), "multi_log_table"
+ * (multi-RHS on-the-fly log near field: 1 (default) the replicated 64-bin log table, 0 the
+ * 512-bin one), "p2p_place" (directed matvecs: 0 (default) the near field beside stage A,
+ * 1 beside stage B, -1 timed on matvec calls 1-4; results bit-identical; H2D_EINVAL outside
+ * -1..1).  Defaults come from the H2D_* environment variables at build time.  H2D_EINVAL for
+ * an unknown name. */
 int hodlr2d_set_diag(hodlr2d_t h, const char* name, int value);
 
 /* Write a fresh NCCL unique id (H2D_COMM_ID_BYTES bytes) to id[] for options.nccl_id
